@@ -1,0 +1,201 @@
+/*
+ * intfsim_b200.h -- C ABI of the B200 (sm_100a) hot path of the intfsim
+ * reference (arXiv 2512.18725 simulator, /root/reference/pkg/src/intfsim).
+ *
+ * The reference is pure Python with no FFI; its drop-in boundary is the
+ * package surface `intfsim/__init__.py:7-51`.  Each entry point below is the
+ * batched, device-resident replacement of one reference function (cited), and
+ * is what `paper_2512_18725_b200` (the Python mirror of that surface) binds
+ * with ctypes.  INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Every pointer inside the descriptor structs is a DEVICE pointer (CUDA
+ *    global memory, caller-owned); the descriptor structs themselves are host
+ *    memory, read during the call.  No torch types, no allocation in the hot
+ *    calls: scratch comes from caller buffers.
+ *  - Calls are asynchronous on `stream` (a cudaStream_t, passed as void*).
+ *  - Return value: INTF_OK or an INTF_E_* code for launch/argument errors;
+ *    per-scenario invariant violations (the reference's SimulationError
+ *    checks, `simcore.py:118-121,155-159,175-179,302-303`) are reported in the
+ *    device status word of that scenario (INTF_ST_* bit flags).
+ *  - intf_last_error() returns a description of the most recent failure.
+ *  - Reentrant per stream; one process per GPU for multi-GPU runs.
+ */
+#ifndef INTFSIM_B200_H
+#define INTFSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define INTF_ABI_VERSION 1
+
+/* return codes */
+#define INTF_OK 0
+#define INTF_E_BAD_INPUT 1  /* ValueError / ScenarioError / ProfileError analogue */
+#define INTF_E_CUDA 2       /* CUDA launch or runtime error */
+#define INTF_E_NONFINITE 3  /* PredictError (`predict.py:34-36`) */
+
+/* device status bits, one int32 per scenario (SimulationError analogues) */
+#define INTF_ST_PAST_EVENT 1      /* `simcore.py:118-121,205-206` */
+#define INTF_ST_CAP 2             /* `simcore.py:155-159` */
+#define INTF_ST_PROGRESS 4        /* `simcore.py:175-179` */
+#define INTF_ST_NONQUIESCENT 8    /* `simcore.py:302-303` */
+#define INTF_ST_OVERFLOW 16       /* a caller capacity (requests/segments) was too small: grow and retry */
+#define INTF_ST_SEG_STRIDE 32     /* a batch exceeded seg_stride open segments: grow and retry */
+
+/* Profile table (`profiles.py:18-66`): row = model_index*max_bs + (bs-1). */
+typedef struct intf_table {
+  const double *solo_ms; /* [n_rows] solo_duration_ms */
+  const double *thr;     /* [n_rows*3] (l2, dram, sm) throughput fractions */
+  int32_t n_rows, max_bs;
+} intf_table;
+
+/* One scenario (`workload.py:35-58` ScenarioSpec + `oracle.py:13-19`). */
+typedef struct intf_scenario {
+  int32_t n_models, model_off; /* deployed models: intf_model[model_off .. +n_models) */
+  int32_t req_off, req_cap;    /* request / batch slot region */
+  int32_t seg_off, seg_cap;    /* segment region */
+  int32_t max_bs, cap;         /* max_batch_size, concurrency_cap */
+  double duration_s, window_ms, sigma;
+  double beta[3];              /* (l2, dram, sm) contention sensitivities */
+  uint64_t seed, oracle_seed;  /* arrival seed, InterferenceOracle.seed */
+} intf_scenario;
+
+/* One deployed model of a scenario (`workload.py:22-32` DeployedModel). */
+typedef struct intf_model {
+  int32_t entry_base;          /* table row of (model, bs=1) */
+  int32_t name_rank;           /* rank of model_id among the scenario's ids in str order */
+  uint32_t crc;                /* zlib crc32(model_id) (`profiles.py:239-243`) */
+  int32_t list_off, list_cap;  /* per-model arrival list region */
+  int32_t scen;                /* index of the owning scenario */
+  double rate_rps, slo_ms;
+} intf_model;
+
+/* A batch of scenarios: descriptor arrays in device memory plus host-side
+ * totals (so launches need no device->host reads). */
+typedef struct intf_batch {
+  const intf_scenario *scen;   /* device [n_scen] */
+  const intf_model *models;    /* device [n_models] */
+  int32_t n_scen, n_models;    /* totals */
+  int32_t max_req_cap;         /* max over scenarios of req_cap */
+  int32_t pad_;
+} intf_batch;
+
+/* Device buffers of the replay pipeline.  Index spaces:
+ *   request / batch / outcome slot: req_off + i   (i < req_cap)
+ *   per-model list:                 list_off + j  (j < list_cap)
+ *   segment:                        seg_off + k   (k < seg_cap)      */
+typedef struct intf_replay_buffers {
+  double *arr_t;       /* arrival_time_ms, merged, (t, model_id) order */
+  int32_t *arr_model;  /* deployed-model index */
+  double *list_t;      /* per-model arrival times */
+  int32_t *list_rid;   /* per-model request ids */
+  int32_t *n_req;      /* [n_scen] */
+  int32_t *n_list;     /* [total models] */
+  int32_t *b_model, *b_size;   /* per batch id */
+  double *b_formed, *b_start, *b_completion, *b_measured;
+  int32_t *b_seg_off, *b_nseg; /* absolute segment index, count */
+  int32_t *out_order;          /* batch id of the k-th outcome, (completion, batch_id) order */
+  int32_t *r_batch;            /* per request */
+  uint8_t *r_slo_met;          /* per request (written by intf_slo_report) */
+  double *s_tbegin, *s_tend, *s_slowdown, *s_colo; /* s_colo: [3*k] */
+  int32_t *n_batches, *n_segments, *n_reseats, *status; /* [n_scen] */
+  double *slot_seg;            /* scratch: n_scen*cap_max*seg_stride*5 doubles */
+  int32_t seg_stride, cap_max;
+} intf_replay_buffers;
+
+/* generate_arrivals (`workload.py:74-104`): per-model Poisson streams
+ * (PCG64 keyed by [seed, crc32(model)], glibc log1p), merged by
+ * (t, model_id).  Fills list_t/list_rid/n_list and arr_t/arr_model/n_req.
+ * `scen`, `models`: device arrays. */
+int intf_generate_arrivals(const intf_batch *batch, const intf_replay_buffers *buf, void *stream);
+
+/* Build per-model lists from caller-supplied merged arrivals (arr_t,
+ * arr_model, n_req) -- for traces not produced by intf_generate_arrivals. */
+int intf_split_arrivals(const intf_batch *batch, const intf_replay_buffers *buf, void *stream);
+
+/* run_scenario (`simcore.py:218-310`): dynamic batching (`batcher.py:59-85`),
+ * FIFO capped admission and reseats (`simcore.py:126-171`), noise
+ * (`oracle.py:24-33`), slowdown (`oracle.py:36-47`), completion
+ * (`simcore.py:56-66,173-198`), request->batch records (`:264-279`).
+ * Bit-exact with the reference.  One CUDA thread per scenario. */
+int intf_replay(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf, void *stream);
+
+/* Per-(scenario, model) SLO report (`metrics.py:49-79`, nearest-rank
+ * `percentile` `:28-36`) plus per-request slo_met (`simcore.py:268-277`).
+ * warm_cutoff: device [n_scen] arrival-time cutoff or NULL (no warm-up trim).
+ * Outputs indexed by model_off+m: n, met (int32), p (double[3]: p50,p95,p99). */
+int intf_slo_report(const intf_batch *batch, const intf_replay_buffers *buf, const double *warm_cutoff,
+                    int32_t *out_n, int32_t *out_met, double *out_p, void *stream);
+
+/* Feature mode + linear predictor (`colocation.py:14-35`, `predict.py:26-44`). */
+typedef struct intf_predictor {
+  int32_t ewma;  /* 0 = static snapshot, 1 = EWMA */
+  int32_t pad_;
+  double alpha;  /* EWMA alpha in (0, 1] */
+  double w[7];   /* w0..w5, b */
+} intf_predictor;
+
+/* samples_from_outcomes + predict (`colocation.py:95-105`, `predict.py:43-44`)
+ * over replay outputs, one sample per outcome in outcome order:
+ *   X[p][req_off+k][6] (f64), y[req_off+k] (f64), yhat[p][req_off+k] (f64)
+ * for each of the n_pred predictors (host array).  X may be NULL. */
+int intf_features_predict(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf,
+                          const intf_predictor *preds, int32_t n_pred, int64_t slot_stride, double *X, double *y,
+                          double *yhat, void *stream);
+
+/* Candidate co-location sets: every own table row x
+ * every multiset of <= cap-1 peer rows, implicitly enumerated.  For each of
+ * n_dec decisions and each candidate writes the coarse (static + coarse
+ * model) and fine (EWMA(alpha) over the departure history + fine model)
+ * predicted interference ratio as fp32:
+ *   out[((dec*2 + {0 coarse,1 fine}) * n_cand) + c].
+ * coefs: device [n_dec][2][7] (w0..w5, b).  Candidate order: own-major, then
+ * multisets in colex order of size 0,1,..,cap-1.           */
+int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t *n_cand);
+int intf_predict_candidates(const intf_table *table, int32_t cap, double alpha, const double *coefs, int32_t n_dec,
+                            float *out, void *stream);
+/* Host-buffer variant (the end-to-end call): copies coefs in and all
+ * predictions out (pinned or pageable host memory).                        */
+int intf_predict_candidates_host(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
+                                 int32_t n_dec, float *h_out, float *d_scratch, void *stream);
+
+/* OLS normal-equation statistics (`predict.py:53-66`, `rls_init` `:112-131`):
+ * for n samples X[n][6] (f64), y[n] accumulate G = Z^T Z (7x7, row-major,
+ * full), r = Z^T y (7), with Z = [X, 1].  out: device double[56] (G then r);
+ * accumulates (+=) so several shards / ranks can be summed.                 */
+int intf_ols_stats(const double *X, const double *y, int64_t n, double *out, void *stream);
+/* Solve the 7x7 system from stats (fp64): rank test mirroring
+ * np.linalg.matrix_rank on the Gram eigenvalues, ridge fallback
+ * (RIDGE_EPS=1e-8) when rank-deficient, else Cholesky.  out_params[7]
+ * (w0..w5, b); out_info[0] = 1 if the ridge fallback was used; out_Pinv
+ * (optional, 49) = inv(Z^T Z) for rls_init.                                 */
+int intf_ols_solve(const double *stats, double *out_params, int32_t *out_info, double *out_Pinv, void *stream);
+
+/* Prequential online learners (`predict.py:75-205`, `score_and_update`):
+ * n_streams independent streams, stream s = samples [off[s], off[s+1]) of
+ * X/y.  Each stream starts from params0[s][7] (and P0[s][49] for RLS),
+ * scores each sample before updating, writes the pre-update prediction to
+ * pred[i] and the final params (and P) back in place.                        */
+int intf_sgd_streams(const double *X, const double *y, const int64_t *off, int32_t n_streams, const double *eta,
+                     double *params, double *pred, int32_t *status, void *stream);
+int intf_rls_streams(const double *X, const double *y, const int64_t *off, int32_t n_streams, const double *lam,
+                     double *params, double *P, double *pred, int32_t *status, void *stream);
+
+/* EvalReport (`predict.py:176-205`): per segment s of [off[s], off[s+1])
+ * out[s][6] = (mse, rel_p25, rel_p50, rel_p75, rel_p95, n).                  */
+int intf_eval_report(const double *yhat, const double *y, const int64_t *off, int32_t n_seg, double *out,
+                     void *stream);
+
+/* last error text (thread-local); returns strlen */
+int intf_last_error(char *buf, int32_t n);
+int intf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INTFSIM_B200_H */

@@ -1,0 +1,32 @@
+// capi_common.h -- error plumbing shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/intfsim_b200.h"
+
+namespace intf {
+
+void set_last_error(const char* fmt, ...);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// check the launch that was just issued
+inline int launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_error("%s: %s", what, cudaGetErrorString(e));
+    return INTF_E_CUDA;
+  }
+  return INTF_OK;
+}
+
+inline int bad_input(const char* what) {
+  set_last_error("%s", what);
+  return INTF_E_BAD_INPUT;
+}
+
+inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace intf

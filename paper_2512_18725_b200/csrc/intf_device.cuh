@@ -1,0 +1,329 @@
+// intf_device.cuh -- bit-exact device arithmetic under the reference replay.
+//
+// The reference's noise draw (`oracle.py:24-33`) is
+//   np.random.default_rng([oracle.seed, batch_id, seg_idx]).lognormal(0, sigma)
+// i.e. numpy SeedSequence -> PCG64 -> 256-level ziggurat normal -> glibc exp,
+// and its arrivals (`workload.py:85-90`) use PCG64 doubles + glibc log1p.
+// Everything here is written so that the sm_100a result is bit-identical to
+// the x86 host the reference runs on:
+//   * the whole translation unit is compiled with -fmad=false, so a*b+c is
+//     two roundings unless written as fma();
+//   * exp/log1p follow the glibc 2.39 FMA builds (libm+0x79b60 /
+//     libm+0x7aff0) operation by operation, including which products are
+//     fused;
+//   * ddot for n<=7 is an fma chain from 0 (OpenBLAS tail loop).
+#pragma once
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+// INTF_HOST_CHECK: the same source compiled by g++ (-ffp-contract=off) into a
+// test-only host library (tests/hostcheck), used to debug the recurrence
+// logic without a GPU.  The shipped library is the sm_100a build only.
+#ifdef INTF_HOST_CHECK
+#define INTF_FN static inline
+#define INTF_NOINLINE static
+#define INTF_TABLE_QUAL
+#else
+#define INTF_FN __device__ __forceinline__
+#define INTF_NOINLINE __device__ __noinline__
+#define INTF_TABLE_QUAL __device__
+#endif
+
+#include "intf_tables.h"
+
+namespace intf {
+
+#ifdef INTF_HOST_CHECK
+INTF_FN uint64_t bits(double x) { uint64_t u; memcpy(&u, &x, 8); return u; }
+INTF_FN double dbl(uint64_t u) { double x; memcpy(&x, &u, 8); return x; }
+#else
+INTF_FN uint64_t bits(double x) { return (uint64_t)__double_as_longlong(x); }
+INTF_FN double dbl(uint64_t u) { return __longlong_as_double((long long)u); }
+#endif
+
+// ------------------------------------------------------------------ exp
+INTF_NOINLINE double exp_special(double tmp, uint64_t sbits, uint64_t ki) {
+  if ((ki & 0x80000000ull) == 0) {
+    sbits -= 1009ull << 52;
+    double scale = dbl(sbits);
+    return 0x1p1009 * fma(scale, tmp, scale);
+  }
+  sbits += 1022ull << 52;
+  double scale = dbl(sbits);
+  double st = tmp * scale;
+  double y = scale + st;
+  if (1.0 > y) {
+    double hi = y + 1.0;
+    double lo = (scale - y) + st;
+    double t = ((1.0 - hi) + y) + lo;
+    y = (t + hi) - 1.0;
+    if (y == 0.0) y = 0.0;
+  }
+  return 0x1p-1022 * y;
+}
+
+// glibc __exp (AVX2/FMA build): exp(x) = 2^(k/128) * exp(r).
+INTF_FN double glibc_exp(double x) {
+  const double InvLn2N = dbl(INTF_EXP_INVLN2N_BITS), Shift = dbl(INTF_EXP_SHIFT_BITS);
+  const double NegLn2hiN = dbl(INTF_EXP_NEGLN2HIN_BITS), NegLn2loN = dbl(INTF_EXP_NEGLN2LON_BITS);
+  const double C2 = dbl(INTF_EXP_C2_BITS), C3 = dbl(INTF_EXP_C3_BITS);
+  const double C4 = dbl(INTF_EXP_C4_BITS), C5 = dbl(INTF_EXP_C5_BITS);
+  uint64_t ix = bits(x);
+  uint32_t abstop = (uint32_t)(ix >> 52) & 0x7ffu;
+  if (abstop - 0x3c9u > 0x3eu) {
+    if ((int32_t)(abstop - 0x3c9u) < 0) return 1.0 + x;
+    if (abstop > 0x408u) {
+      if (ix == 0xfff0000000000000ull) return 0.0;
+      if (abstop == 0x7ffu) return 1.0 + x;
+      return (ix >> 63) ? 0.0 : dbl(0x7ff0000000000000ull);
+    }
+    abstop = 0;
+  }
+  double kd = fma(x, InvLn2N, Shift);
+  uint64_t ki = bits(kd);
+  kd = kd - Shift;
+  double r = fma(kd, NegLn2hiN, x);
+  r = fma(kd, NegLn2loN, r);
+  uint32_t idx = 2u * (uint32_t)(ki & 0x7f);
+  uint64_t top = ki << 45;
+  double tail_r = r + dbl(INTF_EXP_TAB[idx]);
+  uint64_t sbits = INTF_EXP_TAB[idx + 1] + top;
+  double r2 = r * r;
+  double p23 = fma(r, C3, C2);
+  double p45 = fma(r, C5, C4);
+  double t = fma(p23, r2, tail_r);
+  double tmp = fma(r2 * r2, p45, t);
+  if (abstop == 0) return exp_special(tmp, sbits, ki);
+  double scale = dbl(sbits);
+  return fma(scale, tmp, scale);
+}
+
+// ---------------------------------------------------------------- log1p
+// glibc __log1p (fdlibm s_log1p.c), AVX2/FMA build.
+INTF_NOINLINE double glibc_log1p(double x) {
+  const double Lp1 = 0x1.5555555555593p-1, Lp2 = 0x1.999999997fa04p-2, Lp3 = 0x1.2492494229359p-2,
+               Lp4 = 0x1.c71c51d8e78afp-3, Lp5 = 0x1.7466496cb03dep-3, Lp6 = 0x1.39a09d078c69fp-3,
+               Lp7 = 0x1.2f112df3e5244p-3;
+  const double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
+  const double two3rd = 0x1.5555555555555p-1;
+  uint64_t ix = bits(x);
+  int32_t hx = (int32_t)(ix >> 32);
+  uint32_t hu = 0;
+  int k = 0;
+  double c = 0.0, u = 0.0, f, hfsq;
+  bool poly_direct = false;
+  if (hx > 0x3fda8279) {
+    if (hx > 0x7fefffff) return x + x;
+    if (hx > 0x433fffff) {
+      k = (hx >> 20) - 1023;
+      hu = (uint32_t)hx;
+      u = x;
+      c = 0.0;
+      goto normalize;
+    }
+  } else {
+    uint32_t ax = (uint32_t)hx & 0x7fffffffu;
+    if (ax > 0x3fefffffu) {
+      if (x == -1.0) return dbl(0xfff0000000000000ull);
+      return (x - x) / (x - x);
+    }
+    if (ax <= 0x3e1fffffu) {
+      if (ax <= 0x3c8fffffu) return x;
+      return fma(-(x * x), 0.5, x);
+    }
+    if ((uint32_t)((uint32_t)hx + 0x402d413cu) > 0x402d413cu) poly_direct = true;
+  }
+  if (poly_direct) {
+    k = 0;
+    f = x;
+    hfsq = (x * 0.5) * x;
+  } else {
+    u = x + 1.0;
+    hu = (uint32_t)(bits(u) >> 32);
+    k = ((int32_t)hu >> 20) - 1023;
+    c = (k > 0) ? 1.0 - (u - x) : x - (u - 1.0);
+    c = c / u;
+  normalize:
+    hu &= 0xfffffu;
+    if (hu > 0x6a09du) {
+      k += 1;
+      u = dbl(((uint64_t)(hu | 0x3fe00000u) << 32) | (bits(u) & 0xffffffffull));
+      hu = (0x00100000u - hu) >> 2;
+    } else {
+      u = dbl(((uint64_t)(hu | 0x3ff00000u) << 32) | (bits(u) & 0xffffffffull));
+    }
+    f = u - 1.0;
+    hfsq = (f * 0.5) * f;
+    if (hu == 0) {
+      if (f == 0.0) {
+        if (k == 0) return 0.0;
+        c = fma((double)k, ln2_lo, c);
+        return fma((double)k, ln2_hi, c);
+      }
+      double R = fma(-f, two3rd, 1.0) * hfsq;
+      if (k == 0) return f - R;
+      double t = fma((double)k, ln2_lo, c);
+      return fma((double)k, ln2_hi, -((R - t) - f));
+    }
+  }
+  double s = f / (f + 2.0);
+  double z = s * s;
+  double R2 = fma(z, Lp3, Lp2);
+  double R3 = fma(z, Lp5, Lp4);
+  double R4 = fma(z, Lp7, Lp6);
+  double z2 = z * z;
+  double z4 = z2 * z2;
+  double z6 = z2 * z4;
+  double R = fma(z, Lp1, z2 * R2);
+  R = fma(z4, R3, R);
+  R = fma(z6, R4, R);
+  double sh = (R + hfsq) * s;
+  if (k == 0) return f - (hfsq - sh);
+  double t = fma((double)k, ln2_lo, c);
+  t = t + sh;
+  t = hfsq - t;
+  t = t - f;
+  return fma((double)k, ln2_hi, -t);
+}
+
+// ------------------------------------------------- SeedSequence / PCG64
+// numpy SeedSequence(pool_size=4).generate_state(4, uint64) over entropy
+// words; at most 8 words here (seed <= 2^64, batch id, segment index).
+struct Pcg64 {
+  unsigned __int128 state, inc;
+};
+
+INTF_FN uint32_t ss_hashmix(uint32_t v, uint32_t& hc) {
+  v ^= hc;
+  hc *= 0x931e8875u;
+  v *= hc;
+  v ^= v >> 16;
+  return v;
+}
+INTF_FN uint32_t ss_mix(uint32_t x, uint32_t y) {
+  uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+  return r ^ (r >> 16);
+}
+
+INTF_FN void pcg_step(Pcg64& g) {
+  const unsigned __int128 mult =
+      ((unsigned __int128)0x2360ed051fc65da4ull << 64) | (unsigned __int128)0x4385df649fccf645ull;
+  g.state = g.state * mult + g.inc;
+}
+INTF_FN uint64_t pcg_next64(Pcg64& g) {
+  pcg_step(g);
+  uint64_t hi = (uint64_t)(g.state >> 64), lo = (uint64_t)g.state;
+  uint32_t rot = (uint32_t)(hi >> 58);
+  uint64_t v = hi ^ lo;
+  return (v >> rot) | (v << ((64u - rot) & 63u));
+}
+INTF_FN double pcg_next_double(Pcg64& g) {
+  return (double)(pcg_next64(g) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// words: entropy as uint32 words (n in [1, 8]).
+INTF_FN Pcg64 pcg_seed_words(const uint32_t* w, int n) {
+  uint32_t pool[4];
+  uint32_t hc = 0x43b0d7e5u;
+#pragma unroll
+  for (int i = 0; i < 4; i++) pool[i] = ss_hashmix(i < n ? w[i] : 0u, hc);
+#pragma unroll
+  for (int s = 0; s < 4; s++)
+#pragma unroll
+    for (int d = 0; d < 4; d++)
+      if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], hc));
+  for (int s = 4; s < n; s++)
+#pragma unroll
+    for (int d = 0; d < 4; d++) pool[d] = ss_mix(pool[d], ss_hashmix(w[s], hc));
+  uint32_t hb = 0x8b51f9ddu, out[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    uint32_t v = pool[i & 3] ^ hb;
+    hb *= 0x58f38dedu;
+    v *= hb;
+    out[i] = v ^ (v >> 16);
+  }
+  uint64_t s0 = (uint64_t)out[0] | ((uint64_t)out[1] << 32), s1 = (uint64_t)out[2] | ((uint64_t)out[3] << 32);
+  uint64_t s2 = (uint64_t)out[4] | ((uint64_t)out[5] << 32), s3 = (uint64_t)out[6] | ((uint64_t)out[7] << 32);
+  Pcg64 g;
+  g.state = 0;
+  g.inc = ((((unsigned __int128)s2 << 64) | s3) << 1) | 1u;
+  pcg_step(g);
+  g.state += ((unsigned __int128)s0 << 64) | s1;
+  pcg_step(g);
+  return g;
+}
+
+// numpy _int_to_uint32_array: little-endian 32-bit words, 0 -> [0].
+INTF_FN int push_words(uint32_t* w, int n, uint64_t v) {
+  if (v == 0) {
+    w[n++] = 0;
+    return n;
+  }
+  while (v) {
+    w[n++] = (uint32_t)v;
+    v >>= 32;
+  }
+  return n;
+}
+
+// numpy random_standard_normal: 256-level ziggurat (tables: intf_tables.h).
+INTF_NOINLINE double zig_normal_slow(Pcg64& g, int idx, uint64_t rabs, double x, bool& accept) {
+  const double r_ = 3.6541528853610088, inv_r = 0.27366123732975828;
+  if (idx == 0) {
+    for (;;) {
+      double xx = -inv_r * glibc_log1p(-pcg_next_double(g));
+      double yy = -glibc_log1p(-pcg_next_double(g));
+      if (yy + yy > xx * xx) {
+        accept = true;
+        return ((rabs >> 8) & 1) ? -(r_ + xx) : r_ + xx;
+      }
+    }
+  }
+  double fi1 = dbl(INTF_ZIG_FI_BITS[idx - 1]), fi0 = dbl(INTF_ZIG_FI_BITS[idx]);
+  accept = ((fi1 - fi0) * pcg_next_double(g) + fi0) < glibc_exp(-0.5 * x * x);
+  return x;
+}
+
+INTF_FN double zig_normal(Pcg64& g) {
+  for (;;) {
+    uint64_t u = pcg_next64(g);
+    int idx = (int)(u & 0xff);
+    u >>= 8;
+    bool sign = u & 1;
+    uint64_t rabs = (u >> 1) & 0x000fffffffffffffull;
+    double x = (double)rabs * dbl(INTF_ZIG_WI_BITS[idx]);
+    if (sign) x = -x;
+    if (rabs < INTF_ZIG_KI[idx]) return x;
+    bool accept = false;
+    double v = zig_normal_slow(g, idx, rabs, x, accept);
+    if (accept) return v;
+  }
+}
+
+// InterferenceOracle.noise_draw (`oracle.py:24-33`).
+INTF_FN double noise_draw(uint64_t oracle_seed, uint32_t batch_id, uint32_t seg_idx, double sigma) {
+  if (sigma == 0.0) return 1.0;
+  uint32_t w[8];
+  int n = push_words(w, 0, oracle_seed);
+  n = push_words(w, n, batch_id);
+  n = push_words(w, n, seg_idx);
+  Pcg64 g = pcg_seed_words(w, n);
+  double z = zig_normal(g);
+  return glibc_exp(0.0 + sigma * z);
+}
+
+// oracle_slowdown (`oracle.py:36-47`); dot = OpenBLAS ddot (fma chain).
+INTF_FN double slowdown(const double own[3], const double colo[3], const double beta[3],
+                                           double noise) {
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    double v = (own[i] + colo[i]) - 1.0;
+    acc = fma(beta[i], v > 0.0 ? v : 0.0, acc);
+  }
+  return (1.0 + acc) * noise;
+}
+
+}  // namespace intf

@@ -1,0 +1,309 @@
+// replay.cu -- arrivals, scheduler replay, SLO accounting and per-outcome
+// features for batches of scenarios (sm_100a).
+//
+// Layout in HBM (see include/intfsim_b200.h): scenarios are packed
+// back-to-back; every per-request / per-batch array is indexed by
+// req_off + i, per-model arrival lists by list_off + j, segments by
+// seg_off + k.  All fp64 (the reference's arithmetic; bit-exactness needs
+// the exact IEEE operations), compiled with -fmad=false.
+#include <math.h>
+
+#include "capi_common.h"
+#include "replay_core.cuh"
+
+using namespace intf;
+
+namespace {
+
+// ---- K0a: one thread per deployed model generates its Poisson stream.
+__global__ void k_gen_arrivals(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                               int n_models_total, intf_replay_buffers B) {
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_models_total) return;
+  const intf_model M = models[g];
+  const intf_scenario S = scen[M.scen];
+  int n = gen_model_arrivals(S, M, B.list_t + M.list_off, M.list_cap);
+  if (n > M.list_cap) atomicOr(&B.status[M.scen], INTF_ST_OVERFLOW);
+  B.n_list[g] = n;
+  atomicAdd(&B.n_req[M.scen], n);
+}
+
+// ---- K0b: merge per-model lists by (t, model_id) via rank = own index +
+// elements of the other lists that precede it (binary search); one block per
+// model list.  Writes the merged arrays and each element's request id.
+__global__ void k_merge_arrivals(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                                 intf_replay_buffers B) {
+  const int g = blockIdx.x;
+  const intf_model M = models[g];
+  const intf_scenario S = scen[M.scen];
+  const int n = min(B.n_list[g], M.list_cap);
+  if (B.status[M.scen] & INTF_ST_OVERFLOW) return;
+  const double* lt = B.list_t + M.list_off;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double t = lt[j];
+    int pos = j;
+    for (int q = 0; q < S.n_models; q++) {
+      const int gq = S.model_off + q;
+      if (gq == g) continue;
+      const intf_model& Q = models[gq];
+      pos += count_before(B.list_t + Q.list_off, min(B.n_list[gq], Q.list_cap), t, Q.name_rank < M.name_rank);
+    }
+    if (pos < S.req_cap) {
+      B.list_rid[M.list_off + j] = pos;
+      B.arr_t[S.req_off + pos] = t;
+      B.arr_model[S.req_off + pos] = g - S.model_off;
+    }
+  }
+}
+
+// ---- split caller-supplied merged arrivals into per-model lists (serial
+// per scenario; only for externally supplied traces).
+__global__ void k_split_arrivals(const intf_scenario* __restrict__ scen, int n_scen,
+                                 const intf_model* __restrict__ models, intf_replay_buffers B) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_scen) return;
+  const intf_scenario S = scen[s];
+  int cnt[kMaxModels];
+  for (int m = 0; m < S.n_models && m < kMaxModels; m++) cnt[m] = 0;
+  const int n = B.n_req[s];
+  int st = 0;
+  for (int i = 0; i < n; i++) {
+    const int m = B.arr_model[S.req_off + i];
+    const intf_model& M = models[S.model_off + m];
+    if (cnt[m] < M.list_cap) {
+      B.list_t[M.list_off + cnt[m]] = B.arr_t[S.req_off + i];
+      B.list_rid[M.list_off + cnt[m]] = i;
+    } else {
+      st |= INTF_ST_OVERFLOW;
+    }
+    cnt[m]++;
+  }
+  for (int m = 0; m < S.n_models && m < kMaxModels; m++) B.n_list[S.model_off + m] = cnt[m];
+  B.status[s] |= st;
+}
+
+// ---- K2: the replay recurrence, one thread per scenario.
+__global__ void __launch_bounds__(64) k_replay(const intf_scenario* __restrict__ scen, int n_scen,
+                                               const intf_model* __restrict__ models, intf_table tab,
+                                               intf_replay_buffers B) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_scen) return;
+  if (B.status[s] & INTF_ST_OVERFLOW) return;  // arrivals did not fit
+  replay_scenario(s, scen, models, tab, B);
+}
+
+// ---- K3: SLO records + per-model nearest-rank percentiles, one block per
+// scenario.  Percentiles by 8-pass MSB radix select on the latency bits
+// (latency >= 0, so IEEE bit order == numeric order); three order
+// statistics per model share each pass's histograms (shared memory).
+constexpr int kSloThreads = 256;
+constexpr int kSloGroup = 8;  // models per radix pass group
+
+__device__ __forceinline__ unsigned long long lat_key(double v) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_lat(unsigned long long k) {
+  unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+__global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __restrict__ scen,
+                                                     const intf_model* __restrict__ models, intf_replay_buffers B,
+                                                     const double* __restrict__ warm_cutoff, int32_t* out_n,
+                                                     int32_t* out_met, double* out_p) {
+  const int s = blockIdx.x;
+  const intf_scenario S = scen[s];
+  const int n = B.n_req[s];
+  const int ro = S.req_off;
+  __shared__ int cnt_n[kMaxModels], cnt_met[kMaxModels];
+  __shared__ unsigned int hist[kSloGroup][3][256];
+  __shared__ unsigned long long prefix[kSloGroup][3];
+  __shared__ int rank_left[kSloGroup][3];
+  __shared__ int use_all;
+  if ((B.status[s] & (INTF_ST_OVERFLOW | INTF_ST_SEG_STRIDE)) || S.n_models > kMaxModels) return;
+  const double cutoff = warm_cutoff ? warm_cutoff[s] : -INFINITY;
+  for (int m = threadIdx.x; m < kMaxModels; m += blockDim.x) cnt_n[m] = cnt_met[m] = 0;
+  if (threadIdx.x == 0) use_all = 0;
+  __syncthreads();
+  // pass 0: records (`simcore.py:264-279`) and counts
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int b = B.r_batch[ro + i];
+    const double at = B.arr_t[ro + i];
+    const int m = B.arr_model[ro + i];
+    const double lat = B.b_completion[ro + b] - at;
+    const bool met = lat <= models[S.model_off + m].slo_ms;
+    B.r_slo_met[ro + i] = met;
+    if (at >= cutoff) {
+      atomicAdd(&cnt_n[m], 1);
+      atomicAdd(&cnt_met[m], met ? 1 : 0);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int m = 0; m < S.n_models; m++) tot += cnt_n[m];
+    if (tot == 0 && n > 0) use_all = 1;  // `metrics.py:67`: trimmed or records
+  }
+  __syncthreads();
+  if (use_all) {
+    __syncthreads();
+    for (int m = threadIdx.x; m < kMaxModels; m += blockDim.x) cnt_n[m] = cnt_met[m] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int m = B.arr_model[ro + i];
+      atomicAdd(&cnt_n[m], 1);
+      atomicAdd(&cnt_met[m], B.r_slo_met[ro + i] ? 1 : 0);
+    }
+    __syncthreads();
+  }
+  const double cut = use_all ? -INFINITY : cutoff;
+  for (int m = threadIdx.x; m < S.n_models; m += blockDim.x) {
+    out_n[S.model_off + m] = cnt_n[m];
+    out_met[S.model_off + m] = cnt_met[m];
+  }
+  const double pq[3] = {50.0, 95.0, 99.0};
+  for (int g0 = 0; g0 < S.n_models; g0 += kSloGroup) {
+    const int gm = min(kSloGroup, S.n_models - g0);
+    if (threadIdx.x < gm * 3) {
+      const int mm = threadIdx.x / 3, q = threadIdx.x % 3;
+      const int nm = cnt_n[g0 + mm];
+      // rank = max(1, ceil(p/100 * n)) (`metrics.py:35`)
+      int rk = (int)ceil((pq[q] / 100.0) * (double)nm);
+      rk = rk < 1 ? 1 : rk;
+      rank_left[mm][q] = rk - 1;
+      prefix[mm][q] = 0ull;
+    }
+    for (int pass = 0; pass < 8; pass++) {
+      const int shift = 56 - 8 * pass;
+      for (int k = threadIdx.x; k < kSloGroup * 3 * 256; k += blockDim.x) (&hist[0][0][0])[k] = 0u;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int m = B.arr_model[ro + i] - g0;
+        if (m < 0 || m >= gm) continue;
+        const double at = B.arr_t[ro + i];
+        if (!(at >= cut)) continue;
+        const unsigned long long key = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
+        const unsigned int d = (unsigned int)(key >> shift) & 0xffu;
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+          const bool match = pass == 0 || ((key ^ prefix[m][q]) >> (shift + 8)) == 0ull;
+          if (match) atomicAdd(&hist[m][q][d], 1u);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < gm * 3) {
+        const int mm = threadIdx.x / 3, q = threadIdx.x % 3;
+        int left = rank_left[mm][q];
+        unsigned int d = 0;
+        for (; d < 255u; d++) {
+          const int h = (int)hist[mm][q][d];
+          if (left < h) break;
+          left -= h;
+        }
+        rank_left[mm][q] = left;
+        prefix[mm][q] |= (unsigned long long)d << shift;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < gm * 3) {
+      const int mm = threadIdx.x / 3, q = threadIdx.x % 3;
+      out_p[3 * (S.model_off + g0 + mm) + q] = cnt_n[g0 + mm] ? key_lat(prefix[mm][q]) : NAN;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- K4+K5: features + predictions per outcome; grid (chunks, scenarios).
+constexpr int kMaxPred = 8;
+struct PredBlock {
+  intf_predictor p[kMaxPred];
+};
+
+__global__ void k_features(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                           intf_table tab, intf_replay_buffers B, PredBlock P, int n_pred, long long slot_stride,
+                           double* __restrict__ X, double* __restrict__ Y, double* __restrict__ Yhat) {
+  const int s = blockIdx.y;
+  const intf_scenario& S = scen[s];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= B.n_batches[s]) return;
+  const long long slot = (long long)S.req_off + k;
+  const int b = B.out_order[slot];
+  const long long bslot = (long long)S.req_off + b;
+  const int entry = models[S.model_off + B.b_model[bslot]].entry_base + B.b_size[bslot] - 1;
+  const double own[3] = {tab.thr[3 * entry], tab.thr[3 * entry + 1], tab.thr[3 * entry + 2]};
+  const double* colo = B.s_colo + 3ll * B.b_seg_off[bslot];
+  const int nseg = B.b_nseg[bslot];
+  Y[slot] = B.b_measured[bslot] / tab.solo_ms[entry];  // interference ratio (`simcore.py:83-85`)
+  for (int p = 0; p < n_pred; p++) {
+    double x[6];
+    features_one(own, colo, nseg, P.p[p].ewma, P.p[p].alpha, x);
+    if (X) {
+      double* xo = X + (p * slot_stride + slot) * 6;
+#pragma unroll
+      for (int i = 0; i < 6; i++) xo[i] = x[i];
+    }
+    Yhat[p * slot_stride + slot] = predict7(P.p[p].w, x);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, void* stream) {
+  if (!bt || !bt->scen || !bt->models || !buf || bt->n_scen <= 0) return bad_input("intf_generate_arrivals: null argument");
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(buf->n_req, 0, sizeof(int32_t) * bt->n_scen, st);
+  cudaMemsetAsync(buf->status, 0, sizeof(int32_t) * bt->n_scen, st);
+  if (bt->n_models <= 0) return INTF_OK;
+  int rc;
+  k_gen_arrivals<<<ceil_div(bt->n_models, 64), 64, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+  if ((rc = launch_status("k_gen_arrivals"))) return rc;
+  k_merge_arrivals<<<bt->n_models, 256, 0, st>>>(bt->scen, bt->models, *buf);
+  return launch_status("k_merge_arrivals");
+}
+
+int intf_split_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, void* stream) {
+  if (!bt || !bt->scen || !bt->models || !buf || bt->n_scen <= 0) return bad_input("intf_split_arrivals: null argument");
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(buf->status, 0, sizeof(int32_t) * bt->n_scen, st);
+  k_split_arrivals<<<ceil_div(bt->n_scen, 64), 64, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
+  return launch_status("k_split_arrivals");
+}
+
+int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf, void* stream) {
+  if (!bt || !bt->scen || !bt->models || !buf || !table || bt->n_scen <= 0) return bad_input("intf_replay: null argument");
+  if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1)
+    return bad_input("intf_replay: cap_max must be in [1, 8] and seg_stride >= 1");
+  k_replay<<<ceil_div(bt->n_scen, 64), 64, 0, as_stream(stream)>>>(bt->scen, bt->n_scen, bt->models, *table, *buf);
+  return launch_status("k_replay");
+}
+
+int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const double* warm_cutoff, int32_t* out_n,
+                    int32_t* out_met, double* out_p, void* stream) {
+  if (!bt || !bt->scen || !bt->models || !buf || !out_n || !out_met || !out_p || bt->n_scen <= 0)
+    return bad_input("intf_slo_report: null argument");
+  k_slo<<<bt->n_scen, kSloThreads, 0, as_stream(stream)>>>(bt->scen, bt->models, *buf, warm_cutoff, out_n, out_met,
+                                                          out_p);
+  return launch_status("k_slo");
+}
+
+int intf_features_predict(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
+                          const intf_predictor* preds, int32_t n_pred, int64_t slot_stride, double* X, double* y,
+                          double* yhat, void* stream) {
+  if (!bt || !bt->scen || !bt->models || !buf || !table || !y || (n_pred && !yhat) || bt->n_scen <= 0 ||
+      bt->n_scen > 65535)
+    return bad_input("intf_features_predict: bad argument");
+  if (n_pred < 0 || n_pred > kMaxPred || (n_pred && !preds)) return bad_input("intf_features_predict: n_pred in [0,8]");
+  PredBlock P;
+  memset(&P, 0, sizeof(P));
+  for (int i = 0; i < n_pred; i++) P.p[i] = preds[i];
+  if (bt->max_req_cap <= 0) return INTF_OK;
+  dim3 grid(ceil_div(bt->max_req_cap, 128), bt->n_scen);
+  k_features<<<grid, 128, 0, as_stream(stream)>>>(bt->scen, bt->models, *table, *buf, P, n_pred,
+                                                  (long long)slot_stride, X, y, yhat);
+  return launch_status("k_features");
+}
+
+}  // extern "C"
