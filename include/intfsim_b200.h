@@ -167,8 +167,10 @@ int intf_predict_candidates_host(const intf_table *table, int32_t cap, double al
 /* OLS normal-equation statistics (`predict.py:53-66`, `rls_init` `:112-131`):
  * for n samples X[n][6] (f64), y[n] accumulate G = Z^T Z (7x7, row-major,
  * full), r = Z^T y (7), with Z = [X, 1].  out: device double[56] (G then r);
- * accumulates (+=) so several shards / ranks can be summed.                 */
-int intf_ols_stats(const double *X, const double *y, int64_t n, double *out, void *stream);
+ * accumulates (+=) so several shards / ranks can be summed.  Deterministic:
+ * fixed-order two-stage reduction through `ws` (INTF_OLS_WS_DOUBLES).       */
+#define INTF_OLS_WS_DOUBLES (592 * 35) /* workspace for intf_ols_stats (per-block partials) */
+int intf_ols_stats(const double *X, const double *y, int64_t n, double *out, double *ws, void *stream);
 /* Solve the 7x7 system from stats (fp64): rank test mirroring
  * np.linalg.matrix_rank on the Gram eigenvalues, ridge fallback
  * (RIDGE_EPS=1e-8) when rank-deficient, else Cholesky.  out_params[7]
@@ -190,6 +192,45 @@ int intf_rls_streams(const double *X, const double *y, const int64_t *off, int32
  * out[s][6] = (mse, rel_p25, rel_p50, rel_p75, rel_p95, n).                  */
 int intf_eval_report(const double *yhat, const double *y, const int64_t *off, int32_t n_seg, double *out,
                      void *stream);
+
+/* ---- array-level entry points behind the per-object reference API ---- */
+
+/* samples_from_outcomes over arbitrary outcome rows (`colocation.py:95-105`):
+ * row i has own throughputs own[3i..3i+2], colo history colo[3*(seg_off[i]+k)]
+ * for k < nseg[i]; y[i] = measured[i]/profiled[i] (`simcore.py:83-85`);
+ * X[p][i][6], yhat[p][i] per predictor.  X, y, yhat may be NULL.           */
+int intf_features_rows(const double *own, const int64_t *seg_off, const int32_t *nseg, const double *colo,
+                       const double *measured, const double *profiled, int64_t n, const intf_predictor *preds,
+                       int32_t n_pred, double *X, double *y, double *yhat, void *stream);
+
+/* predict (`predict.py:43-44`) for rows X[n][6] and one model w[7]. */
+int intf_predict_rows(const double *X, int64_t n, const double *w, double *out, void *stream);
+
+/* nearest-rank percentiles (`metrics.py:28-36`) of values[n] at ps[nq]
+ * (nq <= 8), one block, exact (radix select on IEEE bit order).            */
+int intf_quantiles(const double *values, int64_t n, const double *ps, int32_t nq, double *out, void *stream);
+
+/* slo_report over record arrays (`metrics.py:49-79`): per group g < n_groups
+ * the count, met count and p50/p95/p99 of completion - arrival over records
+ * with arrival >= cutoff (pass -inf for no warm-up trim).                    */
+int intf_latency_report(const int32_t *group, const double *arrival, const double *completion, const uint8_t *met,
+                        int64_t n, int32_t n_groups, double cutoff, int32_t *out_n, int32_t *out_met, double *out_p,
+                        void *stream);
+
+/* InterferenceOracle.noise_draw (`oracle.py:24-33`) for n keys: lognormal
+ * noise of default_rng([seed, batch[i], seg[i]]), bit-exact.              */
+int intf_noise_draws(uint64_t seed, double sigma, const int64_t *batch, const int64_t *seg, int64_t n, double *out,
+                     void *stream);
+
+/* oracle_slowdown (`oracle.py:36-47`) for n rows: own[3i..], colo[3i..],
+ * beta[3] (device), noise[n] (device, or NULL = 1.0).                      */
+int intf_slowdowns(const double *own, const double *colo, const double *beta, const double *noise, int64_t n,
+                   double *out, void *stream);
+
+/* One numpy Generator stream (SeedSequence(words) -> PCG64): n values of
+ * standard_normal (uniform=0) or random() (uniform=1); serial, for pinning
+ * the device RNG against numpy.                                            */
+int intf_rng_stream(const uint32_t *words, int32_t n_words, int64_t n, int32_t uniform, double *out, void *stream);
 
 /* last error text (thread-local); returns strlen */
 int intf_last_error(char *buf, int32_t n);

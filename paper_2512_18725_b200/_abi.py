@@ -66,6 +66,8 @@ class Predictor(ctypes.Structure):
     _fields_ = [("ewma", c_int32), ("pad_", c_int32), ("alpha", c_double), ("w", c_double * 7)]
 
 
+OLS_WS_DOUBLES = 592 * 35
+
 # status bits (INTF_ST_*)
 ST_PAST_EVENT, ST_CAP, ST_PROGRESS, ST_NONQUIESCENT, ST_OVERFLOW, ST_SEG_STRIDE = 1, 2, 4, 8, 16, 32
 
@@ -79,11 +81,18 @@ SIGNATURES = {
     "intf_candidate_count": (c_int32, [c_int32, c_int32, P]),
     "intf_predict_candidates": (c_int32, [P, c_int32, c_double, P, c_int32, P, P]),
     "intf_predict_candidates_host": (c_int32, [P, c_int32, c_double, P, c_int32, P, P, P]),
-    "intf_ols_stats": (c_int32, [P, P, c_int64, P, P]),
+    "intf_ols_stats": (c_int32, [P, P, c_int64, P, P, P]),
     "intf_ols_solve": (c_int32, [P, P, P, P, P]),
     "intf_sgd_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P]),
     "intf_rls_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P, P]),
     "intf_eval_report": (c_int32, [P, P, P, c_int32, P, P]),
+    "intf_features_rows": (c_int32, [P, P, P, P, P, P, c_int64, P, c_int32, P, P, P, P]),
+    "intf_predict_rows": (c_int32, [P, c_int64, P, P, P]),
+    "intf_quantiles": (c_int32, [P, c_int64, P, c_int32, P, P]),
+    "intf_latency_report": (c_int32, [P, P, P, P, c_int64, c_int32, c_double, P, P, P, P]),
+    "intf_noise_draws": (c_int32, [ctypes.c_uint64, c_double, P, P, c_int64, P, P]),
+    "intf_slowdowns": (c_int32, [P, P, P, P, c_int64, P, P]),
+    "intf_rng_stream": (c_int32, [P, c_int32, c_int64, c_int32, P, P]),
     "intf_last_error": (c_int32, [ctypes.c_char_p, c_int32]),
     "intf_abi_version": (c_int32, []),
 }

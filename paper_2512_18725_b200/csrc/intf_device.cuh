@@ -26,7 +26,7 @@
 #define INTF_TABLE_QUAL
 #else
 #define INTF_FN __device__ __forceinline__
-#define INTF_NOINLINE __device__ __noinline__
+#define INTF_NOINLINE static __device__ __noinline__
 #define INTF_TABLE_QUAL __device__
 #endif
 
@@ -303,7 +303,7 @@ INTF_FN double zig_normal(Pcg64& g) {
 }
 
 // InterferenceOracle.noise_draw (`oracle.py:24-33`).
-INTF_FN double noise_draw(uint64_t oracle_seed, uint32_t batch_id, uint32_t seg_idx, double sigma) {
+INTF_FN double noise_draw(uint64_t oracle_seed, uint64_t batch_id, uint64_t seg_idx, double sigma) {
   if (sigma == 0.0) return 1.0;
   uint32_t w[8];
   int n = push_words(w, 0, oracle_seed);

@@ -220,3 +220,267 @@ def _warm_cutoffs(pipe: ReplayPipeline, frac: float):
             cut[s] = t0 + frac * (t1 - t0)
     return to_device(cut, pipe.dev)
 
+
+
+# ---------------------------------------------------------------- array ops
+def _f64(a, dev, shape=None):
+    t = torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64))
+    if shape is not None:
+        t = t.reshape(shape)
+    return t.to(dev)
+
+
+def _preds_struct(preds):
+    n = len(preds)
+    return (_abi.Predictor * max(n, 1))(*preds), n
+
+
+def features_rows(own, seg_off, nseg, colo, measured, profiled, preds, want_x=True):
+    """`colocation.py:95-105` over outcome rows -> (X[p][n][6], y[n], yhat[p][n]) numpy."""
+    dev = require_cuda()
+    n = len(seg_off)
+    P, npred = _preds_struct(preds)
+    d_own = _f64(own, dev)
+    d_off = torch.as_tensor(np.ascontiguousarray(seg_off, dtype=np.int64)).to(dev)
+    d_ns = torch.as_tensor(np.ascontiguousarray(nseg, dtype=np.int32)).to(dev)
+    d_colo = _f64(colo if len(colo) else np.zeros((1, 3)), dev)
+    d_m, d_p = _f64(measured, dev), _f64(profiled, dev)
+    X = torch.empty(max(npred, 1) * max(n, 1) * 6, dtype=torch.float64, device=dev) if want_x else None
+    y = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    yh = torch.empty(max(npred, 1) * max(n, 1), dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_features_rows(d_own.data_ptr(), d_off.data_ptr(), d_ns.data_ptr(), d_colo.data_ptr(),
+                                              d_m.data_ptr(), d_p.data_ptr(), n,
+                                              ctypes.cast(P, ctypes.c_void_p) if npred else None, npred,
+                                              _abi.addr(X), y.data_ptr(), yh.data_ptr(), stream_ptr()),
+               "intf_features_rows")
+    Xh = X.cpu().numpy()[: npred * n * 6].reshape(npred, n, 6) if want_x else None
+    return Xh, y.cpu().numpy()[:n], yh.cpu().numpy()[: npred * n].reshape(npred, n)
+
+
+def predict_rows(X, w7) -> np.ndarray:
+    dev = require_cuda()
+    X = np.asarray(X, dtype=np.float64).reshape(-1, 6)
+    n = len(X)
+    if n == 0:
+        return np.zeros(0)
+    dX, dw = _f64(X, dev), _f64(w7, dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_predict_rows(dX.data_ptr(), n, dw.data_ptr(), out.data_ptr(), stream_ptr()),
+               "intf_predict_rows")
+    return out.cpu().numpy()
+
+
+def quantiles(values, ps) -> np.ndarray:
+    dev = require_cuda()
+    v = _f64(values, dev)
+    p = _f64(ps, dev)
+    out = torch.empty(len(ps), dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_quantiles(v.data_ptr(), v.numel(), p.data_ptr(), len(ps), out.data_ptr(), stream_ptr()),
+               "intf_quantiles")
+    return out.cpu().numpy()
+
+
+def latency_report(group, arrival, completion, met, n_groups, cutoff=-np.inf):
+    dev = require_cuda()
+    g = torch.as_tensor(np.ascontiguousarray(group, dtype=np.int32)).to(dev)
+    a, c = _f64(arrival, dev), _f64(completion, dev)
+    m = torch.as_tensor(np.ascontiguousarray(met, dtype=np.uint8)).to(dev)
+    on = torch.empty(n_groups, dtype=torch.int32, device=dev)
+    om = torch.empty(n_groups, dtype=torch.int32, device=dev)
+    op = torch.empty(3 * n_groups, dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_latency_report(g.data_ptr(), a.data_ptr(), c.data_ptr(), m.data_ptr(), g.numel(),
+                                               n_groups, float(cutoff), on.data_ptr(), om.data_ptr(), op.data_ptr(),
+                                               stream_ptr()), "intf_latency_report")
+    return on.cpu().numpy(), om.cpu().numpy(), op.cpu().numpy().reshape(n_groups, 3)
+
+
+def ols_stats(X, y, out=None):
+    """Z^T Z | Z^T y accumulation (`predict.py:56-63`) -> device double[56]."""
+    dev = require_cuda()
+    dX = X if isinstance(X, torch.Tensor) else _f64(np.asarray(X, dtype=np.float64).reshape(-1, 6), dev)
+    dy = y if isinstance(y, torch.Tensor) else _f64(y, dev)
+    if out is None:
+        out = torch.zeros(56, dtype=torch.float64, device=dev)
+    ws = torch.empty(_abi.OLS_WS_DOUBLES, dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_ols_stats(dX.data_ptr(), dy.data_ptr(), dy.numel(), out.data_ptr(), ws.data_ptr(),
+                                          stream_ptr()), "intf_ols_stats")
+    return out
+
+
+def ols_solve(stats, want_pinv=False):
+    """-> (params[7], ridge_used, nonfinite, Pinv or None) on host."""
+    dev = require_cuda()
+    params = torch.empty(7, dtype=torch.float64, device=dev)
+    info = torch.zeros(2, dtype=torch.int32, device=dev)
+    pinv = torch.empty(49, dtype=torch.float64, device=dev) if want_pinv else None
+    _abi.check(_abi.load().intf_ols_solve(stats.data_ptr(), params.data_ptr(), info.data_ptr(), _abi.addr(pinv),
+                                          stream_ptr()), "intf_ols_solve")
+    inf = info.cpu().numpy()
+    return (params.cpu().numpy(), bool(inf[0]), bool(inf[1]),
+            pinv.cpu().numpy().reshape(7, 7) if want_pinv else None)
+
+
+def _streams(X_list, y_list, dev):
+    off = np.zeros(len(X_list) + 1, dtype=np.int64)
+    for i, y in enumerate(y_list):
+        off[i + 1] = off[i] + len(y)
+    X = np.concatenate([np.asarray(x, dtype=np.float64).reshape(-1, 6) for x in X_list]) if off[-1] else np.zeros((1, 6))
+    Y = np.concatenate([np.asarray(y, dtype=np.float64) for y in y_list]) if off[-1] else np.zeros(1)
+    return off, _f64(X, dev), _f64(Y, dev), torch.as_tensor(off).to(dev)
+
+
+def sgd_streams(X_list, y_list, params, eta):
+    """Prequential SGD (`predict.py:88-95,157-172`) over independent streams.
+    params: [S][7] initial (w, b); eta: [S].  -> (preds list, params, status)."""
+    dev = require_cuda()
+    off, dX, dY, doff = _streams(X_list, y_list, dev)
+    S = len(X_list)
+    dp = _f64(params, dev)
+    de = _f64(np.broadcast_to(np.asarray(eta, dtype=np.float64), (S,)), dev)
+    pred = torch.empty(max(int(off[-1]), 1), dtype=torch.float64, device=dev)
+    st = torch.zeros(max(S, 1), dtype=torch.int32, device=dev)
+    _abi.check(_abi.load().intf_sgd_streams(dX.data_ptr(), dY.data_ptr(), doff.data_ptr(), S, de.data_ptr(),
+                                            dp.data_ptr(), pred.data_ptr(), st.data_ptr(), stream_ptr()),
+               "intf_sgd_streams")
+    ph = pred.cpu().numpy()
+    return [ph[off[i]:off[i + 1]] for i in range(S)], dp.cpu().numpy().reshape(S, 7), st.cpu().numpy()[:S]
+
+
+def rls_streams(X_list, y_list, params, P, lam):
+    """Prequential RLS (`predict.py:137-154,157-172`).  -> (preds, params, P, status)."""
+    dev = require_cuda()
+    off, dX, dY, doff = _streams(X_list, y_list, dev)
+    S = len(X_list)
+    dp = _f64(params, dev)
+    dP = _f64(P, dev)
+    dl = _f64(np.broadcast_to(np.asarray(lam, dtype=np.float64), (S,)), dev)
+    pred = torch.empty(max(int(off[-1]), 1), dtype=torch.float64, device=dev)
+    st = torch.zeros(max(S, 1), dtype=torch.int32, device=dev)
+    _abi.check(_abi.load().intf_rls_streams(dX.data_ptr(), dY.data_ptr(), doff.data_ptr(), S, dl.data_ptr(),
+                                            dp.data_ptr(), dP.data_ptr(), pred.data_ptr(), st.data_ptr(), stream_ptr()),
+               "intf_rls_streams")
+    ph = pred.cpu().numpy()
+    return ([ph[off[i]:off[i + 1]] for i in range(S)], dp.cpu().numpy().reshape(S, 7),
+            dP.cpu().numpy().reshape(S, 7, 7), st.cpu().numpy()[:S])
+
+
+def eval_reports(yhat_list, y_list) -> np.ndarray:
+    """EvalReport rows (`predict.py:195-205`): [S][6] = mse, p25, p50, p75, p95, n."""
+    dev = require_cuda()
+    off = np.zeros(len(y_list) + 1, dtype=np.int64)
+    for i, y in enumerate(y_list):
+        off[i + 1] = off[i] + len(y)
+    yh = _f64(np.concatenate([np.asarray(a, dtype=np.float64) for a in yhat_list]), dev)
+    yy = _f64(np.concatenate([np.asarray(a, dtype=np.float64) for a in y_list]), dev)
+    doff = torch.as_tensor(off).to(dev)
+    out = torch.empty(6 * len(y_list), dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_eval_report(yh.data_ptr(), yy.data_ptr(), doff.data_ptr(), len(y_list), out.data_ptr(),
+                                            stream_ptr()), "intf_eval_report")
+    return out.cpu().numpy().reshape(-1, 6)
+
+
+def candidate_count(n_rows: int, cap: int) -> int:
+    n = ctypes.c_int64(0)
+    _abi.check(_abi.load().intf_candidate_count(n_rows, cap, ctypes.byref(n)), "intf_candidate_count")
+    return int(n.value)
+
+
+class CandidateScorer:
+    """Every candidate co-location set over a profile table,
+    scored by a coarse (static) and a fine (EWMA) linear predictor for n_dec
+    decisions.  Output (device, fp32): [n_dec][2][E][n_sets]."""
+
+    def __init__(self, table: _pack.TableArrays, cap: int, alpha: float = 0.5, dtable: DeviceTable | None = None):
+        self.dev = require_cuda()
+        self.dtable = dtable or DeviceTable(table, self.dev)
+        self.E = table.n_rows
+        self.cap = int(cap)
+        self.alpha = float(alpha)
+        self.n_cand = candidate_count(self.E, self.cap)
+        self.n_sets = self.n_cand // self.E
+
+    def alloc(self, n_dec: int) -> torch.Tensor:
+        return torch.empty(n_dec * 2 * self.n_cand, dtype=torch.float32, device=self.dev)
+
+    def score(self, coefs: torch.Tensor, out: torch.Tensor) -> None:
+        """coefs: device float64 [n_dec][2][7]; enqueue only (no sync)."""
+        n_dec = coefs.numel() // 14
+        _abi.check(_abi.load().intf_predict_candidates(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
+                                                       coefs.data_ptr(), n_dec, out.data_ptr(), stream_ptr()),
+                   "intf_predict_candidates")
+
+    def score_host(self, coefs_host: np.ndarray, out_host: np.ndarray, scratch: torch.Tensor) -> None:
+        """End-to-end variant: host coefs in, host predictions out."""
+        n_dec = coefs_host.size // 14
+        _abi.check(_abi.load().intf_predict_candidates_host(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
+                                                            coefs_host.ctypes.data, n_dec, out_host.ctypes.data,
+                                                            scratch.data_ptr(), stream_ptr()),
+                   "intf_predict_candidates_host")
+
+
+def multiset_rank(peers, E: int, cap: int) -> int:
+    """Index of a peer multiset within one own row (size-major, colex)."""
+    p = sorted(int(q) for q in peers)
+    k = len(p)
+    r = sum(_comb(E + j - 1, j) for j in range(k))
+    for i, q in enumerate(p, start=1):
+        r += _comb(q + i - 1, i)
+    return r
+
+
+def _comb(n: int, k: int) -> int:
+    import math
+
+    return math.comb(n, k) if 0 <= k <= n else 0
+
+
+def arrivals(specs, table: _pack.TableArrays, max_retries: int = 6):
+    """generate_arrivals for a batch of scenario dicts (`workload.py:74-104`)
+    -> list of (arrival_ms, deployed index) numpy pairs."""
+    scale = 1.0
+    for _ in range(max_retries + 1):
+        pipe = ReplayPipeline(specs, table, scale=scale, seg_stride=1)
+        _abi.check(_abi.load().intf_generate_arrivals(ctypes.byref(pipe.batch), ctypes.byref(pipe.B), stream_ptr()),
+                   "intf_generate_arrivals")
+        if np.any(pipe.status() & _abi.ST_OVERFLOW):
+            scale *= 2.0
+            continue
+        n_req = pipe.t["n_req"][: pipe.pb.n_scen].cpu().numpy()
+        at, am = pipe.t["arr_t"].cpu().numpy(), pipe.t["arr_model"].cpu().numpy()
+        out = []
+        for s in range(pipe.pb.n_scen):
+            S = pipe.pb.scen[s]
+            out.append((at[S.req_off:S.req_off + n_req[s]].copy(), am[S.req_off:S.req_off + n_req[s]].copy()))
+        return out
+    raise RuntimeError("arrival buffers still overflowing after retries")
+
+
+def noise_draws(seed: int, sigma: float, batch_ids, seg_idx) -> np.ndarray:
+    dev = require_cuda()
+    b = torch.as_tensor(np.ascontiguousarray(batch_ids, dtype=np.int64)).to(dev)
+    k = torch.as_tensor(np.ascontiguousarray(seg_idx, dtype=np.int64)).to(dev)
+    out = torch.empty(max(b.numel(), 1), dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_noise_draws(int(seed), float(sigma), b.data_ptr(), k.data_ptr(), b.numel(),
+                                            out.data_ptr(), stream_ptr()), "intf_noise_draws")
+    return out.cpu().numpy()[: b.numel()]
+
+
+def slowdowns(own, colo, beta, noise=None) -> np.ndarray:
+    dev = require_cuda()
+    o, c = _f64(np.asarray(own).reshape(-1, 3), dev), _f64(np.asarray(colo).reshape(-1, 3), dev)
+    bt = _f64(beta, dev)
+    nz = _f64(noise, dev) if noise is not None else None
+    n = o.shape[0]
+    out = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_slowdowns(o.data_ptr(), c.data_ptr(), bt.data_ptr(), _abi.addr(nz), n, out.data_ptr(),
+                                          stream_ptr()), "intf_slowdowns")
+    return out.cpu().numpy()[:n]
+
+
+def rng_stream(words, n: int, uniform: bool = False) -> np.ndarray:
+    dev = require_cuda()
+    w = torch.as_tensor(np.ascontiguousarray(words, dtype=np.uint32).view(np.int32)).to(dev)
+    out = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    _abi.check(_abi.load().intf_rng_stream(w.data_ptr(), w.numel(), n, int(uniform), out.data_ptr(), stream_ptr()),
+               "intf_rng_stream")
+    return out.cpu().numpy()[:n]

@@ -1,0 +1,84 @@
+"""The drop-in API (`import paper_2512_18725_b200 as intfsim`) returns the
+reference's objects with bit-identical values (goldens)."""
+import numpy as np
+import pytest
+
+from tests import _golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _spec(name):
+    from paper_2512_18725_b200.workload import scenario_from_dict
+
+    return scenario_from_dict(_golden.spec(name))
+
+
+def test_run_scenario_objects_bit_exact():
+    import paper_2512_18725_b200 as p
+
+    G = _golden.replay()
+    table = p.gen_synthetic_profiles()
+    for name in ("bundled_seed7", "churn0_2", "rand7"):
+        res = p.run_scenario(_spec(name), table)
+        assert [o.batch_id for o in res.outcomes] == list(G[name + "/o_batch"])
+        assert [o.completion_time_ms for o in res.outcomes] == list(G[name + "/o_completion"])
+        assert [o.measured_duration_ms for o in res.outcomes] == list(G[name + "/o_measured"])
+        segs = [s for o in res.outcomes for s in o.segments]
+        assert [s.slowdown for s in segs] == list(G[name + "/s_slowdown"])
+        assert [r.batch_id for r in res.records] == list(G[name + "/r_batch"])
+        assert [r.slo_met for r in res.records] == [bool(v) for v in G[name + "/r_slo"]]
+        mi = 0 if res.outcomes and _spec(name).colocation_mode.kind == "static" else 2
+        np.testing.assert_array_equal(np.array([s.x for s in res.samples]).reshape(-1, 6), G[f"{name}/x_mode{mi}"])
+        rep = p.slo_report(res.records)
+        for j, m in enumerate(G[name + "/slo_models"]):
+            r = rep[str(m)]
+            assert (r.n_requests, r.slo_satisfaction) == (G[name + "/slo_n"][j], G[name + "/slo_sat"][j])
+            assert [r.p50_latency_ms, r.p95_latency_ms, r.p99_latency_ms] == list(G[name + "/slo_p"][j])
+
+
+def test_generate_arrivals_bit_exact():
+    import paper_2512_18725_b200 as p
+
+    G = _golden.replay()
+    for name in ("bundled_seed0", "c4slice"):
+        ev = p.generate_arrivals(_spec(name))
+        assert [e.arrival_time_ms for e in ev] == list(G[name + "/arr_t"])
+
+
+def test_samples_from_arbitrary_outcomes_and_estimators():
+    import paper_2512_18725_b200 as p
+
+    table = p.gen_synthetic_profiles()
+    res = p.run_scenario(_spec("churn0_0"), table)
+    plain = list(res.outcomes)  # drop the fast-path arrays: rebuild from objects
+    for mode in (p.STATIC_MODE, p.ewma_mode(0.5)):
+        a = p.samples_from_outcomes(plain, table, mode)
+        b = p.samples_from_outcomes(res.outcomes, table, mode)
+        np.testing.assert_array_equal([s.x for s in a], [s.x for s in b])
+    est = p.init_estimate(0, p.ewma_mode(0.5), (0.4, 0.4, 0.4))
+    p.observe(est, (0.8, 0.0, 0.4))
+    np.testing.assert_allclose(est.r_hat, [0.6, 0.2, 0.4])
+
+
+def test_percentile_examples():
+    import paper_2512_18725_b200 as p
+
+    assert p.percentile([1, 2, 3, 4], 50) == 2
+    assert p.percentile([15, 20, 35, 40, 50], 40) == 20
+    assert p.percentile([3, 1, 2], 100) == 3
+    with pytest.raises(ValueError):
+        p.percentile([], 50)
+
+
+def test_empty_trace_and_edge_shapes():
+    import paper_2512_18725_b200 as p
+
+    table = p.gen_synthetic_profiles()
+    spec = p.ScenarioSpec(deployed=(p.DeployedModel("resnet50", 0.0, 10.0),), duration_s=1.0)
+    res = p.run_scenario(spec, table)
+    assert res.outcomes == [] and res.records == []
+    one = p.ScenarioSpec(deployed=(p.DeployedModel("resnet50", 500.0, 10.0),), duration_s=0.5,
+                         batching_window_ms=0.0, max_batch_size=1, concurrency_cap=1)
+    res = p.run_scenario(one, table)
+    assert all(o.interference_ratio == 1.0 for o in res.outcomes)  # cap 1: never co-located

@@ -1,0 +1,78 @@
+"""GPU parity of the candidate-set predictor (C2) against predictions
+composed from reference functions (tests/golden/candidates_golden.npz) and
+the oracle; fp32 output, tolerance 1e-5 relative."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests import _golden
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+def _scorer(cap):
+    from paper_2512_18725_b200 import engine
+
+    return engine.CandidateScorer(_golden.table("default"), cap=cap, alpha=0.5)
+
+
+def test_candidate_counts():
+    from paper_2512_18725_b200 import engine
+
+    assert [engine.candidate_count(48, c) for c in (2, 3, 4)] == [2352, 58800, 999600]
+
+
+@pytest.mark.parametrize("cap", [2, 3])
+def test_candidates_match_reference_composition(cap):
+    from paper_2512_18725_b200 import engine
+
+    C = _golden.load("candidates_golden.npz")
+    sc = _scorer(cap)
+    coefs = torch.tensor(C["w"], dtype=torch.float64, device="cuda").reshape(1, 2, 7).contiguous()
+    out = sc.alloc(1)
+    sc.score(coefs, out)
+    y = out.cpu().numpy().reshape(2, sc.E, sc.n_sets)
+    own, peers = C[f"cap{cap}/own"], C[f"cap{cap}/peers"]
+    idx = np.array([engine.multiset_rank([q for q in pe if q >= 0], sc.E, cap) for pe in peers])
+    np.testing.assert_allclose(y[0, own, idx], C[f"cap{cap}/y_coarse"], rtol=RTOL)
+    np.testing.assert_allclose(y[1, own, idx], C[f"cap{cap}/y_fine"], rtol=RTOL)
+
+
+def test_cap4_full_enumeration_sampled_against_oracle():
+    from paper_2512_18725_b200 import engine
+
+    tab = _golden.table("default")
+    sc = _scorer(4)
+    rng = np.random.default_rng(1)
+    W = rng.normal(0, 0.5, size=(3, 2, 7))
+    coefs = torch.tensor(W, dtype=torch.float64, device="cuda").contiguous()
+    out = sc.alloc(3)
+    sc.score(coefs, out)
+    y = out.cpu().numpy().reshape(3, 2, sc.E, sc.n_sets)
+    assert np.isfinite(y).all()
+    import itertools
+
+    sets = [()]
+    for k in range(1, 4):
+        sets += list(itertools.combinations_with_replacement(range(sc.E), k))
+    for _ in range(300):
+        d, o, si = rng.integers(3), rng.integers(sc.E), rng.integers(len(sets))
+        pe = sets[si]
+        r = engine.multiset_rank(pe, sc.E, 4)
+        yc, yf = O.candidate_predictions(int(o), list(pe), tab.solo, tab.thr, W[d, 0], W[d, 1], 0.5)
+        np.testing.assert_allclose([y[d, 0, o, r], y[d, 1, o, r]], [yc, yf], rtol=RTOL, atol=1e-6)
+
+
+def test_host_buffer_variant_equals_device_variant():
+    sc = _scorer(3)
+    C = _golden.load("candidates_golden.npz")
+    W = np.stack([C["w"], C["w"] * 0.5])
+    dev_out = sc.alloc(2)
+    sc.score(torch.tensor(W, device="cuda").contiguous(), dev_out)
+    host_out = np.empty(2 * 2 * sc.n_cand, dtype=np.float32)
+    scratch = torch.empty(2 * 2 * 7 * 2 + host_out.size, dtype=torch.float32, device="cuda")
+    sc.score_host(np.ascontiguousarray(W), host_out, scratch)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(host_out, dev_out.cpu().numpy())

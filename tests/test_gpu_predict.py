@@ -1,0 +1,104 @@
+"""GPU parity of the refit path: OLS statistics + solve, prequential SGD /
+RLS streams, evaluation reports, and the experiment drivers, against the
+reference's golden outputs.  Tolerance 1e-5 relative (north star); SGD is
+additionally checked bit-exact (same rounding sequence as numpy)."""
+import numpy as np
+import pytest
+
+from tests import _golden
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+def _samples(X, y):
+    import paper_2512_18725_b200 as p
+
+    return [p.Sample(x=X[i], y=float(y[i]), batch_id=i) for i in range(len(y))]
+
+
+def test_fit_ols_matches_lstsq():
+    import paper_2512_18725_b200 as p
+
+    P = _golden.load("predict_golden.npz")
+    for mi in range(4):
+        X, y, cut = P[f"ewma/mode{mi}/X"], P[f"ewma/mode{mi}/y"], int(P[f"ewma/mode{mi}/ncut"])
+        m = p.fit_ols(_samples(X[:cut], y[:cut]))
+        np.testing.assert_allclose(m.w7(), np.append(P[f"ewma/mode{mi}/w"], P[f"ewma/mode{mi}/b"]), rtol=RTOL,
+                                   atol=1e-9)
+        rep = p.evaluate(m, _samples(X[cut:], y[cut:]))
+        np.testing.assert_allclose([rep.mse, rep.rel_p25, rep.rel_p50, rep.rel_p75, rep.rel_p95, rep.n_samples],
+                                   P[f"ewma/mode{mi}/report"], rtol=RTOL)
+
+
+def test_ridge_fallback_when_rank_deficient():
+    import paper_2512_18725_b200 as p
+
+    P = _golden.load("predict_golden.npz")
+    m = p.fit_ols_xy(P["ridge/X"], P["ridge/y"])
+    np.testing.assert_allclose(m.w7(), P["ridge/w"], rtol=RTOL, atol=1e-7)
+
+
+def test_exact_recovery_and_rls_equals_ols():
+    # `test_predict.py:45-50` and criterion 1 (`test_acceptance.py:45-65`)
+    import paper_2512_18725_b200 as p
+
+    rng = np.random.default_rng(0)
+    w_true = np.array([0.5, -0.2, 0.8, 0.1, 0.3, -0.4])
+    X = rng.uniform(0, 2, size=(200, 6))
+    y = X @ w_true + 0.2
+    m = p.fit_ols(_samples(X, y))
+    np.testing.assert_allclose(m.w, w_true, atol=1e-8)
+    y2 = y + 0.2 * rng.standard_normal(200)
+    s = _samples(X, y2)
+    st = p.rls_init(p.fit_ols(s[:80]), lam=1.0, X_train=X[:80])
+    p.evaluate(st, s[80:], online=True)
+    full = p.fit_ols(s)
+    np.testing.assert_allclose(st.model.w7(), full.w7(), atol=1e-8)
+
+
+def test_prequential_streams_match_golden():
+    import paper_2512_18725_b200 as p
+
+    P = _golden.load("predict_golden.npz")
+    for seed in (0, 1):
+        pre = f"drift{seed}/"
+        m0 = p.LinearModel(w=P[pre + "w0"].copy(), b=float(P[pre + "b0"]))
+        Xtr = P[pre + "Xtrain"]
+        rls0 = p.rls_init(m0, lam=0.99, X_train=Xtr)
+        np.testing.assert_allclose(rls0.P, P[pre + "P0"], rtol=1e-6, atol=1e-6 * np.abs(P[pre + "P0"]).max())
+        for ts in ("TestSet1", "TestSet2", "TestSet3"):
+            X, y = P[pre + ts + "/X"], P[pre + ts + "/y"]
+            sgd = p.SgdState(m0.copy(), eta=0.01)
+            rls = rls0.copy()
+            rs = p.evaluate_many([sgd, rls], [_samples(X, y)] * 2, online=True)
+            np.testing.assert_array_equal(sgd.model.w7(), P[pre + ts + "/sgd_w"])  # bit-exact
+            np.testing.assert_allclose(rls.model.w7(), P[pre + ts + "/rls_w"], rtol=RTOL, atol=1e-8)
+            ref = p.evaluate(p.SgdState(m0.copy(), eta=0.01), _samples(X, y), online=True)
+            assert rs[0] == ref
+
+
+def test_drift_experiment_matches_reference():
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200 import experiments as ex
+
+    P = _golden.load("predict_golden.npz")
+    table = p.gen_synthetic_profiles()
+    for seed in (0, 1):
+        cells = ex.drift_experiment(ex.default_drift_base(table, seed), table)
+        keys = [f"{c.dataset}/{c.method}" for c in cells]
+        assert keys == [str(k) for k in P[f"drift{seed}/cell_keys"]]
+        np.testing.assert_allclose([[c.mse, c.n_samples] for c in cells], P[f"drift{seed}/cells"], rtol=RTOL)
+
+
+def test_ewma_experiment_matches_reference():
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200 import experiments as ex
+
+    P = _golden.load("predict_golden.npz")
+    table = p.gen_synthetic_profiles()
+    rows = ex.ewma_experiment(ex.high_churn_suite(table, 0), table)
+    for mi, row in enumerate(rows):
+        r = row.report
+        np.testing.assert_allclose([r.mse, r.rel_p25, r.rel_p50, r.rel_p75, r.rel_p95, r.n_samples],
+                                   P[f"ewma/mode{mi}/report"], rtol=RTOL)

@@ -1,0 +1,134 @@
+"""Pin the CPU oracle (oracle/) to the reference's golden outputs before it
+is trusted as the checker (tests/golden/make_golden.py ran the unmodified
+reference).  CPU only."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from tests import _golden
+
+
+def _otab(name="default"):
+    t = _golden.table(name)
+    return O.TableArrays(t.models, t.max_bs, t.solo, t.thr)
+
+
+@pytest.mark.parametrize("name", _golden.scenario_names())
+def test_oracle_replay_bit_exact(name):
+    spec = _golden.spec(name)
+    tab = _otab(str(_golden.replay()[name + "/table"]))
+    rep = O.run_scenario(spec, tab)
+    assert rep["status"] == 0
+    assert _golden.compare_replay(rep, name) == []
+    G = _golden.replay()
+    for mi, (ewma, alpha) in enumerate(_golden.MODES):
+        X, y, _ = O.samples_from_replay(rep, spec, tab, bool(ewma), alpha)
+        np.testing.assert_array_equal(X, G[f"{name}/x_mode{mi}"])
+        np.testing.assert_array_equal(y, G[f"{name}/y_mode{mi}"])
+
+
+def test_oracle_slo_report_matches_golden():
+    G = _golden.replay()
+    for name in ("bundled_seed7", "churn0_1", "c4slice", "rand13"):
+        spec = _golden.spec(name)
+        tab = _otab(str(G[name + "/table"]))
+        rep = O.run_scenario(spec, tab)
+        ids = [d["model_id"] for d in spec["deployed"]]
+        models = [ids[m] for m in rep["arr_model"]]
+        comp = rep["b_completion"][rep["r_batch"]]
+        out = O.slo_report(models, rep["arr_t"], comp, rep["r_slo_met"])
+        for j, m in enumerate(G[name + "/slo_models"]):
+            n, sat, p50, p95, p99 = out[str(m)]
+            assert n == G[name + "/slo_n"][j] and sat == G[name + "/slo_sat"][j]
+            assert [p50, p95, p99] == list(G[name + "/slo_p"][j])
+        warm = O.slo_report(models, rep["arr_t"], comp, rep["r_slo_met"], warmup_fraction=0.2)
+        np.testing.assert_array_equal(np.array([list(warm[k]) for k in sorted(warm)]), G[name + "/slo_warm_p"])
+
+
+def test_oracle_rng_known_answers():
+    R = _golden.load("rng_golden.npz")
+    keys = R["noise_keys"]
+    got = np.array([O.noise_draw(int(s), int(b), int(k), 0.05) for s, b, k in keys])
+    np.testing.assert_array_equal(got, R["noise_sigma005"])
+    got2 = np.array([O.noise_draw(int(s), int(b), int(k), 0.02) for s, b, k in keys[:400]])
+    np.testing.assert_array_equal(got2, R["noise_sigma002"])
+    np.testing.assert_array_equal(O.random_doubles(O.int_words(*R["uniform_seed"]), 5000), R["uniform"])
+    np.testing.assert_array_equal(O.standard_normals(O.int_words(*R["normal_seed"]), len(R["normal"])), R["normal"])
+    np.testing.assert_array_equal([O.c_exp(float(x)) for x in R["exp_x"]], R["exp_y"])
+    np.testing.assert_array_equal([O.c_log1p(float(x)) for x in R["log1p_x"]], R["log1p_y"])
+
+
+def test_oracle_noise_sigma_zero_is_one():
+    assert O.noise_draw(5, 3, 1, 0.0) == 1.0
+
+
+def test_oracle_predictor_restatement_matches_golden():
+    P = _golden.load("predict_golden.npz")
+    for mi in range(4):
+        X, y, cut = P[f"ewma/mode{mi}/X"], P[f"ewma/mode{mi}/y"], int(P[f"ewma/mode{mi}/ncut"])
+        w, b = O.fit_ols_xy(X[:cut], y[:cut])
+        np.testing.assert_array_equal(w, P[f"ewma/mode{mi}/w"])
+        assert b == float(P[f"ewma/mode{mi}/b"])
+        rep = O.eval_report([O.predict(w, b, x) for x in X[cut:]], y[cut:])
+        np.testing.assert_array_equal(np.array(rep), P[f"ewma/mode{mi}/report"])
+    for seed in (0, 1):
+        p = f"drift{seed}/"
+        w0, b0 = O.fit_ols_xy(P[p + "Xtrain"], P[p + "ytrain"])
+        np.testing.assert_array_equal(w0, P[p + "w0"])
+        np.testing.assert_array_equal(O.rls_init_P(P[p + "Xtrain"]), P[p + "P0"])
+        for ts in ("TestSet1", "TestSet2", "TestSet3"):
+            X, y = P[p + ts + "/X"], P[p + ts + "/y"]
+            pr, w, b, _ = O.prequential(w0, b0, X, y, "sgd")
+            np.testing.assert_array_equal(pr, P[p + ts + "/sgd_pred"])
+            np.testing.assert_array_equal(np.append(w, b), P[p + ts + "/sgd_w"])
+            pr, w, b, Pm = O.prequential(w0, b0, X, y, "rls", P=O.rls_init_P(P[p + "Xtrain"]))
+            np.testing.assert_array_equal(pr, P[p + ts + "/rls_pred"])
+            np.testing.assert_array_equal(Pm, P[p + ts + "/rls_P"])
+    w, b = O.fit_ols_xy(P["ridge/X"], P["ridge/y"])
+    np.testing.assert_array_equal(np.append(w, b), P["ridge/w"])
+
+
+def test_oracle_candidates_match_golden():
+    C = _golden.load("candidates_golden.npz")
+    tab = _otab()
+    for cap in (2, 3):
+        own, peers = C[f"cap{cap}/own"], C[f"cap{cap}/peers"]
+        for i in range(0, len(own), 7):
+            pe = [q for q in peers[i] if q >= 0]
+            yc, yf = O.candidate_predictions(int(own[i]), pe, tab.solo, tab.thr, C["w"][0], C["w"][1], 0.5)
+            assert yc == C[f"cap{cap}/y_coarse"][i] and yf == C[f"cap{cap}/y_fine"][i]
+
+
+# ---- known-answer tests carried over from the reference suite
+def test_oracle_hand_example_slowdown():
+    # `test_simcore.py:49-53`: own=colo=(0.6,0.5,0.4) -> excess (0.2,0,0) -> 1.2
+    import ctypes
+
+    L = O.lib()
+    a = np.array([1.0, 1.5, 0.5])
+    e = np.array([0.6 + 0.6 - 1.0, 0.0, 0.0])
+    dot = L.oracle_ddot(a.ctypes.data_as(O.PD), e.ctypes.data_as(O.PD), 3)
+    assert math.isclose(1.0 + dot, 1.2, rel_tol=1e-12)
+    del ctypes
+
+
+def test_oracle_ewma_hand_example():
+    # `test_colocation.py:61-64`: EWMA(0.5) from (0.4,0.4,0.4) observing (0.8,0,0.4) -> (0.6,0.2,0.4)
+    x = O.features(np.array([[0.4, 0.4, 0.4], [0.8, 0.0, 0.4]]), np.zeros(3), True, 0.5)
+    np.testing.assert_allclose(x[3:], [0.6, 0.2, 0.4])
+
+
+def test_oracle_sgd_hand_step():
+    # `test_predict.py:115-121`: zero model, x=(1,0,...), y=10, eta=0.01 -> w0=0.1, b=0.1
+    w, b = O.sgd_update(np.zeros(6), 0.0, np.array([1.0, 0, 0, 0, 0, 0]), 10.0, 0.01)
+    assert math.isclose(w[0], 0.1) and math.isclose(b, 0.1)
+
+
+def test_oracle_percentile_examples():
+    # `test_metrics.py:26-31`
+    assert O.percentile([1, 2, 3, 4], 50) == 2
+    assert O.percentile([15, 20, 35, 40, 50], 40) == 20
+    assert O.percentile([3, 1, 2], 100) == 3
+    assert O.percentile([5], 0) == 5
