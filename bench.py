@@ -1,0 +1,377 @@
+"""Benchmark of the intfsim hot path on B200 (contract: one JSON line).
+
+Headline workload (BASELINE.json configs[1], C2): every candidate co-located
+batch set over the 48 bundled profile entries at concurrency cap 4 (999,600
+own x peer-multiset candidates), scored by the coarse (static
+features) and fine (EWMA(1/2) features) linear predictors for D = 32
+scheduling decisions per step, each decision with its own refit
+coefficients (OLS on growing windows of the bundled trace's samples).
+One step = one launch of k_candidates writing 63,974,400 fp32 predictions
+(256 MB > L2, so no flush is needed between steps).
+
+Secondary workload (configs[4] shape, C5): a sweep of synthetic scenarios
+replayed end to end per step (arrivals -> replay -> SLO -> features +
+3 predictors), reported as scenario replays/s.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): decisions and scenarios shard
+across ranks with no data-path collective (weak scaling); per-rank times are
+reduced with MAX.  `--impl reference` times the CPU oracle port on the host
+cores instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEC = 32
+CAP = 4
+ALPHA = 0.5
+REPLAY_SCEN = 4096
+METRIC = "candidate co-location predictions/sec and scenario replays/sec at 1/2/4/8 B200"
+
+
+def _env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _traffic():
+    """ncu dram bytes per launch of k_candidates, if a capture was committed."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("k_candidates", {}).get("dram_bytes_per_launch")
+    return None
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def wait_first(self, timeout: float = 5.0):
+        """Block until nvidia-smi has written its first sample."""
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < timeout:
+            if os.path.getsize(self.f.name) > 0:
+                return
+            time.sleep(0.05)
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 7 for i in range(4) if "Active" in r[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------- workloads
+def decision_coefs(n_dec: int) -> np.ndarray:
+    """[n_dec][2][7]: coarse (static) / fine (EWMA 1/2) OLS refits on growing
+    windows of the bundled trace's samples (windowed refit, `predict.py:53-72`)."""
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200 import engine
+    from paper_2512_18725_b200.colocation import features_for_modes
+    from paper_2512_18725_b200.workload import scenario_from_dict
+    from tests import _golden
+
+    table = p.gen_synthetic_profiles()
+    res = p.run_scenario(scenario_from_dict(_golden.spec("bundled_seed7")), table)
+    X, y, _ = features_for_modes(res.outcomes, table, [p.STATIC_MODE, p.ewma_mode(ALPHA)])
+    n = len(y)
+    W = np.zeros((n_dec, 2, 7))
+    for d in range(n_dec):
+        hi = max(64, int(n * (d + 1) / n_dec))
+        for k in range(2):
+            params, _, _, _ = engine.ols_solve(engine.ols_stats(X[k, :hi], y[:hi]))
+            W[d, k] = params
+    return W
+
+
+def cpu_candidate_rate(table, W, seconds: float, seed: int = 0):
+    """Oracle port (`oracle.candidate_predictions`, restated from the
+    reference's functions) on a sample of cap-4 candidates, one core."""
+    import itertools
+
+    import oracle as O
+
+    rng = np.random.default_rng(seed)
+    E = len(table.solo)
+    sets = [()]
+    for k in range(1, CAP):
+        sets += list(itertools.combinations_with_replacement(range(E), k))
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        for _ in range(200):
+            o = int(rng.integers(E))
+            pe = sets[int(rng.integers(len(sets)))]
+            O.candidate_predictions(o, list(pe), table.solo, table.thr, W[0, 0], W[0, 1], ALPHA)
+            n += 2
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def _ref_worker(args):
+    seconds, seed = args
+    from paper_2512_18725_b200.profiles import gen_synthetic_profiles
+
+    table = gen_synthetic_profiles().arrays()
+    W = np.random.default_rng(7).normal(0, 0.3, size=(1, 2, 7))
+    return cpu_candidate_rate(table, W, seconds, seed)[1]
+
+
+def replay_stage_times(pipe, stream) -> dict:
+    """One extra (untimed) pass of the replay pipeline with events between
+    its launches: per-stage device time in ms."""
+    import ctypes
+
+    import torch
+    from paper_2512_18725_b200 import _abi
+
+    L, s = _abi.load(), stream.cuda_stream
+    bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev[0].record(stream)
+    _abi.check(L.intf_generate_arrivals(bt, B, s), "arrivals")
+    ev[1].record(stream)
+    _abi.check(L.intf_replay(bt, ctypes.byref(pipe.dtable.struct), B, s), "replay")
+    ev[2].record(stream)
+    pipe.run_slo_features(slo=True, features=False)
+    ev[3].record(stream)
+    pipe.run_slo_features(slo=False, features=True)
+    ev[4].record(stream)
+    torch.cuda.synchronize()
+    names = ["arrivals", "replay", "slo", "features"]
+    return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
+
+
+# -------------------------------------------------------------- reference
+def reference_arm(a):
+    rank, world, _ = _env()
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    per_step = 1.0
+    with mp.get_context("fork").Pool(cores) as pool:
+        for _ in range(a.warmup):
+            pool.map(_ref_worker, [(0.2, s) for s in range(cores)])
+        times, preds = [], 0
+        for k in range(a.steps):
+            t0 = time.perf_counter()
+            n = sum(pool.map(_ref_worker, [(per_step, 1000 * k + s) for s in range(cores)]))
+            times.append(time.perf_counter() - t0)
+            preds += n
+    tot = sum(times)
+    v = preds / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "predictions/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 candidate sets, cap 4 over the 48 bundled profile entries, coarse+fine "
+                               "predictors (bounded random sample of candidates per step)", "cap": CAP},
+        "cpu_baseline": {"value": v, "unit": "predictions/s", "cores": cores, "kind": "port",
+                         "sample": f"{per_step:.1f} s of random cap-4 candidates per core per step "
+                                   f"(oracle.candidate_predictions, reference functions restated)"},
+        "e2e": {"value": v, "unit": "predictions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------- product
+def product_arm(a):
+    import torch
+
+    rank, world, local = _env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2512_18725_b200 import _abi, engine
+    from paper_2512_18725_b200.profiles import gen_synthetic_profiles
+    from paper_2512_18725_b200.sweep import c5_scenarios
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    table = gen_synthetic_profiles()
+    ta = table.arrays()
+    W = decision_coefs(N_DEC)
+    W = W * (1.0 + 1e-3 * rank)  # each rank scores its own decisions (weak scaling)
+    scorer = engine.CandidateScorer(ta, cap=CAP, alpha=ALPHA)
+    coefs = torch.tensor(W, dtype=torch.float64, device="cuda").contiguous()
+    out = scorer.alloc(N_DEC)
+    n_pred = N_DEC * 2 * scorer.n_cand  # useful predictions per step (row padding excluded)
+    n_elems = scorer.out_elems(N_DEC)
+    stream = torch.cuda.current_stream()
+
+    # ---- device-resident timed region (clocks sampled across every timed region)
+    clocks = Clocks(local)
+    clocks.wait_first()
+    for _ in range(a.warmup):
+        scorer.score(coefs, out)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(a.steps):
+        ev[k][0].record(stream)
+        scorer.score(coefs, out)
+        ev[k][1].record(stream)
+    t_end.record(stream)
+    barrier()
+    ms_total = max_over_ranks(t_start.elapsed_time(t_end))
+    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
+    ms_step = ms_total / a.steps
+    value = world * n_pred / (ms_step / 1e3)
+
+    # ---- end to end through the host-buffer C-ABI call
+    h_out = torch.empty(n_elems, dtype=torch.float32).pin_memory()
+    h_coefs = torch.tensor(W, dtype=torch.float64).pin_memory()
+    scratch = torch.empty(N_DEC * 2 * 7 * 2 + n_elems, dtype=torch.float32, device="cuda")
+    hc = h_coefs.numpy()
+    ho = h_out.numpy()
+    for _ in range(max(1, a.warmup)):
+        scorer.score_host(hc, ho, scratch)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(a.steps, 10))
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        scorer.score_host(hc, ho, scratch)
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+    ok = bool(np.isfinite(ho[:1000]).all())
+
+    # ---- secondary: scenario replay sweep (C5 shape)
+    specs = c5_scenarios(table, REPLAY_SCEN, start=rank * REPLAY_SCEN)
+    preds = [_abi.Predictor(ewma=0, alpha=1.0, w=tuple(W[-1, 0])), _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[-1, 1])),
+             _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[0, 1]))]
+    pipe = engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5)
+    for _ in range(max(1, a.warmup)):
+        pipe.run()
+    barrier()
+    st = pipe.status()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r_steps = max(1, min(a.steps, 5))
+    r0.record(stream)
+    for _ in range(r_steps):
+        pipe.run()
+    r1.record(stream)
+    barrier()
+    rep_ms = max_over_ranks(r0.elapsed_time(r1)) / r_steps
+    clk = clocks.stop()
+    stage_ms = replay_stage_times(pipe, stream)
+    n_batches = int(pipe.t["n_batches"][: pipe.pb.n_scen].sum().item())
+    n_req = int(pipe.t["n_req"][: pipe.pb.n_scen].sum().item())
+
+    # ---- CPU baseline (rank 0, N=1 only): oracle port on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        rate, n, dt = cpu_candidate_rate(ta, W, a.cpu_seconds)
+        cpu = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port",
+               "sample": f"{n} predictions ({n // 2} random cap-4 candidates x coarse+fine, 1 decision) in {dt:.1f} s"}
+
+    peak, peak_src = _peaks()
+    bytes_per_launch = 4.0 * n_pred  # implicit enumeration: fp32 output only
+    achieved = bytes_per_launch / (kern_ms / 1e3) / 1e9
+    traffic = _traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": "predictions/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 forward (f64 features)", "data": "synthetic",
+        "config": {"workload": "C2: all candidate co-location sets (cap 4, 48 bundled profile entries = 999,600 "
+                               "candidates) x {coarse static, fine EWMA(1/2)} predictors x 32 refit decisions per "
+                               "step per GPU; output fp32", "global_batch": n_pred * world,
+                   "parallelism": f"dp{world} (decisions sharded, no collective)", "l2": "output 256 MB/step > L2"},
+        "e2e": {"value": world * n_pred / (e2e_ms / 1e3), "unit": "predictions/s",
+                "h2d_bytes_per_step": int(W.size * 8), "d2h_bytes_per_step": int(4 * n_elems),
+                "call": "intf_predict_candidates_host (pinned host buffers)", "finite": ok},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_candidates",
+                     "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": bytes_per_launch},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": a.steps,
+        "replay": {"metric": "scenario replays/sec", "value": world * REPLAY_SCEN / (rep_ms / 1e3),
+                   "unit": "replays/s", "ms_per_step": rep_ms, "scenarios_per_gpu": REPLAY_SCEN,
+                   "requests": n_req, "batches": n_batches, "status_nonzero": int(np.count_nonzero(st)),
+                   "workload": "C5-shape synthetic scenarios (default_rng([2512,i]), 1 s, cap 1-3): arrivals + "
+                               "replay + SLO + features/3 predictors", "launches_per_step": 5,
+                   "stage_ms": stage_ms},
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.impl == "reference":
+        return reference_arm(a)
+    return product_arm(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

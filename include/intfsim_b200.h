@@ -149,18 +149,21 @@ int intf_features_predict(const intf_batch *batch, const intf_table *table, cons
                           double *yhat, void *stream);
 
 /* Candidate co-location sets: every own table row x
- * every multiset of <= cap-1 peer rows, implicitly enumerated.  For each of
- * n_dec decisions and each candidate writes the coarse (static + coarse
- * model) and fine (EWMA(alpha) over the departure history + fine model)
- * predicted interference ratio as fp32:
- *   out[((dec*2 + {0 coarse,1 fine}) * n_cand) + c].
- * coefs: device [n_dec][2][7] (w0..w5, b).  Candidate order: own-major, then
- * multisets in colex order of size 0,1,..,cap-1.           */
-int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t *n_cand);
+ * every multiset of <= cap-1 peer rows, implicitly enumerated (nothing is
+ * read per candidate).  For each of n_dec decisions and each candidate writes
+ * the coarse (static features + coarse model) and fine (EWMA(alpha) over the
+ * candidate's departure history + fine model) predicted interference ratio,
+ * fp32 (fp64 features, fp32 forward: within the 1e-5 tolerance):
+ *   out[((dec*2 + kind) * n_rows + own) * ld + r],  kind 0 coarse, 1 fine,
+ * r < n_sets the multiset rank (size-major, colex within a size), ld = n_sets
+ * rounded up to 4 (pad entries written as 0).
+ * coefs: device [n_dec][2][7] (w0..w5, b).                                  */
+int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t *n_cand, int64_t *n_sets, int64_t *ld);
 int intf_predict_candidates(const intf_table *table, int32_t cap, double alpha, const double *coefs, int32_t n_dec,
                             float *out, void *stream);
 /* Host-buffer variant (the end-to-end call): copies coefs in and all
- * predictions out (pinned or pageable host memory).                        */
+ * predictions out (h_out: n_dec*2*n_rows*ld floats; d_scratch: 28*n_dec +
+ * that many floats of device memory).                                       */
 int intf_predict_candidates_host(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
                                  int32_t n_dec, float *h_out, float *d_scratch, void *stream);
 

@@ -78,7 +78,7 @@ SIGNATURES = {
     "intf_replay": (c_int32, [P, P, P, P]),
     "intf_slo_report": (c_int32, [P, P, P, P, P, P, P]),
     "intf_features_predict": (c_int32, [P, P, P, P, c_int32, c_int64, P, P, P, P]),
-    "intf_candidate_count": (c_int32, [c_int32, c_int32, P]),
+    "intf_candidate_count": (c_int32, [c_int32, c_int32, P, P, P]),
     "intf_predict_candidates": (c_int32, [P, c_int32, c_double, P, c_int32, P, P]),
     "intf_predict_candidates_host": (c_int32, [P, c_int32, c_double, P, c_int32, P, P, P]),
     "intf_ols_stats": (c_int32, [P, P, c_int64, P, P, P]),

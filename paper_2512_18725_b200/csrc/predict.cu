@@ -20,6 +20,10 @@ namespace {
 // the multisets are ranked size-major (k = 0, 1, ..) and in colex order
 // within a size: multiset p1<=..<=pk <-> combination c_i = p_i + (i-1) of
 // {0..E+k-2}, rank = sum_i C(c_i, i).
+//
+// Output layout (fp32): out[((dec*2 + kind) * E + own) * ld + r], r < n_sets,
+// ld = n_sets rounded up to a multiple of 4 (pad lanes written as 0) so every
+// thread emits 16-byte streaming stores.
 constexpr int kMaxPeers = 7;  // cap <= 8
 
 __host__ __device__ __forceinline__ long long binom(long long n, int k) {
@@ -29,126 +33,177 @@ __host__ __device__ __forceinline__ long long binom(long long n, int k) {
   return r;
 }
 
-__device__ __forceinline__ int unrank_multiset(long long r, int E, int cap, int* p) {
+long long n_multisets(int E, int cap) {
+  long long sets = 0;
+  for (int k = 0; k < cap; k++) sets += binom(E + k - 1, k);
+  return sets;
+}
+
+constexpr int kCandThreads = 128;
+constexpr int kOwnChunk = 8;
+constexpr int kDecChunk = 8;
+constexpr int kGroup = 4;  // multisets per thread (one float4 per output row)
+
+// binomial table in shared memory: C[i][n] = binom(n, i), i <= kmax, n < nmax
+struct BinomTab {
+  const unsigned long long* c;
+  int nmax;
+  __device__ __forceinline__ unsigned long long operator()(int n, int i) const {
+    return (n < i || n < 0) ? 0ull : c[i * nmax + n];
+  }
+};
+
+template <int KMAX>
+__device__ __forceinline__ int unrank_multiset(long long r, int E, int cap, const BinomTab& C, int* p) {
   int k = 0;
   for (; k < cap; k++) {
-    long long nk = binom(E + k - 1, k);
+    const long long nk = (long long)C(E + k - 1, k);
     if (r < nk) break;
     r -= nk;
   }
-  for (int i = k; i >= 1; i--) {
-    // largest c with C(c, i) <= r, c in [i-1, E+k-2]
-    int lo = i - 1, hi = E + k - 2;
+#pragma unroll
+  for (int i = KMAX; i >= 1; i--) {
+    if (i > k) continue;
+    int lo = i - 1, hi = E + k - 2;  // largest c with C(c, i) <= r
     while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (binom(mid, i) <= r) lo = mid;
+      const int mid = (lo + hi + 1) >> 1;
+      if ((long long)C(mid, i) <= r) lo = mid;
       else hi = mid - 1;
     }
-    r -= binom(lo, i);
+    r -= (long long)C(lo, i);
     p[i - 1] = lo - (i - 1);
   }
   return k;
 }
 
-constexpr int kCandThreads = 128;
-constexpr int kOwnChunk = 8;
-constexpr int kMaxDec = 64;
-
-// grid: x = multiset chunks, y = own-row chunks.  Shared: per (dec, kind, own
-// in chunk) the partial fma chain over the own features, so each prediction
-// is 3 fma + 1 add in fp64 (same op order as the full 6-term chain) rounded
-// once to fp32.
-__global__ void __launch_bounds__(kCandThreads) k_candidates(const double* __restrict__ solo,
+// grid: x = groups of kGroup multisets, y = own-row chunks, z = decision chunks.
+// Per multiset (fp64, amortised over kOwnChunk owns x kDecChunk decisions):
+// colo snapshot with all peers ((0+p1)+p2).. (`simcore.py:126-131`), the
+// departure history in (solo, row) order and its EWMA(alpha) prefixes
+// (`colocation.py:54-63`).  Per prediction (fp32, within the 1e-5 budget):
+// y = part_own + w3*c0 + w4*c1 + w5*c2 + b, part_own = fp64 fma chain over the
+// own features precomputed in shared memory.
+template <int KMAX>
+__global__ void __launch_bounds__(kCandThreads, 3) k_candidates(const double* __restrict__ solo,
                                                              const double* __restrict__ thr, int E, int cap,
-                                                             long long n_sets, double alpha,
+                                                             long long n_sets, long long ld, double alpha,
                                                              const double* __restrict__ coefs, int n_dec,
                                                              float* __restrict__ out) {
-  __shared__ double part[kMaxDec][2][kOwnChunk];
-  __shared__ double wc[kMaxDec][2][4];  // w3, w4, w5, b per (dec, kind)
+  extern __shared__ unsigned long long binom_smem[];
+  __shared__ float part[kDecChunk][2][kOwnChunk];
+  __shared__ float wc[kDecChunk][2][4];
   __shared__ double own_solo[kOwnChunk];
-  const int o0 = blockIdx.y * kOwnChunk;
-  const int no = min(kOwnChunk, E - o0);
-  for (int t = threadIdx.x; t < n_dec * 2 * kOwnChunk; t += blockDim.x) {
+  const int nmax = E + KMAX + 1;
+  for (int t = threadIdx.x; t < (KMAX + 1) * nmax; t += blockDim.x) {
+    const int i = t / nmax, n = t % nmax;
+    binom_smem[t] = (unsigned long long)binom(n, i);
+  }
+  const int o0 = blockIdx.y * kOwnChunk, no = min(kOwnChunk, E - o0);
+  const int d0 = blockIdx.z * kDecChunk, nd = min(kDecChunk, n_dec - d0);
+  for (int t = threadIdx.x; t < kDecChunk * 2 * kOwnChunk; t += blockDim.x) {
     const int oi = t % kOwnChunk, kind = (t / kOwnChunk) & 1, d = t / (2 * kOwnChunk);
-    if (oi < no) {
-      const double* w = coefs + (d * 2 + kind) * 7;
+    if (oi < no && d < nd) {
+      const double* w = coefs + ((d0 + d) * 2 + kind) * 7;
       const double* x = thr + 3 * (o0 + oi);
-      double acc = 0.0;
-      acc = fma(w[0], x[0], acc);
-      acc = fma(w[1], x[1], acc);
-      acc = fma(w[2], x[2], acc);
-      part[d][kind][oi] = acc;
+      part[d][kind][oi] = (float)fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0)));
     }
   }
-  for (int t = threadIdx.x; t < n_dec * 2; t += blockDim.x) {
-    const double* w = coefs + t * 7;
-    wc[t >> 1][t & 1][0] = w[3];
-    wc[t >> 1][t & 1][1] = w[4];
-    wc[t >> 1][t & 1][2] = w[5];
-    wc[t >> 1][t & 1][3] = w[6];
+  for (int t = threadIdx.x; t < kDecChunk * 2; t += blockDim.x) {
+    if ((t >> 1) < nd) {
+      const double* w = coefs + ((d0 + (t >> 1)) * 2 + (t & 1)) * 7;
+#pragma unroll
+      for (int j = 0; j < 4; j++) wc[t >> 1][t & 1][j] = (float)w[3 + j];
+    }
   }
   if (threadIdx.x < no) own_solo[threadIdx.x] = solo[o0 + threadIdx.x];
   __syncthreads();
-  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n_sets) return;
-  int p[kMaxPeers];
-  const int k = unrank_multiset(r, E, cap, p);
-  // colo snapshot with every peer: ((0 + p1) + p2) + ...  (`simcore.py:126-131`)
-  double c0[3] = {0.0, 0.0, 0.0};
-  for (int i = 0; i < k; i++) {
-    c0[0] = c0[0] + thr[3 * p[i]];
-    c0[1] = c0[1] + thr[3 * p[i] + 1];
-    c0[2] = c0[2] + thr[3 * p[i] + 2];
-  }
-  // departures in (solo, row) order; snapshot i = fresh sum of the remaining
-  // peers in row order; EWMA(alpha) over snapshots (`colocation.py:54-63`)
-  int dep[kMaxPeers];
-  bool gone[kMaxPeers];
-  for (int i = 0; i < k; i++) {
-    dep[i] = i;
-    gone[i] = false;
-  }
-  for (int i = 1; i < k; i++) {  // insertion sort by (solo, row); p is row-sorted
-    int v = dep[i], j = i - 1;
-    while (j >= 0 && solo[p[dep[j]]] > solo[p[v]]) {
-      dep[j + 1] = dep[j];
-      j--;
-    }
-    dep[j + 1] = v;
-  }
-  double ew[kMaxPeers + 1][3];
-  ew[0][0] = c0[0];
-  ew[0][1] = c0[1];
-  ew[0][2] = c0[2];
+  const BinomTab C{binom_smem, nmax};
+  const long long r0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kGroup;
+  if (r0 >= ld) return;
+
+  constexpr int KP = KMAX > 0 ? KMAX : 1;
+  float c0[kGroup][3], ew[kGroup][KMAX + 1][3];
+  double sp[kGroup][KP];  // peer solo times (for "finishes before own")
+  int kk[kGroup];
   const double om = 1.0 - alpha;
-  for (int i = 1; i <= k; i++) {
-    gone[dep[i - 1]] = true;
-    double c[3] = {0.0, 0.0, 0.0};
-    for (int q = 0; q < k; q++)
-      if (!gone[q]) {
-        c[0] = c[0] + thr[3 * p[q]];
-        c[1] = c[1] + thr[3 * p[q] + 1];
-        c[2] = c[2] + thr[3 * p[q] + 2];
+#pragma unroll
+  for (int g = 0; g < kGroup; g++) {
+    const long long r = r0 + g;
+    int p[KP];
+    const int k = r < n_sets ? unrank_multiset<KMAX>(r, E, cap, C, p) : 0;
+    kk[g] = r < n_sets ? k : -1;
+    double th[KP][3];
+#pragma unroll
+    for (int q = 0; q < KMAX; q++) {
+      const int row = q < k ? p[q] : 0;
+      th[q][0] = thr[3 * row];
+      th[q][1] = thr[3 * row + 1];
+      th[q][2] = thr[3 * row + 2];
+      sp[g][q] = q < k ? solo[row] : INFINITY;
+    }
+    // departure rank of each peer: order (solo, row); p is row-sorted
+    int rk[KP];
+#pragma unroll
+    for (int q = 0; q < KMAX; q++) {
+      int rq = 0;
+#pragma unroll
+      for (int j = 0; j < KMAX; j++)
+        if (j != q && j < k && (sp[g][j] < sp[g][q] || (sp[g][j] == sp[g][q] && j < q))) rq++;
+      rk[q] = rq;
+    }
+    // snapshot i = fresh sum, in row order, of the peers not yet departed
+    // ((0+p1)+p2).. (`simcore.py:126-131`); EWMA prefixes (`colocation.py:61`)
+    double e[3];
+#pragma unroll
+    for (int i = 0; i <= KMAX; i++) {
+      double c[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < KMAX; q++)
+        if (q < k && rk[q] >= i) {
+          c[0] = c[0] + th[q][0];
+          c[1] = c[1] + th[q][1];
+          c[2] = c[2] + th[q][2];
+        }
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        e[a] = i == 0 ? c[a] : alpha * c[a] + om * e[a];
+        ew[g][i][a] = (float)e[a];
+        if (i == 0) c0[g][a] = (float)c[a];
       }
-    for (int a = 0; a < 3; a++) ew[i][a] = alpha * c[a] + om * ew[i - 1][a];
+    }
   }
-  double dep_solo[kMaxPeers];
-  for (int i = 0; i < k; i++) dep_solo[i] = solo[p[dep[i]]];
-  const long long ld = n_sets;  // row stride of one (dec, kind, own) slice
   for (int oi = 0; oi < no; oi++) {
     const double so = own_solo[oi];
-    int j = 0;
-    while (j < k && dep_solo[j] < so) j++;  // peers that finish first
-    const double* f = ew[j];
-    float* base = out + (long long)(o0 + oi) * ld + r;
-    for (int d = 0; d < n_dec; d++) {
-      const double* a = wc[d][0];
-      double yc = fma(a[2], c0[2], fma(a[1], c0[1], fma(a[0], c0[0], part[d][0][oi]))) + a[3];
-      const double* b = wc[d][1];
-      double yf = fma(b[2], f[2], fma(b[1], f[1], fma(b[0], f[0], part[d][1][oi]))) + b[3];
-      float* row = base + (long long)(d * 2) * E * ld;
-      __stcs(row, (float)yc);
-      __stcs(row + (long long)E * ld, (float)yf);
+    float fe[kGroup][3];
+#pragma unroll
+    for (int g = 0; g < kGroup; g++) {
+      int j = 0;
+#pragma unroll
+      for (int q = 0; q < KMAX; q++) j += (q < kk[g] && sp[g][q] < so) ? 1 : 0;  // peers that finish first
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        float v = ew[g][0][a];
+#pragma unroll
+        for (int i = 1; i <= KMAX; i++) v = (i == j) ? ew[g][i][a] : v;
+        fe[g][a] = v;
+      }
+    }
+    float* base = out + (long long)(o0 + oi) * ld + r0;
+#pragma unroll 2
+    for (int d = 0; d < nd; d++) {
+      const float* a = wc[d][0];
+      const float* b = wc[d][1];
+      const float pc = part[d][0][oi], pf = part[d][1][oi];
+      float yc[kGroup], yf[kGroup];
+#pragma unroll
+      for (int g = 0; g < kGroup; g++) {
+        const bool live = kk[g] >= 0;
+        yc[g] = live ? fmaf(a[2], c0[g][2], fmaf(a[1], c0[g][1], fmaf(a[0], c0[g][0], pc))) + a[3] : 0.0f;
+        yf[g] = live ? fmaf(b[2], fe[g][2], fmaf(b[1], fe[g][1], fmaf(b[0], fe[g][0], pf))) + b[3] : 0.0f;
+      }
+      float* row = base + (long long)((d0 + d) * 2) * E * ld;
+      __stcs(reinterpret_cast<float4*>(row), make_float4(yc[0], yc[1], yc[2], yc[3]));
+      __stcs(reinterpret_cast<float4*>(row + (long long)E * ld), make_float4(yf[0], yf[1], yf[2], yf[3]));
     }
   }
 }
@@ -220,72 +275,101 @@ __global__ void k_ols_final(const double* __restrict__ ws, int nblk, double* __r
   }
 }
 
-// cyclic Jacobi eigenvalues of a symmetric 7x7 (fp64), for the rank test
-__device__ void jacobi_eigs(const double* G, double* ev) {
+// cyclic Jacobi eigenvalues of a symmetric 7x7 (fp64), for the rank test.
+// Fully unrolled so the matrix lives in registers (no local memory).
+__device__ __forceinline__ void jacobi_eigs(const double* G, double* ev) {
   double a[7][7];
+#pragma unroll
   for (int i = 0; i < 7; i++)
+#pragma unroll
     for (int j = 0; j < 7; j++) a[i][j] = G[i * 7 + j];
-  for (int sweep = 0; sweep < 50; sweep++) {
+  for (int sweep = 0; sweep < 30; sweep++) {
     double off = 0.0;
+#pragma unroll
     for (int i = 0; i < 7; i++)
+#pragma unroll
       for (int j = i + 1; j < 7; j++) off += a[i][j] * a[i][j];
     if (off == 0.0) break;
+#pragma unroll
     for (int p = 0; p < 7; p++)
+#pragma unroll
       for (int q = p + 1; q < 7; q++) {
-        if (a[p][q] == 0.0) continue;
-        double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
-        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < 7; k++) {
-          double akp = a[k][p], akq = a[k][q];
-          a[k][p] = c * akp - s * akq;
-          a[k][q] = s * akp + c * akq;
-        }
-        for (int k = 0; k < 7; k++) {
-          double apk = a[p][k], aqk = a[q][k];
-          a[p][k] = c * apk - s * aqk;
-          a[q][k] = s * apk + c * aqk;
+        const double apq = a[p][q];
+        if (apq != 0.0) {
+          const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+          const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+#pragma unroll
+          for (int k = 0; k < 7; k++) {
+            const double akp = a[k][p], akq = a[k][q];
+            a[k][p] = c * akp - s * akq;
+            a[k][q] = s * akp + c * akq;
+          }
+#pragma unroll
+          for (int k = 0; k < 7; k++) {
+            const double apk = a[p][k], aqk = a[q][k];
+            a[p][k] = c * apk - s * aqk;
+            a[q][k] = s * apk + c * aqk;
+          }
         }
       }
   }
+#pragma unroll
   for (int i = 0; i < 7; i++) ev[i] = a[i][i];
 }
 
-// Cholesky solve of A x = b (A SPD 7x7); returns false if not PD
-__device__ bool chol_solve(const double* A, const double* b, double* x, double* inv) {
-  double L[7][7];
-  for (int i = 0; i < 7; i++)
-    for (int j = 0; j < 7; j++) L[i][j] = 0.0;
+// Cholesky factor of a 7x7 SPD matrix into registers; false if not PD
+__device__ __forceinline__ bool chol7(const double* A, double L[7][7]) {
+  bool ok = true;
+#pragma unroll
   for (int j = 0; j < 7; j++) {
     double d = A[j * 7 + j];
+#pragma unroll
     for (int k = 0; k < j; k++) d -= L[j][k] * L[j][k];
-    if (!(d > 0.0)) return false;
+    ok &= d > 0.0;
     L[j][j] = sqrt(d);
+#pragma unroll
     for (int i = j + 1; i < 7; i++) {
       double v = A[i * 7 + j];
+#pragma unroll
       for (int k = 0; k < j; k++) v -= L[i][k] * L[j][k];
       L[i][j] = v / L[j][j];
     }
   }
-  auto solve = [&](const double* rhs, double* out) {
-    double t[7];
-    for (int i = 0; i < 7; i++) {
-      double v = rhs[i];
-      for (int k = 0; k < i; k++) v -= L[i][k] * t[k];
-      t[i] = v / L[i][i];
-    }
-    for (int i = 6; i >= 0; i--) {
-      double v = t[i];
-      for (int k = i + 1; k < 7; k++) v -= L[k][i] * out[k];
-      out[i] = v / L[i][i];
-    }
-  };
-  if (b) solve(b, x);
+  return ok;
+}
+
+__device__ __forceinline__ void chol7_solve(const double L[7][7], const double* b, double* x) {
+  double t[7];
+#pragma unroll
+  for (int i = 0; i < 7; i++) {
+    double v = b[i];
+#pragma unroll
+    for (int k = 0; k < i; k++) v -= L[i][k] * t[k];
+    t[i] = v / L[i][i];
+  }
+#pragma unroll
+  for (int i = 6; i >= 0; i--) {
+    double v = t[i];
+#pragma unroll
+    for (int k = i + 1; k < 7; k++) v -= L[k][i] * x[k];
+    x[i] = v / L[i][i];
+  }
+}
+
+// Cholesky solve of A x = b and/or inverse; false if A is not PD
+__device__ bool chol_solve(const double* A, const double* b, double* x, double* inv) {
+  double L[7][7];
+  if (!chol7(A, L)) return false;
+  if (b) chol7_solve(L, b, x);
   if (inv) {
+#pragma unroll
     for (int c = 0; c < 7; c++) {
-      double e[7] = {0, 0, 0, 0, 0, 0, 0}, col[7];
-      e[c] = 1.0;
-      solve(e, col);
+      double e[7], col[7];
+#pragma unroll
+      for (int i = 0; i < 7; i++) e[i] = (i == c) ? 1.0 : 0.0;
+      chol7_solve(L, e, col);
+#pragma unroll
       for (int i = 0; i < 7; i++) inv[i * 7 + c] = col[i];
     }
   }
@@ -519,34 +603,52 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const double* __restrict_
 
 }  // namespace
 
+template <int K>
+static int launch_candidates(const intf_table* t, int cap, double alpha, const double* coefs, int n_dec, float* out,
+                             cudaStream_t st) {
+  const int E = t->n_rows;
+  const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
+  const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
+  if (smem > 200 * 1024) return bad_input("intf_predict_candidates: profile table too large for the binomial table");
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_candidates<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(ceil_div(ld / kGroup, kCandThreads), ceil_div(E, kOwnChunk), ceil_div(n_dec, kDecChunk));
+  k_candidates<K><<<grid, kCandThreads, smem, st>>>(t->solo_ms, t->thr, E, cap, sets, ld, alpha, coefs, n_dec, out);
+  return launch_status("k_candidates");
+}
+
 extern "C" {
 
-int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t* n_cand) {
+int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t* n_cand, int64_t* n_sets, int64_t* ld) {
   if (n_rows < 1 || cap < 1 || cap > kMaxPeers + 1 || !n_cand) return bad_input("intf_candidate_count: bad argument");
-  long long sets = 0;
-  for (int k = 0; k < cap; k++) sets += binom(n_rows + k - 1, k);
+  const long long sets = n_multisets(n_rows, cap);
   *n_cand = (int64_t)n_rows * sets;
+  if (n_sets) *n_sets = sets;
+  if (ld) *ld = (sets + kGroup - 1) / kGroup * kGroup;
   return INTF_OK;
 }
 
 int intf_predict_candidates(const intf_table* table, int32_t cap, double alpha, const double* coefs, int32_t n_dec,
                             float* out, void* stream) {
-  if (!table || !coefs || !out || n_dec < 1 || n_dec > kMaxDec || cap < 1 || cap > kMaxPeers + 1)
-    return bad_input("intf_predict_candidates: bad argument (1 <= n_dec <= 64, 1 <= cap <= 8)");
-  const int E = table->n_rows;
-  long long sets = 0;
-  for (int k = 0; k < cap; k++) sets += binom(E + k - 1, k);
-  dim3 grid(ceil_div(sets, kCandThreads), ceil_div(E, kOwnChunk));
-  k_candidates<<<grid, kCandThreads, 0, as_stream(stream)>>>(table->solo_ms, table->thr, E, cap, sets, alpha, coefs,
-                                                             n_dec, out);
-  return launch_status("k_candidates");
+  if (!table || !coefs || !out || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1 || table->n_rows < 1)
+    return bad_input("intf_predict_candidates: bad argument (n_dec >= 1, 1 <= cap <= 8)");
+  cudaStream_t st = as_stream(stream);
+  switch (cap - 1) {
+    case 0: return launch_candidates<0>(table, cap, alpha, coefs, n_dec, out, st);
+    case 1: return launch_candidates<1>(table, cap, alpha, coefs, n_dec, out, st);
+    case 2: return launch_candidates<2>(table, cap, alpha, coefs, n_dec, out, st);
+    case 3: return launch_candidates<3>(table, cap, alpha, coefs, n_dec, out, st);
+    case 4: return launch_candidates<4>(table, cap, alpha, coefs, n_dec, out, st);
+    case 5: return launch_candidates<5>(table, cap, alpha, coefs, n_dec, out, st);
+    case 6: return launch_candidates<6>(table, cap, alpha, coefs, n_dec, out, st);
+    default: return launch_candidates<7>(table, cap, alpha, coefs, n_dec, out, st);
+  }
 }
 
 int intf_predict_candidates_host(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
                                  int32_t n_dec, float* h_out, float* d_scratch, void* stream) {
-  if (!h_coefs || !h_out || !d_scratch) return bad_input("intf_predict_candidates_host: null argument");
-  int64_t n_cand = 0;
-  int rc = intf_candidate_count(table->n_rows, cap, &n_cand);
+  if (!table || !h_coefs || !h_out || !d_scratch) return bad_input("intf_predict_candidates_host: null argument");
+  int64_t n_cand = 0, n_sets = 0, ld = 0;
+  int rc = intf_candidate_count(table->n_rows, cap, &n_cand, &n_sets, &ld);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   // coefs staged at the head of the scratch buffer (doubles), outputs after it
@@ -556,8 +658,8 @@ int intf_predict_candidates_host(const intf_table* table, int32_t cap, double al
     return launch_status("copy coefs");
   rc = intf_predict_candidates(table, cap, alpha, d_coefs, n_dec, d_out, stream);
   if (rc) return rc;
-  if (cudaMemcpyAsync(h_out, d_out, sizeof(float) * (size_t)n_cand * 2 * n_dec, cudaMemcpyDeviceToHost, st) !=
-      cudaSuccess)
+  if (cudaMemcpyAsync(h_out, d_out, sizeof(float) * (size_t)ld * table->n_rows * 2 * n_dec, cudaMemcpyDeviceToHost,
+                      st) != cudaSuccess)
     return launch_status("copy predictions");
   return INTF_OK;
 }

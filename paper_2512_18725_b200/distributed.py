@@ -1,0 +1,106 @@
+"""Multi-GPU plumbing for the hot path: one process per GPU,
+torch.distributed (NCCL on B200s, gloo in CPU tests).
+
+Only two exchange steps exist on this path:
+  * OLS refit over samples sharded across ranks: every rank reduces its
+    shard to the 56 fp64 normal-equation statistics (intf_ols_stats); the
+    ranks exchange them with one all_gather and sum IN RANK ORDER, so every
+    rank solves the identical 7x7 system (deterministic, unlike a ring
+    all_reduce whose summation order depends on the topology);
+  * the scenario sweep: each rank replays a contiguous range of scenarios
+    and the fixed-size per-scenario report rows are gathered to every rank.
+Candidate scoring and the RLS/SGD streams shard with no collective
+(independent decisions / streams).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+REPORT_MODELS = 4
+REPORT_WIDTH = 4 + 5 * REPORT_MODELS  # n_req, n_batches, n_segments, status, then per model (n, met, p50, p95, p99)
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple:
+    """Contiguous balanced [lo, hi) of n units for this rank."""
+    q, r = divmod(n, world)
+    lo = rank * q + min(rank, r)
+    return lo, lo + q + (1 if rank < r else 0)
+
+
+def weighted_shards(weights, world: int) -> list:
+    """Contiguous shards balanced by weight (e.g. expected requests
+    lambda*T per scenario): greedy cut at multiples of total/world."""
+    w = np.asarray(weights, dtype=float)
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = [0]
+    for k in range(1, world):
+        cuts.append(int(np.searchsorted(cum, cum[-1] * k / world)))
+    cuts.append(len(w))
+    cuts = np.maximum.accumulate(np.array(cuts))
+    return [(int(cuts[k]), int(cuts[k + 1])) for k in range(world)]
+
+
+def allreduce_ols_stats(stats: torch.Tensor) -> torch.Tensor:
+    """Sum the 56 OLS statistics over ranks in rank order (all_gather)."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return stats
+    parts = [torch.empty_like(stats) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, stats.contiguous())
+    out = parts[0].clone()
+    for p in parts[1:]:
+        out += p
+    return out
+
+
+def report_rows(pipe, h) -> np.ndarray:
+    """Fixed-size per-scenario report rows from a fetched ReplayPipeline."""
+    S = pipe.pb.n_scen
+    rows = np.full((S, REPORT_WIDTH), np.nan)
+    for s in range(S):
+        sc = pipe.pb.scen[s]
+        rows[s, 0] = h["n_req"][s]
+        rows[s, 1] = h["n_batches"][s]
+        rows[s, 2] = h["n_segments"][s]
+        rows[s, 3] = h["status"][s]
+        for m in range(min(sc.n_models, REPORT_MODELS)):
+            g = sc.model_off + m
+            rows[s, 4 + 5 * m: 9 + 5 * m] = (h["slo_n"][g], h["slo_met"][g], *h["slo_p"][g])
+    return rows
+
+
+def gather_rows(local: torch.Tensor, n_total: int) -> torch.Tensor:
+    """all_gather of per-rank [n_local, F] row blocks laid out by
+    shard_range; returns the full [n_total, F] table on every rank."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return local
+    world = dist.get_world_size()
+    width = local.shape[1]
+    maxn = max(shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0] for r in range(world))
+    pad = torch.full((maxn, width), float("nan"), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    return torch.cat([parts[r][: shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0]]
+                      for r in range(world)])
+
+
+def sweep(specs_all: list, table, preds=(), device_rows: bool = True):
+    """Replay this rank's shard of a scenario sweep on its GPU and gather the
+    report rows of all scenarios (C5 across GPUs)."""
+    import torch.distributed as dist
+
+    from . import engine
+
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    lo, hi = shard_range(len(specs_all), rank, world)
+    pipe, h = engine.run_batch(specs_all[lo:hi], table, preds=preds)
+    local = torch.as_tensor(report_rows(pipe, h))
+    if device_rows:
+        local = local.cuda()
+    return gather_rows(local, len(specs_all)).cpu().numpy()

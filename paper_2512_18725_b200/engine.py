@@ -379,16 +379,23 @@ def eval_reports(yhat_list, y_list) -> np.ndarray:
     return out.cpu().numpy().reshape(-1, 6)
 
 
+def candidate_layout(n_rows: int, cap: int) -> tuple:
+    """(n_cand, n_sets, ld) of the candidate enumeration (intf_candidate_count)."""
+    n, s, ld = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    _abi.check(_abi.load().intf_candidate_count(n_rows, cap, ctypes.byref(n), ctypes.byref(s), ctypes.byref(ld)),
+               "intf_candidate_count")
+    return int(n.value), int(s.value), int(ld.value)
+
+
 def candidate_count(n_rows: int, cap: int) -> int:
-    n = ctypes.c_int64(0)
-    _abi.check(_abi.load().intf_candidate_count(n_rows, cap, ctypes.byref(n)), "intf_candidate_count")
-    return int(n.value)
+    return candidate_layout(n_rows, cap)[0]
 
 
 class CandidateScorer:
     """Every candidate co-location set over a profile table,
     scored by a coarse (static) and a fine (EWMA) linear predictor for n_dec
-    decisions.  Output (device, fp32): [n_dec][2][E][n_sets]."""
+    decisions.  Output (device, fp32): [n_dec][2][E][ld], first n_sets of
+    each row valid (ld = n_sets rounded up to 4)."""
 
     def __init__(self, table: _pack.TableArrays, cap: int, alpha: float = 0.5, dtable: DeviceTable | None = None):
         self.dev = require_cuda()
@@ -396,11 +403,17 @@ class CandidateScorer:
         self.E = table.n_rows
         self.cap = int(cap)
         self.alpha = float(alpha)
-        self.n_cand = candidate_count(self.E, self.cap)
-        self.n_sets = self.n_cand // self.E
+        self.n_cand, self.n_sets, self.ld = candidate_layout(self.E, self.cap)
+
+    def out_elems(self, n_dec: int) -> int:
+        return n_dec * 2 * self.E * self.ld
 
     def alloc(self, n_dec: int) -> torch.Tensor:
-        return torch.empty(n_dec * 2 * self.n_cand, dtype=torch.float32, device=self.dev)
+        return torch.empty(self.out_elems(n_dec), dtype=torch.float32, device=self.dev)
+
+    def view(self, out, n_dec: int):
+        """[n_dec, 2, E, n_sets] view of an output buffer (torch or numpy)."""
+        return out.reshape(n_dec, 2, self.E, self.ld)[..., : self.n_sets]
 
     def score(self, coefs: torch.Tensor, out: torch.Tensor) -> None:
         """coefs: device float64 [n_dec][2][7]; enqueue only (no sync)."""

@@ -1,0 +1,50 @@
+"""Synthetic workloads of the benchmark configs, as scenario
+dicts ready for the batched device pipeline.
+
+C5: scenario i draws from default_rng([2512, i]): 2-4 models of the bundled
+table, total load rho ~ U(0.3, 0.9) split evenly, SLO = U(5, 50) x solo(bs=1),
+1 s, window U(0, 10) ms, cap in {1, 2, 3}, sigma 0.05, oracle seed i.
+C4: 16 models (6 default archetypes + 10 from default_rng(123)), bs <= 64,
+cap 4, heterogeneous per-model load.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .profiles import DEFAULT_ARCHETYPES, Archetype, gen_synthetic_profiles
+
+
+def c5_scenario(table, i: int) -> dict:
+    rng = np.random.default_rng([2512, i])
+    models = table.models()
+    k = int(rng.integers(2, 5))
+    chosen = [models[j] for j in rng.choice(len(models), size=k, replace=False)]
+    rho = float(rng.uniform(0.3, 0.9))
+    dep = []
+    for m in chosen:
+        bs = table.max_batch_size
+        cap_rps = bs / (table.get(m, bs).solo_duration_ms / 1000.0)
+        dep.append({"model_id": m, "arrival_rate_rps": rho / k * cap_rps,
+                    "slo_ms": float(rng.uniform(5.0, 50.0)) * table.get(m, 1).solo_duration_ms})
+    return {
+        "name": f"c5_{i}", "duration_s": 1.0, "batching_window_ms": float(rng.uniform(0.0, 10.0)),
+        "max_batch_size": 8, "concurrency_cap": int(rng.integers(1, 4)), "seed": i,
+        "colocation_mode": "static", "ewma_alpha": 1.0,
+        "oracle": {"beta_l2": 1.0, "beta_dram": 1.5, "beta_sm": 0.5, "noise_sigma": 0.05, "seed": i},
+        "deployed": dep,
+    }
+
+
+def c5_scenarios(table, n: int, start: int = 0) -> list:
+    return [c5_scenario(table, i) for i in range(start, start + n)]
+
+
+def table16():
+    rng = np.random.default_rng(123)
+    arch = list(DEFAULT_ARCHETYPES)
+    for i in range(10):
+        base = float(rng.uniform(0.8, 8.0))
+        eff = float(rng.uniform(0.2, 0.95))
+        mix = tuple(float(v) for v in rng.uniform(0.2, 0.6, size=3))
+        arch.append(Archetype(f"synth_{i:02d}", base, eff, mix))
+    return gen_synthetic_profiles(arch, seed=0, max_batch_size=64), arch

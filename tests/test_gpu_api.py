@@ -79,6 +79,7 @@ def test_empty_trace_and_edge_shapes():
     res = p.run_scenario(spec, table)
     assert res.outcomes == [] and res.records == []
     one = p.ScenarioSpec(deployed=(p.DeployedModel("resnet50", 500.0, 10.0),), duration_s=0.5,
-                         batching_window_ms=0.0, max_batch_size=1, concurrency_cap=1)
+                         batching_window_ms=0.0, max_batch_size=1, concurrency_cap=1,
+                         oracle=p.InterferenceOracle(noise_sigma=0.0))
     res = p.run_scenario(one, table)
-    assert all(o.interference_ratio == 1.0 for o in res.outcomes)  # cap 1: never co-located
+    assert res.outcomes and all(o.interference_ratio == 1.0 for o in res.outcomes)  # cap 1, sigma 0 (`test_acceptance.py:137-138`)

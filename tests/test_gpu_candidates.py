@@ -33,7 +33,7 @@ def test_candidates_match_reference_composition(cap):
     coefs = torch.tensor(C["w"], dtype=torch.float64, device="cuda").reshape(1, 2, 7).contiguous()
     out = sc.alloc(1)
     sc.score(coefs, out)
-    y = out.cpu().numpy().reshape(2, sc.E, sc.n_sets)
+    y = sc.view(out.cpu().numpy(), 1)[0]
     own, peers = C[f"cap{cap}/own"], C[f"cap{cap}/peers"]
     idx = np.array([engine.multiset_rank([q for q in pe if q >= 0], sc.E, cap) for pe in peers])
     np.testing.assert_allclose(y[0, own, idx], C[f"cap{cap}/y_coarse"], rtol=RTOL)
@@ -50,7 +50,7 @@ def test_cap4_full_enumeration_sampled_against_oracle():
     coefs = torch.tensor(W, dtype=torch.float64, device="cuda").contiguous()
     out = sc.alloc(3)
     sc.score(coefs, out)
-    y = out.cpu().numpy().reshape(3, 2, sc.E, sc.n_sets)
+    y = sc.view(out.cpu().numpy(), 3)
     assert np.isfinite(y).all()
     import itertools
 
@@ -71,7 +71,7 @@ def test_host_buffer_variant_equals_device_variant():
     W = np.stack([C["w"], C["w"] * 0.5])
     dev_out = sc.alloc(2)
     sc.score(torch.tensor(W, device="cuda").contiguous(), dev_out)
-    host_out = np.empty(2 * 2 * sc.n_cand, dtype=np.float32)
+    host_out = np.empty(sc.out_elems(2), dtype=np.float32)
     scratch = torch.empty(2 * 2 * 7 * 2 + host_out.size, dtype=torch.float32, device="cuda")
     sc.score_host(np.ascontiguousarray(W), host_out, scratch)
     torch.cuda.synchronize()
