@@ -105,7 +105,9 @@ typedef struct intf_replay_buffers {
   double *s_tbegin, *s_tend, *s_slowdown, *s_colo; /* s_colo: [3*k] */
   int32_t *n_batches, *n_segments, *n_reseats, *status; /* [n_scen] */
   double *slot_seg;            /* scratch: n_scen*cap_max*seg_stride*5 doubles */
+  double *noise_tab;           /* scratch: [req slots][noise_k] precomputed noise draws */
   int32_t seg_stride, cap_max;
+  int32_t noise_k, pad_;       /* segments per batch whose noise is precomputed (0 = inline) */
 } intf_replay_buffers;
 
 /* generate_arrivals (`workload.py:74-104`): per-model Poisson streams
@@ -122,7 +124,10 @@ int intf_split_arrivals(const intf_batch *batch, const intf_replay_buffers *buf,
  * FIFO capped admission and reseats (`simcore.py:126-171`), noise
  * (`oracle.py:24-33`), slowdown (`oracle.py:36-47`), completion
  * (`simcore.py:56-66,173-198`), request->batch records (`:264-279`).
- * Bit-exact with the reference.  One CUDA thread per scenario. */
+ * Bit-exact with the reference.  Three launches: k_form (batch formation,
+ * thread per scenario), k_noise_table (the first noise_k noise draws of every
+ * batch, fully parallel; skipped if noise_k == 0) and k_replay (the serial
+ * admission/reseat/completion recurrence, thread per scenario). */
 int intf_replay(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf, void *stream);
 
 /* Per-(scenario, model) SLO report (`metrics.py:49-79`, nearest-rank
@@ -225,8 +230,8 @@ int intf_latency_report(const int32_t *group, const double *arrival, const doubl
 int intf_noise_draws(uint64_t seed, double sigma, const int64_t *batch, const int64_t *seg, int64_t n, double *out,
                      void *stream);
 
-/* oracle_slowdown (`oracle.py:36-47`) for n rows: own[3i..], colo[3i..],
- * beta[3] (device), noise[n] (device, or NULL = 1.0).                      */
+/* oracle_slowdown (`oracle.py:36-47`) for n rows: own[3i..], colo[3i..]
+ * (device), beta[3] (HOST, read at launch), noise[n] (device, or NULL = 1.0). */
 int intf_slowdowns(const double *own, const double *colo, const double *beta, const double *noise, int64_t n,
                    double *out, void *stream);
 

@@ -54,12 +54,13 @@ REPLAY_BUFFER_FIELDS = [
     "b_model", "b_size", "b_formed", "b_start", "b_completion", "b_measured", "b_seg_off", "b_nseg",
     "out_order", "r_batch", "r_slo_met",
     "s_tbegin", "s_tend", "s_slowdown", "s_colo",
-    "n_batches", "n_segments", "n_reseats", "status", "slot_seg",
+    "n_batches", "n_segments", "n_reseats", "status", "slot_seg", "noise_tab",
 ]
 
 
 class ReplayBuffers(ctypes.Structure):
-    _fields_ = [(f, P) for f in REPLAY_BUFFER_FIELDS] + [("seg_stride", c_int32), ("cap_max", c_int32)]
+    _fields_ = [(f, P) for f in REPLAY_BUFFER_FIELDS] + [("seg_stride", c_int32), ("cap_max", c_int32),
+                                                          ("noise_k", c_int32), ("pad_", c_int32)]
 
 
 class Predictor(ctypes.Structure):

@@ -82,14 +82,40 @@ __global__ void k_split_arrivals(const intf_scenario* __restrict__ scen, int n_s
   B.status[s] |= st;
 }
 
+// ---- K1: batch formation, one thread per scenario (no GPU state, no RNG).
+__global__ void __launch_bounds__(32) k_form(const intf_scenario* __restrict__ scen, int n_scen,
+                                             const intf_model* __restrict__ models, intf_replay_buffers B) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_scen) return;
+  if (B.status[s] & INTF_ST_OVERFLOW) {  // arrivals did not fit
+    B.n_batches[s] = 0;
+    return;
+  }
+  form_scenario(s, scen, models, B);
+}
+
+// ---- K1b: noise draws of the first noise_k segments of every formed batch
+// (`oracle.py:24-33`), fully parallel: takes the SeedSequence/PCG64/ziggurat/
+// exp chain off the serial replay recurrence.  grid: (slots, scenarios).
+__global__ void k_noise_table(const intf_scenario* __restrict__ scen, intf_replay_buffers B) {
+  const int s = blockIdx.y;
+  const intf_scenario& S = scen[s];
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = B.noise_k;
+  const long long b = i / K;
+  if (b >= B.n_batches[s]) return;
+  const int k = (int)(i % K);
+  B.noise_tab[(long long)(S.req_off + b) * K + k] = noise_draw(S.oracle_seed, (uint64_t)b, (uint64_t)k, S.sigma);
+}
+
 // ---- K2: the replay recurrence, one thread per scenario.
-__global__ void __launch_bounds__(64) k_replay(const intf_scenario* __restrict__ scen, int n_scen,
+__global__ void __launch_bounds__(32) k_replay(const intf_scenario* __restrict__ scen, int n_scen,
                                                const intf_model* __restrict__ models, intf_table tab,
                                                intf_replay_buffers B) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_scen) return;
   if (B.status[s] & INTF_ST_OVERFLOW) return;  // arrivals did not fit
-  replay_scenario(s, scen, models, tab, B);
+  replay_formed(s, scen, models, tab, B);
 }
 
 // ---- K3: SLO records + per-model nearest-rank percentiles, one block per
@@ -274,9 +300,20 @@ int intf_split_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, vo
 
 int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf, void* stream) {
   if (!bt || !bt->scen || !bt->models || !buf || !table || bt->n_scen <= 0) return bad_input("intf_replay: null argument");
-  if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1)
-    return bad_input("intf_replay: cap_max must be in [1, 8] and seg_stride >= 1");
-  k_replay<<<ceil_div(bt->n_scen, 64), 64, 0, as_stream(stream)>>>(bt->scen, bt->n_scen, bt->models, *table, *buf);
+  if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1 || buf->noise_k < 0)
+    return bad_input("intf_replay: cap_max must be in [1, 8], seg_stride >= 1, noise_k >= 0");
+  if (buf->noise_k > 0 && (!buf->noise_tab || bt->n_scen > 65535))
+    return bad_input("intf_replay: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
+  cudaStream_t st = as_stream(stream);
+  int rc;
+  k_form<<<ceil_div(bt->n_scen, 32), 32, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
+  if ((rc = launch_status("k_form"))) return rc;
+  if (buf->noise_k > 0 && bt->max_req_cap > 0) {
+    dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
+    k_noise_table<<<grid, 128, 0, st>>>(bt->scen, *buf);
+    if ((rc = launch_status("k_noise_table"))) return rc;
+  }
+  k_replay<<<ceil_div(bt->n_scen, 32), 32, 0, st>>>(bt->scen, bt->n_scen, bt->models, *table, *buf);
   return launch_status("k_replay");
 }
 

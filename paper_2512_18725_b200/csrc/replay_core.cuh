@@ -113,6 +113,7 @@ INTF_FN FormEv next_formation(const double* lt, const int32_t* lrid, int n, int 
 
 struct Slot {
   double start, total, progress, done, own[3];
+  double cur_tb, cur_sd;  // the open (last) segment, mirrored from scratch
   int32_t batch, entry, nseg, n_non1;
 };
 
@@ -140,7 +141,11 @@ INTF_FN void reseat(ReplayCtx& c, Slot* slots, const int* run, int nrun, int si,
     colo[2] = colo[2] + o.own[2];
   }
   const intf_scenario& S = *c.S;
-  double noise = noise_draw(S.oracle_seed, (uint32_t)rb.batch, (uint32_t)rb.nseg, S.sigma);
+  double noise;
+  if (rb.nseg < c.buf->noise_k)  // precomputed by k_noise_table (same draw)
+    noise = c.buf->noise_tab[(size_t)(S.req_off + rb.batch) * c.buf->noise_k + rb.nseg];
+  else
+    noise = noise_draw(S.oracle_seed, (uint64_t)rb.batch, (uint64_t)rb.nseg, S.sigma);
   double sd = slowdown(rb.own, colo, S.beta, noise);
   if (rb.nseg >= c.buf->seg_stride) {
     c.status |= INTF_ST_SEG_STRIDE;
@@ -153,6 +158,8 @@ INTF_FN void reseat(ReplayCtx& c, Slot* slots, const int* run, int nrun, int si,
     p[4] = colo[2];
   }
   rb.nseg++;
+  rb.cur_tb = now;
+  rb.cur_sd = sd;
   if (sd != 1.0) rb.n_non1++;
   c.n_reseats++;
   rb.done = now + (rb.total - rb.progress) * sd;
@@ -161,34 +168,27 @@ INTF_FN void reseat(ReplayCtx& c, Slot* slots, const int* run, int nrun, int si,
 
 // RunningBatch.close_segment (`simcore.py:56-66`)
 INTF_FN void close_segment(ReplayCtx& c, Slot& rb, int si, double now) {
-  int k = rb.nseg - 1;
-  if (k >= c.buf->seg_stride) {
-    rb.nseg--;  // overflowed segment (already flagged)
-    return;
-  }
-  const double* p = seg_ptr(c, si, k);
-  if (now == p[0]) {
+  (void)c;
+  (void)si;
+  if (now == rb.cur_tb) {  // zero-length interval: drop it, reuse its index
     rb.nseg--;
-    if (p[1] != 1.0) rb.n_non1--;
+    if (rb.cur_sd != 1.0) rb.n_non1--;
     return;
   }
-  rb.progress = rb.progress + (now - p[0]) / p[1];
+  rb.progress = rb.progress + (now - rb.cur_tb) / rb.cur_sd;
 }
 
-// One full run_scenario for scenario s.
-INTF_FN void replay_scenario(int s, const intf_scenario* scens, const intf_model* models, const intf_table& tab,
-                             const intf_replay_buffers& B) {
+// Batch formation for scenario s (`batcher.py:44-85` + the WINDOW/ARRIVAL
+// branches of `simcore.py:246-256,289-299`): merges the per-model formation
+// events in heap order (time, kind, key) and assigns global batch ids.
+// Writes b_model, b_size, b_formed, r_batch and n_batches.  GPU-state free.
+INTF_FN void form_scenario(int s, const intf_scenario* scens, const intf_model* models,
+                           const intf_replay_buffers& B) {
   const intf_scenario& S = scens[s];
   const int M = S.n_models;
-  ReplayCtx c;
-  c.S = &S;
-  c.tab = &tab;
-  c.buf = &B;
-  c.seg = B.slot_seg + (size_t)s * (size_t)B.cap_max * (size_t)B.seg_stride * 5;
-  c.status = 0;
-  c.n_reseats = 0;
   if (M > kMaxModels || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 || S.max_bs < 1) {
     B.status[s] = INTF_ST_CAP;
+    B.n_batches[s] = 0;
     return;
   }
   const intf_model* md = models + S.model_off;
@@ -196,10 +196,48 @@ INTF_FN void replay_scenario(int s, const intf_scenario* scens, const intf_model
   int head[kMaxModels];
   for (int m = 0; m < M; m++) {
     head[m] = 0;
-    const intf_model& mm = md[m];
-    ev[m] = next_formation(B.list_t + mm.list_off, B.list_rid + mm.list_off, B.n_list[S.model_off + m], 0,
-                           S.window_ms, S.max_bs, mm.crc);
+    ev[m] = next_formation(B.list_t + md[m].list_off, B.list_rid + md[m].list_off, B.n_list[S.model_off + m], 0,
+                           S.window_ms, S.max_bs, md[m].crc);
   }
+  const int ro = S.req_off;
+  int n_formed = 0;
+  for (;;) {
+    int fm = -1;
+    for (int m = 0; m < M; m++)
+      if (ev[m].kind && (fm < 0 || form_less(ev[m], ev[fm]))) fm = m;
+    if (fm < 0) break;
+    const FormEv e = ev[fm];
+    const intf_model& mm = md[fm];
+    const int b = n_formed++;
+    B.b_model[ro + b] = fm;
+    B.b_size[ro + b] = e.cnt;
+    B.b_formed[ro + b] = e.t;
+    const int32_t* lrid = B.list_rid + mm.list_off;
+    for (int j = 0; j < e.cnt; j++) B.r_batch[ro + lrid[head[fm] + j]] = b;
+    head[fm] += e.cnt;
+    ev[fm] = next_formation(B.list_t + mm.list_off, lrid, B.n_list[S.model_off + fm], head[fm], S.window_ms,
+                            S.max_bs, mm.crc);
+  }
+  B.n_batches[s] = n_formed;
+}
+
+// The replay proper for scenario s over its formed batches: FIFO capped
+// admission, reseats, completions, outcome order.  Formation events are the
+// batches in id order (their (time, kind, key) order was resolved by
+// form_scenario); a completion precedes a formation at equal time (kind 0).
+INTF_FN void replay_formed(int s, const intf_scenario* scens, const intf_model* models, const intf_table& tab,
+                           const intf_replay_buffers& B) {
+  const intf_scenario& S = scens[s];
+  ReplayCtx c;
+  c.S = &S;
+  c.tab = &tab;
+  c.buf = &B;
+  c.seg = B.slot_seg + (size_t)s * (size_t)B.cap_max * (size_t)B.seg_stride * 5;
+  c.status = B.status[s];
+  c.n_reseats = 0;
+  if (c.status & INTF_ST_CAP) return;
+  const intf_model* md = models + S.model_off;
+  const int nb = B.n_batches[s];
   Slot slots[kMaxCap];
   int run[kMaxCap], free_slots[kMaxCap], nfree = S.cap, nrun = 0;
   for (int i = 0; i < S.cap; i++) free_slots[i] = S.cap - 1 - i;
@@ -208,9 +246,6 @@ INTF_FN void replay_scenario(int s, const intf_scenario* scens, const intf_model
   const int ro = S.req_off;
 
   for (;;) {
-    int fm = -1;
-    for (int m = 0; m < M; m++)
-      if (ev[m].kind && (fm < 0 || form_less(ev[m], ev[fm]))) fm = m;
     int ci = -1;
     for (int i = 0; i < nrun; i++) {
       if (ci < 0) {
@@ -221,8 +256,9 @@ INTF_FN void replay_scenario(int s, const intf_scenario* scens, const intf_model
       const Slot& b = slots[run[ci]];
       if (a.done < b.done || (a.done == b.done && a.batch < b.batch)) ci = i;
     }
-    if (ci < 0 && fm < 0) break;
-    if (ci >= 0 && (fm < 0 || slots[run[ci]].done <= ev[fm].t)) {
+    const bool have_form = n_formed < nb;
+    if (ci < 0 && !have_form) break;
+    if (ci >= 0 && (!have_form || slots[run[ci]].done <= B.b_formed[ro + n_formed])) {
       // ---- COMPLETION (`simcore.py:173-198`, `:283-288`)
       const int si = run[ci];
       Slot& rb = slots[si];
@@ -279,19 +315,10 @@ INTF_FN void replay_scenario(int s, const intf_scenario* scens, const intf_model
         reseat(c, slots, run, nrun, run[i], now);
       }
     } else {
-      // ---- FORMATION (ARRIVAL at max_bs, or WINDOW expiry)
-      const FormEv e = ev[fm];
-      now = now > e.t ? now : e.t;
-      const intf_model& mm = md[fm];
-      const int b = n_formed++;
-      B.b_model[ro + b] = fm;
-      B.b_size[ro + b] = e.cnt;
-      B.b_formed[ro + b] = now;
-      const int32_t* lrid = B.list_rid + mm.list_off;
-      for (int j = 0; j < e.cnt; j++) B.r_batch[ro + lrid[head[fm] + j]] = b;
-      head[fm] += e.cnt;
-      ev[fm] = next_formation(B.list_t + mm.list_off, lrid, B.n_list[S.model_off + fm], head[fm], S.window_ms,
-                              S.max_bs, mm.crc);
+      // ---- FORMATION: batch n_formed enters the FIFO dispatch queue
+      const double t = B.b_formed[ro + n_formed];
+      now = now > t ? now : t;
+      n_formed++;
     }
     // ---- try_dispatch (`simcore.py:258-262`) -> GpuState.dispatch (`:153-171`)
     while (dq < n_formed && nrun < S.cap) {
@@ -318,10 +345,16 @@ INTF_FN void replay_scenario(int s, const intf_scenario* scens, const intf_model
     }
   }
   if (nrun || dq < n_formed) c.status |= INTF_ST_NONQUIESCENT;
-  B.n_batches[s] = n_formed;
   B.n_segments[s] = seg_cursor;
   B.n_reseats[s] = c.n_reseats;
   B.status[s] = c.status;
+}
+
+// One full run_scenario for scenario s (formation + replay, no noise table).
+INTF_FN void replay_scenario(int s, const intf_scenario* scens, const intf_model* models, const intf_table& tab,
+                             const intf_replay_buffers& B) {
+  form_scenario(s, scens, models, B);
+  replay_formed(s, scens, models, tab, B);
 }
 
 // -------------------------------------------------------- features + predict

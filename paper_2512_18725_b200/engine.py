@@ -58,18 +58,19 @@ class ReplayPipeline:
     """
 
     def __init__(self, specs, table: _pack.TableArrays, seg_stride: int = 64, scale: float = 1.0,
-                 preds=(), list_caps=None, dtable: DeviceTable | None = None):
+                 preds=(), list_caps=None, dtable: DeviceTable | None = None, noise_k: int = 4):
         self.dev = require_cuda()
         self.lib = _abi.load()
         self.pb = _pack.pack(list(specs), table, scale=scale, list_caps=list_caps)
         self.seg_stride = int(seg_stride)
         self.dtable = dtable or DeviceTable(table, self.dev)
-        sz = _pack.sizes(self.pb, self.seg_stride)
+        self.noise_k = int(noise_k) if self.pb.n_scen <= 65535 else 0
+        sz = _pack.sizes(self.pb, self.seg_stride, self.noise_k)
         self.t = {f: torch.zeros(sz[k], dtype=_TORCH_DT[dt], device=self.dev) for f, dt, k in _pack.BUFFER_PLAN}
         self.B = _abi.ReplayBuffers()
         for f in _abi.REPLAY_BUFFER_FIELDS:
             setattr(self.B, f, self.t[f].data_ptr())
-        self.B.seg_stride, self.B.cap_max = self.seg_stride, self.pb.cap_max
+        self.B.seg_stride, self.B.cap_max, self.B.noise_k = self.seg_stride, self.pb.cap_max, self.noise_k
         self.d_scen = to_device(_struct_bytes(self.pb.scen), self.dev)
         self.d_models = to_device(_struct_bytes(self.pb.models), self.dev)
         self.batch = _abi.Batch(self.d_scen.data_ptr(), self.d_models.data_ptr(), self.pb.n_scen, self.pb.n_models,
@@ -481,11 +482,11 @@ def noise_draws(seed: int, sigma: float, batch_ids, seg_idx) -> np.ndarray:
 def slowdowns(own, colo, beta, noise=None) -> np.ndarray:
     dev = require_cuda()
     o, c = _f64(np.asarray(own).reshape(-1, 3), dev), _f64(np.asarray(colo).reshape(-1, 3), dev)
-    bt = _f64(beta, dev)
+    bt = np.ascontiguousarray(beta, dtype=np.float64)  # host array (read at launch)
     nz = _f64(noise, dev) if noise is not None else None
     n = o.shape[0]
     out = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
-    _abi.check(_abi.load().intf_slowdowns(o.data_ptr(), c.data_ptr(), bt.data_ptr(), _abi.addr(nz), n, out.data_ptr(),
+    _abi.check(_abi.load().intf_slowdowns(o.data_ptr(), c.data_ptr(), bt.ctypes.data, _abi.addr(nz), n, out.data_ptr(),
                                           stream_ptr()), "intf_slowdowns")
     return out.cpu().numpy()[:n]
 

@@ -32,14 +32,14 @@ def lib():
     return _lib
 
 
-def run(specs, table: _pack.TableArrays, seg_stride=64, preds=()):
+def run(specs, table: _pack.TableArrays, seg_stride=64, preds=(), noise_k=3):
     pb = _pack.pack(specs, table)
-    sz = _pack.sizes(pb, seg_stride)
+    sz = _pack.sizes(pb, seg_stride, noise_k)
     bufs = {f: np.zeros(sz[k], dtype=dt) for f, dt, k in _pack.BUFFER_PLAN}
     B = _abi.ReplayBuffers()
     for f in _abi.REPLAY_BUFFER_FIELDS:
         setattr(B, f, bufs[f].ctypes.data)
-    B.seg_stride, B.cap_max = seg_stride, pb.cap_max
+    B.seg_stride, B.cap_max, B.noise_k = seg_stride, pb.cap_max, noise_k
     solo = np.ascontiguousarray(table.solo, dtype=np.float64)
     thr = np.ascontiguousarray(table.thr, dtype=np.float64).reshape(-1)
     T = _abi.Table(solo.ctypes.data, thr.ctypes.data, len(solo), table.max_bs)

@@ -42,8 +42,21 @@ extern "C" int hc_run(const intf_batch* bt, const intf_table* tab, const intf_re
     }
   }
   for (int s = 0; s < S_n; s++) {
+    if (B->status[s] & INTF_ST_OVERFLOW) {
+      B->n_batches[s] = 0;
+      continue;
+    }
+    form_scenario(s, bt->scen, bt->models, *B);
+  }
+  for (int s = 0; s < S_n; s++) {  // mirrors k_noise_table
+    const intf_scenario& S = bt->scen[s];
+    for (int b = 0; b < B->n_batches[s]; b++)
+      for (int k = 0; k < B->noise_k; k++)
+        B->noise_tab[(long long)(S.req_off + b) * B->noise_k + k] = noise_draw(S.oracle_seed, b, k, S.sigma);
+  }
+  for (int s = 0; s < S_n; s++) {
     if (B->status[s] & INTF_ST_OVERFLOW) continue;
-    replay_scenario(s, bt->scen, bt->models, *tab, *B);
+    replay_formed(s, bt->scen, bt->models, *tab, *B);
   }
   return 0;
 }
