@@ -81,17 +81,17 @@ __device__ __forceinline__ int unrank_multiset(long long r, int E, int cap, cons
 // colo snapshot with all peers ((0+p1)+p2).. (`simcore.py:126-131`), the
 // departure history in (solo, row) order and its EWMA(alpha) prefixes
 // (`colocation.py:54-63`).  Per prediction (fp32, within the 1e-5 budget):
-// y = part_own + w3*c0 + w4*c1 + w5*c2 + b, part_own = fp64 fma chain over the
-// own features precomputed in shared memory.
+// y = fma(w5, c2, fma(w4, c1, fma(w3, c0, bias))), bias = b + fp64 fma chain
+// over the own features, one float4 {w3, w4, w5, bias} per (dec, kind, own)
+// in shared memory.
 template <int KMAX>
-__global__ void __launch_bounds__(kCandThreads, 3) k_candidates(const double* __restrict__ solo,
-                                                             const double* __restrict__ thr, int E, int cap,
-                                                             long long n_sets, long long ld, double alpha,
-                                                             const double* __restrict__ coefs, int n_dec,
-                                                             float* __restrict__ out) {
+__global__ void __launch_bounds__(kCandThreads, 4) k_candidates(const double* __restrict__ solo,
+                                                                const double* __restrict__ thr, int E, int cap,
+                                                                long long n_sets, long long ld, double alpha,
+                                                                const double* __restrict__ coefs, int n_dec,
+                                                                float* __restrict__ out) {
   extern __shared__ unsigned long long binom_smem[];
-  __shared__ float part[kDecChunk][2][kOwnChunk];
-  __shared__ float wc[kDecChunk][2][4];
+  __shared__ float4 cw[kDecChunk][2][kOwnChunk];
   __shared__ double own_solo[kOwnChunk];
   const int nmax = E + KMAX + 1;
   for (int t = threadIdx.x; t < (KMAX + 1) * nmax; t += blockDim.x) {
@@ -105,14 +105,8 @@ __global__ void __launch_bounds__(kCandThreads, 3) k_candidates(const double* __
     if (oi < no && d < nd) {
       const double* w = coefs + ((d0 + d) * 2 + kind) * 7;
       const double* x = thr + 3 * (o0 + oi);
-      part[d][kind][oi] = (float)fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0)));
-    }
-  }
-  for (int t = threadIdx.x; t < kDecChunk * 2; t += blockDim.x) {
-    if ((t >> 1) < nd) {
-      const double* w = coefs + ((d0 + (t >> 1)) * 2 + (t & 1)) * 7;
-#pragma unroll
-      for (int j = 0; j < 4; j++) wc[t >> 1][t & 1][j] = (float)w[3 + j];
+      const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
+      cw[d][kind][oi] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
     }
   }
   if (threadIdx.x < no) own_solo[threadIdx.x] = solo[o0 + threadIdx.x];
@@ -123,23 +117,23 @@ __global__ void __launch_bounds__(kCandThreads, 3) k_candidates(const double* __
 
   constexpr int KP = KMAX > 0 ? KMAX : 1;
   float c0[kGroup][3], ew[kGroup][KMAX + 1][3];
-  double sp[kGroup][KP];  // peer solo times (for "finishes before own")
-  int kk[kGroup];
+  unsigned jpack[kGroup];  // 3-bit departure counts, one per own in the chunk
+  bool live[kGroup];
   const double om = 1.0 - alpha;
 #pragma unroll
   for (int g = 0; g < kGroup; g++) {
     const long long r = r0 + g;
     int p[KP];
-    const int k = r < n_sets ? unrank_multiset<KMAX>(r, E, cap, C, p) : 0;
-    kk[g] = r < n_sets ? k : -1;
-    double th[KP][3];
+    live[g] = r < n_sets;
+    const int k = live[g] ? unrank_multiset<KMAX>(r, E, cap, C, p) : 0;
+    double th[KP][3], sp[KP];
 #pragma unroll
     for (int q = 0; q < KMAX; q++) {
       const int row = q < k ? p[q] : 0;
       th[q][0] = thr[3 * row];
       th[q][1] = thr[3 * row + 1];
       th[q][2] = thr[3 * row + 2];
-      sp[g][q] = q < k ? solo[row] : INFINITY;
+      sp[q] = q < k ? solo[row] : INFINITY;
     }
     // departure rank of each peer: order (solo, row); p is row-sorted
     int rk[KP];
@@ -148,7 +142,7 @@ __global__ void __launch_bounds__(kCandThreads, 3) k_candidates(const double* __
       int rq = 0;
 #pragma unroll
       for (int j = 0; j < KMAX; j++)
-        if (j != q && j < k && (sp[g][j] < sp[g][q] || (sp[g][j] == sp[g][q] && j < q))) rq++;
+        if (j != q && j < k && (sp[j] < sp[q] || (sp[j] == sp[q] && j < q))) rq++;
       rk[q] = rq;
     }
     // snapshot i = fresh sum, in row order, of the peers not yet departed
@@ -171,39 +165,48 @@ __global__ void __launch_bounds__(kCandThreads, 3) k_candidates(const double* __
         if (i == 0) c0[g][a] = (float)c[a];
       }
     }
+    // peers that finish before each own row of the chunk (fp64 compare)
+    unsigned jp = 0u;
+#pragma unroll
+    for (int oi = 0; oi < kOwnChunk; oi++) {
+      const double so = own_solo[oi < no ? oi : 0];
+      unsigned j = 0;
+#pragma unroll
+      for (int q = 0; q < KMAX; q++) j += (sp[q] < so) ? 1u : 0u;
+      jp |= j << (3 * oi);
+    }
+    jpack[g] = jp;
   }
+  const long long dstride = 2ll * E * ld;  // next decision, same kind/own
   for (int oi = 0; oi < no; oi++) {
-    const double so = own_solo[oi];
     float fe[kGroup][3];
 #pragma unroll
     for (int g = 0; g < kGroup; g++) {
-      int j = 0;
-#pragma unroll
-      for (int q = 0; q < KMAX; q++) j += (q < kk[g] && sp[g][q] < so) ? 1 : 0;  // peers that finish first
+      const unsigned j = (jpack[g] >> (3 * oi)) & 7u;
 #pragma unroll
       for (int a = 0; a < 3; a++) {
         float v = ew[g][0][a];
 #pragma unroll
-        for (int i = 1; i <= KMAX; i++) v = (i == j) ? ew[g][i][a] : v;
+        for (int i = 1; i <= KMAX; i++) v = (i == (int)j) ? ew[g][i][a] : v;
         fe[g][a] = v;
       }
     }
-    float* base = out + (long long)(o0 + oi) * ld + r0;
-#pragma unroll 2
-    for (int d = 0; d < nd; d++) {
-      const float* a = wc[d][0];
-      const float* b = wc[d][1];
-      const float pc = part[d][0][oi], pf = part[d][1][oi];
-      float yc[kGroup], yf[kGroup];
+    float* rowc = out + ((long long)d0 * 2 * E + o0 + oi) * ld + r0;
 #pragma unroll
-      for (int g = 0; g < kGroup; g++) {
-        const bool live = kk[g] >= 0;
-        yc[g] = live ? fmaf(a[2], c0[g][2], fmaf(a[1], c0[g][1], fmaf(a[0], c0[g][0], pc))) + a[3] : 0.0f;
-        yf[g] = live ? fmaf(b[2], fe[g][2], fmaf(b[1], fe[g][1], fmaf(b[0], fe[g][0], pf))) + b[3] : 0.0f;
+    for (int d = 0; d < kDecChunk; d++) {
+      if (d < nd) {
+        const float4 a = cw[d][0][oi];
+        const float4 b = cw[d][1][oi];
+        float yc[kGroup], yf[kGroup];
+#pragma unroll
+        for (int g = 0; g < kGroup; g++) {
+          yc[g] = live[g] ? fmaf(a.z, c0[g][2], fmaf(a.y, c0[g][1], fmaf(a.x, c0[g][0], a.w))) : 0.0f;
+          yf[g] = live[g] ? fmaf(b.z, fe[g][2], fmaf(b.y, fe[g][1], fmaf(b.x, fe[g][0], b.w))) : 0.0f;
+        }
+        __stcs(reinterpret_cast<float4*>(rowc), make_float4(yc[0], yc[1], yc[2], yc[3]));
+        __stcs(reinterpret_cast<float4*>(rowc + (long long)E * ld), make_float4(yf[0], yf[1], yf[2], yf[3]));
+        rowc += dstride;
       }
-      float* row = base + (long long)((d0 + d) * 2) * E * ld;
-      __stcs(reinterpret_cast<float4*>(row), make_float4(yc[0], yc[1], yc[2], yc[3]));
-      __stcs(reinterpret_cast<float4*>(row + (long long)E * ld), make_float4(yf[0], yf[1], yf[2], yf[3]));
     }
   }
 }

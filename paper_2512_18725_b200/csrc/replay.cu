@@ -10,22 +10,29 @@
 
 #include "capi_common.h"
 #include "replay_core.cuh"
+#include "replay_warp.cuh"
 
 using namespace intf;
 
 namespace {
 
-// ---- K0a: one thread per deployed model generates its Poisson stream.
-__global__ void k_gen_arrivals(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                               int n_models_total, intf_replay_buffers B) {
-  int g = blockIdx.x * blockDim.x + threadIdx.x;
+// ---- K0a: one warp per deployed model generates its Poisson stream
+// (warp-cooperative PCG64 jump-ahead, sequential cumulative sum).
+constexpr int kGenWarps = 4;
+__global__ void __launch_bounds__(32 * kGenWarps) k_gen_arrivals(const intf_scenario* __restrict__ scen,
+                                                                 const intf_model* __restrict__ models,
+                                                                 int n_models_total, intf_replay_buffers B) {
+  __shared__ double gaps[kGenWarps][32];
+  const int g = blockIdx.x * kGenWarps + (threadIdx.x >> 5);
   if (g >= n_models_total) return;
-  const intf_model M = models[g];
-  const intf_scenario S = scen[M.scen];
-  int n = gen_model_arrivals(S, M, B.list_t + M.list_off, M.list_cap);
-  if (n > M.list_cap) atomicOr(&B.status[M.scen], INTF_ST_OVERFLOW);
-  B.n_list[g] = n;
-  atomicAdd(&B.n_req[M.scen], n);
+  const intf_model& M = models[g];
+  const intf_scenario& S = scen[M.scen];
+  const int n = gen_model_arrivals_warp(S, M, B.list_t + M.list_off, M.list_cap, gaps[threadIdx.x >> 5]);
+  if ((threadIdx.x & 31) == 0) {
+    if (n > M.list_cap) atomicOr(&B.status[M.scen], INTF_ST_OVERFLOW);
+    B.n_list[g] = n;
+    atomicAdd(&B.n_req[M.scen], n);
+  }
 }
 
 // ---- K0b: merge per-model lists by (t, model_id) via rank = own index +
@@ -82,16 +89,14 @@ __global__ void k_split_arrivals(const intf_scenario* __restrict__ scen, int n_s
   B.status[s] |= st;
 }
 
-// ---- K1: batch formation, one thread per scenario (no GPU state, no RNG).
-__global__ void __launch_bounds__(32) k_form(const intf_scenario* __restrict__ scen, int n_scen,
-                                             const intf_model* __restrict__ models, intf_replay_buffers B) {
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
+// ---- K1: batch formation, one warp per scenario (no GPU state, no RNG).
+constexpr int kFormWarps = 4;
+__global__ void __launch_bounds__(32 * kFormWarps) k_form(const intf_scenario* __restrict__ scen, int n_scen,
+                                                          const intf_model* __restrict__ models,
+                                                          intf_replay_buffers B) {
+  const int s = blockIdx.x * kFormWarps + (threadIdx.x >> 5);
   if (s >= n_scen) return;
-  if (B.status[s] & INTF_ST_OVERFLOW) {  // arrivals did not fit
-    B.n_batches[s] = 0;
-    return;
-  }
-  form_scenario(s, scen, models, B);
+  form_warp(s, scen, models, B);
 }
 
 // ---- K1b: noise draws of the first noise_k segments of every formed batch
@@ -108,14 +113,14 @@ __global__ void k_noise_table(const intf_scenario* __restrict__ scen, intf_repla
   B.noise_tab[(long long)(S.req_off + b) * K + k] = noise_draw(S.oracle_seed, (uint64_t)b, (uint64_t)k, S.sigma);
 }
 
-// ---- K2: the replay recurrence, one thread per scenario.
-__global__ void __launch_bounds__(32) k_replay(const intf_scenario* __restrict__ scen, int n_scen,
-                                               const intf_model* __restrict__ models, intf_table tab,
-                                               intf_replay_buffers B) {
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
+// ---- K2: the replay recurrence, one warp per scenario (replay_warp.cuh).
+constexpr int kReplayWarps = 4;
+__global__ void __launch_bounds__(32 * kReplayWarps) k_replay_warp(const intf_scenario* __restrict__ scen, int n_scen,
+                                                                 const intf_model* __restrict__ models,
+                                                                 intf_table tab, intf_replay_buffers B) {
+  const int s = blockIdx.x * kReplayWarps + (threadIdx.x >> 5);
   if (s >= n_scen) return;
-  if (B.status[s] & INTF_ST_OVERFLOW) return;  // arrivals did not fit
-  replay_formed(s, scen, models, tab, B);
+  replay_warp(s, scen, models, tab, B);
 }
 
 // ---- K3: SLO records + per-model nearest-rank percentiles, one block per
@@ -284,7 +289,8 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
   cudaMemsetAsync(buf->status, 0, sizeof(int32_t) * bt->n_scen, st);
   if (bt->n_models <= 0) return INTF_OK;
   int rc;
-  k_gen_arrivals<<<ceil_div(bt->n_models, 64), 64, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+  k_gen_arrivals<<<ceil_div(bt->n_models, kGenWarps), 32 * kGenWarps, 0, st>>>(bt->scen, bt->models, bt->n_models,
+                                                                               *buf);
   if ((rc = launch_status("k_gen_arrivals"))) return rc;
   k_merge_arrivals<<<bt->n_models, 256, 0, st>>>(bt->scen, bt->models, *buf);
   return launch_status("k_merge_arrivals");
@@ -306,15 +312,16 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
     return bad_input("intf_replay: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
   cudaStream_t st = as_stream(stream);
   int rc;
-  k_form<<<ceil_div(bt->n_scen, 32), 32, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
+  k_form<<<ceil_div(bt->n_scen, kFormWarps), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
   if ((rc = launch_status("k_form"))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
     dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
     k_noise_table<<<grid, 128, 0, st>>>(bt->scen, *buf);
     if ((rc = launch_status("k_noise_table"))) return rc;
   }
-  k_replay<<<ceil_div(bt->n_scen, 32), 32, 0, st>>>(bt->scen, bt->n_scen, bt->models, *table, *buf);
-  return launch_status("k_replay");
+  k_replay_warp<<<ceil_div(bt->n_scen, kReplayWarps), 32 * kReplayWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models,
+                                                                                  *table, *buf);
+  return launch_status("k_replay_warp");
 }
 
 int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const double* warm_cutoff, int32_t* out_n,

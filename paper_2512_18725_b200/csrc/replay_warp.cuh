@@ -1,0 +1,472 @@
+// replay_warp.cuh -- warp-per-scenario form of the replay recurrence
+// (sm_100a).  Same events, same arithmetic, same outputs as replay_formed()
+// in replay_core.cuh (which remains the readable/host-checkable statement);
+// this version maps one scenario to one warp:
+//   * lane l < cap owns running slot l -- its batch state lives in that
+//     lane's registers (no local-memory slot arrays);
+//   * the running-list (dispatch) order is a warp-uniform list of 4-bit lane
+//     ids, so every lane computes its colo sum ((0 + p1) + p2).. in list
+//     order from shuffles, and all reseats of one event run in parallel
+//     (they are independent: colo reads only `own`, noise is keyed by
+//     (batch, segment index));
+//   * the next completion is a (done_at, batch_id) lexicographic min over
+//     lanes (shuffle butterfly), compared with the next formation exactly as
+//     the reference heap would (completion first at equal time);
+//   * formation times, and the model/size/first noise draws of the batches
+//     about to be dispatched, stream through two 32-batch register windows
+//     refilled by coalesced loads, keeping global latency off the chain.
+#pragma once
+#include "replay_core.cuh"
+
+namespace intf {
+
+constexpr int kWarpNoiseK = 4;  // noise draws prefetched per dispatched batch
+
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ int shfl_i(int v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+__device__ __noinline__ void replay_warp(int s, const intf_scenario* __restrict__ scens,
+                                         const intf_model* __restrict__ models, const intf_table tab,
+                                         const intf_replay_buffers B) {
+  const int lane = threadIdx.x & 31;
+  const intf_scenario& S = scens[s];
+  int status = B.status[s];
+  if (status & (INTF_ST_CAP | INTF_ST_OVERFLOW)) return;
+  const int cap = S.cap, nb = B.n_batches[s], ro = S.req_off;
+  const intf_model* md = models + S.model_off;
+  const int K = B.noise_k < kWarpNoiseK ? B.noise_k : kWarpNoiseK;
+  double* myseg = B.slot_seg + ((size_t)s * B.cap_max + lane) * (size_t)B.seg_stride * 5;
+
+  // ---- per-lane slot state (valid while `act`)
+  bool act = false;
+  double start = 0.0, total = 0.0, progress = 0.0, done = 0.0, own0 = 0.0, own1 = 0.0, own2 = 0.0;
+  double cur_tb = 0.0, cur_sd = 1.0, nz0 = 1.0, nz1 = 1.0, nz2 = 1.0, nz3 = 1.0;
+  int batch = 0, nseg = 0, n_non1 = 0;
+
+  // ---- warp-uniform state
+  unsigned long long runlist = 0ull;  // 4-bit lane ids in dispatch order
+  int nrun = 0;
+  unsigned freemask = (cap >= 32) ? 0xffffffffu : ((1u << cap) - 1u);
+  double now = 0.0;
+  int n_formed = 0, dq = 0, n_done = 0, seg_cursor = 0, n_reseats = 0;
+
+  // formation-time window: lane l holds b_formed of batch fbase + l
+  int fbase = 0;
+  double wf = lane < nb ? B.b_formed[ro + lane] : 0.0;
+  // dispatch window: lane l holds model/size/noise of batch dbase + l
+  int dbase = 0, wm = 0, wsz = 0;
+  double wn0 = 1.0, wn1 = 1.0, wn2 = 1.0, wn3 = 1.0;
+  auto load_dispatch_window = [&](int base) {
+    const int b = base + lane;
+    if (b < nb) {
+      wm = B.b_model[ro + b];
+      wsz = B.b_size[ro + b];
+      const double* nt = B.noise_tab + (size_t)(ro + b) * B.noise_k;
+      wn0 = K > 0 ? nt[0] : 1.0;
+      wn1 = K > 1 ? nt[1] : 1.0;
+      wn2 = K > 2 ? nt[2] : 1.0;
+      wn3 = K > 3 ? nt[3] : 1.0;
+    }
+  };
+  load_dispatch_window(0);
+
+  // reseat of this lane's batch at `now` (`simcore.py:133-141`); every active
+  // lane calls it together (uniform shuffles inside)
+  auto reseat_lane = [&](bool doit) {
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    for (int k = 0; k < nrun; k++) {  // warp-uniform loop, running-list order
+      const int j = (int)((runlist >> (4 * k)) & 15ull);
+      const double a0 = shfl_d(own0, j), a1 = shfl_d(own1, j), a2 = shfl_d(own2, j);
+      if (j != lane) {
+        c0 = c0 + a0;
+        c1 = c1 + a1;
+        c2 = c2 + a2;
+      }
+    }
+    if (!doit) return;
+    double noise;
+    if (nseg < K) noise = nseg == 0 ? nz0 : nseg == 1 ? nz1 : nseg == 2 ? nz2 : nz3;
+    else noise = noise_draw(S.oracle_seed, (uint64_t)batch, (uint64_t)nseg, S.sigma);
+    const double o[3] = {own0, own1, own2}, colo[3] = {c0, c1, c2};
+    const double sd = slowdown(o, colo, S.beta, noise);
+    if (nseg < B.seg_stride) {
+      double* p = myseg + (size_t)nseg * 5;
+      p[0] = now;
+      p[1] = sd;
+      p[2] = c0;
+      p[3] = c1;
+      p[4] = c2;
+    } else {
+      status |= INTF_ST_SEG_STRIDE;
+    }
+    nseg++;
+    cur_tb = now;
+    cur_sd = sd;
+    if (sd != 1.0) n_non1++;
+    done = now + (total - progress) * sd;
+    if (done < now - 1e-9) status |= INTF_ST_PAST_EVENT;
+  };
+  // RunningBatch.close_segment (`simcore.py:56-66`)
+  auto close_lane = [&]() {
+    if (now == cur_tb) {
+      nseg--;
+      if (cur_sd != 1.0) n_non1--;
+    } else {
+      progress = progress + (now - cur_tb) / cur_sd;
+    }
+  };
+
+  for (;;) {
+    // next completion: lexicographic min of (done, batch) over active lanes
+    double dmin = act ? done : INFINITY;
+    int bmin = act ? batch : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double d2 = __shfl_xor_sync(0xffffffffu, dmin, o);
+      const int b2 = __shfl_xor_sync(0xffffffffu, bmin, o);
+      if (d2 < dmin || (d2 == dmin && b2 < bmin)) {
+        dmin = d2;
+        bmin = b2;
+      }
+    }
+    const bool have_form = n_formed < nb;
+    if (have_form && n_formed - fbase >= 32) {
+      fbase += 32;
+      wf = fbase + lane < nb ? B.b_formed[ro + fbase + lane] : 0.0;
+    }
+    const double tf = shfl_d(wf, (n_formed - fbase) & 31);
+    if (nrun == 0 && !have_form) break;
+    if (nrun > 0 && (!have_form || dmin <= tf)) {
+      // ---- COMPLETION (`simcore.py:173-198`)
+      if (dmin < now - 1e-9) status |= INTF_ST_PAST_EVENT;
+      now = now > dmin ? now : dmin;
+      const unsigned cmask = __ballot_sync(0xffffffffu, act && batch == bmin);
+      const int cl = __ffs(cmask) - 1;
+      int nseg_c = 0, off = 0;
+      if (lane == cl) {
+        close_lane();
+        if (fabs(progress - total) > 1e-6 * total) status |= INTF_ST_PROGRESS;
+        const double measured = n_non1 == 0 ? total : now - start;  // `:181-185`
+        B.b_start[ro + batch] = start;
+        B.b_completion[ro + batch] = now;
+        B.b_measured[ro + batch] = measured;
+        nseg_c = nseg < B.seg_stride ? nseg : B.seg_stride;
+        if (seg_cursor + nseg_c > S.seg_cap) {
+          status |= INTF_ST_OVERFLOW;
+          nseg_c = 0;
+        }
+        off = S.seg_off + seg_cursor;
+        B.b_seg_off[ro + batch] = off;
+        B.b_nseg[ro + batch] = nseg_c;
+        act = false;
+      }
+      __syncwarp();  // lane cl's outcome/segment writes visible to the warp
+      nseg_c = shfl_i(nseg_c, cl);
+      off = shfl_i(off, cl);
+      // lanes copy the completed batch's segments (segment k <- lane k)
+      const double* cseg = B.slot_seg + ((size_t)s * B.cap_max + cl) * (size_t)B.seg_stride * 5;
+      for (int k = lane; k < nseg_c; k += 32) {
+        const double* p = cseg + (size_t)k * 5;
+        B.s_tbegin[off + k] = p[0];
+        B.s_tend[off + k] = (k + 1 < nseg_c) ? p[5] : now;
+        B.s_slowdown[off + k] = p[1];
+        B.s_colo[3 * (size_t)(off + k) + 0] = p[2];
+        B.s_colo[3 * (size_t)(off + k) + 1] = p[3];
+        B.s_colo[3 * (size_t)(off + k) + 2] = p[4];
+      }
+      seg_cursor += nseg_c;
+      // outcome order (completion, batch_id) (`simcore.py:305`): only runs of
+      // equal completion time can need an insertion
+      if (lane == 0) {
+        int pos = n_done;
+        while (pos > 0) {
+          const int prev = B.out_order[ro + pos - 1];
+          if (B.b_completion[ro + prev] == now && prev > bmin) {
+            B.out_order[ro + pos] = prev;
+            pos--;
+          } else {
+            break;
+          }
+        }
+        B.out_order[ro + pos] = bmin;
+      }
+      __syncwarp();
+      n_done++;
+      // remove cl from the running list, keep order
+      unsigned long long nl = 0ull;
+      int w = 0;
+      for (int k = 0; k < nrun; k++) {
+        const unsigned long long j = (runlist >> (4 * k)) & 15ull;
+        if ((int)j != cl) nl |= j << (4 * w++);
+      }
+      runlist = nl;
+      nrun = w;
+      freemask |= 1u << cl;
+      // _colo_changed(survivors) (`simcore.py:143-146`)
+      if (act) close_lane();
+      reseat_lane(act);
+      n_reseats += nrun;
+    } else {
+      // ---- FORMATION: batch n_formed joins the FIFO dispatch queue
+      now = now > tf ? now : tf;
+      n_formed++;
+    }
+    // ---- try_dispatch (`simcore.py:258-262`) -> dispatch (`:153-171`)
+    while (dq < n_formed && nrun < cap) {
+      const int b = dq++;
+      if (b - dbase >= 32) {
+        dbase += 32;
+        load_dispatch_window(dbase);
+      }
+      const int src = (b - dbase) & 31;
+      const int m = shfl_i(wm, src), sz = shfl_i(wsz, src);
+      const double n0 = shfl_d(wn0, src), n1 = shfl_d(wn1, src), n2 = shfl_d(wn2, src), n3 = shfl_d(wn3, src);
+      const int L = __ffs(freemask) - 1;
+      freemask &= ~(1u << L);
+      runlist |= (unsigned long long)L << (4 * nrun);
+      nrun++;
+      const bool was_act = act;
+      if (lane == L) {
+        const int entry = md[m].entry_base + sz - 1;
+        act = true;
+        batch = b;
+        start = now;
+        total = tab.solo_ms[entry];
+        progress = 0.0;
+        nseg = 0;
+        n_non1 = 0;
+        own0 = tab.thr[3 * entry];
+        own1 = tab.thr[3 * entry + 1];
+        own2 = tab.thr[3 * entry + 2];
+        nz0 = n0;
+        nz1 = n1;
+        nz2 = n2;
+        nz3 = n3;
+      }
+      // new batch first, then survivors: independent, so in parallel
+      if (was_act) close_lane();
+      reseat_lane(act);
+      n_reseats += nrun;
+    }
+  }
+  if (nrun || dq < n_formed) status |= INTF_ST_NONQUIESCENT;
+  status = __reduce_or_sync(0xffffffffu, (unsigned)status);
+  if (lane == 0) {
+    B.n_segments[s] = seg_cursor;
+    B.n_reseats[s] = n_reseats;
+    B.status[s] = status;
+  }
+}
+
+}  // namespace intf
+
+namespace intf {
+
+// ---------------------------------------------------------------------------
+// Warp-per-scenario batch formation (same result as form_scenario()): lane m
+// holds model m's pending formation event (time, kind, key, count); the next
+// batch is the lexicographic (time, kind, key) min over lanes (heap order,
+// `simcore.py:98-100,122`); its next event is recomputed cooperatively -- the
+// window membership test t < D is monotone along the sorted list, so the
+// member count is a ballot popcount.
+__device__ __forceinline__ void warp_next_formation(const double* lt, const int32_t* lrid, int n, int h,
+                                                    double window, int max_bs, uint32_t crc, double& t,
+                                                    int& kind, uint32_t& key, int& cnt) {
+  const int lane = threadIdx.x & 31;
+  if (h >= n) {
+    kind = 0;
+    t = 0.0;
+    key = 0;
+    cnt = 0;
+    return;
+  }
+  const double D = lt[h] + window;  // every lane loads the same word (broadcast)
+  int c = 1;
+  for (int j0 = 1; j0 < max_bs; j0 += 32) {
+    const int j = j0 + lane;
+    const bool in = j < max_bs && h + j < n && lt[h + j] < D;
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+    const int add = __popc(m);
+    c += add;
+    if (add < 32) break;
+  }
+  cnt = c;
+  if (c == max_bs) {
+    t = lt[h + c - 1];
+    kind = KIND_ARRIVAL;
+    key = (uint32_t)lrid[h + c - 1];
+  } else {
+    t = D;
+    kind = KIND_WINDOW;
+    key = crc;
+  }
+}
+
+__device__ __noinline__ void form_warp(int s, const intf_scenario* __restrict__ scens,
+                                       const intf_model* __restrict__ models, const intf_replay_buffers B) {
+  const int lane = threadIdx.x & 31;
+  const intf_scenario& S = scens[s];
+  const int M = S.n_models;
+  if ((B.status[s] & INTF_ST_OVERFLOW) || M > 32 || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 ||
+      S.max_bs < 1) {
+    if (lane == 0) {
+      if (!(B.status[s] & INTF_ST_OVERFLOW)) B.status[s] = INTF_ST_CAP;
+      B.n_batches[s] = 0;
+    }
+    return;
+  }
+  const intf_model* md = models + S.model_off;
+  // lane m: model m's list and pending event
+  const bool has = lane < M;
+  const int lo = has ? md[lane].list_off : 0;
+  const int ln = has ? B.n_list[S.model_off + lane] : 0;
+  const uint32_t crc = has ? md[lane].crc : 0u;
+  int head = 0;
+  double et = 0.0;
+  int ekind = 0, ecnt = 0;
+  uint32_t ekey = 0;
+  for (int m = 0; m < M; m++) {  // initial events, computed cooperatively
+    double t;
+    int kind, cnt;
+    uint32_t key;
+    const int lom = __shfl_sync(0xffffffffu, lo, m), lnm = __shfl_sync(0xffffffffu, ln, m);
+    const uint32_t crm = __shfl_sync(0xffffffffu, crc, m);
+    warp_next_formation(B.list_t + lom, B.list_rid + lom, lnm, 0, S.window_ms, S.max_bs, crm, t, kind, key, cnt);
+    if (lane == m) {
+      et = t;
+      ekind = kind;
+      ekey = key;
+      ecnt = cnt;
+    }
+  }
+  const int ro = S.req_off;
+  int n_formed = 0;
+  for (;;) {
+    // (time, kind, key) min over lanes with a pending event
+    double bt = ekind ? et : INFINITY;
+    int bk = ekind ? ekind : 3;
+    uint32_t bkey = ekind ? ekey : 0xffffffffu;
+    int bm = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+      const int k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+      const uint32_t y2 = __shfl_xor_sync(0xffffffffu, bkey, o);
+      const int m2 = __shfl_xor_sync(0xffffffffu, bm, o);
+      const bool less = t2 < bt || (t2 == bt && (k2 < bk || (k2 == bk && (y2 < bkey || (y2 == bkey && m2 < bm)))));
+      if (less) {
+        bt = t2;
+        bk = k2;
+        bkey = y2;
+        bm = m2;
+      }
+    }
+    if (bk == 3) break;
+    const int fm = bm;
+    const int cnt = __shfl_sync(0xffffffffu, ecnt, fm);
+    const int h = __shfl_sync(0xffffffffu, head, fm);
+    const int lom = __shfl_sync(0xffffffffu, lo, fm), lnm = __shfl_sync(0xffffffffu, ln, fm);
+    const uint32_t crm = __shfl_sync(0xffffffffu, crc, fm);
+    const int b = n_formed++;
+    if (lane == 0) {
+      B.b_model[ro + b] = fm;
+      B.b_size[ro + b] = cnt;
+      B.b_formed[ro + b] = bt;
+    }
+    for (int j = lane; j < cnt; j += 32) B.r_batch[ro + B.list_rid[lom + h + j]] = b;
+    double t;
+    int kind, c2;
+    uint32_t key;
+    warp_next_formation(B.list_t + lom, B.list_rid + lom, lnm, h + cnt, S.window_ms, S.max_bs, crm, t, kind, key,
+                        c2);
+    if (lane == fm) {
+      head = h + cnt;
+      et = t;
+      ekind = kind;
+      ekey = key;
+      ecnt = c2;
+    }
+  }
+  if (lane == 0) B.n_batches[s] = n_formed;
+}
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative arrival stream of one deployed model (`workload.py:80-94`).
+// Lane l produces draws l, l+32, ... of the model's PCG64 stream using LCG
+// jump-ahead (state_{i+1} = A_{i+1} state_0 + C_{i+1}; stride 32 with
+// (A_32, C_32)), so the RNG and glibc log1p run 32-wide; the cumulative sum
+// t += max(gap, 1e-12) stays strictly sequential (one lane, shared memory),
+// exactly as the reference rounds it.
+__device__ __forceinline__ void lcg_pow(unsigned __int128 mult, unsigned __int128 inc, unsigned long long n,
+                                       unsigned __int128& A, unsigned __int128& C) {
+  // (A, C) such that n steps of x -> mult*x + inc equal x -> A*x + C
+  unsigned __int128 acc_mult = 1, acc_plus = 0, cur_mult = mult, cur_plus = inc;
+  while (n) {
+    if (n & 1ull) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    n >>= 1;
+  }
+  A = acc_mult;
+  C = acc_plus;
+}
+
+__device__ __forceinline__ uint64_t pcg_output(unsigned __int128 st) {
+  const uint64_t hi = (uint64_t)(st >> 64), lo = (uint64_t)st;
+  const uint32_t rot = (uint32_t)(hi >> 58);
+  const uint64_t v = hi ^ lo;
+  return (v >> rot) | (v << ((64u - rot) & 63u));
+}
+
+// returns the count; writes at most list_cap times; gaps: 32 doubles of smem
+__device__ __noinline__ int gen_model_arrivals_warp(const intf_scenario& S, const intf_model& M, double* list_t,
+                                                    int list_cap, volatile double* gaps) {
+  const int lane = threadIdx.x & 31;
+  if (M.rate_rps == 0.0) return 0;
+  uint32_t w[4];
+  int nw = push_words(w, 0, S.seed);
+  nw = push_words(w, nw, M.crc);
+  Pcg64 g = pcg_seed_words(w, nw);
+  const unsigned __int128 mult =
+      ((unsigned __int128)0x2360ed051fc65da4ull << 64) | (unsigned __int128)0x4385df649fccf645ull;
+  unsigned __int128 Al, Cl, A32, C32;
+  lcg_pow(mult, g.inc, (unsigned long long)(lane + 1), Al, Cl);
+  lcg_pow(mult, g.inc, 32ull, A32, C32);
+  unsigned __int128 st = Al * g.state + Cl;  // state after lane+1 steps
+  const double horizon = S.duration_s * 1000.0;
+  const double neg_mean_gap = -(1000.0 / M.rate_rps);
+  double t = 0.0;  // running time (lane 0 keeps the authoritative copy)
+  int n = 0;
+  for (;;) {
+    const double u = (double)(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
+    st = A32 * st + C32;
+    const double gap = neg_mean_gap * glibc_log1p(-u);
+    gaps[lane] = gap > 1e-12 ? gap : 1e-12;
+    __syncwarp();
+    if (lane == 0) {
+      double tt = t;
+#pragma unroll 8
+      for (int k = 0; k < 32; k++) {
+        tt = tt + gaps[k];
+        gaps[k] = tt;
+      }
+      t = tt;
+    }
+    __syncwarp();
+    const double tl = gaps[lane];
+    const unsigned inside = __ballot_sync(0xffffffffu, tl < horizon);
+    // times are increasing: the first t >= horizon ends the stream
+    const int k_in = __popc(inside) == 32 ? 32 : __ffs(~inside) - 1;
+    if (lane < k_in && n + lane < list_cap) list_t[n + lane] = tl;
+    n += k_in;
+    if (k_in < 32) break;
+    t = __shfl_sync(0xffffffffu, t, 0);
+    __syncwarp();
+  }
+  return n;
+}
+
+}  // namespace intf
