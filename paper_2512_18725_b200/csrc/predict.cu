@@ -40,8 +40,8 @@ long long n_multisets(int E, int cap) {
 }
 
 constexpr int kCandThreads = 128;
-constexpr int kOwnChunk = 8;
-constexpr int kDecChunk = 8;
+constexpr int kOwnChunk = 4;
+constexpr int kDecChunk = 32;
 constexpr int kGroup = 4;  // multisets per thread (one float4 per output row)
 
 // binomial table in shared memory: C[i][n] = binom(n, i), i <= kmax, n < nmax
@@ -84,8 +84,15 @@ __device__ __forceinline__ int unrank_multiset(long long r, int E, int cap, cons
 // y = fma(w5, c2, fma(w4, c1, fma(w3, c0, bias))), bias = b + fp64 fma chain
 // over the own features, one float4 {w3, w4, w5, bias} per (dec, kind, own)
 // in shared memory.
+// round to fp32 here (keeps the selects below on 32-bit registers)
+__device__ __forceinline__ float to_f32(double v) {
+  float r;
+  asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(r) : "d"(v));
+  return r;
+}
+
 template <int KMAX>
-__global__ void __launch_bounds__(kCandThreads, 4) k_candidates(const double* __restrict__ solo,
+__global__ void __launch_bounds__(kCandThreads, 2) k_candidates(const double* __restrict__ solo,
                                                                 const double* __restrict__ thr, int E, int cap,
                                                                 long long n_sets, long long ld, double alpha,
                                                                 const double* __restrict__ coefs, int n_dec,
@@ -161,8 +168,8 @@ __global__ void __launch_bounds__(kCandThreads, 4) k_candidates(const double* __
 #pragma unroll
       for (int a = 0; a < 3; a++) {
         e[a] = i == 0 ? c[a] : alpha * c[a] + om * e[a];
-        ew[g][i][a] = (float)e[a];
-        if (i == 0) c0[g][a] = (float)c[a];
+        ew[g][i][a] = to_f32(e[a]);
+        if (i == 0) c0[g][a] = ew[g][0][a];
       }
     }
     // peers that finish before each own row of the chunk (fp64 compare)
@@ -178,6 +185,7 @@ __global__ void __launch_bounds__(kCandThreads, 4) k_candidates(const double* __
     jpack[g] = jp;
   }
   const long long dstride = 2ll * E * ld;  // next decision, same kind/own
+  const bool all_live = live[kGroup - 1];
   for (int oi = 0; oi < no; oi++) {
     float fe[kGroup][3];
 #pragma unroll
@@ -191,22 +199,29 @@ __global__ void __launch_bounds__(kCandThreads, 4) k_candidates(const double* __
         fe[g][a] = v;
       }
     }
+    // dead pad lanes (r >= n_sets) compute from zeroed features; zero them at store
     float* rowc = out + ((long long)d0 * 2 * E + o0 + oi) * ld + r0;
+    const long long kstride = (long long)E * ld;
+#pragma unroll 4
+    for (int d = 0; d < nd; d++) {
+      const float4 a = cw[d][0][oi];
+      const float4 b = cw[d][1][oi];
+      float yc[kGroup], yf[kGroup];
 #pragma unroll
-    for (int d = 0; d < kDecChunk; d++) {
-      if (d < nd) {
-        const float4 a = cw[d][0][oi];
-        const float4 b = cw[d][1][oi];
-        float yc[kGroup], yf[kGroup];
-#pragma unroll
-        for (int g = 0; g < kGroup; g++) {
-          yc[g] = live[g] ? fmaf(a.z, c0[g][2], fmaf(a.y, c0[g][1], fmaf(a.x, c0[g][0], a.w))) : 0.0f;
-          yf[g] = live[g] ? fmaf(b.z, fe[g][2], fmaf(b.y, fe[g][1], fmaf(b.x, fe[g][0], b.w))) : 0.0f;
-        }
-        __stcs(reinterpret_cast<float4*>(rowc), make_float4(yc[0], yc[1], yc[2], yc[3]));
-        __stcs(reinterpret_cast<float4*>(rowc + (long long)E * ld), make_float4(yf[0], yf[1], yf[2], yf[3]));
-        rowc += dstride;
+      for (int g = 0; g < kGroup; g++) {
+        yc[g] = fmaf(a.z, c0[g][2], fmaf(a.y, c0[g][1], fmaf(a.x, c0[g][0], a.w)));
+        yf[g] = fmaf(b.z, fe[g][2], fmaf(b.y, fe[g][1], fmaf(b.x, fe[g][0], b.w)));
       }
+      if (all_live) {
+        __stcs(reinterpret_cast<float4*>(rowc), make_float4(yc[0], yc[1], yc[2], yc[3]));
+        __stcs(reinterpret_cast<float4*>(rowc + kstride), make_float4(yf[0], yf[1], yf[2], yf[3]));
+      } else {
+        __stcs(reinterpret_cast<float4*>(rowc), make_float4(live[0] ? yc[0] : 0.f, live[1] ? yc[1] : 0.f,
+                                                            live[2] ? yc[2] : 0.f, live[3] ? yc[3] : 0.f));
+        __stcs(reinterpret_cast<float4*>(rowc + kstride), make_float4(live[0] ? yf[0] : 0.f, live[1] ? yf[1] : 0.f,
+                                                                      live[2] ? yf[2] : 0.f, live[3] ? yf[3] : 0.f));
+      }
+      rowc += dstride;
     }
   }
 }
