@@ -164,13 +164,18 @@ int intf_features_predict(const intf_batch *batch, const intf_table *table, cons
  * rounded up to 4 (pad entries written as 0).
  * coefs: device [n_dec][2][7] (w0..w5, b).                                  */
 int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t *n_cand, int64_t *n_sets, int64_t *ld);
+/* Floats of device workspace for the two-phase form (per-(multiset, own)
+ * features staged once per call -- 12 MB for the 48-row bundled table).   */
+int intf_candidate_workspace(int32_t n_rows, int32_t cap, int64_t *ws_elems);
+/* ws may be NULL (or too small): a single fused kernel then recomputes the
+ * features in registers; with ws, k_cand_prep + k_cand_stream run.          */
 int intf_predict_candidates(const intf_table *table, int32_t cap, double alpha, const double *coefs, int32_t n_dec,
-                            float *out, void *stream);
+                            float *out, float *ws, int64_t ws_elems, void *stream);
 /* Host-buffer variant (the end-to-end call): copies coefs in and all
- * predictions out (h_out: n_dec*2*n_rows*ld floats; d_scratch: 28*n_dec +
- * that many floats of device memory).                                       */
+ * predictions out.  h_out: n_dec*2*n_rows*ld floats; d_scratch: device
+ * floats = 28*n_dec + that output size (+ the workspace to use two-phase). */
 int intf_predict_candidates_host(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
-                                 int32_t n_dec, float *h_out, float *d_scratch, void *stream);
+                                 int32_t n_dec, float *h_out, float *d_scratch, int64_t scratch_elems, void *stream);
 
 /* OLS normal-equation statistics (`predict.py:53-66`, `rls_init` `:112-131`):
  * for n samples X[n][6] (f64), y[n] accumulate G = Z^T Z (7x7, row-major,

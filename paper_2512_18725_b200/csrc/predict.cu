@@ -226,6 +226,140 @@ __global__ void __launch_bounds__(kCandThreads, 2) k_candidates(const double* __
   }
 }
 
+// ---- two-phase form for tables whose per-(multiset, own) feature table
+// fits comfortably in L2 (the 48-row bundled table: 12 MB).
+// Phase 1 (k_cand_prep): one thread per multiset decodes it once and writes
+//   C0[c][r]          static colo snapshot (fp32)
+//   FE[(o*3 + c)][r]  EWMA features seen by own row o (the prefix selected by
+//                     how many peers finish before o), fp32
+// Phase 2 (k_cand_stream): pure streaming -- per thread 4 multisets x 1 own x
+// all decisions: 3 FFMA per prediction, 16-byte streaming stores.
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ solo, const double* __restrict__ thr,
+                                                   int E, int cap, long long n_sets, long long ld, double alpha,
+                                                   float* __restrict__ C0, float* __restrict__ FE) {
+  extern __shared__ unsigned long long binom_smem[];
+  const int nmax = E + KMAX + 1;
+  for (int t = threadIdx.x; t < (KMAX + 1) * nmax; t += blockDim.x) {
+    const int i = t / nmax, n = t % nmax;
+    binom_smem[t] = (unsigned long long)binom(n, i);
+  }
+  __syncthreads();
+  const BinomTab C{binom_smem, nmax};
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= ld) return;
+  constexpr int KP = KMAX > 0 ? KMAX : 1;
+  const bool live = r < n_sets;
+  int p[KP];
+  const int k = live ? unrank_multiset<KMAX>(r, E, cap, C, p) : 0;
+  double th[KP][3], sp[KP];
+#pragma unroll
+  for (int q = 0; q < KMAX; q++) {
+    const int row = q < k ? p[q] : 0;
+    th[q][0] = thr[3 * row];
+    th[q][1] = thr[3 * row + 1];
+    th[q][2] = thr[3 * row + 2];
+    sp[q] = q < k ? solo[row] : INFINITY;
+  }
+  int rk[KP];
+#pragma unroll
+  for (int q = 0; q < KMAX; q++) {
+    int rq = 0;
+#pragma unroll
+    for (int j = 0; j < KMAX; j++)
+      if (j != q && j < k && (sp[j] < sp[q] || (sp[j] == sp[q] && j < q))) rq++;
+    rk[q] = rq;
+  }
+  float ew[KMAX + 1][3];
+  double e[3];
+  const double om = 1.0 - alpha;
+#pragma unroll
+  for (int i = 0; i <= KMAX; i++) {
+    double c[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < KMAX; q++)
+      if (q < k && rk[q] >= i) {
+        c[0] = c[0] + th[q][0];
+        c[1] = c[1] + th[q][1];
+        c[2] = c[2] + th[q][2];
+      }
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      e[a] = i == 0 ? c[a] : alpha * c[a] + om * e[a];
+      ew[i][a] = live ? to_f32(e[a]) : 0.0f;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; a++) C0[a * ld + r] = ew[0][a];
+  for (int o = 0; o < E; o++) {
+    const double so = solo[o];
+    int j = 0;
+#pragma unroll
+    for (int q = 0; q < KMAX; q++) j += (sp[q] < so) ? 1 : 0;  // peers that finish first
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      float v = ew[0][a];
+#pragma unroll
+      for (int i = 1; i <= KMAX; i++) v = (i == j) ? ew[i][a] : v;
+      FE[((long long)o * 3 + a) * ld + r] = v;
+    }
+  }
+}
+
+constexpr int kStreamThreads = 128;
+constexpr int kStreamDec = 64;  // decisions per launch chunk (smem coefficient slab)
+
+// grid: x = groups of 4 multisets, y = own row, z = decision chunks
+__global__ void __launch_bounds__(kStreamThreads) k_cand_stream(const double* __restrict__ thr, int E, long long ld,
+                                                                long long n_sets, const double* __restrict__ coefs,
+                                                                int n_dec,
+                                                                const float* __restrict__ C0,
+                                                                const float* __restrict__ FE,
+                                                                float* __restrict__ out) {
+  __shared__ float4 cw[kStreamDec][2];
+  const int o = blockIdx.y;
+  const int d0 = blockIdx.z * kStreamDec, nd = min(kStreamDec, n_dec - d0);
+  for (int t = threadIdx.x; t < 2 * nd; t += blockDim.x) {
+    const int d = t >> 1, kind = t & 1;
+    const double* w = coefs + ((d0 + d) * 2 + kind) * 7;
+    const double* x = thr + 3 * o;
+    const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
+    cw[d][kind] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
+  }
+  __syncthreads();
+  const long long r0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (r0 >= ld) return;
+  const float4 cx = __ldg(reinterpret_cast<const float4*>(C0 + r0));
+  const float4 cy = __ldg(reinterpret_cast<const float4*>(C0 + ld + r0));
+  const float4 cz = __ldg(reinterpret_cast<const float4*>(C0 + 2 * ld + r0));
+  const float4 fx = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 0) * ld + r0));
+  const float4 fy = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 1) * ld + r0));
+  const float4 fz = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 2) * ld + r0));
+  float* row = out + ((long long)d0 * 2 * E + o) * ld + r0;
+  const long long kstride = (long long)E * ld, dstride = 2 * kstride;
+#pragma unroll 4
+  for (int d = 0; d < nd; d++) {
+    const float4 a = cw[d][0], b = cw[d][1];
+    float4 yc, yf;
+    yc.x = fmaf(a.z, cz.x, fmaf(a.y, cy.x, fmaf(a.x, cx.x, a.w)));
+    yc.y = fmaf(a.z, cz.y, fmaf(a.y, cy.y, fmaf(a.x, cx.y, a.w)));
+    yc.z = fmaf(a.z, cz.z, fmaf(a.y, cy.z, fmaf(a.x, cx.z, a.w)));
+    yc.w = fmaf(a.z, cz.w, fmaf(a.y, cy.w, fmaf(a.x, cx.w, a.w)));
+    yf.x = fmaf(b.z, fz.x, fmaf(b.y, fy.x, fmaf(b.x, fx.x, b.w)));
+    yf.y = fmaf(b.z, fz.y, fmaf(b.y, fy.y, fmaf(b.x, fx.y, b.w)));
+    yf.z = fmaf(b.z, fz.z, fmaf(b.y, fy.z, fmaf(b.x, fx.z, b.w)));
+    yf.w = fmaf(b.z, fz.w, fmaf(b.y, fy.w, fmaf(b.x, fx.w, b.w)));
+    if (r0 + 4 > n_sets) {  // pad lanes of the last group are written as 0
+      const long long nl = n_sets - r0;
+      yc = make_float4(nl > 0 ? yc.x : 0.f, nl > 1 ? yc.y : 0.f, nl > 2 ? yc.z : 0.f, 0.f);
+      yf = make_float4(nl > 0 ? yf.x : 0.f, nl > 1 ? yf.y : 0.f, nl > 2 ? yf.z : 0.f, 0.f);
+    }
+    __stcs(reinterpret_cast<float4*>(row), yc);
+    __stcs(reinterpret_cast<float4*>(row + kstride), yf);
+    row += dstride;
+  }
+}
+
 // ===================================================================== K6
 constexpr int kOlsThreads = 256;
 constexpr int kOlsBlocks = 592;  // 4 x 148 SMs
@@ -621,13 +755,26 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const double* __restrict_
 
 }  // namespace
 
+long long cand_ws_elems(int E, long long ld) { return 3 * ld + 3LL * E * ld; }
+
 template <int K>
 static int launch_candidates(const intf_table* t, int cap, double alpha, const double* coefs, int n_dec, float* out,
-                             cudaStream_t st) {
+                             float* ws, long long ws_elems, cudaStream_t st) {
   const int E = t->n_rows;
   const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
   const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
   if (smem > 200 * 1024) return bad_input("intf_predict_candidates: profile table too large for the binomial table");
+  if (ws && ws_elems >= cand_ws_elems(E, ld)) {  // two-phase: prep (features) + stream (forward)
+    float* C0 = ws;
+    float* FE = ws + 3 * ld;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_prep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cand_prep<K><<<ceil_div(ld, 128), 128, smem, st>>>(t->solo_ms, t->thr, E, cap, sets, ld, alpha, C0, FE);
+    int rc = launch_status("k_cand_prep");
+    if (rc) return rc;
+    dim3 grid(ceil_div(ld / 4, kStreamThreads), E, ceil_div(n_dec, kStreamDec));
+    k_cand_stream<<<grid, kStreamThreads, 0, st>>>(t->thr, E, ld, sets, coefs, n_dec, C0, FE, out);
+    return launch_status("k_cand_stream");
+  }
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_candidates<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(ceil_div(ld / kGroup, kCandThreads), ceil_div(E, kOwnChunk), ceil_div(n_dec, kDecChunk));
   k_candidates<K><<<grid, kCandThreads, smem, st>>>(t->solo_ms, t->thr, E, cap, sets, ld, alpha, coefs, n_dec, out);
@@ -645,39 +792,54 @@ int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t* n_cand, int64_t* 
   return INTF_OK;
 }
 
+int intf_candidate_workspace(int32_t n_rows, int32_t cap, int64_t* ws_elems) {
+  int64_t n_cand, n_sets, ld;
+  int rc = intf_candidate_count(n_rows, cap, &n_cand, &n_sets, &ld);
+  if (rc) return rc;
+  if (!ws_elems) return bad_input("intf_candidate_workspace: null argument");
+  *ws_elems = cand_ws_elems(n_rows, ld);
+  return INTF_OK;
+}
+
 int intf_predict_candidates(const intf_table* table, int32_t cap, double alpha, const double* coefs, int32_t n_dec,
-                            float* out, void* stream) {
+                            float* out, float* ws, int64_t ws_elems, void* stream) {
   if (!table || !coefs || !out || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1 || table->n_rows < 1)
     return bad_input("intf_predict_candidates: bad argument (n_dec >= 1, 1 <= cap <= 8)");
   cudaStream_t st = as_stream(stream);
   switch (cap - 1) {
-    case 0: return launch_candidates<0>(table, cap, alpha, coefs, n_dec, out, st);
-    case 1: return launch_candidates<1>(table, cap, alpha, coefs, n_dec, out, st);
-    case 2: return launch_candidates<2>(table, cap, alpha, coefs, n_dec, out, st);
-    case 3: return launch_candidates<3>(table, cap, alpha, coefs, n_dec, out, st);
-    case 4: return launch_candidates<4>(table, cap, alpha, coefs, n_dec, out, st);
-    case 5: return launch_candidates<5>(table, cap, alpha, coefs, n_dec, out, st);
-    case 6: return launch_candidates<6>(table, cap, alpha, coefs, n_dec, out, st);
-    default: return launch_candidates<7>(table, cap, alpha, coefs, n_dec, out, st);
+    case 0: return launch_candidates<0>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
+    case 1: return launch_candidates<1>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
+    case 2: return launch_candidates<2>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
+    case 3: return launch_candidates<3>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
+    case 4: return launch_candidates<4>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
+    case 5: return launch_candidates<5>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
+    case 6: return launch_candidates<6>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
+    default: return launch_candidates<7>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
   }
 }
 
 int intf_predict_candidates_host(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
-                                 int32_t n_dec, float* h_out, float* d_scratch, void* stream) {
+                                 int32_t n_dec, float* h_out, float* d_scratch, int64_t scratch_elems,
+                                 void* stream) {
   if (!table || !h_coefs || !h_out || !d_scratch) return bad_input("intf_predict_candidates_host: null argument");
-  int64_t n_cand = 0, n_sets = 0, ld = 0;
+  int64_t n_cand = 0, n_sets = 0, ld = 0, ws = 0;
   int rc = intf_candidate_count(table->n_rows, cap, &n_cand, &n_sets, &ld);
   if (rc) return rc;
+  intf_candidate_workspace(table->n_rows, cap, &ws);
+  const long long n_out = (long long)ld * table->n_rows * 2 * n_dec, n_coef = 2LL * n_dec * 2 * 7;
+  if (scratch_elems < n_coef + n_out) return bad_input("intf_predict_candidates_host: scratch too small");
   cudaStream_t st = as_stream(stream);
-  // coefs staged at the head of the scratch buffer (doubles), outputs after it
+  // scratch: [coefs as doubles][outputs][feature workspace, if it fits]
   double* d_coefs = reinterpret_cast<double*>(d_scratch);
-  float* d_out = d_scratch + 2 * (size_t)n_dec * 2 * 7;
+  float* d_out = d_scratch + n_coef;
+  float* d_ws = d_out + n_out;
+  const long long ws_have = scratch_elems - n_coef - n_out;
   if (cudaMemcpyAsync(d_coefs, h_coefs, sizeof(double) * n_dec * 2 * 7, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return launch_status("copy coefs");
-  rc = intf_predict_candidates(table, cap, alpha, d_coefs, n_dec, d_out, stream);
+  rc = intf_predict_candidates(table, cap, alpha, d_coefs, n_dec, d_out, ws_have >= ws ? d_ws : nullptr, ws_have,
+                               stream);
   if (rc) return rc;
-  if (cudaMemcpyAsync(h_out, d_out, sizeof(float) * (size_t)ld * table->n_rows * 2 * n_dec, cudaMemcpyDeviceToHost,
-                      st) != cudaSuccess)
+  if (cudaMemcpyAsync(h_out, d_out, sizeof(float) * n_out, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return launch_status("copy predictions");
   return INTF_OK;
 }

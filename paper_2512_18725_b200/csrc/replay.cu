@@ -115,7 +115,7 @@ __global__ void k_noise_table(const intf_scenario* __restrict__ scen, intf_repla
 
 // ---- K2: the replay recurrence, one warp per scenario (replay_warp.cuh).
 constexpr int kReplayWarps = 4;
-__global__ void __launch_bounds__(32 * kReplayWarps) k_replay_warp(const intf_scenario* __restrict__ scen, int n_scen,
+__global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_warp(const intf_scenario* __restrict__ scen, int n_scen,
                                                                  const intf_model* __restrict__ models,
                                                                  intf_table tab, intf_replay_buffers B) {
   const int s = blockIdx.x * kReplayWarps + (threadIdx.x >> 5);

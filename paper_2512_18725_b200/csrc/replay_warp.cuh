@@ -22,10 +22,16 @@ namespace intf {
 
 constexpr int kWarpNoiseK = 4;  // noise draws prefetched per dispatched batch
 
+// rare path (segment index beyond the precomputed noise table): kept out of
+// line so the SeedSequence/PCG64 state does not inflate the replay's registers
+__device__ __noinline__ double noise_draw_slow(uint64_t seed, uint64_t batch, uint64_t seg, double sigma) {
+  return noise_draw(seed, batch, seg, sigma);
+}
+
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ int shfl_i(int v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-__device__ __noinline__ void replay_warp(int s, const intf_scenario* __restrict__ scens,
+__device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restrict__ scens,
                                          const intf_model* __restrict__ models, const intf_table tab,
                                          const intf_replay_buffers B) {
   const int lane = threadIdx.x & 31;
@@ -86,7 +92,7 @@ __device__ __noinline__ void replay_warp(int s, const intf_scenario* __restrict_
     if (!doit) return;
     double noise;
     if (nseg < K) noise = nseg == 0 ? nz0 : nseg == 1 ? nz1 : nseg == 2 ? nz2 : nz3;
-    else noise = noise_draw(S.oracle_seed, (uint64_t)batch, (uint64_t)nseg, S.sigma);
+    else noise = noise_draw_slow(S.oracle_seed, (uint64_t)batch, (uint64_t)nseg, S.sigma);
     const double o[3] = {own0, own1, own2}, colo[3] = {c0, c1, c2};
     const double sd = slowdown(o, colo, S.beta, noise);
     if (nseg < B.seg_stride) {
@@ -116,12 +122,15 @@ __device__ __noinline__ void replay_warp(int s, const intf_scenario* __restrict_
     }
   };
 
+  // butterfly span: slots live in lanes [0, cap), so log2(cap) rounds suffice
+  int red_hi = 1;
+  while (red_hi < cap) red_hi <<= 1;
+  red_hi >>= 1;
   for (;;) {
     // next completion: lexicographic min of (done, batch) over active lanes
     double dmin = act ? done : INFINITY;
     int bmin = act ? batch : 0x7fffffff;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = red_hi; o > 0; o >>= 1) {
       const double d2 = __shfl_xor_sync(0xffffffffu, dmin, o);
       const int b2 = __shfl_xor_sync(0xffffffffu, bmin, o);
       if (d2 < dmin || (d2 == dmin && b2 < bmin)) {
@@ -129,6 +138,8 @@ __device__ __noinline__ void replay_warp(int s, const intf_scenario* __restrict_
         bmin = b2;
       }
     }
+    dmin = shfl_d(dmin, 0);
+    bmin = shfl_i(bmin, 0);
     const bool have_form = n_formed < nb;
     if (have_form && n_formed - fbase >= 32) {
       fbase += 32;
@@ -341,14 +352,16 @@ __device__ __noinline__ void form_warp(int s, const intf_scenario* __restrict__ 
   }
   const int ro = S.req_off;
   int n_formed = 0;
+  int red_hi = 1;  // models live in lanes [0, M): log2(M) butterfly rounds
+  while (red_hi < M) red_hi <<= 1;
+  red_hi >>= 1;
   for (;;) {
     // (time, kind, key) min over lanes with a pending event
     double bt = ekind ? et : INFINITY;
     int bk = ekind ? ekind : 3;
     uint32_t bkey = ekind ? ekey : 0xffffffffu;
     int bm = lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = red_hi; o > 0; o >>= 1) {
       const double t2 = __shfl_xor_sync(0xffffffffu, bt, o);
       const int k2 = __shfl_xor_sync(0xffffffffu, bk, o);
       const uint32_t y2 = __shfl_xor_sync(0xffffffffu, bkey, o);
@@ -361,6 +374,9 @@ __device__ __noinline__ void form_warp(int s, const intf_scenario* __restrict__ 
         bm = m2;
       }
     }
+    bt = __shfl_sync(0xffffffffu, bt, 0);
+    bk = __shfl_sync(0xffffffffu, bk, 0);
+    bm = __shfl_sync(0xffffffffu, bm, 0);
     if (bk == 3) break;
     const int fm = bm;
     const int cnt = __shfl_sync(0xffffffffu, ecnt, fm);

@@ -398,13 +398,18 @@ class CandidateScorer:
     decisions.  Output (device, fp32): [n_dec][2][E][ld], first n_sets of
     each row valid (ld = n_sets rounded up to 4)."""
 
-    def __init__(self, table: _pack.TableArrays, cap: int, alpha: float = 0.5, dtable: DeviceTable | None = None):
+    def __init__(self, table: _pack.TableArrays, cap: int, alpha: float = 0.5, dtable: DeviceTable | None = None,
+                 two_phase: bool = True):
         self.dev = require_cuda()
         self.dtable = dtable or DeviceTable(table, self.dev)
         self.E = table.n_rows
         self.cap = int(cap)
         self.alpha = float(alpha)
         self.n_cand, self.n_sets, self.ld = candidate_layout(self.E, self.cap)
+        ws = ctypes.c_int64(0)
+        _abi.check(_abi.load().intf_candidate_workspace(self.E, self.cap, ctypes.byref(ws)), "intf_candidate_workspace")
+        self.ws_elems = int(ws.value) if two_phase else 0
+        self.ws = torch.empty(max(self.ws_elems, 1), dtype=torch.float32, device=self.dev) if two_phase else None
 
     def out_elems(self, n_dec: int) -> int:
         return n_dec * 2 * self.E * self.ld
@@ -420,15 +425,19 @@ class CandidateScorer:
         """coefs: device float64 [n_dec][2][7]; enqueue only (no sync)."""
         n_dec = coefs.numel() // 14
         _abi.check(_abi.load().intf_predict_candidates(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
-                                                       coefs.data_ptr(), n_dec, out.data_ptr(), stream_ptr()),
-                   "intf_predict_candidates")
+                                                       coefs.data_ptr(), n_dec, out.data_ptr(), _abi.addr(self.ws),
+                                                       self.ws_elems, stream_ptr()), "intf_predict_candidates")
+
+    def scratch_elems(self, n_dec: int) -> int:
+        """Device floats needed by score_host (coefs + outputs + workspace)."""
+        return 28 * n_dec + self.out_elems(n_dec) + self.ws_elems
 
     def score_host(self, coefs_host: np.ndarray, out_host: np.ndarray, scratch: torch.Tensor) -> None:
         """End-to-end variant: host coefs in, host predictions out."""
         n_dec = coefs_host.size // 14
         _abi.check(_abi.load().intf_predict_candidates_host(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
                                                             coefs_host.ctypes.data, n_dec, out_host.ctypes.data,
-                                                            scratch.data_ptr(), stream_ptr()),
+                                                            scratch.data_ptr(), scratch.numel(), stream_ptr()),
                    "intf_predict_candidates_host")
 
 

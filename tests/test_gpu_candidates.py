@@ -12,10 +12,10 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-5
 
 
-def _scorer(cap):
+def _scorer(cap, two_phase=True):
     from paper_2512_18725_b200 import engine
 
-    return engine.CandidateScorer(_golden.table("default"), cap=cap, alpha=0.5)
+    return engine.CandidateScorer(_golden.table("default"), cap=cap, alpha=0.5, two_phase=two_phase)
 
 
 def test_candidate_counts():
@@ -24,12 +24,12 @@ def test_candidate_counts():
     assert [engine.candidate_count(48, c) for c in (2, 3, 4)] == [2352, 58800, 999600]
 
 
-@pytest.mark.parametrize("cap", [2, 3])
-def test_candidates_match_reference_composition(cap):
+@pytest.mark.parametrize("cap,two_phase", [(2, True), (3, True), (2, False), (3, False)])
+def test_candidates_match_reference_composition(cap, two_phase):
     from paper_2512_18725_b200 import engine
 
     C = _golden.load("candidates_golden.npz")
-    sc = _scorer(cap)
+    sc = _scorer(cap, two_phase)
     coefs = torch.tensor(C["w"], dtype=torch.float64, device="cuda").reshape(1, 2, 7).contiguous()
     out = sc.alloc(1)
     sc.score(coefs, out)
@@ -40,16 +40,19 @@ def test_candidates_match_reference_composition(cap):
     np.testing.assert_allclose(y[1, own, idx], C[f"cap{cap}/y_fine"], rtol=RTOL)
 
 
-def test_cap4_full_enumeration_sampled_against_oracle():
+@pytest.mark.parametrize("two_phase", [True, False])
+def test_cap4_full_enumeration_sampled_against_oracle(two_phase):
     from paper_2512_18725_b200 import engine
 
     tab = _golden.table("default")
-    sc = _scorer(4)
+    sc = _scorer(4, two_phase)
     rng = np.random.default_rng(1)
     W = rng.normal(0, 0.5, size=(3, 2, 7))
     coefs = torch.tensor(W, dtype=torch.float64, device="cuda").contiguous()
     out = sc.alloc(3)
     sc.score(coefs, out)
+    full = out.cpu().numpy().reshape(3, 2, sc.E, sc.ld)
+    assert np.all(full[..., sc.n_sets:] == 0)  # pad entries
     y = sc.view(out.cpu().numpy(), 3)
     assert np.isfinite(y).all()
     import itertools
@@ -72,7 +75,7 @@ def test_host_buffer_variant_equals_device_variant():
     dev_out = sc.alloc(2)
     sc.score(torch.tensor(W, device="cuda").contiguous(), dev_out)
     host_out = np.empty(sc.out_elems(2), dtype=np.float32)
-    scratch = torch.empty(2 * 2 * 7 * 2 + host_out.size, dtype=torch.float32, device="cuda")
+    scratch = torch.empty(sc.scratch_elems(2), dtype=torch.float32, device="cuda")
     sc.score_host(np.ascontiguousarray(W), host_out, scratch)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(host_out, dev_out.cpu().numpy())
