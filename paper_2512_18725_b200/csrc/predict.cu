@@ -234,6 +234,8 @@ __global__ void __launch_bounds__(kCandThreads, 2) k_candidates(const double* __
 //                     how many peers finish before o), fp32
 // Phase 2 (k_cand_stream): pure streaming -- per thread 4 multisets x 1 own x
 // all decisions: 3 FFMA per prediction, 16-byte streaming stores.
+constexpr int kPrepOwn = 8;  // own rows per prep thread (grid.y splits the table)
+
 template <int KMAX>
 __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ solo, const double* __restrict__ thr,
                                                    int E, int cap, long long n_sets, long long ld, double alpha,
@@ -273,6 +275,7 @@ __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ so
   float ew[KMAX + 1][3];
   double e[3];
   const double om = 1.0 - alpha;
+  const int o_begin = blockIdx.y * kPrepOwn, o_end = min(E, o_begin + kPrepOwn);
 #pragma unroll
   for (int i = 0; i <= KMAX; i++) {
     double c[3] = {0.0, 0.0, 0.0};
@@ -289,9 +292,11 @@ __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ so
       ew[i][a] = live ? to_f32(e[a]) : 0.0f;
     }
   }
+  if (blockIdx.y == 0) {
 #pragma unroll
-  for (int a = 0; a < 3; a++) C0[a * ld + r] = ew[0][a];
-  for (int o = 0; o < E; o++) {
+    for (int a = 0; a < 3; a++) C0[a * ld + r] = ew[0][a];
+  }
+  for (int o = o_begin; o < o_end; o++) {
     const double so = solo[o];
     int j = 0;
 #pragma unroll
@@ -308,55 +313,69 @@ __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ so
 
 constexpr int kStreamThreads = 128;
 constexpr int kStreamDec = 64;  // decisions per launch chunk (smem coefficient slab)
+constexpr int kStreamOwn = 4;   // own rows per thread (next row's features prefetched)
 
-// grid: x = groups of 4 multisets, y = own row, z = decision chunks
+// grid: x = groups of 4 multisets, y = chunks of kStreamOwn own rows, z = decision chunks
 __global__ void __launch_bounds__(kStreamThreads) k_cand_stream(const double* __restrict__ thr, int E, long long ld,
                                                                 long long n_sets, const double* __restrict__ coefs,
-                                                                int n_dec,
-                                                                const float* __restrict__ C0,
+                                                                int n_dec, const float* __restrict__ C0,
                                                                 const float* __restrict__ FE,
                                                                 float* __restrict__ out) {
-  __shared__ float4 cw[kStreamDec][2];
-  const int o = blockIdx.y;
+  __shared__ float4 cw[kStreamOwn][kStreamDec][2];
+  const int oa = blockIdx.y * kStreamOwn, no = min(kStreamOwn, E - oa);
   const int d0 = blockIdx.z * kStreamDec, nd = min(kStreamDec, n_dec - d0);
-  for (int t = threadIdx.x; t < 2 * nd; t += blockDim.x) {
-    const int d = t >> 1, kind = t & 1;
-    const double* w = coefs + ((d0 + d) * 2 + kind) * 7;
-    const double* x = thr + 3 * o;
-    const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
-    cw[d][kind] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
-  }
-  __syncthreads();
-  const long long r0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (r0 >= ld) return;
-  const float4 cx = __ldg(reinterpret_cast<const float4*>(C0 + r0));
-  const float4 cy = __ldg(reinterpret_cast<const float4*>(C0 + ld + r0));
-  const float4 cz = __ldg(reinterpret_cast<const float4*>(C0 + 2 * ld + r0));
-  const float4 fx = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 0) * ld + r0));
-  const float4 fy = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 1) * ld + r0));
-  const float4 fz = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 2) * ld + r0));
-  float* row = out + ((long long)d0 * 2 * E + o) * ld + r0;
-  const long long kstride = (long long)E * ld, dstride = 2 * kstride;
-#pragma unroll 4
-  for (int d = 0; d < nd; d++) {
-    const float4 a = cw[d][0], b = cw[d][1];
-    float4 yc, yf;
-    yc.x = fmaf(a.z, cz.x, fmaf(a.y, cy.x, fmaf(a.x, cx.x, a.w)));
-    yc.y = fmaf(a.z, cz.y, fmaf(a.y, cy.y, fmaf(a.x, cx.y, a.w)));
-    yc.z = fmaf(a.z, cz.z, fmaf(a.y, cy.z, fmaf(a.x, cx.z, a.w)));
-    yc.w = fmaf(a.z, cz.w, fmaf(a.y, cy.w, fmaf(a.x, cx.w, a.w)));
-    yf.x = fmaf(b.z, fz.x, fmaf(b.y, fy.x, fmaf(b.x, fx.x, b.w)));
-    yf.y = fmaf(b.z, fz.y, fmaf(b.y, fy.y, fmaf(b.x, fx.y, b.w)));
-    yf.z = fmaf(b.z, fz.z, fmaf(b.y, fy.z, fmaf(b.x, fx.z, b.w)));
-    yf.w = fmaf(b.z, fz.w, fmaf(b.y, fy.w, fmaf(b.x, fx.w, b.w)));
-    if (r0 + 4 > n_sets) {  // pad lanes of the last group are written as 0
-      const long long nl = n_sets - r0;
-      yc = make_float4(nl > 0 ? yc.x : 0.f, nl > 1 ? yc.y : 0.f, nl > 2 ? yc.z : 0.f, 0.f);
-      yf = make_float4(nl > 0 ? yf.x : 0.f, nl > 1 ? yf.y : 0.f, nl > 2 ? yf.z : 0.f, 0.f);
+  for (int t = threadIdx.x; t < kStreamOwn * 2 * nd; t += blockDim.x) {
+    const int oi = t / (2 * nd), d = (t >> 1) % nd, kind = t & 1;
+    if (oi < no) {
+      const double* w = coefs + ((d0 + d) * 2 + kind) * 7;
+      const double* x = thr + 3 * (oa + oi);
+      const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
+      cw[oi][d][kind] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
     }
-    __stcs(reinterpret_cast<float4*>(row), yc);
-    __stcs(reinterpret_cast<float4*>(row + kstride), yf);
-    row += dstride;
+  }
+  const long long r0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const bool inb = r0 < ld;
+  const long long rr = inb ? r0 : 0;
+  const float4 cx = __ldg(reinterpret_cast<const float4*>(C0 + rr));
+  const float4 cy = __ldg(reinterpret_cast<const float4*>(C0 + ld + rr));
+  const float4 cz = __ldg(reinterpret_cast<const float4*>(C0 + 2 * ld + rr));
+  float4 fx = __ldg(reinterpret_cast<const float4*>(FE + ((long long)oa * 3 + 0) * ld + rr));
+  float4 fy = __ldg(reinterpret_cast<const float4*>(FE + ((long long)oa * 3 + 1) * ld + rr));
+  float4 fz = __ldg(reinterpret_cast<const float4*>(FE + ((long long)oa * 3 + 2) * ld + rr));
+  __syncthreads();
+  if (!inb) return;
+  const long long kstride = (long long)E * ld, dstride = 2 * kstride;
+  const long long nl = n_sets - r0;  // < 4 only in the last group: pad lanes are written as 0
+  for (int oi = 0; oi < no; oi++) {
+    // prefetch the next own row's fine features while this row streams out
+    const int on = oa + (oi + 1 < no ? oi + 1 : oi);
+    const float4 gx = __ldg(reinterpret_cast<const float4*>(FE + ((long long)on * 3 + 0) * ld + r0));
+    const float4 gy = __ldg(reinterpret_cast<const float4*>(FE + ((long long)on * 3 + 1) * ld + r0));
+    const float4 gz = __ldg(reinterpret_cast<const float4*>(FE + ((long long)on * 3 + 2) * ld + r0));
+    float* row = out + ((long long)d0 * 2 * E + oa + oi) * ld + r0;
+#pragma unroll 4
+    for (int d = 0; d < nd; d++) {
+      const float4 a = cw[oi][d][0], b = cw[oi][d][1];
+      float4 yc, yf;
+      yc.x = fmaf(a.z, cz.x, fmaf(a.y, cy.x, fmaf(a.x, cx.x, a.w)));
+      yc.y = fmaf(a.z, cz.y, fmaf(a.y, cy.y, fmaf(a.x, cx.y, a.w)));
+      yc.z = fmaf(a.z, cz.z, fmaf(a.y, cy.z, fmaf(a.x, cx.z, a.w)));
+      yc.w = fmaf(a.z, cz.w, fmaf(a.y, cy.w, fmaf(a.x, cx.w, a.w)));
+      yf.x = fmaf(b.z, fz.x, fmaf(b.y, fy.x, fmaf(b.x, fx.x, b.w)));
+      yf.y = fmaf(b.z, fz.y, fmaf(b.y, fy.y, fmaf(b.x, fx.y, b.w)));
+      yf.z = fmaf(b.z, fz.z, fmaf(b.y, fy.z, fmaf(b.x, fx.z, b.w)));
+      yf.w = fmaf(b.z, fz.w, fmaf(b.y, fy.w, fmaf(b.x, fx.w, b.w)));
+      if (nl < 4) {
+        yc = make_float4(nl > 0 ? yc.x : 0.f, nl > 1 ? yc.y : 0.f, nl > 2 ? yc.z : 0.f, 0.f);
+        yf = make_float4(nl > 0 ? yf.x : 0.f, nl > 1 ? yf.y : 0.f, nl > 2 ? yf.z : 0.f, 0.f);
+      }
+      __stcs(reinterpret_cast<float4*>(row), yc);
+      __stcs(reinterpret_cast<float4*>(row + kstride), yf);
+      row += dstride;
+    }
+    fx = gx;
+    fy = gy;
+    fz = gz;
   }
 }
 
@@ -768,10 +787,11 @@ static int launch_candidates(const intf_table* t, int cap, double alpha, const d
     float* C0 = ws;
     float* FE = ws + 3 * ld;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_prep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cand_prep<K><<<ceil_div(ld, 128), 128, smem, st>>>(t->solo_ms, t->thr, E, cap, sets, ld, alpha, C0, FE);
+    k_cand_prep<K><<<dim3(ceil_div(ld, 128), ceil_div(E, kPrepOwn)), 128, smem, st>>>(t->solo_ms, t->thr, E, cap, sets,
+                                                                                    ld, alpha, C0, FE);
     int rc = launch_status("k_cand_prep");
     if (rc) return rc;
-    dim3 grid(ceil_div(ld / 4, kStreamThreads), E, ceil_div(n_dec, kStreamDec));
+    dim3 grid(ceil_div(ld / 4, kStreamThreads), ceil_div(E, kStreamOwn), ceil_div(n_dec, kStreamDec));
     k_cand_stream<<<grid, kStreamThreads, 0, st>>>(t->thr, E, ld, sets, coefs, n_dec, C0, FE, out);
     return launch_status("k_cand_stream");
   }

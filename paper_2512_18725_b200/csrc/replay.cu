@@ -118,9 +118,10 @@ constexpr int kReplayWarps = 4;
 __global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_warp(const intf_scenario* __restrict__ scen, int n_scen,
                                                                  const intf_model* __restrict__ models,
                                                                  intf_table tab, intf_replay_buffers B) {
+  __shared__ double sseg[kReplayWarps][kMaxCap * kSmemSeg * 5];
   const int s = blockIdx.x * kReplayWarps + (threadIdx.x >> 5);
   if (s >= n_scen) return;
-  replay_warp(s, scen, models, tab, B);
+  replay_warp(s, scen, models, tab, B, sseg[threadIdx.x >> 5]);
 }
 
 // ---- K3: SLO records + per-model nearest-rank percentiles, one block per

@@ -21,6 +21,7 @@
 namespace intf {
 
 constexpr int kWarpNoiseK = 4;  // noise draws prefetched per dispatched batch
+constexpr int kSmemSeg = 8;     // open-segment history kept in shared memory per slot (rest in global scratch)
 
 // rare path (segment index beyond the precomputed noise table): kept out of
 // line so the SeedSequence/PCG64 state does not inflate the replay's registers
@@ -31,9 +32,10 @@ __device__ __noinline__ double noise_draw_slow(uint64_t seed, uint64_t batch, ui
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ int shfl_i(int v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
+// sseg: this warp's shared-memory segment history, [kMaxCap][kSmemSeg][5]
 __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restrict__ scens,
                                          const intf_model* __restrict__ models, const intf_table tab,
-                                         const intf_replay_buffers B) {
+                                         const intf_replay_buffers B, double* sseg) {
   const int lane = threadIdx.x & 31;
   const intf_scenario& S = scens[s];
   int status = B.status[s];
@@ -55,6 +57,7 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
   unsigned freemask = (cap >= 32) ? 0xffffffffu : ((1u << cap) - 1u);
   double now = 0.0;
   int n_formed = 0, dq = 0, n_done = 0, seg_cursor = 0, n_reseats = 0;
+  double last_done = -INFINITY;  // completion time of the latest outcome
 
   // formation-time window: lane l holds b_formed of batch fbase + l
   int fbase = 0;
@@ -96,7 +99,7 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
     const double o[3] = {own0, own1, own2}, colo[3] = {c0, c1, c2};
     const double sd = slowdown(o, colo, S.beta, noise);
     if (nseg < B.seg_stride) {
-      double* p = myseg + (size_t)nseg * 5;
+      double* p = nseg < kSmemSeg ? sseg + (lane * kSmemSeg + nseg) * 5 : myseg + (size_t)nseg * 5;
       p[0] = now;
       p[1] = sd;
       p[2] = c0;
@@ -176,10 +179,12 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
       off = shfl_i(off, cl);
       // lanes copy the completed batch's segments (segment k <- lane k)
       const double* cseg = B.slot_seg + ((size_t)s * B.cap_max + cl) * (size_t)B.seg_stride * 5;
+      const double* csm = sseg + cl * kSmemSeg * 5;
       for (int k = lane; k < nseg_c; k += 32) {
-        const double* p = cseg + (size_t)k * 5;
+        const double* p = k < kSmemSeg ? csm + k * 5 : cseg + (size_t)k * 5;
+        const double* q = k + 1 < kSmemSeg ? csm + (k + 1) * 5 : cseg + (size_t)(k + 1) * 5;
         B.s_tbegin[off + k] = p[0];
-        B.s_tend[off + k] = (k + 1 < nseg_c) ? p[5] : now;
+        B.s_tend[off + k] = (k + 1 < nseg_c) ? q[0] : now;
         B.s_slowdown[off + k] = p[1];
         B.s_colo[3 * (size_t)(off + k) + 0] = p[2];
         B.s_colo[3 * (size_t)(off + k) + 1] = p[3];
@@ -188,7 +193,9 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
       seg_cursor += nseg_c;
       // outcome order (completion, batch_id) (`simcore.py:305`): only runs of
       // equal completion time can need an insertion
-      if (lane == 0) {
+      if (lane == 0 && now != last_done) {
+        B.out_order[ro + n_done] = bmin;  // strictly later than every earlier outcome
+      } else if (lane == 0) {
         int pos = n_done;
         while (pos > 0) {
           const int prev = B.out_order[ro + pos - 1];
@@ -203,6 +210,7 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
       }
       __syncwarp();
       n_done++;
+      last_done = now;
       // remove cl from the running list, keep order
       unsigned long long nl = 0ull;
       int w = 0;
