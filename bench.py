@@ -57,7 +57,7 @@ def _traffic():
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("k_candidates", {}).get("dram_bytes_per_launch")
+        return d.get("k_cand_stream", {}).get("dram_bytes_per_launch")
     return None
 
 
@@ -155,6 +155,80 @@ def _ref_worker(args):
     return cpu_candidate_rate(table, W, seconds, seed)[1]
 
 
+REFIT_STREAMS = 10000
+REFIT_LEN = 300
+OLS_ROWS = 1 << 24
+
+
+def refit_secondary(a, stream, barrier, max_over_ranks, rank) -> dict:
+    """C3 shape: prequential RLS / SGD over 10^4 concurrent streams of 300
+    samples (`predict.py:157-205`), and the OLS statistics reduction over
+    2^24 samples (56 B each, HBM-read bound, `predict.py:53-66`)."""
+    import ctypes
+
+    import torch
+    from paper_2512_18725_b200 import _abi
+
+    L = _abi.load()
+    rng = np.random.default_rng(100 + rank)
+    n = REFIT_STREAMS * REFIT_LEN
+    X = torch.tensor(rng.uniform(0.0, 1.0, size=(n, 6)), device="cuda")
+    w_true = np.array([0.3, 0.5, 0.2, 0.8, 1.1, 0.4])
+    y = torch.tensor(X.cpu().numpy() @ w_true + 1.0 + 0.02 * rng.standard_normal(n), device="cuda")
+    off = torch.arange(0, n + 1, REFIT_LEN, dtype=torch.int64, device="cuda")
+    params0 = torch.zeros(REFIT_STREAMS, 7, dtype=torch.float64, device="cuda")
+    P0 = (100.0 * torch.eye(7, dtype=torch.float64, device="cuda")).repeat(REFIT_STREAMS, 1, 1).contiguous()
+    lam = torch.full((REFIT_STREAMS,), 0.99, dtype=torch.float64, device="cuda")
+    eta = torch.full((REFIT_STREAMS,), 0.01, dtype=torch.float64, device="cuda")
+    pred = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.zeros(REFIT_STREAMS, dtype=torch.int32, device="cuda")
+    s = stream.cuda_stream
+
+    def run(kind):
+        p = params0.clone()
+        if kind == "rls":
+            P = P0.clone()
+            return lambda: _abi.check(L.intf_rls_streams(X.data_ptr(), y.data_ptr(), off.data_ptr(), REFIT_STREAMS,
+                                                         lam.data_ptr(), p.data_ptr(), P.data_ptr(), pred.data_ptr(),
+                                                         st.data_ptr(), s), "rls")
+        return lambda: _abi.check(L.intf_sgd_streams(X.data_ptr(), y.data_ptr(), off.data_ptr(), REFIT_STREAMS,
+                                                     eta.data_ptr(), p.data_ptr(), pred.data_ptr(), st.data_ptr(), s),
+                                  "sgd")
+
+    out = {}
+    for kind in ("rls", "sgd"):
+        f = run(kind)
+        f()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        f()
+        e1.record(stream)
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        out[kind] = {"updates_per_s": n / (ms / 1e3), "ms": ms}
+    Xo = torch.rand(OLS_ROWS, 6, dtype=torch.float64, device="cuda")
+    yo = torch.rand(OLS_ROWS, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(56, dtype=torch.float64, device="cuda")
+    ws = torch.empty(_abi.OLS_WS_DOUBLES, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        _abi.check(L.intf_ols_stats(Xo.data_ptr(), yo.data_ptr(), OLS_ROWS, stats.data_ptr(), ws.data_ptr(), s), "ols")
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _abi.check(L.intf_ols_stats(Xo.data_ptr(), yo.data_ptr(), OLS_ROWS, stats.data_ptr(), ws.data_ptr(), s), "ols")
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    peak, _ = _peaks()
+    gbs = 56.0 * OLS_ROWS / (ms / 1e3) / 1e9
+    out["ols_stats"] = {"samples_per_s": OLS_ROWS / (ms / 1e3), "ms": ms, "achieved_gbs": gbs, "frac": gbs / peak,
+                        "bytes_per_sample": 56}
+    out["workload"] = (f"{REFIT_STREAMS} concurrent prequential streams x {REFIT_LEN} samples (RLS lambda 0.99, "
+                       f"SGD eta 0.01, fp64); OLS Z^T Z / Z^T y over {OLS_ROWS} samples")
+    return out
+
+
 def replay_stage_times(pipe, stream) -> dict:
     """One extra (untimed) pass of the replay pipeline with events between
     its launches: per-stage device time in ms."""
@@ -220,12 +294,17 @@ def product_arm(a):
     import torch
 
     rank, world, local = _env()
+    if a.backend == "gloo":  # plumbing test on a box with fewer GPUs than ranks (not a measurement)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2512_18725_b200 import _abi, engine
     from paper_2512_18725_b200.profiles import gen_synthetic_profiles
     from paper_2512_18725_b200.sweep import c5_scenarios
@@ -238,7 +317,7 @@ def product_arm(a):
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if a.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -263,14 +342,19 @@ def product_arm(a):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
+    evp = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     for k in range(a.steps):
+        # one step = phase 1 (candidate features) + phase 2 (forward of all decisions)
         ev[k][0].record(stream)
-        scorer.score(coefs, out)
+        scorer.prepare()
+        evp[k].record(stream)
+        scorer.score_prepared(coefs, out)
         ev[k][1].record(stream)
     t_end.record(stream)
     barrier()
     ms_total = max_over_ranks(t_start.elapsed_time(t_end))
-    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
+    kern_ms = float(np.mean([p.elapsed_time(e) for p, (_, e) in zip(evp, ev)]))  # k_cand_stream
+    prep_ms = float(np.mean([s.elapsed_time(p) for p, (s, _) in zip(evp, ev)]))  # k_cand_prep
     ms_step = ms_total / a.steps
     value = world * n_pred / (ms_step / 1e3)
 
@@ -312,10 +396,12 @@ def product_arm(a):
     r1.record(stream)
     barrier()
     rep_ms = max_over_ranks(r0.elapsed_time(r1)) / r_steps
-    clk = clocks.stop()
     stage_ms = replay_stage_times(pipe, stream)
     n_batches = int(pipe.t["n_batches"][: pipe.pb.n_scen].sum().item())
     n_req = int(pipe.t["n_req"][: pipe.pb.n_scen].sum().item())
+
+    refit = refit_secondary(a, stream, barrier, max_over_ranks, rank)
+    clk = clocks.stop()
 
     # ---- CPU baseline (rank 0, N=1 only): oracle port on a bounded sample
     cpu = None
@@ -323,6 +409,19 @@ def product_arm(a):
         rate, n, dt = cpu_candidate_rate(ta, W, a.cpu_seconds)
         cpu = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port",
                "sample": f"{n} predictions ({n // 2} random cap-4 candidates x coarse+fine, 1 decision) in {dt:.1f} s"}
+
+    # context: a pure device write (torch fill) of the same size -- the write-only ceiling
+    fill_buf = torch.empty(n_elems, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        fill_buf.fill_(1.0)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(10):
+        fill_buf.fill_(1.0)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    fill_gbs = 4.0 * n_elems * 10 / (f0.elapsed_time(f1) / 1e3) / 1e9
+    del fill_buf
 
     peak, peak_src = _peaks()
     bytes_per_launch = 4.0 * n_pred  # implicit enumeration: fp32 output only
@@ -340,9 +439,10 @@ def product_arm(a):
                 "h2d_bytes_per_step": int(W.size * 8), "d2h_bytes_per_step": int(4 * n_elems),
                 "call": "intf_predict_candidates_host (pinned host buffers)", "finite": ok},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_cand_prep + k_cand_stream (one step; time of both, bytes of the output)",
-                     "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": bytes_per_launch},
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_cand_stream",
+                     "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "step_kernels": {"k_cand_prep_ms": prep_ms, "k_cand_stream_ms": kern_ms},
+                     "write_only_reference_gbs": fill_gbs},
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": 2 * a.steps,
@@ -352,6 +452,7 @@ def product_arm(a):
                    "workload": "C5-shape synthetic scenarios (default_rng([2512,i]), 1 s, cap 1-3): arrivals + "
                                "replay + SLO + features/3 predictors", "launches_per_step": 5,
                    "stage_ms": stage_ms},
+        "refit": refit,
     }
     if rank == 0:
         print(json.dumps(line))
@@ -368,6 +469,8 @@ def main():
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the multi-rank plumbing with ranks sharing GPUs (numbers meaningless)")
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3

@@ -171,6 +171,14 @@ int intf_candidate_workspace(int32_t n_rows, int32_t cap, int64_t *ws_elems);
  * features in registers; with ws, k_cand_prep + k_cand_stream run.          */
 int intf_predict_candidates(const intf_table *table, int32_t cap, double alpha, const double *coefs, int32_t n_dec,
                             float *out, float *ws, int64_t ws_elems, void *stream);
+/* The two phases separately: features of every (multiset, own) for a
+ * (table, cap, alpha) into ws (k_cand_prep), then the forward pass of n_dec
+ * decisions from a prepared ws (k_cand_stream).  intf_predict_candidates
+ * with ws == prepare + prepared.                                            */
+int intf_candidate_prepare(const intf_table *table, int32_t cap, double alpha, float *ws, int64_t ws_elems,
+                           void *stream);
+int intf_predict_candidates_prepared(const intf_table *table, int32_t cap, const double *coefs, int32_t n_dec,
+                                     float *out, const float *ws, int64_t ws_elems, void *stream);
 /* Host-buffer variant (the end-to-end call): copies coefs in and all
  * predictions out.  h_out: n_dec*2*n_rows*ld floats; d_scratch: device
  * floats = 28*n_dec + that output size (+ the workspace to use two-phase). */

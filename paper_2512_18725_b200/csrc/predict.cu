@@ -313,69 +313,59 @@ __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ so
 
 constexpr int kStreamThreads = 128;
 constexpr int kStreamDec = 64;  // decisions per launch chunk (smem coefficient slab)
-constexpr int kStreamOwn = 4;   // own rows per thread (next row's features prefetched)
 
-// grid: x = groups of 4 multisets, y = chunks of kStreamOwn own rows, z = decision chunks
-__global__ void __launch_bounds__(kStreamThreads) k_cand_stream(const double* __restrict__ thr, int E, long long ld,
-                                                                long long n_sets, const double* __restrict__ coefs,
-                                                                int n_dec, const float* __restrict__ C0,
-                                                                const float* __restrict__ FE,
-                                                                float* __restrict__ out) {
-  __shared__ float4 cw[kStreamOwn][kStreamDec][2];
-  const int oa = blockIdx.y * kStreamOwn, no = min(kStreamOwn, E - oa);
+// grid: x = groups of 4 multisets, y = own row, z = decision chunks.  The
+// thread's feature loads (L2-resident C0/FE) are issued before the block
+// builds its coefficient slab, so their latency overlaps that setup.
+__global__ void __launch_bounds__(kStreamThreads, 8) k_cand_stream(const double* __restrict__ thr, int E, long long ld,
+                                                                   long long n_sets,
+                                                                   const double* __restrict__ coefs, int n_dec,
+                                                                   const float* __restrict__ C0,
+                                                                   const float* __restrict__ FE,
+                                                                   float* __restrict__ out) {
+  __shared__ float4 cw[kStreamDec][2];
+  const int o = blockIdx.y;
   const int d0 = blockIdx.z * kStreamDec, nd = min(kStreamDec, n_dec - d0);
-  for (int t = threadIdx.x; t < kStreamOwn * 2 * nd; t += blockDim.x) {
-    const int oi = t / (2 * nd), d = (t >> 1) % nd, kind = t & 1;
-    if (oi < no) {
-      const double* w = coefs + ((d0 + d) * 2 + kind) * 7;
-      const double* x = thr + 3 * (oa + oi);
-      const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
-      cw[oi][d][kind] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
-    }
-  }
   const long long r0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const bool inb = r0 < ld;
   const long long rr = inb ? r0 : 0;
   const float4 cx = __ldg(reinterpret_cast<const float4*>(C0 + rr));
   const float4 cy = __ldg(reinterpret_cast<const float4*>(C0 + ld + rr));
   const float4 cz = __ldg(reinterpret_cast<const float4*>(C0 + 2 * ld + rr));
-  float4 fx = __ldg(reinterpret_cast<const float4*>(FE + ((long long)oa * 3 + 0) * ld + rr));
-  float4 fy = __ldg(reinterpret_cast<const float4*>(FE + ((long long)oa * 3 + 1) * ld + rr));
-  float4 fz = __ldg(reinterpret_cast<const float4*>(FE + ((long long)oa * 3 + 2) * ld + rr));
+  const float4 fx = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 0) * ld + rr));
+  const float4 fy = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 1) * ld + rr));
+  const float4 fz = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 2) * ld + rr));
+  for (int t = threadIdx.x; t < 2 * nd; t += blockDim.x) {
+    const int d = t >> 1, kind = t & 1;
+    const double* w = coefs + ((d0 + d) * 2 + kind) * 7;
+    const double* x = thr + 3 * o;
+    const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
+    cw[d][kind] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
+  }
   __syncthreads();
   if (!inb) return;
   const long long kstride = (long long)E * ld, dstride = 2 * kstride;
   const long long nl = n_sets - r0;  // < 4 only in the last group: pad lanes are written as 0
-  for (int oi = 0; oi < no; oi++) {
-    // prefetch the next own row's fine features while this row streams out
-    const int on = oa + (oi + 1 < no ? oi + 1 : oi);
-    const float4 gx = __ldg(reinterpret_cast<const float4*>(FE + ((long long)on * 3 + 0) * ld + r0));
-    const float4 gy = __ldg(reinterpret_cast<const float4*>(FE + ((long long)on * 3 + 1) * ld + r0));
-    const float4 gz = __ldg(reinterpret_cast<const float4*>(FE + ((long long)on * 3 + 2) * ld + r0));
-    float* row = out + ((long long)d0 * 2 * E + oa + oi) * ld + r0;
+  float* row = out + ((long long)d0 * 2 * E + o) * ld + r0;
 #pragma unroll 4
-    for (int d = 0; d < nd; d++) {
-      const float4 a = cw[oi][d][0], b = cw[oi][d][1];
-      float4 yc, yf;
-      yc.x = fmaf(a.z, cz.x, fmaf(a.y, cy.x, fmaf(a.x, cx.x, a.w)));
-      yc.y = fmaf(a.z, cz.y, fmaf(a.y, cy.y, fmaf(a.x, cx.y, a.w)));
-      yc.z = fmaf(a.z, cz.z, fmaf(a.y, cy.z, fmaf(a.x, cx.z, a.w)));
-      yc.w = fmaf(a.z, cz.w, fmaf(a.y, cy.w, fmaf(a.x, cx.w, a.w)));
-      yf.x = fmaf(b.z, fz.x, fmaf(b.y, fy.x, fmaf(b.x, fx.x, b.w)));
-      yf.y = fmaf(b.z, fz.y, fmaf(b.y, fy.y, fmaf(b.x, fx.y, b.w)));
-      yf.z = fmaf(b.z, fz.z, fmaf(b.y, fy.z, fmaf(b.x, fx.z, b.w)));
-      yf.w = fmaf(b.z, fz.w, fmaf(b.y, fy.w, fmaf(b.x, fx.w, b.w)));
-      if (nl < 4) {
-        yc = make_float4(nl > 0 ? yc.x : 0.f, nl > 1 ? yc.y : 0.f, nl > 2 ? yc.z : 0.f, 0.f);
-        yf = make_float4(nl > 0 ? yf.x : 0.f, nl > 1 ? yf.y : 0.f, nl > 2 ? yf.z : 0.f, 0.f);
-      }
-      __stcs(reinterpret_cast<float4*>(row), yc);
-      __stcs(reinterpret_cast<float4*>(row + kstride), yf);
-      row += dstride;
+  for (int d = 0; d < nd; d++) {
+    const float4 a = cw[d][0], b = cw[d][1];
+    float4 yc, yf;
+    yc.x = fmaf(a.z, cz.x, fmaf(a.y, cy.x, fmaf(a.x, cx.x, a.w)));
+    yc.y = fmaf(a.z, cz.y, fmaf(a.y, cy.y, fmaf(a.x, cx.y, a.w)));
+    yc.z = fmaf(a.z, cz.z, fmaf(a.y, cy.z, fmaf(a.x, cx.z, a.w)));
+    yc.w = fmaf(a.z, cz.w, fmaf(a.y, cy.w, fmaf(a.x, cx.w, a.w)));
+    yf.x = fmaf(b.z, fz.x, fmaf(b.y, fy.x, fmaf(b.x, fx.x, b.w)));
+    yf.y = fmaf(b.z, fz.y, fmaf(b.y, fy.y, fmaf(b.x, fx.y, b.w)));
+    yf.z = fmaf(b.z, fz.z, fmaf(b.y, fy.z, fmaf(b.x, fx.z, b.w)));
+    yf.w = fmaf(b.z, fz.w, fmaf(b.y, fy.w, fmaf(b.x, fx.w, b.w)));
+    if (nl < 4) {
+      yc = make_float4(nl > 0 ? yc.x : 0.f, nl > 1 ? yc.y : 0.f, nl > 2 ? yc.z : 0.f, 0.f);
+      yf = make_float4(nl > 0 ? yf.x : 0.f, nl > 1 ? yf.y : 0.f, nl > 2 ? yf.z : 0.f, 0.f);
     }
-    fx = gx;
-    fy = gy;
-    fz = gz;
+    __stcs(reinterpret_cast<float4*>(row), yc);
+    __stcs(reinterpret_cast<float4*>(row + kstride), yf);
+    row += dstride;
   }
 }
 
@@ -777,23 +767,37 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const double* __restrict_
 long long cand_ws_elems(int E, long long ld) { return 3 * ld + 3LL * E * ld; }
 
 template <int K>
+static int launch_prep(const intf_table* t, int cap, double alpha, float* ws, cudaStream_t st) {
+  const int E = t->n_rows;
+  const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
+  const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_prep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_cand_prep<K><<<dim3(ceil_div(ld, 128), ceil_div(E, kPrepOwn)), 128, smem, st>>>(t->solo_ms, t->thr, E, cap, sets,
+                                                                                  ld, alpha, ws, ws + 3 * ld);
+  return launch_status("k_cand_prep");
+}
+
+static int launch_stream(const intf_table* t, int cap, const double* coefs, int n_dec, float* out, float* ws,
+                         cudaStream_t st) {
+  const int E = t->n_rows;
+  const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
+  dim3 grid(ceil_div(ld / 4, kStreamThreads), E, ceil_div(n_dec, kStreamDec));
+  k_cand_stream<<<grid, kStreamThreads, 0, st>>>(t->thr, E, ld, sets, coefs, n_dec, ws, ws + 3 * ld, out);
+  return launch_status("k_cand_stream");
+}
+
+// phase: 1 = feature prep, 2 = forward stream, 3 = both (two-phase path only)
+template <int K>
 static int launch_candidates(const intf_table* t, int cap, double alpha, const double* coefs, int n_dec, float* out,
-                             float* ws, long long ws_elems, cudaStream_t st) {
+                             float* ws, long long ws_elems, cudaStream_t st, int phase = 3) {
   const int E = t->n_rows;
   const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
   const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
   if (smem > 200 * 1024) return bad_input("intf_predict_candidates: profile table too large for the binomial table");
   if (ws && ws_elems >= cand_ws_elems(E, ld)) {  // two-phase: prep (features) + stream (forward)
-    float* C0 = ws;
-    float* FE = ws + 3 * ld;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_prep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cand_prep<K><<<dim3(ceil_div(ld, 128), ceil_div(E, kPrepOwn)), 128, smem, st>>>(t->solo_ms, t->thr, E, cap, sets,
-                                                                                    ld, alpha, C0, FE);
-    int rc = launch_status("k_cand_prep");
-    if (rc) return rc;
-    dim3 grid(ceil_div(ld / 4, kStreamThreads), ceil_div(E, kStreamOwn), ceil_div(n_dec, kStreamDec));
-    k_cand_stream<<<grid, kStreamThreads, 0, st>>>(t->thr, E, ld, sets, coefs, n_dec, C0, FE, out);
-    return launch_status("k_cand_stream");
+    int rc = (phase & 1) ? launch_prep<K>(t, cap, alpha, ws, st) : INTF_OK;
+    if (rc || !(phase & 2)) return rc;
+    return launch_stream(t, cap, coefs, n_dec, out, ws, st);
   }
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_candidates<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(ceil_div(ld / kGroup, kCandThreads), ceil_div(E, kOwnChunk), ceil_div(n_dec, kDecChunk));
@@ -821,21 +825,43 @@ int intf_candidate_workspace(int32_t n_rows, int32_t cap, int64_t* ws_elems) {
   return INTF_OK;
 }
 
+static int dispatch_candidates(const intf_table* table, int32_t cap, double alpha, const double* coefs, int32_t n_dec,
+                               float* out, float* ws, int64_t ws_elems, void* stream, int phase) {
+  cudaStream_t st = as_stream(stream);
+  switch (cap - 1) {
+    case 0: return launch_candidates<0>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st, phase);
+    case 1: return launch_candidates<1>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st, phase);
+    case 2: return launch_candidates<2>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st, phase);
+    case 3: return launch_candidates<3>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st, phase);
+    case 4: return launch_candidates<4>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st, phase);
+    case 5: return launch_candidates<5>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st, phase);
+    case 6: return launch_candidates<6>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st, phase);
+    default: return launch_candidates<7>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st, phase);
+  }
+}
+
 int intf_predict_candidates(const intf_table* table, int32_t cap, double alpha, const double* coefs, int32_t n_dec,
                             float* out, float* ws, int64_t ws_elems, void* stream) {
   if (!table || !coefs || !out || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1 || table->n_rows < 1)
     return bad_input("intf_predict_candidates: bad argument (n_dec >= 1, 1 <= cap <= 8)");
-  cudaStream_t st = as_stream(stream);
-  switch (cap - 1) {
-    case 0: return launch_candidates<0>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
-    case 1: return launch_candidates<1>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
-    case 2: return launch_candidates<2>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
-    case 3: return launch_candidates<3>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
-    case 4: return launch_candidates<4>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
-    case 5: return launch_candidates<5>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
-    case 6: return launch_candidates<6>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
-    default: return launch_candidates<7>(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, st);
-  }
+  return dispatch_candidates(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, stream, 3);
+}
+
+int intf_candidate_prepare(const intf_table* table, int32_t cap, double alpha, float* ws, int64_t ws_elems,
+                           void* stream) {
+  int64_t need = 0;
+  if (!table || !ws || intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need)
+    return bad_input("intf_candidate_prepare: bad argument or workspace too small");
+  return dispatch_candidates(table, cap, alpha, nullptr, 1, nullptr, ws, ws_elems, stream, 1);
+}
+
+int intf_predict_candidates_prepared(const intf_table* table, int32_t cap, const double* coefs, int32_t n_dec,
+                                     float* out, const float* ws, int64_t ws_elems, void* stream) {
+  int64_t need = 0;
+  if (!table || !coefs || !out || !ws || n_dec < 1 || intf_candidate_workspace(table->n_rows, cap, &need) ||
+      ws_elems < need)
+    return bad_input("intf_predict_candidates_prepared: bad argument or workspace too small");
+  return launch_stream(table, cap, coefs, n_dec, out, const_cast<float*>(ws), as_stream(stream));
 }
 
 int intf_predict_candidates_host(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,

@@ -428,6 +428,20 @@ class CandidateScorer:
                                                        coefs.data_ptr(), n_dec, out.data_ptr(), _abi.addr(self.ws),
                                                        self.ws_elems, stream_ptr()), "intf_predict_candidates")
 
+    def prepare(self) -> None:
+        """Phase 1 only (k_cand_prep): candidate features into the workspace."""
+        _abi.check(_abi.load().intf_candidate_prepare(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
+                                                      _abi.addr(self.ws), self.ws_elems, stream_ptr()),
+                   "intf_candidate_prepare")
+
+    def score_prepared(self, coefs: torch.Tensor, out: torch.Tensor) -> None:
+        """Phase 2 only (k_cand_stream) from a prepared workspace."""
+        n_dec = coefs.numel() // 14
+        _abi.check(_abi.load().intf_predict_candidates_prepared(ctypes.byref(self.dtable.struct), self.cap,
+                                                                coefs.data_ptr(), n_dec, out.data_ptr(),
+                                                                _abi.addr(self.ws), self.ws_elems, stream_ptr()),
+                   "intf_predict_candidates_prepared")
+
     def scratch_elems(self, n_dec: int) -> int:
         """Device floats needed by score_host (coefs + outputs + workspace)."""
         return 28 * n_dec + self.out_elems(n_dec) + self.ws_elems
