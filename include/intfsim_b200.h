@@ -82,7 +82,7 @@ typedef struct intf_batch {
   const intf_model *models;    /* device [n_models] */
   int32_t n_scen, n_models;    /* totals */
   int32_t max_req_cap;         /* max over scenarios of req_cap */
-  int32_t pad_;
+  int32_t max_models;          /* max over scenarios of n_models */
 } intf_batch;
 
 /* Device buffers of the replay pipeline.  Index spaces:

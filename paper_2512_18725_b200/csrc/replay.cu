@@ -89,14 +89,16 @@ __global__ void k_split_arrivals(const intf_scenario* __restrict__ scen, int n_s
   B.status[s] |= st;
 }
 
-// ---- K1: batch formation, one warp per scenario (no GPU state, no RNG).
+// ---- K1: batch formation, one W-lane group per scenario (no GPU state, no
+// RNG); W = 8 (four scenarios per warp) when every scenario deploys <= 8 models.
 constexpr int kFormWarps = 4;
+template <int W>
 __global__ void __launch_bounds__(32 * kFormWarps) k_form(const intf_scenario* __restrict__ scen, int n_scen,
                                                           const intf_model* __restrict__ models,
                                                           intf_replay_buffers B) {
-  const int s = blockIdx.x * kFormWarps + (threadIdx.x >> 5);
+  const int s = (blockIdx.x * kFormWarps + (threadIdx.x >> 5)) * (32 / W) + ((threadIdx.x & 31) / W);
   if (s >= n_scen) return;
-  form_warp(s, scen, models, B);
+  form_group<W>(s, scen, models, B);
 }
 
 // ---- K1b: noise draws of the first noise_k segments of every formed batch
@@ -113,15 +115,18 @@ __global__ void k_noise_table(const intf_scenario* __restrict__ scen, intf_repla
   B.noise_tab[(long long)(S.req_off + b) * K + k] = noise_draw(S.oracle_seed, (uint64_t)b, (uint64_t)k, S.sigma);
 }
 
-// ---- K2: the replay recurrence, one warp per scenario (replay_warp.cuh).
+// ---- K2: the replay recurrence, one 8-lane group per scenario (four
+// scenarios per warp; lane l < cap owns running slot l; replay_warp.cuh).
 constexpr int kReplayWarps = 4;
-__global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_warp(const intf_scenario* __restrict__ scen, int n_scen,
-                                                                 const intf_model* __restrict__ models,
-                                                                 intf_table tab, intf_replay_buffers B) {
-  __shared__ double sseg[kReplayWarps][kMaxCap * kSmemSeg * 5];
-  const int s = blockIdx.x * kReplayWarps + (threadIdx.x >> 5);
+constexpr int kReplayW = 8;
+__global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_warp(const intf_scenario* __restrict__ scen,
+                                                                    int n_scen, const intf_model* __restrict__ models,
+                                                                    intf_table tab, intf_replay_buffers B) {
+  __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
+  const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
+  const int s = blockIdx.x * kReplayWarps * (32 / kReplayW) + g;
   if (s >= n_scen) return;
-  replay_warp(s, scen, models, tab, B, sseg[threadIdx.x >> 5]);
+  replay_group<kReplayW>(s, scen, models, tab, B, sseg[g]);
 }
 
 // ---- K3: SLO records + per-model nearest-rank percentiles, one block per
@@ -313,15 +318,19 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
     return bad_input("intf_replay: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
   cudaStream_t st = as_stream(stream);
   int rc;
-  k_form<<<ceil_div(bt->n_scen, kFormWarps), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
+  if (bt->max_models <= 8)
+    k_form<8><<<ceil_div(bt->n_scen, kFormWarps * 4), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models,
+                                                                               *buf);
+  else
+    k_form<32><<<ceil_div(bt->n_scen, kFormWarps), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
   if ((rc = launch_status("k_form"))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
     dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
     k_noise_table<<<grid, 128, 0, st>>>(bt->scen, *buf);
     if ((rc = launch_status("k_noise_table"))) return rc;
   }
-  k_replay_warp<<<ceil_div(bt->n_scen, kReplayWarps), 32 * kReplayWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models,
-                                                                                  *table, *buf);
+  k_replay_warp<<<ceil_div(bt->n_scen, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, st>>>(
+      bt->scen, bt->n_scen, bt->models, *table, *buf);
   return launch_status("k_replay_warp");
 }
 

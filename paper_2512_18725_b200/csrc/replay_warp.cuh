@@ -1,20 +1,23 @@
-// replay_warp.cuh -- warp-per-scenario form of the replay recurrence
-// (sm_100a).  Same events, same arithmetic, same outputs as replay_formed()
-// in replay_core.cuh (which remains the readable/host-checkable statement);
-// this version maps one scenario to one warp:
-//   * lane l < cap owns running slot l -- its batch state lives in that
-//     lane's registers (no local-memory slot arrays);
-//   * the running-list (dispatch) order is a warp-uniform list of 4-bit lane
-//     ids, so every lane computes its colo sum ((0 + p1) + p2).. in list
-//     order from shuffles, and all reseats of one event run in parallel
-//     (they are independent: colo reads only `own`, noise is keyed by
-//     (batch, segment index));
-//   * the next completion is a (done_at, batch_id) lexicographic min over
-//     lanes (shuffle butterfly), compared with the next formation exactly as
-//     the reference heap would (completion first at equal time);
+// replay_warp.cuh -- lane-group forms of the replay recurrence and of batch
+// formation (sm_100a).  Same events, same arithmetic, same outputs as
+// replay_formed() / form_scenario() in replay_core.cuh (which remain the
+// readable, host-checkable statements).
+//
+// A scenario is mapped to a group of W lanes (W = 8: four scenarios per warp,
+// or W = 32), every collective is masked to the group:
+//   * replay: lane l < cap owns running slot l in registers; the running
+//     (dispatch) order is a group-uniform list of 4-bit lane ids, so each lane
+//     computes its colo sum ((0 + p1) + p2).. in list order from shuffles and
+//     all reseats of one event run in parallel (they are independent: colo
+//     reads only `own`, noise is keyed by (batch, segment index)); the next
+//     completion is a (done_at, batch_id) min over the cap lanes, compared
+//     with the next formation as the reference heap would (completion first
+//     at equal time);
 //   * formation times, and the model/size/first noise draws of the batches
-//     about to be dispatched, stream through two 32-batch register windows
-//     refilled by coalesced loads, keeping global latency off the chain.
+//     about to be dispatched, stream through W-batch register windows
+//     refilled by coalesced loads, keeping global latency off the chain;
+//   * formation: lane m holds model m's pending event, the next batch is the
+//     (time, kind, key) min over lanes, the window-member count is a ballot.
 #pragma once
 #include "replay_core.cuh"
 
@@ -29,14 +32,38 @@ __device__ __noinline__ double noise_draw_slow(uint64_t seed, uint64_t batch, ui
   return noise_draw(seed, batch, seg, sigma);
 }
 
-__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
-__device__ __forceinline__ int shfl_i(int v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+// W-lane group of the calling thread (W divides 32)
+template <int W>
+struct LaneGroup {
+  unsigned mask;
+  int lane, base;
+  __device__ __forceinline__ LaneGroup() {
+    const int l = threadIdx.x & 31;
+    base = l & ~(W - 1);
+    lane = l & (W - 1);
+    mask = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << base);
+  }
+  __device__ __forceinline__ double shfl(double v, int src) const { return __shfl_sync(mask, v, src, W); }
+  __device__ __forceinline__ int shfl(int v, int src) const { return __shfl_sync(mask, v, src, W); }
+  __device__ __forceinline__ unsigned shfl(unsigned v, int src) const { return __shfl_sync(mask, v, src, W); }
+  __device__ __forceinline__ double shfl_xor(double v, int o) const { return __shfl_xor_sync(mask, v, o, W); }
+  __device__ __forceinline__ int shfl_xor(int v, int o) const { return __shfl_xor_sync(mask, v, o, W); }
+  __device__ __forceinline__ unsigned shfl_xor(unsigned v, int o) const { return __shfl_xor_sync(mask, v, o, W); }
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    const unsigned b = __ballot_sync(mask, p) >> base;
+    return W == 32 ? b : (b & ((1u << W) - 1u));
+  }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  __device__ __forceinline__ unsigned reduce_or(unsigned v) const { return __reduce_or_sync(mask, v); }
+};
 
-// sseg: this warp's shared-memory segment history, [kMaxCap][kSmemSeg][5]
-__device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restrict__ scens,
-                                         const intf_model* __restrict__ models, const intf_table tab,
-                                         const intf_replay_buffers B, double* sseg) {
-  const int lane = threadIdx.x & 31;
+// sseg: this group's shared-memory segment history, [kMaxCap][kSmemSeg][5]
+template <int W>
+__device__ __forceinline__ void replay_group(int s, const intf_scenario* __restrict__ scens,
+                                             const intf_model* __restrict__ models, const intf_table tab,
+                                             const intf_replay_buffers B, double* sseg) {
+  const LaneGroup<W> G;
+  const int lane = G.lane;
   const intf_scenario& S = scens[s];
   int status = B.status[s];
   if (status & (INTF_ST_CAP | INTF_ST_OVERFLOW)) return;
@@ -51,7 +78,7 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
   double cur_tb = 0.0, cur_sd = 1.0, nz0 = 1.0, nz1 = 1.0, nz2 = 1.0, nz3 = 1.0;
   int batch = 0, nseg = 0, n_non1 = 0;
 
-  // ---- warp-uniform state
+  // ---- group-uniform state
   unsigned long long runlist = 0ull;  // 4-bit lane ids in dispatch order
   int nrun = 0;
   unsigned freemask = (cap >= 32) ? 0xffffffffu : ((1u << cap) - 1u);
@@ -79,13 +106,13 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
   };
   load_dispatch_window(0);
 
-  // reseat of this lane's batch at `now` (`simcore.py:133-141`); every active
-  // lane calls it together (uniform shuffles inside)
+  // reseat of this lane's batch at `now` (`simcore.py:133-141`); every lane of
+  // the group calls it together (group-uniform shuffles inside)
   auto reseat_lane = [&](bool doit) {
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    for (int k = 0; k < nrun; k++) {  // warp-uniform loop, running-list order
+    for (int k = 0; k < nrun; k++) {  // group-uniform loop, running-list order
       const int j = (int)((runlist >> (4 * k)) & 15ull);
-      const double a0 = shfl_d(own0, j), a1 = shfl_d(own1, j), a2 = shfl_d(own2, j);
+      const double a0 = G.shfl(own0, j), a1 = G.shfl(own1, j), a2 = G.shfl(own2, j);
       if (j != lane) {
         c0 = c0 + a0;
         c1 = c1 + a1;
@@ -134,27 +161,27 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
     double dmin = act ? done : INFINITY;
     int bmin = act ? batch : 0x7fffffff;
     for (int o = red_hi; o > 0; o >>= 1) {
-      const double d2 = __shfl_xor_sync(0xffffffffu, dmin, o);
-      const int b2 = __shfl_xor_sync(0xffffffffu, bmin, o);
+      const double d2 = G.shfl_xor(dmin, o);
+      const int b2 = G.shfl_xor(bmin, o);
       if (d2 < dmin || (d2 == dmin && b2 < bmin)) {
         dmin = d2;
         bmin = b2;
       }
     }
-    dmin = shfl_d(dmin, 0);
-    bmin = shfl_i(bmin, 0);
+    dmin = G.shfl(dmin, 0);
+    bmin = G.shfl(bmin, 0);
     const bool have_form = n_formed < nb;
-    if (have_form && n_formed - fbase >= 32) {
-      fbase += 32;
+    if (have_form && n_formed - fbase >= W) {
+      fbase += W;
       wf = fbase + lane < nb ? B.b_formed[ro + fbase + lane] : 0.0;
     }
-    const double tf = shfl_d(wf, (n_formed - fbase) & 31);
+    const double tf = G.shfl(wf, (n_formed - fbase) & (W - 1));
     if (nrun == 0 && !have_form) break;
     if (nrun > 0 && (!have_form || dmin <= tf)) {
       // ---- COMPLETION (`simcore.py:173-198`)
       if (dmin < now - 1e-9) status |= INTF_ST_PAST_EVENT;
       now = now > dmin ? now : dmin;
-      const unsigned cmask = __ballot_sync(0xffffffffu, act && batch == bmin);
+      const unsigned cmask = G.ballot(act && batch == bmin);
       const int cl = __ffs(cmask) - 1;
       int nseg_c = 0, off = 0;
       if (lane == cl) {
@@ -174,13 +201,13 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
         B.b_nseg[ro + batch] = nseg_c;
         act = false;
       }
-      __syncwarp();  // lane cl's outcome/segment writes visible to the warp
-      nseg_c = shfl_i(nseg_c, cl);
-      off = shfl_i(off, cl);
-      // lanes copy the completed batch's segments (segment k <- lane k)
+      G.sync();  // lane cl's outcome/segment writes visible to the group
+      nseg_c = G.shfl(nseg_c, cl);
+      off = G.shfl(off, cl);
+      // lanes copy the completed batch's segments (segment k <- lane k mod W)
       const double* cseg = B.slot_seg + ((size_t)s * B.cap_max + cl) * (size_t)B.seg_stride * 5;
       const double* csm = sseg + cl * kSmemSeg * 5;
-      for (int k = lane; k < nseg_c; k += 32) {
+      for (int k = lane; k < nseg_c; k += W) {
         const double* p = k < kSmemSeg ? csm + k * 5 : cseg + (size_t)k * 5;
         const double* q = k + 1 < kSmemSeg ? csm + (k + 1) * 5 : cseg + (size_t)(k + 1) * 5;
         B.s_tbegin[off + k] = p[0];
@@ -208,7 +235,7 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
         }
         B.out_order[ro + pos] = bmin;
       }
-      __syncwarp();
+      G.sync();
       n_done++;
       last_done = now;
       // remove cl from the running list, keep order
@@ -233,13 +260,13 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
     // ---- try_dispatch (`simcore.py:258-262`) -> dispatch (`:153-171`)
     while (dq < n_formed && nrun < cap) {
       const int b = dq++;
-      if (b - dbase >= 32) {
-        dbase += 32;
+      if (b - dbase >= W) {
+        dbase += W;
         load_dispatch_window(dbase);
       }
-      const int src = (b - dbase) & 31;
-      const int m = shfl_i(wm, src), sz = shfl_i(wsz, src);
-      const double n0 = shfl_d(wn0, src), n1 = shfl_d(wn1, src), n2 = shfl_d(wn2, src), n3 = shfl_d(wn3, src);
+      const int src = (b - dbase) & (W - 1);
+      const int m = G.shfl(wm, src), sz = G.shfl(wsz, src);
+      const double n0 = G.shfl(wn0, src), n1 = G.shfl(wn1, src), n2 = G.shfl(wn2, src), n3 = G.shfl(wn3, src);
       const int L = __ffs(freemask) - 1;
       freemask &= ~(1u << L);
       runlist |= (unsigned long long)L << (4 * nrun);
@@ -269,7 +296,7 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
     }
   }
   if (nrun || dq < n_formed) status |= INTF_ST_NONQUIESCENT;
-  status = __reduce_or_sync(0xffffffffu, (unsigned)status);
+  status = (int)G.reduce_or((unsigned)status);
   if (lane == 0) {
     B.n_segments[s] = seg_cursor;
     B.n_reseats[s] = n_reseats;
@@ -277,21 +304,17 @@ __device__ __forceinline__ void replay_warp(int s, const intf_scenario* __restri
   }
 }
 
-}  // namespace intf
-
-namespace intf {
-
 // ---------------------------------------------------------------------------
-// Warp-per-scenario batch formation (same result as form_scenario()): lane m
-// holds model m's pending formation event (time, kind, key, count); the next
-// batch is the lexicographic (time, kind, key) min over lanes (heap order,
+// Lane-group batch formation (same result as form_scenario()): lane m holds
+// model m's pending formation event (time, kind, key, count); the next batch
+// is the lexicographic (time, kind, key) min over lanes (heap order,
 // `simcore.py:98-100,122`); its next event is recomputed cooperatively -- the
 // window membership test t < D is monotone along the sorted list, so the
 // member count is a ballot popcount.
-__device__ __forceinline__ void warp_next_formation(const double* lt, const int32_t* lrid, int n, int h,
-                                                    double window, int max_bs, uint32_t crc, double& t,
-                                                    int& kind, uint32_t& key, int& cnt) {
-  const int lane = threadIdx.x & 31;
+template <int W>
+__device__ __forceinline__ void group_next_formation(const LaneGroup<W>& G, const double* lt, const int32_t* lrid,
+                                                     int n, int h, double window, int max_bs, uint32_t crc,
+                                                     double& t, int& kind, uint32_t& key, int& cnt) {
   if (h >= n) {
     kind = 0;
     t = 0.0;
@@ -301,13 +324,12 @@ __device__ __forceinline__ void warp_next_formation(const double* lt, const int3
   }
   const double D = lt[h] + window;  // every lane loads the same word (broadcast)
   int c = 1;
-  for (int j0 = 1; j0 < max_bs; j0 += 32) {
-    const int j = j0 + lane;
+  for (int j0 = 1; j0 < max_bs; j0 += W) {
+    const int j = j0 + G.lane;
     const bool in = j < max_bs && h + j < n && lt[h + j] < D;
-    const unsigned m = __ballot_sync(0xffffffffu, in);
-    const int add = __popc(m);
+    const int add = __popc(G.ballot(in));
     c += add;
-    if (add < 32) break;
+    if (add < W) break;
   }
   cnt = c;
   if (c == max_bs) {
@@ -321,12 +343,14 @@ __device__ __forceinline__ void warp_next_formation(const double* lt, const int3
   }
 }
 
-__device__ __noinline__ void form_warp(int s, const intf_scenario* __restrict__ scens,
-                                       const intf_model* __restrict__ models, const intf_replay_buffers B) {
-  const int lane = threadIdx.x & 31;
+template <int W>
+__device__ __forceinline__ void form_group(int s, const intf_scenario* __restrict__ scens,
+                                           const intf_model* __restrict__ models, const intf_replay_buffers B) {
+  const LaneGroup<W> G;
+  const int lane = G.lane;
   const intf_scenario& S = scens[s];
   const int M = S.n_models;
-  if ((B.status[s] & INTF_ST_OVERFLOW) || M > 32 || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 ||
+  if ((B.status[s] & INTF_ST_OVERFLOW) || M > W || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 ||
       S.max_bs < 1) {
     if (lane == 0) {
       if (!(B.status[s] & INTF_ST_OVERFLOW)) B.status[s] = INTF_ST_CAP;
@@ -348,9 +372,10 @@ __device__ __noinline__ void form_warp(int s, const intf_scenario* __restrict__ 
     double t;
     int kind, cnt;
     uint32_t key;
-    const int lom = __shfl_sync(0xffffffffu, lo, m), lnm = __shfl_sync(0xffffffffu, ln, m);
-    const uint32_t crm = __shfl_sync(0xffffffffu, crc, m);
-    warp_next_formation(B.list_t + lom, B.list_rid + lom, lnm, 0, S.window_ms, S.max_bs, crm, t, kind, key, cnt);
+    const int lom = G.shfl(lo, m), lnm = G.shfl(ln, m);
+    const uint32_t crm = G.shfl(crc, m);
+    group_next_formation<W>(G, B.list_t + lom, B.list_rid + lom, lnm, 0, S.window_ms, S.max_bs, crm, t, kind, key,
+                            cnt);
     if (lane == m) {
       et = t;
       ekind = kind;
@@ -370,10 +395,10 @@ __device__ __noinline__ void form_warp(int s, const intf_scenario* __restrict__ 
     uint32_t bkey = ekind ? ekey : 0xffffffffu;
     int bm = lane;
     for (int o = red_hi; o > 0; o >>= 1) {
-      const double t2 = __shfl_xor_sync(0xffffffffu, bt, o);
-      const int k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-      const uint32_t y2 = __shfl_xor_sync(0xffffffffu, bkey, o);
-      const int m2 = __shfl_xor_sync(0xffffffffu, bm, o);
+      const double t2 = G.shfl_xor(bt, o);
+      const int k2 = G.shfl_xor(bk, o);
+      const uint32_t y2 = G.shfl_xor(bkey, o);
+      const int m2 = G.shfl_xor(bm, o);
       const bool less = t2 < bt || (t2 == bt && (k2 < bk || (k2 == bk && (y2 < bkey || (y2 == bkey && m2 < bm)))));
       if (less) {
         bt = t2;
@@ -382,27 +407,27 @@ __device__ __noinline__ void form_warp(int s, const intf_scenario* __restrict__ 
         bm = m2;
       }
     }
-    bt = __shfl_sync(0xffffffffu, bt, 0);
-    bk = __shfl_sync(0xffffffffu, bk, 0);
-    bm = __shfl_sync(0xffffffffu, bm, 0);
+    bt = G.shfl(bt, 0);
+    bk = G.shfl(bk, 0);
+    bm = G.shfl(bm, 0);
     if (bk == 3) break;
     const int fm = bm;
-    const int cnt = __shfl_sync(0xffffffffu, ecnt, fm);
-    const int h = __shfl_sync(0xffffffffu, head, fm);
-    const int lom = __shfl_sync(0xffffffffu, lo, fm), lnm = __shfl_sync(0xffffffffu, ln, fm);
-    const uint32_t crm = __shfl_sync(0xffffffffu, crc, fm);
+    const int cnt = G.shfl(ecnt, fm);
+    const int h = G.shfl(head, fm);
+    const int lom = G.shfl(lo, fm), lnm = G.shfl(ln, fm);
+    const uint32_t crm = G.shfl(crc, fm);
     const int b = n_formed++;
     if (lane == 0) {
       B.b_model[ro + b] = fm;
       B.b_size[ro + b] = cnt;
       B.b_formed[ro + b] = bt;
     }
-    for (int j = lane; j < cnt; j += 32) B.r_batch[ro + B.list_rid[lom + h + j]] = b;
+    for (int j = lane; j < cnt; j += W) B.r_batch[ro + B.list_rid[lom + h + j]] = b;
     double t;
     int kind, c2;
     uint32_t key;
-    warp_next_formation(B.list_t + lom, B.list_rid + lom, lnm, h + cnt, S.window_ms, S.max_bs, crm, t, kind, key,
-                        c2);
+    group_next_formation<W>(G, B.list_t + lom, B.list_rid + lom, lnm, h + cnt, S.window_ms, S.max_bs, crm, t, kind,
+                            key, c2);
     if (lane == fm) {
       head = h + cnt;
       et = t;
@@ -482,7 +507,7 @@ __device__ __noinline__ int gen_model_arrivals_warp(const intf_scenario& S, cons
     __syncwarp();
     const double tl = gaps[lane];
     const unsigned inside = __ballot_sync(0xffffffffu, tl < horizon);
-    // times are increasing: the first t >= horizon ends the stream
+    // times are non-decreasing: the first t >= horizon ends the stream
     const int k_in = __popc(inside) == 32 ? 32 : __ffs(~inside) - 1;
     if (lane < k_in && n + lane < list_cap) list_t[n + lane] = tl;
     n += k_in;
