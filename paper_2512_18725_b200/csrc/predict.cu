@@ -64,14 +64,25 @@ __device__ __forceinline__ int unrank_multiset(long long r, int E, int cap, cons
 #pragma unroll
   for (int i = KMAX; i >= 1; i--) {
     if (i > k) continue;
-    int lo = i - 1, hi = E + k - 2;  // largest c with C(c, i) <= r
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if ((long long)C(mid, i) <= r) lo = mid;
-      else hi = mid - 1;
+    int c;  // largest c with C(c, i) <= r
+    if (i <= 3) {
+      // closed-form estimate from C(c, i) ~ c^i / i!, then exact integer fix-up
+      const double rr = (double)r;
+      c = i == 1 ? (int)r : i == 2 ? (int)floor(0.5 * (1.0 + sqrt(1.0 + 8.0 * rr))) : (int)floor(cbrt(6.0 * rr)) + 1;
+      c = c < i - 1 ? i - 1 : (c > E + k - 2 ? E + k - 2 : c);
+      while (c > i - 1 && (long long)C(c, i) > r) c--;
+      while (c < E + k - 2 && (long long)C(c + 1, i) <= r) c++;
+    } else {
+      int lo = i - 1, hi = E + k - 2;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((long long)C(mid, i) <= r) lo = mid;
+        else hi = mid - 1;
+      }
+      c = lo;
     }
-    r -= (long long)C(lo, i);
-    p[i - 1] = lo - (i - 1);
+    r -= (long long)C(c, i);
+    p[i - 1] = c - (i - 1);
   }
   return k;
 }
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(kCandThreads, 2) k_candidates(const double* __
 //                     how many peers finish before o), fp32
 // Phase 2 (k_cand_stream): pure streaming -- per thread 4 multisets x 1 own x
 // all decisions: 3 FFMA per prediction, 16-byte streaming stores.
-constexpr int kPrepOwn = 8;  // own rows per prep thread (grid.y splits the table)
+constexpr int kPrepOwn = 12;  // own rows per prep thread (grid.y splits the table)
 
 template <int KMAX>
 __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ solo, const double* __restrict__ thr,
@@ -444,13 +455,19 @@ __device__ __forceinline__ void jacobi_eigs(const double* G, double* ev) {
   for (int i = 0; i < 7; i++)
 #pragma unroll
     for (int j = 0; j < 7; j++) a[i][j] = G[i * 7 + j];
+  double fro = 0.0;  // ||G||_F^2: stop once the off-diagonal mass is below (eps ||G||_F)^2
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = 0; j < 7; j++) fro += a[i][j] * a[i][j];
+  const double stop = fro * 1.2e-34;
   for (int sweep = 0; sweep < 30; sweep++) {
     double off = 0.0;
 #pragma unroll
     for (int i = 0; i < 7; i++)
 #pragma unroll
       for (int j = i + 1; j < 7; j++) off += a[i][j] * a[i][j];
-    if (off == 0.0) break;
+    if (off <= stop) break;
 #pragma unroll
     for (int p = 0; p < 7; p++)
 #pragma unroll

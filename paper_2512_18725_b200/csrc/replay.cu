@@ -90,7 +90,8 @@ __global__ void k_split_arrivals(const intf_scenario* __restrict__ scen, int n_s
 }
 
 // ---- K1: batch formation, one W-lane group per scenario (no GPU state, no
-// RNG); W = 8 (four scenarios per warp) when every scenario deploys <= 8 models.
+// RNG).  W = 32 is used: packing four 8-lane groups per warp measured no
+// faster (the warp waits for its slowest scenario).
 constexpr int kFormWarps = 4;
 template <int W>
 __global__ void __launch_bounds__(32 * kFormWarps) k_form(const intf_scenario* __restrict__ scen, int n_scen,
@@ -115,10 +116,10 @@ __global__ void k_noise_table(const intf_scenario* __restrict__ scen, intf_repla
   B.noise_tab[(long long)(S.req_off + b) * K + k] = noise_draw(S.oracle_seed, (uint64_t)b, (uint64_t)k, S.sigma);
 }
 
-// ---- K2: the replay recurrence, one 8-lane group per scenario (four
-// scenarios per warp; lane l < cap owns running slot l; replay_warp.cuh).
+// ---- K2: the replay recurrence, one kReplayW-lane group per scenario (lane
+// l < cap owns running slot l; replay_warp.cuh).
 constexpr int kReplayWarps = 4;
-constexpr int kReplayW = 8;
+constexpr int kReplayW = 32;  // measured: one scenario per warp beats 4 x 8-lane groups (divergence)
 __global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_warp(const intf_scenario* __restrict__ scen,
                                                                     int n_scen, const intf_model* __restrict__ models,
                                                                     intf_table tab, intf_replay_buffers B) {
@@ -318,11 +319,7 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
     return bad_input("intf_replay: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
   cudaStream_t st = as_stream(stream);
   int rc;
-  if (bt->max_models <= 8)
-    k_form<8><<<ceil_div(bt->n_scen, kFormWarps * 4), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models,
-                                                                               *buf);
-  else
-    k_form<32><<<ceil_div(bt->n_scen, kFormWarps), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
+  k_form<32><<<ceil_div(bt->n_scen, kFormWarps), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
   if ((rc = launch_status("k_form"))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
     dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
