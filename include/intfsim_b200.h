@@ -130,6 +130,21 @@ int intf_split_arrivals(const intf_batch *batch, const intf_replay_buffers *buf,
  * admission/reseat/completion recurrence, thread per scenario). */
 int intf_replay(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf, void *stream);
 
+/* The replay in two steps, for busy-period sharding of long traces (SURVEY
+ * §8e): intf_form_batches = k_form + k_noise_table (batch ids, members,
+ * formation times, noise table); intf_replay_jobs replays jobs
+ * i = batches [job_lo[i], job_hi[i]) of scenario job_scen[i], each started
+ * from an idle GPU, in parallel (one warp per job; slot_seg must hold
+ * n_jobs*cap_max*seg_stride*5 doubles).  Outputs per batch / outcome slot are
+ * exact whenever each job boundary is an idle point: the previous job of the
+ * scenario must satisfy job_last_done <= b_formed[job_lo] (checked by the
+ * caller, which merges failing boundaries and replays again).
+ * job_info[3i..3i+2] = status bits, segment records, reseats.              */
+int intf_form_batches(const intf_batch *batch, const intf_replay_buffers *buf, void *stream);
+int intf_replay_jobs(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf,
+                     const int32_t *job_scen, const int32_t *job_lo, const int32_t *job_hi, int32_t n_jobs,
+                     double *job_last_done, int32_t *job_info, void *stream);
+
 /* Per-(scenario, model) SLO report (`metrics.py:49-79`, nearest-rank
  * `percentile` `:28-36`) plus per-request slo_met (`simcore.py:268-277`).
  * warm_cutoff: device [n_scen] arrival-time cutoff or NULL (no warm-up trim).

@@ -77,6 +77,8 @@ SIGNATURES = {
     "intf_generate_arrivals": (c_int32, [P, P, P]),
     "intf_split_arrivals": (c_int32, [P, P, P]),
     "intf_replay": (c_int32, [P, P, P, P]),
+    "intf_form_batches": (c_int32, [P, P, P]),
+    "intf_replay_jobs": (c_int32, [P, P, P, P, P, P, c_int32, P, P, P]),
     "intf_slo_report": (c_int32, [P, P, P, P, P, P, P]),
     "intf_features_predict": (c_int32, [P, P, P, P, c_int32, c_int64, P, P, P, P]),
     "intf_candidate_count": (c_int32, [c_int32, c_int32, P, P, P]),

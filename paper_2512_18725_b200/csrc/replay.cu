@@ -127,7 +127,51 @@ __global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_warp(const intf
   const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
   const int s = blockIdx.x * kReplayWarps * (32 / kReplayW) + g;
   if (s >= n_scen) return;
-  replay_group<kReplayW>(s, scen, models, tab, B, sseg[g]);
+  const int st0 = B.status[s];
+  if (st0 & (INTF_ST_CAP | INTF_ST_OVERFLOW)) return;
+  const intf_scenario& S = scen[s];
+  const ReplayJob J{s, 0, B.n_batches[s], S.seg_off, S.seg_cap, s};
+  const ReplayJobOut r = replay_group<kReplayW>(J, scen, models, tab, B, sseg[g], st0);
+  if ((threadIdx.x & (kReplayW - 1)) == 0) {
+    B.n_segments[s] = r.n_segments;
+    B.n_reseats[s] = r.n_reseats;
+    B.status[s] = r.status;
+  }
+}
+
+// ---- K2': busy-period segments of long traces.  Job i replays
+// batches [lo[i], hi[i]) of scenario sc[i] from an idle GPU; its segment
+// records go to S.seg_off + lo*(2cap-1) (a disjoint slice: a batch has at
+// most 2cap-1 reseats), its outcome order to positions [lo, hi).
+__global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_jobs(const intf_scenario* __restrict__ scen,
+                                                                    const intf_model* __restrict__ models,
+                                                                    intf_table tab, intf_replay_buffers B,
+                                                                    const int32_t* __restrict__ sc,
+                                                                    const int32_t* __restrict__ lo,
+                                                                    const int32_t* __restrict__ hi, int n_jobs,
+                                                                    double* __restrict__ last_done,
+                                                                    int32_t* __restrict__ info) {
+  __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
+  const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
+  const int i = blockIdx.x * kReplayWarps * (32 / kReplayW) + g;
+  if (i >= n_jobs) return;
+  const int s = sc[i];
+  const int st0 = B.status[s];
+  const bool lead = (threadIdx.x & (kReplayW - 1)) == 0;
+  if (st0 & (INTF_ST_CAP | INTF_ST_OVERFLOW)) {
+    if (lead) info[3 * i] = st0;
+    return;
+  }
+  const intf_scenario& S = scen[s];
+  const int per = 2 * S.cap - 1;
+  const ReplayJob J{s, lo[i], hi[i], S.seg_off + lo[i] * per, (hi[i] - lo[i]) * per, i};
+  const ReplayJobOut r = replay_group<kReplayW>(J, scen, models, tab, B, sseg[g], 0);
+  if (lead) {
+    info[3 * i] = r.status;
+    info[3 * i + 1] = r.n_segments;
+    info[3 * i + 2] = r.n_reseats;
+    last_done[i] = r.last_done;
+  }
 }
 
 // ---- K3: SLO records + per-model nearest-rank percentiles, one block per
@@ -309,6 +353,36 @@ int intf_split_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, vo
   cudaMemsetAsync(buf->status, 0, sizeof(int32_t) * bt->n_scen, st);
   k_split_arrivals<<<ceil_div(bt->n_scen, 64), 64, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
   return launch_status("k_split_arrivals");
+}
+
+int intf_form_batches(const intf_batch* bt, const intf_replay_buffers* buf, void* stream) {
+  if (!bt || !bt->scen || !bt->models || !buf || bt->n_scen <= 0) return bad_input("intf_form_batches: null argument");
+  if (buf->noise_k > 0 && (!buf->noise_tab || bt->n_scen > 65535))
+    return bad_input("intf_form_batches: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
+  cudaStream_t st = as_stream(stream);
+  int rc;
+  k_form<32><<<ceil_div(bt->n_scen, kFormWarps), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
+  if ((rc = launch_status("k_form"))) return rc;
+  if (buf->noise_k > 0 && bt->max_req_cap > 0) {
+    dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
+    k_noise_table<<<grid, 128, 0, st>>>(bt->scen, *buf);
+    if ((rc = launch_status("k_noise_table"))) return rc;
+  }
+  return INTF_OK;
+}
+
+int intf_replay_jobs(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
+                     const int32_t* job_scen, const int32_t* job_lo, const int32_t* job_hi, int32_t n_jobs,
+                     double* job_last_done, int32_t* job_info, void* stream) {
+  if (!bt || !bt->scen || !bt->models || !buf || !table || !job_scen || !job_lo || !job_hi || !job_last_done ||
+      !job_info || n_jobs < 0)
+    return bad_input("intf_replay_jobs: null argument");
+  if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1)
+    return bad_input("intf_replay_jobs: cap_max must be in [1, 8], seg_stride >= 1");
+  if (n_jobs == 0) return INTF_OK;
+  k_replay_jobs<<<ceil_div(n_jobs, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, as_stream(stream)>>>(
+      bt->scen, bt->models, *table, *buf, job_scen, job_lo, job_hi, n_jobs, job_last_done, job_info);
+  return launch_status("k_replay_jobs");
 }
 
 int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf, void* stream) {

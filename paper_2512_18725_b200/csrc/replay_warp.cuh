@@ -57,20 +57,30 @@ struct LaneGroup {
   __device__ __forceinline__ unsigned reduce_or(unsigned v) const { return __reduce_or_sync(mask, v); }
 };
 
+// One replay job: batches [b_lo, b_hi) of scenario s, started from an idle
+// GPU, writing segments into [seg_base, seg_base + seg_cap) and using scratch
+// slot `scratch`.  The whole-scenario replay is the job [0, n_batches).
+struct ReplayJob {
+  int s, b_lo, b_hi, seg_base, seg_cap, scratch;
+};
+struct ReplayJobOut {
+  int status, n_segments, n_reseats;
+  double last_done;
+};
+
 // sseg: this group's shared-memory segment history, [kMaxCap][kSmemSeg][5]
 template <int W>
-__device__ __forceinline__ void replay_group(int s, const intf_scenario* __restrict__ scens,
-                                             const intf_model* __restrict__ models, const intf_table tab,
-                                             const intf_replay_buffers B, double* sseg) {
+__device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const intf_scenario* __restrict__ scens,
+                                                     const intf_model* __restrict__ models, const intf_table tab,
+                                                     const intf_replay_buffers B, double* sseg, int status) {
   const LaneGroup<W> G;
   const int lane = G.lane;
+  const int s = J.s;
   const intf_scenario& S = scens[s];
-  int status = B.status[s];
-  if (status & (INTF_ST_CAP | INTF_ST_OVERFLOW)) return;
-  const int cap = S.cap, nb = B.n_batches[s], ro = S.req_off;
+  const int cap = S.cap, nb = J.b_hi, ro = S.req_off;
   const intf_model* md = models + S.model_off;
   const int K = B.noise_k < kWarpNoiseK ? B.noise_k : kWarpNoiseK;
-  double* myseg = B.slot_seg + ((size_t)s * B.cap_max + lane) * (size_t)B.seg_stride * 5;
+  double* myseg = B.slot_seg + ((size_t)J.scratch * B.cap_max + lane) * (size_t)B.seg_stride * 5;
 
   // ---- per-lane slot state (valid while `act`)
   bool act = false;
@@ -83,14 +93,14 @@ __device__ __forceinline__ void replay_group(int s, const intf_scenario* __restr
   int nrun = 0;
   unsigned freemask = (cap >= 32) ? 0xffffffffu : ((1u << cap) - 1u);
   double now = 0.0;
-  int n_formed = 0, dq = 0, n_done = 0, seg_cursor = 0, n_reseats = 0;
+  int n_formed = J.b_lo, dq = J.b_lo, n_done = J.b_lo, seg_cursor = 0, n_reseats = 0;
   double last_done = -INFINITY;  // completion time of the latest outcome
 
   // formation-time window: lane l holds b_formed of batch fbase + l
-  int fbase = 0;
-  double wf = lane < nb ? B.b_formed[ro + lane] : 0.0;
+  int fbase = J.b_lo;
+  double wf = fbase + lane < nb ? B.b_formed[ro + fbase + lane] : 0.0;
   // dispatch window: lane l holds model/size/noise of batch dbase + l
-  int dbase = 0, wm = 0, wsz = 0;
+  int dbase = J.b_lo, wm = 0, wsz = 0;
   double wn0 = 1.0, wn1 = 1.0, wn2 = 1.0, wn3 = 1.0;
   auto load_dispatch_window = [&](int base) {
     const int b = base + lane;
@@ -104,7 +114,7 @@ __device__ __forceinline__ void replay_group(int s, const intf_scenario* __restr
       wn3 = K > 3 ? nt[3] : 1.0;
     }
   };
-  load_dispatch_window(0);
+  load_dispatch_window(J.b_lo);
 
   // reseat of this lane's batch at `now` (`simcore.py:133-141`); every lane of
   // the group calls it together (group-uniform shuffles inside)
@@ -192,11 +202,11 @@ __device__ __forceinline__ void replay_group(int s, const intf_scenario* __restr
         B.b_completion[ro + batch] = now;
         B.b_measured[ro + batch] = measured;
         nseg_c = nseg < B.seg_stride ? nseg : B.seg_stride;
-        if (seg_cursor + nseg_c > S.seg_cap) {
+        if (seg_cursor + nseg_c > J.seg_cap) {
           status |= INTF_ST_OVERFLOW;
           nseg_c = 0;
         }
-        off = S.seg_off + seg_cursor;
+        off = J.seg_base + seg_cursor;
         B.b_seg_off[ro + batch] = off;
         B.b_nseg[ro + batch] = nseg_c;
         act = false;
@@ -205,7 +215,7 @@ __device__ __forceinline__ void replay_group(int s, const intf_scenario* __restr
       nseg_c = G.shfl(nseg_c, cl);
       off = G.shfl(off, cl);
       // lanes copy the completed batch's segments (segment k <- lane k mod W)
-      const double* cseg = B.slot_seg + ((size_t)s * B.cap_max + cl) * (size_t)B.seg_stride * 5;
+      const double* cseg = B.slot_seg + ((size_t)J.scratch * B.cap_max + cl) * (size_t)B.seg_stride * 5;
       const double* csm = sseg + cl * kSmemSeg * 5;
       for (int k = lane; k < nseg_c; k += W) {
         const double* p = k < kSmemSeg ? csm + k * 5 : cseg + (size_t)k * 5;
@@ -224,7 +234,7 @@ __device__ __forceinline__ void replay_group(int s, const intf_scenario* __restr
         B.out_order[ro + n_done] = bmin;  // strictly later than every earlier outcome
       } else if (lane == 0) {
         int pos = n_done;
-        while (pos > 0) {
+        while (pos > J.b_lo) {
           const int prev = B.out_order[ro + pos - 1];
           if (B.b_completion[ro + prev] == now && prev > bmin) {
             B.out_order[ro + pos] = prev;
@@ -296,12 +306,12 @@ __device__ __forceinline__ void replay_group(int s, const intf_scenario* __restr
     }
   }
   if (nrun || dq < n_formed) status |= INTF_ST_NONQUIESCENT;
-  status = (int)G.reduce_or((unsigned)status);
-  if (lane == 0) {
-    B.n_segments[s] = seg_cursor;
-    B.n_reseats[s] = n_reseats;
-    B.status[s] = status;
-  }
+  ReplayJobOut r;
+  r.status = (int)G.reduce_or((unsigned)status);
+  r.n_segments = seg_cursor;
+  r.n_reseats = n_reseats;
+  r.last_done = last_done;
+  return r;
 }
 
 // ---------------------------------------------------------------------------

@@ -521,3 +521,111 @@ def rng_stream(words, n: int, uniform: bool = False) -> np.ndarray:
     _abi.check(_abi.load().intf_rng_stream(w.data_ptr(), w.numel(), n, int(uniform), out.data_ptr(), stream_ptr()),
                "intf_rng_stream")
     return out.cpu().numpy()[:n]
+
+
+# ------------------------------------------------------ busy-period sharding
+def _candidate_jobs(formed, dur, slow: float, min_len: int):
+    """Split one scenario's batch sequence at likely idle points: a batch
+    starts a job if it forms after every earlier batch's optimistic end
+    formed + slow*solo (cumulative max).  Only a speculation -- the replay
+    verifies each boundary exactly."""
+    n = len(formed)
+    if n == 0:
+        return [0]
+    end = np.maximum.accumulate(formed + slow * dur)
+    cut = np.nonzero(formed[1:] > end[:-1])[0] + 1
+    starts = [0]
+    for c in cut.tolist():
+        if c - starts[-1] >= min_len:
+            starts.append(c)
+    return starts
+
+
+def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 64, max_iters: int = 100000,
+                     arrivals: bool = True, slo: bool = True, features: bool = True) -> dict:
+    """Busy-period sharding of long traces: replay every
+    scenario as parallel jobs split at speculated idle points, verify each
+    boundary (previous job's last completion <= next job's first formation),
+    merge failing boundaries and replay again until every boundary holds.
+    Results are identical to the serial replay.  Returns statistics."""
+    L, st = pipe.lib, stream_ptr()
+    bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
+    if arrivals:
+        _abi.check(L.intf_generate_arrivals(bt, B, st), "intf_generate_arrivals")
+    else:
+        _abi.check(L.intf_split_arrivals(bt, B, st), "intf_split_arrivals")
+    _abi.check(L.intf_form_batches(bt, B, st), "intf_form_batches")
+    nb = pipe.t["n_batches"][: pipe.pb.n_scen].cpu().numpy()
+    formed_all = pipe.t["b_formed"].cpu().numpy()
+    bmod = pipe.t["b_model"].cpu().numpy()
+    bsz = pipe.t["b_size"].cpu().numpy()
+    solo = pipe.pb.table.solo
+    starts = []
+    for s in range(pipe.pb.n_scen):
+        S = pipe.pb.scen[s]
+        ro, n = S.req_off, int(nb[s])
+        base = np.array([pipe.pb.models[S.model_off + m].entry_base for m in range(S.n_models)], dtype=np.int64)
+        rows = base[bmod[ro:ro + n]] + bsz[ro:ro + n] - 1
+        starts.append(_candidate_jobs(formed_all[ro:ro + n], solo[rows] if n else np.zeros(0), slow, min_len))
+    # jobs: (scenario, lo, hi); dirty = needs (re)replay
+    jobs = {s: [[lo, hi, True] for lo, hi in zip(st_, st_[1:] + [int(nb[s])])] for s, st_ in enumerate(starts)}
+    n_initial = sum(len(v) for v in jobs.values())
+    need = max(n_initial, pipe.pb.n_scen) * pipe.pb.cap_max * pipe.seg_stride * 5
+    if pipe.t["slot_seg"].numel() < need:
+        pipe.t["slot_seg"] = torch.zeros(need, dtype=torch.float64, device=pipe.dev)
+        pipe.B.slot_seg = pipe.t["slot_seg"].data_ptr()
+    info_of = {}
+    iters = 0
+    for iters in range(1, max_iters + 1):
+        todo = [(s, j) for s, js in jobs.items() for j, (lo, hi, dirty) in enumerate(js) if dirty and hi > lo]
+        if todo:
+            sc = torch.tensor([s for s, _ in todo], dtype=torch.int32, device=pipe.dev)
+            lo = torch.tensor([jobs[s][j][0] for s, j in todo], dtype=torch.int32, device=pipe.dev)
+            hi = torch.tensor([jobs[s][j][1] for s, j in todo], dtype=torch.int32, device=pipe.dev)
+            last = torch.empty(len(todo), dtype=torch.float64, device=pipe.dev)
+            info = torch.empty(3 * len(todo), dtype=torch.int32, device=pipe.dev)
+            _abi.check(L.intf_replay_jobs(bt, ctypes.byref(pipe.dtable.struct), B, sc.data_ptr(), lo.data_ptr(),
+                                          hi.data_ptr(), len(todo), last.data_ptr(), info.data_ptr(), st),
+                       "intf_replay_jobs")
+            lh, ih = last.cpu().numpy(), info.cpu().numpy().reshape(-1, 3)
+            for k, (s, j) in enumerate(todo):
+                info_of[(s, jobs[s][j][0])] = (float(lh[k]), ih[k])
+                jobs[s][j][2] = False
+        # verify boundaries; merge each failing job into its predecessor
+        changed = False
+        for s, js in jobs.items():
+            S = pipe.pb.scen[s]
+            merged = [js[0]]
+            for lo_, hi_, _ in js[1:]:
+                prev = merged[-1]
+                if prev[2]:  # predecessor grew in this pass: re-verify after its replay
+                    merged.append([lo_, hi_, False])
+                    continue
+                last_prev = info_of[(s, prev[0])][0] if prev[1] > prev[0] else -np.inf
+                if hi_ > lo_ and not (last_prev <= formed_all[S.req_off + lo_]):
+                    prev[1] = hi_
+                    prev[2] = True
+                    changed = True
+                else:
+                    merged.append([lo_, hi_, False])
+            jobs[s] = merged
+        if not changed:
+            break
+    # per-scenario totals of the final jobs
+    n_seg = np.zeros(pipe.pb.n_scen, dtype=np.int32)
+    n_res = np.zeros(pipe.pb.n_scen, dtype=np.int32)
+    status = pipe.t["status"][: pipe.pb.n_scen].cpu().numpy().copy()
+    for s, js in jobs.items():
+        for lo_, hi_, _ in js:
+            if hi_ > lo_:
+                _, inf = info_of[(s, lo_)]
+                status[s] |= int(inf[0])
+                n_seg[s] += int(inf[1])
+                n_res[s] += int(inf[2])
+    pipe.t["n_segments"][: pipe.pb.n_scen].copy_(torch.from_numpy(n_seg))
+    pipe.t["n_reseats"][: pipe.pb.n_scen].copy_(torch.from_numpy(n_res))
+    pipe.t["status"][: pipe.pb.n_scen].copy_(torch.from_numpy(status))
+    pipe.run_slo_features(slo=slo, features=features)
+    n_final = sum(len(v) for v in jobs.values())
+    return {"jobs_initial": n_initial, "jobs_final": n_final, "iterations": iters,
+            "batches": int(nb.sum())}

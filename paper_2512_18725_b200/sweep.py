@@ -48,3 +48,26 @@ def table16():
         mix = tuple(float(v) for v in rng.uniform(0.2, 0.6, size=3))
         arch.append(Archetype(f"synth_{i:02d}", base, eff, mix))
     return gen_synthetic_profiles(arch, seed=0, max_batch_size=64), arch
+
+
+def c4_scenario(table16_, arch, n_requests: float = 1e6, rho: float = 0.5, seed: int = 1) -> dict:
+    """C4: one multi-tenant trace of ~n_requests over 16 models, bs <= 64, cap 4,
+    window 10-20 ms, sigma 0.05, oracle seed 1; heterogeneous per-model load
+    (total utilisation rho at bs 64) so that light models reach large
+    batches and the GPU has many busy periods."""
+    rng = np.random.default_rng([4, seed])
+    share = rng.uniform(0.5, 1.5, size=len(arch))
+    share = share / share.sum()
+    dep = []
+    for a, f in zip(arch, share):
+        solo64 = table16_.get(a.model_id, 64).solo_duration_ms
+        rate = rho * f * 64 / (solo64 / 1000.0)
+        dep.append({"model_id": a.model_id, "arrival_rate_rps": float(rate),
+                    "slo_ms": float(20.0 * table16_.get(a.model_id, 1).solo_duration_ms)})
+    total = sum(d["arrival_rate_rps"] for d in dep)
+    return {
+        "name": "c4", "duration_s": float(n_requests / total), "batching_window_ms": float(rng.uniform(10.0, 20.0)),
+        "max_batch_size": 64, "concurrency_cap": 4, "seed": seed, "colocation_mode": "static", "ewma_alpha": 1.0,
+        "oracle": {"beta_l2": 1.0, "beta_dram": 1.5, "beta_sm": 0.5, "noise_sigma": 0.05, "seed": 1},
+        "deployed": dep,
+    }
