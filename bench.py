@@ -229,6 +229,39 @@ def refit_secondary(a, stream, barrier, max_over_ranks, rank) -> dict:
     return out
 
 
+C4_REQUESTS = 1e6
+
+
+def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
+    """C4 shape: one 10^6-request, 16-model (bs <= 64, cap 4) trace replayed
+    with busy-period sharding (speculative idle boundaries, verified and
+    merged on the host between launches -- those gaps are inside the timed
+    region).  Each rank replays its own trace (weak scaling)."""
+    import torch
+    from paper_2512_18725_b200 import engine
+    from paper_2512_18725_b200.sweep import c4_scenario, table16
+
+    t16, arch = table16()
+    spec = c4_scenario(t16, arch, n_requests=C4_REQUESTS, seed=1 + rank)
+    ta = t16.arrays()
+    pipe = engine.ReplayPipeline([spec], ta, scale=1.2)
+    engine.replay_segmented(pipe)  # warm-up (also sizes the job scratch)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    stats = engine.replay_segmented(pipe)
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    n_req = int(pipe.t["n_req"][0].item())
+    st = int(pipe.t["status"][0].item())
+    return {"metric": "requests replayed/sec (single long trace)", "value": world * n_req / (ms / 1e3),
+            "unit": "requests/s", "ms_per_trace": ms, "requests": n_req, "status": st, **stats,
+            "workload": "C4: 16 models (6 default + 10 rng(123) archetypes), bs 1-64, cap 4, window U(10,20) ms, "
+                        "sigma 0.05, total rho 0.5 at bs 64; one trace per GPU; arrivals + formation + noise + "
+                        "busy-period-sharded replay + SLO + features"}
+
+
 def replay_stage_times(pipe, stream) -> dict:
     """One extra (untimed) pass of the replay pipeline with events between
     its launches: per-stage device time in ms."""
@@ -401,6 +434,7 @@ def product_arm(a):
     n_req = int(pipe.t["n_req"][: pipe.pb.n_scen].sum().item())
 
     refit = refit_secondary(a, stream, barrier, max_over_ranks, rank)
+    longtrace = c4_secondary(a, stream, barrier, max_over_ranks, rank, world) if not a.no_c4 else None
     clk = clocks.stop()
 
     # ---- CPU baseline (rank 0, N=1 only): oracle port on a bounded sample
@@ -453,6 +487,7 @@ def product_arm(a):
                                "replay + SLO + features/3 predictors", "launches_per_step": 5,
                    "stage_ms": stage_ms},
         "refit": refit,
+        "long_trace": longtrace,
     }
     if rank == 0:
         print(json.dumps(line))
@@ -469,6 +504,7 @@ def main():
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 long-trace secondary measurement")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the multi-rank plumbing with ranks sharing GPUs (numbers meaningless)")
     a = ap.parse_args()

@@ -106,6 +106,9 @@ typedef struct intf_replay_buffers {
   int32_t *n_batches, *n_segments, *n_reseats, *status; /* [n_scen] */
   double *slot_seg;            /* scratch: n_scen*cap_max*seg_stride*5 doubles */
   double *noise_tab;           /* scratch: [req slots][noise_k] precomputed noise draws */
+  double *mb_t;                /* scratch, per-model list slots: formation time of the model's c-th batch */
+  int32_t *mb_info;            /* scratch, 4 per list slot: kind, key, size, head (list index of first member) */
+  int32_t *n_mb;               /* scratch: [total models] batches formed per model */
   int32_t seg_stride, cap_max;
   int32_t noise_k, pad_;       /* segments per batch whose noise is precomputed (0 = inline) */
 } intf_replay_buffers;

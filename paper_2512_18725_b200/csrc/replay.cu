@@ -89,17 +89,63 @@ __global__ void k_split_arrivals(const intf_scenario* __restrict__ scen, int n_s
   B.status[s] |= st;
 }
 
-// ---- K1: batch formation, one W-lane group per scenario (no GPU state, no
-// RNG).  W = 32 is used: packing four 8-lane groups per warp measured no
-// faster (the warp waits for its slowest scenario).
-constexpr int kFormWarps = 4;
-template <int W>
-__global__ void __launch_bounds__(32 * kFormWarps) k_form(const intf_scenario* __restrict__ scen, int n_scen,
-                                                          const intf_model* __restrict__ models,
-                                                          intf_replay_buffers B) {
-  const int s = (blockIdx.x * kFormWarps + (threadIdx.x >> 5)) * (32 / W) + ((threadIdx.x & 31) / W);
+// ---- K1 (per model): formation of every deployed model's batch list, one
+// warp per model; then a block per model ranks its batches among all the
+// scenario's batches by the heap key (time, kind, key) -> global batch ids.
+constexpr int kFormModelWarps = 4;
+__global__ void __launch_bounds__(32 * kFormModelWarps) k_form_models(const intf_scenario* __restrict__ scen,
+                                                                      const intf_model* __restrict__ models,
+                                                                      int n_models_total, intf_replay_buffers B) {
+  const int g = blockIdx.x * kFormModelWarps + (threadIdx.x >> 5);
+  if (g >= n_models_total) return;
+  const intf_model& M = models[g];
+  const intf_scenario& S = scen[M.scen];
+  const bool bad = (B.status[M.scen] & INTF_ST_OVERFLOW) || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 ||
+                   S.max_bs < 1 || S.n_models > kMaxModels;
+  if (bad) {
+    if ((threadIdx.x & 31) == 0) B.n_mb[g] = 0;
+    return;
+  }
+  form_model_warp(S, M, min(B.n_list[g], M.list_cap), B, g);
+}
+
+__global__ void k_merge_batches(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                                intf_replay_buffers B) {
+  const int g = blockIdx.x;
+  const intf_model& M = models[g];
+  const intf_scenario& S = scen[M.scen];
+  const int n = B.n_mb[g];
+  const int mloc = g - S.model_off;
+  if (threadIdx.x == 0 && n) atomicAdd(&B.n_batches[M.scen], n);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double t = B.mb_t[M.list_off + j];
+    const int32_t* info = B.mb_info + 4ll * (M.list_off + j);
+    const int kind = info[0], cnt = info[2], head = info[3];
+    const uint32_t key = (uint32_t)info[1];
+    int rank = j;
+    for (int q = 0; q < S.n_models; q++) {
+      const int gq = S.model_off + q;
+      if (gq == g) continue;
+      const intf_model& Q = models[gq];
+      rank += count_form_before(B.mb_t + Q.list_off, B.mb_info + 4ll * Q.list_off, B.n_mb[gq], t, kind, key);
+    }
+    const int ro = S.req_off;
+    B.b_model[ro + rank] = mloc;
+    B.b_size[ro + rank] = cnt;
+    B.b_formed[ro + rank] = t;
+    const int32_t* lrid = B.list_rid + M.list_off;
+    for (int k = 0; k < cnt; k++) B.r_batch[ro + lrid[head + k]] = rank;
+  }
+}
+
+// scenarios whose configuration the replay cannot run are flagged INTF_ST_CAP
+__global__ void k_form_status(const intf_scenario* __restrict__ scen, int n_scen, intf_replay_buffers B) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_scen) return;
-  form_group<W>(s, scen, models, B);
+  const intf_scenario& S = scen[s];
+  if (B.status[s] & INTF_ST_OVERFLOW) return;
+  if (S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 || S.max_bs < 1 || S.n_models > kMaxModels)
+    B.status[s] |= INTF_ST_CAP;
 }
 
 // ---- K1b: noise draws of the first noise_k segments of every formed batch
@@ -329,6 +375,20 @@ __global__ void k_features(const intf_scenario* __restrict__ scen, const intf_mo
   }
 }
 
+int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaStream_t st) {
+  if (!buf->mb_t || !buf->mb_info || !buf->n_mb) return bad_input("formation scratch (mb_t, mb_info, n_mb) missing");
+  int rc;
+  cudaMemsetAsync(buf->n_batches, 0, sizeof(int32_t) * bt->n_scen, st);
+  k_form_status<<<ceil_div(bt->n_scen, 128), 128, 0, st>>>(bt->scen, bt->n_scen, *buf);
+  if ((rc = launch_status("k_form_status"))) return rc;
+  if (bt->n_models <= 0) return INTF_OK;
+  k_form_models<<<ceil_div(bt->n_models, kFormModelWarps), 32 * kFormModelWarps, 0, st>>>(bt->scen, bt->models,
+                                                                                         bt->n_models, *buf);
+  if ((rc = launch_status("k_form_models"))) return rc;
+  k_merge_batches<<<bt->n_models, 128, 0, st>>>(bt->scen, bt->models, *buf);
+  return launch_status("k_merge_batches");
+}
+
 }  // namespace
 
 extern "C" {
@@ -361,8 +421,7 @@ int intf_form_batches(const intf_batch* bt, const intf_replay_buffers* buf, void
     return bad_input("intf_form_batches: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
   cudaStream_t st = as_stream(stream);
   int rc;
-  k_form<32><<<ceil_div(bt->n_scen, kFormWarps), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
-  if ((rc = launch_status("k_form"))) return rc;
+  if ((rc = launch_formation(bt, buf, st))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
     dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
     k_noise_table<<<grid, 128, 0, st>>>(bt->scen, *buf);
@@ -393,8 +452,7 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
     return bad_input("intf_replay: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
   cudaStream_t st = as_stream(stream);
   int rc;
-  k_form<32><<<ceil_div(bt->n_scen, kFormWarps), 32 * kFormWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
-  if ((rc = launch_status("k_form"))) return rc;
+  if ((rc = launch_formation(bt, buf, st))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
     dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
     k_noise_table<<<grid, 128, 0, st>>>(bt->scen, *buf);

@@ -3,8 +3,8 @@
 // replay_formed() / form_scenario() in replay_core.cuh (which remain the
 // readable, host-checkable statements).
 //
-// A scenario is mapped to a group of W lanes (W = 8: four scenarios per warp,
-// or W = 32), every collective is masked to the group:
+// A replay job is mapped to a group of W lanes (W = 32 in use; W = 8 packs
+// four jobs per warp), every collective is masked to the group:
 //   * replay: lane l < cap owns running slot l in registers; the running
 //     (dispatch) order is a group-uniform list of 4-bit lane ids, so each lane
 //     computes its colo sum ((0 + p1) + p2).. in list order from shuffles and
@@ -16,8 +16,9 @@
 //   * formation times, and the model/size/first noise draws of the batches
 //     about to be dispatched, stream through W-batch register windows
 //     refilled by coalesced loads, keeping global latency off the chain;
-//   * formation: lane m holds model m's pending event, the next batch is the
-//     (time, kind, key) min over lanes, the window-member count is a ballot.
+//   * formation: a warp per deployed model walks its arrival list (window
+//     membership by ballot); a rank-merge on the heap key (time, kind, key)
+//     assigns the scenario's global batch ids.
 #pragma once
 #include "replay_core.cuh"
 
@@ -315,12 +316,9 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
 }
 
 // ---------------------------------------------------------------------------
-// Lane-group batch formation (same result as form_scenario()): lane m holds
-// model m's pending formation event (time, kind, key, count); the next batch
-// is the lexicographic (time, kind, key) min over lanes (heap order,
-// `simcore.py:98-100,122`); its next event is recomputed cooperatively -- the
-// window membership test t < D is monotone along the sorted list, so the
-// member count is a ballot popcount.
+// A model's next formation event from list index h, computed by a lane group:
+// the window membership test t < D is monotone along the sorted list, so the
+// member count is a ballot popcount (same result as next_formation()).
 template <int W>
 __device__ __forceinline__ void group_next_formation(const LaneGroup<W>& G, const double* lt, const int32_t* lrid,
                                                      int n, int h, double window, int max_bs, uint32_t crc,
@@ -353,100 +351,53 @@ __device__ __forceinline__ void group_next_formation(const LaneGroup<W>& G, cons
   }
 }
 
-template <int W>
-__device__ __forceinline__ void form_group(int s, const intf_scenario* __restrict__ scens,
-                                           const intf_model* __restrict__ models, const intf_replay_buffers B) {
-  const LaneGroup<W> G;
-  const int lane = G.lane;
-  const intf_scenario& S = scens[s];
-  const int M = S.n_models;
-  if ((B.status[s] & INTF_ST_OVERFLOW) || M > W || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 ||
-      S.max_bs < 1) {
-    if (lane == 0) {
-      if (!(B.status[s] & INTF_ST_OVERFLOW)) B.status[s] = INTF_ST_CAP;
-      B.n_batches[s] = 0;
-    }
-    return;
-  }
-  const intf_model* md = models + S.model_off;
-  // lane m: model m's list and pending event
-  const bool has = lane < M;
-  const int lo = has ? md[lane].list_off : 0;
-  const int ln = has ? B.n_list[S.model_off + lane] : 0;
-  const uint32_t crc = has ? md[lane].crc : 0u;
-  int head = 0;
-  double et = 0.0;
-  int ekind = 0, ecnt = 0;
-  uint32_t ekey = 0;
-  for (int m = 0; m < M; m++) {  // initial events, computed cooperatively
+// ---------------------------------------------------------------------------
+// Per-model formation (warp per deployed model): a model's batch sequence
+// depends only on its own arrivals and window, so every
+// model forms its batches in parallel into per-model lists of
+// (time, kind, key) + (count, head).  A rank-merge then orders all batches
+// of a scenario exactly as the reference heap pops formation events.
+__device__ __forceinline__ void form_model_warp(const intf_scenario& S, const intf_model& Md, int n_list,
+                                                const intf_replay_buffers& B, int g) {
+  const LaneGroup<32> G;
+  const double* lt = B.list_t + Md.list_off;
+  const int32_t* lrid = B.list_rid + Md.list_off;
+  int h = 0, c = 0;
+  for (;;) {
     double t;
     int kind, cnt;
     uint32_t key;
-    const int lom = G.shfl(lo, m), lnm = G.shfl(ln, m);
-    const uint32_t crm = G.shfl(crc, m);
-    group_next_formation<W>(G, B.list_t + lom, B.list_rid + lom, lnm, 0, S.window_ms, S.max_bs, crm, t, kind, key,
-                            cnt);
-    if (lane == m) {
-      et = t;
-      ekind = kind;
-      ekey = key;
-      ecnt = cnt;
+    group_next_formation<32>(G, lt, lrid, n_list, h, S.window_ms, S.max_bs, Md.crc, t, kind, key, cnt);
+    if (!kind) break;
+    if (G.lane == 0) {
+      B.mb_t[Md.list_off + c] = t;
+      int32_t* info = B.mb_info + 4ll * (Md.list_off + c);
+      info[0] = kind;
+      info[1] = (int32_t)key;
+      info[2] = cnt;
+      info[3] = h;
     }
+    h += cnt;
+    c++;
   }
-  const int ro = S.req_off;
-  int n_formed = 0;
-  int red_hi = 1;  // models live in lanes [0, M): log2(M) butterfly rounds
-  while (red_hi < M) red_hi <<= 1;
-  red_hi >>= 1;
-  for (;;) {
-    // (time, kind, key) min over lanes with a pending event
-    double bt = ekind ? et : INFINITY;
-    int bk = ekind ? ekind : 3;
-    uint32_t bkey = ekind ? ekey : 0xffffffffu;
-    int bm = lane;
-    for (int o = red_hi; o > 0; o >>= 1) {
-      const double t2 = G.shfl_xor(bt, o);
-      const int k2 = G.shfl_xor(bk, o);
-      const uint32_t y2 = G.shfl_xor(bkey, o);
-      const int m2 = G.shfl_xor(bm, o);
-      const bool less = t2 < bt || (t2 == bt && (k2 < bk || (k2 == bk && (y2 < bkey || (y2 == bkey && m2 < bm)))));
-      if (less) {
-        bt = t2;
-        bk = k2;
-        bkey = y2;
-        bm = m2;
-      }
-    }
-    bt = G.shfl(bt, 0);
-    bk = G.shfl(bk, 0);
-    bm = G.shfl(bm, 0);
-    if (bk == 3) break;
-    const int fm = bm;
-    const int cnt = G.shfl(ecnt, fm);
-    const int h = G.shfl(head, fm);
-    const int lom = G.shfl(lo, fm), lnm = G.shfl(ln, fm);
-    const uint32_t crm = G.shfl(crc, fm);
-    const int b = n_formed++;
-    if (lane == 0) {
-      B.b_model[ro + b] = fm;
-      B.b_size[ro + b] = cnt;
-      B.b_formed[ro + b] = bt;
-    }
-    for (int j = lane; j < cnt; j += W) B.r_batch[ro + B.list_rid[lom + h + j]] = b;
-    double t;
-    int kind, c2;
-    uint32_t key;
-    group_next_formation<W>(G, B.list_t + lom, B.list_rid + lom, lnm, h + cnt, S.window_ms, S.max_bs, crm, t, kind,
-                            key, c2);
-    if (lane == fm) {
-      head = h + cnt;
-      et = t;
-      ekind = kind;
-      ekey = key;
-      ecnt = c2;
-    }
+  if (G.lane == 0) B.n_mb[g] = c;
+}
+
+// lexicographic heap key of a formation event
+__device__ __forceinline__ bool form_key_less(double t1, int k1, uint32_t y1, double t2, int k2, uint32_t y2) {
+  return t1 < t2 || (t1 == t2 && (k1 < k2 || (k1 == k2 && y1 < y2)));
+}
+
+// number of batches in a per-model list that precede (t, kind, key)
+__device__ __forceinline__ int count_form_before(const double* mt, const int32_t* mi, int n, double t, int kind,
+                                                 uint32_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (form_key_less(mt[mid], mi[4 * mid], (uint32_t)mi[4 * mid + 1], t, kind, key)) lo = mid + 1;
+    else hi = mid;
   }
-  if (lane == 0) B.n_batches[s] = n_formed;
+  return lo;
 }
 
 // ---------------------------------------------------------------------------

@@ -225,7 +225,7 @@ def _warm_cutoffs(pipe: ReplayPipeline, frac: float):
 
 # ---------------------------------------------------------------- array ops
 def _f64(a, dev, shape=None):
-    t = torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64))
+    t = torch.from_numpy(np.array(a, dtype=np.float64, copy=True))
     if shape is not None:
         t = t.reshape(shape)
     return t.to(dev)

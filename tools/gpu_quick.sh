@@ -8,6 +8,6 @@ timeout 900 python -m pytest tests -q -m gpu > $OUT/pytest_gpu_$TAG.log 2>&1; ec
 timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
 for K in "$@"; do
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c 1 -o $OUT/prof_${TAG}_$K \
-    python bench.py --steps 3 --warmup 3 --no-cpu > $OUT/ncu_${TAG}_$K.log 2>&1
+    python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_${TAG}_$K.log 2>&1
 done
 echo done
