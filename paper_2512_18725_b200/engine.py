@@ -524,30 +524,56 @@ def rng_stream(words, n: int, uniform: bool = False) -> np.ndarray:
 
 
 # ------------------------------------------------------ busy-period sharding
-def _candidate_jobs(formed, dur, slow: float, min_len: int):
-    """Split one scenario's batch sequence at likely idle points: a batch
-    starts a job if it forms after every earlier batch's optimistic end
-    formed + slow*solo (cumulative max).  Only a speculation -- the replay
-    verifies each boundary exactly."""
-    n = len(formed)
-    if n == 0:
-        return [0]
-    end = np.maximum.accumulate(formed + slow * dur)
-    cut = np.nonzero(formed[1:] > end[:-1])[0] + 1
-    starts = [0]
-    for c in cut.tolist():
-        if c - starts[-1] >= min_len:
-            starts.append(c)
-    return starts
+def _candidate_starts(pipe, nb, formed_all, bmod, bsz, slow: float, min_len: int):
+    """Speculative job starts for every scenario (vectorised): batch b starts
+    a job if it forms after every earlier batch's optimistic end
+    formed + slow * solo (running max within its scenario) and the job before
+    it has at least min_len batches.  Only a speculation -- the replay
+    verifies each boundary exactly.  Returns (scen, lo) arrays, sorted."""
+    S_n = pipe.pb.n_scen
+    req_off = np.array([pipe.pb.scen[s].req_off for s in range(S_n)], dtype=np.int64)
+    nbv = nb.astype(np.int64)
+    tot = int(nbv.sum())
+    if tot == 0:
+        return np.arange(S_n, dtype=np.int32), np.zeros(S_n, dtype=np.int32)
+    scen = np.repeat(np.arange(S_n), nbv)
+    local = np.arange(tot) - np.repeat(np.cumsum(nbv) - nbv, nbv)
+    slot = req_off[scen] + local
+    mbase = np.array([pipe.pb.models[g].entry_base for g in range(max(pipe.pb.n_models, 1))], dtype=np.int64)
+    moff = np.array([pipe.pb.scen[s].model_off for s in range(S_n)], dtype=np.int64)
+    rows = mbase[moff[scen] + bmod[slot]] + bsz[slot] - 1
+    f = formed_all[slot]
+    end = f + slow * pipe.pb.table.solo[rows]
+    # running max of `end` restricted to each scenario: offset scenarios apart
+    big = (np.abs(end).max() + np.abs(f).max() + 1.0) * 4.0
+    cm = np.maximum.accumulate(end + scen * big) - scen * big
+    cand = np.zeros(tot, dtype=bool)
+    cand[1:] = (f[1:] > cm[:-1]) & (scen[1:] == scen[:-1])
+    first = local == 0
+    starts = first | cand
+    idx = np.nonzero(starts)[0]
+    if min_len > 1 and len(idx) > 1:
+        # keep scenario starts and candidates at least min_len batches after the previous candidate
+        gap = np.diff(idx, prepend=-(10 ** 12))
+        idx = idx[(local[idx] == 0) | (gap >= min_len)]
+    js, jl = scen[idx].astype(np.int32), local[idx].astype(np.int32)
+    # scenarios without batches still get one (empty) job
+    empty = np.nonzero(nbv == 0)[0]
+    if len(empty):
+        js = np.concatenate([js, empty.astype(np.int32)])
+        jl = np.concatenate([jl, np.zeros(len(empty), dtype=np.int32)])
+        o = np.lexsort((jl, js))
+        js, jl = js[o], jl[o]
+    return js, jl
 
 
 def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 64, max_iters: int = 100000,
                      arrivals: bool = True, slo: bool = True, features: bool = True) -> dict:
-    """Busy-period sharding of long traces: replay every
-    scenario as parallel jobs split at speculated idle points, verify each
-    boundary (previous job's last completion <= next job's first formation),
-    merge failing boundaries and replay again until every boundary holds.
-    Results are identical to the serial replay.  Returns statistics."""
+    """Busy-period sharding: replay every scenario as parallel
+    jobs split at speculated idle points, verify every boundary (previous
+    job's last completion <= next job's first formation), remove the failing
+    ones and replay the merged jobs again until all boundaries hold.  The
+    result is identical to the serial replay.  Returns statistics."""
     L, st = pipe.lib, stream_ptr()
     bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
     if arrivals:
@@ -559,73 +585,64 @@ def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 6
     formed_all = pipe.t["b_formed"].cpu().numpy()
     bmod = pipe.t["b_model"].cpu().numpy()
     bsz = pipe.t["b_size"].cpu().numpy()
-    solo = pipe.pb.table.solo
-    starts = []
-    for s in range(pipe.pb.n_scen):
-        S = pipe.pb.scen[s]
-        ro, n = S.req_off, int(nb[s])
-        base = np.array([pipe.pb.models[S.model_off + m].entry_base for m in range(S.n_models)], dtype=np.int64)
-        rows = base[bmod[ro:ro + n]] + bsz[ro:ro + n] - 1
-        starts.append(_candidate_jobs(formed_all[ro:ro + n], solo[rows] if n else np.zeros(0), slow, min_len))
-    # jobs: (scenario, lo, hi); dirty = needs (re)replay
-    jobs = {s: [[lo, hi, True] for lo, hi in zip(st_, st_[1:] + [int(nb[s])])] for s, st_ in enumerate(starts)}
-    n_initial = sum(len(v) for v in jobs.values())
+    js, jl = _candidate_starts(pipe, nb, formed_all, bmod, bsz, slow, min_len)
+    req_off = np.array([pipe.pb.scen[s].req_off for s in range(pipe.pb.n_scen)], dtype=np.int64)
+
+    def ends(js, jl):
+        nxt_same = np.zeros(len(js), dtype=bool)
+        nxt_same[:-1] = js[1:] == js[:-1]
+        jh = np.where(nxt_same, np.roll(jl, -1), nb[js]).astype(np.int32)
+        return jh
+
+    jh = ends(js, jl)
+    n_initial = len(js)
     need = max(n_initial, pipe.pb.n_scen) * pipe.pb.cap_max * pipe.seg_stride * 5
     if pipe.t["slot_seg"].numel() < need:
         pipe.t["slot_seg"] = torch.zeros(need, dtype=torch.float64, device=pipe.dev)
         pipe.B.slot_seg = pipe.t["slot_seg"].data_ptr()
-    info_of = {}
+    last = np.full(len(js), -np.inf)
+    info = np.zeros((len(js), 3), dtype=np.int32)
+    dirty = np.ones(len(js), dtype=bool)
     iters = 0
     for iters in range(1, max_iters + 1):
-        todo = [(s, j) for s, js in jobs.items() for j, (lo, hi, dirty) in enumerate(js) if dirty and hi > lo]
-        if todo:
-            sc = torch.tensor([s for s, _ in todo], dtype=torch.int32, device=pipe.dev)
-            lo = torch.tensor([jobs[s][j][0] for s, j in todo], dtype=torch.int32, device=pipe.dev)
-            hi = torch.tensor([jobs[s][j][1] for s, j in todo], dtype=torch.int32, device=pipe.dev)
-            last = torch.empty(len(todo), dtype=torch.float64, device=pipe.dev)
-            info = torch.empty(3 * len(todo), dtype=torch.int32, device=pipe.dev)
-            _abi.check(L.intf_replay_jobs(bt, ctypes.byref(pipe.dtable.struct), B, sc.data_ptr(), lo.data_ptr(),
-                                          hi.data_ptr(), len(todo), last.data_ptr(), info.data_ptr(), st),
+        todo = np.nonzero(dirty & (jh > jl))[0]
+        if len(todo):
+            d_sc = torch.from_numpy(js[todo].copy()).to(pipe.dev)
+            d_lo = torch.from_numpy(jl[todo].copy()).to(pipe.dev)
+            d_hi = torch.from_numpy(jh[todo].copy()).to(pipe.dev)
+            d_last = torch.empty(len(todo), dtype=torch.float64, device=pipe.dev)
+            d_info = torch.empty(3 * len(todo), dtype=torch.int32, device=pipe.dev)
+            _abi.check(L.intf_replay_jobs(bt, ctypes.byref(pipe.dtable.struct), B, d_sc.data_ptr(), d_lo.data_ptr(),
+                                          d_hi.data_ptr(), len(todo), d_last.data_ptr(), d_info.data_ptr(), st),
                        "intf_replay_jobs")
-            lh, ih = last.cpu().numpy(), info.cpu().numpy().reshape(-1, 3)
-            for k, (s, j) in enumerate(todo):
-                info_of[(s, jobs[s][j][0])] = (float(lh[k]), ih[k])
-                jobs[s][j][2] = False
-        # verify boundaries; merge each failing job into its predecessor
-        changed = False
-        for s, js in jobs.items():
-            S = pipe.pb.scen[s]
-            merged = [js[0]]
-            for lo_, hi_, _ in js[1:]:
-                prev = merged[-1]
-                if prev[2]:  # predecessor grew in this pass: re-verify after its replay
-                    merged.append([lo_, hi_, False])
-                    continue
-                last_prev = info_of[(s, prev[0])][0] if prev[1] > prev[0] else -np.inf
-                if hi_ > lo_ and not (last_prev <= formed_all[S.req_off + lo_]):
-                    prev[1] = hi_
-                    prev[2] = True
-                    changed = True
-                else:
-                    merged.append([lo_, hi_, False])
-            jobs[s] = merged
-        if not changed:
+            last[todo] = d_last.cpu().numpy()
+            info[todo] = d_info.cpu().numpy().reshape(-1, 3)
+        dirty[:] = False
+        # verify: boundary i (same scenario as i-1) holds iff last[i-1] <= formed(first batch of i)
+        same = np.zeros(len(js), dtype=bool)
+        same[1:] = js[1:] == js[:-1]
+        prev_last = np.concatenate([[-np.inf], last[:-1]])
+        ok = ~same | (jh <= jl) | (prev_last <= formed_all[req_off[js] + jl])
+        if ok.all():
             break
+        # drop failing boundaries; jobs that absorbed one are replayed again
+        keep = ok
+        grp = np.cumsum(keep) - 1
+        absorbed = np.zeros(int(keep.sum()), dtype=bool)
+        np.logical_or.at(absorbed, grp[~keep], True)
+        js, jl = js[keep], jl[keep]
+        jh = ends(js, jl)
+        last, info = last[keep], info[keep]
+        dirty = absorbed
     # per-scenario totals of the final jobs
-    n_seg = np.zeros(pipe.pb.n_scen, dtype=np.int32)
-    n_res = np.zeros(pipe.pb.n_scen, dtype=np.int32)
-    status = pipe.t["status"][: pipe.pb.n_scen].cpu().numpy().copy()
-    for s, js in jobs.items():
-        for lo_, hi_, _ in js:
-            if hi_ > lo_:
-                _, inf = info_of[(s, lo_)]
-                status[s] |= int(inf[0])
-                n_seg[s] += int(inf[1])
-                n_res[s] += int(inf[2])
-    pipe.t["n_segments"][: pipe.pb.n_scen].copy_(torch.from_numpy(n_seg))
-    pipe.t["n_reseats"][: pipe.pb.n_scen].copy_(torch.from_numpy(n_res))
-    pipe.t["status"][: pipe.pb.n_scen].copy_(torch.from_numpy(status))
+    S_n = pipe.pb.n_scen
+    live = jh > jl
+    status = pipe.t["status"][:S_n].cpu().numpy().copy()
+    np.bitwise_or.at(status, js[live], info[live, 0])
+    n_seg = np.bincount(js[live], weights=info[live, 1], minlength=S_n).astype(np.int32)
+    n_res = np.bincount(js[live], weights=info[live, 2], minlength=S_n).astype(np.int32)
+    pipe.t["n_segments"][:S_n].copy_(torch.from_numpy(n_seg))
+    pipe.t["n_reseats"][:S_n].copy_(torch.from_numpy(n_res))
+    pipe.t["status"][:S_n].copy_(torch.from_numpy(status))
     pipe.run_slo_features(slo=slo, features=features)
-    n_final = sum(len(v) for v in jobs.values())
-    return {"jobs_initial": n_initial, "jobs_final": n_final, "iterations": iters,
-            "batches": int(nb.sum())}
+    return {"jobs_initial": n_initial, "jobs_final": int(len(js)), "iterations": iters, "batches": int(nb.sum())}

@@ -49,3 +49,26 @@ def test_long_trace_segmented_equals_serial():
     for k in ("s_tbegin", "s_tend", "s_slowdown"):
         assert np.array_equal(a[k][ia], b[k][ib]), k
     assert np.array_equal(a["slo_p"], b["slo_p"]) and a["n_reseats"] == b["n_reseats"]
+
+
+def test_sweep_segmented_equals_whole_scenario_jobs():
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200 import engine
+    from paper_2512_18725_b200.sweep import c5_scenarios
+
+    table = p.gen_synthetic_profiles()
+    specs = c5_scenarios(table, 256)
+    ta = table.arrays()
+    a_pipe = engine.ReplayPipeline(specs, ta, scale=1.5)
+    stats = engine.replay_segmented(a_pipe, min_len=8)
+    ha = a_pipe.fetch()
+    b_pipe = engine.ReplayPipeline(specs, ta, scale=1.5)
+    b_pipe.run()
+    hb = b_pipe.fetch()
+    assert stats["jobs_final"] > len(specs)
+    for s in range(len(specs)):
+        a, b = a_pipe.scenario(ha, s), b_pipe.scenario(hb, s)
+        assert a["status"] == 0 and b["status"] == 0
+        for k in ("order", "b_start", "b_completion", "b_measured", "b_nseg", "r_slo_met", "slo_p", "slo_met"):
+            assert np.array_equal(a[k], b[k]), (s, k)
+        assert a["n_reseats"] == b["n_reseats"]
