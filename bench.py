@@ -419,27 +419,19 @@ def product_arm(a):
     pipe = engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5)
     for _ in range(max(1, a.warmup)):
         pipe.run()
-        seg_stats = engine.replay_segmented(pipe, min_len=16)
     barrier()
     st = pipe.status()
     r_steps = max(1, min(a.steps, 5))
-    # (a) whole-scenario jobs: one warp replays each scenario start to end
+    # one warp replays each scenario start to end (C5 scenarios are short:
+    # busy-period sharding pays only for long traces, see long_trace)
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     r0.record(stream)
     for _ in range(r_steps):
         pipe.run()
     r1.record(stream)
     barrier()
-    rep_ms_serial = max_over_ranks(r0.elapsed_time(r1)) / r_steps
-    stage_ms = replay_stage_times(pipe, stream)
-    # (b) busy-period sharded: every scenario split at verified idle points
-    r0.record(stream)
-    for _ in range(r_steps):
-        seg_stats = engine.replay_segmented(pipe, min_len=16)
-    r1.record(stream)
-    barrier()
     rep_ms = max_over_ranks(r0.elapsed_time(r1)) / r_steps
-    st = st | pipe.status()
+    stage_ms = replay_stage_times(pipe, stream)
     n_batches = int(pipe.t["n_batches"][: pipe.pb.n_scen].sum().item())
     n_req = int(pipe.t["n_req"][: pipe.pb.n_scen].sum().item())
 
@@ -494,10 +486,8 @@ def product_arm(a):
                    "unit": "replays/s", "ms_per_step": rep_ms, "scenarios_per_gpu": REPLAY_SCEN,
                    "requests": n_req, "batches": n_batches, "status_nonzero": int(np.count_nonzero(st)),
                    "workload": "C5-shape synthetic scenarios (default_rng([2512,i]), 1 s, cap 1-3): arrivals + "
-                               "formation + noise + busy-period-sharded replay (host verify/merge between launches, "
-                               "inside the timed region) + SLO + features/3 predictors",
-                   "ms_per_step_whole_scenario_jobs": rep_ms_serial, "segmented": seg_stats,
-                   "stage_ms_whole_scenario_jobs": stage_ms},
+                               "formation + noise + replay (warp per scenario) + SLO + features/3 predictors",
+                   "stage_ms": stage_ms},
         "refit": refit,
         "long_trace": longtrace,
     }

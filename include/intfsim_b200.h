@@ -85,6 +85,8 @@ typedef struct intf_batch {
   int32_t max_models;          /* max over scenarios of n_models */
 } intf_batch;
 
+#define INTF_SLO_WS_INTS (256 + 32 * 3 * 256 + 32 * 3 * 4)
+
 /* Device buffers of the replay pipeline.  Index spaces:
  *   request / batch / outcome slot: req_off + i   (i < req_cap)
  *   per-model list:                 list_off + j  (j < list_cap)
@@ -109,6 +111,7 @@ typedef struct intf_replay_buffers {
   double *mb_t;                /* scratch, per-model list slots: formation time of the model's c-th batch */
   int32_t *mb_info;            /* scratch, 4 per list slot: kind, key, size, head (list index of first member) */
   int32_t *n_mb;               /* scratch: [total models] batches formed per model */
+  int32_t *slo_ws;             /* scratch: INTF_SLO_WS_INTS int32 for the grid-wide SLO path (long traces) */
   int32_t seg_stride, cap_max;
   int32_t noise_k, pad_;       /* segments per batch whose noise is precomputed (0 = inline) */
 } intf_replay_buffers;

@@ -54,8 +54,9 @@ REPLAY_BUFFER_FIELDS = [
     "b_model", "b_size", "b_formed", "b_start", "b_completion", "b_measured", "b_seg_off", "b_nseg",
     "out_order", "r_batch", "r_slo_met",
     "s_tbegin", "s_tend", "s_slowdown", "s_colo",
-    "n_batches", "n_segments", "n_reseats", "status", "slot_seg", "noise_tab", "mb_t", "mb_info", "n_mb",
+    "n_batches", "n_segments", "n_reseats", "status", "slot_seg", "noise_tab", "mb_t", "mb_info", "n_mb", "slo_ws",
 ]
+SLO_WS_INTS = 256 + 32 * 3 * 256 + 32 * 3 * 4
 
 
 class ReplayBuffers(ctypes.Structure):

@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_jobs(const intf
 // (latency >= 0, so IEEE bit order == numeric order); three order
 // statistics per model share each pass's histograms (shared memory).
 constexpr int kSloThreads = 256;
-constexpr int kSloGroup = 8;  // models per radix pass group
+constexpr int kSloGroup = 8;          // models per radix pass group
+constexpr int kSloBigReq = 1 << 16;  // above this request capacity: grid-wide SLO passes
 
 __device__ __forceinline__ unsigned long long lat_key(double v) {
   unsigned long long u = (unsigned long long)__double_as_longlong(v);
@@ -340,6 +341,114 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
     }
     __syncthreads();
   }
+}
+
+// ---- K3 (large scenarios): the same report with grid-wide passes and global
+// histograms, for scenarios too big for one block (long traces, C4).
+// ws layout (int32 units): [0,64) n/met with cutoff, [64,128) n/met without,
+// [128] use_all, then hist [32][3][256] (u32), prefix [32][3] (u64, 8-aligned),
+// left [32][3] (i64).
+constexpr int kSloWsHist = 256;
+constexpr int kSloWsPrefix = kSloWsHist + kMaxModels * 3 * 256;
+constexpr int kSloWsLeft = kSloWsPrefix + kMaxModels * 3 * 2;
+constexpr int kSloWsInts = kSloWsLeft + kMaxModels * 3 * 2;
+static_assert(kSloWsInts == INTF_SLO_WS_INTS, "slo_ws size mismatch with the header");
+
+__global__ void k_slo_big_count(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                                intf_replay_buffers B, int s, const double* __restrict__ warm_cutoff,
+                                int32_t* __restrict__ ws) {
+  const intf_scenario& S = scen[s];
+  const int n = B.n_req[s], ro = S.req_off;
+  const double cutoff = warm_cutoff ? warm_cutoff[s] : -INFINITY;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int b = B.r_batch[ro + i];
+    const double at = B.arr_t[ro + i];
+    const int m = B.arr_model[ro + i];
+    const bool met = (B.b_completion[ro + b] - at) <= models[S.model_off + m].slo_ms;
+    B.r_slo_met[ro + i] = met;
+    atomicAdd(&ws[64 + 2 * m], 1);
+    if (met) atomicAdd(&ws[64 + 2 * m + 1], 1);
+    if (at >= cutoff) {
+      atomicAdd(&ws[2 * m], 1);
+      if (met) atomicAdd(&ws[2 * m + 1], 1);
+    }
+  }
+}
+
+__global__ void k_slo_big_init(const intf_scenario* __restrict__ scen, int s, int32_t* __restrict__ ws,
+                               int32_t* out_n, int32_t* out_met) {
+  const intf_scenario& S = scen[s];
+  __shared__ int use_all;
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int m = 0; m < S.n_models; m++) tot += ws[2 * m];
+    int all = 0;
+    for (int m = 0; m < S.n_models; m++) all += ws[64 + 2 * m];
+    use_all = tot == 0 && all > 0;  // `metrics.py:67`: trimmed or records
+    ws[128] = use_all;
+  }
+  __syncthreads();
+  const double pq[3] = {50.0, 95.0, 99.0};
+  unsigned long long* prefix = reinterpret_cast<unsigned long long*>(ws + kSloWsPrefix);
+  long long* left = reinterpret_cast<long long*>(ws + kSloWsLeft);
+  for (int t = threadIdx.x; t < S.n_models * 3; t += blockDim.x) {
+    const int m = t / 3, q = t % 3;
+    const int nm = ws[(use_all ? 64 : 0) + 2 * m];
+    long long rk = (long long)ceil((pq[q] / 100.0) * (double)nm);
+    left[t] = (rk < 1 ? 1 : rk) - 1;
+    prefix[t] = 0ull;
+    if (q == 0) {
+      out_n[S.model_off + m] = nm;
+      out_met[S.model_off + m] = ws[(use_all ? 64 : 0) + 2 * m + 1];
+    }
+  }
+  for (int t = threadIdx.x; t < kMaxModels * 3 * 256; t += blockDim.x) ws[kSloWsHist + t] = 0;
+}
+
+__global__ void k_slo_big_hist(const intf_scenario* __restrict__ scen, intf_replay_buffers B, int s, int pass,
+                               const double* __restrict__ warm_cutoff, int32_t* __restrict__ ws) {
+  const intf_scenario& S = scen[s];
+  const int n = B.n_req[s], ro = S.req_off;
+  const double cutoff = (warm_cutoff && !ws[128]) ? warm_cutoff[s] : -INFINITY;
+  const int shift = 56 - 8 * pass;
+  const unsigned long long* prefix = reinterpret_cast<const unsigned long long*>(ws + kSloWsPrefix);
+  unsigned int* hist = reinterpret_cast<unsigned int*>(ws + kSloWsHist);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double at = B.arr_t[ro + i];
+    if (!(at >= cutoff)) continue;
+    const int m = B.arr_model[ro + i];
+    const unsigned long long key = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
+    const unsigned d = (unsigned)(key >> shift) & 0xffu;
+#pragma unroll
+    for (int q = 0; q < 3; q++)
+      if (pass == 0 || ((key ^ prefix[m * 3 + q]) >> (shift + 8)) == 0ull) atomicAdd(&hist[(m * 3 + q) * 256 + d], 1u);
+  }
+}
+
+__global__ void k_slo_big_select(const intf_scenario* __restrict__ scen, int s, int pass, int32_t* __restrict__ ws,
+                                 double* out_p) {
+  const intf_scenario& S = scen[s];
+  const int shift = 56 - 8 * pass;
+  unsigned long long* prefix = reinterpret_cast<unsigned long long*>(ws + kSloWsPrefix);
+  long long* left = reinterpret_cast<long long*>(ws + kSloWsLeft);
+  unsigned int* hist = reinterpret_cast<unsigned int*>(ws + kSloWsHist);
+  for (int t = threadIdx.x; t < S.n_models * 3; t += blockDim.x) {
+    long long l = left[t];
+    unsigned d = 0;
+    for (; d < 255u; d++) {
+      if (l < (long long)hist[t * 256 + d]) break;
+      l -= hist[t * 256 + d];
+    }
+    left[t] = l;
+    prefix[t] |= (unsigned long long)d << shift;
+    if (pass == 7) {
+      const int m = t / 3;
+      const int nm = ws[(ws[128] ? 64 : 0) + 2 * m];
+      out_p[3 * (S.model_off + m) + t % 3] = nm ? key_lat(prefix[t]) : NAN;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kMaxModels * 3 * 256; t += blockDim.x) ws[kSloWsHist + t] = 0;
 }
 
 // ---- K4+K5: features + predictions per outcome; grid (chunks, scenarios).
@@ -467,6 +576,25 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
                     int32_t* out_met, double* out_p, void* stream) {
   if (!bt || !bt->scen || !bt->models || !buf || !out_n || !out_met || !out_p || bt->n_scen <= 0)
     return bad_input("intf_slo_report: null argument");
+  if (bt->max_req_cap > kSloBigReq) {  // long traces: grid-wide passes, one scenario at a time
+    if (!buf->slo_ws) return bad_input("intf_slo_report: large scenarios need slo_ws");
+    if (bt->max_models > kMaxModels) return bad_input("intf_slo_report: more than 32 models");
+    cudaStream_t st = as_stream(stream);
+    int rc;
+    for (int s = 0; s < bt->n_scen; s++) {
+      cudaMemsetAsync(buf->slo_ws, 0, sizeof(int32_t) * 256, st);
+      k_slo_big_count<<<4 * 148, 256, 0, st>>>(bt->scen, bt->models, *buf, s, warm_cutoff, buf->slo_ws);
+      if ((rc = launch_status("k_slo_big_count"))) return rc;
+      k_slo_big_init<<<1, 256, 0, st>>>(bt->scen, s, buf->slo_ws, out_n, out_met);
+      if ((rc = launch_status("k_slo_big_init"))) return rc;
+      for (int pass = 0; pass < 8; pass++) {
+        k_slo_big_hist<<<4 * 148, 256, 0, st>>>(bt->scen, *buf, s, pass, warm_cutoff, buf->slo_ws);
+        k_slo_big_select<<<1, 128, 0, st>>>(bt->scen, s, pass, buf->slo_ws, out_p);
+      }
+      if ((rc = launch_status("k_slo_big_select"))) return rc;
+    }
+    return INTF_OK;
+  }
   k_slo<<<bt->n_scen, kSloThreads, 0, as_stream(stream)>>>(bt->scen, bt->models, *buf, warm_cutoff, out_n, out_met,
                                                           out_p);
   return launch_status("k_slo");

@@ -553,9 +553,11 @@ def _candidate_starts(pipe, nb, formed_all, bmod, bsz, slow: float, min_len: int
     starts = first | cand
     idx = np.nonzero(starts)[0]
     if min_len > 1 and len(idx) > 1:
-        # keep scenario starts and candidates at least min_len batches after the previous candidate
-        gap = np.diff(idx, prepend=-(10 ** 12))
-        idx = idx[(local[idx] == 0) | (gap >= min_len)]
+        # thin to at most one candidate per min_len-batch bucket of a scenario (scenario starts always kept)
+        bucket = scen[idx].astype(np.int64) * (1 << 32) + local[idx] // min_len
+        first_in_bucket = np.ones(len(idx), dtype=bool)
+        first_in_bucket[1:] = bucket[1:] != bucket[:-1]
+        idx = idx[first_in_bucket | (local[idx] == 0)]
     js, jl = scen[idx].astype(np.int32), local[idx].astype(np.int32)
     # scenarios without batches still get one (empty) job
     empty = np.nonzero(nbv == 0)[0]
@@ -574,14 +576,20 @@ def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 6
     job's last completion <= next job's first formation), remove the failing
     ones and replay the merged jobs again until all boundaries hold.  The
     result is identical to the serial replay.  Returns statistics."""
+    import time
+
     L, st = pipe.lib, stream_ptr()
     bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
+    tm = {}
+    t0 = time.perf_counter()
     if arrivals:
         _abi.check(L.intf_generate_arrivals(bt, B, st), "intf_generate_arrivals")
     else:
         _abi.check(L.intf_split_arrivals(bt, B, st), "intf_split_arrivals")
     _abi.check(L.intf_form_batches(bt, B, st), "intf_form_batches")
     nb = pipe.t["n_batches"][: pipe.pb.n_scen].cpu().numpy()
+    tm["arrivals+formation"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     formed_all = pipe.t["b_formed"].cpu().numpy()
     bmod = pipe.t["b_model"].cpu().numpy()
     bsz = pipe.t["b_size"].cpu().numpy()
@@ -596,6 +604,8 @@ def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 6
 
     jh = ends(js, jl)
     n_initial = len(js)
+    tm["plan"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     need = max(n_initial, pipe.pb.n_scen) * pipe.pb.cap_max * pipe.seg_stride * 5
     if pipe.t["slot_seg"].numel() < need:
         pipe.t["slot_seg"] = torch.zeros(need, dtype=torch.float64, device=pipe.dev)
@@ -634,6 +644,9 @@ def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 6
         jh = ends(js, jl)
         last, info = last[keep], info[keep]
         dirty = absorbed
+    torch.cuda.synchronize()
+    tm["replay+verify"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     # per-scenario totals of the final jobs
     S_n = pipe.pb.n_scen
     live = jh > jl
@@ -645,4 +658,7 @@ def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 6
     pipe.t["n_reseats"][:S_n].copy_(torch.from_numpy(n_res))
     pipe.t["status"][:S_n].copy_(torch.from_numpy(status))
     pipe.run_slo_features(slo=slo, features=features)
-    return {"jobs_initial": n_initial, "jobs_final": int(len(js)), "iterations": iters, "batches": int(nb.sum())}
+    torch.cuda.synchronize()
+    tm["slo+features"] = time.perf_counter() - t0
+    return {"jobs_initial": n_initial, "jobs_final": int(len(js)), "iterations": iters, "batches": int(nb.sum()),
+            "host_wall_ms": {k: round(v * 1e3, 3) for k, v in tm.items()}}

@@ -49,6 +49,19 @@ def test_long_trace_segmented_equals_serial():
     for k in ("s_tbegin", "s_tend", "s_slowdown"):
         assert np.array_equal(a[k][ia], b[k][ib]), k
     assert np.array_equal(a["slo_p"], b["slo_p"]) and a["n_reseats"] == b["n_reseats"]
+    # against the CPU oracle (heap engine); the SLO report takes the grid-wide path here
+    import oracle as O
+
+    ref = O.run_scenario(spec, O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr))
+    assert np.array_equal(a["order"], ref["order"]) and np.array_equal(a["b_completion"], ref["b_completion"])
+    assert np.array_equal(a["r_slo_met"], ref["r_slo_met"])
+    ids = [d["model_id"] for d in spec["deployed"]]
+    rep = O.slo_report([ids[m] for m in ref["arr_model"]], ref["arr_t"], ref["b_completion"][ref["r_batch"]],
+                       ref["r_slo_met"])
+    for m, mid in enumerate(ids):
+        n, sat, p50, p95, p99 = rep[mid]
+        assert a["slo_n"][m] == n and a["slo_met"][m] / a["slo_n"][m] == sat
+        assert list(a["slo_p"][m]) == [p50, p95, p99]
 
 
 def test_sweep_segmented_equals_whole_scenario_jobs():
