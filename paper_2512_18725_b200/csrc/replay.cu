@@ -40,13 +40,13 @@ __global__ void __launch_bounds__(32 * kGenWarps) k_gen_arrivals(const intf_scen
 // model list.  Writes the merged arrays and each element's request id.
 __global__ void k_merge_arrivals(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
                                  intf_replay_buffers B) {
-  const int g = blockIdx.x;
+  const int g = blockIdx.y;
   const intf_model M = models[g];
   const intf_scenario S = scen[M.scen];
   const int n = min(B.n_list[g], M.list_cap);
   if (B.status[M.scen] & INTF_ST_OVERFLOW) return;
   const double* lt = B.list_t + M.list_off;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const double t = lt[j];
     int pos = j;
     for (int q = 0; q < S.n_models; q++) {
@@ -111,13 +111,13 @@ __global__ void __launch_bounds__(32 * kFormModelWarps) k_form_models(const intf
 
 __global__ void k_merge_batches(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
                                 intf_replay_buffers B) {
-  const int g = blockIdx.x;
+  const int g = blockIdx.y;
   const intf_model& M = models[g];
   const intf_scenario& S = scen[M.scen];
   const int n = B.n_mb[g];
   const int mloc = g - S.model_off;
-  if (threadIdx.x == 0 && n) atomicAdd(&B.n_batches[M.scen], n);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&B.n_batches[M.scen], n);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const double t = B.mb_t[M.list_off + j];
     const int32_t* info = B.mb_info + 4ll * (M.list_off + j);
     const int kind = info[0], cnt = info[2], head = info[3];
@@ -484,6 +484,14 @@ __global__ void k_features(const intf_scenario* __restrict__ scen, const intf_mo
   }
 }
 
+// (element chunks, models): enough blocks per model list that long traces use
+// every SM, one block per model for short ones; y is capped at 65535 models
+dim3 merge_grid(const intf_batch* bt) {
+  const long long per_model = bt->max_list_cap > 0 ? bt->max_list_cap : 1;
+  unsigned x = ceil_div(per_model, 256 * 4);
+  return dim3(x < 1 ? 1 : x, (unsigned)bt->n_models);
+}
+
 int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaStream_t st) {
   if (!buf->mb_t || !buf->mb_info || !buf->n_mb) return bad_input("formation scratch (mb_t, mb_info, n_mb) missing");
   int rc;
@@ -494,7 +502,7 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
   k_form_models<<<ceil_div(bt->n_models, kFormModelWarps), 32 * kFormModelWarps, 0, st>>>(bt->scen, bt->models,
                                                                                          bt->n_models, *buf);
   if ((rc = launch_status("k_form_models"))) return rc;
-  k_merge_batches<<<bt->n_models, 128, 0, st>>>(bt->scen, bt->models, *buf);
+  k_merge_batches<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf);
   return launch_status("k_merge_batches");
 }
 
@@ -512,7 +520,7 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
   k_gen_arrivals<<<ceil_div(bt->n_models, kGenWarps), 32 * kGenWarps, 0, st>>>(bt->scen, bt->models, bt->n_models,
                                                                                *buf);
   if ((rc = launch_status("k_gen_arrivals"))) return rc;
-  k_merge_arrivals<<<bt->n_models, 256, 0, st>>>(bt->scen, bt->models, *buf);
+  k_merge_arrivals<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf);
   return launch_status("k_merge_arrivals");
 }
 

@@ -44,7 +44,8 @@ def run(specs, table: _pack.TableArrays, seg_stride=64, preds=(), noise_k=3):
     thr = np.ascontiguousarray(table.thr, dtype=np.float64).reshape(-1)
     T = _abi.Table(solo.ctypes.data, thr.ctypes.data, len(solo), table.max_bs)
     bt = _abi.Batch(ctypes.addressof(pb.scen), ctypes.addressof(pb.models), pb.n_scen, pb.n_models, pb.max_req_cap,
-                    max((len(n) for n in pb.names), default=0))
+                    max((len(n) for n in pb.names), default=0),
+                    max((pb.models[g].list_cap for g in range(pb.n_models)), default=0), 0)
     lib().hc_run(ctypes.byref(bt), ctypes.byref(T), ctypes.byref(B), 1)
     out = {"pb": pb, "bufs": bufs}
     if preds:
