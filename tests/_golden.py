@@ -29,6 +29,11 @@ def table(name: str = "default"):
                        G[f"_table/{name}/thr"])
 
 
+def table_names():
+    G = replay()
+    return sorted({str(G[n + "/table"]) for n in G["_names"]})
+
+
 def scenario_names(table_name: str | None = None):
     G = replay()
     names = [str(n) for n in G["_names"]]

@@ -68,6 +68,17 @@ def table16():
     return gen_synthetic_profiles(arch, seed=0, max_batch_size=64), arch
 
 
+def table32():
+    """32 models (6 default + 26 from default_rng(321)), bs 1..16: the widest
+    deployment the kernels support (one lane per model)."""
+    rng = np.random.default_rng(321)
+    arch = list(DEFAULT_ARCHETYPES)
+    for i in range(26):
+        arch.append(Archetype(f"wide_{i:02d}", float(rng.uniform(0.8, 6.0)), float(rng.uniform(0.2, 0.95)),
+                              tuple(float(v) for v in rng.uniform(0.1, 0.5, size=3))))
+    return gen_synthetic_profiles(arch, seed=0, max_batch_size=16), arch
+
+
 def table_arrays(table):
     models = table.models()
     mbs = table.max_batch_size
@@ -132,11 +143,34 @@ def scenario_list(table, t16):
             "t16",
         )
     )
+    # edge shapes: widest cap, 32 deployed models, zero-rate models, sigma 0, near-empty traces
+    models = table.models()
+    out.append(("edge_cap8", ScenarioSpec(
+        deployed=tuple(DeployedModel(m, 150.0, default_slo_ms(table, m, 10.0)) for m in models), duration_s=0.8,
+        batching_window_ms=3.0, concurrency_cap=8, seed=11, oracle=InterferenceOracle(noise_sigma=0.05, seed=3),
+        name="edge_cap8"), "default"))
+    out.append(("edge_zero_rate", ScenarioSpec(
+        deployed=(DeployedModel("resnet50", 0.0, 10.0), DeployedModel("vgg19", 220.0, 40.0),
+                  DeployedModel("yolov8n", 0.0, 5.0), DeployedModel("vit_b16", 90.0, 30.0)), duration_s=1.0,
+        batching_window_ms=2.5, concurrency_cap=3, seed=5, oracle=InterferenceOracle(noise_sigma=0.1, seed=9),
+        name="edge_zero_rate"), "default"))
+    out.append(("edge_sigma0_cap4", ScenarioSpec(
+        deployed=tuple(DeployedModel(m, 120.0, default_slo_ms(table, m, 8.0)) for m in models[:4]), duration_s=1.0,
+        batching_window_ms=1.0, concurrency_cap=4, seed=2, oracle=InterferenceOracle(noise_sigma=0.0, seed=0),
+        name="edge_sigma0_cap4"), "default"))
+    out.append(("edge_tiny", ScenarioSpec(
+        deployed=(DeployedModel("roberta_b", 400.0, 30.0), DeployedModel("convnext_b", 300.0, 35.0)),
+        duration_s=0.004, batching_window_ms=0.5, concurrency_cap=2, seed=77, name="edge_tiny"), "default"))
+    t32, arch32 = table32()
+    out.append(("edge_wide32", ScenarioSpec(
+        deployed=tuple(DeployedModel(a.model_id, 40.0, 25 * t32.get(a.model_id, 1).solo_duration_ms) for a in arch32),
+        duration_s=0.6, batching_window_ms=6.0, max_batch_size=16, concurrency_cap=8, seed=21,
+        oracle=InterferenceOracle(noise_sigma=0.05, seed=2**40 + 7), name="edge_wide32"), "t32"))
     return out
 
 
 def replay_golden(table, t16):
-    tabs = {"default": table, "t16": t16[0]}
+    tabs = {"default": table, "t16": t16[0], "t32": table32()[0]}
     arrs = {}
     names = []
     for name, spec, tname in scenario_list(table, t16):

@@ -13,7 +13,7 @@ def gpu_runs():
     from paper_2512_18725_b200 import _abi, engine
 
     runs = {}
-    for tname in ("default", "t16"):
+    for tname in _golden.table_names():
         names = _golden.scenario_names(tname)
         preds = [_abi.Predictor(ewma=e, alpha=a, w=(0.1, -0.2, 0.3, 0.05, 0.4, -0.1, 1.0)) for e, a in _golden.MODES]
         pipe, h = engine.run_batch([_golden.spec(n) for n in names], _golden.table(tname), preds=preds)

@@ -19,7 +19,7 @@ def _run(specs, table, **kw):
 
 @pytest.mark.parametrize("slow,min_len", [(2.0, 64), (0.0, 1), (0.5, 4)])
 def test_segmented_replay_matches_goldens(slow, min_len):
-    for tname in ("default", "t16"):
+    for tname in _golden.table_names():
         names = _golden.scenario_names(tname)
         pipe, h, stats = _run([_golden.spec(n) for n in names], _golden.table(tname), slow=slow, min_len=min_len)
         for s, n in enumerate(names):

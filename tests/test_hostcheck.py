@@ -11,7 +11,7 @@ from tests.hostcheck import driver
 @pytest.fixture(scope="module")
 def runs():
     out = {}
-    for tname in ("default", "t16"):
+    for tname in _golden.table_names():
         names = _golden.scenario_names(tname)
         preds = []
         from paper_2512_18725_b200 import _abi
