@@ -104,6 +104,7 @@ typedef struct intf_replay_buffers {
   double *b_formed, *b_start, *b_completion, *b_measured;
   int32_t *b_seg_off, *b_nseg; /* absolute segment index, count */
   int32_t *out_order;          /* batch id of the k-th outcome, (completion, batch_id) order */
+  int32_t *b_running;          /* dispatch trace: running batches right after this batch's dispatch */
   int32_t *r_batch;            /* per request */
   uint8_t *r_slo_met;          /* per request (written by intf_slo_report) */
   double *s_tbegin, *s_tend, *s_slowdown, *s_colo; /* s_colo: [3*k] */

@@ -56,7 +56,7 @@ class ReplayOut(ctypes.Structure):
     _fields_ = [
         ("b_model", PI), ("b_size", PI), ("b_first_req", PI),
         ("b_formed", PD), ("b_start", PD), ("b_completion", PD), ("b_measured", PD), ("b_profiled", PD),
-        ("b_seg_off", PI), ("b_nseg", PI), ("b_done_rank", PI),
+        ("b_seg_off", PI), ("b_nseg", PI), ("b_done_rank", PI), ("b_running", PI),
         ("s_tbegin", PD), ("s_tend", PD), ("s_slowdown", PD), ("s_colo", PD),
         ("r_batch", PI), ("r_slo_met", ctypes.POINTER(ctypes.c_ubyte)),
         ("cap_batches", I), ("cap_segments", I),
@@ -204,7 +204,7 @@ def run_scenario(spec: dict, tab: TableArrays, arrivals=None) -> dict:
         ("b_model", np.int32, cap_b), ("b_size", np.int32, cap_b), ("b_first_req", np.int32, cap_b),
         ("b_formed", np.float64, cap_b), ("b_start", np.float64, cap_b), ("b_completion", np.float64, cap_b),
         ("b_measured", np.float64, cap_b), ("b_profiled", np.float64, cap_b), ("b_seg_off", np.int32, cap_b),
-        ("b_nseg", np.int32, cap_b), ("b_done_rank", np.int32, cap_b),
+        ("b_nseg", np.int32, cap_b), ("b_done_rank", np.int32, cap_b), ("b_running", np.int32, cap_b),
         ("s_tbegin", np.float64, cap_s), ("s_tend", np.float64, cap_s), ("s_slowdown", np.float64, cap_s),
         ("s_colo", np.float64, 3 * cap_s), ("r_batch", np.int32, max(n, 1)), ("r_slo_met", np.uint8, max(n, 1)),
     ]:

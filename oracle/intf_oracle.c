@@ -443,6 +443,7 @@ typedef struct {
   int *b_model, *b_size, *b_first_req; /* first member (arrival index) */
   double *b_formed, *b_start, *b_completion, *b_measured, *b_profiled;
   int *b_seg_off, *b_nseg, *b_done_rank;
+  int *b_running; /* running batches right after this batch's dispatch (the spy of `test_acceptance.py:98-106`) */
   /* per segment (grouped per batch, in completion order of batches) */
   double *s_tbegin, *s_tend, *s_slowdown, *s_colo; /* colo [n*3] */
   /* per request (arrival index) */
@@ -613,6 +614,7 @@ int oracle_run_scenario(const ScenarioIn *s, const double *arr_t, const int *arr
       rb->entry = s->entry_base[o->b_model[b]] + o->b_size[b] - 1;
       rb->start = S.now;
       rb->total = s->tab_solo[rb->entry];
+      o->b_running[b] = S.nrun;
       sim_reseat(&S, rb);
       for (int i = 0; i + 1 < S.nrun; i++) { sim_close(&S, &S.run[i]); sim_reseat(&S, &S.run[i]); }
     }

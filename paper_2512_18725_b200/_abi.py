@@ -52,7 +52,7 @@ class Batch(ctypes.Structure):
 REPLAY_BUFFER_FIELDS = [
     "arr_t", "arr_model", "list_t", "list_rid", "n_req", "n_list",
     "b_model", "b_size", "b_formed", "b_start", "b_completion", "b_measured", "b_seg_off", "b_nseg",
-    "out_order", "r_batch", "r_slo_met",
+    "out_order", "b_running", "r_batch", "r_slo_met",
     "s_tbegin", "s_tend", "s_slowdown", "s_colo",
     "n_batches", "n_segments", "n_reseats", "status", "slot_seg", "noise_tab", "mb_t", "mb_info", "n_mb", "slo_ws",
 ]

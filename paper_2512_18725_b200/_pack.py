@@ -131,6 +131,7 @@ BUFFER_PLAN = [
     ("b_model", np.int32, "req"), ("b_size", np.int32, "req"), ("b_formed", np.float64, "req"),
     ("b_start", np.float64, "req"), ("b_completion", np.float64, "req"), ("b_measured", np.float64, "req"),
     ("b_seg_off", np.int32, "req"), ("b_nseg", np.int32, "req"), ("out_order", np.int32, "req"),
+    ("b_running", np.int32, "req"),
     ("r_batch", np.int32, "req"), ("r_slo_met", np.uint8, "req"),
     ("s_tbegin", np.float64, "seg"), ("s_tend", np.float64, "seg"), ("s_slowdown", np.float64, "seg"),
     ("s_colo", np.float64, "seg3"),

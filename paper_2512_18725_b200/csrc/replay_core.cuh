@@ -337,6 +337,7 @@ INTF_FN void replay_formed(int s, const intf_scenario* scens, const intf_model* 
       rb.own[1] = tab.thr[3 * rb.entry + 1];
       rb.own[2] = tab.thr[3 * rb.entry + 2];
       run[nrun++] = si;
+      if (B.b_running) B.b_running[ro + b] = nrun;  // dispatch trace
       reseat(c, slots, run, nrun, si, now);
       for (int i = 0; i + 1 < nrun; i++) {
         close_segment(c, slots[run[i]], run[i], now);

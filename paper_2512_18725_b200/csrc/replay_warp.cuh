@@ -285,6 +285,7 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
       const bool was_act = act;
       if (lane == L) {
         const int entry = md[m].entry_base + sz - 1;
+        if (B.b_running) B.b_running[ro + b] = nrun;  // dispatch trace
         act = true;
         batch = b;
         start = now;

@@ -154,7 +154,7 @@ class ReplayPipeline:
         S = self.pb.scen[s]
         ro, n, nb = S.req_off, int(h["n_req"][s]), int(h["n_batches"][s])
         v = {k: h[k][ro:ro + nb] for k in ("b_model", "b_size", "b_formed", "b_start", "b_completion",
-                                             "b_measured", "b_seg_off", "b_nseg")}
+                                             "b_measured", "b_seg_off", "b_nseg", "b_running")}
         v["order"] = h["out_order"][ro:ro + nb]
         for k in ("r_batch", "r_slo_met", "arr_t", "arr_model"):
             v[k] = h[k][ro:ro + n]

@@ -66,3 +66,17 @@ def test_slo_report_matches_reference(gpu_runs):
                 assert v["slo_n"][m] == G[f"{name}/slo_n"][j]
                 assert v["slo_met"][m] / v["slo_n"][m] == G[f"{name}/slo_sat"][j]
                 np.testing.assert_array_equal(v["slo_p"][m], G[f"{name}/slo_p"][j], err_msg=f"{name} {mid}")
+
+
+def test_dispatch_trace_matches_oracle_and_cap(gpu_runs):
+    """Running-set size at every dispatch (the spy of `test_acceptance.py:98-106`,
+    `test_simcore.py:259-277`): equal to the heap-engine oracle's, never above cap."""
+    import oracle as O
+
+    for name, v in _views(gpu_runs):
+        spec = _golden.spec(name)
+        t = _golden.table(str(_golden.replay()[name + "/table"]))
+        ref = O.run_scenario(spec, O.TableArrays(t.models, t.max_bs, t.solo, t.thr))
+        assert np.array_equal(v["b_running"], ref["b_running"]), name
+        if len(v["b_running"]):
+            assert 1 <= v["b_running"].min() and v["b_running"].max() <= spec["concurrency_cap"]

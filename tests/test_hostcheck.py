@@ -33,6 +33,19 @@ def test_hostcheck_replay_bit_exact(runs):
     assert not bad, bad
 
 
+def test_hostcheck_dispatch_trace(runs):
+    import oracle as O
+
+    for tname, (names, res) in runs.items():
+        pb, b = res["pb"], res["bufs"]
+        for s, n in enumerate(names):
+            S = pb.scen[s]
+            nb = int(b["n_batches"][s])
+            t = _golden.table(tname)
+            ref = O.run_scenario(_golden.spec(n), O.TableArrays(t.models, t.max_bs, t.solo, t.thr))
+            assert np.array_equal(b["b_running"][S.req_off:S.req_off + nb], ref["b_running"]), n
+
+
 def test_hostcheck_features_bit_exact(runs):
     G = _golden.replay()
     for tname, (names, res) in runs.items():
