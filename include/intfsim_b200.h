@@ -154,6 +154,38 @@ int intf_replay_jobs(const intf_batch *batch, const intf_table *table, const int
                      const int32_t *job_scen, const int32_t *job_lo, const int32_t *job_hi, int32_t n_jobs,
                      double *job_last_done, int32_t *job_info, void *stream);
 
+/* Device-planned busy-period sharding.  Job slots of scenario s are
+ * [joff[s], joff[s] + jcap[s]) (host-planned capacities; planning keeps at
+ * most one job start per min_len batches, so jcap = ceil(req_cap/min_len)+1
+ * suffices).  intf_jobs_plan: speculative starts (a batch forming after every
+ * earlier batch's formed + slow*solo, prefix max per scenario), all jobs put
+ * on the todo list.  intf_jobs_replay: replays the todo list.
+ * intf_jobs_verify: per scenario, checks every boundary (previous job's last
+ * completion <= first formation), merges failing ones, puts merged jobs on a
+ * fresh todo list and, for scenarios whose boundaries all hold, writes the
+ * per-scenario totals (n_segments, n_reseats, status).  Host loop: plan; then
+ * while *todo_count: replay, reset count, verify.  The k-th todo entry of a
+ * replay call uses slot_seg scratch k (size it for *todo_count jobs).      */
+typedef struct intf_jobs {
+  int32_t *joff, *jcap;        /* [n_scen] slot offset / capacity */
+  int32_t *lo, *hi;            /* [slots] batch range of each job */
+  int32_t *n_jobs;             /* [n_scen] */
+  double *last;                /* [slots] last completion of the job's replay */
+  int32_t *info;               /* [slots][3] status, segment records, reseats */
+  uint8_t *dirty;              /* [slots] */
+  int32_t *todo;               /* [slots] slots to replay */
+  int32_t *todo_count;         /* [1] */
+  int32_t *slot_scen;          /* [slots] owning scenario of each slot (host-filled) */
+  double slow;                 /* optimism factor of the speculative end estimate */
+  int32_t min_len, total_slots;
+} intf_jobs;
+
+int intf_jobs_plan(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf,
+                   const intf_jobs *jobs, void *stream);
+int intf_jobs_replay(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf,
+                     const intf_jobs *jobs, int32_t n_todo, void *stream);
+int intf_jobs_verify(const intf_batch *batch, const intf_replay_buffers *buf, const intf_jobs *jobs, void *stream);
+
 /* Per-(scenario, model) SLO report (`metrics.py:49-79`, nearest-rank
  * `percentile` `:28-36`) plus per-request slo_met (`simcore.py:268-277`).
  * warm_cutoff: device [n_scen] arrival-time cutoff or NULL (no warm-up trim).

@@ -64,6 +64,12 @@ class ReplayBuffers(ctypes.Structure):
                                                           ("noise_k", c_int32), ("pad_", c_int32)]
 
 
+class Jobs(ctypes.Structure):
+    _fields_ = [(f, P) for f in ("joff", "jcap", "lo", "hi", "n_jobs", "last", "info", "dirty", "todo",
+                                 "todo_count", "slot_scen")] + [("slow", c_double), ("min_len", c_int32),
+                                                                ("total_slots", c_int32)]
+
+
 class Predictor(ctypes.Structure):
     _fields_ = [("ewma", c_int32), ("pad_", c_int32), ("alpha", c_double), ("w", c_double * 7)]
 
@@ -80,6 +86,9 @@ SIGNATURES = {
     "intf_replay": (c_int32, [P, P, P, P]),
     "intf_form_batches": (c_int32, [P, P, P]),
     "intf_replay_jobs": (c_int32, [P, P, P, P, P, P, c_int32, P, P, P]),
+    "intf_jobs_plan": (c_int32, [P, P, P, P, P]),
+    "intf_jobs_replay": (c_int32, [P, P, P, P, c_int32, P]),
+    "intf_jobs_verify": (c_int32, [P, P, P, P]),
     "intf_slo_report": (c_int32, [P, P, P, P, P, P, P]),
     "intf_features_predict": (c_int32, [P, P, P, P, c_int32, c_int64, P, P, P, P]),
     "intf_candidate_count": (c_int32, [c_int32, c_int32, P, P, P]),

@@ -220,6 +220,150 @@ __global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_jobs(const intf
   }
 }
 
+// ---- device-planned busy-period jobs (see intf_jobs in the header)
+__global__ void __launch_bounds__(128) k_jobs_plan(const intf_scenario* __restrict__ scen, int n_scen,
+                                                   const intf_model* __restrict__ models, intf_table tab,
+                                                   intf_replay_buffers B, intf_jobs J) {
+  const int s = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (s >= n_scen) return;
+  const LaneGroup<32> G;
+  const int lane = G.lane;
+  const intf_scenario& S = scen[s];
+  const int nb = B.n_batches[s], ro = S.req_off, joff = J.joff[s], jcap = J.jcap[s];
+  const intf_model* md = models + S.model_off;
+  const bool bad = (B.status[s] & (INTF_ST_CAP | INTF_ST_OVERFLOW)) != 0;
+  double carry = -INFINITY;  // max over earlier batches of formed + slow * solo
+  int nj = 0;
+  long long last_bucket = -1;
+  if (!bad && nb > 0) {
+    for (int base = 0; base < nb; base += 32) {
+      const int b = base + lane;
+      double f = 0.0, e = -INFINITY;
+      if (b < nb) {
+        f = B.b_formed[ro + b];
+        const int entry = md[B.b_model[ro + b]].entry_base + B.b_size[ro + b] - 1;
+        e = f + J.slow * tab.solo_ms[entry];
+      }
+      double incl = e;  // inclusive prefix max over the chunk (max is exact: order-free)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double v = G.shfl_up(incl, o);
+        if (lane >= o) incl = incl > v ? incl : v;
+      }
+      double excl = G.shfl_up(incl, 1);
+      if (lane == 0) excl = -INFINITY;
+      const double before = carry > excl ? carry : excl;
+      const bool cand = b < nb && (b == 0 || f > before);
+      unsigned m = G.ballot(cand);
+      while (m) {  // in batch order: one start per min_len bucket
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const int bb = base + l;
+        const long long bucket = bb / J.min_len;
+        if (bb == 0 || bucket != last_bucket) {
+          if (nj < jcap && lane == 0) J.lo[joff + nj] = bb;
+          nj += nj < jcap ? 1 : 0;
+          last_bucket = bucket;
+        }
+      }
+      const double tot = G.shfl(incl, 31);
+      carry = carry > tot ? carry : tot;
+    }
+  }
+  if (lane == 0) {
+    J.n_jobs[s] = nj;
+    for (int j = 0; j < nj; j++) {
+      J.hi[joff + j] = j + 1 < nj ? J.lo[joff + j + 1] : nb;
+      J.dirty[joff + j] = 1;
+      J.todo[atomicAdd(J.todo_count, 1)] = joff + j;
+    }
+    if (nj == 0) {  // nothing to replay: totals are zero
+      B.n_segments[s] = 0;
+      B.n_reseats[s] = 0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kReplayWarps, 4) k_jobs_replay(const intf_scenario* __restrict__ scen,
+                                                                    const intf_model* __restrict__ models,
+                                                                    intf_table tab, intf_replay_buffers B,
+                                                                    intf_jobs J, int n_todo) {
+  __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
+  const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
+  const int k = blockIdx.x * kReplayWarps * (32 / kReplayW) + g;
+  if (k >= n_todo) return;
+  const int slot = J.todo[k];
+  const int s = J.slot_scen[slot];
+  const intf_scenario& S = scen[s];
+  const int per = 2 * S.cap - 1;
+  const int jlo = J.lo[slot], jhi = J.hi[slot];
+  const ReplayJob RJ{s, jlo, jhi, S.seg_off + jlo * per, (jhi - jlo) * per, k};
+  const ReplayJobOut r = replay_group<kReplayW>(RJ, scen, models, tab, B, sseg[g], 0);
+  if ((threadIdx.x & (kReplayW - 1)) == 0) {
+    J.info[3 * slot] = r.status;
+    J.info[3 * slot + 1] = r.n_segments;
+    J.info[3 * slot + 2] = r.n_reseats;
+    J.last[slot] = r.last_done;
+    J.dirty[slot] = 0;
+  }
+}
+
+// one thread per scenario: check boundaries in order, merge failing jobs into
+// their predecessor (compacting the scenario's slots), queue merged jobs
+__global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen, intf_replay_buffers B,
+                              intf_jobs J) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_scen) return;
+  const intf_scenario& S = scen[s];
+  const int n = J.n_jobs[s], joff = J.joff[s], ro = S.req_off;
+  if (n == 0) return;
+  int w = 0;  // write cursor (kept jobs)
+  bool merged_prev = false, failed = false;
+  for (int j = 0; j < n; j++) {
+    const int sj = joff + j;
+    bool keep = true;
+    if (j > 0 && !merged_prev) {
+      const double prev_last = J.last[sj - 1];  // fresh: every job was replayed before this pass
+      keep = J.hi[sj] <= J.lo[sj] || prev_last <= B.b_formed[ro + J.lo[sj]];
+    }
+    if (keep) {
+      const int dw = joff + w;
+      if (dw != sj) {
+        J.lo[dw] = J.lo[sj];
+        J.hi[dw] = J.hi[sj];
+        J.last[dw] = J.last[sj];
+        J.info[3 * dw] = J.info[3 * sj];
+        J.info[3 * dw + 1] = J.info[3 * sj + 1];
+        J.info[3 * dw + 2] = J.info[3 * sj + 2];
+        J.dirty[dw] = 0;
+      }
+      w++;
+      merged_prev = false;
+    } else {  // boundary j fails: job j joins the previous kept job
+      const int dp = joff + w - 1;
+      J.hi[dp] = J.hi[sj];
+      J.dirty[dp] = 1;
+      merged_prev = true;
+      failed = true;
+    }
+  }
+  J.n_jobs[s] = w;
+  if (failed) {
+    for (int j = 0; j < w; j++)
+      if (J.dirty[joff + j]) J.todo[atomicAdd(J.todo_count, 1)] = joff + j;
+    return;
+  }
+  int st = B.status[s], segs = 0, res = 0;
+  for (int j = 0; j < w; j++) {
+    st |= J.info[3 * (joff + j)];
+    segs += J.info[3 * (joff + j) + 1];
+    res += J.info[3 * (joff + j) + 2];
+  }
+  B.status[s] = st;
+  B.n_segments[s] = segs;
+  B.n_reseats[s] = res;
+}
+
 // ---- K3: SLO records + per-model nearest-rank percentiles, one block per
 // scenario.  Percentiles by 8-pass MSB radix select on the latency bits
 // (latency >= 0, so IEEE bit order == numeric order); three order
@@ -559,6 +703,35 @@ int intf_replay_jobs(const intf_batch* bt, const intf_table* table, const intf_r
   k_replay_jobs<<<ceil_div(n_jobs, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, as_stream(stream)>>>(
       bt->scen, bt->models, *table, *buf, job_scen, job_lo, job_hi, n_jobs, job_last_done, job_info);
   return launch_status("k_replay_jobs");
+}
+
+int intf_jobs_plan(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf, const intf_jobs* jobs,
+                   void* stream) {
+  if (!bt || !bt->scen || !table || !buf || !jobs || !jobs->todo_count || jobs->min_len < 1)
+    return bad_input("intf_jobs_plan: bad argument");
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(jobs->todo_count, 0, sizeof(int32_t), st);
+  k_jobs_plan<<<ceil_div(bt->n_scen, 4), 128, 0, st>>>(bt->scen, bt->n_scen, bt->models, *table, *buf, *jobs);
+  return launch_status("k_jobs_plan");
+}
+
+int intf_jobs_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
+                     const intf_jobs* jobs, int32_t n_todo, void* stream) {
+  if (!bt || !bt->scen || !table || !buf || !jobs || n_todo < 0) return bad_input("intf_jobs_replay: bad argument");
+  if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1)
+    return bad_input("intf_jobs_replay: cap_max must be in [1, 8], seg_stride >= 1");
+  if (n_todo == 0) return INTF_OK;
+  k_jobs_replay<<<ceil_div(n_todo, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, as_stream(stream)>>>(
+      bt->scen, bt->models, *table, *buf, *jobs, n_todo);
+  return launch_status("k_jobs_replay");
+}
+
+int intf_jobs_verify(const intf_batch* bt, const intf_replay_buffers* buf, const intf_jobs* jobs, void* stream) {
+  if (!bt || !bt->scen || !buf || !jobs || !jobs->todo_count) return bad_input("intf_jobs_verify: bad argument");
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(jobs->todo_count, 0, sizeof(int32_t), st);
+  k_jobs_verify<<<ceil_div(bt->n_scen, 128), 128, 0, st>>>(bt->scen, bt->n_scen, *buf, *jobs);
+  return launch_status("k_jobs_verify");
 }
 
 int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf, void* stream) {

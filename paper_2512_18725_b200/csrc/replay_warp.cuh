@@ -48,6 +48,7 @@ struct LaneGroup {
   __device__ __forceinline__ int shfl(int v, int src) const { return __shfl_sync(mask, v, src, W); }
   __device__ __forceinline__ unsigned shfl(unsigned v, int src) const { return __shfl_sync(mask, v, src, W); }
   __device__ __forceinline__ double shfl_xor(double v, int o) const { return __shfl_xor_sync(mask, v, o, W); }
+  __device__ __forceinline__ double shfl_up(double v, int d) const { return __shfl_up_sync(mask, v, d, W); }
   __device__ __forceinline__ int shfl_xor(int v, int o) const { return __shfl_xor_sync(mask, v, o, W); }
   __device__ __forceinline__ unsigned shfl_xor(unsigned v, int o) const { return __shfl_xor_sync(mask, v, o, W); }
   __device__ __forceinline__ unsigned ballot(bool p) const {

@@ -570,8 +570,8 @@ def _candidate_starts(pipe, nb, formed_all, bmod, bsz, slow: float, min_len: int
     return js, jl
 
 
-def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 64, max_iters: int = 100000,
-                     arrivals: bool = True, slo: bool = True, features: bool = True) -> dict:
+def replay_segmented_host(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 64, max_iters: int = 100000,
+                          arrivals: bool = True, slo: bool = True, features: bool = True) -> dict:
     """Busy-period sharding: replay every scenario as parallel
     jobs split at speculated idle points, verify every boundary (previous
     job's last completion <= next job's first formation), remove the failing
@@ -663,3 +663,68 @@ def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 6
     tm["slo+features"] = time.perf_counter() - t0
     return {"jobs_initial": n_initial, "jobs_final": int(len(js)), "iterations": iters, "batches": int(nb.sum()),
             "host_wall_ms": {k: round(v * 1e3, 3) for k, v in tm.items()}}
+
+
+class _DeviceJobs:
+    """Job-slot buffers of the device-planned busy-period sharding."""
+
+    def __init__(self, pipe: "ReplayPipeline", slow: float, min_len: int):
+        pb = pipe.pb
+        jcap = np.array([pb.scen[s].req_cap // min_len + 2 for s in range(pb.n_scen)], dtype=np.int32)
+        joff = np.concatenate([[0], np.cumsum(jcap)[:-1]]).astype(np.int32)
+        total = int(jcap.sum())
+        dev = pipe.dev
+        self.t = {
+            "joff": torch.from_numpy(joff).to(dev), "jcap": torch.from_numpy(jcap).to(dev),
+            "lo": torch.zeros(total, dtype=torch.int32, device=dev), "hi": torch.zeros(total, dtype=torch.int32, device=dev),
+            "n_jobs": torch.zeros(pb.n_scen, dtype=torch.int32, device=dev),
+            "last": torch.zeros(total, dtype=torch.float64, device=dev),
+            "info": torch.zeros(3 * total, dtype=torch.int32, device=dev),
+            "dirty": torch.zeros(total, dtype=torch.uint8, device=dev),
+            "todo": torch.zeros(total, dtype=torch.int32, device=dev),
+            "todo_count": torch.zeros(1, dtype=torch.int32, device=dev),
+            "slot_scen": torch.from_numpy(np.repeat(np.arange(pb.n_scen, dtype=np.int32), jcap)).to(dev),
+        }
+        self.J = _abi.Jobs(**{k: v.data_ptr() for k, v in self.t.items()}, slow=float(slow), min_len=int(min_len),
+                           total_slots=total)
+        self.key = (float(slow), int(min_len))
+
+
+def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 16, max_iters: int = 100000,
+                     arrivals: bool = True, slo: bool = True, features: bool = True) -> dict:
+    """Busy-period sharding, planned and verified on the device:
+    speculative idle boundaries (k_jobs_plan), parallel job replay
+    (k_jobs_replay), boundary verification and merging (k_jobs_verify),
+    repeated until every boundary holds.  The host only reads the size of the
+    todo list between launches.  Bit-identical to the serial replay."""
+    L, st = pipe.lib, stream_ptr()
+    bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
+    jobs = getattr(pipe, "_jobs", None)
+    if jobs is None or jobs.key != (float(slow), int(min_len)):
+        jobs = _DeviceJobs(pipe, slow, min_len)
+        pipe._jobs = jobs
+    J = ctypes.byref(jobs.J)
+    if arrivals:
+        _abi.check(L.intf_generate_arrivals(bt, B, st), "intf_generate_arrivals")
+    else:
+        _abi.check(L.intf_split_arrivals(bt, B, st), "intf_split_arrivals")
+    _abi.check(L.intf_form_batches(bt, B, st), "intf_form_batches")
+    tab = ctypes.byref(pipe.dtable.struct)
+    _abi.check(L.intf_jobs_plan(bt, tab, B, J, st), "intf_jobs_plan")
+    iters, first = 0, None
+    for iters in range(1, max_iters + 1):
+        n = int(jobs.t["todo_count"].item())
+        if first is None:
+            first = n
+        if n == 0:
+            break
+        need = n * pipe.pb.cap_max * pipe.seg_stride * 5
+        if pipe.t["slot_seg"].numel() < need:
+            pipe.t["slot_seg"] = torch.zeros(need, dtype=torch.float64, device=pipe.dev)
+            pipe.B.slot_seg = pipe.t["slot_seg"].data_ptr()
+        _abi.check(L.intf_jobs_replay(bt, tab, B, J, n, st), "intf_jobs_replay")
+        _abi.check(L.intf_jobs_verify(bt, B, J, st), "intf_jobs_verify")
+    pipe.run_slo_features(slo=slo, features=features)
+    final = int(jobs.t["n_jobs"].sum().item())
+    return {"jobs_initial": int(first or 0), "jobs_final": final, "iterations": iters,
+            "batches": int(pipe.t["n_batches"][: pipe.pb.n_scen].sum().item())}

@@ -85,3 +85,19 @@ def test_sweep_segmented_equals_whole_scenario_jobs():
         for k in ("order", "b_start", "b_completion", "b_measured", "b_nseg", "r_slo_met", "slo_p", "slo_met"):
             assert np.array_equal(a[k], b[k]), (s, k)
         assert a["n_reseats"] == b["n_reseats"]
+
+
+def test_device_and_host_planned_sharding_agree():
+    from paper_2512_18725_b200 import engine
+
+    names = _golden.scenario_names("default")
+    specs = [_golden.spec(n) for n in names]
+    a = engine.ReplayPipeline(specs, _golden.table("default"), scale=1.5)
+    engine.replay_segmented(a, slow=0.5, min_len=4)
+    b = engine.ReplayPipeline(specs, _golden.table("default"), scale=1.5)
+    engine.replay_segmented_host(b, slow=0.5, min_len=4)
+    ha, hb = a.fetch(), b.fetch()
+    for s, n in enumerate(names):
+        va, vb = a.scenario(ha, s), b.scenario(hb, s)
+        assert _golden.compare_replay(va, n) == [] and _golden.compare_replay(vb, n) == []
+        assert va["n_reseats"] == vb["n_reseats"] and va["n_segments"] == vb["n_segments"]
