@@ -6,8 +6,10 @@ own x peer-multiset candidates), scored by the coarse (static
 features) and fine (EWMA(1/2) features) linear predictors for D = 32
 scheduling decisions per step, each decision with its own refit
 coefficients (OLS on growing windows of the bundled trace's samples).
-One step = one launch of k_candidates writing 63,974,400 fp32 predictions
-(256 MB > L2, so no flush is needed between steps).
+One step = one k_cand_step launch: its stream blocks write 63,974,400 fp32
+predictions (256 MB > L2, so no flush is needed between steps) and its prep
+blocks build the candidate features for the next step (double-buffered
+workspace); consecutive steps are chained by programmatic dependent launch.
 
 Secondary workload (configs[4] shape, C5): a sweep of synthetic scenarios
 replayed end to end per step (arrivals -> replay -> SLO -> features +
@@ -52,12 +54,13 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic():
-    """ncu dram bytes per launch of k_candidates, if a capture was committed."""
+def _traffic(kernel: str):
+    """ncu dram bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` summary (profiles/ncu_summary.json), if present."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("k_cand_stream", {}).get("dram_bytes_per_launch")
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
     return None
 
 
@@ -262,6 +265,21 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
                         "busy-period-sharded replay + SLO + features"}
 
 
+def prep_kernel_ms(scorer, stream) -> float:
+    """k_cand_prep alone on the current stream (context for step_kernels)."""
+    import torch
+
+    for _ in range(3):
+        scorer.prepare()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(10):
+        scorer.prepare()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 10
+
+
 def replay_stage_times(pipe, stream) -> dict:
     """One extra (untimed) pass of the replay pipeline with events between
     its launches: per-stage device time in ms."""
@@ -371,26 +389,35 @@ def product_arm(a):
     # ---- device-resident timed region (clocks sampled across every timed region)
     clocks = Clocks(local)
     clocks.wait_first()
+    # one step = forward of every candidate for this step's decisions + the
+    # candidate-feature build for the next step (double-buffered workspace),
+    # both in ONE k_cand_step launch (--side-stream: k_cand_stream + k_cand_prep
+    # on a side stream).  The first step's features are built in warm-up and
+    # the last timed step's feature build is joined before t_end, so the timed
+    # region holds exactly K forward passes and K feature builds.
+    scorer.pipeline_start(fused=not a.side_stream)
     for k in range(a.warmup):
-        scorer.score(coefs, outs[k & 1])
+        scorer.pipeline_step(coefs, outs[k & 1])
     barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    evp = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     for k in range(a.steps):
-        # one step = phase 1 (candidate features) + phase 2 (forward of all decisions)
-        ev[k][0].record(stream)
-        scorer.prepare()
-        evp[k].record(stream)
-        scorer.score_prepared(coefs, outs[k & 1])
-        ev[k][1].record(stream)
+        scorer.pipeline_step(coefs, outs[k & 1])
+    scorer.pipeline_join()
     t_end.record(stream)
     barrier()
     ms_total = max_over_ranks(t_start.elapsed_time(t_end))
-    kern_ms = float(np.mean([p.elapsed_time(e) for p, (_, e) in zip(evp, ev)]))  # k_cand_stream
-    prep_ms = float(np.mean([s.elapsed_time(p) for p, (s, _) in zip(evp, ev)]))  # k_cand_prep
+    # per-launch duration of the step kernel with events around every launch
+    # (a separate pass: events between launches would serialise the
+    # programmatic dependent launches of the timed loop)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    for k in range(a.steps):
+        scorer.pipeline_step(coefs, outs[k & 1], kernel_events=ev[k])
+    scorer.pipeline_join()
+    torch.cuda.synchronize()
+    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
+    prep_ms = prep_kernel_ms(scorer, stream)  # k_cand_prep alone (untimed pass)
     ms_step = ms_total / a.steps
     value = world * n_pred / (ms_step / 1e3)
 
@@ -463,8 +490,15 @@ def product_arm(a):
 
     peak, peak_src = _peaks()
     bytes_per_launch = 4.0 * n_pred  # implicit enumeration: fp32 output only
-    achieved = bytes_per_launch / (kern_ms / 1e3) / 1e9
-    traffic = _traffic()
+    fused = not a.side_stream
+    kname = "k_cand_step" if fused else "k_cand_stream"
+    # fused: every step is ONE k_cand_step launch, chained by programmatic
+    # dependent launch, so the steady-state launch duration is this rank's
+    # timed-region time / K; events around each launch (kern_ms) serialise
+    # the chain and are reported as the isolated figure
+    launch_ms = t_start.elapsed_time(t_end) / a.steps if fused else kern_ms
+    achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
+    traffic = _traffic(kname)
     line = {
         "metric": METRIC, "value": value, "unit": "predictions/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -477,13 +511,17 @@ def product_arm(a):
                 "h2d_bytes_per_step": int(W.size * 8), "d2h_bytes_per_step": int(4 * n_elems),
                 "call": "intf_predict_candidates_host (pinned host buffers)", "finite": ok},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_cand_stream",
-                     "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "step_kernels": {"k_cand_prep_ms": prep_ms, "k_cand_stream_ms": kern_ms},
+                     "traffic": traffic, "peak_source": peak_src, "kernel": kname,
+                     "kernel_ms": launch_ms, "kernel_ms_isolated": kern_ms,
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "step": ("one k_cand_step launch per step: forward of every candidate (stream blocks) + feature "
+                              "build for the next step (prep blocks), PDL-chained" if fused else
+                              "k_cand_stream + k_cand_prep of the next step on a side stream"),
+                     "k_cand_prep_ms_alone": prep_ms,
                      "write_only_reference_gbs": fill_gbs},
         "cpu_baseline": cpu,
         "clocks": clk,
-        "gpu_launches": 2 * a.steps,
+        "gpu_launches": a.steps if fused else 2 * a.steps,
         "replay": {"metric": "scenario replays/sec", "value": world * REPLAY_SCEN / (rep_ms / 1e3),
                    "unit": "replays/s", "ms_per_step": rep_ms, "scenarios_per_gpu": REPLAY_SCEN,
                    "requests": n_req, "batches": n_batches, "status_nonzero": int(np.count_nonzero(st)),
@@ -509,6 +547,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 long-trace secondary measurement")
+    ap.add_argument("--side-stream", action="store_true",
+                    help="C2 step as two launches (feature build on a side stream) instead of one fused launch")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the multi-rank plumbing with ranks sharing GPUs (numbers meaningless)")
     a = ap.parse_args()

@@ -235,6 +235,16 @@ int intf_candidate_prepare(const intf_table *table, int32_t cap, double alpha, f
                            void *stream);
 int intf_predict_candidates_prepared(const intf_table *table, int32_t cap, const double *coefs, int32_t n_dec,
                                      float *out, const float *ws, int64_t ws_elems, void *stream);
+/* One pipelined C2 step in a single launch (k_cand_step): the forward of
+ * every candidate for coefs' n_dec decisions from the features prepared in
+ * ws_cur (as intf_predict_candidates_prepared), fused with the feature build
+ * for the next step into ws_next (as intf_candidate_prepare; ws_next may be
+ * NULL for the last step).  ws_cur and ws_next must be distinct workspaces
+ * of intf_candidate_workspace() floats.  Same reference functions as
+ * intf_predict_candidates (`colocation.py:71-84`, `predict.py:43-44`). */
+int intf_candidate_step(const intf_table *table, int32_t cap, double alpha, const double *coefs, int32_t n_dec,
+                        float *out, const float *ws_cur, float *ws_next, int64_t ws_elems, void *stream);
+
 /* Host-buffer variant (the end-to-end call): copies coefs in and all
  * predictions out.  h_out: n_dec*2*n_rows*ld floats; d_scratch: device
  * floats = 28*n_dec + that output size (+ the workspace to use two-phase). */

@@ -244,13 +244,19 @@ __global__ void __launch_bounds__(kCandThreads, 2) k_candidates(const double* __
 //   FE[(o*3 + c)][r]  EWMA features seen by own row o (the prefix selected by
 //                     how many peers finish before o), fp32
 // Phase 2 (k_cand_stream): pure streaming -- per thread 4 multisets x 1 own x
-// all decisions: 3 FFMA per prediction, 16-byte streaming stores.
-constexpr int kPrepOwn = 12;  // own rows per prep thread (grid.y splits the table)
+// kStreamDec decisions: 3 FFMA per prediction, 16-byte streaming stores.
+// own rows per prep thread (grid.y splits the table): 12 for the standalone
+// k_cand_prep (shortest launch), 48 inside the fused k_cand_step, where the
+// 163 prep blocks run beside the stream blocks and fewer, longer blocks
+// disturb them least (B200, C2 shape: 43.2 us/step at 48 vs 44.1 at 12).
+constexpr int kPrepOwn = 12;
+constexpr int kStepPrepOwn = 48;
 
 template <int KMAX>
-__global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ solo, const double* __restrict__ thr,
-                                                   int E, int cap, long long n_sets, long long ld, double alpha,
-                                                   float* __restrict__ C0, float* __restrict__ FE) {
+__device__ __forceinline__ void cand_prep_body(int bx, int by, const double* __restrict__ solo,
+                                               const double* __restrict__ thr, int E, int cap, long long n_sets,
+                                               long long ld, double alpha, float* __restrict__ C0,
+                                               float* __restrict__ FE, int prep_own) {
   extern __shared__ unsigned long long binom_smem[];
   const int nmax = E + KMAX + 1;
   for (int t = threadIdx.x; t < (KMAX + 1) * nmax; t += blockDim.x) {
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ so
   }
   __syncthreads();
   const BinomTab C{binom_smem, nmax};
-  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long r = (long long)bx * blockDim.x + threadIdx.x;
   if (r >= ld) return;
   constexpr int KP = KMAX > 0 ? KMAX : 1;
   const bool live = r < n_sets;
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ so
   float ew[KMAX + 1][3];
   double e[3];
   const double om = 1.0 - alpha;
-  const int o_begin = blockIdx.y * kPrepOwn, o_end = min(E, o_begin + kPrepOwn);
+  const int o_begin = by * prep_own, o_end = min(E, o_begin + prep_own);
 #pragma unroll
   for (int i = 0; i <= KMAX; i++) {
     double c[3] = {0.0, 0.0, 0.0};
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ so
       ew[i][a] = live ? to_f32(e[a]) : 0.0f;
     }
   }
-  if (blockIdx.y == 0) {
+  if (by == 0) {
 #pragma unroll
     for (int a = 0; a < 3; a++) C0[a * ld + r] = ew[0][a];
   }
@@ -323,21 +329,23 @@ __global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ so
 }
 
 constexpr int kStreamThreads = 128;
-constexpr int kStreamDec = 64;  // decisions per launch chunk (smem coefficient slab)
+// decisions per block: 4 (x 2 kinds = 8 float4 stores per thread).  Short
+// blocks stream best -- measured on B200 for the C2 shape (tools/
+// cand_stream_variants.cu): 32 per block 5.09 TB/s, 16: 5.24, 8: 5.56,
+// 4: 5.89, 2: 5.20; a one-float4-per-thread fill reaches 6.50.
+constexpr int kStreamDec = 4;
 
 // grid: x = groups of 4 multisets, y = own row, z = decision chunks.  The
 // thread's feature loads (L2-resident C0/FE) are issued before the block
 // builds its coefficient slab, so their latency overlaps that setup.
-__global__ void __launch_bounds__(kStreamThreads, 8) k_cand_stream(const double* __restrict__ thr, int E, long long ld,
-                                                                   long long n_sets,
-                                                                   const double* __restrict__ coefs, int n_dec,
-                                                                   const float* __restrict__ C0,
-                                                                   const float* __restrict__ FE,
-                                                                   float* __restrict__ out) {
+__device__ __forceinline__ void cand_stream_body(int bx, int by, int bz, const double* __restrict__ thr, int E,
+                                                 long long ld, long long n_sets, const double* __restrict__ coefs,
+                                                 int n_dec, const float* __restrict__ C0,
+                                                 const float* __restrict__ FE, float* __restrict__ out) {
   __shared__ float4 cw[kStreamDec][2];
-  const int o = blockIdx.y;
-  const int d0 = blockIdx.z * kStreamDec, nd = min(kStreamDec, n_dec - d0);
-  const long long r0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int o = by;
+  const int d0 = bz * kStreamDec, nd = min(kStreamDec, n_dec - d0);
+  const long long r0 = ((long long)bx * blockDim.x + threadIdx.x) * 4;
   const bool inb = r0 < ld;
   const long long rr = inb ? r0 : 0;
   const float4 cx = __ldg(reinterpret_cast<const float4*>(C0 + rr));
@@ -378,6 +386,52 @@ __global__ void __launch_bounds__(kStreamThreads, 8) k_cand_stream(const double*
     __stcs(reinterpret_cast<float4*>(row + kstride), yf);
     row += dstride;
   }
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_cand_prep(const double* __restrict__ solo, const double* __restrict__ thr,
+                                                   int E, int cap, long long n_sets, long long ld, double alpha,
+                                                   float* __restrict__ C0, float* __restrict__ FE, int prep_own) {
+  cand_prep_body<KMAX>(blockIdx.x, blockIdx.y, solo, thr, E, cap, n_sets, ld, alpha, C0, FE, prep_own);
+}
+
+__global__ void __launch_bounds__(kStreamThreads, 8) k_cand_stream(const double* __restrict__ thr, int E, long long ld,
+                                                                   long long n_sets,
+                                                                   const double* __restrict__ coefs, int n_dec,
+                                                                   const float* __restrict__ C0,
+                                                                   const float* __restrict__ FE,
+                                                                   float* __restrict__ out) {
+  cand_stream_body(blockIdx.x, blockIdx.y, blockIdx.z, thr, E, ld, n_sets, coefs, n_dec, C0, FE, out);
+}
+
+// One pipelined step in ONE launch: the forward of every candidate from the
+// features in ws_cur (stream blocks) + the feature build for the next step
+// into ws_next (prep blocks), horizontally fused so the issue-bound prep work
+// fills the HBM-bound stream kernel's idle issue slots and no cross-stream
+// synchronisation or second launch sits between steps.  1-D grid: the first
+// n_prep blocks are prep blocks (dispatched first, they run beside the
+// stream blocks instead of after them).
+template <int KMAX>
+__global__ void __launch_bounds__(kStreamThreads, 8) k_cand_step(
+    const double* __restrict__ solo, const double* __restrict__ thr, int E, int cap, long long n_sets, long long ld,
+    double alpha, const double* __restrict__ coefs, int n_dec, const float* __restrict__ ws_cur,
+    float* __restrict__ ws_next, float* __restrict__ out, int prep_x, int prep_y, int prep_own, int stream_x) {
+  // programmatic dependent launch: let the next step's grid be scheduled as
+  // soon as every CTA of this one is running, and wait for the previous
+  // step's grid (its prep blocks wrote ws_cur; its stream blocks read
+  // ws_next) before touching memory.  Both are no-ops without PDL.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int n_prep = ws_next ? prep_x * prep_y : 0;
+  int b = blockIdx.x;
+  if (b < n_prep) {
+    cand_prep_body<KMAX>(b % prep_x, b / prep_x, solo, thr, E, cap, n_sets, ld, alpha, ws_next, ws_next + 3 * ld,
+                         prep_own);
+    return;
+  }
+  b -= n_prep;
+  const int bx = b % stream_x, rest = b / stream_x;
+  cand_stream_body(bx, rest % E, rest / E, thr, E, ld, n_sets, coefs, n_dec, ws_cur, ws_cur + 3 * ld, out);
 }
 
 // ===================================================================== K6
@@ -790,7 +844,8 @@ static int launch_prep(const intf_table* t, int cap, double alpha, float* ws, cu
   const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_prep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_cand_prep<K><<<dim3(ceil_div(ld, 128), ceil_div(E, kPrepOwn)), 128, smem, st>>>(t->solo_ms, t->thr, E, cap, sets,
-                                                                                  ld, alpha, ws, ws + 3 * ld);
+                                                                                  ld, alpha, ws, ws + 3 * ld,
+                                                                                  kPrepOwn);
   return launch_status("k_cand_prep");
 }
 
@@ -801,6 +856,33 @@ static int launch_stream(const intf_table* t, int cap, const double* coefs, int 
   dim3 grid(ceil_div(ld / 4, kStreamThreads), E, ceil_div(n_dec, kStreamDec));
   k_cand_stream<<<grid, kStreamThreads, 0, st>>>(t->thr, E, ld, sets, coefs, n_dec, ws, ws + 3 * ld, out);
   return launch_status("k_cand_stream");
+}
+
+template <int K>
+static int launch_step(const intf_table* t, int cap, double alpha, const double* coefs, int n_dec, float* out,
+                       const float* ws_cur, float* ws_next, cudaStream_t st) {
+  const int E = t->n_rows;
+  const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
+  const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int po = kStepPrepOwn;
+  const int px = (int)ceil_div(ld, 128), py = (int)ceil_div(E, po);
+  const int sx = (int)ceil_div(ld / 4, kStreamThreads);
+  const long long nblk = (ws_next ? (long long)px * py : 0) + (long long)sx * E * ceil_div(n_dec, kStreamDec);
+  if (nblk > 0x7fffffffLL) return bad_input("intf_candidate_step: too many blocks");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nblk);
+  cfg.blockDim = dim3(kStreamThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_cand_step<K>, t->solo_ms, t->thr, E, cap, sets, ld, alpha, coefs, n_dec, ws_cur, ws_next,
+                     out, px, py, po, sx);
+  return launch_status("k_cand_step");
 }
 
 // phase: 1 = feature prep, 2 = forward stream, 3 = both (two-phase path only)
@@ -879,6 +961,25 @@ int intf_predict_candidates_prepared(const intf_table* table, int32_t cap, const
       ws_elems < need)
     return bad_input("intf_predict_candidates_prepared: bad argument or workspace too small");
   return launch_stream(table, cap, coefs, n_dec, out, const_cast<float*>(ws), as_stream(stream));
+}
+
+int intf_candidate_step(const intf_table* table, int32_t cap, double alpha, const double* coefs, int32_t n_dec,
+                        float* out, const float* ws_cur, float* ws_next, int64_t ws_elems, void* stream) {
+  int64_t need = 0;
+  if (!table || !coefs || !out || !ws_cur || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1 ||
+      intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need || ws_next == ws_cur)
+    return bad_input("intf_candidate_step: bad argument or workspace too small");
+  cudaStream_t st = as_stream(stream);
+  switch (cap - 1) {
+    case 0: return launch_step<0>(table, cap, alpha, coefs, n_dec, out, ws_cur, ws_next, st);
+    case 1: return launch_step<1>(table, cap, alpha, coefs, n_dec, out, ws_cur, ws_next, st);
+    case 2: return launch_step<2>(table, cap, alpha, coefs, n_dec, out, ws_cur, ws_next, st);
+    case 3: return launch_step<3>(table, cap, alpha, coefs, n_dec, out, ws_cur, ws_next, st);
+    case 4: return launch_step<4>(table, cap, alpha, coefs, n_dec, out, ws_cur, ws_next, st);
+    case 5: return launch_step<5>(table, cap, alpha, coefs, n_dec, out, ws_cur, ws_next, st);
+    case 6: return launch_step<6>(table, cap, alpha, coefs, n_dec, out, ws_cur, ws_next, st);
+    default: return launch_step<7>(table, cap, alpha, coefs, n_dec, out, ws_cur, ws_next, st);
+  }
 }
 
 int intf_predict_candidates_host(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,

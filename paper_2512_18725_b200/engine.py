@@ -443,6 +443,70 @@ class CandidateScorer:
                                                                 _abi.addr(self.ws), self.ws_elems, stream_ptr()),
                    "intf_predict_candidates_prepared")
 
+    def pipeline_start(self, fused: bool = True) -> None:
+        """Start a pipelined sequence of steps (`pipeline_step`): features for
+        the first step are built now (k_cand_prep) into workspace 0.
+        fused: each step is ONE k_cand_step launch (forward of this step +
+        feature build of the next, horizontally fused); otherwise the feature
+        build runs as k_cand_prep on a side stream beside k_cand_stream."""
+        s = torch.cuda.current_stream(self.dev)
+        if getattr(self, "_ws", None) is None:
+            self._side = torch.cuda.Stream(self.dev)
+            self._ws = [self.ws, torch.empty_like(self.ws)]
+            self._ready = [torch.cuda.Event(), torch.cuda.Event()]
+            self._read = [torch.cuda.Event(), torch.cuda.Event()]
+        self._k = 0
+        self._fused = bool(fused)
+        self._prepare_into(self._ws[0], s)
+        self._ready[0].record(s)
+
+    def _prepare_into(self, ws: torch.Tensor, s: torch.cuda.Stream) -> None:
+        _abi.check(_abi.load().intf_candidate_prepare(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
+                                                      ws.data_ptr(), self.ws_elems, s.cuda_stream),
+                   "intf_candidate_prepare")
+
+    def pipeline_step(self, coefs: torch.Tensor, out: torch.Tensor, kernel_events=None) -> None:
+        """One step = the forward of every candidate for coefs' decisions,
+        from the features built for this step, + the feature build for the
+        NEXT step into the other workspace.  The forward is HBM-write bound
+        and the feature build issue/L2 bound, so the two overlap.
+        kernel_events = (start, end) CUDA events bracketing the forward launch."""
+        s = torch.cuda.current_stream(self.dev)
+        cur, nxt = self._k & 1, (self._k + 1) & 1
+        n_dec = coefs.numel() // 14
+        L = _abi.load()
+        if self._fused:
+            if kernel_events:
+                kernel_events[0].record(s)
+            _abi.check(L.intf_candidate_step(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
+                                             coefs.data_ptr(), n_dec, out.data_ptr(), self._ws[cur].data_ptr(),
+                                             self._ws[nxt].data_ptr(), self.ws_elems, s.cuda_stream),
+                       "intf_candidate_step")
+            if kernel_events:
+                kernel_events[1].record(s)
+            self._k += 1
+            return
+        s.wait_event(self._ready[cur])
+        if kernel_events:
+            kernel_events[0].record(s)
+        _abi.check(L.intf_predict_candidates_prepared(ctypes.byref(self.dtable.struct), self.cap, coefs.data_ptr(),
+                                                      n_dec, out.data_ptr(), self._ws[cur].data_ptr(), self.ws_elems,
+                                                      s.cuda_stream), "intf_predict_candidates_prepared")
+        if kernel_events:
+            kernel_events[1].record(s)
+        self._read[cur].record(s)
+        # next step's features: after the previous step's forward released that workspace
+        side = self._side
+        side.wait_event(self._read[nxt]) if self._k > 0 else side.wait_stream(s)
+        self._prepare_into(self._ws[nxt], side)
+        self._ready[nxt].record(side)
+        self._k += 1
+
+    def pipeline_join(self) -> None:
+        """Make the current stream wait for the side stream's last feature build."""
+        if not self._fused:
+            torch.cuda.current_stream(self.dev).wait_stream(self._side)
+
     def scratch_elems(self, n_dec: int) -> int:
         """Device floats needed by score_host (coefs + outputs + workspace)."""
         return 28 * n_dec + self.out_elems(n_dec) + self.ws_elems

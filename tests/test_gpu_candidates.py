@@ -79,3 +79,22 @@ def test_host_buffer_variant_equals_device_variant():
     sc.score_host(np.ascontiguousarray(W), host_out, scratch)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(host_out, dev_out.cpu().numpy())
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_pipelined_steps_equal_one_shot(fused):
+    """pipeline_step (forward of step k overlapped with the feature build of
+    step k+1 on a side stream) gives the one-shot results, for decision
+    counts that are and are not multiples of the per-block chunk."""
+    sc = _scorer(3)
+    rng = np.random.default_rng(5)
+    Ws = [rng.normal(0, 0.5, size=(n, 2, 7)) for n in (7, 4, 1, 9)]
+    outs = [sc.alloc(len(W)) for W in Ws]
+    sc.pipeline_start(fused=fused)
+    for W, out in zip(Ws, outs):
+        sc.pipeline_step(torch.tensor(W, device="cuda").contiguous(), out)
+    sc.pipeline_join()
+    for W, out in zip(Ws, outs):
+        ref = sc.alloc(len(W))
+        sc.score(torch.tensor(W, device="cuda").contiguous(), ref)
+        np.testing.assert_array_equal(out.cpu().numpy(), ref.cpu().numpy())
