@@ -319,6 +319,27 @@ int intf_slowdowns(const double *own, const double *colo, const double *beta, co
  * the device RNG against numpy.                                            */
 int intf_rng_stream(const uint32_t *words, int32_t n_words, int64_t n, int32_t uniform, double *out, void *stream);
 
+/* ---- host-side CSV materialisation (no device work) ----------------------
+ * The reference writes its artifacts with csv.writer rows of repr(float) /
+ * int / str fields (`simcore.py:319-369` outcomes + segments, `metrics.py:
+ * 82-128` requests + slo_report, `colocation.py:108-126` samples,
+ * `workload.py:173-178` arrivals; writer `cli.py:34-39`).  intf_csv_rows
+ * formats n_rows rows of n_cols typed SoA columns into `out` with the same
+ * bytes: INTF_COL_I64 = int64 column in decimal, INTF_COL_F64_REPR = double
+ * column as CPython repr(float), INTF_COL_STR = int32 indices into strtab
+ * (strings already csv-quoted by the caller, lengths in strlen_tab).  Fields
+ * are joined by ',' and every row ends in "\r\n".  *out_len = bytes needed;
+ * out = NULL only measures.                                                  */
+#define INTF_COL_I64 0
+#define INTF_COL_F64_REPR 1
+#define INTF_COL_STR 2
+#define INTF_COL_F64_NPREPR 3 /* double column as numpy 2's repr of np.float64: "np.float64(<repr>)" */
+int intf_csv_rows(int64_t n_rows, int32_t n_cols, const int32_t *kinds, const void *const *cols,
+                  const char *const *strtab, const int32_t *strlen_tab, char *out, int64_t out_cap,
+                  int64_t *out_len);
+/* CPython repr(float) of one double into out (NUL-terminated, cap >= 32). */
+int intf_repr_f64(double v, char *out, int32_t cap);
+
 /* last error text (thread-local); returns strlen */
 int intf_last_error(char *buf, int32_t n);
 int intf_abi_version(void);
