@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 N_DEC = 32
 CAP = 4
 ALPHA = 0.5
-REPLAY_SCEN = 4096
+REPLAY_SCEN = 10000  # BASELINE configs[4]: a sweep of 10^4 synthetic scenarios (per GPU)
 METRIC = "candidate co-location predictions/sec and scenario replays/sec at 1/2/4/8 B200"
 
 
@@ -147,6 +147,30 @@ def cpu_candidate_rate(table, W, seconds: float, seed: int = 0):
             n += 2
     dt = time.perf_counter() - t0
     return n / dt, n, dt
+
+
+def cpu_replay_rate(table, seconds: float, start: int = 0):
+    """The oracle's C restatement of `run_scenario` (`simcore.py:218-310`,
+    literal heap engine) + its arrival generator on one core, over C5
+    scenarios start, start+1, ... until `seconds` elapse: (replays/s, n, s)."""
+    import oracle as O
+    from paper_2512_18725_b200.sweep import c5_scenario
+
+    ta = table.arrays()
+    otab = O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr)
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        O.run_scenario(c5_scenario(table, start + n), otab)
+        n += 1
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def _ref_replay_worker(args):
+    seconds, start = args
+    from paper_2512_18725_b200.profiles import gen_synthetic_profiles
+
+    return cpu_replay_rate(gen_synthetic_profiles(), seconds, start)[1]
 
 
 def _ref_worker(args):
@@ -323,6 +347,10 @@ def reference_arm(a):
             n = sum(pool.map(_ref_worker, [(per_step, 1000 * k + s) for s in range(cores)]))
             times.append(time.perf_counter() - t0)
             preds += n
+        # scenario replays on every core (context; the driver's ratio uses `value`)
+        t0 = time.perf_counter()
+        n_rep = sum(pool.map(_ref_replay_worker, [(per_step, 100000 * (s + 1)) for s in range(cores)]))
+        rep_rate = n_rep / (time.perf_counter() - t0)
     tot = sum(times)
     v = preds / tot
     line = {
@@ -335,6 +363,8 @@ def reference_arm(a):
                          "sample": f"{per_step:.1f} s of random cap-4 candidates per core per step "
                                    f"(oracle.candidate_predictions, reference functions restated)"},
         "e2e": {"value": v, "unit": "predictions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "replay": {"metric": "scenario replays/sec", "value": rep_rate, "unit": "replays/s", "cores": cores,
+                   "sample": f"{n_rep} C5 scenarios (oracle C replay: heap engine + arrivals), {per_step:.1f} s per core"},
     }
     print(json.dumps(line))
     return 0
@@ -470,11 +500,14 @@ def product_arm(a):
     clk = clocks.stop()
 
     # ---- CPU baseline (rank 0, N=1 only): oracle port on a bounded sample
-    cpu = None
+    cpu = replay_cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         rate, n, dt = cpu_candidate_rate(ta, W, a.cpu_seconds)
         cpu = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port",
                "sample": f"{n} predictions ({n // 2} random cap-4 candidates x coarse+fine, 1 decision) in {dt:.1f} s"}
+        rrate, rn, rdt = cpu_replay_rate(table, min(5.0, a.cpu_seconds))
+        replay_cpu = {"value": rrate, "unit": "replays/s", "cores": 1, "kind": "port",
+                      "sample": f"{rn} C5 scenarios (oracle C replay: heap engine + arrivals) in {rdt:.1f} s"}
 
     # context: a pure device write (torch fill) of the same size, alternating
     # two buffers like the timed loop -- the write-only ceiling on this part
@@ -527,7 +560,7 @@ def product_arm(a):
                    "requests": n_req, "batches": n_batches, "status_nonzero": int(np.count_nonzero(st)),
                    "workload": "C5-shape synthetic scenarios (default_rng([2512,i]), 1 s, cap 1-3): arrivals + "
                                "formation + noise + replay (warp per scenario) + SLO + features/3 predictors",
-                   "stage_ms": stage_ms},
+                   "stage_ms": stage_ms, "cpu_baseline": replay_cpu},
         "refit": refit,
         "long_trace": longtrace,
     }

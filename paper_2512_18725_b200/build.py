@@ -53,7 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in sources():
         obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-c", src, "-o", obj]
+        extra = os.environ.get("INTF_NVCC_EXTRA", "").split()  # tuning experiments (tools/), e.g. -DINTF_REPLAY_MINB=6
+        cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(-4, "-Xptxas=-v")
             print(" ".join(cmd))

@@ -164,9 +164,12 @@ __global__ void k_noise_table(const intf_scenario* __restrict__ scen, intf_repla
 
 // ---- K2: the replay recurrence, one kReplayW-lane group per scenario (lane
 // l < cap owns running slot l; replay_warp.cuh).
+#ifndef INTF_REPLAY_MINB
+#define INTF_REPLAY_MINB 4
+#endif
 constexpr int kReplayWarps = 4;
 constexpr int kReplayW = 32;  // measured: one scenario per warp beats 4 x 8-lane groups (divergence)
-__global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_warp(const intf_scenario* __restrict__ scen,
+__global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_replay_warp(const intf_scenario* __restrict__ scen,
                                                                     int n_scen, const intf_model* __restrict__ models,
                                                                     intf_table tab, intf_replay_buffers B) {
   __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
