@@ -63,6 +63,9 @@ typedef struct intf_scenario {
   double duration_s, window_ms, sigma;
   double beta[3];              /* (l2, dram, sm) contention sensitivities */
   uint64_t seed, oracle_seed;  /* arrival seed, InterferenceOracle.seed */
+  uint64_t batch_id_base;      /* noise key of batch b = batch_id_base + b (`oracle.py:24-33`): 0 for
+                                  run_scenario; callers numbering batches across scenarios set it
+                                  (full_overlap_ratios `experiments.py:266-282`) */
 } intf_scenario;
 
 /* One deployed model of a scenario (`workload.py:22-32` DeployedModel). */

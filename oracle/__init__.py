@@ -49,6 +49,7 @@ class ScenarioIn(ctypes.Structure):
         ("name_rank", PI), ("entry_base", PI), ("tab_solo", PD), ("tab_thr", PD),
         ("duration_s", D), ("window_ms", D), ("sigma", D), ("beta", D * 3),
         ("max_bs", I), ("cap", I), ("seed", ctypes.c_uint64), ("oracle_seed", ctypes.c_uint64),
+        ("batch_id_base", ctypes.c_uint64),
     ]
 
 
@@ -161,6 +162,7 @@ def scenario_in(spec: dict, tab: TableArrays):
     s.cap = int(spec.get("concurrency_cap", 2))
     s.seed = int(spec.get("seed", 0))
     s.oracle_seed = int(orc.get("seed", 0))
+    s.batch_id_base = int(spec.get("batch_id_base", 0))
     k.struct = s
     return k
 
@@ -433,3 +435,54 @@ def candidate_predictions(own, peers, solo, thr, w_coarse, w_fine, alpha):
     xs = features(hist, thr[own], False, 1.0)
     xf = features(hist, thr[own], True, alpha)
     return predict(w_coarse[:6], w_coarse[6], xs), predict(w_fine[:6], w_fine[6], xf)
+
+
+# ------------------------------------------------ calibration driver (§8f)
+def _slowdown(own, colo, betas, noise: float) -> float:
+    """`oracle.py:36-47`: (1 + betas @ max(0, own + colo - 1)) * noise, the
+    dot an fma chain from 0 (OpenBLAS ddot)."""
+    excess = np.maximum(0.0, (np.asarray(own, dtype=float) + np.asarray(colo, dtype=float)) - 1.0)
+    b = np.ascontiguousarray(betas, dtype=np.float64)
+    dot = lib().oracle_ddot(_p(b), _p(np.ascontiguousarray(excess)), 3)
+    return (1.0 + dot) * noise
+
+
+def full_overlap_ratios(tab: TableArrays, model_a="roberta_b", model_b="roberta_b", batch_size=8, n_pairs=200,
+                        seed=0, sigma=0.05, betas=(1.0, 1.5, 0.5)):
+    """`experiments.py:255-291` restated on GpuState's semantics
+    (`simcore.py:103-198`): per pair, batches 2k (model_a) and 2k+1 (model_b)
+    dispatched at t = 0 in that order (the second dispatch pops the first
+    batch's zero-length segment and reseats it at segment index 0), then
+    completions in (remaining * slowdown, batch_id) order, now += that
+    product, the survivor reseated alone.  Returns the interference ratios
+    in completion order."""
+    def noise(b, i):
+        return 1.0 if sigma == 0.0 else noise_draw(seed, b, i, sigma)
+
+    out = []
+    for k in range(n_pairs):
+        ids = (2 * k, 2 * k + 1)
+        rows = (tab.row(model_a, batch_size), tab.row(model_b, batch_size))
+        own = [np.asarray(tab.thr[r], dtype=float) for r in rows]
+        total = [float(tab.solo[r]) for r in rows]
+        # dispatch a: alone; dispatch b: b reseated (colo = own_a), a's zero-length segment popped and
+        # a reseated with colo = own_b at segment index 0 again
+        sd = [_slowdown(own[0], np.zeros(3) + own[1], betas, noise(ids[0], 0)),
+              _slowdown(own[1], np.zeros(3) + own[0], betas, noise(ids[1], 0))]
+        hist = [[sd[0]], [sd[1]]]
+        prog = [0.0, 0.0]
+        now = 0.0
+        first = min((0, 1), key=lambda j: ((total[j] - prog[j]) * sd[j], ids[j]))
+        now += (total[first] - prog[first]) * sd[first]
+        order = [first, 1 - first]
+        j = first
+        prog[j] += (now - 0.0) / sd[j]
+        out.append((total[j] if all(s == 1.0 for s in hist[j]) else now - 0.0) / total[j])
+        y = 1 - first  # survivor: close its segment [0, now), reseat alone at segment index 1
+        prog[y] += (now - 0.0) / sd[y]
+        sd[y] = _slowdown(own[y], np.zeros(3), betas, noise(ids[y], 1))
+        hist[y].append(sd[y])
+        now += (total[y] - prog[y]) * sd[y]
+        out.append((total[y] if all(s == 1.0 for s in hist[y]) else now - 0.0) / total[y])
+        del order
+    return out

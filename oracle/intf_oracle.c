@@ -358,6 +358,7 @@ typedef struct {
   double duration_s, window_ms, sigma, beta[3];
   int max_bs, cap;
   uint64_t seed, oracle_seed;
+  uint64_t batch_id_base; /* noise key offset (batches numbered across scenarios) */
 } ScenarioIn;
 
 typedef struct { double t; int rank; int model; } Arr;
@@ -491,7 +492,7 @@ static void sim_reseat(Sim *S, RB *rb) {
     const double *p = &s->tab_thr[3 * o->entry];
     colo[0] += p[0]; colo[1] += p[1]; colo[2] += p[2];
   }
-  double noise = oracle_noise_draw(s->oracle_seed, (uint64_t)rb->batch, (uint64_t)rb->nseg, s->sigma);
+  double noise = oracle_noise_draw(s->oracle_seed, s->batch_id_base + (uint64_t)rb->batch, (uint64_t)rb->nseg, s->sigma);
   double sd = oracle_slowdown(&s->tab_thr[3 * rb->entry], colo, s->beta, noise);
   if (rb->nseg == rb->segcap) {
     rb->segcap = rb->segcap ? 2 * rb->segcap : 8;

@@ -32,7 +32,7 @@ class Scenario(ctypes.Structure):
         ("max_bs", c_int32), ("cap", c_int32),
         ("duration_s", c_double), ("window_ms", c_double), ("sigma", c_double),
         ("beta", c_double * 3),
-        ("seed", ctypes.c_uint64), ("oracle_seed", ctypes.c_uint64),
+        ("seed", ctypes.c_uint64), ("oracle_seed", ctypes.c_uint64), ("batch_id_base", ctypes.c_uint64),
     ]
 
 

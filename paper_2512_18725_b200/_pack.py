@@ -74,7 +74,9 @@ def pack(specs: list, table: TableArrays, scale: float = 1.0, list_caps=None) ->
     for si, spec in enumerate(specs):
         dep = spec["deployed"]
         ids = [d["model_id"] for d in dep]
-        if len(set(ids)) != len(ids):
+        # duplicates only for internal drivers whose batches never tie on a
+        # WINDOW heap key (full_overlap_ratios: every batch emits at max_bs)
+        if len(set(ids)) != len(ids) and not spec.get("allow_duplicate_models"):
             raise ValueError("duplicate model_id in deployed list")
         names.append(ids)
         order = sorted(range(len(ids)), key=lambda i: ids[i])
@@ -93,6 +95,7 @@ def pack(specs: list, table: TableArrays, scale: float = 1.0, list_caps=None) ->
         S.beta[2] = float(orc.get("beta_sm", 0.5))
         S.seed = int(spec.get("seed", 0))
         S.oracle_seed = int(orc.get("seed", 0))
+        S.batch_id_base = int(spec.get("batch_id_base", 0))
         if S.max_bs > table.max_bs:
             raise ValueError(f"max_batch_size {S.max_bs} exceeds the profile table's {table.max_bs}")
         req_cap = 0

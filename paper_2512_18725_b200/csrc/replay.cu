@@ -159,7 +159,7 @@ __global__ void k_noise_table(const intf_scenario* __restrict__ scen, intf_repla
   const long long b = i / K;
   if (b >= B.n_batches[s]) return;
   const int k = (int)(i % K);
-  B.noise_tab[(long long)(S.req_off + b) * K + k] = noise_draw(S.oracle_seed, (uint64_t)b, (uint64_t)k, S.sigma);
+  B.noise_tab[(long long)(S.req_off + b) * K + k] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)b, (uint64_t)k, S.sigma);
 }
 
 // ---- K2: the replay recurrence, one kReplayW-lane group per scenario (lane

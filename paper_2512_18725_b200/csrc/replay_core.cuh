@@ -145,7 +145,7 @@ INTF_FN void reseat(ReplayCtx& c, Slot* slots, const int* run, int nrun, int si,
   if (rb.nseg < c.buf->noise_k)  // precomputed by k_noise_table (same draw)
     noise = c.buf->noise_tab[(size_t)(S.req_off + rb.batch) * c.buf->noise_k + rb.nseg];
   else
-    noise = noise_draw(S.oracle_seed, (uint64_t)rb.batch, (uint64_t)rb.nseg, S.sigma);
+    noise = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)rb.batch, (uint64_t)rb.nseg, S.sigma);
   double sd = slowdown(rb.own, colo, S.beta, noise);
   if (rb.nseg >= c.buf->seg_stride) {
     c.status |= INTF_ST_SEG_STRIDE;

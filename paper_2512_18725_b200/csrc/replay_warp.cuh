@@ -134,7 +134,7 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
     if (!doit) return;
     double noise;
     if (nseg < K) noise = nseg == 0 ? nz0 : nseg == 1 ? nz1 : nseg == 2 ? nz2 : nz3;
-    else noise = noise_draw_slow(S.oracle_seed, (uint64_t)batch, (uint64_t)nseg, S.sigma);
+    else noise = noise_draw_slow(S.oracle_seed, S.batch_id_base + (uint64_t)batch, (uint64_t)nseg, S.sigma);
     const double o[3] = {own0, own1, own2}, colo[3] = {c0, c1, c2};
     const double sd = slowdown(o, colo, S.beta, noise);
     if (nseg < B.seg_stride) {

@@ -52,7 +52,7 @@ extern "C" int hc_run(const intf_batch* bt, const intf_table* tab, const intf_re
     const intf_scenario& S = bt->scen[s];
     for (int b = 0; b < B->n_batches[s]; b++)
       for (int k = 0; k < B->noise_k; k++)
-        B->noise_tab[(long long)(S.req_off + b) * B->noise_k + k] = noise_draw(S.oracle_seed, b, k, S.sigma);
+        B->noise_tab[(long long)(S.req_off + b) * B->noise_k + k] = noise_draw(S.oracle_seed, S.batch_id_base + b, k, S.sigma);
   }
   for (int s = 0; s < S_n; s++) {
     if (B->status[s] & INTF_ST_OVERFLOW) continue;
