@@ -542,7 +542,9 @@ def product_arm(a):
                    "parallelism": f"dp{world} (decisions sharded, no collective)", "l2": "output 256 MB/step > L2; two output buffers alternated per step"},
         "e2e": {"value": world * n_pred / (e2e_ms / 1e3), "unit": "predictions/s",
                 "h2d_bytes_per_step": int(W.size * 8), "d2h_bytes_per_step": int(4 * n_elems),
-                "call": "intf_predict_candidates_host (pinned host buffers)", "finite": ok},
+                "call": "intf_predict_candidates_host (pinned host buffers)", "finite": ok,
+                "pcie_gbs": (W.size * 8 + 4 * n_elems) / (e2e_ms / 1e3) / 1e9,
+                "bound": "PCIe D2H of every fp32 prediction (the kernel is ~1% of the step)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": kname,
                      "kernel_ms": launch_ms, "kernel_ms_isolated": kern_ms,
