@@ -39,8 +39,9 @@ __global__ void __launch_bounds__(32 * kGenWarps) k_gen_arrivals(const intf_scen
 // elements of the other lists that precede it (binary search); one block per
 // model list.  Writes the merged arrays and each element's request id.
 __global__ void k_merge_arrivals(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                                 intf_replay_buffers B) {
-  const int g = blockIdx.y;
+                                 intf_replay_buffers B, int n_models) {
+  const int g = blockIdx.z * gridDim.y + blockIdx.y;  // model lists beyond 65535 spill into grid.z
+  if (g >= n_models) return;
   const intf_model M = models[g];
   const intf_scenario S = scen[M.scen];
   const int n = min(B.n_list[g], M.list_cap);
@@ -110,8 +111,9 @@ __global__ void __launch_bounds__(32 * kFormModelWarps) k_form_models(const intf
 }
 
 __global__ void k_merge_batches(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                                intf_replay_buffers B) {
-  const int g = blockIdx.y;
+                                intf_replay_buffers B, int n_models) {
+  const int g = blockIdx.z * gridDim.y + blockIdx.y;
+  if (g >= n_models) return;
   const intf_model& M = models[g];
   const intf_scenario& S = scen[M.scen];
   const int n = B.n_mb[g];
@@ -151,15 +153,19 @@ __global__ void k_form_status(const intf_scenario* __restrict__ scen, int n_scen
 // ---- K1b: noise draws of the first noise_k segments of every formed batch
 // (`oracle.py:24-33`), fully parallel: takes the SeedSequence/PCG64/ziggurat/
 // exp chain off the serial replay recurrence.  grid: (slots, scenarios).
-__global__ void k_noise_table(const intf_scenario* __restrict__ scen, intf_replay_buffers B) {
-  const int s = blockIdx.y;
-  const intf_scenario& S = scen[s];
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+// grid: one block per scenario (grid-stride over scenarios), looping over
+// the scenario's formed batches x noise_k, so no block is launched for
+// unused capacity slots.
+__global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __restrict__ scen, int n_scen,
+                                                     intf_replay_buffers B) {
   const int K = B.noise_k;
-  const long long b = i / K;
-  if (b >= B.n_batches[s]) return;
-  const int k = (int)(i % K);
-  B.noise_tab[(long long)(S.req_off + b) * K + k] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)b, (uint64_t)k, S.sigma);
+  for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
+    const intf_scenario& S = scen[s];
+    const long long n = (long long)B.n_batches[s] * K;
+    double* out = B.noise_tab + (long long)S.req_off * K;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x)
+      out[i] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)(i / K), (uint64_t)(i % K), S.sigma);
+  }
 }
 
 // ---- K2: the replay recurrence, one kReplayW-lane group per scenario (lane
@@ -604,39 +610,45 @@ struct PredBlock {
   intf_predictor p[kMaxPred];
 };
 
-__global__ void k_features(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+__global__ void k_features(const intf_scenario* __restrict__ scen, int n_scen, const intf_model* __restrict__ models,
                            intf_table tab, intf_replay_buffers B, PredBlock P, int n_pred, long long slot_stride,
                            double* __restrict__ X, double* __restrict__ Y, double* __restrict__ Yhat) {
-  const int s = blockIdx.y;
-  const intf_scenario& S = scen[s];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= B.n_batches[s]) return;
-  const long long slot = (long long)S.req_off + k;
-  const int b = B.out_order[slot];
-  const long long bslot = (long long)S.req_off + b;
-  const int entry = models[S.model_off + B.b_model[bslot]].entry_base + B.b_size[bslot] - 1;
-  const double own[3] = {tab.thr[3 * entry], tab.thr[3 * entry + 1], tab.thr[3 * entry + 2]};
-  const double* colo = B.s_colo + 3ll * B.b_seg_off[bslot];
-  const int nseg = B.b_nseg[bslot];
-  Y[slot] = B.b_measured[bslot] / tab.solo_ms[entry];  // interference ratio (`simcore.py:83-85`)
-  for (int p = 0; p < n_pred; p++) {
-    double x[6];
-    features_one(own, colo, nseg, P.p[p].ewma, P.p[p].alpha, x);
-    if (X) {
-      double* xo = X + (p * slot_stride + slot) * 6;
+  // one block per scenario (grid-stride), a thread per outcome: no blocks
+  // for unused capacity slots
+  for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
+    const intf_scenario& S = scen[s];
+    const int nb = B.n_batches[s];
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      const long long slot = (long long)S.req_off + k;
+      const int b = B.out_order[slot];
+      const long long bslot = (long long)S.req_off + b;
+      const int entry = models[S.model_off + B.b_model[bslot]].entry_base + B.b_size[bslot] - 1;
+      const double own[3] = {tab.thr[3 * entry], tab.thr[3 * entry + 1], tab.thr[3 * entry + 2]};
+      const double* colo = B.s_colo + 3ll * B.b_seg_off[bslot];
+      const int nseg = B.b_nseg[bslot];
+      Y[slot] = B.b_measured[bslot] / tab.solo_ms[entry];  // interference ratio (`simcore.py:83-85`)
+      for (int p = 0; p < n_pred; p++) {
+        double x[6];
+        features_one(own, colo, nseg, P.p[p].ewma, P.p[p].alpha, x);
+        if (X) {
+          double* xo = X + (p * slot_stride + slot) * 6;
 #pragma unroll
-      for (int i = 0; i < 6; i++) xo[i] = x[i];
+          for (int i = 0; i < 6; i++) xo[i] = x[i];
+        }
+        Yhat[p * slot_stride + slot] = predict7(P.p[p].w, x);
+      }
     }
-    Yhat[p * slot_stride + slot] = predict7(P.p[p].w, x);
   }
 }
 
 // (element chunks, models): enough blocks per model list that long traces use
-// every SM, one block per model for short ones; y is capped at 65535 models
+// every SM, one block per model for short ones; models beyond 65535 spill into z
 dim3 merge_grid(const intf_batch* bt) {
   const long long per_model = bt->max_list_cap > 0 ? bt->max_list_cap : 1;
   unsigned x = ceil_div(per_model, 256 * 4);
-  return dim3(x < 1 ? 1 : x, (unsigned)bt->n_models);
+  const unsigned m = bt->n_models > 0 ? (unsigned)bt->n_models : 1u;
+  const unsigned y = m < 65535u ? m : 65535u;
+  return dim3(x < 1 ? 1 : x, y, ceil_div(m, y));
 }
 
 int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaStream_t st) {
@@ -649,7 +661,7 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
   k_form_models<<<ceil_div(bt->n_models, kFormModelWarps), 32 * kFormModelWarps, 0, st>>>(bt->scen, bt->models,
                                                                                          bt->n_models, *buf);
   if ((rc = launch_status("k_form_models"))) return rc;
-  k_merge_batches<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf);
+  k_merge_batches<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
   return launch_status("k_merge_batches");
 }
 
@@ -667,7 +679,7 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
   k_gen_arrivals<<<ceil_div(bt->n_models, kGenWarps), 32 * kGenWarps, 0, st>>>(bt->scen, bt->models, bt->n_models,
                                                                                *buf);
   if ((rc = launch_status("k_gen_arrivals"))) return rc;
-  k_merge_arrivals<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf);
+  k_merge_arrivals<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
   return launch_status("k_merge_arrivals");
 }
 
@@ -681,14 +693,12 @@ int intf_split_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, vo
 
 int intf_form_batches(const intf_batch* bt, const intf_replay_buffers* buf, void* stream) {
   if (!bt || !bt->scen || !bt->models || !buf || bt->n_scen <= 0) return bad_input("intf_form_batches: null argument");
-  if (buf->noise_k > 0 && (!buf->noise_tab || bt->n_scen > 65535))
-    return bad_input("intf_form_batches: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
+  if (buf->noise_k > 0 && !buf->noise_tab) return bad_input("intf_form_batches: noise_k > 0 needs noise_tab");
   cudaStream_t st = as_stream(stream);
   int rc;
   if ((rc = launch_formation(bt, buf, st))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
-    dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
-    k_noise_table<<<grid, 128, 0, st>>>(bt->scen, *buf);
+    k_noise_table<<<bt->n_scen < 65535 ? bt->n_scen : 65535, 256, 0, st>>>(bt->scen, bt->n_scen, *buf);
     if ((rc = launch_status("k_noise_table"))) return rc;
   }
   return INTF_OK;
@@ -741,14 +751,12 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
   if (!bt || !bt->scen || !bt->models || !buf || !table || bt->n_scen <= 0) return bad_input("intf_replay: null argument");
   if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1 || buf->noise_k < 0)
     return bad_input("intf_replay: cap_max must be in [1, 8], seg_stride >= 1, noise_k >= 0");
-  if (buf->noise_k > 0 && (!buf->noise_tab || bt->n_scen > 65535))
-    return bad_input("intf_replay: noise_k > 0 needs noise_tab (and <= 65535 scenarios per call)");
+  if (buf->noise_k > 0 && !buf->noise_tab) return bad_input("intf_replay: noise_k > 0 needs noise_tab");
   cudaStream_t st = as_stream(stream);
   int rc;
   if ((rc = launch_formation(bt, buf, st))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
-    dim3 grid(ceil_div((long long)bt->max_req_cap * buf->noise_k, 128), bt->n_scen);
-    k_noise_table<<<grid, 128, 0, st>>>(bt->scen, *buf);
+    k_noise_table<<<bt->n_scen < 65535 ? bt->n_scen : 65535, 256, 0, st>>>(bt->scen, bt->n_scen, *buf);
     if ((rc = launch_status("k_noise_table"))) return rc;
   }
   k_replay_warp<<<ceil_div(bt->n_scen, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, st>>>(
@@ -787,17 +795,15 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
 int intf_features_predict(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
                           const intf_predictor* preds, int32_t n_pred, int64_t slot_stride, double* X, double* y,
                           double* yhat, void* stream) {
-  if (!bt || !bt->scen || !bt->models || !buf || !table || !y || (n_pred && !yhat) || bt->n_scen <= 0 ||
-      bt->n_scen > 65535)
+  if (!bt || !bt->scen || !bt->models || !buf || !table || !y || (n_pred && !yhat) || bt->n_scen <= 0)
     return bad_input("intf_features_predict: bad argument");
   if (n_pred < 0 || n_pred > kMaxPred || (n_pred && !preds)) return bad_input("intf_features_predict: n_pred in [0,8]");
   PredBlock P;
   memset(&P, 0, sizeof(P));
   for (int i = 0; i < n_pred; i++) P.p[i] = preds[i];
   if (bt->max_req_cap <= 0) return INTF_OK;
-  dim3 grid(ceil_div(bt->max_req_cap, 128), bt->n_scen);
-  k_features<<<grid, 128, 0, as_stream(stream)>>>(bt->scen, bt->models, *table, *buf, P, n_pred,
-                                                  (long long)slot_stride, X, y, yhat);
+  k_features<<<bt->n_scen < 65535 ? bt->n_scen : 65535, 128, 0, as_stream(stream)>>>(
+      bt->scen, bt->n_scen, bt->models, *table, *buf, P, n_pred, (long long)slot_stride, X, y, yhat);
   return launch_status("k_features");
 }
 

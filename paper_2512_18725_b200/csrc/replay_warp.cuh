@@ -70,6 +70,94 @@ struct ReplayJobOut {
   double last_done;
 };
 
+// ---------------------------------------------------------------------------
+// concurrency_cap == 1: the same recurrence with nothing to co-locate.  Every
+// batch runs alone, in FIFO (= batch id) order, as one segment [start, done)
+// with colo = 0 and noise draw (b, 0):
+//   start_b = max(now, formed_b)      (formation / completion event order, `simcore.py:246-262`)
+//   done_b  = start_b + total_b * sd_b  (`_reseat` `simcore.py:141`, progress 0)
+// so the serial chain per batch is one max and one add; the slowdowns, the
+// products total*sd and every output are computed 32 batches at a time in
+// parallel.  Same values, same rounding, same status checks as replay_group
+// (zero-length pop, progress check, measured = total if sd == 1.0).
+template <int W>
+__device__ __noinline__ ReplayJobOut replay_cap1(const ReplayJob J, const intf_scenario& S,
+                                                 const intf_model* __restrict__ md, const intf_table tab,
+                                                 const intf_replay_buffers B, int status) {
+  const LaneGroup<W> G;
+  const int lane = G.lane;
+  const int nb = J.b_hi, ro = S.req_off;
+  double now = 0.0, last_done = -INFINITY;
+  int seg_cursor = 0, n_reseats = 0;
+  for (int base = J.b_lo; base < nb; base += W) {
+    const int b = base + lane;
+    const bool valid = b < nb;
+    double tf = 0.0, w = 0.0, total = 1.0, sd = 1.0;
+    if (valid) {
+      const int entry = md[B.b_model[ro + b]].entry_base + B.b_size[ro + b] - 1;
+      tf = B.b_formed[ro + b];
+      total = tab.solo_ms[entry];
+      const double own[3] = {tab.thr[3 * entry], tab.thr[3 * entry + 1], tab.thr[3 * entry + 2]};
+      const double colo[3] = {0.0, 0.0, 0.0};
+      const double noise = B.noise_k > 0 ? B.noise_tab[(size_t)(ro + b) * B.noise_k]
+                                         : noise_draw_slow(S.oracle_seed, S.batch_id_base + (uint64_t)b, 0ull, S.sigma);
+      sd = slowdown(own, colo, S.beta, noise);
+      w = total * sd;  // remaining_work_ms * slowdown, remaining = total - 0.0
+    }
+    // the serial chain, uniform over the group (shuffles are off the chain)
+    const int n = nb - base < W ? nb - base : W;
+    double my_start = 0.0, my_done = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < n; i++) {
+      const double tfi = G.shfl(tf, i), wi = G.shfl(w, i);
+      now = now > tfi ? now : tfi;  // formation (or the completion that freed the GPU)
+      const double st = now;
+      now = now + wi;               // completion: now = done
+      if (i == lane) {
+        my_start = st;
+        my_done = now;
+      }
+    }
+    // close_segment + complete (`simcore.py:56-66,173-198`), in parallel
+    const bool kept = valid && my_done != my_start;  // zero-length segment is popped
+    const double progress = kept ? 0.0 + (my_done - my_start) / sd : 0.0;
+    if (valid && fabs(progress - total) > 1e-6 * total) status |= INTF_ST_PROGRESS;
+    const double measured = (kept && sd != 1.0) ? my_done - my_start : total;
+    const unsigned kmask = G.ballot(kept);
+    const int before = __popc(kmask & ((1u << lane) - 1u));
+    const int nkeep = __popc(kmask);
+    const bool fits = seg_cursor + nkeep <= J.seg_cap;
+    if (!fits) status |= INTF_ST_OVERFLOW;
+    if (valid) {
+      const int off = J.seg_base + seg_cursor + before;
+      B.b_start[ro + b] = my_start;
+      B.b_completion[ro + b] = my_done;
+      B.b_measured[ro + b] = measured;
+      B.b_seg_off[ro + b] = fits ? off : J.seg_base + seg_cursor;
+      B.b_nseg[ro + b] = (kept && fits) ? 1 : 0;
+      B.out_order[ro + b] = b;  // completions are non-decreasing in batch id
+      if (B.b_running) B.b_running[ro + b] = 1;
+      if (kept && fits) {
+        B.s_tbegin[off] = my_start;
+        B.s_tend[off] = my_done;
+        B.s_slowdown[off] = sd;
+        B.s_colo[3 * (size_t)off + 0] = 0.0;
+        B.s_colo[3 * (size_t)off + 1] = 0.0;
+        B.s_colo[3 * (size_t)off + 2] = 0.0;
+      }
+    }
+    if (fits) seg_cursor += nkeep;
+    n_reseats += n;
+    last_done = now;
+  }
+  ReplayJobOut r;
+  r.status = (int)G.reduce_or((unsigned)status);
+  r.n_segments = seg_cursor;
+  r.n_reseats = n_reseats;
+  r.last_done = last_done;
+  return r;
+}
+
 // sseg: this group's shared-memory segment history, [kMaxCap][kSmemSeg][5]
 template <int W>
 __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const intf_scenario* __restrict__ scens,
@@ -81,6 +169,7 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
   const intf_scenario& S = scens[s];
   const int cap = S.cap, nb = J.b_hi, ro = S.req_off;
   const intf_model* md = models + S.model_off;
+  if (cap == 1) return replay_cap1<W>(J, S, md, tab, B, status);
   const int K = B.noise_k < kWarpNoiseK ? B.noise_k : kWarpNoiseK;
   double* myseg = B.slot_seg + ((size_t)J.scratch * B.cap_max + lane) * (size_t)B.seg_stride * 5;
 
@@ -134,6 +223,7 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
     if (!doit) return;
     double noise;
     if (nseg < K) noise = nseg == 0 ? nz0 : nseg == 1 ? nz1 : nseg == 2 ? nz2 : nz3;
+    else if (nseg < B.noise_k) noise = B.noise_tab[(size_t)(ro + batch) * B.noise_k + nseg];  // precomputed, L2
     else noise = noise_draw_slow(S.oracle_seed, S.batch_id_base + (uint64_t)batch, (uint64_t)nseg, S.sigma);
     const double o[3] = {own0, own1, own2}, colo[3] = {c0, c1, c2};
     const double sd = slowdown(o, colo, S.beta, noise);

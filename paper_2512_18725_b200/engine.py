@@ -58,13 +58,13 @@ class ReplayPipeline:
     """
 
     def __init__(self, specs, table: _pack.TableArrays, seg_stride: int = 64, scale: float = 1.0,
-                 preds=(), list_caps=None, dtable: DeviceTable | None = None, noise_k: int = 4):
+                 preds=(), list_caps=None, dtable: DeviceTable | None = None, noise_k: int = 6):
         self.dev = require_cuda()
         self.lib = _abi.load()
         self.pb = _pack.pack(list(specs), table, scale=scale, list_caps=list_caps)
         self.seg_stride = int(seg_stride)
         self.dtable = dtable or DeviceTable(table, self.dev)
-        self.noise_k = int(noise_k) if self.pb.n_scen <= 65535 else 0
+        self.noise_k = int(noise_k)
         sz = _pack.sizes(self.pb, self.seg_stride, self.noise_k)
         self.t = {f: torch.zeros(sz[k], dtype=_TORCH_DT[dt], device=self.dev) for f, dt, k in _pack.BUFFER_PLAN}
         self.B = _abi.ReplayBuffers()

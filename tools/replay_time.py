@@ -10,10 +10,11 @@ from paper_2512_18725_b200.profiles import gen_synthetic_profiles
 from paper_2512_18725_b200.sweep import c5_scenarios
 
 table = gen_synthetic_profiles()
-for n in [int(a) for a in sys.argv[1:]] or [10000]:
+NK = [int(a) for a in os.environ.get("NOISE_K", "4").split(",")]
+for n, nk in [(int(a), k) for a in (sys.argv[1:] or ["10000"]) for k in NK]:
     specs = c5_scenarios(table, n, start=0)
     specs.sort(key=lambda d: -sum(m["arrival_rate_rps"] for m in d["deployed"]) * d["duration_s"])
-    pipe = engine.ReplayPipeline(specs, table.arrays(), scale=1.5)
+    pipe = engine.ReplayPipeline(specs, table.arrays(), scale=1.5, noise_k=nk)
     for _ in range(2):
         pipe.run()
     torch.cuda.synchronize()
@@ -24,4 +25,4 @@ for n in [int(a) for a in sys.argv[1:]] or [10000]:
     e[1].record()
     torch.cuda.synchronize()
     ms = e[0].elapsed_time(e[1]) / 5
-    print(f"n={n} {ms:.3f} ms/step {n / ms * 1e3:.0f} replays/s status_nonzero={int((pipe.status() != 0).sum())}")
+    print(f"n={n} noise_k={nk} {ms:.3f} ms/step {n / ms * 1e3:.0f} replays/s status_nonzero={int((pipe.status() != 0).sum())}")
