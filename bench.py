@@ -185,6 +185,7 @@ def _ref_worker(args):
 REFIT_STREAMS = 10000
 REFIT_LEN = 300
 OLS_ROWS = 1 << 24
+REFIT_WINDOW = 64
 
 
 def refit_secondary(a, stream, barrier, max_over_ranks, rank) -> dict:
@@ -251,8 +252,32 @@ def refit_secondary(a, stream, barrier, max_over_ranks, rank) -> dict:
     gbs = 56.0 * OLS_ROWS / (ms / 1e3) / 1e9
     out["ols_stats"] = {"samples_per_s": OLS_ROWS / (ms / 1e3), "ms": ms, "achieved_gbs": gbs, "frac": gbs / peak,
                         "bytes_per_sample": 56}
+    # refit each window (configs[2]): fit_ols_xy on every REFIT_WINDOW-sample window, one stats + one solve launch
+    n_win = (OLS_ROWS + REFIT_WINDOW - 1) // REFIT_WINDOW
+    wstats = torch.empty(n_win * 56, dtype=torch.float64, device="cuda")
+    wparams = torch.empty(n_win * 7, dtype=torch.float64, device="cuda")
+    winfo = torch.empty(n_win * 3, dtype=torch.int32, device="cuda")
+
+    def windows():
+        _abi.check(L.intf_ols_windows(Xo.data_ptr(), yo.data_ptr(), OLS_ROWS, REFIT_WINDOW, wstats.data_ptr(),
+                                      wparams.data_ptr(), winfo.data_ptr(), s), "ols_windows")
+
+    for _ in range(3):
+        windows()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    windows()
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    gbs = 56.0 * OLS_ROWS / (ms / 1e3) / 1e9
+    out["ols_windows"] = {"fits_per_s": n_win / (ms / 1e3), "samples_per_s": OLS_ROWS / (ms / 1e3), "ms": ms,
+                          "window": REFIT_WINDOW, "fits": n_win, "achieved_gbs": gbs, "frac": gbs / peak,
+                          "ridge_windows": int((winfo.view(-1, 3)[:, 0] != 0).sum().item())}
     out["workload"] = (f"{REFIT_STREAMS} concurrent prequential streams x {REFIT_LEN} samples (RLS lambda 0.99, "
-                       f"SGD eta 0.01, fp64); OLS Z^T Z / Z^T y over {OLS_ROWS} samples")
+                       f"SGD eta 0.01, fp64); OLS Z^T Z / Z^T y over {OLS_ROWS} samples; refit each window of "
+                       f"{REFIT_WINDOW} samples over the same {OLS_ROWS} samples")
     return out
 
 

@@ -268,6 +268,18 @@ int intf_ols_stats(const double *X, const double *y, int64_t n, double *out, dou
  * (optional, 49) = inv(Z^T Z) for rls_init.                                 */
 int intf_ols_solve(const double *stats, double *out_params, int32_t *out_info, double *out_Pinv, void *stream);
 
+/* Windowed refit ("refit each window", BASELINE configs[2]): fit_ols_xy
+ * (`predict.py:53-72`) on every window of `window` consecutive rows of X
+ * (n x 6, row-major) / y: n_win = ceil(n / window) fits.  stats: caller
+ * scratch of n_win*56 doubles (Z^T Z | Z^T y per window; may be NULL for
+ * windows of <= 128 rows, which are reduced and solved in one launch);
+ * params: n_win*7
+ * (w0..w5, b); info: n_win*3 int32 = ridge fallback used, non-finite result
+ * (PredictError), fewer than 7 rows (fit_ols raises PredictError for those;
+ * fit_ols_xy solves them through the ridge fallback, as here).            */
+int intf_ols_windows(const double *X, const double *y, int64_t n, int32_t window, double *stats, double *params,
+                     int32_t *info, void *stream);
+
 /* Prequential online learners (`predict.py:75-205`, `score_and_update`):
  * n_streams independent streams, stream s = samples [off[s], off[s+1]) of
  * X/y.  Each stream starts from params0[s][7] (and P0[s][49] for RLS),

@@ -102,6 +102,7 @@ SIGNATURES = {
     "intf_repr_f64": (c_int32, [c_double, P, c_int32]),
     "intf_ols_stats": (c_int32, [P, P, c_int64, P, P, P]),
     "intf_ols_solve": (c_int32, [P, P, P, P, P]),
+    "intf_ols_windows": (c_int32, [P, P, c_int64, c_int32, P, P, P, P]),
     "intf_sgd_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P]),
     "intf_rls_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P, P]),
     "intf_eval_report": (c_int32, [P, P, P, c_int32, P, P]),

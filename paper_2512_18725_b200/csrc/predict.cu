@@ -611,19 +611,46 @@ __device__ bool chol_solve(const double* A, const double* b, double* x, double* 
 // fit_ols_xy (`predict.py:53-66`): matrix_rank(Z) < 7 -> ridge solve, else
 // least squares (normal equations; lstsq and Cholesky agree to ~cond*eps).
 // rank test: S_i = sqrt(eig(Z^T Z)); rank = #(S_i > S_max * max(n, 7) * eps).
-__global__ void k_ols_solve(const double* __restrict__ stats, double* params, int32_t* info, double* Pinv) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, double* params, int32_t* info,
+                                              double* Pinv) {
   double G[49], r[7], ev[7];
   for (int i = 0; i < 49; i++) G[i] = stats[i];
   for (int i = 0; i < 7; i++) r[i] = stats[49 + i];
   const double n = G[48];
-  jacobi_eigs(G, ev);
-  double smax = 0.0;
-  for (int i = 0; i < 7; i++) smax = fmax(smax, sqrt(fmax(ev[i], 0.0)));
-  const double tol = smax * fmax(n, 7.0) * 2.220446049250313e-16;
-  int rank = 0;
-  for (int i = 0; i < 7; i++) rank += sqrt(fmax(ev[i], 0.0)) > tol;
-  const bool ridge = rank < 7;
+  // rank test.  Screen first: with G = LL^T and Ginv from L, ev_min >=
+  // 1/||Ginv||_F and ev_max <= ||G||_F, so ||G||_F ||Ginv||_F < 1e10 proves
+  // ev_min > 1e-10 ev_max, far above both the SVD tolerance (max(n,7) eps)^2
+  // ev_max and the eigenvalue error (~1e-15 ev_max) -- the eigenvalue test
+  // below would find rank 7.  Only windows that fail the screen pay for it.
+  bool full = false;
+  {
+    double L[7][7];
+    if (chol7(G, L)) {
+      double gf = 0.0, hf = 0.0;
+#pragma unroll
+      for (int i = 0; i < 49; i++) gf += G[i] * G[i];
+#pragma unroll
+      for (int c = 0; c < 7; c++) {
+        double e[7], col[7];
+#pragma unroll
+        for (int i = 0; i < 7; i++) e[i] = (i == c) ? 1.0 : 0.0;
+        chol7_solve(L, e, col);
+#pragma unroll
+        for (int i = 0; i < 7; i++) hf += col[i] * col[i];
+      }
+      full = isfinite(hf) && sqrt(gf) * sqrt(hf) < 1e10;
+    }
+  }
+  bool ridge = false;
+  if (!full) {
+    jacobi_eigs(G, ev);
+    double smax = 0.0;
+    for (int i = 0; i < 7; i++) smax = fmax(smax, sqrt(fmax(ev[i], 0.0)));
+    const double tol = smax * fmax(n, 7.0) * 2.220446049250313e-16;
+    int rank = 0;
+    for (int i = 0; i < 7; i++) rank += sqrt(fmax(ev[i], 0.0)) > tol;
+    ridge = rank < 7;
+  }
   double A[49];
   for (int i = 0; i < 49; i++) A[i] = G[i];
   if (ridge)
@@ -651,6 +678,121 @@ __global__ void k_ols_solve(const double* __restrict__ stats, double* params, in
       chol_solve(B, nullptr, nullptr, Pinv);
     }
   }
+}
+
+__global__ void k_ols_solve(const double* __restrict__ stats, double* params, int32_t* info, double* Pinv) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  ols_solve_one(stats, params, info, Pinv);
+}
+
+// ---- windowed refit (C3, "refit each window"): fit_ols on every window of
+// `window` consecutive samples (`predict.py:53-72` per window).  Statistics:
+// one warp per window, lanes stride the rows, a fixed xor-butterfly sum (so
+// the result is deterministic); solve: one thread per window.
+constexpr int kWinWarps = 8;
+__global__ void __launch_bounds__(32 * kWinWarps) k_ols_window_stats(const double* __restrict__ X,
+                                                                   const double* __restrict__ y, long long n,
+                                                                   int window, long long n_win,
+                                                                   double* __restrict__ stats) {
+  const long long w = (long long)blockIdx.x * kWinWarps + (threadIdx.x >> 5);
+  if (w >= n_win) return;
+  const int lane = threadIdx.x & 31;
+  const long long lo = w * window, hi = lo + window < n ? lo + window : n;
+  double acc[kStats];
+#pragma unroll
+  for (int i = 0; i < kStats; i++) acc[i] = 0.0;
+  for (long long row = lo + lane; row < hi; row += 32) {
+    double z[7];
+#pragma unroll
+    for (int i = 0; i < 6; i++) z[i] = X[row * 6 + i];
+    z[6] = 1.0;
+    const double yy = y[row];
+    int t = 0;
+#pragma unroll
+    for (int i = 0; i < 7; i++)
+#pragma unroll
+      for (int j = i; j < 7; j++) acc[t] = fma(z[i], z[j], acc[t]), t++;
+#pragma unroll
+    for (int i = 0; i < 7; i++) acc[28 + i] = fma(z[i], yy, acc[28 + i]);
+  }
+  double* out = stats + w * 56;
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = i; j < 7; j++, t++) {
+      const double v = warp_sum(acc[t]);
+      if (lane == (t & 31)) {  // spread the 56 stores over the lanes
+        out[i * 7 + j] = v;
+        out[j * 7 + i] = v;
+      }
+    }
+#pragma unroll
+  for (int i = 0; i < 7; i++) {
+    const double v = warp_sum(acc[28 + i]);
+    if (lane == i) out[49 + i] = v;
+  }
+}
+
+// small windows (<= kFusedWindow rows): one thread per window accumulates its
+// statistics sequentially in registers (no cross-lane reduction) and solves
+// in place; the statistics reach HBM only if the caller asked for them.
+constexpr int kFusedWindow = 128;
+__global__ void __launch_bounds__(128) k_ols_windows_fused(const double* __restrict__ X, const double* __restrict__ y,
+                                                           long long n, int window, long long n_win,
+                                                           double* __restrict__ stats, double* __restrict__ params,
+                                                           int32_t* __restrict__ info) {
+  const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n_win) return;
+  const long long lo = w * window, hi = lo + window < n ? lo + window : n;
+  double acc[kStats];
+#pragma unroll
+  for (int i = 0; i < kStats; i++) acc[i] = 0.0;
+#pragma unroll 4  // four rows' loads in flight per thread (memory-level parallelism at 2 blocks/SM)
+  for (long long row = lo; row < hi; row++) {
+    const double2* xr = reinterpret_cast<const double2*>(X + row * 6);
+    const double2 a = __ldg(xr), b = __ldg(xr + 1), c = __ldg(xr + 2);
+    const double z[7] = {a.x, a.y, b.x, b.y, c.x, c.y, 1.0};
+    const double yy = __ldg(y + row);
+    int t = 0;
+#pragma unroll
+    for (int i = 0; i < 7; i++)
+#pragma unroll
+      for (int j = i; j < 7; j++) acc[t] = fma(z[i], z[j], acc[t]), t++;
+#pragma unroll
+    for (int i = 0; i < 7; i++) acc[28 + i] = fma(z[i], yy, acc[28 + i]);
+  }
+  double st[56];
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = i; j < 7; j++, t++) st[i * 7 + j] = st[j * 7 + i] = acc[t];
+#pragma unroll
+  for (int i = 0; i < 7; i++) st[49 + i] = acc[28 + i];
+  if (stats) {
+#pragma unroll
+    for (int i = 0; i < 56; i++) stats[w * 56 + i] = st[i];
+  }
+  int32_t inf2[2] = {0, 0};
+  ols_solve_one(st, params + w * 7, inf2, nullptr);
+  info[3 * w] = inf2[0];
+  info[3 * w + 1] = inf2[1];
+  info[3 * w + 2] = hi - lo < 7 ? 1 : 0;
+}
+
+// info[3w..]: ridge used, non-finite params, fewer than 7 rows (fit_ols raises
+// PredictError for those; fit_ols_xy solves them through the ridge fallback)
+__global__ void k_ols_window_solve(const double* __restrict__ stats, long long n_win, long long n, int window,
+                                   double* __restrict__ params, int32_t* __restrict__ info) {
+  const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n_win) return;
+  const long long cnt = (w + 1) * window <= n ? window : n - w * window;
+  int32_t inf2[2] = {0, 0};
+  ols_solve_one(stats + w * 56, params + w * 7, inf2, nullptr);
+  info[3 * w] = inf2[0];
+  info[3 * w + 1] = inf2[1];
+  info[3 * w + 2] = cnt < 7 ? 1 : 0;
 }
 
 // ===================================================================== K7
@@ -1026,6 +1168,24 @@ int intf_ols_solve(const double* stats, double* out_params, int32_t* out_info, d
   if (!stats || !out_params) return bad_input("intf_ols_solve: null argument");
   k_ols_solve<<<1, 32, 0, as_stream(stream)>>>(stats, out_params, out_info, out_Pinv);
   return launch_status("k_ols_solve");
+}
+
+int intf_ols_windows(const double* X, const double* y, int64_t n, int32_t window, double* stats, double* params,
+                     int32_t* info, void* stream) {
+  if (!X || !y || !params || !info || n < 0 || window < 1 || (!stats && window > kFusedWindow))
+    return bad_input("intf_ols_windows: bad argument (stats scratch needed for windows > 128 rows)");
+  const long long n_win = (n + window - 1) / window;
+  if (n_win == 0) return INTF_OK;
+  cudaStream_t st = as_stream(stream);
+  if (window <= kFusedWindow) {
+    k_ols_windows_fused<<<ceil_div(n_win, 128), 128, 0, st>>>(X, y, (long long)n, window, n_win, stats, params, info);
+    return launch_status("k_ols_windows_fused");
+  }
+  k_ols_window_stats<<<ceil_div(n_win, kWinWarps), 32 * kWinWarps, 0, st>>>(X, y, (long long)n, window, n_win, stats);
+  int rc = launch_status("k_ols_window_stats");
+  if (rc) return rc;
+  k_ols_window_solve<<<ceil_div(n_win, 128), 128, 0, st>>>(stats, n_win, (long long)n, window, params, info);
+  return launch_status("k_ols_window_solve");
 }
 
 int intf_sgd_streams(const double* X, const double* y, const int64_t* off, int32_t n_streams, const double* eta,

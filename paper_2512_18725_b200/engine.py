@@ -322,6 +322,22 @@ def ols_solve(stats, want_pinv=False):
             pinv.cpu().numpy().reshape(7, 7) if want_pinv else None)
 
 
+def ols_windows(X, y, window: int):
+    """fit_ols_xy on every window of `window` consecutive rows (one launch of
+    statistics, one of solves) -> host (params[n_win, 7], info[n_win, 3])."""
+    dev = require_cuda()
+    dX = X if isinstance(X, torch.Tensor) else _f64(np.asarray(X, dtype=np.float64).reshape(-1, 6), dev)
+    dy = y if isinstance(y, torch.Tensor) else _f64(y, dev)
+    n = dy.numel()
+    n_win = (n + window - 1) // window
+    stats = torch.empty(max(n_win, 1) * 56, dtype=torch.float64, device=dev)
+    params = torch.empty(max(n_win, 1) * 7, dtype=torch.float64, device=dev)
+    info = torch.zeros(max(n_win, 1) * 3, dtype=torch.int32, device=dev)
+    _abi.check(_abi.load().intf_ols_windows(dX.data_ptr(), dy.data_ptr(), n, int(window), stats.data_ptr(),
+                                            params.data_ptr(), info.data_ptr(), stream_ptr()), "intf_ols_windows")
+    return params.cpu().numpy().reshape(-1, 7)[:n_win], info.cpu().numpy().reshape(-1, 3)[:n_win]
+
+
 def _streams(X_list, y_list, dev):
     off = np.zeros(len(X_list) + 1, dtype=np.int64)
     for i, y in enumerate(y_list):

@@ -82,6 +82,26 @@ def fit_ols(samples) -> LinearModel:
     return fit_ols_xy(*_design(samples))
 
 
+def fit_ols_windows(X, y, window: int) -> list:
+    """Refit each window: `[fit_ols_xy(X[i:i+window], y[i:i+window]) for i
+    in range(0, n, window)]` (`predict.py:53-66`), all windows in one
+    statistics launch and one solve launch (a window of fewer than 7 rows is
+    rank-deficient and takes the ridge fallback, as in fit_ols_xy)."""
+    from . import engine
+
+    X = np.asarray(X, dtype=float).reshape(-1, 6)
+    y = np.asarray(y, dtype=float)
+    params, info = engine.ols_windows(X, y, int(window))
+    out = []
+    for k, (p, inf) in enumerate(zip(params, info)):
+        if inf[0]:
+            log.warning("rank-deficient design matrix (window %d), using ridge fallback", k)
+        model = LinearModel(w=p[:6].copy(), b=float(p[6]))
+        model.check_finite("after OLS fit")
+        out.append(model)
+    return out
+
+
 @dataclass
 class SgdState:
     model: LinearModel

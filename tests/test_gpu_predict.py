@@ -102,3 +102,23 @@ def test_ewma_experiment_matches_reference():
         r = row.report
         np.testing.assert_allclose([r.mse, r.rel_p25, r.rel_p50, r.rel_p75, r.rel_p95, r.n_samples],
                                    P[f"ewma/mode{mi}/report"], rtol=RTOL)
+
+
+@pytest.mark.parametrize("window", [64, 100, 333])
+def test_windowed_refit_matches_reference(window):
+    """Refit each window (BASELINE configs[2]): one statistics + one solve
+    launch for every window vs the reference's fit_ols_xy per window
+    (tests/golden/refit_golden.npz), incl. a rank-deficient (ridge) window and
+    a 1-row tail window."""
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200.predict import fit_ols_windows
+
+    R = _golden.load("refit_golden.npz")
+    fits = fit_ols_windows(R["X"], R["y"], window)
+    got = np.array([m.w7() for m in fits])
+    ref = R[f"w{window}"]
+    assert got.shape == ref.shape
+    np.testing.assert_allclose(got, ref, rtol=RTOL, atol=1e-7)
+    # the first window equals the single-fit path
+    m0 = p.fit_ols_xy(R["X"][:window], R["y"][:window])
+    np.testing.assert_allclose(got[0], m0.w7(), rtol=1e-9, atol=1e-12)
