@@ -87,7 +87,7 @@ typedef struct intf_batch {
   int32_t max_req_cap;         /* max over scenarios of req_cap */
   int32_t max_models;          /* max over scenarios of n_models */
   int32_t max_list_cap;        /* max over deployed models of list_cap */
-  int32_t pad_;
+  int32_t req_slots;           /* sum over scenarios of req_cap (packed request / batch slot space) */
 } intf_batch;
 
 #define INTF_SLO_WS_INTS (256 + 32 * 3 * 256 + 32 * 3 * 4)

@@ -46,7 +46,8 @@ class Model(ctypes.Structure):
 
 class Batch(ctypes.Structure):
     _fields_ = [("scen", P), ("models", P), ("n_scen", c_int32), ("n_models", c_int32),
-                ("max_req_cap", c_int32), ("max_models", c_int32), ("max_list_cap", c_int32), ("pad_", c_int32)]
+                ("max_req_cap", c_int32), ("max_models", c_int32), ("max_list_cap", c_int32),
+                ("req_slots", c_int32)]
 
 
 REPLAY_BUFFER_FIELDS = [

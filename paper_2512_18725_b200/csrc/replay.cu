@@ -153,18 +153,43 @@ __global__ void k_form_status(const intf_scenario* __restrict__ scen, int n_scen
 // ---- K1b: noise draws of the first noise_k segments of every formed batch
 // (`oracle.py:24-33`), fully parallel: takes the SeedSequence/PCG64/ziggurat/
 // exp chain off the serial replay recurrence.  grid: (slots, scenarios).
-// grid: one block per scenario (grid-stride over scenarios), looping over
-// the scenario's formed batches x noise_k, so no block is launched for
-// unused capacity slots.
+// scenario owning packed request slot `slot` (req_off is increasing)
+__device__ __forceinline__ int scen_of_slot(const intf_scenario* __restrict__ scen, int n_scen, long long slot) {
+  int lo = 0, hi = n_scen - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (scen[mid].req_off <= slot) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Two launch shapes over the same draws: many scenarios -> one block per
+// scenario (grid-stride over scenarios, looping over its formed batches x
+// noise_k); few scenarios (long traces) -> grid-stride over the packed
+// (request slot, draw) space, the owning scenario found by binary search.
+constexpr int kPerScenarioMin = 4 * 148;  // below this many scenarios, flatten
 __global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __restrict__ scen, int n_scen,
-                                                     intf_replay_buffers B) {
+                                                     long long req_slots, intf_replay_buffers B) {
   const int K = B.noise_k;
-  for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
+  if (n_scen >= kPerScenarioMin) {
+    for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
+      const intf_scenario& S = scen[s];
+      const long long n = (long long)B.n_batches[s] * K;
+      double* out = B.noise_tab + (long long)S.req_off * K;
+      for (long long i = threadIdx.x; i < n; i += blockDim.x)
+        out[i] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)(i / K), (uint64_t)(i % K), S.sigma);
+    }
+    return;
+  }
+  const long long n = req_slots * K;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long slot = i / K;
+    const int s = scen_of_slot(scen, n_scen, slot);
     const intf_scenario& S = scen[s];
-    const long long n = (long long)B.n_batches[s] * K;
-    double* out = B.noise_tab + (long long)S.req_off * K;
-    for (long long i = threadIdx.x; i < n; i += blockDim.x)
-      out[i] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)(i / K), (uint64_t)(i % K), S.sigma);
+    const long long b = slot - S.req_off;
+    if (b < B.n_batches[s])
+      B.noise_tab[i] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)b, (uint64_t)(i % K), S.sigma);
   }
 }
 
@@ -610,35 +635,59 @@ struct PredBlock {
   intf_predictor p[kMaxPred];
 };
 
-__global__ void k_features(const intf_scenario* __restrict__ scen, int n_scen, const intf_model* __restrict__ models,
-                           intf_table tab, intf_replay_buffers B, PredBlock P, int n_pred, long long slot_stride,
-                           double* __restrict__ X, double* __restrict__ Y, double* __restrict__ Yhat) {
-  // one block per scenario (grid-stride), a thread per outcome: no blocks
-  // for unused capacity slots
-  for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
-    const intf_scenario& S = scen[s];
-    const int nb = B.n_batches[s];
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-      const long long slot = (long long)S.req_off + k;
-      const int b = B.out_order[slot];
-      const long long bslot = (long long)S.req_off + b;
-      const int entry = models[S.model_off + B.b_model[bslot]].entry_base + B.b_size[bslot] - 1;
-      const double own[3] = {tab.thr[3 * entry], tab.thr[3 * entry + 1], tab.thr[3 * entry + 2]};
-      const double* colo = B.s_colo + 3ll * B.b_seg_off[bslot];
-      const int nseg = B.b_nseg[bslot];
-      Y[slot] = B.b_measured[bslot] / tab.solo_ms[entry];  // interference ratio (`simcore.py:83-85`)
-      for (int p = 0; p < n_pred; p++) {
-        double x[6];
-        features_one(own, colo, nseg, P.p[p].ewma, P.p[p].alpha, x);
-        if (X) {
-          double* xo = X + (p * slot_stride + slot) * 6;
+// features + predictions of outcome slot `slot` of scenario S
+__device__ __forceinline__ void features_slot(const intf_scenario& S, long long slot,
+                                              const intf_model* __restrict__ models, const intf_table& tab,
+                                              const intf_replay_buffers& B, const PredBlock& P, int n_pred,
+                                              long long slot_stride, double* __restrict__ X, double* __restrict__ Y,
+                                              double* __restrict__ Yhat) {
+  const int b = B.out_order[slot];
+  const long long bslot = (long long)S.req_off + b;
+  const int entry = models[S.model_off + B.b_model[bslot]].entry_base + B.b_size[bslot] - 1;
+  const double own[3] = {tab.thr[3 * entry], tab.thr[3 * entry + 1], tab.thr[3 * entry + 2]};
+  const double* colo = B.s_colo + 3ll * B.b_seg_off[bslot];
+  const int nseg = B.b_nseg[bslot];
+  Y[slot] = B.b_measured[bslot] / tab.solo_ms[entry];  // interference ratio (`simcore.py:83-85`)
+  for (int p = 0; p < n_pred; p++) {
+    double x[6];
+    features_one(own, colo, nseg, P.p[p].ewma, P.p[p].alpha, x);
+    if (X) {
+      double* xo = X + (p * slot_stride + slot) * 6;
 #pragma unroll
-          for (int i = 0; i < 6; i++) xo[i] = x[i];
-        }
-        Yhat[p * slot_stride + slot] = predict7(P.p[p].w, x);
-      }
+      for (int i = 0; i < 6; i++) xo[i] = x[i];
     }
+    Yhat[p * slot_stride + slot] = predict7(P.p[p].w, x);
   }
+}
+
+// thread per outcome; launch shape as k_noise_table (block per scenario for
+// many scenarios, grid-stride over packed slots for few long ones)
+__global__ void k_features(const intf_scenario* __restrict__ scen, int n_scen, long long req_slots,
+                           const intf_model* __restrict__ models, intf_table tab, intf_replay_buffers B, PredBlock P,
+                           int n_pred, long long slot_stride, double* __restrict__ X, double* __restrict__ Y,
+                           double* __restrict__ Yhat) {
+  if (n_scen >= kPerScenarioMin) {
+    for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
+      const intf_scenario& S = scen[s];
+      const int nb = B.n_batches[s];
+      for (int k = threadIdx.x; k < nb; k += blockDim.x)
+        features_slot(S, (long long)S.req_off + k, models, tab, B, P, n_pred, slot_stride, X, Y, Yhat);
+    }
+    return;
+  }
+  for (long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x; slot < req_slots;
+       slot += (long long)gridDim.x * blockDim.x) {
+    const int s = scen_of_slot(scen, n_scen, slot);
+    if (slot - scen[s].req_off < B.n_batches[s])
+      features_slot(scen[s], slot, models, tab, B, P, n_pred, slot_stride, X, Y, Yhat);
+  }
+}
+
+unsigned noise_grid(const intf_batch* bt, int K) {
+  if (bt->n_scen >= kPerScenarioMin) return bt->n_scen < 65535 ? bt->n_scen : 65535;
+  const long long n = (long long)bt->req_slots * K;
+  const long long blocks = (n + 255) / 256;
+  return (unsigned)(blocks < 148 * 16 ? (blocks > 0 ? blocks : 1) : 148 * 16);
 }
 
 // (element chunks, models): enough blocks per model list that long traces use
@@ -698,7 +747,8 @@ int intf_form_batches(const intf_batch* bt, const intf_replay_buffers* buf, void
   int rc;
   if ((rc = launch_formation(bt, buf, st))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
-    k_noise_table<<<bt->n_scen < 65535 ? bt->n_scen : 65535, 256, 0, st>>>(bt->scen, bt->n_scen, *buf);
+    k_noise_table<<<noise_grid(bt, buf->noise_k), 256, 0, st>>>(bt->scen, bt->n_scen, (long long)bt->req_slots,
+                                                                 *buf);
     if ((rc = launch_status("k_noise_table"))) return rc;
   }
   return INTF_OK;
@@ -756,7 +806,8 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
   int rc;
   if ((rc = launch_formation(bt, buf, st))) return rc;
   if (buf->noise_k > 0 && bt->max_req_cap > 0) {
-    k_noise_table<<<bt->n_scen < 65535 ? bt->n_scen : 65535, 256, 0, st>>>(bt->scen, bt->n_scen, *buf);
+    k_noise_table<<<noise_grid(bt, buf->noise_k), 256, 0, st>>>(bt->scen, bt->n_scen, (long long)bt->req_slots,
+                                                                 *buf);
     if ((rc = launch_status("k_noise_table"))) return rc;
   }
   k_replay_warp<<<ceil_div(bt->n_scen, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, st>>>(
@@ -802,8 +853,12 @@ int intf_features_predict(const intf_batch* bt, const intf_table* table, const i
   memset(&P, 0, sizeof(P));
   for (int i = 0; i < n_pred; i++) P.p[i] = preds[i];
   if (bt->max_req_cap <= 0) return INTF_OK;
-  k_features<<<bt->n_scen < 65535 ? bt->n_scen : 65535, 128, 0, as_stream(stream)>>>(
-      bt->scen, bt->n_scen, bt->models, *table, *buf, P, n_pred, (long long)slot_stride, X, y, yhat);
+  const long long blocks = ((long long)bt->req_slots + 127) / 128;
+  const unsigned grid = bt->n_scen >= kPerScenarioMin ? (bt->n_scen < 65535 ? bt->n_scen : 65535)
+                                                      : (unsigned)(blocks < 148 * 32 ? (blocks > 0 ? blocks : 1) : 148 * 32);
+  k_features<<<grid, 128, 0, as_stream(stream)>>>(
+      bt->scen, bt->n_scen, (long long)bt->req_slots, bt->models, *table, *buf, P, n_pred, (long long)slot_stride, X,
+      y, yhat);
   return launch_status("k_features");
 }
 

@@ -75,7 +75,8 @@ class ReplayPipeline:
         self.d_models = to_device(_struct_bytes(self.pb.models), self.dev)
         self.batch = _abi.Batch(self.d_scen.data_ptr(), self.d_models.data_ptr(), self.pb.n_scen, self.pb.n_models,
                                 self.pb.max_req_cap, max((len(n) for n in self.pb.names), default=0),
-                                max((self.pb.models[g].list_cap for g in range(self.pb.n_models)), default=0), 0)
+                                max((self.pb.models[g].list_cap for g in range(self.pb.n_models)), default=0),
+                                self.pb.total_req)
         n_models = max(self.pb.n_models, 1)
         self.slo_n = torch.zeros(n_models, dtype=torch.int32, device=self.dev)
         self.slo_met = torch.zeros(n_models, dtype=torch.int32, device=self.dev)

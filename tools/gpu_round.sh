@@ -12,7 +12,7 @@ timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_launch_$TAG.log 2>&1
-for K in k_cand_step k_cand_stream k_cand_prep k_replay_warp k_form k_noise_table k_gen_arrivals k_slo k_rls k_ols_partial; do
+for K in k_cand_step k_replay_warp k_form_models k_merge_batches k_noise_table k_gen_arrivals k_slo k_features k_rls k_sgd k_ols_partial k_ols_windows_fused; do
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_${TAG}_$K \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_${TAG}_$K.log 2>&1
 done
