@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __rest
 // ---- K2: the replay recurrence, one kReplayW-lane group per scenario (lane
 // l < cap owns running slot l; replay_warp.cuh).
 #ifndef INTF_REPLAY_MINB
-#define INTF_REPLAY_MINB 4
+#define INTF_REPLAY_MINB 3  // 170 registers: no spills in the cap-templated replay (B200: C5 10^4 7.36 -> 6.77 ms)
 #endif
 constexpr int kReplayWarps = 4;
 constexpr int kReplayW = 32;  // measured: one scenario per warp beats 4 x 8-lane groups (divergence)

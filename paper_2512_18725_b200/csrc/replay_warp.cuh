@@ -159,17 +159,19 @@ __device__ __noinline__ ReplayJobOut replay_cap1(const ReplayJob J, const intf_s
 }
 
 // sseg: this group's shared-memory segment history, [kMaxCap][kSmemSeg][5]
-template <int W>
-__device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const intf_scenario* __restrict__ scens,
-                                                     const intf_model* __restrict__ models, const intf_table tab,
-                                                     const intf_replay_buffers B, double* sseg, int status) {
+// CAPT > 0: the concurrency cap as a compile-time constant (unrolled
+// running-list loops, constant reduction span); 0: runtime cap.
+template <int W, int CAPT>
+__device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const intf_scenario* __restrict__ scens,
+                                                    const intf_model* __restrict__ models, const intf_table tab,
+                                                    const intf_replay_buffers B, double* sseg, int status) {
+  constexpr int KU = CAPT > 0 ? CAPT : kMaxCap;  // bound of the running-list loops
   const LaneGroup<W> G;
   const int lane = G.lane;
   const int s = J.s;
   const intf_scenario& S = scens[s];
-  const int cap = S.cap, nb = J.b_hi, ro = S.req_off;
+  const int cap = CAPT > 0 ? CAPT : S.cap, nb = J.b_hi, ro = S.req_off;
   const intf_model* md = models + S.model_off;
-  if (cap == 1) return replay_cap1<W>(J, S, md, tab, B, status);
   const int K = B.noise_k < kWarpNoiseK ? B.noise_k : kWarpNoiseK;
   double* myseg = B.slot_seg + ((size_t)J.scratch * B.cap_max + lane) * (size_t)B.seg_stride * 5;
 
@@ -181,6 +183,11 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
 
   // ---- group-uniform state
   unsigned long long runlist = 0ull;  // 4-bit lane ids in dispatch order
+  // (CAPT > 0) throughputs of the running batches in running-list order, held
+  // by every lane: colo sums without shuffles
+  double u0[KU], u1[KU], u2[KU];
+#pragma unroll
+  for (int k = 0; k < KU; k++) u0[k] = u1[k] = u2[k] = 0.0;
   int nrun = 0;
   unsigned freemask = (cap >= 32) ? 0xffffffffu : ((1u << cap) - 1u);
   double now = 0.0;
@@ -211,13 +218,26 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
   // the group calls it together (group-uniform shuffles inside)
   auto reseat_lane = [&](bool doit) {
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    for (int k = 0; k < nrun; k++) {  // group-uniform loop, running-list order
-      const int j = (int)((runlist >> (4 * k)) & 15ull);
-      const double a0 = G.shfl(own0, j), a1 = G.shfl(own1, j), a2 = G.shfl(own2, j);
-      if (j != lane) {
-        c0 = c0 + a0;
-        c1 = c1 + a1;
-        c2 = c2 + a2;
+    if constexpr (CAPT > 0) {
+#pragma unroll
+      for (int k = 0; k < KU; k++) {  // running-list order, skipping this lane's own batch
+        if (k < nrun && (int)((runlist >> (4 * k)) & 15ull) != lane) {
+          c0 = c0 + u0[k];
+          c1 = c1 + u1[k];
+          c2 = c2 + u2[k];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < KU; k++) {  // group-uniform loop, running-list order
+        if (k >= nrun) break;
+        const int j = (int)((runlist >> (4 * k)) & 15ull);
+        const double a0 = G.shfl(own0, j), a1 = G.shfl(own1, j), a2 = G.shfl(own2, j);
+        if (j != lane) {
+          c0 = c0 + a0;
+          c1 = c1 + a1;
+          c2 = c2 + a2;
+        }
       }
     }
     if (!doit) return;
@@ -342,13 +362,26 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
       last_done = now;
       // remove cl from the running list, keep order
       unsigned long long nl = 0ull;
-      int w = 0;
-      for (int k = 0; k < nrun; k++) {
+      int w = 0, pc = 0;
+#pragma unroll
+      for (int k = 0; k < KU; k++) {
+        if (k >= nrun) break;
         const unsigned long long j = (runlist >> (4 * k)) & 15ull;
         if ((int)j != cl) nl |= j << (4 * w++);
+        else pc = k;
       }
       runlist = nl;
       nrun = w;
+      if constexpr (CAPT > 0) {
+#pragma unroll
+        for (int k = 0; k + 1 < KU; k++) {
+          if (k >= pc) {
+            u0[k] = u0[k + 1];
+            u1[k] = u1[k + 1];
+            u2[k] = u2[k + 1];
+          }
+        }
+      }
       freemask |= 1u << cl;
       // _colo_changed(survivors) (`simcore.py:143-146`)
       if (act) close_lane();
@@ -374,6 +407,18 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
       runlist |= (unsigned long long)L << (4 * nrun);
       nrun++;
       const bool was_act = act;
+      if constexpr (CAPT > 0) {  // every lane appends the new batch's throughputs (broadcast loads)
+        const int e = md[m].entry_base + sz - 1;
+        const double t0 = tab.thr[3 * e], t1 = tab.thr[3 * e + 1], t2 = tab.thr[3 * e + 2];
+#pragma unroll
+        for (int k = 0; k < KU; k++) {
+          if (k == nrun - 1) {
+            u0[k] = t0;
+            u1[k] = t1;
+            u2[k] = t2;
+          }
+        }
+      }
       if (lane == L) {
         const int entry = md[m].entry_base + sz - 1;
         if (B.b_running) B.b_running[ro + b] = nrun;  // dispatch trace
@@ -405,6 +450,21 @@ __device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const in
   r.n_reseats = n_reseats;
   r.last_done = last_done;
   return r;
+}
+
+// the replay of one job: dispatch on the concurrency cap (uniform per group)
+template <int W>
+__device__ __forceinline__ ReplayJobOut replay_group(const ReplayJob J, const intf_scenario* __restrict__ scens,
+                                                     const intf_model* __restrict__ models, const intf_table tab,
+                                                     const intf_replay_buffers B, double* sseg, int status) {
+  const intf_scenario& S = scens[J.s];
+  switch (S.cap) {
+    case 1: return replay_cap1<W>(J, S, models + S.model_off, tab, B, status);
+    case 2: return replay_group_t<W, 2>(J, scens, models, tab, B, sseg, status);
+    case 3: return replay_group_t<W, 3>(J, scens, models, tab, B, sseg, status);
+    case 4: return replay_group_t<W, 4>(J, scens, models, tab, B, sseg, status);
+    default: return replay_group_t<W, 0>(J, scens, models, tab, B, sseg, status);
+  }
 }
 
 // ---------------------------------------------------------------------------
