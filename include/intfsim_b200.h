@@ -117,7 +117,8 @@ typedef struct intf_replay_buffers {
   double *mb_t;                /* scratch, per-model list slots: formation time of the model's c-th batch */
   int32_t *mb_info;            /* scratch, 4 per list slot: kind, key, size, head (list index of first member) */
   int32_t *n_mb;               /* scratch: [total models] batches formed per model */
-  int32_t *slo_ws;             /* scratch: INTF_SLO_WS_INTS int32 for the grid-wide SLO path (long traces) */
+  int32_t *slo_ws;             /* scratch: INTF_SLO_WS_INTS int32 for the grid-wide SLO path (long traces);
+                                  slo_ws[0] is also intf_replay's scenario work counter */
   int32_t seg_stride, cap_max;
   int32_t noise_k, pad_;       /* segments per batch whose noise is precomputed (0 = inline) */
 } intf_replay_buffers;

@@ -200,22 +200,31 @@ __global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __rest
 #endif
 constexpr int kReplayWarps = 4;
 constexpr int kReplayW = 32;  // measured: one scenario per warp beats 4 x 8-lane groups (divergence)
+// Persistent: one block per resident slot (INTF_REPLAY_MINB per SM); each warp
+// pulls the next scenario index from a counter (B.slo_ws[0], free until the
+// SLO pass) as soon as its previous scenario is done, so a long scenario
+// never holds a block's other warps idle (block-granular scheduling would).
 __global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_replay_warp(const intf_scenario* __restrict__ scen,
                                                                     int n_scen, const intf_model* __restrict__ models,
                                                                     intf_table tab, intf_replay_buffers B) {
   __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
   const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
-  const int s = blockIdx.x * kReplayWarps * (32 / kReplayW) + g;
-  if (s >= n_scen) return;
-  const int st0 = B.status[s];
-  if (st0 & (INTF_ST_CAP | INTF_ST_OVERFLOW)) return;
-  const intf_scenario& S = scen[s];
-  const ReplayJob J{s, 0, B.n_batches[s], S.seg_off, S.seg_cap, s};
-  const ReplayJobOut r = replay_group<kReplayW>(J, scen, models, tab, B, sseg[g], st0);
-  if ((threadIdx.x & (kReplayW - 1)) == 0) {
-    B.n_segments[s] = r.n_segments;
-    B.n_reseats[s] = r.n_reseats;
-    B.status[s] = r.status;
+  for (;;) {
+    int s = 0;
+    if ((threadIdx.x & 31) == 0) s = atomicAdd(B.slo_ws, 1);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (s >= n_scen) return;
+    const int st0 = B.status[s];
+    if (st0 & (INTF_ST_CAP | INTF_ST_OVERFLOW)) continue;
+    const intf_scenario& S = scen[s];
+    const ReplayJob J{s, 0, B.n_batches[s], S.seg_off, S.seg_cap, s};
+    const ReplayJobOut r = replay_group<kReplayW>(J, scen, models, tab, B, sseg[g], st0);
+    if ((threadIdx.x & (kReplayW - 1)) == 0) {
+      B.n_segments[s] = r.n_segments;
+      B.n_reseats[s] = r.n_reseats;
+      B.status[s] = r.status;
+    }
+    __syncwarp();
   }
 }
 
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_replay_
 // batches [lo[i], hi[i]) of scenario sc[i] from an idle GPU; its segment
 // records go to S.seg_off + lo*(2cap-1) (a disjoint slice: a batch has at
 // most 2cap-1 reseats), its outcome order to positions [lo, hi).
-__global__ void __launch_bounds__(32 * kReplayWarps, 4) k_replay_jobs(const intf_scenario* __restrict__ scen,
+__global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_replay_jobs(const intf_scenario* __restrict__ scen,
                                                                     const intf_model* __restrict__ models,
                                                                     intf_table tab, intf_replay_buffers B,
                                                                     const int32_t* __restrict__ sc,
@@ -318,7 +327,7 @@ __global__ void __launch_bounds__(128) k_jobs_plan(const intf_scenario* __restri
   }
 }
 
-__global__ void __launch_bounds__(32 * kReplayWarps, 4) k_jobs_replay(const intf_scenario* __restrict__ scen,
+__global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_jobs_replay(const intf_scenario* __restrict__ scen,
                                                                     const intf_model* __restrict__ models,
                                                                     intf_table tab, intf_replay_buffers B,
                                                                     intf_jobs J, int n_todo) {
@@ -810,8 +819,11 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
                                                                  *buf);
     if ((rc = launch_status("k_noise_table"))) return rc;
   }
-  k_replay_warp<<<ceil_div(bt->n_scen, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, st>>>(
-      bt->scen, bt->n_scen, bt->models, *table, *buf);
+  if (!buf->slo_ws) return bad_input("intf_replay: slo_ws scratch (work counter) missing");
+  cudaMemsetAsync(buf->slo_ws, 0, sizeof(int32_t), st);
+  const unsigned per_wave = 148u * INTF_REPLAY_MINB, need = ceil_div(bt->n_scen, kReplayWarps * (32 / kReplayW));
+  k_replay_warp<<<need < per_wave ? need : per_wave, 32 * kReplayWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models,
+                                                                                  *table, *buf);
   return launch_status("k_replay_warp");
 }
 
