@@ -182,6 +182,8 @@ typedef struct intf_jobs {
   int32_t *slot_scen;          /* [slots] owning scenario of each slot (host-filled) */
   double slow;                 /* optimism factor of the speculative end estimate */
   int32_t min_len, total_slots;
+  double *scratch;             /* [6 * total_slots] doubles: block-parallel plan/verify of long traces
+                                  (scenarios with req_cap >= 32768: one 1024-thread block each) */
 } intf_jobs;
 
 int intf_jobs_plan(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf,

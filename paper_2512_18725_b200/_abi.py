@@ -68,7 +68,7 @@ class ReplayBuffers(ctypes.Structure):
 class Jobs(ctypes.Structure):
     _fields_ = [(f, P) for f in ("joff", "jcap", "lo", "hi", "n_jobs", "last", "info", "dirty", "todo",
                                  "todo_count", "slot_scen")] + [("slow", c_double), ("min_len", c_int32),
-                                                                ("total_slots", c_int32)]
+                                                                ("total_slots", c_int32), ("scratch", P)]
 
 
 class Predictor(ctypes.Structure):

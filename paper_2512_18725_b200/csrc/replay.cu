@@ -16,6 +16,113 @@ using namespace intf;
 
 namespace {
 
+constexpr int kBigList = 4096;  // model lists this long: parallel gaps + one-thread scan (long traces)
+constexpr int kBigJobs = 1 << 15;  // scenarios this long: block-parallel job plan / verify
+constexpr int kGapRun = 8;      // consecutive draws per thread in k_gen_gaps
+
+// ---- K0a (long lists, e.g. one 10^6-request trace): every draw's gap of
+// every long model stream in parallel (`workload.py:89-90`): draw d uses the
+// PCG64 state after d+1 steps (LCG jump-ahead), u = (out >> 11) 2^-53,
+// gap = max(-(1000/rate) log1p(-u), 1e-12), written into list_t as scratch.
+__global__ void __launch_bounds__(256) k_gen_gaps(const intf_scenario* __restrict__ scen,
+                                                  const intf_model* __restrict__ models, int n_models_total,
+                                                  intf_replay_buffers B) {
+  const int g = blockIdx.z * gridDim.y + blockIdx.y;
+  if (g >= n_models_total) return;
+  const intf_model& M = models[g];
+  if (M.list_cap < kBigList || M.rate_rps == 0.0) return;
+  const long long d0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kGapRun;
+  if (d0 >= M.list_cap) return;
+  const intf_scenario& S = scen[M.scen];
+  uint32_t w[4];
+  int nw = push_words(w, 0, S.seed);
+  nw = push_words(w, nw, M.crc);
+  const Pcg64 pg = pcg_seed_words(w, nw);
+  const unsigned __int128 mult =
+      ((unsigned __int128)0x2360ed051fc65da4ull << 64) | (unsigned __int128)0x4385df649fccf645ull;
+  unsigned __int128 A, C;
+  lcg_pow(mult, pg.inc, (unsigned long long)(d0 + 1), A, C);
+  unsigned __int128 st = A * pg.state + C;
+  const double neg_mean_gap = -(1000.0 / M.rate_rps);
+  double* out = B.list_t + M.list_off;
+#pragma unroll
+  for (int r = 0; r < kGapRun; r++) {
+    if (d0 + r >= M.list_cap) break;
+    const double u = (double)(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
+    const double gap = neg_mean_gap * glibc_log1p(-u);
+    out[d0 + r] = gap > 1e-12 ? gap : 1e-12;
+    st = mult * st + pg.inc;
+  }
+}
+
+// ---- K0a' (long lists): the cumulative sum t += gap stays strictly
+// sequential (`workload.py:91`: the reference's rounding), one thread per
+// long model, but as a pure add chain that stores only every kScanChunk-th
+// partial sum (into mb_t, free until formation); k_fill_gaps then redoes
+// each chunk's adds -- the same operations in the same order, so the same
+// values -- in parallel and finds the horizon crossing.
+constexpr int kScanChunk = 32;
+__global__ void k_scan_gaps(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                            int n_models_total, intf_replay_buffers B) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_models_total) return;
+  const intf_model& M = models[g];
+  if (M.list_cap < kBigList || M.rate_rps == 0.0) return;
+  const double* lt = B.list_t + M.list_off;
+  double* ends = B.mb_t + M.list_off;
+  constexpr int CH = kScanChunk;
+  const int full = M.list_cap / CH * CH;
+  double t = 0.0;
+  double cur[CH], nxt[CH];
+#pragma unroll
+  for (int k = 0; k < CH; k++) cur[k] = k < full ? lt[k] : 0.0;
+  for (int base = 0; base < full; base += CH) {
+    const bool more = base + CH < full;
+#pragma unroll
+    for (int k = 0; k < CH; k++) nxt[k] = more ? lt[base + CH + k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < CH; k++) t = t + cur[k];
+    ends[base / CH] = t;
+#pragma unroll
+    for (int k = 0; k < CH; k++) cur[k] = nxt[k];
+  }
+}
+
+// thread per (long model, chunk): rebuild the chunk's arrival times from the
+// previous chunk's end; the chunk holding the horizon crossing sets n_list
+__global__ void k_fill_gaps(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                            int n_models_total, intf_replay_buffers B) {
+  const int g = blockIdx.z * gridDim.y + blockIdx.y;
+  if (g >= n_models_total) return;
+  const intf_model& M = models[g];
+  if (M.list_cap < kBigList) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cap = M.list_cap, nch = (cap + kScanChunk - 1) / kScanChunk;
+  if (c >= nch) return;
+  int n = -1;  // set by the thread that decides the count
+  if (M.rate_rps == 0.0) {
+    if (c == 0) n = 0;
+  } else {
+    const double horizon = scen[M.scen].duration_s * 1000.0;
+    double* lt = B.list_t + M.list_off;
+    const double* ends = B.mb_t + M.list_off;
+    double t = c == 0 ? 0.0 : ends[c - 1];
+    const int lo = c * kScanChunk, hi = lo + kScanChunk < cap ? lo + kScanChunk : cap;
+    const bool below0 = t < horizon;  // (the ragged tail chunk also starts at ends[c - 1])
+    for (int d = lo; d < hi; d++) {
+      t = t + lt[d];
+      lt[d] = t;
+      if (n < 0 && below0 && t >= horizon) n = d;
+    }
+    if (n < 0 && hi == cap && t < horizon) n = cap + 1;  // still below the horizon: overflow
+  }
+  if (n >= 0) {
+    if (n > M.list_cap) atomicOr(&B.status[M.scen], INTF_ST_OVERFLOW);
+    B.n_list[g] = n;
+    atomicAdd(&B.n_req[M.scen], n);
+  }
+}
+
 // ---- K0a: one warp per deployed model generates its Poisson stream
 // (warp-cooperative PCG64 jump-ahead, sequential cumulative sum).
 constexpr int kGenWarps = 4;
@@ -26,6 +133,7 @@ __global__ void __launch_bounds__(32 * kGenWarps) k_gen_arrivals(const intf_scen
   const int g = blockIdx.x * kGenWarps + (threadIdx.x >> 5);
   if (g >= n_models_total) return;
   const intf_model& M = models[g];
+  if (M.list_cap >= kBigList) return;  // long lists: k_gen_gaps + k_scan_gaps
   const intf_scenario& S = scen[M.scen];
   const int n = gen_model_arrivals_warp(S, M, B.list_t + M.list_off, M.list_cap, gaps[threadIdx.x >> 5]);
   if ((threadIdx.x & 31) == 0) {
@@ -272,6 +380,7 @@ __global__ void __launch_bounds__(128) k_jobs_plan(const intf_scenario* __restri
   const LaneGroup<32> G;
   const int lane = G.lane;
   const intf_scenario& S = scen[s];
+  if (S.req_cap >= kBigJobs) return;  // k_jobs_plan_big
   const int nb = B.n_batches[s], ro = S.req_off, joff = J.joff[s], jcap = J.jcap[s];
   const intf_model* md = models + S.model_off;
   const bool bad = (B.status[s] & (INTF_ST_CAP | INTF_ST_OVERFLOW)) != 0;
@@ -327,6 +436,221 @@ __global__ void __launch_bounds__(128) k_jobs_plan(const intf_scenario* __restri
   }
 }
 
+// ---- long traces (req_cap >= kBigJobs): plan and verify with one 1024-thread
+// block per scenario instead of one warp / one thread (a 10^6-request trace
+// has ~4x10^5 batches and ~10^4 jobs).  Same decisions as k_jobs_plan /
+// k_jobs_verify: the prefix maxima, first candidate per bucket, keep/merge
+// pattern and compaction are computed with block scans.
+constexpr int kBigThreads = 1024;
+
+// block-wide exclusive scan (op = max for doubles, + for ints) of one value per thread
+__device__ __forceinline__ double block_excl_max(double v, double* sh) {
+  const int t = threadIdx.x;
+  sh[t] = v;
+  __syncthreads();
+  for (int o = 1; o < kBigThreads; o <<= 1) {
+    const double a = t >= o ? sh[t - o] : -INFINITY;
+    __syncthreads();
+    sh[t] = sh[t] > a ? sh[t] : a;
+    __syncthreads();
+  }
+  const double r = t > 0 ? sh[t - 1] : -INFINITY;
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ int block_excl_sum(int v, int* sh, int* total) {
+  const int t = threadIdx.x;
+  sh[t] = v;
+  __syncthreads();
+  for (int o = 1; o < kBigThreads; o <<= 1) {
+    const int a = t >= o ? sh[t - o] : 0;
+    __syncthreads();
+    sh[t] += a;
+    __syncthreads();
+  }
+  const int r = t > 0 ? sh[t - 1] : 0;
+  if (total) *total = sh[kBigThreads - 1];
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ int block_excl_maxi(int v, int* sh) {
+  const int t = threadIdx.x;
+  sh[t] = v;
+  __syncthreads();
+  for (int o = 1; o < kBigThreads; o <<= 1) {
+    const int a = t >= o ? sh[t - o] : -1;
+    __syncthreads();
+    sh[t] = sh[t] > a ? sh[t] : a;
+    __syncthreads();
+  }
+  const int r = t > 0 ? sh[t - 1] : -1;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_jobs_plan_big(const intf_scenario* __restrict__ scen,
+                                                               const intf_model* __restrict__ models, intf_table tab,
+                                                               intf_replay_buffers B, intf_jobs J) {
+  __shared__ double shd[kBigThreads];
+  __shared__ int shi[kBigThreads];
+  __shared__ int todo_base;
+  const int s = blockIdx.x;
+  const intf_scenario& S = scen[s];
+  if (S.req_cap < kBigJobs) return;
+  const int t = threadIdx.x;
+  const int nb = B.n_batches[s], ro = S.req_off, joff = J.joff[s], jcap = J.jcap[s];
+  const bool bad = (B.status[s] & (INTF_ST_CAP | INTF_ST_OVERFLOW)) != 0;
+  const intf_model* md = models + S.model_off;
+  const int n = bad ? 0 : nb;
+  const int R = (n + kBigThreads - 1) / kBigThreads, b0 = t * R, b1 = min(n, b0 + R);
+  const int nbk = (n + J.min_len - 1) / J.min_len;
+  int* first = reinterpret_cast<int*>(J.scratch + 6ll * joff);  // [nbk <= 12 jcap] first candidate per bucket
+  for (int k = t; k < nbk; k += kBigThreads) first[k] = 0x7fffffff;
+  // pass 1: max of formed + slow*solo over this thread's range
+  double m = -INFINITY;
+  for (int b = b0; b < b1; b++) {
+    const double e = B.b_formed[ro + b] + J.slow * tab.solo_ms[md[B.b_model[ro + b]].entry_base + B.b_size[ro + b] - 1];
+    m = m > e ? m : e;
+  }
+  double before = block_excl_max(m, shd);  // also orders the first[] initialisation before the atomics
+  // pass 2: candidates (forming after every earlier batch's optimistic end)
+  for (int b = b0; b < b1; b++) {
+    const double f = B.b_formed[ro + b];
+    const double e = f + J.slow * tab.solo_ms[md[B.b_model[ro + b]].entry_base + B.b_size[ro + b] - 1];
+    if (b == 0 || f > before) atomicMin(&first[b / J.min_len], b);
+    before = before > e ? before : e;
+  }
+  __syncthreads();
+  // pass 3: the first candidate of every bucket starts a job (compaction)
+  const int K = (nbk + kBigThreads - 1) / kBigThreads, k0 = t * K, k1 = min(nbk, k0 + K);
+  int cnt = 0;
+  for (int k = k0; k < k1; k++) cnt += first[k] != 0x7fffffff;
+  int total = 0;
+  int r = block_excl_sum(cnt, shi, &total);
+  for (int k = k0; k < k1; k++)
+    if (first[k] != 0x7fffffff) {
+      if (r < jcap) J.lo[joff + r] = first[k];
+      r++;
+    }
+  const int nj = total < jcap ? total : jcap;
+  if (t == 0) {
+    J.n_jobs[s] = nj;
+    todo_base = nj ? atomicAdd(J.todo_count, nj) : 0;
+    if (nj == 0) {
+      B.n_segments[s] = 0;
+      B.n_reseats[s] = 0;
+    }
+  }
+  __syncthreads();
+  for (int j = t; j < nj; j += kBigThreads) {
+    J.hi[joff + j] = j + 1 < nj ? J.lo[joff + j + 1] : nb;
+    J.dirty[joff + j] = 1;
+    J.todo[todo_base + j] = joff + j;
+  }
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_jobs_verify_big(const intf_scenario* __restrict__ scen,
+                                                                 intf_replay_buffers B, intf_jobs J) {
+  __shared__ int shi[kBigThreads];
+  __shared__ int todo_base, any_fail;
+  const int s = blockIdx.x;
+  const intf_scenario& S = scen[s];
+  if (S.req_cap < kBigJobs) return;
+  const int t = threadIdx.x;
+  const int n = J.n_jobs[s], joff = J.joff[s], ro = S.req_off;
+  if (n == 0) return;
+  if (t == 0) any_fail = 0;
+  const int R = (n + kBigThreads - 1) / kBigThreads, j0 = t * R, j1 = min(n, j0 + R);
+  // boundary j fails iff the previous job (fresh: every job was just replayed)
+  // ends after job j's first formation
+  auto fails = [&](int j) -> bool {
+    if (j == 0) return false;
+    const int sj = joff + j;
+    return !(J.hi[sj] <= J.lo[sj] || J.last[sj - 1] <= B.b_formed[ro + J.lo[sj]]);
+  };
+  // L_j = last non-failing index <= j (job 0 never fails); inside a run of
+  // failures the sequential rule keeps every other job: keep_j = !f_j || (j - L_j) even
+  int lastok = -1;
+  for (int j = j0; j < j1; j++)
+    if (!fails(j)) lastok = j;
+  const int Lin = block_excl_maxi(lastok, shi);
+  auto keep_of = [&](int j, int L) -> bool { return !fails(j) || ((j - L) % 2 == 0); };
+  int L = Lin, cnt = 0;
+  for (int j = j0; j < j1; j++) {
+    const bool f = fails(j);
+    if (!f) L = j;
+    cnt += keep_of(j, L) ? 1 : 0;
+  }
+  int w = 0;
+  int r = block_excl_sum(cnt, shi, &w);
+  // compact into the shadow (6 doubles per slot), then copy back
+  double* sh = J.scratch + 6ll * joff;
+  L = Lin;
+  bool fail_seen = false;
+  for (int j = j0; j < j1; j++) {
+    const int sj = joff + j;
+    const bool f = fails(j);
+    if (!f) L = j;
+    fail_seen |= f;
+    if (!keep_of(j, L)) continue;
+    bool absorbs = false;
+    if (j + 1 < n) {
+      const bool f1 = fails(j + 1);
+      const int L1 = f1 ? L : j + 1;
+      absorbs = !keep_of(j + 1, L1);
+    }
+    double* d = sh + 6ll * r;
+    d[0] = J.lo[sj];
+    d[1] = absorbs ? J.hi[sj + 1] : J.hi[sj];
+    d[2] = J.last[sj];
+    d[3] = J.info[3 * sj];
+    d[4] = J.info[3 * sj + 1];
+    d[5] = absorbs ? -1.0 - (double)J.info[3 * sj + 2] : (double)J.info[3 * sj + 2];  // sign = dirty
+    r++;
+  }
+  if (fail_seen) atomicOr(&any_fail, 1);
+  __syncthreads();
+  int st = 0, segs = 0, res = 0, nd = 0;
+  for (int j = t; j < w; j += kBigThreads) {
+    const double* d = sh + 6ll * j;
+    const int dj = joff + j;
+    const bool dirty = d[5] < 0.0;
+    J.lo[dj] = (int)d[0];
+    J.hi[dj] = (int)d[1];
+    J.last[dj] = d[2];
+    J.info[3 * dj] = (int)d[3];
+    J.info[3 * dj + 1] = (int)d[4];
+    J.info[3 * dj + 2] = dirty ? (int)(-1.0 - d[5]) : (int)d[5];
+    J.dirty[dj] = dirty ? 1 : 0;
+    st |= (int)d[3];
+    segs += (int)d[4];
+    res += dirty ? 0 : (int)d[5];
+    nd += dirty ? 1 : 0;
+  }
+  if (t == 0) J.n_jobs[s] = w;
+  if (any_fail) {  // queue the merged (dirty) jobs
+    int ndt = 0;
+    int base = block_excl_sum(nd, shi, &ndt);
+    if (t == 0) todo_base = ndt ? atomicAdd(J.todo_count, ndt) : 0;
+    __syncthreads();
+    for (int j = t; j < w; j += kBigThreads)
+      if (J.dirty[joff + j]) J.todo[todo_base + base++] = joff + j;
+    return;
+  }
+  // every boundary holds: per-scenario totals
+  atomicOr(&B.status[s], st);
+  __shared__ int tot_segs, tot_res;
+  if (t == 0) tot_segs = tot_res = 0;
+  __syncthreads();
+  atomicAdd(&tot_segs, segs);
+  atomicAdd(&tot_res, res);
+  __syncthreads();
+  if (t == 0) {
+    B.n_segments[s] = tot_segs;
+    B.n_reseats[s] = tot_res;
+  }
+}
+
 __global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_jobs_replay(const intf_scenario* __restrict__ scen,
                                                                     const intf_model* __restrict__ models,
                                                                     intf_table tab, intf_replay_buffers B,
@@ -358,6 +682,7 @@ __global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_scen) return;
   const intf_scenario& S = scen[s];
+  if (S.req_cap >= kBigJobs) return;  // k_jobs_verify_big
   const int n = J.n_jobs[s], joff = J.joff[s], ro = S.req_off;
   if (n == 0) return;
   int w = 0;  // write cursor (kept jobs)
@@ -737,6 +1062,17 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
   k_gen_arrivals<<<ceil_div(bt->n_models, kGenWarps), 32 * kGenWarps, 0, st>>>(bt->scen, bt->models, bt->n_models,
                                                                                *buf);
   if ((rc = launch_status("k_gen_arrivals"))) return rc;
+  if (bt->max_list_cap >= kBigList) {  // long model streams (the warp kernel skipped them)
+    const unsigned m = (unsigned)bt->n_models, y = m < 65535u ? m : 65535u;
+    k_gen_gaps<<<dim3(ceil_div(bt->max_list_cap, 256 * kGapRun), y, ceil_div(m, y)), 256, 0, st>>>(
+        bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_gen_gaps"))) return rc;
+    k_scan_gaps<<<ceil_div(bt->n_models, 128), 128, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_scan_gaps"))) return rc;
+    k_fill_gaps<<<dim3(ceil_div(ceil_div(bt->max_list_cap, kScanChunk), 128), y, ceil_div(m, y)), 128, 0, st>>>(
+        bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_fill_gaps"))) return rc;
+  }
   k_merge_arrivals<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
   return launch_status("k_merge_arrivals");
 }
@@ -784,7 +1120,11 @@ int intf_jobs_plan(const intf_batch* bt, const intf_table* table, const intf_rep
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(jobs->todo_count, 0, sizeof(int32_t), st);
   k_jobs_plan<<<ceil_div(bt->n_scen, 4), 128, 0, st>>>(bt->scen, bt->n_scen, bt->models, *table, *buf, *jobs);
-  return launch_status("k_jobs_plan");
+  int rc = launch_status("k_jobs_plan");
+  if (rc || bt->max_req_cap < kBigJobs) return rc;
+  if (!jobs->scratch) return bad_input("intf_jobs_plan: long traces need jobs->scratch");
+  k_jobs_plan_big<<<bt->n_scen, kBigThreads, 0, st>>>(bt->scen, bt->models, *table, *buf, *jobs);
+  return launch_status("k_jobs_plan_big");
 }
 
 int intf_jobs_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
@@ -803,7 +1143,11 @@ int intf_jobs_verify(const intf_batch* bt, const intf_replay_buffers* buf, const
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(jobs->todo_count, 0, sizeof(int32_t), st);
   k_jobs_verify<<<ceil_div(bt->n_scen, 128), 128, 0, st>>>(bt->scen, bt->n_scen, *buf, *jobs);
-  return launch_status("k_jobs_verify");
+  int rc = launch_status("k_jobs_verify");
+  if (rc || bt->max_req_cap < kBigJobs) return rc;
+  if (!jobs->scratch) return bad_input("intf_jobs_verify: long traces need jobs->scratch");
+  k_jobs_verify_big<<<bt->n_scen, kBigThreads, 0, st>>>(bt->scen, *buf, *jobs);
+  return launch_status("k_jobs_verify_big");
 }
 
 int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf, void* stream) {

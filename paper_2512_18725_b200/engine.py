@@ -765,6 +765,7 @@ class _DeviceJobs:
             "todo": torch.zeros(total, dtype=torch.int32, device=dev),
             "todo_count": torch.zeros(1, dtype=torch.int32, device=dev),
             "slot_scen": torch.from_numpy(np.repeat(np.arange(pb.n_scen, dtype=np.int32), jcap)).to(dev),
+            "scratch": torch.zeros(6 * total, dtype=torch.float64, device=dev),  # long-trace plan/verify
         }
         self.J = _abi.Jobs(**{k: v.data_ptr() for k, v in self.t.items()}, slow=float(slow), min_len=int(min_len),
                            total_slots=total)

@@ -83,3 +83,23 @@ def test_empty_trace_and_edge_shapes():
                          oracle=p.InterferenceOracle(noise_sigma=0.0))
     res = p.run_scenario(one, table)
     assert res.outcomes and all(o.interference_ratio == 1.0 for o in res.outcomes)  # cap 1, sigma 0 (`test_acceptance.py:137-138`)
+
+
+def test_long_stream_arrivals_bit_exact_vs_oracle():
+    """Model streams of >= 4096 requests take the long-list path (every gap in
+    parallel, k_gen_gaps; one sequential cumulative sum per model,
+    k_scan_gaps): bit-exact against the oracle's sequential generator, incl.
+    the overflow/retry path (scale 1.0 first) and a zero-rate model."""
+    import oracle as O
+    from paper_2512_18725_b200 import engine
+    from paper_2512_18725_b200.sweep import c4_scenario, table16
+
+    t16, arch = table16()
+    spec = c4_scenario(t16, arch, n_requests=2e5, seed=3)
+    spec["deployed"][5]["arrival_rate_rps"] = 0.0
+    ta = t16.arrays()
+    (at, am), = engine.arrivals([spec], ta)
+    ot, om = O.generate_arrivals(spec, O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr))
+    assert len(at) > 150000
+    np.testing.assert_array_equal(at, ot)
+    np.testing.assert_array_equal(am, om)

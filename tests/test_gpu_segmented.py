@@ -29,14 +29,19 @@ def test_segmented_replay_matches_goldens(slow, min_len):
         assert stats["jobs_final"] <= stats["jobs_initial"]
 
 
-def test_long_trace_segmented_equals_serial():
+@pytest.mark.parametrize("slow,min_len", [(2.0, 16), (0.5, 4), (0.0, 1)])
+def test_long_trace_segmented_equals_serial(slow, min_len):
+    """A 2x10^5-request trace (req_cap >= 32768: block-parallel plan/verify,
+    long-list arrivals) replayed as busy-period jobs -- also with most
+    speculative boundaries failing (slow 0.5 / 0.0: long runs of merges) --
+    equals the whole-trace replay and the CPU oracle."""
     from paper_2512_18725_b200 import engine
     from paper_2512_18725_b200.sweep import c4_scenario, table16
 
     t16, arch = table16()
     spec = c4_scenario(t16, arch, n_requests=2e5)
     ta = t16.arrays()
-    pipe, h, stats = _run([spec], ta)
+    pipe, h, stats = _run([spec], ta, slow=slow, min_len=min_len)
     assert stats["jobs_final"] > 10, stats  # the trace really was replayed in parallel pieces
     ser, hs = engine.run_batch([spec], ta)
     a, b = pipe.scenario(h, 0), ser.scenario(hs, 0)
@@ -85,6 +90,26 @@ def test_sweep_segmented_equals_whole_scenario_jobs():
         for k in ("order", "b_start", "b_completion", "b_measured", "b_nseg", "r_slo_met", "slo_p", "slo_met"):
             assert np.array_equal(a[k], b[k]), (s, k)
         assert a["n_reseats"] == b["n_reseats"]
+
+
+def test_two_long_traces_in_one_batch():
+    """Two long traces + short scenarios in one batch: per-scenario regions of
+    the block-parallel plan/verify scratch do not collide."""
+    from paper_2512_18725_b200 import engine
+    from paper_2512_18725_b200.sweep import c4_scenario, table16
+
+    t16, arch = table16()
+    specs = [c4_scenario(t16, arch, n_requests=1e5, seed=5), _golden.spec("c4slice"),
+             c4_scenario(t16, arch, n_requests=1.2e5, seed=6)]
+    ta = t16.arrays()
+    pipe, h, stats = _run(specs, ta, slow=1.0, min_len=8)
+    ser, hs = engine.run_batch(specs, ta)
+    for s in range(3):
+        a, b = pipe.scenario(h, s), ser.scenario(hs, s)
+        assert a["status"] == 0 and b["status"] == 0
+        for k in ("order", "b_start", "b_completion", "b_measured", "b_nseg", "r_slo_met"):
+            assert np.array_equal(a[k], b[k]), (s, k)
+        assert a["n_reseats"] == b["n_reseats"] and a["n_segments"] == b["n_segments"]
 
 
 def test_device_and_host_planned_sharding_agree():
