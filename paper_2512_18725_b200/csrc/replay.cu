@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(32 * kFormModelWarps) k_form_models(const intf
   const int g = blockIdx.x * kFormModelWarps + (threadIdx.x >> 5);
   if (g >= n_models_total) return;
   const intf_model& M = models[g];
+  if (M.list_cap >= kBigList) return;  // long lists: k_form_nxt .. k_form_emit
   const intf_scenario& S = scen[M.scen];
   const bool bad = (B.status[M.scen] & INTF_ST_OVERFLOW) || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 ||
                    S.max_bs < 1 || S.n_models > kMaxModels;
@@ -216,6 +217,129 @@ __global__ void __launch_bounds__(32 * kFormModelWarps) k_form_models(const intf
     return;
   }
   form_model_warp(S, M, min(B.n_list[g], M.list_cap), B, g);
+}
+
+// ---- K1a' (long model lists, e.g. a 10^6-request trace): the batch starts
+// of one model are the orbit h_0 = 0, h_{i+1} = nxt(h_i) = h_i + cnt(h_i),
+// cnt(h) = next_formation's member count from head h (`batcher.py:44-85`),
+// which is a pure function of h.  nxt for every h is computed in parallel,
+// then the orbit by pointer doubling (J_{k+1} = J_k o J_k; path entries
+// [2^k, 2^{k+1}) = J_k of entries [0, 2^k)), so the serial walk over the
+// batches disappears.  Same batches, same events as form_model_warp.
+__device__ __forceinline__ int form_cnt(const double* lt, int n, int h, double window, int max_bs) {
+  const double D = lt[h] + window;  // arm_window at the first arrival (`batcher.py:66-68`)
+  int lo = h + 1, hi = min(n, h + max_bs);  // first j in [h+1, hi) with lt[j] >= D, else hi
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (lt[mid] < D) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo - h;
+}
+
+struct LongModel {  // model g of a long-list launch (grid.y/z = model, grid.x = list chunk)
+  int g, n, i;
+  bool ok;
+};
+__device__ __forceinline__ LongModel long_model(const intf_scenario* scen, const intf_model* models, int n_models,
+                                                const intf_replay_buffers& B) {
+  LongModel r;
+  r.g = blockIdx.z * gridDim.y + blockIdx.y;
+  r.ok = false;
+  if (r.g >= n_models) return r;
+  const intf_model& M = models[r.g];
+  const intf_scenario& S = scen[M.scen];
+  if (M.list_cap < kBigList) return r;
+  if ((B.status[M.scen] & INTF_ST_OVERFLOW) || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 || S.max_bs < 1 ||
+      S.n_models > kMaxModels)
+    return r;
+  r.n = min(B.n_list[r.g], M.list_cap);
+  r.i = blockIdx.x * blockDim.x + threadIdx.x;
+  r.ok = true;
+  return r;
+}
+
+// J_0 = nxt into table 0; path[0] = 0
+__global__ void k_form_nxt(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                           int n_models, intf_replay_buffers B) {
+  const LongModel L = long_model(scen, models, n_models, B);
+  if (!L.ok || L.i >= L.n) return;
+  const intf_model& M = models[L.g];
+  const intf_scenario& S = scen[M.scen];
+  int32_t* ws = B.form_ws + 3ll * M.list_off;  // [J table A | J table B | path], list_cap each
+  ws[L.i] = L.i + form_cnt(B.list_t + M.list_off, L.n, L.i, S.window_ms, S.max_bs);
+  if (L.i == 0) ws[2 * M.list_cap] = 0;
+}
+
+// level k: path[r] = J_k(path[r - 2^k]) for r in [2^k, 2^{k+1}); then J_{k+1} = J_k o J_k
+__global__ void k_form_extend(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                              int n_models, intf_replay_buffers B, int k) {
+  const LongModel L = long_model(scen, models, n_models, B);
+  if (!L.ok) return;
+  const intf_model& M = models[L.g];
+  int32_t* ws = B.form_ws + 3ll * M.list_off;
+  const int32_t* J = ws + (k & 1) * M.list_cap;
+  int32_t* path = ws + 2 * M.list_cap;
+  const int step = 1 << k, r = step + L.i;
+  if (L.i < step && r < L.n) {
+    const int prev = path[r - step];
+    path[r] = prev < L.n ? J[prev] : L.n;
+  }
+}
+__global__ void k_form_double(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                              int n_models, intf_replay_buffers B, int k) {
+  const LongModel L = long_model(scen, models, n_models, B);
+  if (!L.ok || L.i >= L.n) return;
+  const intf_model& M = models[L.g];
+  int32_t* ws = B.form_ws + 3ll * M.list_off;
+  const int32_t* J = ws + (k & 1) * M.list_cap;
+  int32_t* Jn = ws + ((k + 1) & 1) * M.list_cap;
+  const int a = J[L.i];
+  Jn[L.i] = a < L.n ? J[a] : L.n;
+}
+
+// batch r of the model: head path[r] (while < n); writes what form_model_warp writes
+__global__ void k_form_emit(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                            int n_models, intf_replay_buffers B) {
+  const LongModel L = long_model(scen, models, n_models, B);
+  if (!L.ok) {
+    // long models of bad scenarios form nothing
+    const int g = blockIdx.z * gridDim.y + blockIdx.y;
+    if (g < n_models && models[g].list_cap >= kBigList && blockIdx.x == 0 && threadIdx.x == 0) B.n_mb[g] = 0;
+    return;
+  }
+  if (L.n == 0) {
+    if (L.i == 0) B.n_mb[L.g] = 0;
+    return;
+  }
+  if (L.i >= L.n) return;
+  const intf_model& M = models[L.g];
+  const intf_scenario& S = scen[M.scen];
+  const int32_t* path = B.form_ws + 3ll * M.list_off + 2 * M.list_cap;
+  const int h = path[L.i];
+  if (h >= L.n) return;
+  if (L.i + 1 == L.n || path[L.i + 1] >= L.n) B.n_mb[L.g] = L.i + 1;  // last batch of the orbit
+  const double* lt = B.list_t + M.list_off;
+  const int32_t* lrid = B.list_rid + M.list_off;
+  const int cnt = form_cnt(lt, L.n, h, S.window_ms, S.max_bs);
+  double t;
+  int kind;
+  uint32_t key;
+  if (cnt == S.max_bs) {  // early emit at max_batch_size (`batcher.py:70-71`)
+    t = lt[h + cnt - 1];
+    kind = KIND_ARRIVAL;
+    key = (uint32_t)lrid[h + cnt - 1];
+  } else {  // window expiry (`batcher.py:74-85`)
+    t = lt[h] + S.window_ms;
+    kind = KIND_WINDOW;
+    key = M.crc;
+  }
+  B.mb_t[M.list_off + L.i] = t;
+  int32_t* info = B.mb_info + 4ll * (M.list_off + L.i);
+  info[0] = kind;
+  info[1] = (int32_t)key;
+  info[2] = cnt;
+  info[3] = h;
 }
 
 __global__ void k_merge_batches(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
@@ -1044,6 +1168,23 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
   k_form_models<<<ceil_div(bt->n_models, kFormModelWarps), 32 * kFormModelWarps, 0, st>>>(bt->scen, bt->models,
                                                                                          bt->n_models, *buf);
   if ((rc = launch_status("k_form_models"))) return rc;
+  if (bt->max_list_cap >= kBigList) {  // long model lists: pointer-doubling formation
+    if (!buf->form_ws) return bad_input("formation of long lists needs form_ws scratch");
+    const unsigned m = (unsigned)bt->n_models, y = m < 65535u ? m : 65535u;
+    const dim3 grid(ceil_div(bt->max_list_cap, 256), y, ceil_div(m, y));
+    k_form_nxt<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_form_nxt"))) return rc;
+    for (int k = 0; (1ll << k) < bt->max_list_cap; k++) {
+      k_form_extend<<<dim3(ceil_div(1ll << k < bt->max_list_cap ? 1ll << k : bt->max_list_cap, 256), y,
+                           ceil_div(m, y)), 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, k);
+      if ((rc = launch_status("k_form_extend"))) return rc;
+      if ((2ll << k) >= bt->max_list_cap) break;  // the path is complete
+      k_form_double<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, k);
+      if ((rc = launch_status("k_form_double"))) return rc;
+    }
+    k_form_emit<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_form_emit"))) return rc;
+  }
   k_merge_batches<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
   return launch_status("k_merge_batches");
 }
