@@ -112,7 +112,7 @@ def pack(specs: list, table: TableArrays, scale: float = 1.0, list_caps=None) ->
             M.list_off = list_off
             lc = list_caps[g] if list_caps is not None else _list_capacity(M.rate_rps, S.duration_s, scale)
             M.list_cap = int(lc)
-            list_off += M.list_cap
+            list_off += M.list_cap + (M.list_cap & 1)  # even offsets: 16-byte aligned list rows
             req_cap += M.list_cap
             g += 1
         S.req_off, S.req_cap = req_off, req_cap

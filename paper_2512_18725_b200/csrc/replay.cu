@@ -62,30 +62,81 @@ __global__ void __launch_bounds__(256) k_gen_gaps(const intf_scenario* __restric
 // each chunk's adds -- the same operations in the same order, so the same
 // values -- in parallel and finds the horizon crossing.
 constexpr int kScanChunk = 32;
-__global__ void k_scan_gaps(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                            int n_models_total, intf_replay_buffers B) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n_models_total) return;
+constexpr int kScanStage = 512;  // doubles per bulk copy (4 KB)
+constexpr int kScanStages = 4;   // copies in flight ahead of the add chain
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one bulk global->shared copy completing on `bar` (bytes % 16 == 0, 16-byte aligned)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar), d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+  }
+}
+
+// one block (one active thread) per long model: the gaps stream through
+// shared memory by bulk copies kScanStages x 4 KB ahead of the add chain, so
+// the chain runs at fp64 add latency; every 32nd partial sum goes to mb_t.
+__global__ void __launch_bounds__(32) k_scan_gaps(const intf_scenario* __restrict__ scen,
+                                                  const intf_model* __restrict__ models, int n_models_total,
+                                                  intf_replay_buffers B) {
+  __shared__ alignas(128) double buf[kScanStages][kScanStage];
+  __shared__ alignas(8) uint64_t bar[kScanStages];
+  const int g = blockIdx.x;
+  if (g >= n_models_total || threadIdx.x != 0) return;
   const intf_model& M = models[g];
   if (M.list_cap < kBigList || M.rate_rps == 0.0) return;
-  const double* lt = B.list_t + M.list_off;
+  const double* lt = B.list_t + M.list_off;  // list_off is even: 16-byte aligned
   double* ends = B.mb_t + M.list_off;
-  constexpr int CH = kScanChunk;
-  const int full = M.list_cap / CH * CH;
+  const int cap = M.list_cap, nch = (cap + kScanStage - 1) / kScanStage, n32 = cap / kScanChunk;
+  const double horizon = scen[M.scen].duration_s * 1000.0;
+  for (int i = 0; i < kScanStages; i++) mbar_init(&bar[i]);
+  int issued = 0;
+  auto issue = [&](int c) {
+    const int lo = c * kScanStage, len = min(kScanStage, cap - lo);
+    bulk_load(buf[c % kScanStages], lt + lo, (unsigned)((len + 1) & ~1) * 8u, &bar[c % kScanStages]);
+    issued = c + 1;
+  };
+  for (int c = 0; c < kScanStages && c < nch; c++) issue(c);
   double t = 0.0;
-  double cur[CH], nxt[CH];
+  bool past = false;
+  int c = 0;
+  for (; c < nch && !past; c++) {
+    mbar_wait(&bar[c % kScanStages], (unsigned)(c / kScanStages) & 1u);
+    const double* sb = buf[c % kScanStages];
+    const int lo = c * kScanStage, len = min(kScanStage, cap - lo);
+    for (int k0 = 0; k0 < len; k0 += kScanChunk) {
+      const int m = min(kScanChunk, len - k0);
+      if (m == kScanChunk) {
 #pragma unroll
-  for (int k = 0; k < CH; k++) cur[k] = k < full ? lt[k] : 0.0;
-  for (int base = 0; base < full; base += CH) {
-    const bool more = base + CH < full;
-#pragma unroll
-    for (int k = 0; k < CH; k++) nxt[k] = more ? lt[base + CH + k] : 0.0;
-#pragma unroll
-    for (int k = 0; k < CH; k++) t = t + cur[k];
-    ends[base / CH] = t;
-#pragma unroll
-    for (int k = 0; k < CH; k++) cur[k] = nxt[k];
+        for (int k = 0; k < kScanChunk; k++) t = t + sb[k0 + k];
+        ends[(lo + k0) / kScanChunk] = t;
+        if (t >= horizon) {  // later 32-chunks lie past the horizon: k_fill_gaps skips them
+          for (int e = (lo + k0) / kScanChunk + 1; e < n32; e++) ends[e] = INFINITY;
+          past = true;
+          break;
+        }
+      }  // a ragged tail (< 32) needs no end entry
+    }
+    if (!past && c + kScanStages < nch) issue(c + kScanStages);
   }
+  // copies still in flight must land before the block (and its smem) exits
+  for (int d = c; d < issued; d++) mbar_wait(&bar[d % kScanStages], (unsigned)(d / kScanStages) & 1u);
 }
 
 // thread per (long model, chunk): rebuild the chunk's arrival times from the
@@ -1208,7 +1259,7 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
     k_gen_gaps<<<dim3(ceil_div(bt->max_list_cap, 256 * kGapRun), y, ceil_div(m, y)), 256, 0, st>>>(
         bt->scen, bt->models, bt->n_models, *buf);
     if ((rc = launch_status("k_gen_gaps"))) return rc;
-    k_scan_gaps<<<ceil_div(bt->n_models, 128), 128, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    k_scan_gaps<<<bt->n_models, 32, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
     if ((rc = launch_status("k_scan_gaps"))) return rc;
     k_fill_gaps<<<dim3(ceil_div(ceil_div(bt->max_list_cap, kScanChunk), 128), y, ceil_div(m, y)), 128, 0, st>>>(
         bt->scen, bt->models, bt->n_models, *buf);
