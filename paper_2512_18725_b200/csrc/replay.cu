@@ -1044,6 +1044,11 @@ static_assert(kSloWsInts == INTF_SLO_WS_INTS, "slo_ws size mismatch with the hea
 __global__ void k_slo_big_count(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
                                 intf_replay_buffers B, int s, const double* __restrict__ warm_cutoff,
                                 int32_t* __restrict__ ws) {
+  // per-block counters in shared memory, one global atomic per block and
+  // counter (10^6 requests onto <= 128 global counters would serialise)
+  __shared__ int cnt[128];
+  for (int k = threadIdx.x; k < 128; k += blockDim.x) cnt[k] = 0;
+  __syncthreads();
   const intf_scenario& S = scen[s];
   const int n = B.n_req[s], ro = S.req_off;
   const double cutoff = warm_cutoff ? warm_cutoff[s] : -INFINITY;
@@ -1053,13 +1058,16 @@ __global__ void k_slo_big_count(const intf_scenario* __restrict__ scen, const in
     const int m = B.arr_model[ro + i];
     const bool met = (B.b_completion[ro + b] - at) <= models[S.model_off + m].slo_ms;
     B.r_slo_met[ro + i] = met;
-    atomicAdd(&ws[64 + 2 * m], 1);
-    if (met) atomicAdd(&ws[64 + 2 * m + 1], 1);
+    atomicAdd(&cnt[64 + 2 * m], 1);
+    if (met) atomicAdd(&cnt[64 + 2 * m + 1], 1);
     if (at >= cutoff) {
-      atomicAdd(&ws[2 * m], 1);
-      if (met) atomicAdd(&ws[2 * m + 1], 1);
+      atomicAdd(&cnt[2 * m], 1);
+      if (met) atomicAdd(&cnt[2 * m + 1], 1);
     }
   }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 128; k += blockDim.x)
+    if (cnt[k]) atomicAdd(&ws[k], cnt[k]);
 }
 
 __global__ void k_slo_big_init(const intf_scenario* __restrict__ scen, int s, int32_t* __restrict__ ws,
@@ -1100,15 +1108,29 @@ __global__ void k_slo_big_hist(const intf_scenario* __restrict__ scen, intf_repl
   const int shift = 56 - 8 * pass;
   const unsigned long long* prefix = reinterpret_cast<const unsigned long long*>(ws + kSloWsPrefix);
   unsigned int* hist = reinterpret_cast<unsigned int*>(ws + kSloWsHist);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const double at = B.arr_t[ro + i];
-    if (!(at >= cutoff)) continue;
-    const int m = B.arr_model[ro + i];
-    const unsigned long long key = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
-    const unsigned d = (unsigned)(key >> shift) & 0xffu;
+  // warp-aggregated increments: latencies of one model share the high key
+  // bytes, so most lanes of a warp hit the same bin (one atomic per distinct bin)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long i0 = start - (threadIdx.x & 31); i0 < n; i0 += stride) {
+    const long long i = i0 + (threadIdx.x & 31);
+    int bins[3] = {-1, -1, -1};
+    if (i < n) {
+      const double at = B.arr_t[ro + i];
+      if (at >= cutoff) {
+        const int m = B.arr_model[ro + i];
+        const unsigned long long key = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
+        const unsigned d = (unsigned)(key >> shift) & 0xffu;
 #pragma unroll
-    for (int q = 0; q < 3; q++)
-      if (pass == 0 || ((key ^ prefix[m * 3 + q]) >> (shift + 8)) == 0ull) atomicAdd(&hist[(m * 3 + q) * 256 + d], 1u);
+        for (int q = 0; q < 3; q++)
+          if (pass == 0 || ((key ^ prefix[m * 3 + q]) >> (shift + 8)) == 0ull) bins[q] = (m * 3 + q) * 256 + (int)d;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      const unsigned same = __match_any_sync(0xffffffffu, bins[q]);
+      if (bins[q] >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&hist[bins[q]], (unsigned)__popc(same));
+    }
   }
 }
 
