@@ -772,7 +772,7 @@ class _DeviceJobs:
         self.key = (float(slow), int(min_len))
 
 
-def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 16, max_iters: int = 100000,
+def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 64, max_iters: int = 100000,
                      arrivals: bool = True, slo: bool = True, features: bool = True) -> dict:
     """Busy-period sharding, planned and verified on the device:
     speculative idle boundaries (k_jobs_plan), parallel job replay
