@@ -724,6 +724,150 @@ __global__ void __launch_bounds__(kBigThreads) k_jobs_plan_big(const intf_scenar
   }
 }
 
+// ---- the same plan, grid-parallel (C4's ~4x10^5 batches over ~200 blocks):
+// p1 block maxima of formed + slow*solo, p2 exclusive scan of the maxima,
+// p3 candidates -> first candidate per bucket, p4 compaction (one block).
+constexpr int kPlanChunk = 2048;  // batches per block (256 threads x 8)
+__device__ __forceinline__ double plan_e(const intf_scenario& S, const intf_model* md, const intf_table& tab,
+                                         const intf_replay_buffers& B, double slow, int b) {
+  const int ro = S.req_off;
+  return B.b_formed[ro + b] + slow * tab.solo_ms[md[B.b_model[ro + b]].entry_base + B.b_size[ro + b] - 1];
+}
+__global__ void __launch_bounds__(256) k_plan_p1(const intf_scenario* __restrict__ scen,
+                                                 const intf_model* __restrict__ models, intf_table tab,
+                                                 intf_replay_buffers B, intf_jobs J) {
+  __shared__ double red[256];
+  const int s = blockIdx.y;
+  const intf_scenario& S = scen[s];
+  if (S.req_cap < kBigJobs) return;
+  const int nb = (B.status[s] & (INTF_ST_CAP | INTF_ST_OVERFLOW)) ? 0 : B.n_batches[s];
+  const int b0 = blockIdx.x * kPlanChunk;
+  if (b0 >= max(nb, 1)) return;
+  const int joff = J.joff[s], jcap = J.jcap[s];
+  int* first = reinterpret_cast<int*>(J.scratch + 6ll * joff);
+  double* bmax = J.scratch + 6ll * joff + jcap;
+  const int k0 = b0 / J.min_len, k1 = min((b0 + kPlanChunk - 1) / J.min_len, (nb - 1) / J.min_len);
+  for (int k = k0 + threadIdx.x; k <= k1; k += blockDim.x) first[k] = 0x7fffffff;
+  const intf_model* md = models + S.model_off;
+  double m = -INFINITY;
+  for (int i = 0; i < kPlanChunk / 256; i++) {
+    const int b = b0 + threadIdx.x * (kPlanChunk / 256) + i;
+    if (b < nb) {
+      const double e = plan_e(S, md, tab, B, J.slow, b);
+      m = m > e ? m : e;
+    }
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = red[threadIdx.x] > red[threadIdx.x + o] ? red[threadIdx.x] : red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bmax[blockIdx.x] = red[0];
+}
+__global__ void __launch_bounds__(kBigThreads) k_plan_p2(const intf_scenario* __restrict__ scen,
+                                                         intf_replay_buffers B, intf_jobs J) {
+  __shared__ double shd[kBigThreads];
+  const int s = blockIdx.x;
+  if (scen[s].req_cap < kBigJobs) return;
+  const int nb = (B.status[s] & (INTF_ST_CAP | INTF_ST_OVERFLOW)) ? 0 : B.n_batches[s];
+  const int nblk = (nb + kPlanChunk - 1) / kPlanChunk;
+  double* bmax = J.scratch + 6ll * J.joff[s] + J.jcap[s];
+  // exclusive max-scan in place, kBigThreads entries per round
+  double carry = -INFINITY;
+  for (int base = 0; base < nblk; base += kBigThreads) {
+    const int i = base + threadIdx.x;
+    const double v = i < nblk ? bmax[i] : -INFINITY;
+    const double ex = block_excl_max(v, shd);
+    const double pre = carry > ex ? carry : ex;
+    if (i < nblk) bmax[i] = pre;
+    const double incl = pre > v ? pre : v;
+    shd[threadIdx.x] = incl;
+    __syncthreads();
+    carry = shd[kBigThreads - 1];
+    __syncthreads();
+  }
+}
+__global__ void __launch_bounds__(256) k_plan_p3(const intf_scenario* __restrict__ scen,
+                                                 const intf_model* __restrict__ models, intf_table tab,
+                                                 intf_replay_buffers B, intf_jobs J) {
+  __shared__ double sh[256];
+  const int s = blockIdx.y;
+  const intf_scenario& S = scen[s];
+  if (S.req_cap < kBigJobs) return;
+  const int nb = (B.status[s] & (INTF_ST_CAP | INTF_ST_OVERFLOW)) ? 0 : B.n_batches[s];
+  const int b0 = blockIdx.x * kPlanChunk;
+  if (b0 >= nb) return;
+  const int joff = J.joff[s], jcap = J.jcap[s];
+  int* first = reinterpret_cast<int*>(J.scratch + 6ll * joff);
+  const double* bmax = J.scratch + 6ll * joff + jcap;
+  const intf_model* md = models + S.model_off;
+  constexpr int PER = kPlanChunk / 256;
+  const int bt = b0 + threadIdx.x * PER;
+  double e[PER], m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    e[i] = bt + i < nb ? plan_e(S, md, tab, B, J.slow, bt + i) : -INFINITY;
+    m = m > e[i] ? m : e[i];
+  }
+  // exclusive max over earlier threads of the block (Hillis-Steele), then the block's prefix
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const double a = threadIdx.x >= o ? sh[threadIdx.x - o] : -INFINITY;
+    __syncthreads();
+    sh[threadIdx.x] = sh[threadIdx.x] > a ? sh[threadIdx.x] : a;
+    __syncthreads();
+  }
+  double before = threadIdx.x ? sh[threadIdx.x - 1] : -INFINITY;
+  before = before > bmax[blockIdx.x] ? before : bmax[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int b = bt + i;
+    if (b >= nb) break;
+    if (b == 0 || B.b_formed[S.req_off + b] > before) atomicMin(&first[b / J.min_len], b);
+    before = before > e[i] ? before : e[i];
+  }
+}
+__global__ void __launch_bounds__(kBigThreads) k_plan_p4(const intf_scenario* __restrict__ scen, intf_replay_buffers B,
+                                                         intf_jobs J) {
+  __shared__ int shi[kBigThreads];
+  __shared__ int todo_base;
+  const int s = blockIdx.x;
+  const intf_scenario& S = scen[s];
+  if (S.req_cap < kBigJobs) return;
+  const int t = threadIdx.x;
+  const int nb = (B.status[s] & (INTF_ST_CAP | INTF_ST_OVERFLOW)) ? 0 : B.n_batches[s];
+  const int joff = J.joff[s], jcap = J.jcap[s];
+  const int* first = reinterpret_cast<const int*>(J.scratch + 6ll * joff);
+  const int nbk = (nb + J.min_len - 1) / J.min_len;
+  const int K = (nbk + kBigThreads - 1) / kBigThreads, k0 = t * K, k1 = min(nbk, k0 + K);
+  int cnt = 0;
+  for (int k = k0; k < k1; k++) cnt += first[k] != 0x7fffffff;
+  int total = 0;
+  int r = block_excl_sum(cnt, shi, &total);
+  for (int k = k0; k < k1; k++)
+    if (first[k] != 0x7fffffff) {
+      if (r < jcap) J.lo[joff + r] = first[k];
+      r++;
+    }
+  const int nj = total < jcap ? total : jcap;
+  if (t == 0) {
+    J.n_jobs[s] = nj;
+    todo_base = nj ? atomicAdd(J.todo_count, nj) : 0;
+    if (nj == 0) {
+      B.n_segments[s] = 0;
+      B.n_reseats[s] = 0;
+    }
+  }
+  __syncthreads();
+  for (int j = t; j < nj; j += kBigThreads) {
+    J.hi[joff + j] = j + 1 < nj ? J.lo[joff + j + 1] : nb;
+    J.dirty[joff + j] = 1;
+    J.todo[todo_base + j] = joff + j;
+  }
+}
+
 __global__ void __launch_bounds__(kBigThreads) k_jobs_verify_big(const intf_scenario* __restrict__ scen,
                                                                  intf_replay_buffers B, intf_jobs J) {
   __shared__ int shi[kBigThreads];
@@ -1337,8 +1481,19 @@ int intf_jobs_plan(const intf_batch* bt, const intf_table* table, const intf_rep
   int rc = launch_status("k_jobs_plan");
   if (rc || bt->max_req_cap < kBigJobs) return rc;
   if (!jobs->scratch) return bad_input("intf_jobs_plan: long traces need jobs->scratch");
-  k_jobs_plan_big<<<bt->n_scen, kBigThreads, 0, st>>>(bt->scen, bt->models, *table, *buf, *jobs);
-  return launch_status("k_jobs_plan_big");
+  if (bt->n_scen > 65535 || jobs->min_len > 8192) {  // one block per long scenario
+    k_jobs_plan_big<<<bt->n_scen, kBigThreads, 0, st>>>(bt->scen, bt->models, *table, *buf, *jobs);
+    return launch_status("k_jobs_plan_big");
+  }
+  const dim3 grid(ceil_div(bt->max_req_cap, kPlanChunk), bt->n_scen);
+  k_plan_p1<<<grid, 256, 0, st>>>(bt->scen, bt->models, *table, *buf, *jobs);
+  if ((rc = launch_status("k_plan_p1"))) return rc;
+  k_plan_p2<<<bt->n_scen, kBigThreads, 0, st>>>(bt->scen, *buf, *jobs);
+  if ((rc = launch_status("k_plan_p2"))) return rc;
+  k_plan_p3<<<grid, 256, 0, st>>>(bt->scen, bt->models, *table, *buf, *jobs);
+  if ((rc = launch_status("k_plan_p3"))) return rc;
+  k_plan_p4<<<bt->n_scen, kBigThreads, 0, st>>>(bt->scen, *buf, *jobs);
+  return launch_status("k_plan_p4");
 }
 
 int intf_jobs_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
