@@ -1,5 +1,6 @@
 #!/bin/bash
-# One gpurun session: GPU tests, smoke, bench, ncu launch list + top-kernel captures.
+# One gpurun session: GPU tests, smoke, bench, reference bench, ncu launch list
+# + `ncu --set full` captures of the top kernels (bench + the C4 long-trace path).
 # usage (from the repo root, under gpurun):  bash tools/gpu_round.sh TAG
 TAG=${1:-r1}
 OUT=gpurun_out
@@ -10,10 +11,23 @@ timeout 900 python -m pytest tests -q -m gpu > $OUT/pytest_gpu_$TAG.log 2>&1; ec
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1
 timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches_$TAG.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_launch_$TAG.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c4_$TAG.csv \
+    python tools/c4_breakdown.py > $OUT/ncu_launch_c4_$TAG.log 2>&1
 for K in k_cand_step k_replay_warp k_form_models k_merge_batches k_noise_table k_gen_arrivals k_slo k_features k_rls k_sgd k_ols_partial k_ols_windows_fused; do
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_${TAG}_$K \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_${TAG}_$K.log 2>&1
 done
+for K in k_scan_gaps k_gen_gaps k_form_double k_jobs_replay k_plan_p3 k_slo_big_hist; do
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_${TAG}_$K \
+    python tools/c4_breakdown.py > $OUT/ncu_${TAG}_$K.log 2>&1
+done
+
+# summarise on the box (ncu is there) and keep gpurun_out under the 64 MiB copy-back limit
+python tools/ncu_summary.py $TAG $OUT/prof_${TAG}_*.ncu-rep --launches $OUT/launches_$TAG.csv > $OUT/summary_$TAG.log 2>&1
+cp profiles/ncu_$TAG.md profiles/ncu_summary.json $OUT/ 2>/dev/null
+
+find $OUT -name "prof_${TAG}_*.ncu-rep" ! -name "prof_${TAG}_k_cand_step.ncu-rep" ! -name "prof_${TAG}_k_replay_warp.ncu-rep" ! -name "prof_${TAG}_k_scan_gaps.ncu-rep" -delete
+du -sh $OUT
 echo done
