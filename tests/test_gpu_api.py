@@ -103,3 +103,27 @@ def test_long_stream_arrivals_bit_exact_vs_oracle():
     assert len(at) > 150000
     np.testing.assert_array_equal(at, ot)
     np.testing.assert_array_equal(am, om)
+
+
+def test_long_stream_overflow_is_flagged_then_retried():
+    """A long-list capacity below the stream length must raise the overflow
+    status (k_fill_gaps: every draw below the horizon), and the retrying
+    caller (engine.arrivals grows the capacity) still gets the exact stream."""
+    import ctypes
+
+    from paper_2512_18725_b200 import _abi, engine
+    from paper_2512_18725_b200.sweep import c4_scenario, table16
+
+    t16, arch = table16()
+    spec = c4_scenario(t16, arch, n_requests=1e5, seed=4)
+    ta = t16.arrays()
+    pipe = engine.ReplayPipeline([spec], ta, scale=0.6, seg_stride=1)
+    _abi.check(_abi.load().intf_generate_arrivals(ctypes.byref(pipe.batch), ctypes.byref(pipe.B),
+                                                  engine.stream_ptr()), "arrivals")
+    assert pipe.status()[0] & _abi.ST_OVERFLOW
+    import oracle as O
+
+    (at, am), = engine.arrivals([spec], ta)
+    ot, om = O.generate_arrivals(spec, O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr))
+    np.testing.assert_array_equal(at, ot)
+    np.testing.assert_array_equal(am, om)
