@@ -1058,6 +1058,7 @@ __global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen
 constexpr int kSloThreads = 256;
 constexpr int kSloGroup = 8;          // models per radix pass group
 constexpr int kSloBigReq = 1 << 16;  // above this request capacity: grid-wide SLO passes
+constexpr int kSloCache = 4096;      // records whose latency keys k_slo keeps in shared memory
 
 __device__ __forceinline__ unsigned long long lat_key(double v) {
   unsigned long long u = (unsigned long long)__double_as_longlong(v);
@@ -1123,6 +1124,20 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
     out_met[S.model_off + m] = cnt_met[m];
   }
   const double pq[3] = {50.0, 95.0, 99.0};
+  // latency keys (and model ids) of the trimmed records, cached in shared
+  // memory once when they fit (kSloCache records), so the 8 radix passes
+  // re-read shared memory instead of four global arrays
+  extern __shared__ unsigned long long kcache[];
+  unsigned char* mcache = reinterpret_cast<unsigned char*>(kcache + kSloCache);
+  const bool cached = n <= kSloCache;
+  if (cached) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double at = B.arr_t[ro + i];
+      const bool in = at >= cut;
+      kcache[i] = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
+      mcache[i] = in ? (unsigned char)B.arr_model[ro + i] : (unsigned char)255;
+    }
+  }
   for (int g0 = 0; g0 < S.n_models; g0 += kSloGroup) {
     const int gm = min(kSloGroup, S.n_models - g0);
     if (threadIdx.x < gm * 3) {
@@ -1136,14 +1151,22 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
     }
     for (int pass = 0; pass < 8; pass++) {
       const int shift = 56 - 8 * pass;
-      for (int k = threadIdx.x; k < kSloGroup * 3 * 256; k += blockDim.x) (&hist[0][0][0])[k] = 0u;
+      for (int k = threadIdx.x; k < gm * 3 * 256; k += blockDim.x) (&hist[0][0][0])[k] = 0u;  // used rows only
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int m = B.arr_model[ro + i] - g0;
-        if (m < 0 || m >= gm) continue;
-        const double at = B.arr_t[ro + i];
-        if (!(at >= cut)) continue;
-        const unsigned long long key = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
+        int m;
+        unsigned long long key;
+        if (cached) {
+          m = (int)mcache[i] - g0;
+          if (m < 0 || m >= gm) continue;  // (255 = trimmed record)
+          key = kcache[i];
+        } else {
+          m = B.arr_model[ro + i] - g0;
+          if (m < 0 || m >= gm) continue;
+          const double at = B.arr_t[ro + i];
+          if (!(at >= cut)) continue;
+          key = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
+        }
         const unsigned int d = (unsigned int)(key >> shift) & 0xffu;
 #pragma unroll
         for (int q = 0; q < 3; q++) {
@@ -1152,17 +1175,38 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
         }
       }
       __syncthreads();
-      if (threadIdx.x < gm * 3) {
-        const int mm = threadIdx.x / 3, q = threadIdx.x % 3;
-        int left = rank_left[mm][q];
-        unsigned int d = 0;
-        for (; d < 255u; d++) {
-          const int h = (int)hist[mm][q][d];
-          if (left < h) break;
-          left -= h;
+      // digit selection: one warp per (model, quantile), lanes scan 8 bins each
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int t = warp; t < gm * 3; t += kSloThreads / 32) {
+        const int mm = t / 3, q = t % 3;
+        const unsigned int* h = hist[mm][q];
+        int c8[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          c8[j] = (int)h[lane * 8 + j];
+          sum += c8[j];
         }
-        rank_left[mm][q] = left;
-        prefix[mm][q] |= (unsigned long long)d << shift;
+        int incl = sum;  // inclusive scan over lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int excl = incl - sum, left = rank_left[mm][q];
+        // the lane whose bins contain rank `left` (the last lane if ranks run out,
+        // as the sequential scan stops at digit 255)
+        const bool mine = (left >= excl && left < incl) || (lane == 31 && left >= incl);
+        const unsigned who = __ballot_sync(0xffffffffu, mine);
+        if (lane == __ffs(who) - 1) {
+          int l = left - excl;
+          unsigned int d = lane * 8;
+          for (int j = 0; j < 8; j++, d++) {
+            if (d == 255u || l < c8[j]) break;
+            l -= c8[j];
+          }
+          rank_left[mm][q] = l;
+          prefix[mm][q] |= (unsigned long long)d << shift;
+        }
       }
       __syncthreads();
     }
@@ -1563,8 +1607,14 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
     }
     return INTF_OK;
   }
-  k_slo<<<bt->n_scen, kSloThreads, 0, as_stream(stream)>>>(bt->scen, bt->models, *buf, warm_cutoff, out_n, out_met,
-                                                          out_p);
+  const size_t smem = (size_t)kSloCache * 9;  // keys (8 B) + model ids (1 B)
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_slo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_slo<<<bt->n_scen, kSloThreads, smem, as_stream(stream)>>>(bt->scen, bt->models, *buf, warm_cutoff, out_n, out_met,
+                                                             out_p);
   return launch_status("k_slo");
 }
 
