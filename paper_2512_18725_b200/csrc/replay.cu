@@ -1607,12 +1607,8 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
     }
     return INTF_OK;
   }
-  const size_t smem = (size_t)kSloCache * 9;  // keys (8 B) + model ids (1 B)
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_slo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  const size_t smem = (size_t)kSloCache * 9;  // keys (8 B) + model ids (1 B): 36 KB, under the 48 KB default
+  static_assert(kSloCache * 9 <= 48 * 1024, "k_slo cache needs an opt-in shared memory attribute");
   k_slo<<<bt->n_scen, kSloThreads, smem, as_stream(stream)>>>(bt->scen, bt->models, *buf, warm_cutoff, out_n, out_met,
                                                              out_p);
   return launch_status("k_slo");
