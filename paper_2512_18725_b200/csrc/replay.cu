@@ -1607,8 +1607,16 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
     }
     return INTF_OK;
   }
-  const size_t smem = (size_t)kSloCache * 9;  // keys (8 B) + model ids (1 B): 36 KB, under the 48 KB default
-  static_assert(kSloCache * 9 <= 48 * 1024, "k_slo cache needs an opt-in shared memory attribute");
+  // keys (8 B) + model ids (1 B): 36 KB dynamic on top of ~25 KB static -> opt-in
+  // attribute, set once per device (setting it twice is harmless)
+  const size_t smem = (size_t)kSloCache * 9;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool attr_set[64] = {};
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    cudaFuncSetAttribute(k_slo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
   k_slo<<<bt->n_scen, kSloThreads, smem, as_stream(stream)>>>(bt->scen, bt->models, *buf, warm_cutoff, out_n, out_met,
                                                              out_p);
   return launch_status("k_slo");
