@@ -387,6 +387,24 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       if (act) close_lane();
       reseat_lane(act);
       n_reseats += nrun;
+    } else if (nrun == cap) {
+      // ---- FORMATIONS while the GPU is full: until the next completion they
+      // only lengthen the FIFO queue (try_dispatch cannot dispatch), so every
+      // formation before dmin (strictly: a completion at the same instant
+      // goes first) is consumed at once, now = max(now, its time)
+      for (;;) {
+        const int off = n_formed - fbase;  // window lane of the next formation
+        // formation times are non-decreasing: the qualifying lanes are contiguous from `off`
+        const unsigned q = G.ballot(lane >= off && fbase + lane < nb && wf < dmin);
+        const int cnt = __popc(q);
+        if (cnt == 0) break;
+        const double tl = G.shfl(wf, off + cnt - 1);
+        now = now > tl ? now : tl;
+        n_formed += cnt;
+        if (n_formed >= nb || off + cnt < W) break;  // stopped inside this window
+        fbase += W;
+        wf = fbase + lane < nb ? B.b_formed[ro + fbase + lane] : 0.0;
+      }
     } else {
       // ---- FORMATION: batch n_formed joins the FIFO dispatch queue
       now = now > tf ? now : tf;
