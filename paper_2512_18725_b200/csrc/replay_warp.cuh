@@ -193,6 +193,7 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
   double now = 0.0;
   int n_formed = J.b_lo, dq = J.b_lo, n_done = J.b_lo, seg_cursor = 0, n_reseats = 0;
   double last_done = -INFINITY;  // completion time of the latest outcome
+  bool refill = false;           // the completion just processed is followed by a dispatch
 
   // formation-time window: lane l holds b_formed of batch fbase + l
   int fbase = J.b_lo;
@@ -385,7 +386,12 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       freemask |= 1u << cl;
       // _colo_changed(survivors) (`simcore.py:143-146`)
       if (act) close_lane();
-      reseat_lane(act);
+      // a queued batch dispatches at this same instant and reseats every
+      // survivor again; the reseat here would open a zero-length segment that
+      // the dispatch pops (same noise index, progress and counts restored), so
+      // only the dispatch's reseat is computed (both are counted)
+      refill = dq < n_formed;
+      if (!refill) reseat_lane(act);
       n_reseats += nrun;
     } else if (nrun == cap) {
       // ---- FORMATIONS while the GPU is full: until the next completion they
@@ -456,7 +462,8 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
         nz3 = n3;
       }
       // new batch first, then survivors: independent, so in parallel
-      if (was_act) close_lane();
+      if (was_act && !refill) close_lane();  // (after a completion that refills: already closed)
+      refill = false;
       reseat_lane(act);
       n_reseats += nrun;
     }

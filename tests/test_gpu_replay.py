@@ -80,3 +80,21 @@ def test_dispatch_trace_matches_oracle_and_cap(gpu_runs):
         assert np.array_equal(v["b_running"], ref["b_running"]), name
         if len(v["b_running"]):
             assert 1 <= v["b_running"].min() and v["b_running"].max() <= spec["concurrency_cap"]
+
+
+def test_reseat_and_segment_counts_match_oracle(gpu_runs):
+    """Event-level shortcuts in the warp replay (cap-1 chain, bulk formations
+    while full, the completion reseat a same-instant dispatch pops) must keep
+    the reference's reseat count (`simcore.py:133-141`, every `_reseat` call,
+    3,590 for the bundled seed-7 trace) and kept-segment count."""
+    import oracle as O
+
+    for tname, (names, pipe, h) in gpu_runs.items():
+        tab = _golden.table(tname)
+        otab = O.TableArrays(tab.models, tab.max_bs, tab.solo, tab.thr)
+        for s, n in enumerate(names):
+            v = pipe.scenario(h, s)
+            ref = O.run_scenario(_golden.spec(n), otab)
+            assert (v["n_reseats"], v["n_segments"]) == (ref["n_reseats"], ref["n_segments"]), n
+    v = dict(_views(gpu_runs))["bundled_seed7"]
+    assert v["n_reseats"] == 3590 and v["n_segments"] == 3200
