@@ -307,8 +307,10 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       const unsigned cmask = G.ballot(act && batch == bmin);
       const int cl = __ffs(cmask) - 1;
       int nseg_c = 0, off = 0;
+      // RunningBatch.close_segment of the completing batch (`simcore.py:174`)
+      // and of every survivor (`:145`): independent, so one parallel step
+      if (act) close_lane();
       if (lane == cl) {
-        close_lane();
         if (fabs(progress - total) > 1e-6 * total) status |= INTF_ST_PROGRESS;
         const double measured = n_non1 == 0 ? total : now - start;  // `:181-185`
         B.b_start[ro + batch] = start;
@@ -384,8 +386,7 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
         }
       }
       freemask |= 1u << cl;
-      // _colo_changed(survivors) (`simcore.py:143-146`)
-      if (act) close_lane();
+      // _colo_changed(survivors) (`simcore.py:143-146`): closed above;
       // a queued batch dispatches at this same instant and reseats every
       // survivor again; the reseat here would open a zero-length segment that
       // the dispatch pops (same noise index, progress and counts restored), so
