@@ -286,9 +286,10 @@ C4_REQUESTS = 1e6
 
 def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     """C4 shape: one 10^6-request, 16-model (bs <= 64, cap 4) trace replayed
-    with busy-period sharding (speculative idle boundaries, verified and
-    merged on the host between launches -- those gaps are inside the timed
-    region).  Each rank replays its own trace (weak scaling)."""
+    with busy-period sharding (speculative idle boundaries planned, verified
+    and merged on the device; the host reads the todo-list size between
+    launches, inside the timed region).  Each rank replays its own trace
+    (weak scaling)."""
     import torch
     from paper_2512_18725_b200 import engine
     from paper_2512_18725_b200.sweep import c4_scenario, table16
@@ -297,7 +298,7 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     spec = c4_scenario(t16, arch, n_requests=C4_REQUESTS, seed=1 + rank)
     ta = t16.arrays()
     pipe = engine.ReplayPipeline([spec], ta, scale=1.2)
-    engine.replay_segmented(pipe)  # warm-up (also sizes the job scratch)
+    engine.replay_segmented(pipe)  # warm-up (also sizes the job scratch); default slow 2.0, min_len 64
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -307,8 +308,20 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     ms = max_over_ranks(e0.elapsed_time(e1))
     n_req = int(pipe.t["n_req"][0].item())
     st = int(pipe.t["status"][0].item())
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        # the oracle's C heap-engine replay of the same trace (+ its arrivals), one core, once
+        import oracle as O
+
+        t0 = time.perf_counter()
+        ref = O.run_scenario(spec, O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr))
+        dt = time.perf_counter() - t0
+        cpu = {"value": len(ref["arr_t"]) / dt, "unit": "requests/s", "cores": 1, "kind": "port",
+               "sample": f"the whole {len(ref['arr_t'])}-request trace (oracle C replay: heap engine + arrivals) "
+                         f"in {dt:.2f} s"}
     return {"metric": "requests replayed/sec (single long trace)", "value": world * n_req / (ms / 1e3),
             "unit": "requests/s", "ms_per_trace": ms, "requests": n_req, "status": st, **stats,
+            "cpu_baseline": cpu,
             "workload": "C4: 16 models (6 default + 10 rng(123) archetypes), bs 1-64, cap 4, window U(10,20) ms, "
                         "sigma 0.05, total rho 0.5 at bs 64; one trace per GPU; arrivals + formation + noise + "
                         "busy-period-sharded replay + SLO + features"}
