@@ -903,6 +903,120 @@ __global__ void __launch_bounds__(64) k_rls(const double* __restrict__ X, const 
   if (status) status[s] = st;
 }
 
+// Lane-parallel RLS: 8 lanes per stream, lane r < 7 owns row r of P (the
+// 7x7 gain matrix), so the 49 divisions by lambda of each update run 7-wide
+// and a warp advances 4 streams.  Per element the operations are exactly
+// k_rls's (same fma chains, same order), so the results are identical:
+//   Pz_r = P[r,:] . z (fma chain)        -> gathered by shuffles
+//   zPz  = z . Pz (fma chain, every lane) -> denom, reset rule
+//   k_r  = Pz_r / denom                   -> gathered
+//   w   += k e (every lane keeps w)
+//   P[r,:] = (P[r,:] - k_r Pz) / lambda; then 0.5 (P + P^T) via a shared-memory transpose
+constexpr int kRlsGroup = 8;
+__global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, const double* __restrict__ Y,
+                                                const long long* __restrict__ off, int n_streams,
+                                                const double* __restrict__ lamv, double* params, double* Pg,
+                                                double* pred, int32_t* status) {
+  __shared__ double tr[128 / kRlsGroup][7][8];
+  const int gi = threadIdx.x / kRlsGroup, r = threadIdx.x % kRlsGroup;
+  const int s = blockIdx.x * (128 / kRlsGroup) + gi;
+  const unsigned gmask = 0xffu << ((threadIdx.x & 31) & ~(kRlsGroup - 1));
+  const bool live = s < n_streams;
+  const int ss = live ? s : 0;
+  const int rr = r < 7 ? r : 6;  // lane 7 shadows row 6 (keeps every shuffle full-group)
+  double w[7], P[7];
+#pragma unroll
+  for (int i = 0; i < 7; i++) w[i] = params[ss * 7 + i];
+#pragma unroll
+  for (int j = 0; j < 7; j++) P[j] = Pg[(long long)ss * 49 + rr * 7 + j];
+  const double lam = lamv[ss];
+  int st = 0;
+  const long long i0 = live ? off[s] : 0, i1 = live ? off[s + 1] : 0;
+  // the next sample's row is loaded one update ahead (off the update chain)
+  double zn[6], yn = 0.0;
+#pragma unroll
+  for (int j = 0; j < 6; j++) zn[j] = i0 < i1 ? X[i0 * 6 + j] : 0.0;
+  if (i0 < i1) yn = Y[i0];
+  for (long long it = i0; it < i1; it++) {
+    double z[7];
+#pragma unroll
+    for (int j = 0; j < 6; j++) z[j] = zn[j];
+    z[6] = 1.0;
+    const double ycur = yn;
+    if (it + 1 < i1) {
+#pragma unroll
+      for (int j = 0; j < 6; j++) zn[j] = X[(it + 1) * 6 + j];
+      yn = Y[it + 1];
+    }
+    const double yh = predict7(w, z);
+    if (r == 0) pred[it] = yh;
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < 7; j++) a = fma(P[j], z[j], a);
+    double Pz[7];
+#pragma unroll
+    for (int j = 0; j < 7; j++) Pz[j] = __shfl_sync(gmask, a, j, kRlsGroup);
+    double zPz = 0.0;
+#pragma unroll
+    for (int j = 0; j < 7; j++) zPz = fma(z[j], Pz[j], zPz);
+    double denom = lam + zPz;
+    if (!(denom > 0.0) || !isfinite(denom)) {  // P reset (`predict.py:142-146`)
+      st |= 2;
+#pragma unroll
+      for (int j = 0; j < 7; j++) P[j] = (j == rr) ? 100.0 : 0.0;
+#pragma unroll
+      for (int j = 0; j < 7; j++) Pz[j] = 100.0 * z[j];
+      zPz = 0.0;
+#pragma unroll
+      for (int j = 0; j < 7; j++) zPz = fma(z[j], Pz[j], zPz);
+      denom = lam + zPz;
+    }
+    double pzr = Pz[0];  // Pz[rr] without dynamic register indexing
+#pragma unroll
+    for (int j = 1; j < 7; j++) pzr = j == rr ? Pz[j] : pzr;
+    const double kr = pzr / denom;
+    double k[7];
+#pragma unroll
+    for (int j = 0; j < 7; j++) k[j] = __shfl_sync(gmask, kr, j, kRlsGroup);
+    const double e = ycur - yh;
+#pragma unroll
+    for (int j = 0; j < 7; j++) w[j] = w[j] + k[j] * e;
+#pragma unroll
+    for (int j = 0; j < 7; j++) P[j] = (P[j] - kr * Pz[j]) / lam;
+    // symmetrize: lane r needs P[j][r] of every row j
+    double(*T)[8] = tr[gi];
+    if (r < 7) {
+#pragma unroll
+      for (int j = 0; j < 7; j++) T[r][j] = P[j];
+    }
+    __syncwarp(gmask);
+#pragma unroll
+    for (int j = 0; j < 7; j++) {
+      if (j == rr) continue;
+      const double pt = T[j][rr];
+      P[j] = 0.5 * (P[j] + pt);  // == 0.5 (P[rr][j] + P[j][rr]) == the (j, rr) entry
+    }
+    __syncwarp(gmask);
+    bool fin = true;
+#pragma unroll
+    for (int j = 0; j < 7; j++) fin &= isfinite(w[j]);
+    if (!fin) {
+      st |= 1;
+      break;
+    }
+  }
+  if (!live) return;
+  if (r == 0) {
+#pragma unroll
+    for (int i = 0; i < 7; i++) params[s * 7 + i] = w[i];
+    if (status) status[s] = st;
+  }
+  if (r < 7) {
+#pragma unroll
+    for (int j = 0; j < 7; j++) Pg[(long long)s * 49 + r * 7 + j] = P[j];
+  }
+}
+
 // ===================================================================== K8
 constexpr int kEvalThreads = 256;
 
@@ -1202,9 +1316,9 @@ int intf_rls_streams(const double* X, const double* y, const int64_t* off, int32
   if (!X || !y || !off || !lam || !params || !P || !pred || n_streams < 0)
     return bad_input("intf_rls_streams: bad argument");
   if (n_streams == 0) return INTF_OK;
-  k_rls<<<ceil_div(n_streams, 64), 64, 0, as_stream(stream)>>>(X, y, (const long long*)off, n_streams, lam, params, P,
-                                                               pred, status);
-  return launch_status("k_rls");
+  k_rls_g8<<<ceil_div(n_streams, 128 / kRlsGroup), 128, 0, as_stream(stream)>>>(X, y, (const long long*)off, n_streams,
+                                                                               lam, params, P, pred, status);
+  return launch_status("k_rls_g8");
 }
 
 int intf_eval_report(const double* yhat, const double* y, const int64_t* off, int32_t n_seg, double* out,
