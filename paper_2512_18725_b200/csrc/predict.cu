@@ -3,7 +3,7 @@
 //       predictions for many decisions (HBM-write bound)
 //   K6  OLS normal-equation statistics (HBM-read bound) + 7x7 fp64 solve
 //                                                   `predict.py:53-72,112-134`
-//   K7  prequential SGD / RLS streams, one thread per stream `predict.py:75-205`
+//   K7  prequential SGD (thread per stream) / RLS (8 lanes per stream) `predict.py:75-205`
 //   K8  EvalReport: MSE + nearest-rank relative-error quantiles
 //                                                   `predict.py:176-205`
 #include <math.h>
@@ -826,87 +826,10 @@ __global__ void k_sgd(const double* __restrict__ X, const double* __restrict__ Y
   if (status) status[s] = st;
 }
 
-// rls_update (`predict.py:137-154`); P kept in registers (fully unrolled).
-__global__ void __launch_bounds__(64) k_rls(const double* __restrict__ X, const double* __restrict__ Y,
-                                            const long long* __restrict__ off, int n_streams,
-                                            const double* __restrict__ lamv, double* params, double* Pg,
-                                            double* pred, int32_t* status) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n_streams) return;
-  double w[7], P[49];
-#pragma unroll
-  for (int i = 0; i < 7; i++) w[i] = params[s * 7 + i];
-#pragma unroll
-  for (int i = 0; i < 49; i++) P[i] = Pg[(long long)s * 49 + i];
-  const double lam = lamv[s];
-  int st = 0;
-  for (long long it = off[s]; it < off[s + 1]; it++) {
-    double z[7];
-#pragma unroll
-    for (int j = 0; j < 6; j++) z[j] = X[it * 6 + j];
-    z[6] = 1.0;
-    const double yh = predict7(w, z);
-    pred[it] = yh;
-    double Pz[7];
-#pragma unroll
-    for (int i = 0; i < 7; i++) {
-      double a = 0.0;
-#pragma unroll
-      for (int j = 0; j < 7; j++) a = fma(P[i * 7 + j], z[j], a);
-      Pz[i] = a;
-    }
-    double zPz = 0.0;
-#pragma unroll
-    for (int j = 0; j < 7; j++) zPz = fma(z[j], Pz[j], zPz);
-    double denom = lam + zPz;
-    if (!(denom > 0.0) || !isfinite(denom)) {  // P reset (`predict.py:142-146`)
-      st |= 2;
-#pragma unroll
-      for (int i = 0; i < 49; i++) P[i] = (i % 8 == 0) ? 100.0 : 0.0;
-#pragma unroll
-      for (int i = 0; i < 7; i++) Pz[i] = 100.0 * z[i];
-      zPz = 0.0;
-#pragma unroll
-      for (int j = 0; j < 7; j++) zPz = fma(z[j], Pz[j], zPz);
-      denom = lam + zPz;
-    }
-    double k[7];
-#pragma unroll
-    for (int i = 0; i < 7; i++) k[i] = Pz[i] / denom;
-    const double e = Y[it] - yh;
-#pragma unroll
-    for (int i = 0; i < 7; i++) w[i] = w[i] + k[i] * e;
-#pragma unroll
-    for (int i = 0; i < 7; i++)
-#pragma unroll
-      for (int j = 0; j < 7; j++) P[i * 7 + j] = (P[i * 7 + j] - k[i] * Pz[j]) / lam;
-#pragma unroll
-    for (int i = 0; i < 7; i++)
-#pragma unroll
-      for (int j = i + 1; j < 7; j++) {
-        const double v = 0.5 * (P[i * 7 + j] + P[j * 7 + i]);
-        P[i * 7 + j] = v;
-        P[j * 7 + i] = v;
-      }
-    bool fin = true;
-#pragma unroll
-    for (int j = 0; j < 7; j++) fin &= isfinite(w[j]);
-    if (!fin) {
-      st |= 1;
-      break;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 7; i++) params[s * 7 + i] = w[i];
-#pragma unroll
-  for (int i = 0; i < 49; i++) Pg[(long long)s * 49 + i] = P[i];
-  if (status) status[s] = st;
-}
-
-// Lane-parallel RLS: 8 lanes per stream, lane r < 7 owns row r of P (the
-// 7x7 gain matrix), so the 49 divisions by lambda of each update run 7-wide
-// and a warp advances 4 streams.  Per element the operations are exactly
-// k_rls's (same fma chains, same order), so the results are identical:
+// rls_update (`predict.py:137-154`), lane-parallel: 8 lanes per stream, lane
+// r < 7 owns row r of P (the 7x7 gain matrix), so the 49 divisions by lambda
+// of each update run 7-wide and a warp advances 4 streams.  Per element the
+// operations are the reference's, in its order:
 //   Pz_r = P[r,:] . z (fma chain)        -> gathered by shuffles
 //   zPz  = z . Pz (fma chain, every lane) -> denom, reset rule
 //   k_r  = Pz_r / denom                   -> gathered
