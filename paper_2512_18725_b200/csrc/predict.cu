@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(kStreamThreads, 8) k_cand_step(
 
 // ===================================================================== K6
 constexpr int kOlsThreads = 256;
-constexpr int kOlsBlocks = 592;  // 4 x 148 SMs
+constexpr int kOlsBlocks = 296;  // one wave: 2 x 148 SMs at 128 registers x 256 threads
 constexpr int kStats = 35;       // 28 upper-triangular G terms + 7 r terms
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -451,13 +451,15 @@ __global__ void __launch_bounds__(kOlsThreads) k_ols_partial(const double* __res
   double acc[kStats];
 #pragma unroll
   for (int i = 0; i < kStats; i++) acc[i] = 0.0;
+  // 16-byte loads, four rows in flight per thread (X rows are 48 B: 16-byte
+  // aligned); the accumulation order per thread is unchanged (row order)
+#pragma unroll 4
   for (long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x; row < n;
        row += (long long)gridDim.x * blockDim.x) {
-    double z[7];
-#pragma unroll
-    for (int i = 0; i < 6; i++) z[i] = X[row * 6 + i];
-    z[6] = 1.0;
-    const double yy = y[row];
+    const double2* xr = reinterpret_cast<const double2*>(X + row * 6);
+    const double2 a = __ldg(xr), b = __ldg(xr + 1), c = __ldg(xr + 2);
+    const double z[7] = {a.x, a.y, b.x, b.y, c.x, c.y, 1.0};
+    const double yy = __ldg(y + row);
     int t = 0;
 #pragma unroll
     for (int i = 0; i < 7; i++)
