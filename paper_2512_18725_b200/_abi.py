@@ -56,7 +56,7 @@ REPLAY_BUFFER_FIELDS = [
     "out_order", "b_running", "r_batch", "r_slo_met",
     "s_tbegin", "s_tend", "s_slowdown", "s_colo",
     "n_batches", "n_segments", "n_reseats", "status", "slot_seg", "noise_tab", "mb_t", "mb_info", "n_mb", "slo_ws",
-    "form_ws",
+    "form_ws", "order",
 ]
 SLO_WS_INTS = 256 + 32 * 3 * 256 + 32 * 3 * 4
 

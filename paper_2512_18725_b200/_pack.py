@@ -141,7 +141,7 @@ BUFFER_PLAN = [
     ("n_batches", np.int32, "scen"), ("n_segments", np.int32, "scen"), ("n_reseats", np.int32, "scen"),
     ("status", np.int32, "scen"), ("slot_seg", np.float64, "slots"), ("noise_tab", np.float64, "noise"),
     ("mb_t", np.float64, "list"), ("mb_info", np.int32, "list4"), ("n_mb", np.int32, "models"),
-    ("slo_ws", np.int32, "slows"), ("form_ws", np.int32, "list3"),
+    ("slo_ws", np.int32, "slows"), ("form_ws", np.int32, "list3"), ("order", np.int32, "scen1"),
 ]
 
 
@@ -150,7 +150,7 @@ def sizes(pb: PackedBatch, seg_stride: int, noise_k: int = 0) -> dict:
         "noise": max(pb.total_req, 1) * max(noise_k, 1),
         "req": max(pb.total_req, 1), "list": max(pb.total_list, 1), "list4": 4 * max(pb.total_list, 1),
         "list3": 3 * max(pb.total_list, 1),
-        "scen": max(pb.n_scen, 1),
+        "scen": max(pb.n_scen, 1), "scen1": pb.n_scen + 1,
         "models": max(pb.n_models, 1), "seg": max(pb.total_seg, 1), "seg3": 3 * max(pb.total_seg, 1),
         "slots": max(pb.n_scen, 1) * pb.cap_max * seg_stride * 5,
         "slows": _abi.SLO_WS_INTS,

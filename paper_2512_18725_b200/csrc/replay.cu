@@ -483,6 +483,52 @@ __global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __rest
 #endif
 constexpr int kReplayWarps = 4;
 constexpr int kReplayW = 32;  // measured: one scenario per warp beats 4 x 8-lane groups (divergence)
+// Replay order = longest-processing-time first by the device's own work
+// estimate: formed batches, cap-1 scenarios weighted 1/5 (their max-plus chain
+// is ~5x cheaper per batch).  A counting sort over 4,096 buckets (descending):
+// histogram, one-block scan, scatter; `order` receives the permutation.
+constexpr int kOrderBuckets = 4096;
+__device__ __forceinline__ int order_bucket(const intf_scenario* scen, const intf_replay_buffers& B, int s) {
+  const int nb = B.n_batches[s];
+  const int w = scen[s].cap == 1 ? nb / 5 : nb;
+  const int k = w / 2;
+  return kOrderBuckets - 1 - (k < kOrderBuckets - 1 ? k : kOrderBuckets - 1);  // heavy -> bucket 0
+}
+__global__ void k_order_hist(const intf_scenario* __restrict__ scen, int n_scen, intf_replay_buffers B,
+                             int32_t* __restrict__ cnt) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_scen) atomicAdd(&cnt[order_bucket(scen, B, s)], 1);
+}
+__global__ void __launch_bounds__(1024) k_order_scan(int32_t* __restrict__ cnt) {
+  __shared__ int sh[1024];
+  const int t = threadIdx.x;  // 4 buckets per thread
+  int v[4], sum = 0;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    v[j] = cnt[4 * t + j];
+    sum += v[j];
+  }
+  sh[t] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int x = t >= o ? sh[t - o] : 0;
+    __syncthreads();
+    sh[t] += x;
+    __syncthreads();
+  }
+  int run = sh[t] - sum;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    cnt[4 * t + j] = run;
+    run += v[j];
+  }
+}
+__global__ void k_order_scatter(const intf_scenario* __restrict__ scen, int n_scen, intf_replay_buffers B,
+                                int32_t* __restrict__ cnt) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_scen) B.order[atomicAdd(&cnt[order_bucket(scen, B, s)], 1)] = s;
+}
+
 // Persistent: one block per resident slot (INTF_REPLAY_MINB per SM); each warp
 // pulls the next scenario index from a counter (B.slo_ws[0], free until the
 // SLO pass) as soon as its previous scenario is done, so a long scenario
@@ -493,10 +539,11 @@ __global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_replay_
   __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
   const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
   for (;;) {
-    int s = 0;
-    if ((threadIdx.x & 31) == 0) s = atomicAdd(B.slo_ws, 1);
-    s = __shfl_sync(0xffffffffu, s, 0);
-    if (s >= n_scen) return;
+    int k = 0;
+    if ((threadIdx.x & 31) == 0) k = atomicAdd(B.slo_ws, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= n_scen) return;
+    const int s = B.order[k];  // longest-processing-time first (k_order_*)
     const int st0 = B.status[s];
     if (st0 & (INTF_ST_CAP | INTF_ST_OVERFLOW)) continue;
     const intf_scenario& S = scen[s];
@@ -1576,8 +1623,14 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
                                                                  *buf);
     if ((rc = launch_status("k_noise_table"))) return rc;
   }
-  if (!buf->slo_ws) return bad_input("intf_replay: slo_ws scratch (work counter) missing");
-  cudaMemsetAsync(buf->slo_ws, 0, sizeof(int32_t), st);
+  if (!buf->slo_ws || !buf->order) return bad_input("intf_replay: slo_ws / order scratch missing");
+  // LPT order via slo_ws (free until the SLO pass): [0] work counter, [1, 1 + 4096) bucket counts
+  int32_t* cnt = buf->slo_ws + 1;
+  cudaMemsetAsync(buf->slo_ws, 0, sizeof(int32_t) * (1 + kOrderBuckets), st);
+  k_order_hist<<<ceil_div(bt->n_scen, 256), 256, 0, st>>>(bt->scen, bt->n_scen, *buf, cnt);
+  k_order_scan<<<1, 1024, 0, st>>>(cnt);
+  k_order_scatter<<<ceil_div(bt->n_scen, 256), 256, 0, st>>>(bt->scen, bt->n_scen, *buf, cnt);
+  if ((rc = launch_status("k_order_*"))) return rc;
   const unsigned per_wave = 148u * INTF_REPLAY_MINB, need = ceil_div(bt->n_scen, kReplayWarps * (32 / kReplayW));
   k_replay_warp<<<need < per_wave ? need : per_wave, 32 * kReplayWarps, 0, st>>>(bt->scen, bt->n_scen, bt->models,
                                                                                   *table, *buf);
