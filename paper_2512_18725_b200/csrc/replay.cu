@@ -16,7 +16,11 @@ using namespace intf;
 
 namespace {
 
-constexpr int kBigList = 4096;  // model lists this long: parallel gaps + one-thread scan (long traces)
+#ifndef INTF_BIG_LIST
+#define INTF_BIG_LIST 4096
+#endif
+constexpr int kBigList = INTF_BIG_LIST;  // model lists this long: parallel gaps + one-thread scan (long traces)
+constexpr int kLongForm = 4096;         // model lists this long: pointer-doubling batch formation
 constexpr int kBigJobs = 1 << 15;  // scenarios this long: block-parallel job plan / verify
 constexpr int kGapRun = 8;      // consecutive draws per thread in k_gen_gaps
 
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(32 * kFormModelWarps) k_form_models(const intf
   const int g = blockIdx.x * kFormModelWarps + (threadIdx.x >> 5);
   if (g >= n_models_total) return;
   const intf_model& M = models[g];
-  if (M.list_cap >= kBigList) return;  // long lists: k_form_nxt .. k_form_emit
+  if (M.list_cap >= kLongForm) return;  // long lists: k_form_nxt .. k_form_emit
   const intf_scenario& S = scen[M.scen];
   const bool bad = (B.status[M.scen] & INTF_ST_OVERFLOW) || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 ||
                    S.max_bs < 1 || S.n_models > kMaxModels;
@@ -300,7 +304,7 @@ __device__ __forceinline__ LongModel long_model(const intf_scenario* scen, const
   if (r.g >= n_models) return r;
   const intf_model& M = models[r.g];
   const intf_scenario& S = scen[M.scen];
-  if (M.list_cap < kBigList) return r;
+  if (M.list_cap < kLongForm) return r;
   if ((B.status[M.scen] & INTF_ST_OVERFLOW) || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 || S.max_bs < 1 ||
       S.n_models > kMaxModels)
     return r;
@@ -356,7 +360,7 @@ __global__ void k_form_emit(const intf_scenario* __restrict__ scen, const intf_m
   if (!L.ok) {
     // long models of bad scenarios form nothing
     const int g = blockIdx.z * gridDim.y + blockIdx.y;
-    if (g < n_models && models[g].list_cap >= kBigList && blockIdx.x == 0 && threadIdx.x == 0) B.n_mb[g] = 0;
+    if (g < n_models && models[g].list_cap >= kLongForm && blockIdx.x == 0 && threadIdx.x == 0) B.n_mb[g] = 0;
     return;
   }
   if (L.n == 0) {
@@ -1476,7 +1480,7 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
   k_form_models<<<ceil_div(bt->n_models, kFormModelWarps), 32 * kFormModelWarps, 0, st>>>(bt->scen, bt->models,
                                                                                          bt->n_models, *buf);
   if ((rc = launch_status("k_form_models"))) return rc;
-  if (bt->max_list_cap >= kBigList) {  // long model lists: pointer-doubling formation
+  if (bt->max_list_cap >= kLongForm) {  // long model lists: pointer-doubling formation
     if (!buf->form_ws) return bad_input("formation of long lists needs form_ws scratch");
     const unsigned m = (unsigned)bt->n_models, y = m < 65535u ? m : 65535u;
     const dim3 grid(ceil_div(bt->max_list_cap, 256), y, ceil_div(m, y));
