@@ -1107,9 +1107,9 @@ __global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen
 // (latency >= 0, so IEEE bit order == numeric order); three order
 // statistics per model share each pass's histograms (shared memory).
 constexpr int kSloThreads = 256;
-constexpr int kSloGroup = 8;          // models per radix pass group
+constexpr int kSloGroup = 4;          // models per radix pass group (smem: 12 KB of histograms)
 constexpr int kSloBigReq = 1 << 16;  // above this request capacity: grid-wide SLO passes
-constexpr int kSloCache = 4096;      // records whose latency keys k_slo keeps in shared memory
+constexpr int kSloCache = 2048;      // records whose latency keys k_slo keeps in shared memory (18 KB)
 
 __device__ __forceinline__ unsigned long long lat_key(double v) {
   unsigned long long u = (unsigned long long)__double_as_longlong(v);
