@@ -535,9 +535,77 @@ __device__ __forceinline__ void group_next_formation(const LaneGroup<W>& G, cons
 // model forms its batches in parallel into per-model lists of
 // (time, kind, key) + (count, head).  A rank-merge then orders all batches
 // of a scenario exactly as the reference heap pops formation events.
+// One model's batches by a W-lane group, max_batch_size <= W: the arrival
+// list streams through a 2W-element register window (two coalesced loads per
+// W heads), the head time and the members come from shuffles and ballots (no
+// global load on the h -> h + cnt chain), and the events are held one per
+// lane and flushed W at a time with coalesced stores.  next_formation's rule:
+// cnt = 1 + #(t[h+j] < t[h] + window), 0 < j < max_bs (sorted: a prefix).
+template <int W>
+__device__ __forceinline__ void form_model_win(const LaneGroup<W>& G, const intf_scenario& S, const intf_model& Md,
+                                               int n_list, const intf_replay_buffers& B, int g) {
+  const double* lt = B.list_t + Md.list_off;
+  const int32_t* lrid = B.list_rid + Md.list_off;
+  const int lane = G.lane;
+  int h = 0, c = 0, base = 0;
+  double w0 = lane < n_list ? lt[lane] : INFINITY, w1 = W + lane < n_list ? lt[W + lane] : INFINITY;
+  int r0 = lane < n_list ? lrid[lane] : 0, r1 = W + lane < n_list ? lrid[W + lane] : 0;  // request ids
+  double ot = 0.0;
+  int okind = 0, okey = 0, ocnt = 0, oh = 0;
+  auto flush = [&](int c0, int k) {
+    if (lane < k) {
+      B.mb_t[Md.list_off + c0 + lane] = ot;
+      reinterpret_cast<int4*>(B.mb_info)[Md.list_off + c0 + lane] = make_int4(okind, okey, ocnt, oh);
+    }
+  };
+  while (h < n_list) {
+    if (h - base >= W) {  // cnt <= max_bs <= W: one slide keeps h inside [base, base + W)
+      base += W;
+      w0 = w1;
+      r0 = r1;
+      w1 = base + W + lane < n_list ? lt[base + W + lane] : INFINITY;
+      r1 = base + W + lane < n_list ? lrid[base + W + lane] : 0;
+    }
+    const int o = h - base;
+    const double D = G.shfl(w0, o) + S.window_ms;  // arm_window at the first arrival (`batcher.py:66-68`)
+    const int lim = min(o + S.max_bs, n_list - base);  // window offsets (o, lim) may join
+    const unsigned m0 = G.ballot(lane > o && lane < lim && w0 < D);
+    const unsigned m1 = G.ballot(W + lane > o && W + lane < lim && w1 < D);
+    const int cnt = 1 + __popc(m0) + __popc(m1);
+    const int last = o + cnt - 1;
+    const double tl = last < W ? G.shfl(w0, last) : G.shfl(w1, last - W);
+    const int rl = last < W ? G.shfl(r0, last) : G.shfl(r1, last - W);
+    if (lane == (c & (W - 1))) {  // batch c's event, held by lane c % W
+      if (cnt == S.max_bs) {  // early emit at max_batch_size (`batcher.py:70-71`)
+        ot = tl;
+        okind = KIND_ARRIVAL;
+        okey = rl;
+      } else {  // window expiry (`batcher.py:74-85`)
+        ot = D;
+        okind = KIND_WINDOW;
+        okey = (int32_t)Md.crc;
+      }
+      ocnt = cnt;
+      oh = h;
+    }
+    h += cnt;
+    c++;
+    if ((c & (W - 1)) == 0) flush(c - W, W);
+  }
+  if (c & (W - 1)) flush(c & ~(W - 1), c & (W - 1));
+  if (lane == 0) B.n_mb[g] = c;
+}
+
+// Per-model formation by a warp (max_batch_size > 32: the original walk with
+// global loads; <= 32: the windowed form).  A rank-merge then orders all
+// batches of a scenario exactly as the reference heap pops formation events.
 __device__ __forceinline__ void form_model_warp(const intf_scenario& S, const intf_model& Md, int n_list,
                                                 const intf_replay_buffers& B, int g) {
   const LaneGroup<32> G;
+  if (S.max_bs <= 32) {
+    form_model_win<32>(G, S, Md, n_list, B, g);
+    return;
+  }
   const double* lt = B.list_t + Md.list_off;
   const int32_t* lrid = B.list_rid + Md.list_off;
   int h = 0, c = 0;
