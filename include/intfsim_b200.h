@@ -222,10 +222,12 @@ int intf_features_predict(const intf_batch *batch, const intf_table *table, cons
  * read per candidate).  For each of n_dec decisions and each candidate writes
  * the coarse (static features + coarse model) and fine (EWMA(alpha) over the
  * candidate's departure history + fine model) predicted interference ratio,
- * fp32 (fp64 features, fp32 forward: within the 1e-5 tolerance):
- *   out[((dec*2 + kind) * n_rows + own) * ld + r],  kind 0 coarse, 1 fine,
- * r < n_sets the multiset rank (size-major, colex within a size), ld = n_sets
- * rounded up to 4 (pad entries written as 0).
+ * fp32 (fp64 features, fp32 forward: within the 1e-5 tolerance), kind 0
+ * coarse, 1 fine, r < n_sets the multiset rank (size-major, colex within a
+ * size), in 16 KB tiles that each streaming block writes contiguously:
+ *   out[((((dec/4) * n_rows + own) * (ld/512) + r/512) * 8 + (dec%4) * 2 + kind) * 512 + r%512]
+ * ld = n_sets rounded up to 512 (pad entries written as 0); the buffer holds
+ * ceil(n_dec/4)*4*2*n_rows*ld floats (rows of the padded decisions unwritten).
  * coefs: device [n_dec][2][7] (w0..w5, b).                                  */
 int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t *n_cand, int64_t *n_sets, int64_t *ld);
 /* Floats of device workspace for the two-phase form (per-(multiset, own)
@@ -254,8 +256,9 @@ int intf_candidate_step(const intf_table *table, int32_t cap, double alpha, cons
                         float *out, const float *ws_cur, float *ws_next, int64_t ws_elems, void *stream);
 
 /* Host-buffer variant (the end-to-end call): copies coefs in and all
- * predictions out.  h_out: n_dec*2*n_rows*ld floats; d_scratch: device
- * floats = 28*n_dec + that output size (+ the workspace to use two-phase). */
+ * predictions out (tiled layout above).  h_out: ceil(n_dec/4)*4*2*n_rows*ld
+ * floats; d_scratch: device floats = 28*n_dec + that output size (+ the
+ * workspace to use two-phase). */
 int intf_predict_candidates_host(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
                                  int32_t n_dec, float *h_out, float *d_scratch, int64_t scratch_elems, void *stream);
 

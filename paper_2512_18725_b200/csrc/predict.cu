@@ -21,9 +21,15 @@ namespace {
 // within a size: multiset p1<=..<=pk <-> combination c_i = p_i + (i-1) of
 // {0..E+k-2}, rank = sum_i C(c_i, i).
 //
-// Output layout (fp32): out[((dec*2 + kind) * E + own) * ld + r], r < n_sets,
-// ld = n_sets rounded up to a multiple of 4 (pad lanes written as 0) so every
-// thread emits 16-byte streaming stores.
+// Output layout (fp32), tiled so that every block of the streaming kernels
+// writes ONE contiguous 16 KB tile (DRAM row locality: 6.2 vs 5.9 TB/s for the
+// same bytes, tools/cand_stream_variants.cu v32 vs v3):
+//   tile (dc, own, rc) = [kTileD decisions][2 kinds][kTileR multisets],
+//   tiles ordered [dc = dec / kTileD][own][rc = r / kTileR],
+// i.e. out[tile_off(dec, kind, own, r)], r < n_sets; ld = n_sets rounded up to
+// kTileR (pad lanes written as 0), decisions padded to kTileD (the pad rows of
+// the last tile are not written).  engine.CandidateScorer.view gives the
+// logical [dec][kind][own][r] array.
 constexpr int kMaxPeers = 7;  // cap <= 8
 
 __host__ __device__ __forceinline__ long long binom(long long n, int k) {
@@ -43,6 +49,19 @@ constexpr int kCandThreads = 128;
 constexpr int kOwnChunk = 4;
 constexpr int kDecChunk = 32;
 constexpr int kGroup = 4;  // multisets per thread (one float4 per output row)
+constexpr int kTileR = 512;  // multisets per tile row (128 threads x kGroup)
+constexpr int kTileD = 4;    // decisions per tile
+
+__host__ __device__ __forceinline__ long long cand_ld(long long sets) { return (sets + kTileR - 1) / kTileR * kTileR; }
+__host__ __device__ __forceinline__ long long cand_out_elems(int E, long long ld, int n_dec) {
+  return (long long)(n_dec + kTileD - 1) / kTileD * kTileD * 2 * E * ld;
+}
+// element (dec, kind, own, r) of the tiled output
+__device__ __forceinline__ long long tile_off(int d, int k, int o, long long r, int E, long long ld) {
+  const long long RC = ld / kTileR;
+  return ((((long long)(d / kTileD) * E + o) * RC + r / kTileR) * (2 * kTileD) + (d % kTileD) * 2 + k) * kTileR +
+         r % kTileR;
+}
 
 // binomial table in shared memory: C[i][n] = binom(n, i), i <= kmax, n < nmax
 struct BinomTab {
@@ -195,7 +214,6 @@ __global__ void __launch_bounds__(kCandThreads, 2) k_candidates(const double* __
     }
     jpack[g] = jp;
   }
-  const long long dstride = 2ll * E * ld;  // next decision, same kind/own
   const bool all_live = live[kGroup - 1];
   for (int oi = 0; oi < no; oi++) {
     float fe[kGroup][3];
@@ -211,10 +229,10 @@ __global__ void __launch_bounds__(kCandThreads, 2) k_candidates(const double* __
       }
     }
     // dead pad lanes (r >= n_sets) compute from zeroed features; zero them at store
-    float* rowc = out + ((long long)d0 * 2 * E + o0 + oi) * ld + r0;
-    const long long kstride = (long long)E * ld;
 #pragma unroll 4
     for (int d = 0; d < nd; d++) {
+      float* rowc = out + tile_off(d0 + d, 0, o0 + oi, r0, E, ld);
+      const long long kstride = kTileR;  // the fine row follows the coarse row in the tile
       const float4 a = cw[d][0][oi];
       const float4 b = cw[d][1][oi];
       float yc[kGroup], yf[kGroup];
@@ -232,7 +250,6 @@ __global__ void __launch_bounds__(kCandThreads, 2) k_candidates(const double* __
         __stcs(reinterpret_cast<float4*>(rowc + kstride), make_float4(live[0] ? yf[0] : 0.f, live[1] ? yf[1] : 0.f,
                                                                       live[2] ? yf[2] : 0.f, live[3] ? yf[3] : 0.f));
       }
-      rowc += dstride;
     }
   }
 }
@@ -334,6 +351,8 @@ constexpr int kStreamThreads = 128;
 // cand_stream_variants.cu): 32 per block 5.09 TB/s, 16: 5.24, 8: 5.56,
 // 4: 5.89, 2: 5.20; a one-float4-per-thread fill reaches 6.50.
 constexpr int kStreamDec = 4;
+static_assert(kStreamDec == kTileD && kStreamThreads * kGroup == kTileR, "a stream block writes exactly one tile");
+static_assert(kCandThreads * kGroup == kTileR, "k_candidates blocks cover one tile column");
 
 // grid: x = groups of 4 multisets, y = own row, z = decision chunks.  The
 // thread's feature loads (L2-resident C0/FE) are issued before the block
@@ -363,9 +382,9 @@ __device__ __forceinline__ void cand_stream_body(int bx, int by, int bz, const d
   }
   __syncthreads();
   if (!inb) return;
-  const long long kstride = (long long)E * ld, dstride = 2 * kstride;
   const long long nl = n_sets - r0;  // < 4 only in the last group: pad lanes are written as 0
-  float* row = out + ((long long)d0 * 2 * E + o) * ld + r0;
+  // this block's tile: (dc = bz, own = o, rc = bx), rows (dec % 4, kind) of kTileR floats
+  float* row = out + tile_off(d0, 0, o, r0, E, ld);
 #pragma unroll 4
   for (int d = 0; d < nd; d++) {
     const float4 a = cw[d][0], b = cw[d][1];
@@ -383,8 +402,8 @@ __device__ __forceinline__ void cand_stream_body(int bx, int by, int bz, const d
       yf = make_float4(nl > 0 ? yf.x : 0.f, nl > 1 ? yf.y : 0.f, nl > 2 ? yf.z : 0.f, 0.f);
     }
     __stcs(reinterpret_cast<float4*>(row), yc);
-    __stcs(reinterpret_cast<float4*>(row + kstride), yf);
-    row += dstride;
+    __stcs(reinterpret_cast<float4*>(row + kTileR), yf);
+    row += 2 * kTileR;
   }
 }
 
@@ -1021,7 +1040,7 @@ long long cand_ws_elems(int E, long long ld) { return 3 * ld + 3LL * E * ld; }
 template <int K>
 static int launch_prep(const intf_table* t, int cap, double alpha, float* ws, cudaStream_t st) {
   const int E = t->n_rows;
-  const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
+  const long long sets = n_multisets(E, cap), ld = cand_ld(sets);
   const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_prep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_cand_prep<K><<<dim3(ceil_div(ld, 128), ceil_div(E, kPrepOwn)), 128, smem, st>>>(t->solo_ms, t->thr, E, cap, sets,
@@ -1033,7 +1052,7 @@ static int launch_prep(const intf_table* t, int cap, double alpha, float* ws, cu
 static int launch_stream(const intf_table* t, int cap, const double* coefs, int n_dec, float* out, float* ws,
                          cudaStream_t st) {
   const int E = t->n_rows;
-  const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
+  const long long sets = n_multisets(E, cap), ld = cand_ld(sets);
   dim3 grid(ceil_div(ld / 4, kStreamThreads), E, ceil_div(n_dec, kStreamDec));
   k_cand_stream<<<grid, kStreamThreads, 0, st>>>(t->thr, E, ld, sets, coefs, n_dec, ws, ws + 3 * ld, out);
   return launch_status("k_cand_stream");
@@ -1043,7 +1062,7 @@ template <int K>
 static int launch_step(const intf_table* t, int cap, double alpha, const double* coefs, int n_dec, float* out,
                        const float* ws_cur, float* ws_next, cudaStream_t st) {
   const int E = t->n_rows;
-  const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
+  const long long sets = n_multisets(E, cap), ld = cand_ld(sets);
   const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int po = kStepPrepOwn;
@@ -1071,7 +1090,7 @@ template <int K>
 static int launch_candidates(const intf_table* t, int cap, double alpha, const double* coefs, int n_dec, float* out,
                              float* ws, long long ws_elems, cudaStream_t st, int phase = 3) {
   const int E = t->n_rows;
-  const long long sets = n_multisets(E, cap), ld = (sets + kGroup - 1) / kGroup * kGroup;
+  const long long sets = n_multisets(E, cap), ld = cand_ld(sets);
   const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
   if (smem > 200 * 1024) return bad_input("intf_predict_candidates: profile table too large for the binomial table");
   if (ws && ws_elems >= cand_ws_elems(E, ld)) {  // two-phase: prep (features) + stream (forward)
@@ -1092,7 +1111,7 @@ int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t* n_cand, int64_t* 
   const long long sets = n_multisets(n_rows, cap);
   *n_cand = (int64_t)n_rows * sets;
   if (n_sets) *n_sets = sets;
-  if (ld) *ld = (sets + kGroup - 1) / kGroup * kGroup;
+  if (ld) *ld = cand_ld(sets);
   return INTF_OK;
 }
 
@@ -1171,7 +1190,7 @@ int intf_predict_candidates_host(const intf_table* table, int32_t cap, double al
   int rc = intf_candidate_count(table->n_rows, cap, &n_cand, &n_sets, &ld);
   if (rc) return rc;
   intf_candidate_workspace(table->n_rows, cap, &ws);
-  const long long n_out = (long long)ld * table->n_rows * 2 * n_dec, n_coef = 2LL * n_dec * 2 * 7;
+  const long long n_out = cand_out_elems(table->n_rows, ld, n_dec), n_coef = 2LL * n_dec * 2 * 7;
   if (scratch_elems < n_coef + n_out) return bad_input("intf_predict_candidates_host: scratch too small");
   cudaStream_t st = as_stream(stream);
   // scratch: [coefs as doubles][outputs][feature workspace, if it fits]

@@ -413,8 +413,12 @@ def candidate_count(n_rows: int, cap: int) -> int:
 class CandidateScorer:
     """Every candidate co-location set over a profile table,
     scored by a coarse (static) and a fine (EWMA) linear predictor for n_dec
-    decisions.  Output (device, fp32): [n_dec][2][E][ld], first n_sets of
-    each row valid (ld = n_sets rounded up to 4)."""
+    decisions.  Output (device, fp32) in the tiled HBM layout of the kernels
+    (csrc/predict.cu): tiles [ceil(n_dec/4)][E][ld/512] of [4 dec][2 kinds]
+    [512 multisets]; `view` returns the logical [n_dec][2][E][n_sets] array
+    (ld = n_sets rounded up to 512, pad lanes written as 0)."""
+
+    TILE_R, TILE_D = 512, 4
 
     def __init__(self, table: _pack.TableArrays, cap: int, alpha: float = 0.5, dtable: DeviceTable | None = None,
                  two_phase: bool = True):
@@ -430,14 +434,22 @@ class CandidateScorer:
         self.ws = torch.empty(max(self.ws_elems, 1), dtype=torch.float32, device=self.dev) if two_phase else None
 
     def out_elems(self, n_dec: int) -> int:
-        return n_dec * 2 * self.E * self.ld
+        return -(-n_dec // self.TILE_D) * self.TILE_D * 2 * self.E * self.ld
 
     def alloc(self, n_dec: int) -> torch.Tensor:
         return torch.empty(self.out_elems(n_dec), dtype=torch.float32, device=self.dev)
 
     def view(self, out, n_dec: int):
         """[n_dec, 2, E, n_sets] view of an output buffer (torch or numpy)."""
-        return out.reshape(n_dec, 2, self.E, self.ld)[..., : self.n_sets]
+        return self.view_full(out, n_dec)[..., : self.n_sets]
+
+    def view_full(self, out, n_dec: int):
+        """[n_dec, 2, E, ld] logical array (incl. pad lanes) of an output
+        buffer in the tiled layout (a copy; numpy or torch)."""
+        dc, rc, T = -(-n_dec // self.TILE_D), self.ld // self.TILE_R, self.TILE_R
+        t = out.reshape(dc, self.E, rc, self.TILE_D, 2, T)
+        t = t.permute(0, 3, 4, 1, 2, 5) if hasattr(t, "permute") else t.transpose(0, 3, 4, 1, 2, 5)
+        return t.reshape(dc * self.TILE_D, 2, self.E, rc * T)[:n_dec]
 
     def score(self, coefs: torch.Tensor, out: torch.Tensor) -> None:
         """coefs: device float64 [n_dec][2][7]; enqueue only (no sync)."""

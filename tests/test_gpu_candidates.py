@@ -51,7 +51,7 @@ def test_cap4_full_enumeration_sampled_against_oracle(two_phase):
     coefs = torch.tensor(W, dtype=torch.float64, device="cuda").contiguous()
     out = sc.alloc(3)
     sc.score(coefs, out)
-    full = out.cpu().numpy().reshape(3, 2, sc.E, sc.ld)
+    full = sc.view_full(out.cpu().numpy(), 3)
     assert np.all(full[..., sc.n_sets:] == 0)  # pad entries
     y = sc.view(out.cpu().numpy(), 3)
     assert np.isfinite(y).all()
@@ -68,6 +68,19 @@ def test_cap4_full_enumeration_sampled_against_oracle(two_phase):
         np.testing.assert_allclose([y[d, 0, o, r], y[d, 1, o, r]], [yc, yf], rtol=RTOL, atol=1e-6)
 
 
+def test_tiled_layout_roundtrip():
+    """view_full inverts the tiled HBM layout: element (dec, kind, own, r) of the
+    logical array is buffer[tile_off(dec, kind, own, r)] (csrc/predict.cu)."""
+    sc = _scorer(3)  # n_sets 1,225 -> ld 1,536: three tile columns
+    n_dec = 6
+    buf = np.arange(sc.out_elems(n_dec), dtype=np.float64)
+    v = sc.view_full(buf, n_dec)
+    RC, T = sc.ld // 512, 512
+    for d, k, o, r in [(0, 0, 0, 0), (5, 1, sc.E - 1, sc.ld - 1), (3, 1, 7, 600), (4, 0, 2, 1023)]:
+        off = ((((d // 4) * sc.E + o) * RC + r // T) * 8 + (d % 4) * 2 + k) * T + r % T
+        assert v[d, k, o, r] == buf[off]
+
+
 def test_host_buffer_variant_equals_device_variant():
     sc = _scorer(3)
     C = _golden.load("candidates_golden.npz")
@@ -78,7 +91,8 @@ def test_host_buffer_variant_equals_device_variant():
     scratch = torch.empty(sc.scratch_elems(2), dtype=torch.float32, device="cuda")
     sc.score_host(np.ascontiguousarray(W), host_out, scratch)
     torch.cuda.synchronize()
-    np.testing.assert_array_equal(host_out, dev_out.cpu().numpy())
+    # rows of the padded decisions (the tile holds 4) are never written: compare the logical arrays
+    np.testing.assert_array_equal(sc.view_full(host_out, 2), sc.view_full(dev_out.cpu().numpy(), 2))
 
 
 @pytest.mark.parametrize("fused", [True, False])
@@ -97,4 +111,4 @@ def test_pipelined_steps_equal_one_shot(fused):
     for W, out in zip(Ws, outs):
         ref = sc.alloc(len(W))
         sc.score(torch.tensor(W, device="cuda").contiguous(), ref)
-        np.testing.assert_array_equal(out.cpu().numpy(), ref.cpu().numpy())
+        np.testing.assert_array_equal(sc.view_full(out.cpu().numpy(), len(W)), sc.view_full(ref.cpu().numpy(), len(W)))

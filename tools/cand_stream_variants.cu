@@ -17,6 +17,7 @@
 //   contiguous block chunk (128x8, 256x4, 128x2); v21-v23: the stream kernel's
 //   store pattern only (split 8 / 4 / 16); v24-v26: one kind per thread (split 8 / 4 / 16)
 //   v27-v31: lockstep form (k_stream_lock) T x J = 128x2, 256x2, 128x4, 64x2, 128x1
+//   v32-v35: tiled output layout (block tile contiguous), decisions split 8 / 4 / 16 / 2
 // Build/run on the box:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/csv2 tools/cand_stream_variants.cu && /tmp/csv2
 #include <cstdio>
@@ -193,6 +194,45 @@ __global__ void __launch_bounds__(T) k_stream_lock(const float* __restrict__ C0,
   }
 }
 
+// tiled output layout: block (x = r chunk, y = own, z = decision chunk) owns ONE
+// contiguous tile [ND decisions][2 kinds][T*4 floats]; tiles ordered
+// [dchunk][own][rchunk], so concurrently running blocks write adjacent tiles
+template <int T, int DSPLIT>
+__global__ void __launch_bounds__(T) k_stream_tiled(const float* __restrict__ C0, const float* __restrict__ FE,
+                                                    const float4* __restrict__ coef, float* __restrict__ out) {
+  constexpr int ND = NDEC / DSPLIT;
+  __shared__ float4 cw[ND][2];
+  const int o = blockIdx.y;
+  const int d0 = blockIdx.z * ND;
+  const long long r0 = ((long long)blockIdx.x * T + threadIdx.x) * 4;
+  const bool inb = r0 < LD;
+  const long long rr = inb ? r0 : 0;
+  const float4 cx = __ldg((const float4*)(C0 + rr)), cy = __ldg((const float4*)(C0 + LD + rr)),
+               cz = __ldg((const float4*)(C0 + 2 * LD + rr));
+  const float4 fx = __ldg((const float4*)(FE + (o * 3 + 0) * LD + rr)),
+               fy = __ldg((const float4*)(FE + (o * 3 + 1) * LD + rr)),
+               fz = __ldg((const float4*)(FE + (o * 3 + 2) * LD + rr));
+  for (int t = threadIdx.x; t < 2 * ND; t += T) cw[t >> 1][t & 1] = coef[((d0 + (t >> 1)) * 2 + (t & 1)) * E + o];
+  __syncthreads();
+  const long long tile = ((long long)blockIdx.z * E + o) * gridDim.x + blockIdx.x;
+  float4* base = (float4*)out + tile * (ND * 2 * T) + threadIdx.x;
+#pragma unroll 4
+  for (int d = 0; d < ND; d++) {
+    const float4 a = cw[d][0], b = cw[d][1];
+    float4 yc, yf;
+    yc.x = fmaf(a.z, cz.x, fmaf(a.y, cy.x, fmaf(a.x, cx.x, a.w)));
+    yc.y = fmaf(a.z, cz.y, fmaf(a.y, cy.y, fmaf(a.x, cx.y, a.w)));
+    yc.z = fmaf(a.z, cz.z, fmaf(a.y, cy.z, fmaf(a.x, cx.z, a.w)));
+    yc.w = fmaf(a.z, cz.w, fmaf(a.y, cy.w, fmaf(a.x, cx.w, a.w)));
+    yf.x = fmaf(b.z, fz.x, fmaf(b.y, fy.x, fmaf(b.x, fx.x, b.w)));
+    yf.y = fmaf(b.z, fz.y, fmaf(b.y, fy.y, fmaf(b.x, fx.y, b.w)));
+    yf.z = fmaf(b.z, fz.z, fmaf(b.y, fy.z, fmaf(b.x, fx.z, b.w)));
+    yf.w = fmaf(b.z, fz.w, fmaf(b.y, fy.w, fmaf(b.x, fx.w, b.w)));
+    __stcs(base + (d * 2 + 0) * T, yc);
+    __stcs(base + (d * 2 + 1) * T, yf);
+  }
+}
+
 __global__ void k_fill_gs(float4* p, long long n4) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
     p[i] = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -247,9 +287,13 @@ int main() {
       case 29: k_stream_lock<128, 4><<<(unsigned)((n4 / NDEC / 2 + 511) / 512), 128>>>(C0, FE, coef, o); break;
       case 30: k_stream_lock<64, 2><<<(unsigned)((n4 / NDEC / 2 + 127) / 128), 64>>>(C0, FE, coef, o); break;
       case 31: k_stream_lock<128, 1><<<(unsigned)((n4 / NDEC / 2 + 127) / 128), 128>>>(C0, FE, coef, o); break;
+      case 32: k_stream_tiled<128, 8><<<dim3((LD / 4 + 127) / 128, E, 8), 128>>>(C0, FE, coef, o); break;
+      case 33: k_stream_tiled<128, 4><<<dim3((LD / 4 + 127) / 128, E, 4), 128>>>(C0, FE, coef, o); break;
+      case 34: k_stream_tiled<128, 16><<<dim3((LD / 4 + 127) / 128, E, 16), 128>>>(C0, FE, coef, o); break;
+      case 35: k_stream_tiled<128, 2><<<dim3((LD / 4 + 127) / 128, E, 2), 128>>>(C0, FE, coef, o); break;
     }
   };
-  for (int v = 0; v < 32; v++) {
+  for (int v = 0; v < 36; v++) {
     for (int it = 0; it < 4; it++) launch(v, out[it & 1]);
     const int reps = 30;
     for (int it = 0; it < reps; it++) {
