@@ -18,6 +18,7 @@
 //   store pattern only (split 8 / 4 / 16); v24-v26: one kind per thread (split 8 / 4 / 16)
 //   v27-v31: lockstep form (k_stream_lock) T x J = 128x2, 256x2, 128x4, 64x2, 128x1
 //   v32-v35: tiled output layout (block tile contiguous), decisions split 8 / 4 / 16 / 2
+//            (v32: 6.2 TB/s vs v3's 5.9 -> the product layout, csrc/predict.cu)
 // Build/run on the box:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/csv2 tools/cand_stream_variants.cu && /tmp/csv2
 #include <cstdio>
