@@ -520,12 +520,38 @@ def product_arm(a):
     barrier()
     st = pipe.status()
     r_steps = max(1, min(a.steps, 5))
+    # per-scenario SLO metrics of every rank gathered (NCCL all_gather, N > 1):
+    # per deployed model n, met, p50/p95/p99, padded to the largest rank
+    n_mod = pipe.pb.n_models
+    gather_len = n_mod
+    if dist is not None:
+        t = torch.tensor([n_mod], device="cuda" if a.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gather_len = int(t.item())
+    rows = torch.zeros(gather_len, 5, dtype=torch.float64, device="cuda")
+    parts = [torch.empty_like(rows) for _ in range(world)] if dist is not None else None
+
+    def gather_metrics():
+        if dist is None:
+            return
+        rows[:n_mod, 0] = pipe.slo_n[:n_mod]
+        rows[:n_mod, 1] = pipe.slo_met[:n_mod]
+        rows[:n_mod, 2:] = pipe.slo_p[: 3 * n_mod].view(n_mod, 3)
+        if a.backend == "nccl":
+            dist.all_gather(parts, rows)
+        else:
+            cpu_parts = [p.cpu() for p in parts]
+            dist.all_gather(cpu_parts, rows.cpu())
+
+    gather_metrics()
+    barrier()
     # one warp replays each scenario start to end (C5 scenarios are short:
     # busy-period sharding pays only for long traces, see long_trace)
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     r0.record(stream)
     for _ in range(r_steps):
         pipe.run()
+        gather_metrics()
     r1.record(stream)
     barrier()
     rep_ms = max_over_ranks(r0.elapsed_time(r1)) / r_steps
@@ -599,7 +625,8 @@ def product_arm(a):
                    "unit": "replays/s", "ms_per_step": rep_ms, "scenarios_per_gpu": REPLAY_SCEN,
                    "requests": n_req, "batches": n_batches, "status_nonzero": int(np.count_nonzero(st)),
                    "workload": "C5-shape synthetic scenarios (default_rng([2512,i]), 1 s, cap 1-3): arrivals + "
-                               "formation + noise + replay (warp per scenario) + SLO + features/3 predictors",
+                               "formation + noise + replay (warp per scenario) + SLO + features/3 predictors; N > 1: "
+                               "+ all_gather of every rank's per-model SLO metrics each step",
                    "stage_ms": stage_ms, "cpu_baseline": replay_cpu},
         "refit": refit,
         "long_trace": longtrace,
