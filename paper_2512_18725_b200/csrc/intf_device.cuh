@@ -247,10 +247,9 @@ INTF_FN Pcg64 pcg_seed_words(const uint32_t* w, int n) {
   uint64_t s0 = (uint64_t)out[0] | ((uint64_t)out[1] << 32), s1 = (uint64_t)out[2] | ((uint64_t)out[3] << 32);
   uint64_t s2 = (uint64_t)out[4] | ((uint64_t)out[5] << 32), s3 = (uint64_t)out[6] | ((uint64_t)out[7] << 32);
   Pcg64 g;
-  g.state = 0;
   g.inc = ((((unsigned __int128)s2 << 64) | s3) << 1) | 1u;
-  pcg_step(g);
-  g.state += ((unsigned __int128)s0 << 64) | s1;
+  // numpy's pcg64_srandom: state = 0; step (0 * mult + inc = inc); state += initstate; step
+  g.state = g.inc + (((unsigned __int128)s0 << 64) | s1);
   pcg_step(g);
   return g;
 }
