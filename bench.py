@@ -252,14 +252,13 @@ def refit_secondary(a, stream, barrier, max_over_ranks, rank) -> dict:
     gbs = 56.0 * OLS_ROWS / (ms / 1e3) / 1e9
     out["ols_stats"] = {"samples_per_s": OLS_ROWS / (ms / 1e3), "ms": ms, "achieved_gbs": gbs, "frac": gbs / peak,
                         "bytes_per_sample": 56}
-    # refit each window (configs[2]): fit_ols_xy on every REFIT_WINDOW-sample window, one stats + one solve launch
+    # refit each window (configs[2]): fit_ols_xy on every REFIT_WINDOW-sample window, one launch (k_ols_windows_tma)
     n_win = (OLS_ROWS + REFIT_WINDOW - 1) // REFIT_WINDOW
-    wstats = torch.empty(n_win * 56, dtype=torch.float64, device="cuda")
     wparams = torch.empty(n_win * 7, dtype=torch.float64, device="cuda")
     winfo = torch.empty(n_win * 3, dtype=torch.int32, device="cuda")
 
     def windows():
-        _abi.check(L.intf_ols_windows(Xo.data_ptr(), yo.data_ptr(), OLS_ROWS, REFIT_WINDOW, wstats.data_ptr(),
+        _abi.check(L.intf_ols_windows(Xo.data_ptr(), yo.data_ptr(), OLS_ROWS, REFIT_WINDOW, None,
                                       wparams.data_ptr(), winfo.data_ptr(), s), "ols_windows")
 
     for _ in range(3):

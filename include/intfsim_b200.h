@@ -278,9 +278,12 @@ int intf_ols_solve(const double *stats, double *out_params, int32_t *out_info, d
 
 /* Windowed refit ("refit each window", BASELINE configs[2]): fit_ols_xy
  * (`predict.py:53-72`) on every window of `window` consecutive rows of X
- * (n x 6, row-major) / y: n_win = ceil(n / window) fits.  stats: caller
- * scratch of n_win*56 doubles (Z^T Z | Z^T y per window; may be NULL for
- * windows of <= 128 rows, which are reduced and solved in one launch);
+ * (n x 6, row-major) / y: n_win = ceil(n / window) fits.  stats: NULL, or
+ * n_win*56 doubles that receive Z^T Z | Z^T y of every window; it is
+ * required (as scratch) only for windows of > 128 rows that are not a
+ * multiple of 8 (two launches).  Windows of a multiple of 8 rows with
+ * 16-byte-aligned X and y are reduced and solved in one tensor-map-staged
+ * launch, other windows of <= 128 rows in one thread-per-window launch;
  * params: n_win*7
  * (w0..w5, b); info: n_win*3 int32 = ridge fallback used, non-finite result
  * (PredictError), fewer than 7 rows (fit_ols raises PredictError for those;

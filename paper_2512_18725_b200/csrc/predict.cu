@@ -10,6 +10,9 @@
 
 #include "capi_common.h"
 #include "replay_core.cuh"
+#include "tma.cuh"
+
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
 using namespace intf;
 
@@ -629,49 +632,155 @@ __device__ bool chol_solve(const double* A, const double* b, double* x, double* 
   return true;
 }
 
+// inverse of a lower-triangular 7x7 factor (Li = L^-1, lower triangular)
+__device__ __forceinline__ void tri_inv7(const double L[7][7], double Li[7][7]) {
+  double d[7];
+#pragma unroll
+  for (int i = 0; i < 7; i++) d[i] = 1.0 / L[i][i];
+#pragma unroll
+  for (int j = 0; j < 7; j++) {
+    Li[j][j] = d[j];
+#pragma unroll
+    for (int i = j + 1; i < 7; i++) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = j; k < i; k++) s = fma(L[i][k], Li[k][j], s);
+      Li[i][j] = -s * d[i];
+    }
+  }
+}
+
+// numpy.linalg.matrix_rank(Z) from the rows themselves (Z = [X[lo:lo+cnt], 1]):
+// R = QR(Z) by Givens row updates, then the singular values of R by one-sided
+// Jacobi (relative accuracy ~eps S_max, like the SVD of Z), tol = S_max *
+// max(cnt, 7) * eps.  The eigenvalues of Z^T Z cannot separate a singular
+// value below ~sqrt(eps) S_max (exactly collinear rows, e.g. duplicated
+// samples in a short window) from rounding; this can.  Cold path: only for
+// windows whose Z^T Z fails the condition screen.
+__device__ __noinline__ int matrix_rank_rows(const double* __restrict__ X, long long lo, long long cnt) {
+  double R[7][7];
+  for (int i = 0; i < 7; i++)
+    for (int j = 0; j < 7; j++) R[i][j] = 0.0;
+  for (long long k = 0; k < cnt; k++) {
+    double v[7];
+    for (int j = 0; j < 6; j++) v[j] = X[(lo + k) * 6 + j];
+    v[6] = 1.0;
+    for (int i = 0; i < 7; i++) {
+      if (v[i] == 0.0) continue;
+      const double h = hypot(R[i][i], v[i]), c = R[i][i] / h, sn = v[i] / h;
+      for (int j = i; j < 7; j++) {
+        const double a = R[i][j], b = v[j];
+        R[i][j] = c * a + sn * b;
+        v[j] = c * b - sn * a;
+      }
+    }
+  }
+  // one-sided Jacobi on the columns of R
+  for (int sweep = 0; sweep < 40; sweep++) {
+    bool rotated = false;
+    for (int p = 0; p < 6; p++)
+      for (int q = p + 1; q < 7; q++) {
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = 0; i < 7; i++) {
+          al += R[i][p] * R[i][p];
+          be += R[i][q] * R[i][q];
+          ga += R[i][p] * R[i][q];
+        }
+        if (ga == 0.0 || fabs(ga) <= 2.220446049250313e-16 * sqrt(al * be)) continue;
+        rotated = true;
+        const double ze = (be - al) / (2.0 * ga);
+        const double t = (ze >= 0.0 ? 1.0 : -1.0) / (fabs(ze) + sqrt(1.0 + ze * ze));
+        const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+        for (int i = 0; i < 7; i++) {
+          const double a = R[i][p], b = R[i][q];
+          R[i][p] = c * a - sn * b;
+          R[i][q] = sn * a + c * b;
+        }
+      }
+    if (!rotated) break;
+  }
+  double sv[7], smax = 0.0;
+  for (int j = 0; j < 7; j++) {
+    double t = 0.0;
+    for (int i = 0; i < 7; i++) t += R[i][j] * R[i][j];
+    sv[j] = sqrt(t);
+    smax = fmax(smax, sv[j]);
+  }
+  const double tol = smax * fmax((double)cnt, 7.0) * 2.220446049250313e-16;
+  int rank = 0;
+  for (int j = 0; j < 7; j++) rank += sv[j] > tol;
+  return rank;
+}
+
 // fit_ols_xy (`predict.py:53-66`): matrix_rank(Z) < 7 -> ridge solve, else
 // least squares (normal equations; lstsq and Cholesky agree to ~cond*eps).
 // rank test: S_i = sqrt(eig(Z^T Z)); rank = #(S_i > S_max * max(n, 7) * eps).
+// rows: when given (X + [lo, lo+cnt)), the rank of a window that fails the
+// screen comes from the rows (matrix_rank_rows), else from eig(Z^T Z).
 __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, double* params, int32_t* info,
-                                              double* Pinv) {
+                                              double* Pinv, const double* __restrict__ rows = nullptr,
+                                              long long lo = 0, long long cnt = 0) {
   double G[49], r[7], ev[7];
   for (int i = 0; i < 49; i++) G[i] = stats[i];
   for (int i = 0; i < 7; i++) r[i] = stats[49 + i];
   const double n = G[48];
-  // rank test.  Screen first: with G = LL^T and Ginv from L, ev_min >=
-  // 1/||Ginv||_F and ev_max <= ||G||_F, so ||G||_F ||Ginv||_F < 1e10 proves
-  // ev_min > 1e-10 ev_max, far above both the SVD tolerance (max(n,7) eps)^2
-  // ev_max and the eigenvalue error (~1e-15 ev_max) -- the eigenvalue test
-  // below would find rank 7.  Only windows that fail the screen pay for it.
-  bool full = false;
+  // rank test, screened first: with G = L L^T and Li = L^-1, ev_max <= trace(G)
+  // and 1/ev_min = ||G^-1||_2 <= trace(G^-1) = ||Li||_F^2, so
+  // trace(G) ||Li||_F^2 < 1e10 proves ev_min > 1e-10 ev_max, far above both
+  // the SVD tolerance (max(n,7) eps)^2 ev_max and the eigenvalue error
+  // (~1e-15 ev_max): the eigenvalue test below would find rank 7.  Screened
+  // windows solve x = Li^T (Li r) from the same factor; only windows that
+  // fail the screen pay for the eigenvalues.
   {
     double L[7][7];
     if (chol7(G, L)) {
-      double gf = 0.0, hf = 0.0;
+      double Li[7][7];
+      tri_inv7(L, Li);
+      double tr = 0.0, ti = 0.0;
 #pragma unroll
-      for (int i = 0; i < 49; i++) gf += G[i] * G[i];
+      for (int i = 0; i < 7; i++) tr += G[i * 8];
 #pragma unroll
-      for (int c = 0; c < 7; c++) {
-        double e[7], col[7];
+      for (int i = 0; i < 7; i++)
 #pragma unroll
-        for (int i = 0; i < 7; i++) e[i] = (i == c) ? 1.0 : 0.0;
-        chol7_solve(L, e, col);
+        for (int j = 0; j <= i; j++) ti = fma(Li[i][j], Li[i][j], ti);
+      if (isfinite(ti) && tr * ti < 1e10) {
+        double t[7];
 #pragma unroll
-        for (int i = 0; i < 7; i++) hf += col[i] * col[i];
+        for (int i = 0; i < 7; i++) {
+          double v = 0.0;
+#pragma unroll
+          for (int k = 0; k <= i; k++) v = fma(Li[i][k], r[k], v);
+          t[i] = v;
+        }
+        int fin = 1;
+#pragma unroll
+        for (int i = 0; i < 7; i++) {
+          double v = 0.0;
+#pragma unroll
+          for (int k = i; k < 7; k++) v = fma(Li[k][i], t[k], v);
+          params[i] = v;
+          fin &= isfinite(v);
+        }
+        if (info) {
+          info[0] = 0;
+          info[1] = fin ? 0 : 1;
+        }
+        if (Pinv) chol_solve(G, nullptr, nullptr, Pinv);  // rls_init P0 = inv(Z^T Z) (`predict.py:126-131`)
+        return;
       }
-      full = isfinite(hf) && sqrt(gf) * sqrt(hf) < 1e10;
     }
   }
-  bool ridge = false;
-  if (!full) {
+  int rank = 0;
+  if (rows) {
+    rank = matrix_rank_rows(rows, lo, cnt);
+  } else {
     jacobi_eigs(G, ev);
     double smax = 0.0;
     for (int i = 0; i < 7; i++) smax = fmax(smax, sqrt(fmax(ev[i], 0.0)));
     const double tol = smax * fmax(n, 7.0) * 2.220446049250313e-16;
-    int rank = 0;
     for (int i = 0; i < 7; i++) rank += sqrt(fmax(ev[i], 0.0)) > tol;
-    ridge = rank < 7;
   }
+  const bool ridge = rank < 7;
   double A[49];
   for (int i = 0; i < 49; i++) A[i] = G[i];
   if (ridge)
@@ -755,9 +864,44 @@ __global__ void __launch_bounds__(32 * kWinWarps) k_ols_window_stats(const doubl
   }
 }
 
-// small windows (<= kFusedWindow rows): one thread per window accumulates its
-// statistics sequentially in registers (no cross-lane reduction) and solves
-// in place; the statistics reach HBM only if the caller asked for them.
+// one row's contribution to the 35 statistics (z = [x, 1])
+__device__ __forceinline__ void ols_acc_row(double* acc, const double* x6, double yy) {
+  const double z[7] = {x6[0], x6[1], x6[2], x6[3], x6[4], x6[5], 1.0};
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = i; j < 7; j++) acc[t] = fma(z[i], z[j], acc[t]), t++;
+#pragma unroll
+  for (int i = 0; i < 7; i++) acc[28 + i] = fma(z[i], yy, acc[28 + i]);
+}
+
+// the window's statistics (optionally to HBM), its solve and its info row
+__device__ __forceinline__ void ols_window_finish(const double* acc, const double* __restrict__ X, long long w,
+                                                  long long lo, long long cnt, double* stats, double* params,
+                                                  int32_t* info) {
+  double st[56];
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = i; j < 7; j++, t++) st[i * 7 + j] = st[j * 7 + i] = acc[t];
+#pragma unroll
+  for (int i = 0; i < 7; i++) st[49 + i] = acc[28 + i];
+  if (stats) {
+#pragma unroll
+    for (int i = 0; i < 56; i++) stats[w * 56 + i] = st[i];
+  }
+  int32_t inf2[2] = {0, 0};
+  ols_solve_one(st, params + w * 7, inf2, nullptr, X, lo, cnt);
+  info[3 * w] = inf2[0];
+  info[3 * w + 1] = inf2[1];
+  info[3 * w + 2] = cnt < 7 ? 1 : 0;
+}
+
+// other windows of <= kFusedWindow rows: one thread per window accumulates
+// its statistics sequentially in registers (no cross-lane reduction) and
+// solves in place; the statistics reach HBM only if the caller asked for them.
 constexpr int kFusedWindow = 128;
 __global__ void __launch_bounds__(128) k_ols_windows_fused(const double* __restrict__ X, const double* __restrict__ y,
                                                            long long n, int window, long long n_win,
@@ -773,44 +917,114 @@ __global__ void __launch_bounds__(128) k_ols_windows_fused(const double* __restr
   for (long long row = lo; row < hi; row++) {
     const double2* xr = reinterpret_cast<const double2*>(X + row * 6);
     const double2 a = __ldg(xr), b = __ldg(xr + 1), c = __ldg(xr + 2);
-    const double z[7] = {a.x, a.y, b.x, b.y, c.x, c.y, 1.0};
-    const double yy = __ldg(y + row);
-    int t = 0;
-#pragma unroll
-    for (int i = 0; i < 7; i++)
-#pragma unroll
-      for (int j = i; j < 7; j++) acc[t] = fma(z[i], z[j], acc[t]), t++;
-#pragma unroll
-    for (int i = 0; i < 7; i++) acc[28 + i] = fma(z[i], yy, acc[28 + i]);
+    const double x6[6] = {a.x, a.y, b.x, b.y, c.x, c.y};
+    ols_acc_row(acc, x6, __ldg(y + row));
   }
-  double st[56];
-  int t = 0;
+  ols_window_finish(acc, X, w, lo, hi - lo, stats, params, info);
+}
+
+// windows of a multiple of 8 rows: one warp per block, persistent over groups
+// of 32 consecutive windows (lane = window).  A chunk is rows [8c, 8c+8) of
+// the group's 32 windows, fetched by TWO tensor-map boxes -- X as
+// {16 doubles, 3 groups of 16, 32 windows} (128-byte swizzle) and y as
+// {8 rows, 32 windows} (64-byte swizzle) -- into one of kWinTmaStages
+// shared-memory stages; the chunk stream runs on across groups, so the next
+// group's boxes are in flight while the lanes solve.  Each lane reads its
+// 384-byte X slab through the swizzle (conflict-free 16-byte loads).  Windows
+// past the last full one (the trailing partial window) read global memory.
+// (Per-lane 1-D bulk copies -- 64 small copies per chunk -- ran at 0.77 of
+// this rate, thread-per-window global loads at 0.40: tools/refit_variants.cu.)
+constexpr int kWinTmaRows = 8;
+constexpr int kWinTmaStages = 3;
+constexpr int kWinTmaPerSm = 4;  // 1-warp blocks resident per SM (43 KB shared memory each)
+constexpr int kWinTmaXBytes = 32 * kWinTmaRows * 48, kWinTmaYBytes = 32 * kWinTmaRows * 8;
+constexpr int kWinTmaSmem = kWinTmaStages * (kWinTmaXBytes + kWinTmaYBytes) + 1024 + 64;
+
+__global__ void __launch_bounds__(32) k_ols_windows_tma(const __grid_constant__ CUtensorMap mx,
+                                                        const __grid_constant__ CUtensorMap my,
+                                                        const double* __restrict__ X, const double* __restrict__ y,
+                                                        long long n, int window, long long n_win,
+                                                        double* __restrict__ stats, double* __restrict__ params,
+                                                        int32_t* __restrict__ info) {
+  constexpr int R = kWinTmaRows, S = kWinTmaStages, XB = kWinTmaXBytes, YB = kWinTmaYBytes;
+  extern __shared__ unsigned char win_dsm[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(win_dsm) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S * (XB + YB));
+  const int lane = threadIdx.x;
+  const long long n_full = n / window;  // windows whose rows the boxes cover
+  const long long n_grp = (n_win + 31) / 32;
+  const int nch = window / R;
+  const long long g0 = blockIdx.x, gs = gridDim.x;
+  const long long my_grps = g0 < n_grp ? (n_grp - 1 - g0) / gs + 1 : 0;
+  if (lane == 0)
+    for (int s = 0; s < S; s++) mbar_init(&bar[s]);
+  __syncwarp();
+  long long i_grp = g0;  // issue cursor: group, chunk, stage
+  int i_c = 0, i_st = 0;
+  long long i_left = my_grps * nch;
+  auto issue = [&]() {
+    if (lane == 0) {
+      unsigned char* dst = sm + i_st * (XB + YB);
+      mbar_arrive_expect(&bar[i_st], (unsigned)(XB + YB));  // out-of-range boxes are zero-filled: always full bytes
+      tma_load_3d(dst, &mx, 0, i_c * 3, (int)(i_grp * 32), &bar[i_st]);
+      tma_load_2d(dst + XB, &my, i_c * R, (int)(i_grp * 32), &bar[i_st]);
+    }
+    if (++i_c == nch) i_c = 0, i_grp += gs;
+    if (++i_st == S) i_st = 0;
+    i_left--;
+  };
+  for (int s = 0; s < S - 1 && i_left > 0; s++) issue();
+  double acc[kStats];
+  int st = 0;
+  unsigned ph = 0;
+  for (long long gi = 0; gi < my_grps; gi++) {
+    const long long w = (g0 + gi * gs) * 32 + lane;
+    const long long lo = w * window;
+    const long long cnt = w < n_win ? (lo + window < n ? window : n - lo) : 0;
+    const bool staged = w < n_full;
 #pragma unroll
-  for (int i = 0; i < 7; i++)
+    for (int i = 0; i < kStats; i++) acc[i] = 0.0;
+    for (int c = 0; c < nch; c++) {
+      if (i_left > 0) issue();
+      mbar_wait(&bar[st], ph);
+      if (staged) {
+        const unsigned char* xs = sm + st * (XB + YB);
+        const unsigned char* ys = xs + XB;
 #pragma unroll
-    for (int j = i; j < 7; j++, t++) st[i * 7 + j] = st[j * 7 + i] = acc[t];
+        for (int r = 0; r < R; r += 2) {
+          double z[12];
 #pragma unroll
-  for (int i = 0; i < 7; i++) st[49 + i] = acc[28 + i];
-  if (stats) {
-#pragma unroll
-    for (int i = 0; i < 56; i++) stats[w * 56 + i] = st[i];
+          for (int jj = 0; jj < 6; jj++) {
+            const int u = 3 * r + jj;             // 16-byte unit of this lane's 384-byte slab
+            const int rho = lane * 3 + (u >> 3);  // 128-byte row of the box; swizzle: unit ^= row % 8
+            const double2 v = *reinterpret_cast<const double2*>(xs + rho * 128 + (((u & 7) ^ (rho & 7)) << 4));
+            z[2 * jj] = v.x;
+            z[2 * jj + 1] = v.y;
+          }
+          // 64-byte rows: 16-byte unit ^= (row / 2) % 4
+          const double2 yy = *reinterpret_cast<const double2*>(ys + lane * 64 + (((r >> 1) ^ ((lane >> 1) & 3)) << 4));
+          ols_acc_row(acc, z, yy.x);
+          ols_acc_row(acc, z + 6, yy.y);
+        }
+      } else {
+        for (int r = c * R; r < c * R + R && r < cnt; r++) ols_acc_row(acc, X + (lo + r) * 6, y[lo + r]);
+      }
+      __syncwarp();  // every lane is done with the stage before it is refilled
+      if (++st == S) st = 0, ph ^= 1u;
+    }
+    if (w < n_win) ols_window_finish(acc, X, w, lo, cnt, stats, params, info);
   }
-  int32_t inf2[2] = {0, 0};
-  ols_solve_one(st, params + w * 7, inf2, nullptr);
-  info[3 * w] = inf2[0];
-  info[3 * w + 1] = inf2[1];
-  info[3 * w + 2] = hi - lo < 7 ? 1 : 0;
 }
 
 // info[3w..]: ridge used, non-finite params, fewer than 7 rows (fit_ols raises
 // PredictError for those; fit_ols_xy solves them through the ridge fallback)
-__global__ void k_ols_window_solve(const double* __restrict__ stats, long long n_win, long long n, int window,
-                                   double* __restrict__ params, int32_t* __restrict__ info) {
+__global__ void k_ols_window_solve(const double* __restrict__ stats, const double* __restrict__ X, long long n_win,
+                                   long long n, int window, double* __restrict__ params, int32_t* __restrict__ info) {
   const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= n_win) return;
   const long long cnt = (w + 1) * window <= n ? window : n - w * window;
   int32_t inf2[2] = {0, 0};
-  ols_solve_one(stats + w * 56, params + w * 7, inf2, nullptr);
+  ols_solve_one(stats + w * 56, params + w * 7, inf2, nullptr, X, w * window, cnt);
   info[3 * w] = inf2[0];
   info[3 * w + 1] = inf2[1];
   info[3 * w + 2] = cnt < 7 ? 1 : 0;
@@ -1104,6 +1318,40 @@ static int launch_candidates(const intf_table* t, int cap, double alpha, const d
   return launch_status("k_candidates");
 }
 
+// tensor maps of the windowed refit's inputs over the n_full full windows:
+// X as {16 doubles, window*6/16 groups, n_full windows} (128-byte swizzle),
+// y as {window rows, n_full windows} (64-byte swizzle).  The encoder is the
+// driver's, reached through the runtime (no libcuda link).
+static int ols_window_maps(const double* X, const double* y, int window, long long n_full, CUtensorMap* mx, CUtensorMap* my) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      set_last_error("intf_ols_windows: cuTensorMapEncodeTiled unavailable");
+      return INTF_E_CUDA;
+    }
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dx[3] = {16, (cuuint64_t)(window * 6 / 16), (cuuint64_t)n_full};
+  const cuuint64_t sx[2] = {128, (cuuint64_t)window * 48};
+  const cuuint32_t bx[3] = {16, 3, 32}, ex[3] = {1, 1, 1};
+  const cuuint64_t dy[2] = {(cuuint64_t)window, (cuuint64_t)n_full};
+  const cuuint64_t sy[1] = {(cuuint64_t)window * 8};
+  const cuuint32_t by[2] = {kWinTmaRows, 32}, ey[2] = {1, 1};
+  const CUresult r1 = enc(mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dx, sx, bx, ex,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r2 = enc(my, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(y), dy, sy, by, ey,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+    set_last_error("intf_ols_windows: tensor map encoding failed (%d, %d)", (int)r1, (int)r2);
+    return INTF_E_CUDA;
+  }
+  return INTF_OK;
+}
+
 extern "C" {
 
 int intf_candidate_count(int32_t n_rows, int32_t cap, int64_t* n_cand, int64_t* n_sets, int64_t* ld) {
@@ -1230,19 +1478,38 @@ int intf_ols_solve(const double* stats, double* out_params, int32_t* out_info, d
 
 int intf_ols_windows(const double* X, const double* y, int64_t n, int32_t window, double* stats, double* params,
                      int32_t* info, void* stream) {
-  if (!X || !y || !params || !info || n < 0 || window < 1 || (!stats && window > kFusedWindow))
-    return bad_input("intf_ols_windows: bad argument (stats scratch needed for windows > 128 rows)");
+  if (!X || !y || !params || !info || n < 0 || window < 1)
+    return bad_input("intf_ols_windows: bad argument");
   const long long n_win = (n + window - 1) / window;
   if (n_win == 0) return INTF_OK;
   cudaStream_t st = as_stream(stream);
+  const long long n_full = n / window;
+  if (window % kWinTmaRows == 0 && n_full >= 1 && n_full < (1ll << 31) && ((uintptr_t)X & 15) == 0 &&
+      ((uintptr_t)y & 15) == 0) {
+    CUtensorMap mx, my;
+    int rc = ols_window_maps(X, y, window, n_full, &mx, &my);
+    if (rc) return rc;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static bool attr_set[64] = {};
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+      cudaFuncSetAttribute(k_ols_windows_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kWinTmaSmem);
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    }
+    const long long n_grp = (n_win + 31) / 32;
+    const unsigned grid = (unsigned)(n_grp < 148 * kWinTmaPerSm ? n_grp : 148 * kWinTmaPerSm);
+    k_ols_windows_tma<<<grid, 32, kWinTmaSmem, st>>>(mx, my, X, y, (long long)n, window, n_win, stats, params, info);
+    return launch_status("k_ols_windows_tma");
+  }
   if (window <= kFusedWindow) {
     k_ols_windows_fused<<<ceil_div(n_win, 128), 128, 0, st>>>(X, y, (long long)n, window, n_win, stats, params, info);
     return launch_status("k_ols_windows_fused");
   }
+  if (!stats) return bad_input("intf_ols_windows: stats scratch needed for windows > 128 rows that are not a multiple of 8");
   k_ols_window_stats<<<ceil_div(n_win, kWinWarps), 32 * kWinWarps, 0, st>>>(X, y, (long long)n, window, n_win, stats);
   int rc = launch_status("k_ols_window_stats");
   if (rc) return rc;
-  k_ols_window_solve<<<ceil_div(n_win, 128), 128, 0, st>>>(stats, n_win, (long long)n, window, params, info);
+  k_ols_window_solve<<<ceil_div(n_win, 128), 128, 0, st>>>(stats, X, n_win, (long long)n, window, params, info);
   return launch_status("k_ols_window_solve");
 }
 

@@ -11,6 +11,7 @@
 #include "capi_common.h"
 #include "replay_core.cuh"
 #include "replay_warp.cuh"
+#include "tma.cuh"
 
 using namespace intf;
 
@@ -68,30 +69,6 @@ __global__ void __launch_bounds__(256) k_gen_gaps(const intf_scenario* __restric
 constexpr int kScanChunk = 32;
 constexpr int kScanStage = 512;  // doubles per bulk copy (4 KB)
 constexpr int kScanStages = 4;   // copies in flight ahead of the add chain
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// one bulk global->shared copy completing on `bar` (bytes % 16 == 0, 16-byte aligned)
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar), d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
-               "l"(src), "r"(bytes), "r"(b)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(b), "r"(parity)
-        : "memory");
-  }
-}
 
 // one block (one active thread) per long model: the gaps stream through
 // shared memory by bulk copies kScanStages x 4 KB ahead of the add chain, so

@@ -324,18 +324,23 @@ def ols_solve(stats, want_pinv=False):
 
 
 def ols_windows(X, y, window: int):
-    """fit_ols_xy on every window of `window` consecutive rows (one launch of
-    statistics, one of solves) -> host (params[n_win, 7], info[n_win, 3])."""
+    """fit_ols_xy on every window of `window` consecutive rows -> host
+    (params[n_win, 7], info[n_win, 3]).  One launch: tensor-map staged when
+    the window is a multiple of 8 rows, thread per window otherwise (two
+    launches, statistics through HBM, for windows > 128 rows)."""
     dev = require_cuda()
     dX = X if isinstance(X, torch.Tensor) else _f64(np.asarray(X, dtype=np.float64).reshape(-1, 6), dev)
     dy = y if isinstance(y, torch.Tensor) else _f64(y, dev)
     n = dy.numel()
     n_win = (n + window - 1) // window
-    stats = torch.empty(max(n_win, 1) * 56, dtype=torch.float64, device=dev)
+    # statistics scratch only for the two-launch path (windows > 128 rows, not a multiple of 8)
+    stats = (torch.empty(max(n_win, 1) * 56, dtype=torch.float64, device=dev)
+             if window > 128 and window % 8 else None)
     params = torch.empty(max(n_win, 1) * 7, dtype=torch.float64, device=dev)
     info = torch.zeros(max(n_win, 1) * 3, dtype=torch.int32, device=dev)
-    _abi.check(_abi.load().intf_ols_windows(dX.data_ptr(), dy.data_ptr(), n, int(window), stats.data_ptr(),
-                                            params.data_ptr(), info.data_ptr(), stream_ptr()), "intf_ols_windows")
+    _abi.check(_abi.load().intf_ols_windows(dX.data_ptr(), dy.data_ptr(), n, int(window),
+                                            stats.data_ptr() if stats is not None else None, params.data_ptr(),
+                                            info.data_ptr(), stream_ptr()), "intf_ols_windows")
     return params.cpu().numpy().reshape(-1, 7)[:n_win], info.cpu().numpy().reshape(-1, 3)[:n_win]
 
 

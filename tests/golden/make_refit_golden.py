@@ -23,7 +23,7 @@ def main():
     X = np.concatenate([P["ewma/mode2/X"], P["ridge/X"]])
     y = np.concatenate([P["ewma/mode2/y"], P["ridge/y"]])
     arrs = {"X": X, "y": y}
-    for W in (64, 100, 333):
+    for W in (8, 24, 64, 100, 256, 333):
         fits = []
         for i in range(0, len(y), W):
             m = fit_ols_xy(X[i:i + W], y[i:i + W])

@@ -104,7 +104,7 @@ def test_ewma_experiment_matches_reference():
                                    P[f"ewma/mode{mi}/report"], rtol=RTOL)
 
 
-@pytest.mark.parametrize("window", [64, 100, 333])
+@pytest.mark.parametrize("window", [8, 24, 64, 100, 256, 333])
 def test_windowed_refit_matches_reference(window):
     """Refit each window (BASELINE configs[2]): one statistics + one solve
     launch for every window vs the reference's fit_ols_xy per window

@@ -12,14 +12,14 @@ L = _abi.load()
 n = 1 << 24
 X = torch.rand(n, 6, dtype=torch.float64, device="cuda")
 y = torch.rand(n, dtype=torch.float64, device="cuda")
-for W in (32, 64, 256, 1024):
+for W in (8, 32, 64, 100, 256, 1024):
     nw = (n + W - 1) // W
     st = torch.empty(nw * 56, dtype=torch.float64, device="cuda")
     pr = torch.empty(nw * 7, dtype=torch.float64, device="cuda")
     inf = torch.empty(nw * 3, dtype=torch.int32, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
-    f = lambda: _abi.check(L.intf_ols_windows(X.data_ptr(), y.data_ptr(), n, W, st.data_ptr(), pr.data_ptr(),
-                                              inf.data_ptr(), s), "w")
+    f = lambda: _abi.check(L.intf_ols_windows(X.data_ptr(), y.data_ptr(), n, W, None if W % 8 == 0 else st.data_ptr(),
+                                              pr.data_ptr(), inf.data_ptr(), s), "w")
     for _ in range(3):
         f()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
