@@ -270,11 +270,25 @@ int intf_predict_candidates_host(const intf_table *table, int32_t cap, double al
 #define INTF_OLS_WS_DOUBLES (592 * 35) /* workspace for intf_ols_stats (per-block partials) */
 int intf_ols_stats(const double *X, const double *y, int64_t n, double *out, double *ws, void *stream);
 /* Solve the 7x7 system from stats (fp64): rank test mirroring
- * np.linalg.matrix_rank on the Gram eigenvalues, ridge fallback
- * (RIDGE_EPS=1e-8) when rank-deficient, else Cholesky.  out_params[7]
- * (w0..w5, b); out_info[0] = 1 if the ridge fallback was used; out_Pinv
- * (optional, 49) = inv(Z^T Z) for rls_init.                                 */
+ * np.linalg.matrix_rank -- a condition screen on the Cholesky factor proves
+ * rank 7 for well-conditioned statistics, otherwise the Gram eigenvalues --
+ * ridge fallback (RIDGE_EPS=1e-8) when rank-deficient, else Cholesky.
+ * out_params[7] (w0..w5, b); out_info[0] = 1 if the ridge fallback was used;
+ * out_Pinv (optional, 49) = inv(Z^T Z) for rls_init.                        */
 int intf_ols_solve(const double *stats, double *out_params, int32_t *out_info, double *out_Pinv, void *stream);
+/* fit_ols_xy (`predict.py:53-66`) given the rows as well as their stats
+ * (intf_ols_stats): as intf_ols_solve, but statistics that fail the screen
+ * take matrix_rank(Z) -- and at rank 7 the solution -- from the rows: a
+ * tall-skinny QR of [Z | y] by Givens rotations over the n rows (fixed merge
+ * tree, deterministic) and a one-sided Jacobi SVD of R.  The Gram
+ * eigenvalues cannot resolve singular values below ~sqrt(eps) S_max (exactly
+ * collinear samples: a constant feature, duplicated rows), and the normal
+ * equations lose cond(Z)^2 eps where lstsq (and R^-1 Q^T y) lose cond(Z) eps.
+ * Well-conditioned statistics return after the screen (three launches, two
+ * of them exit at once).  ws: INTF_OLS_FIT_WS_DOUBLES.                       */
+#define INTF_OLS_FIT_WS_DOUBLES (128 * 35 + 8)
+int intf_ols_fit_rows(const double *X, const double *y, int64_t n, const double *stats, double *ws,
+                      double *out_params, int32_t *out_info, double *out_Pinv, void *stream);
 
 /* Windowed refit ("refit each window", BASELINE configs[2]): fit_ols_xy
  * (`predict.py:53-72`) on every window of `window` consecutive rows of X

@@ -77,6 +77,7 @@ class Predictor(ctypes.Structure):
 
 
 OLS_WS_DOUBLES = 592 * 35
+OLS_FIT_WS_DOUBLES = 128 * 35 + 8
 
 # status bits (INTF_ST_*)
 ST_PAST_EVENT, ST_CAP, ST_PROGRESS, ST_NONQUIESCENT, ST_OVERFLOW, ST_SEG_STRIDE = 1, 2, 4, 8, 16, 32
@@ -104,6 +105,7 @@ SIGNATURES = {
     "intf_repr_f64": (c_int32, [c_double, P, c_int32]),
     "intf_ols_stats": (c_int32, [P, P, c_int64, P, P, P]),
     "intf_ols_solve": (c_int32, [P, P, P, P, P]),
+    "intf_ols_fit_rows": (c_int32, [P, P, c_int64, P, P, P, P, P, P]),
     "intf_ols_windows": (c_int32, [P, P, c_int64, c_int32, P, P, P, P]),
     "intf_sgd_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P]),
     "intf_rls_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P, P]),

@@ -650,33 +650,81 @@ __device__ __forceinline__ void tri_inv7(const double L[7][7], double Li[7][7]) 
   }
 }
 
-// numpy.linalg.matrix_rank(Z) from the rows themselves (Z = [X[lo:lo+cnt], 1]):
-// R = QR(Z) by Givens row updates, then the singular values of R by one-sided
-// Jacobi (relative accuracy ~eps S_max, like the SVD of Z), tol = S_max *
-// max(cnt, 7) * eps.  The eigenvalues of Z^T Z cannot separate a singular
-// value below ~sqrt(eps) S_max (exactly collinear rows, e.g. duplicated
-// samples in a short window) from rounding; this can.  Cold path: only for
-// windows whose Z^T Z fails the condition screen.
-__device__ __noinline__ int matrix_rank_rows(const double* __restrict__ X, long long lo, long long cnt) {
-  double R[7][7];
-  for (int i = 0; i < 7; i++)
-    for (int j = 0; j < 7; j++) R[i][j] = 0.0;
-  for (long long k = 0; k < cnt; k++) {
-    double v[7];
-    for (int j = 0; j < 6; j++) v[j] = X[(lo + k) * 6 + j];
-    v[6] = 1.0;
-    for (int i = 0; i < 7; i++) {
-      if (v[i] == 0.0) continue;
-      const double h = hypot(R[i][i], v[i]), c = R[i][i] / h, sn = v[i] / h;
-      for (int j = i; j < 7; j++) {
-        const double a = R[i][j], b = v[j];
-        R[i][j] = c * a + sn * b;
-        v[j] = c * b - sn * a;
-      }
+// The rows themselves, for statistics that fail the condition screen
+// (ols_solve_one's cold path).  [Z | y] = Q [R | c] by Givens row updates
+// (R 7x7 upper triangular, c = Q^T y), then
+//   * matrix_rank(Z) (`predict.py:58`) from the singular values of R by
+//     one-sided Jacobi (relative accuracy ~eps S_max, like the SVD of Z),
+//     tol = S_max * max(n, 7) * eps.  The eigenvalues of Z^T Z cannot
+//     separate a singular value below ~sqrt(eps) S_max (exactly collinear
+//     samples: duplicated rows in a short window, a constant feature) from
+//     rounding; R can;
+//   * at rank 7, x = R^-1 c: accurate to ~cond(Z) eps like lstsq
+//     (`predict.py:63`), where the normal equations give ~cond(Z)^2 eps.
+// A factor is 7 rows x 8 columns ([R | c]); packed upper part = 35 doubles.
+constexpr int kQrPacked = 35;
+
+// fold row v = [z, y] (destroyed) into the factor F
+__device__ __forceinline__ void givens_row(double F[7][8], double* v) {
+#pragma unroll
+  for (int i = 0; i < 7; i++) {
+    if (v[i] == 0.0) continue;
+    const double h = hypot(F[i][i], v[i]), c = F[i][i] / h, sn = v[i] / h;
+#pragma unroll
+    for (int j = i; j < 8; j++) {
+      const double a = F[i][j], b = v[j];
+      F[i][j] = c * a + sn * b;
+      v[j] = c * b - sn * a;
     }
   }
-  // one-sided Jacobi on the columns of R
-  for (int sweep = 0; sweep < 40; sweep++) {
+}
+
+__device__ __forceinline__ void qr_zero(double F[7][8]) {
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) F[i][j] = 0.0;
+}
+
+// fold rows [lo, lo+cnt) of (X, y) (z = [x, 1]) into F
+__device__ __forceinline__ void qr_rows(double F[7][8], const double* __restrict__ X, const double* __restrict__ y,
+                                        long long lo, long long cnt) {
+  for (long long k = 0; k < cnt; k++) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 6; j++) v[j] = X[(lo + k) * 6 + j];
+    v[6] = 1.0;
+    v[7] = y[lo + k];
+    givens_row(F, v);
+  }
+}
+
+__device__ __forceinline__ void qr_store(const double F[7][8], double* p) {
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = i; j < 8; j++) p[t++] = F[i][j];
+}
+// fold the packed factor p into F (its rows are rows of an equivalent [Z | y])
+__device__ __forceinline__ void qr_merge(double F[7][8], const double* p) {
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 7; i++) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) v[j] = j < i ? 0.0 : p[t + j - i];
+    t += 8 - i;
+    givens_row(F, v);
+  }
+}
+
+// matrix_rank from F's R block; at rank 7 also x = R^-1 c into x
+__device__ __noinline__ int qr_rank_solve(const double F[7][8], double n_rows, double* x) {
+  double R[7][7];
+  for (int i = 0; i < 7; i++)
+    for (int j = 0; j < 7; j++) R[i][j] = F[i][j];
+  for (int sweep = 0; sweep < 40; sweep++) {  // one-sided Jacobi on the columns of R
     bool rotated = false;
     for (int p = 0; p < 6; p++)
       for (int q = p + 1; q < 7; q++) {
@@ -706,20 +754,38 @@ __device__ __noinline__ int matrix_rank_rows(const double* __restrict__ X, long 
     sv[j] = sqrt(t);
     smax = fmax(smax, sv[j]);
   }
-  const double tol = smax * fmax((double)cnt, 7.0) * 2.220446049250313e-16;
+  const double tol = smax * fmax(n_rows, 7.0) * 2.220446049250313e-16;
   int rank = 0;
   for (int j = 0; j < 7; j++) rank += sv[j] > tol;
+  if (rank == 7)
+    for (int i = 6; i >= 0; i--) {
+      double v = F[i][7];
+      for (int j = i + 1; j < 7; j++) v -= F[i][j] * x[j];
+      x[i] = v / F[i][i];
+    }
   return rank;
+}
+
+// rank (and the rank-7 solution) of rows [lo, lo+cnt), one thread
+__device__ __noinline__ int qr_rank_rows(const double* __restrict__ X, const double* __restrict__ y, long long lo,
+                                         long long cnt, double* x) {
+  double F[7][8];
+  qr_zero(F);
+  qr_rows(F, X, y, lo, cnt);
+  return qr_rank_solve(F, (double)cnt, x);
 }
 
 // fit_ols_xy (`predict.py:53-66`): matrix_rank(Z) < 7 -> ridge solve, else
 // least squares (normal equations; lstsq and Cholesky agree to ~cond*eps).
 // rank test: S_i = sqrt(eig(Z^T Z)); rank = #(S_i > S_max * max(n, 7) * eps).
-// rows: when given (X + [lo, lo+cnt)), the rank of a window that fails the
-// screen comes from the rows (matrix_rank_rows), else from eig(Z^T Z).
+// Statistics that fail the screen take their rank -- and, at rank 7, their
+// solution -- from the rows: qr = [rank, x0..x6] computed by the pooled QR
+// kernels (qr[0] < 0: not computed), or rows X, y + [lo, lo+cnt) (a window,
+// qr_rank_rows here), else the rank from eig(Z^T Z) and the normal equations.
 __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, double* params, int32_t* info,
                                               double* Pinv, const double* __restrict__ rows = nullptr,
-                                              long long lo = 0, long long cnt = 0) {
+                                              const double* __restrict__ rows_y = nullptr, long long lo = 0,
+                                              long long cnt = 0, const double* __restrict__ qr = nullptr) {
   double G[49], r[7], ev[7];
   for (int i = 0; i < 49; i++) G[i] = stats[i];
   for (int i = 0; i < 7; i++) r[i] = stats[49 + i];
@@ -771,14 +837,41 @@ __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, 
     }
   }
   int rank = 0;
-  if (rows) {
-    rank = matrix_rank_rows(rows, lo, cnt);
+  double xq[7];
+  bool have_x = false;
+  if (qr && qr[0] >= 0.0) {
+    rank = (int)qr[0];
+    for (int i = 0; i < 7; i++) xq[i] = qr[1 + i];
+    have_x = rank == 7;
+  } else if (rows) {
+    rank = qr_rank_rows(rows, rows_y, lo, cnt, xq);
+    have_x = rank == 7;
   } else {
     jacobi_eigs(G, ev);
     double smax = 0.0;
     for (int i = 0; i < 7; i++) smax = fmax(smax, sqrt(fmax(ev[i], 0.0)));
     const double tol = smax * fmax(n, 7.0) * 2.220446049250313e-16;
     for (int i = 0; i < 7; i++) rank += sqrt(fmax(ev[i], 0.0)) > tol;
+  }
+  if (have_x) {  // full rank, ill-conditioned: the QR solution (lstsq's accuracy)
+    int fin = 1;
+    for (int i = 0; i < 7; i++) {
+      params[i] = xq[i];
+      fin &= isfinite(xq[i]);
+    }
+    if (info) {
+      info[0] = 0;
+      info[1] = fin ? 0 : 1;
+    }
+    if (Pinv) {
+      double B[49];
+      for (int i = 0; i < 49; i++) B[i] = G[i];
+      if (!chol_solve(B, nullptr, nullptr, Pinv)) {
+        for (int i = 0; i < 7; i++) B[i * 8] += 1e-8;
+        chol_solve(B, nullptr, nullptr, Pinv);
+      }
+    }
+    return;
   }
   const bool ridge = rank < 7;
   double A[49];
@@ -810,9 +903,85 @@ __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, 
   }
 }
 
-__global__ void k_ols_solve(const double* __restrict__ stats, double* params, int32_t* info, double* Pinv) {
+__global__ void k_ols_solve(const double* __restrict__ stats, const double* __restrict__ qr, double* params,
+                            int32_t* info, double* Pinv) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  ols_solve_one(stats, params, info, Pinv);
+  ols_solve_one(stats, params, info, Pinv, nullptr, nullptr, 0, 0, qr);
+}
+
+// the condition screen of ols_solve_one alone: true = rank 7 proven
+__device__ bool ols_screen(const double* __restrict__ stats) {
+  double G[49];
+  for (int i = 0; i < 49; i++) G[i] = stats[i];
+  double L[7][7];
+  if (!chol7(G, L)) return false;
+  double Li[7][7];
+  tri_inv7(L, Li);
+  double tr = 0.0, ti = 0.0;
+  for (int i = 0; i < 7; i++) tr += G[i * 8];
+  for (int i = 0; i < 7; i++)
+    for (int j = 0; j <= i; j++) ti = fma(Li[i][j], Li[i][j], ti);
+  return isfinite(ti) && tr * ti < 1e10;
+}
+
+// pooled samples (tall-skinny QR): thread = contiguous run of rows folded
+// into its factor by Givens rotations, then a fixed binary tree of merges
+// per block (deterministic) -> ws[block]; k_ols_qr_final merges the blocks'
+// factors by the same tree -> qr = [rank, x].  Both exit at once when the
+// statistics pass the screen (rank 7 proven; qr[0] = -1).
+constexpr int kQrThreads = 64, kQrBlocks = 128;
+__global__ void __launch_bounds__(kQrThreads) k_ols_qr_rows(const double* __restrict__ X, const double* __restrict__ y,
+                                                            long long n, const double* __restrict__ stats,
+                                                            double* ws) {
+  __shared__ double sh[kQrThreads][kQrPacked];
+  __shared__ bool pass;
+  if (threadIdx.x == 0) pass = ols_screen(stats);
+  __syncthreads();
+  if (pass) return;
+  const long long T = (long long)gridDim.x * kQrThreads, t = (long long)blockIdx.x * kQrThreads + threadIdx.x;
+  const long long per = (n + T - 1) / T, lo = t * per, hi = lo + per < n ? lo + per : n;
+  double F[7][8];
+  qr_zero(F);
+  if (lo < hi) qr_rows(F, X, y, lo, hi - lo);
+  qr_store(F, sh[threadIdx.x]);
+  __syncthreads();
+  for (int s = 1; s < kQrThreads; s <<= 1) {
+    if ((threadIdx.x & (2 * s - 1)) == 0) {
+      qr_merge(F, sh[threadIdx.x + s]);
+      qr_store(F, sh[threadIdx.x]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < kQrPacked) ws[blockIdx.x * kQrPacked + threadIdx.x] = sh[0][threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kQrBlocks) k_ols_qr_final(const double* __restrict__ stats, const double* ws,
+                                                            int n_blocks, double n_rows, double* qr) {
+  __shared__ double sh[kQrBlocks][kQrPacked];
+  __shared__ bool pass;
+  if (threadIdx.x == 0) pass = ols_screen(stats);
+  __syncthreads();
+  if (pass) {
+    if (threadIdx.x == 0) qr[0] = -1.0;
+    return;
+  }
+  double F[7][8];
+  qr_zero(F);
+  if (threadIdx.x < n_blocks) qr_merge(F, ws + threadIdx.x * kQrPacked);
+  qr_store(F, sh[threadIdx.x]);
+  __syncthreads();
+  for (int s = 1; s < kQrBlocks; s <<= 1) {
+    if ((threadIdx.x & (2 * s - 1)) == 0) {
+      qr_merge(F, sh[threadIdx.x + s]);
+      qr_store(F, sh[threadIdx.x]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double x[7] = {0, 0, 0, 0, 0, 0, 0};
+    qr[0] = (double)qr_rank_solve(F, n_rows, x);
+    for (int i = 0; i < 7; i++) qr[1 + i] = x[i];
+  }
 }
 
 // ---- windowed refit (C3, "refit each window"): fit_ols on every window of
@@ -877,9 +1046,9 @@ __device__ __forceinline__ void ols_acc_row(double* acc, const double* x6, doubl
 }
 
 // the window's statistics (optionally to HBM), its solve and its info row
-__device__ __forceinline__ void ols_window_finish(const double* acc, const double* __restrict__ X, long long w,
-                                                  long long lo, long long cnt, double* stats, double* params,
-                                                  int32_t* info) {
+__device__ __forceinline__ void ols_window_finish(const double* acc, const double* __restrict__ X,
+                                                  const double* __restrict__ y, long long w, long long lo,
+                                                  long long cnt, double* stats, double* params, int32_t* info) {
   double st[56];
   int t = 0;
 #pragma unroll
@@ -893,7 +1062,7 @@ __device__ __forceinline__ void ols_window_finish(const double* acc, const doubl
     for (int i = 0; i < 56; i++) stats[w * 56 + i] = st[i];
   }
   int32_t inf2[2] = {0, 0};
-  ols_solve_one(st, params + w * 7, inf2, nullptr, X, lo, cnt);
+  ols_solve_one(st, params + w * 7, inf2, nullptr, X, y, lo, cnt);
   info[3 * w] = inf2[0];
   info[3 * w + 1] = inf2[1];
   info[3 * w + 2] = cnt < 7 ? 1 : 0;
@@ -920,7 +1089,7 @@ __global__ void __launch_bounds__(128) k_ols_windows_fused(const double* __restr
     const double x6[6] = {a.x, a.y, b.x, b.y, c.x, c.y};
     ols_acc_row(acc, x6, __ldg(y + row));
   }
-  ols_window_finish(acc, X, w, lo, hi - lo, stats, params, info);
+  ols_window_finish(acc, X, y, w, lo, hi - lo, stats, params, info);
 }
 
 // windows of a multiple of 8 rows: one warp per block, persistent over groups
@@ -1012,19 +1181,20 @@ __global__ void __launch_bounds__(32) k_ols_windows_tma(const __grid_constant__ 
       __syncwarp();  // every lane is done with the stage before it is refilled
       if (++st == S) st = 0, ph ^= 1u;
     }
-    if (w < n_win) ols_window_finish(acc, X, w, lo, cnt, stats, params, info);
+    if (w < n_win) ols_window_finish(acc, X, y, w, lo, cnt, stats, params, info);
   }
 }
 
 // info[3w..]: ridge used, non-finite params, fewer than 7 rows (fit_ols raises
 // PredictError for those; fit_ols_xy solves them through the ridge fallback)
-__global__ void k_ols_window_solve(const double* __restrict__ stats, const double* __restrict__ X, long long n_win,
-                                   long long n, int window, double* __restrict__ params, int32_t* __restrict__ info) {
+__global__ void k_ols_window_solve(const double* __restrict__ stats, const double* __restrict__ X,
+                                   const double* __restrict__ y, long long n_win, long long n, int window,
+                                   double* __restrict__ params, int32_t* __restrict__ info) {
   const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= n_win) return;
   const long long cnt = (w + 1) * window <= n ? window : n - w * window;
   int32_t inf2[2] = {0, 0};
-  ols_solve_one(stats + w * 56, params + w * 7, inf2, nullptr, X, w * window, cnt);
+  ols_solve_one(stats + w * 56, params + w * 7, inf2, nullptr, X, y, w * window, cnt);
   info[3 * w] = inf2[0];
   info[3 * w + 1] = inf2[1];
   info[3 * w + 2] = cnt < 7 ? 1 : 0;
@@ -1472,7 +1642,23 @@ int intf_ols_stats(const double* X, const double* y, int64_t n, double* out, dou
 
 int intf_ols_solve(const double* stats, double* out_params, int32_t* out_info, double* out_Pinv, void* stream) {
   if (!stats || !out_params) return bad_input("intf_ols_solve: null argument");
-  k_ols_solve<<<1, 32, 0, as_stream(stream)>>>(stats, out_params, out_info, out_Pinv);
+  k_ols_solve<<<1, 32, 0, as_stream(stream)>>>(stats, nullptr, out_params, out_info, out_Pinv);
+  return launch_status("k_ols_solve");
+}
+
+int intf_ols_fit_rows(const double* X, const double* y, int64_t n, const double* stats, double* ws,
+                      double* out_params, int32_t* out_info, double* out_Pinv, void* stream) {
+  if (!X || !y || !stats || !ws || !out_params || n < 0) return bad_input("intf_ols_fit_rows: bad argument");
+  cudaStream_t st = as_stream(stream);
+  const long long want = (n + 32ll * kQrThreads - 1) / (32ll * kQrThreads);  // >= 32 rows per thread
+  const int nb = (int)(want < 1 ? 1 : want > kQrBlocks ? kQrBlocks : want);
+  double* qr = ws + kQrBlocks * kQrPacked;
+  k_ols_qr_rows<<<nb, kQrThreads, 0, st>>>(X, y, (long long)n, stats, ws);
+  int rc = launch_status("k_ols_qr_rows");
+  if (rc) return rc;
+  k_ols_qr_final<<<1, kQrBlocks, 0, st>>>(stats, ws, nb, (double)n, qr);
+  if ((rc = launch_status("k_ols_qr_final"))) return rc;
+  k_ols_solve<<<1, 32, 0, st>>>(stats, qr, out_params, out_info, out_Pinv);
   return launch_status("k_ols_solve");
 }
 
@@ -1509,7 +1695,7 @@ int intf_ols_windows(const double* X, const double* y, int64_t n, int32_t window
   k_ols_window_stats<<<ceil_div(n_win, kWinWarps), 32 * kWinWarps, 0, st>>>(X, y, (long long)n, window, n_win, stats);
   int rc = launch_status("k_ols_window_stats");
   if (rc) return rc;
-  k_ols_window_solve<<<ceil_div(n_win, 128), 128, 0, st>>>(stats, X, n_win, (long long)n, window, params, info);
+  k_ols_window_solve<<<ceil_div(n_win, 128), 128, 0, st>>>(stats, X, y, n_win, (long long)n, window, params, info);
   return launch_status("k_ols_window_solve");
 }
 

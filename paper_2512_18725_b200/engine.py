@@ -323,6 +323,24 @@ def ols_solve(stats, want_pinv=False):
             pinv.cpu().numpy().reshape(7, 7) if want_pinv else None)
 
 
+def ols_fit(X, y):
+    """fit_ols_xy on the device (`predict.py:53-66`): statistics, then the
+    solve; an ill-conditioned design takes its rank (and its rank-7
+    solution) from a QR of its rows.  -> (params[7], ridge_used, nonfinite)."""
+    dev = require_cuda()
+    dX = X if isinstance(X, torch.Tensor) else _f64(np.asarray(X, dtype=np.float64).reshape(-1, 6), dev)
+    dy = y if isinstance(y, torch.Tensor) else _f64(y, dev)
+    stats = ols_stats(dX, dy)
+    ws = torch.empty(_abi.OLS_FIT_WS_DOUBLES, dtype=torch.float64, device=dev)
+    params = torch.empty(7, dtype=torch.float64, device=dev)
+    info = torch.zeros(2, dtype=torch.int32, device=dev)
+    _abi.check(_abi.load().intf_ols_fit_rows(dX.data_ptr(), dy.data_ptr(), dy.numel(), stats.data_ptr(),
+                                             ws.data_ptr(), params.data_ptr(), info.data_ptr(), None, stream_ptr()),
+               "intf_ols_fit_rows")
+    inf = info.cpu().numpy()
+    return params.cpu().numpy(), bool(inf[0]), bool(inf[1])
+
+
 def ols_windows(X, y, window: int):
     """fit_ols_xy on every window of `window` consecutive rows -> host
     (params[n_win, 7], info[n_win, 3]).  One launch: tensor-map staged when

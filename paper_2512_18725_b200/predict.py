@@ -63,12 +63,12 @@ def _design(samples):
 
 def fit_ols_xy(X, y) -> LinearModel:
     """Least squares with intercept; ridge fallback if rank-deficient
-    (`predict.py:53-66`).  Z^T Z / Z^T y reduced on the device in fp64."""
+    (`predict.py:53-66`).  Z^T Z / Z^T y reduced on the device in fp64; an
+    ill-conditioned design takes its rank and solution from a device QR of
+    its rows."""
     from . import engine
 
-    X = np.asarray(X, dtype=float)
-    stats = engine.ols_stats(X, np.asarray(y, dtype=float))
-    params, ridge, nonfinite, _ = engine.ols_solve(stats)
+    params, ridge, nonfinite = engine.ols_fit(np.asarray(X, dtype=float), np.asarray(y, dtype=float))
     if ridge:
         log.warning("rank-deficient design matrix (n=%d), using ridge fallback", len(X))
     model = LinearModel(w=params[:6].copy(), b=float(params[6]))

@@ -104,6 +104,44 @@ def test_ewma_experiment_matches_reference():
                                    P[f"ewma/mode{mi}/report"], rtol=RTOL)
 
 
+@pytest.mark.parametrize("name", ["identical", "constant", "proportional", "duplicates", "near_collinear",
+                                  "constant_big", "control"])
+def test_fit_ols_ill_conditioned_matches_reference(name):
+    """fit_ols_xy where matrix_rank(Z) and lstsq decide (the reference's
+    collinear-design test and friends, tests/golden/ols_rank_golden.npz):
+    the device QR of the rows gives the reference's rank (ridge or not) and,
+    for the nearly collinear full-rank design, lstsq's accuracy."""
+    import logging
+
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200 import engine
+    from tests.golden.ols_rank_designs import designs
+
+    from paper_2512_18725_b200.predict import predict
+
+    G = _golden.load("ols_rank_golden.npz")
+    X, y = designs()[name]
+    params, ridge, nonfinite = engine.ols_fit(X, y)
+    ref = G[f"{name}/params"]
+    assert ridge == bool(G[f"{name}/ridge"]) and not nonfinite
+    if ridge:
+        # solve(Z^T Z + 1e-8 I, Z^T y) fixes the component along Z's null
+        # direction only through the rounding of Z^T Z and Z^T y (the
+        # reference's BLAS order): parity is the ridge decision and the fit
+        Z = np.column_stack([X, np.ones(len(y))])
+        np.testing.assert_allclose(Z @ params, Z @ ref, rtol=RTOL, atol=1e-7)
+    else:
+        np.testing.assert_allclose(params, ref, rtol=RTOL, atol=1e-7)
+    logging.disable(logging.WARNING)
+    try:
+        m = p.fit_ols_xy(X, y)
+    finally:
+        logging.disable(logging.NOTSET)
+    np.testing.assert_array_equal(m.w7(), params)
+    if name == "identical":  # the reference's test_ols_ridge_fallback_on_collinear_design
+        assert abs(predict(m, X[0]) - 1.5) <= 1e-3
+
+
 @pytest.mark.parametrize("window", [8, 24, 64, 100, 256, 333])
 def test_windowed_refit_matches_reference(window):
     """Refit each window (BASELINE configs[2]): one statistics + one solve

@@ -90,6 +90,19 @@ def test_oracle_predictor_restatement_matches_golden():
     np.testing.assert_array_equal(np.append(w, b), P["ridge/w"])
 
 
+def test_oracle_fit_ols_ill_conditioned_matches_golden():
+    """The oracle's fit_ols_xy on the rank-deficient / ill-conditioned designs
+    of tests/golden/ols_rank_golden.npz (reference results)."""
+    from tests.golden.ols_rank_designs import designs
+
+    G = _golden.load("ols_rank_golden.npz")
+    for name, (X, y) in designs().items():
+        if len(y) > 10000:
+            continue  # the 2*10^5-row design is for the device QR only (time)
+        w, b = O.fit_ols_xy(X, y)
+        np.testing.assert_array_equal(np.append(w, b), G[f"{name}/params"])
+
+
 def test_oracle_candidates_match_golden():
     C = _golden.load("candidates_golden.npz")
     tab = _otab()
