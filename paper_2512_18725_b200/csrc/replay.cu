@@ -17,6 +17,9 @@ using namespace intf;
 
 namespace {
 
+#ifndef INTF_SCAN_SEQ
+#define INTF_SCAN_SEQ 0  // 1: the one-thread add chain k_scan_gaps (A/B reference for k_scan_binade)
+#endif
 #ifndef INTF_BIG_LIST
 #define INTF_BIG_LIST 4096
 #endif
@@ -60,13 +63,14 @@ __global__ void __launch_bounds__(256) k_gen_gaps(const intf_scenario* __restric
   }
 }
 
-// ---- K0a' (long lists): the cumulative sum t += gap stays strictly
-// sequential (`workload.py:91`: the reference's rounding), one thread per
-// long model, but as a pure add chain that stores only every kScanChunk-th
-// partial sum (into mb_t, free until formation); k_fill_gaps then redoes
-// each chunk's adds -- the same operations in the same order, so the same
-// values -- in parallel and finds the horizon crossing.
+// ---- K0a' (long lists): every kScanChunk-th partial sum of t += gap
+// (`workload.py:91`) goes into mb_t (free until formation) -- k_scan_binade
+// (below, the product) or the one-thread add chain k_scan_gaps (A/B
+// reference, INTF_SCAN_SEQ=1); k_fill_gaps then redoes each chunk's adds --
+// the same operations in the same order, so the same values -- in parallel
+// and finds the horizon crossing.
 constexpr int kScanChunk = 32;
+#if INTF_SCAN_SEQ
 constexpr int kScanStage = 512;  // doubles per bulk copy (4 KB)
 constexpr int kScanStages = 4;   // copies in flight ahead of the add chain
 
@@ -119,6 +123,8 @@ __global__ void __launch_bounds__(32) k_scan_gaps(const intf_scenario* __restric
   // copies still in flight must land before the block (and its smem) exits
   for (int d = c; d < issued; d++) mbar_wait(&bar[d % kScanStages], (unsigned)(d / kScanStages) & 1u);
 }
+
+#endif  // INTF_SCAN_SEQ
 
 // thread per (long model, chunk): rebuild the chunk's arrival times from the
 // previous chunk's end; the chunk holding the horizon crossing sets n_list
@@ -689,6 +695,230 @@ __device__ __forceinline__ int block_excl_maxi(int v, int* sh) {
   const int r = t > 0 ? sh[t - 1] : -1;
   __syncthreads();
   return r;
+}
+
+// ---- K0a' (long lists), exact and parallel: the cumulative sum t += gap
+// (`workload.py:91`) reproduced bit for bit without a 3x10^5-long add chain.
+// Inside one binade [2^e, 2^(e+1)) every double is a multiple of u =
+// 2^(e-52), so fl(t + g) = t + u * rint(g / u) as long as the sum stays in
+// the binade and g / u is not a half-integer (ties-to-even would depend on
+// t's last bit): a run of such steps is an exact INTEGER prefix sum.  Per
+// long model, one block:
+//   1. chunk c (32 gaps) sum S_c, block scan -> T_c, an estimate of t at the
+//      chunk start (only a prediction: everything below is verified);
+//   2. chunk c is "clean" if [T_c - d, T_c + S_c + d] lies inside one binade
+//      e (d bounds the estimate's error) and no gap is a half-integer
+//      multiple of u_e; then N_c = sum rint(g / u_e) (int64);
+//   3. runs of consecutive clean chunks of one binade: segmented prefix sums
+//      P_c of N_c;
+//   4. one thread walks the runs and the other chunks in order: a run
+//      starting at the exact t_run ends at t_run + u P_last, verified inside
+//      [2^e, 2^(e+1)) (so every intermediate sum was in the binade); anything
+//      else -- a binade crossing, a tie, a failed verification -- takes the
+//      32 real fp64 adds per chunk from the exact t;
+//   5. every run's chunk ends t_run + u P_c in parallel (exact).
+// Output as k_scan_gaps: every 32nd partial sum in mb_t, INF past the horizon.
+constexpr int kBinThreads = 1024;
+constexpr int kBinOff = 2048;      // chunk code = e + kBinOff (clean), -1 (sequential)
+constexpr int kBinHead = 1 << 20;  // code bit: first chunk of a run
+
+__global__ void __launch_bounds__(kBinThreads) k_scan_binade(const intf_scenario* __restrict__ scen,
+                                                             const intf_model* __restrict__ models, int n_models_total,
+                                                             intf_replay_buffers B) {
+  __shared__ double shd[kBinThreads];
+  __shared__ long long shl[kBinThreads];
+  __shared__ int shf[kBinThreads], shc[kBinThreads], shn[kBinThreads];
+  const int g = blockIdx.x;
+  if (g >= n_models_total) return;
+  const intf_model& M = models[g];
+  if (M.list_cap < kBigList || M.rate_rps == 0.0) return;
+  const int t = threadIdx.x;
+  const double* lt = B.list_t + M.list_off;
+  const int cap = M.list_cap, n32 = cap / kScanChunk;
+  double* ends = B.mb_t + M.list_off;  // mb_t is free until formation: ends, then P (int64), then codes
+  long long* P = reinterpret_cast<long long*>(ends + n32);
+  int* code = reinterpret_cast<int*>(ends + 2 * n32);
+  const double horizon = scen[M.scen].duration_s * 1000.0;
+  // 1 + 2: chunk sums, scan, classification.  A warp owns 32 consecutive
+  // chunks (lane l: chunk base + 32 w + l) but reads them coalesced, one
+  // chunk per load (lane = gap), reducing across the lanes.
+  const int lane = t & 31, wbase = t & ~31;
+  double carry = 0.0;
+  for (int base = 0; base < n32; base += kBinThreads) {
+    const int c = base + t;
+    double S = 0.0;
+    for (int j = 0; j < 32; j++) {
+      const int cj = base + wbase + j;
+      double v = cj < n32 ? lt[(long long)cj * kScanChunk + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == j) S = v;
+    }
+    shd[t] = S;
+    __syncthreads();
+    for (int o = 1; o < kBinThreads; o <<= 1) {
+      const double a = t >= o ? shd[t - o] : 0.0;
+      __syncthreads();
+      shd[t] += a;
+      __syncthreads();
+    }
+    const double T = carry + (shd[t] - S);  // exclusive (estimate)
+    carry += shd[kBinThreads - 1];
+    __syncthreads();
+    // candidate binade of this lane's chunk: [T - d, T + S + d] inside one binade
+    int e = -100000;
+    if (c < n32 && c > 0) {
+      const double hi_est = T + S;
+      const double d = hi_est * 0x1p-40 + 4.0 * cap * ldexp(1.0, ilogb(hi_est > 0.0 ? hi_est : 1.0) - 52);
+      if (T - d > 0.0 && ilogb(T - d) == ilogb(hi_est + d)) e = ilogb(T - d);
+    }
+    // N = sum rint(g / u_e) and the tie test, chunk by chunk across the warp
+    long long N = 0;
+    int cd = -1;
+    for (int j = 0; j < 32; j++) {
+      const int ej = __shfl_sync(0xffffffffu, e, j);
+      const int cj = base + wbase + j;
+      if (ej == -100000 || cj >= n32) continue;  // warp-uniform
+      const double x = lt[(long long)cj * kScanChunk + lane] * ldexp(1.0, 52 - ej);
+      const double r = rint(x);
+      const bool ok = __all_sync(0xffffffffu, x < 0x1p53 && fabs(x - r) != 0.5);
+      long long v = (long long)r;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == j) {
+        N = v;
+        cd = ok ? ej + kBinOff : -1;
+      }
+    }
+    if (c < n32) {
+      code[c] = cd;
+      P[c] = N;
+    }
+  }
+  __syncthreads();
+  // 3: run heads and segmented prefix sums of N
+  long long run = 0;  // the open run's sum carried across rounds
+  for (int base = 0; base < n32; base += kBinThreads) {
+    const int c = base + t;
+    int cd = -1;
+    long long v = 0;
+    int head = 1;
+    if (c < n32) {
+      cd = code[c];
+      v = P[c];
+      const int prev = c > 0 ? (code[c - 1] & ~kBinHead) : -1;
+      head = cd < 0 || prev != cd;
+    }
+    shl[t] = v;
+    shf[t] = head;
+    __syncthreads();
+    for (int o = 1; o < kBinThreads; o <<= 1) {
+      const long long a = t >= o ? shl[t - o] : 0;
+      const int af = t >= o ? shf[t - o] : 0;
+      __syncthreads();
+      if (!shf[t]) shl[t] += a;
+      shf[t] |= af;
+      __syncthreads();
+    }
+    const long long incl = shf[t] ? shl[t] : run + shl[t];
+    if (c < n32) {
+      P[c] = incl;
+      if (cd >= 0 && head) code[c] = cd | kBinHead;
+    }
+    __syncthreads();
+    run = shf[kBinThreads - 1] ? shl[kBinThreads - 1] : run + shl[kBinThreads - 1];
+    __syncthreads();
+  }
+  // 4: events = sequential chunks and run heads, compacted in order (evpos),
+  // each chunk's event index (evidx = events up to it - 1)
+  int* evidx = code + n32;
+  int* evpos = evidx + n32;
+  double* evT = ends + 4 * n32;  // per event: the exact t at the run start, NAN if the run was walked
+  int evbase = 0;
+  for (int base = 0; base < n32; base += kBinThreads) {
+    const int c = base + t;
+    int f = 0;
+    if (c < n32) {
+      const int cd = code[c];
+      f = cd < 0 || (cd & kBinHead);
+    }
+    shf[t] = f;
+    __syncthreads();
+    for (int o = 1; o < kBinThreads; o <<= 1) {
+      const int a = t >= o ? shf[t - o] : 0;
+      __syncthreads();
+      shf[t] += a;
+      __syncthreads();
+    }
+    if (c < n32) {
+      evidx[c] = evbase + shf[t] - 1;
+      if (f) evpos[evbase + shf[t] - 1] = c;
+    }
+    evbase += shf[kBinThreads - 1];
+    __syncthreads();
+  }
+  // 5: the walk over events (one thread; each batch of events staged in
+  // shared memory first): a run advances t by its last prefix sum, verified;
+  // a sequential chunk (or a run that fails the verification, chunk by
+  // chunk) takes the real adds
+  double tc = 0.0;
+  for (int b0 = 0; b0 < evbase; b0 += kBinThreads) {
+    const int i = b0 + t;
+    if (i < evbase) {
+      const int c = evpos[i], nxt = i + 1 < evbase ? evpos[i + 1] : n32;
+      shc[t] = c;
+      shn[t] = nxt;
+      shf[t] = code[c];
+      shl[t] = P[nxt - 1];
+    }
+    __syncthreads();
+    if (t == 0) {
+      const int nb = min(kBinThreads, evbase - b0);
+      for (int k = 0; k < nb; k++) {
+        const int cd = shf[k];
+        bool walked = true;
+        if (cd >= 0) {
+          const int e = (cd & ~kBinHead) - kBinOff;
+          const double te = tc + ldexp(1.0, e - 52) * (double)shl[k];
+          if (tc >= ldexp(1.0, e) && te < ldexp(1.0, e + 1)) {
+            evT[b0 + k] = tc;
+            tc = te;
+            walked = false;
+          }
+        }
+        if (walked) {
+          evT[b0 + k] = NAN;
+          for (int cc = shc[k]; cc < shn[k]; cc++) {
+            double gv[kScanChunk];
+#pragma unroll
+            for (int q = 0; q < kScanChunk; q++) gv[q] = lt[cc * kScanChunk + q];
+#pragma unroll
+            for (int q = 0; q < kScanChunk; q++) tc = tc + gv[q];
+            ends[cc] = tc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // 6: the runs' chunk ends in parallel (exact: trun + u P_c, inside the
+  // verified binade), then INF past the first chunk that reaches the horizon
+  __shared__ int first_past;
+  if (t == 0) first_past = n32;
+  __syncthreads();
+  for (int c = t; c < n32; c += kBinThreads) {
+    const int i = evidx[c];
+    const double trun = evT[i];
+    if (!isnan(trun)) {
+      const int e = (code[evpos[i]] & ~kBinHead) - kBinOff;
+      ends[c] = trun + ldexp(1.0, e - 52) * (double)P[c];
+    }
+  }
+  __syncthreads();
+  for (int c = t; c < n32; c += kBinThreads)
+    if (ends[c] >= horizon) atomicMin(&first_past, c);
+  __syncthreads();
+  for (int c = first_past + 1 + t; c < n32; c += kBinThreads) ends[c] = INFINITY;
 }
 
 __global__ void __launch_bounds__(kBigThreads) k_jobs_plan_big(const intf_scenario* __restrict__ scen,
@@ -1497,8 +1727,13 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
     k_gen_gaps<<<dim3(ceil_div(bt->max_list_cap, 256 * kGapRun), y, ceil_div(m, y)), 256, 0, st>>>(
         bt->scen, bt->models, bt->n_models, *buf);
     if ((rc = launch_status("k_gen_gaps"))) return rc;
+#if INTF_SCAN_SEQ
     k_scan_gaps<<<bt->n_models, 32, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
     if ((rc = launch_status("k_scan_gaps"))) return rc;
+#else
+    k_scan_binade<<<bt->n_models, kBinThreads, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_scan_binade"))) return rc;
+#endif
     k_fill_gaps<<<dim3(ceil_div(ceil_div(bt->max_list_cap, kScanChunk), 128), y, ceil_div(m, y)), 128, 0, st>>>(
         bt->scen, bt->models, bt->n_models, *buf);
     if ((rc = launch_status("k_fill_gaps"))) return rc;
