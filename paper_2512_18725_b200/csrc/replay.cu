@@ -18,7 +18,7 @@ using namespace intf;
 namespace {
 
 #ifndef INTF_SCAN_SEQ
-#define INTF_SCAN_SEQ 0  // 1: the one-thread add chain k_scan_gaps (A/B reference for k_scan_binade)
+#define INTF_SCAN_SEQ 0  // 1: the one-thread add chain k_scan_gaps (A/B reference for the k_bin_* kernels)
 #endif
 #ifndef INTF_BIG_LIST
 #define INTF_BIG_LIST 4096
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_gen_gaps(const intf_scenario* __restric
 }
 
 // ---- K0a' (long lists): every kScanChunk-th partial sum of t += gap
-// (`workload.py:91`) goes into mb_t (free until formation) -- k_scan_binade
+// (`workload.py:91`) goes into mb_t (free until formation) -- the k_bin_* kernels
 // (below, the product) or the one-thread add chain k_scan_gaps (A/B
 // reference, INTF_SCAN_SEQ=1); k_fill_gaps then redoes each chunk's adds --
 // the same operations in the same order, so the same values -- in parallel
@@ -702,174 +702,251 @@ __device__ __forceinline__ int block_excl_maxi(int v, int* sh) {
 // Inside one binade [2^e, 2^(e+1)) every double is a multiple of u =
 // 2^(e-52), so fl(t + g) = t + u * rint(g / u) as long as the sum stays in
 // the binade and g / u is not a half-integer (ties-to-even would depend on
-// t's last bit): a run of such steps is an exact INTEGER prefix sum.  Per
-// long model, one block:
-//   1. chunk c (32 gaps) sum S_c, block scan -> T_c, an estimate of t at the
-//      chunk start (only a prediction: everything below is verified);
-//   2. chunk c is "clean" if [T_c - d, T_c + S_c + d] lies inside one binade
-//      e (d bounds the estimate's error) and no gap is a half-integer
-//      multiple of u_e; then N_c = sum rint(g / u_e) (int64);
-//   3. runs of consecutive clean chunks of one binade: segmented prefix sums
-//      P_c of N_c;
-//   4. one thread walks the runs and the other chunks in order: a run
-//      starting at the exact t_run ends at t_run + u P_last, verified inside
-//      [2^e, 2^(e+1)) (so every intermediate sum was in the binade); anything
-//      else -- a binade crossing, a tie, a failed verification -- takes the
-//      32 real fp64 adds per chunk from the exact t;
-//   5. every run's chunk ends t_run + u P_c in parallel (exact).
-// Output as k_scan_gaps: every 32nd partial sum in mb_t, INF past the horizon.
+// t's last bit): a run of such steps is an exact INTEGER prefix sum.
+//   k_bin_sums      (grid)  chunk c (32 gaps): S_c;
+//   k_bin_scan      (block per model) T_c = sum of S before c: an estimate of
+//                   t at the chunk start (a prediction only: all below is verified);
+//   k_bin_classify  (grid)  chunk c is "clean" if [T_c - d, T_c + S_c + d]
+//                   lies in one binade e (d bounds the estimate's error) and
+//                   no gap is a half-integer multiple of u_e; N_c = sum rint(g / u_e);
+//   k_bin_runs      (block per model) runs of clean chunks of one binade:
+//                   segmented prefix sums P_c; one thread walks the runs and
+//                   the other chunks in order: a run starting at the exact
+//                   t_run ends at t_run + u P_last, verified inside [2^e,
+//                   2^(e+1)) (so every intermediate sum was in the binade);
+//                   anything else -- a binade crossing, a tie, a failed
+//                   verification -- takes the 32 real fp64 adds per chunk;
+//   k_bin_fill      (grid)  every run chunk's end t_run + u P_c (exact).
+// Output: every 32nd partial sum in mb_t (ends), for k_fill_gaps.  mb_t is
+// free until formation; per long model it holds (n32 = list_cap / 32 chunks)
+// ends | S | T | P (int64) | code, evidx, evpos (int) | evT.
 constexpr int kBinThreads = 1024;
 constexpr int kBinOff = 2048;      // chunk code = e + kBinOff (clean), -1 (sequential)
 constexpr int kBinHead = 1 << 20;  // code bit: first chunk of a run
 
-__global__ void __launch_bounds__(kBinThreads) k_scan_binade(const intf_scenario* __restrict__ scen,
-                                                             const intf_model* __restrict__ models, int n_models_total,
+struct BinScratch {
+  double *ends, *S, *T, *evT;
+  long long* P;
+  int *code, *evidx, *evpos;
+  int n32;
+};
+__device__ __forceinline__ BinScratch bin_scratch(const intf_model& M, const intf_replay_buffers& B) {
+  BinScratch b;
+  b.n32 = M.list_cap / kScanChunk;
+  b.ends = B.mb_t + M.list_off;
+  b.S = b.ends + b.n32;
+  b.T = b.ends + 2 * b.n32;
+  b.P = reinterpret_cast<long long*>(b.ends + 3 * b.n32);
+  b.code = reinterpret_cast<int*>(b.ends + 4 * b.n32);
+  b.evidx = b.code + b.n32;
+  b.evpos = b.evidx + b.n32;
+  b.evT = b.ends + 6 * b.n32;
+  return b;
+}
+
+// grid (chunk blocks, models): a warp stages its 32 chunks (32 x 32 gaps)
+// through shared memory with coalesced loads; lane l then owns chunk cb + l
+constexpr int kBinWarps = 4;
+__device__ __forceinline__ const intf_model* bin_model(const intf_model* models, int n_models_total) {
+  const int g = blockIdx.z * gridDim.y + blockIdx.y;
+  if (g >= n_models_total) return nullptr;
+  const intf_model* M = models + g;
+  return (M->list_cap < kBigList || M->rate_rps == 0.0) ? nullptr : M;
+}
+__device__ __forceinline__ int bin_stage(double (*sm)[33], const double* lt, int cb, int n32) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < 32; j++) {
+    const int c = cb + j;
+    sm[j][lane] = c < n32 ? lt[(long long)c * kScanChunk + lane] : 0.0;
+  }
+  __syncwarp();
+  return cb + lane;
+}
+
+__global__ void __launch_bounds__(32 * kBinWarps) k_bin_sums(const intf_model* __restrict__ models, int n_models_total,
                                                              intf_replay_buffers B) {
-  __shared__ double shd[kBinThreads];
+  __shared__ double sm[kBinWarps][32][33];
+  const intf_model* M = bin_model(models, n_models_total);
+  if (!M) return;
+  const BinScratch b = bin_scratch(*M, B);
+  const int cb = (blockIdx.x * kBinWarps + (threadIdx.x >> 5)) * 32;
+  if (cb >= b.n32) return;
+  const int c = bin_stage(sm[threadIdx.x >> 5], B.list_t + M->list_off, cb, b.n32);
+  double S = 0.0;
+  for (int k = 0; k < kScanChunk; k++) S += sm[threadIdx.x >> 5][threadIdx.x & 31][k];
+  if (c < b.n32) b.S[c] = S;
+}
+
+// block-wide inclusive scan (+) of one value per thread (1024 threads): warp
+// shuffles, then the 32 warp totals; `tot` = the block total
+template <typename V>
+__device__ __forceinline__ V bin_block_incl(V v, V* sw, V* tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const V a = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += a;
+  }
+  if (lane == 31) sw[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    V x = sw[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const V a = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += a;
+    }
+    sw[lane] = x;
+  }
+  __syncthreads();
+  const V r = v + (w ? sw[w - 1] : V(0));
+  *tot = sw[31];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kBinThreads) k_bin_scan(const intf_model* __restrict__ models, int n_models_total,
+                                                          intf_replay_buffers B) {
+  __shared__ double sw[32];
+  const int g = blockIdx.x;
+  if (g >= n_models_total) return;
+  const intf_model& M = models[g];
+  if (M.list_cap < kBigList || M.rate_rps == 0.0) return;
+  const BinScratch b = bin_scratch(M, B);
+  double carry = 0.0;
+  for (int base = 0; base < b.n32; base += kBinThreads) {
+    const int c = base + threadIdx.x;
+    const double v = c < b.n32 ? b.S[c] : 0.0;
+    double tot;
+    const double incl = bin_block_incl(v, sw, &tot);
+    if (c < b.n32) b.T[c] = carry + (incl - v);
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kBinWarps) k_bin_classify(const intf_model* __restrict__ models,
+                                                                 int n_models_total, intf_replay_buffers B) {
+  __shared__ double sm[kBinWarps][32][33];
+  const intf_model* M = bin_model(models, n_models_total);
+  if (!M) return;
+  const BinScratch b = bin_scratch(*M, B);
+  const int cb = (blockIdx.x * kBinWarps + (threadIdx.x >> 5)) * 32;
+  if (cb >= b.n32) return;
+  const int c = bin_stage(sm[threadIdx.x >> 5], B.list_t + M->list_off, cb, b.n32);
+  if (c >= b.n32) return;
+  const double T = b.T[c], hi_est = T + b.S[c];
+  const double d = hi_est * 0x1p-40 + 4.0 * M->list_cap * ldexp(1.0, ilogb(hi_est > 0.0 ? hi_est : 1.0) - 52);
+  int cd = -1;
+  long long N = 0;
+  if (c > 0 && T - d > 0.0 && ilogb(T - d) == ilogb(hi_est + d)) {
+    const int e = ilogb(T - d);
+    const double inv = ldexp(1.0, 52 - e);
+    bool ok = true;
+    for (int k = 0; k < kScanChunk; k++) {
+      const double x = sm[threadIdx.x >> 5][threadIdx.x & 31][k] * inv;
+      const double r = rint(x);
+      ok &= x < 0x1p53 && fabs(x - r) != 0.5;
+      N += (long long)r;
+    }
+    if (ok) cd = e + kBinOff;
+  }
+  b.code[c] = cd;
+  b.P[c] = N;
+}
+
+__global__ void __launch_bounds__(kBinThreads) k_bin_runs(const intf_model* __restrict__ models, int n_models_total,
+                                                          intf_replay_buffers B) {
+  __shared__ long long swl[32];
+  __shared__ int swf[32], swi[32];
   __shared__ long long shl[kBinThreads];
   __shared__ int shf[kBinThreads], shc[kBinThreads], shn[kBinThreads];
   const int g = blockIdx.x;
   if (g >= n_models_total) return;
   const intf_model& M = models[g];
   if (M.list_cap < kBigList || M.rate_rps == 0.0) return;
-  const int t = threadIdx.x;
+  const BinScratch b = bin_scratch(M, B);
+  const int n32 = b.n32, t = threadIdx.x, lane = t & 31, w = t >> 5;
   const double* lt = B.list_t + M.list_off;
-  const int cap = M.list_cap, n32 = cap / kScanChunk;
-  double* ends = B.mb_t + M.list_off;  // mb_t is free until formation: ends, then P (int64), then codes
-  long long* P = reinterpret_cast<long long*>(ends + n32);
-  int* code = reinterpret_cast<int*>(ends + 2 * n32);
-  const double horizon = scen[M.scen].duration_s * 1000.0;
-  // 1 + 2: chunk sums, scan, classification.  A warp owns 32 consecutive
-  // chunks (lane l: chunk base + 32 w + l) but reads them coalesced, one
-  // chunk per load (lane = gap), reducing across the lanes.
-  const int lane = t & 31, wbase = t & ~31;
-  double carry = 0.0;
-  for (int base = 0; base < n32; base += kBinThreads) {
-    const int c = base + t;
-    double S = 0.0;
-    for (int j = 0; j < 32; j++) {
-      const int cj = base + wbase + j;
-      double v = cj < n32 ? lt[(long long)cj * kScanChunk + lane] : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == j) S = v;
-    }
-    shd[t] = S;
-    __syncthreads();
-    for (int o = 1; o < kBinThreads; o <<= 1) {
-      const double a = t >= o ? shd[t - o] : 0.0;
-      __syncthreads();
-      shd[t] += a;
-      __syncthreads();
-    }
-    const double T = carry + (shd[t] - S);  // exclusive (estimate)
-    carry += shd[kBinThreads - 1];
-    __syncthreads();
-    // candidate binade of this lane's chunk: [T - d, T + S + d] inside one binade
-    int e = -100000;
-    if (c < n32 && c > 0) {
-      const double hi_est = T + S;
-      const double d = hi_est * 0x1p-40 + 4.0 * cap * ldexp(1.0, ilogb(hi_est > 0.0 ? hi_est : 1.0) - 52);
-      if (T - d > 0.0 && ilogb(T - d) == ilogb(hi_est + d)) e = ilogb(T - d);
-    }
-    // N = sum rint(g / u_e) and the tie test, chunk by chunk across the warp
-    long long N = 0;
-    int cd = -1;
-    for (int j = 0; j < 32; j++) {
-      const int ej = __shfl_sync(0xffffffffu, e, j);
-      const int cj = base + wbase + j;
-      if (ej == -100000 || cj >= n32) continue;  // warp-uniform
-      const double x = lt[(long long)cj * kScanChunk + lane] * ldexp(1.0, 52 - ej);
-      const double r = rint(x);
-      const bool ok = __all_sync(0xffffffffu, x < 0x1p53 && fabs(x - r) != 0.5);
-      long long v = (long long)r;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == j) {
-        N = v;
-        cd = ok ? ej + kBinOff : -1;
-      }
-    }
-    if (c < n32) {
-      code[c] = cd;
-      P[c] = N;
-    }
-  }
-  __syncthreads();
-  // 3: run heads and segmented prefix sums of N
+  // runs: head = clean and (first chunk, or the previous chunk is not of
+  // this run); segmented inclusive prefix sums of N (P, in place); events
+  // (sequential chunks and run heads) compacted in order
   long long run = 0;  // the open run's sum carried across rounds
-  for (int base = 0; base < n32; base += kBinThreads) {
-    const int c = base + t;
-    int cd = -1;
-    long long v = 0;
-    int head = 1;
-    if (c < n32) {
-      cd = code[c];
-      v = P[c];
-      const int prev = c > 0 ? (code[c - 1] & ~kBinHead) : -1;
-      head = cd < 0 || prev != cd;
-    }
-    shl[t] = v;
-    shf[t] = head;
-    __syncthreads();
-    for (int o = 1; o < kBinThreads; o <<= 1) {
-      const long long a = t >= o ? shl[t - o] : 0;
-      const int af = t >= o ? shf[t - o] : 0;
-      __syncthreads();
-      if (!shf[t]) shl[t] += a;
-      shf[t] |= af;
-      __syncthreads();
-    }
-    const long long incl = shf[t] ? shl[t] : run + shl[t];
-    if (c < n32) {
-      P[c] = incl;
-      if (cd >= 0 && head) code[c] = cd | kBinHead;
-    }
-    __syncthreads();
-    run = shf[kBinThreads - 1] ? shl[kBinThreads - 1] : run + shl[kBinThreads - 1];
-    __syncthreads();
-  }
-  // 4: events = sequential chunks and run heads, compacted in order (evpos),
-  // each chunk's event index (evidx = events up to it - 1)
-  int* evidx = code + n32;
-  int* evpos = evidx + n32;
-  double* evT = ends + 4 * n32;  // per event: the exact t at the run start, NAN if the run was walked
   int evbase = 0;
   for (int base = 0; base < n32; base += kBinThreads) {
     const int c = base + t;
-    int f = 0;
+    int cd = -1, head = 1;
+    long long v = 0;
     if (c < n32) {
-      const int cd = code[c];
-      f = cd < 0 || (cd & kBinHead);
+      cd = b.code[c];
+      v = b.P[c];
+      head = cd < 0 || c == 0 || (b.code[c - 1] & ~kBinHead) != cd;  // (the previous round may have set its head bit)
     }
-    shf[t] = f;
+    // warp segmented scan
+    int f = head;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long a = __shfl_up_sync(0xffffffffu, v, o);
+      const int af = __shfl_up_sync(0xffffffffu, f, o);
+      if (lane >= o) {
+        if (!f) v += a;
+        f |= af;
+      }
+    }
+    if (lane == 31) {
+      swl[w] = v;
+      swf[w] = f;
+    }
     __syncthreads();
-    for (int o = 1; o < kBinThreads; o <<= 1) {
-      const int a = t >= o ? shf[t - o] : 0;
-      __syncthreads();
-      shf[t] += a;
-      __syncthreads();
+    if (w == 0) {  // exclusive segmented scan of the warp aggregates, seeded by the carried run
+      long long x = swl[lane];
+      int xf = swf[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long a = __shfl_up_sync(0xffffffffu, x, o);
+        const int af = __shfl_up_sync(0xffffffffu, xf, o);
+        if (lane >= o) {
+          if (!xf) x += a;
+          xf |= af;
+        }
+      }
+      // exclusive: the aggregate before warp `lane`, incl. the carry
+      long long ex = __shfl_up_sync(0xffffffffu, x, 1);
+      int exf = __shfl_up_sync(0xffffffffu, xf, 1);
+      if (lane == 0) ex = 0, exf = 0;
+      swl[lane] = exf ? ex : run + ex;
+      swf[lane] = xf;  // inclusive flag of warps 0..lane (for the next carry)
     }
+    __syncthreads();
+    const long long incl = f ? v : swl[w] + v;
+    // events
+    const int fe = c < n32 && (cd < 0 || head);
+    int etot;
+    const int eincl = bin_block_incl(fe, swi, &etot);
     if (c < n32) {
-      evidx[c] = evbase + shf[t] - 1;
-      if (f) evpos[evbase + shf[t] - 1] = c;
+      b.P[c] = incl;
+      b.evidx[c] = evbase + eincl - 1;
+      if (fe) b.evpos[evbase + eincl - 1] = c;
     }
-    evbase += shf[kBinThreads - 1];
+    // the next round's carry: the last chunk's inclusive value
+    if (t == kBinThreads - 1) shl[0] = incl;
     __syncthreads();
+    run = shl[0];
+    evbase += etot;
+    __syncthreads();
+    if (c < n32 && cd >= 0 && head) b.code[c] = cd | kBinHead;
   }
-  // 5: the walk over events (one thread; each batch of events staged in
-  // shared memory first): a run advances t by its last prefix sum, verified;
-  // a sequential chunk (or a run that fails the verification, chunk by
-  // chunk) takes the real adds
+  __syncthreads();
+  // the walk over events (one thread; each batch of events staged in shared
+  // memory first)
   double tc = 0.0;
   for (int b0 = 0; b0 < evbase; b0 += kBinThreads) {
     const int i = b0 + t;
     if (i < evbase) {
-      const int c = evpos[i], nxt = i + 1 < evbase ? evpos[i + 1] : n32;
+      const int c = b.evpos[i], nxt = i + 1 < evbase ? b.evpos[i + 1] : n32;
       shc[t] = c;
       shn[t] = nxt;
-      shf[t] = code[c];
-      shl[t] = P[nxt - 1];
+      shf[t] = b.code[c];
+      shl[t] = b.P[nxt - 1];
     }
     __syncthreads();
     if (t == 0) {
@@ -881,44 +958,39 @@ __global__ void __launch_bounds__(kBinThreads) k_scan_binade(const intf_scenario
           const int e = (cd & ~kBinHead) - kBinOff;
           const double te = tc + ldexp(1.0, e - 52) * (double)shl[k];
           if (tc >= ldexp(1.0, e) && te < ldexp(1.0, e + 1)) {
-            evT[b0 + k] = tc;
+            b.evT[b0 + k] = tc;
             tc = te;
             walked = false;
           }
         }
         if (walked) {
-          evT[b0 + k] = NAN;
+          b.evT[b0 + k] = NAN;
           for (int cc = shc[k]; cc < shn[k]; cc++) {
             double gv[kScanChunk];
 #pragma unroll
             for (int q = 0; q < kScanChunk; q++) gv[q] = lt[cc * kScanChunk + q];
 #pragma unroll
             for (int q = 0; q < kScanChunk; q++) tc = tc + gv[q];
-            ends[cc] = tc;
+            b.ends[cc] = tc;
           }
         }
       }
     }
     __syncthreads();
   }
-  // 6: the runs' chunk ends in parallel (exact: trun + u P_c, inside the
-  // verified binade), then INF past the first chunk that reaches the horizon
-  __shared__ int first_past;
-  if (t == 0) first_past = n32;
-  __syncthreads();
-  for (int c = t; c < n32; c += kBinThreads) {
-    const int i = evidx[c];
-    const double trun = evT[i];
-    if (!isnan(trun)) {
-      const int e = (code[evpos[i]] & ~kBinHead) - kBinOff;
-      ends[c] = trun + ldexp(1.0, e - 52) * (double)P[c];
-    }
-  }
-  __syncthreads();
-  for (int c = t; c < n32; c += kBinThreads)
-    if (ends[c] >= horizon) atomicMin(&first_past, c);
-  __syncthreads();
-  for (int c = first_past + 1 + t; c < n32; c += kBinThreads) ends[c] = INFINITY;
+}
+
+__global__ void k_bin_fill(const intf_model* __restrict__ models, int n_models_total, intf_replay_buffers B) {
+  const intf_model* M = bin_model(models, n_models_total);
+  if (!M) return;
+  const BinScratch b = bin_scratch(*M, B);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= b.n32) return;
+  const int i = b.evidx[c];
+  const double trun = b.evT[i];
+  if (isnan(trun)) return;  // walked: already exact
+  const int e = (b.code[b.evpos[i]] & ~kBinHead) - kBinOff;
+  b.ends[c] = trun + ldexp(1.0, e - 52) * (double)b.P[c];
 }
 
 __global__ void __launch_bounds__(kBigThreads) k_jobs_plan_big(const intf_scenario* __restrict__ scen,
@@ -1731,8 +1803,14 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
     k_scan_gaps<<<bt->n_models, 32, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
     if ((rc = launch_status("k_scan_gaps"))) return rc;
 #else
-    k_scan_binade<<<bt->n_models, kBinThreads, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
-    if ((rc = launch_status("k_scan_binade"))) return rc;
+    const dim3 cgrid(ceil_div(ceil_div(bt->max_list_cap, kScanChunk), 32 * kBinWarps), y, ceil_div(m, y));
+    k_bin_sums<<<cgrid, 32 * kBinWarps, 0, st>>>(bt->models, bt->n_models, *buf);
+    k_bin_scan<<<bt->n_models, kBinThreads, 0, st>>>(bt->models, bt->n_models, *buf);
+    k_bin_classify<<<cgrid, 32 * kBinWarps, 0, st>>>(bt->models, bt->n_models, *buf);
+    k_bin_runs<<<bt->n_models, kBinThreads, 0, st>>>(bt->models, bt->n_models, *buf);
+    k_bin_fill<<<dim3(ceil_div(ceil_div(bt->max_list_cap, kScanChunk), 128), y, ceil_div(m, y)), 128, 0, st>>>(
+        bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_bin_*"))) return rc;
 #endif
     k_fill_gaps<<<dim3(ceil_div(ceil_div(bt->max_list_cap, kScanChunk), 128), y, ceil_div(m, y)), 128, 0, st>>>(
         bt->scen, bt->models, bt->n_models, *buf);

@@ -1,5 +1,5 @@
 """Experiment (tools/): the C4 arrivals stage alone -- k_gen_gaps, the
-cumulative-sum kernel (k_scan_binade, or k_scan_gaps when built with
+cumulative-sum kernels (k_bin_*, or k_scan_gaps when built with
 INTF_SCAN_SEQ=1), k_fill_gaps -- timed with events, plus the binade scan's
 chunk classes per long model (clean / sequential / run heads)."""
 import ctypes
@@ -36,7 +36,7 @@ for g in range(pipe.pb.n_models):
         continue
     n32 = cap // 32
     seg = mb[m.list_off: m.list_off + cap]
-    code = seg[2 * n32: 2 * n32 + (n32 + 1) // 2].view(np.int32)[:n32]
+    code = seg[4 * n32: 4 * n32 + (n32 + 1) // 2].view(np.int32)[:n32]
     clean = code >= 0
     heads = (code >= 0) & ((code & (1 << 20)) != 0)
     print(f"model {g}: cap {cap} chunks {n32} clean {clean.sum()} sequential {(~clean).sum()} runs {heads.sum()}")
