@@ -513,12 +513,18 @@ def product_arm(a):
     specs.sort(key=lambda d: -sum(m["arrival_rate_rps"] for m in d["deployed"]) * d["duration_s"])
     preds = [_abi.Predictor(ewma=0, alpha=1.0, w=tuple(W[-1, 0])), _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[-1, 1])),
              _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[0, 1]))]
-    pipe = engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5)
+    # two pipelines (double-buffered sweeps) on two streams: consecutive steps
+    # overlap, so one sweep's arrivals / formation / SLO run beside the other
+    # sweep's replay tail (the replay is bounded by its longest scenario's chain)
+    n_pipes = int(os.environ.get("INTF_BENCH_PIPES", "2"))
+    pipes = [engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5) for _ in range(n_pipes)]
+    pipe = pipes[0]
     for _ in range(max(1, a.warmup)):
-        pipe.run()
+        for p in pipes:
+            p.run()
     barrier()
     st = pipe.status()
-    r_steps = max(1, min(a.steps, 5))
+    r_steps = max(n_pipes, min(a.steps, 3 * n_pipes))
     # per-scenario SLO metrics of every rank gathered (NCCL all_gather, N > 1):
     # per deployed model n, met, p50/p95/p99, padded to the largest rank
     n_mod = pipe.pb.n_models
@@ -527,12 +533,13 @@ def product_arm(a):
         t = torch.tensor([n_mod], device="cuda" if a.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         gather_len = int(t.item())
-    rows = torch.zeros(gather_len, 5, dtype=torch.float64, device="cuda")
-    parts = [torch.empty_like(rows) for _ in range(world)] if dist is not None else None
+    rows_k = [torch.zeros(gather_len, 5, dtype=torch.float64, device="cuda") for _ in pipes]
+    parts_k = [[torch.empty_like(r) for _ in range(world)] for r in rows_k] if dist is not None else None
 
-    def gather_metrics():
+    def gather_metrics(k=0):
         if dist is None:
             return
+        pipe, rows, parts = pipes[k], rows_k[k], parts_k[k]
         rows[:n_mod, 0] = pipe.slo_n[:n_mod]
         rows[:n_mod, 1] = pipe.slo_met[:n_mod]
         rows[:n_mod, 2:] = pipe.slo_p[: 3 * n_mod].view(n_mod, 3)
@@ -547,10 +554,16 @@ def product_arm(a):
     # one warp replays each scenario start to end (C5 scenarios are short:
     # busy-period sharding pays only for long traces, see long_trace)
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rstreams = [torch.cuda.Stream() for _ in pipes]
     r0.record(stream)
-    for _ in range(r_steps):
-        pipe.run()
-        gather_metrics()
+    for rs in rstreams:
+        rs.wait_stream(stream)
+    for k in range(r_steps):
+        with torch.cuda.stream(rstreams[k % n_pipes]):
+            pipes[k % n_pipes].run()
+            gather_metrics(k % n_pipes)
+    for rs in rstreams:
+        stream.wait_stream(rs)
     r1.record(stream)
     barrier()
     rep_ms = max_over_ranks(r0.elapsed_time(r1)) / r_steps
@@ -625,7 +638,10 @@ def product_arm(a):
                    "requests": n_req, "batches": n_batches, "status_nonzero": int(np.count_nonzero(st)),
                    "workload": "C5-shape synthetic scenarios (default_rng([2512,i]), 1 s, cap 1-3): arrivals + "
                                "formation + noise + replay (warp per scenario) + SLO + features/3 predictors; N > 1: "
-                               "+ all_gather of every rank's per-model SLO metrics each step",
+                               "+ all_gather of every rank's per-model SLO metrics each step; consecutive steps "
+                               "double-buffered on two streams (two pipelines), so a step's arrivals/formation/SLO "
+                               "overlap the previous step's replay tail",
+                   "steps_timed": r_steps,
                    "stage_ms": stage_ms, "cpu_baseline": replay_cpu},
         "refit": refit,
         "long_trace": longtrace,
