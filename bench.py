@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 N_DEC = 32
 CAP = 4
 ALPHA = 0.5
+C4_PASSES = 4  # replay + verify passes queued per long trace (3 needed at slow 2.0, min_len 64)
 REPLAY_SCEN = 10000  # BASELINE configs[4]: a sweep of 10^4 synthetic scenarios (per GPU)
 METRIC = "candidate co-location predictions/sec and scenario replays/sec at 1/2/4/8 B200"
 
@@ -286,9 +287,10 @@ C4_REQUESTS = 1e6
 def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     """C4 shape: one 10^6-request, 16-model (bs <= 64, cap 4) trace replayed
     with busy-period sharding (speculative idle boundaries planned, verified
-    and merged on the device; the host reads the todo-list size between
-    launches, inside the timed region).  Each rank replays its own trace
-    (weak scaling)."""
+    and merged on the device; C4_PASSES passes queued with device-side job
+    counts, one host read per trace, inside the timed region).  Each rank
+    replays its own trace (weak scaling).  Also: back-to-back traces on two
+    streams (`pipelined`)."""
     import torch
     from paper_2512_18725_b200 import engine
     from paper_2512_18725_b200.sweep import c4_scenario, table16
@@ -296,17 +298,45 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     t16, arch = table16()
     spec = c4_scenario(t16, arch, n_requests=C4_REQUESTS, seed=1 + rank)
     ta = t16.arrays()
-    pipe = engine.ReplayPipeline([spec], ta, scale=1.2)
-    engine.replay_segmented(pipe)  # warm-up (also sizes the job scratch); default slow 2.0, min_len 64
+    pipes = [engine.ReplayPipeline([spec], ta, scale=1.2) for _ in range(2)]
+    for p in pipes:  # warm-up (also sizes the job scratch); default slow 2.0, min_len 64
+        engine.replay_segmented(p, passes=C4_PASSES)
+    pipe = pipes[0]
     barrier()
+    # one trace: C4_PASSES replay + verify passes queued with device-side job
+    # counts, one host read at the end (more passes if ever needed)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    stats = engine.replay_segmented(pipe)
+    stats = engine.replay_segmented(pipe, passes=C4_PASSES)
     e1.record(stream)
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     n_req = int(pipe.t["n_req"][0].item())
     st = int(pipe.t["status"][0].item())
+    # back-to-back traces double-buffered on two streams (each trace fully
+    # stream-ordered: its low-parallelism phases overlap the other's work);
+    # every trace's pending-job count is kept and checked after the timing
+    K = 6
+    rstreams = [torch.cuda.Stream() for _ in pipes]
+    pending = torch.zeros(K, dtype=torch.int32, device="cuda")
+    fins = []
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    p0.record(stream)
+    for rs in rstreams:
+        rs.wait_stream(stream)
+    for k in range(K):
+        with torch.cuda.stream(rstreams[k & 1]):
+            fins.append(engine.replay_segmented(pipes[k & 1], passes=C4_PASSES, stats=False))
+            pending[k:k + 1].copy_(pipes[k & 1]._jobs.t["todo_count"])
+    for rs in rstreams:
+        stream.wait_stream(rs)
+    p1.record(stream)
+    barrier()
+    pms = max_over_ranks(p0.elapsed_time(p1)) / K
+    complete = int(pending.sum().item()) == 0 and all(int(p.t["status"][0].item()) == 0 for p in pipes)
+    for f in fins[-2:]:
+        f()
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         # the oracle's C heap-engine replay of the same trace (+ its arrivals), one core, once
@@ -320,6 +350,8 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
                          f"in {dt:.2f} s"}
     return {"metric": "requests replayed/sec (single long trace)", "value": world * n_req / (ms / 1e3),
             "unit": "requests/s", "ms_per_trace": ms, "requests": n_req, "status": st, **stats,
+            "pipelined": {"value": world * n_req / (pms / 1e3), "unit": "requests/s", "ms_per_trace": pms,
+                          "traces": K, "streams": 2, "complete": complete},
             "cpu_baseline": cpu,
             "workload": "C4: 16 models (6 default + 10 rng(123) archetypes), bs 1-64, cap 4, window U(10,20) ms, "
                         "sigma 0.05, total rho 0.5 at bs 64; one trace per GPU; arrivals + formation + noise + "

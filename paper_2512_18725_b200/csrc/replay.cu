@@ -1306,21 +1306,25 @@ __global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_jobs_re
                                                                     intf_jobs J, int n_todo) {
   __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
   const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
-  const int k = blockIdx.x * kReplayWarps * (32 / kReplayW) + g;
-  if (k >= n_todo) return;
-  const int slot = J.todo[k];
-  const int s = J.slot_scen[slot];
-  const intf_scenario& S = scen[s];
-  const int per = 2 * S.cap - 1;
-  const int jlo = J.lo[slot], jhi = J.hi[slot];
-  const ReplayJob RJ{s, jlo, jhi, S.seg_off + jlo * per, (jhi - jlo) * per, k};
-  const ReplayJobOut r = replay_group<kReplayW>(RJ, scen, models, tab, B, sseg[g], 0);
-  if ((threadIdx.x & (kReplayW - 1)) == 0) {
-    J.info[3 * slot] = r.status;
-    J.info[3 * slot + 1] = r.n_segments;
-    J.info[3 * slot + 2] = r.n_reseats;
-    J.last[slot] = r.last_done;
-    J.dirty[slot] = 0;
+  // n_todo < 0: the count is the device's (*J.todo_count, set by the plan /
+  // the last verify), so passes can be queued without a host round trip
+  const int n = n_todo >= 0 ? n_todo : *J.todo_count;
+  const int stride = gridDim.x * kReplayWarps * (32 / kReplayW);
+  for (int k = blockIdx.x * kReplayWarps * (32 / kReplayW) + g; k < n; k += stride) {
+    const int slot = J.todo[k];
+    const int s = J.slot_scen[slot];
+    const intf_scenario& S = scen[s];
+    const int per = 2 * S.cap - 1;
+    const int jlo = J.lo[slot], jhi = J.hi[slot];
+    const ReplayJob RJ{s, jlo, jhi, S.seg_off + jlo * per, (jhi - jlo) * per, k};
+    const ReplayJobOut r = replay_group<kReplayW>(RJ, scen, models, tab, B, sseg[g], 0);
+    if ((threadIdx.x & (kReplayW - 1)) == 0) {
+      J.info[3 * slot] = r.status;
+      J.info[3 * slot + 1] = r.n_segments;
+      J.info[3 * slot + 2] = r.n_reseats;
+      J.last[slot] = r.last_done;
+      J.dirty[slot] = 0;
+    }
   }
 }
 
@@ -1883,12 +1887,16 @@ int intf_jobs_plan(const intf_batch* bt, const intf_table* table, const intf_rep
 
 int intf_jobs_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
                      const intf_jobs* jobs, int32_t n_todo, void* stream) {
-  if (!bt || !bt->scen || !table || !buf || !jobs || n_todo < 0) return bad_input("intf_jobs_replay: bad argument");
+  if (!bt || !bt->scen || !table || !buf || !jobs || (n_todo < 0 && !jobs->todo_count))
+    return bad_input("intf_jobs_replay: bad argument");
   if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1)
     return bad_input("intf_jobs_replay: cap_max must be in [1, 8], seg_stride >= 1");
   if (n_todo == 0) return INTF_OK;
-  k_jobs_replay<<<ceil_div(n_todo, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, as_stream(stream)>>>(
-      bt->scen, bt->models, *table, *buf, *jobs, n_todo);
+  // n_todo < 0: up to -n_todo jobs, the count read on the device; a grid of
+  // at most one wave, its warps striding over the todo list
+  const long long want = ceil_div(n_todo > 0 ? n_todo : -(long long)n_todo, kReplayWarps * (32 / kReplayW));
+  const unsigned grid = n_todo > 0 ? (unsigned)want : (unsigned)(want < 148 * INTF_REPLAY_MINB ? want : 148 * INTF_REPLAY_MINB);
+  k_jobs_replay<<<grid, 32 * kReplayWarps, 0, as_stream(stream)>>>(bt->scen, bt->models, *table, *buf, *jobs, n_todo);
   return launch_status("k_jobs_replay");
 }
 

@@ -808,12 +808,18 @@ class _DeviceJobs:
 
 
 def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 64, max_iters: int = 100000,
-                     arrivals: bool = True, slo: bool = True, features: bool = True) -> dict:
+                     arrivals: bool = True, slo: bool = True, features: bool = True, passes: int = 0,
+                     stats: bool = True) -> dict:
     """Busy-period sharding, planned and verified on the device:
     speculative idle boundaries (k_jobs_plan), parallel job replay
     (k_jobs_replay), boundary verification and merging (k_jobs_verify),
-    repeated until every boundary holds.  The host only reads the size of the
-    todo list between launches.  Bit-identical to the serial replay."""
+    repeated until every boundary holds.  Bit-identical to the serial replay.
+    passes > 0: that many replay + verify passes are queued with the job
+    count read ON THE DEVICE (no host round trip; spare passes find an empty
+    todo list), then the host checks the count once and continues if needed.
+    passes = 0: the host reads the todo-list size between launches.
+    stats=False skips the statistics' host reads (nothing left to sync on:
+    the whole call is stream-ordered)."""
     L, st = pipe.lib, stream_ptr()
     bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
     jobs = getattr(pipe, "_jobs", None)
@@ -829,7 +835,40 @@ def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 6
     tab = ctypes.byref(pipe.dtable.struct)
     _abi.check(L.intf_jobs_plan(bt, tab, B, J, st), "intf_jobs_plan")
     iters, first = 0, None
-    for iters in range(1, max_iters + 1):
+    if passes > 0:
+        total = int(jobs.J.total_slots)
+        need = total * pipe.pb.cap_max * pipe.seg_stride * 5
+        if pipe.t["slot_seg"].numel() < need:
+            pipe.t["slot_seg"] = torch.zeros(need, dtype=torch.float64, device=pipe.dev)
+            pipe.B.slot_seg = pipe.t["slot_seg"].data_ptr()
+        if stats:
+            jobs.t["n_jobs0"] = jobs.t["n_jobs"].clone()
+        for _ in range(passes):
+            _abi.check(L.intf_jobs_replay(bt, tab, B, J, -total, st), "intf_jobs_replay")
+            _abi.check(L.intf_jobs_verify(bt, B, J, st), "intf_jobs_verify")
+        iters = passes
+        if not stats:
+            # deferred: SLO / features queued now; finish() (one host read)
+            # checks that the passes sufficed, else completes and redoes them
+            pipe.run_slo_features(slo=slo, features=features)
+
+            def finish() -> dict:
+                if int(jobs.t["todo_count"].item()) == 0:
+                    return {"iterations": passes}
+                return replay_segmented_continue(pipe, jobs, passes, max_iters, slo, features, None)
+
+            return finish
+        first = int(jobs.t["n_jobs0"].sum().item())
+    return replay_segmented_continue(pipe, jobs, iters, max_iters, slo, features, first)
+
+
+def replay_segmented_continue(pipe, jobs, iters, max_iters, slo, features, first) -> dict:
+    """The host-driven tail of replay_segmented: read the todo-list size,
+    replay and verify until it is empty, then SLO / features."""
+    L, st = pipe.lib, stream_ptr()
+    bt, B, J = ctypes.byref(pipe.batch), ctypes.byref(pipe.B), ctypes.byref(jobs.J)
+    tab = ctypes.byref(pipe.dtable.struct)
+    for iters in range(iters + 1, max_iters + 1):
         n = int(jobs.t["todo_count"].item())
         if first is None:
             first = n

@@ -29,20 +29,29 @@ def test_segmented_replay_matches_goldens(slow, min_len):
         assert stats["jobs_final"] <= stats["jobs_initial"]
 
 
-@pytest.mark.parametrize("slow,min_len", [(2.0, 16), (0.5, 4), (0.0, 1)])
-def test_long_trace_segmented_equals_serial(slow, min_len):
+@pytest.mark.parametrize("slow,min_len,passes", [(2.0, 16, 0), (0.5, 4, 0), (0.0, 1, 0), (2.0, 64, 4), (2.0, 64, 1),
+                                                 (0.5, 4, -3)])
+def test_long_trace_segmented_equals_serial(slow, min_len, passes):
     """A 2x10^5-request trace (req_cap >= 32768: block-parallel plan/verify,
     long-list arrivals) replayed as busy-period jobs -- also with most
     speculative boundaries failing (slow 0.5 / 0.0: long runs of merges) --
-    equals the whole-trace replay and the CPU oracle."""
+    equals the whole-trace replay and the CPU oracle.  passes > 0: passes
+    queued with device-side job counts (1: too few, the host loop finishes);
+    passes < 0: the same, deferred (finish() after the queued SLO)."""
     from paper_2512_18725_b200 import engine
     from paper_2512_18725_b200.sweep import c4_scenario, table16
 
     t16, arch = table16()
     spec = c4_scenario(t16, arch, n_requests=2e5)
     ta = t16.arrays()
-    pipe, h, stats = _run([spec], ta, slow=slow, min_len=min_len)
-    assert stats["jobs_final"] > 10, stats  # the trace really was replayed in parallel pieces
+    if passes >= 0:
+        pipe, h, stats = _run([spec], ta, slow=slow, min_len=min_len, passes=passes)
+        assert stats["jobs_final"] > 10, stats  # the trace really was replayed in parallel pieces
+    else:
+        pipe = engine.ReplayPipeline([spec], ta, scale=1.5)
+        fin = engine.replay_segmented(pipe, slow=slow, min_len=min_len, passes=-passes, stats=False)
+        fin()
+        h = pipe.fetch()
     ser, hs = engine.run_batch([spec], ta)
     a, b = pipe.scenario(h, 0), ser.scenario(hs, 0)
     assert a["status"] == 0 and b["status"] == 0
