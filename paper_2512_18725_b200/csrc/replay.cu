@@ -1563,6 +1563,27 @@ constexpr int kSloWsLeft = kSloWsPrefix + kMaxModels * 3 * 2;
 constexpr int kSloWsInts = kSloWsLeft + kMaxModels * 3 * 2;
 static_assert(kSloWsInts == INTF_SLO_WS_INTS, "slo_ws size mismatch with the header");
 
+// per-request latency keys + model codes for the radix passes of a long
+// trace, in the scenario's arrival-list buffers (list_t / list_rid: free once
+// the batches are formed); cap = the scenario's list capacity (>= n_req
+// unless the lists overflowed -- then the passes gather as before)
+constexpr int kSloWarm = 0x100;  // code bit: arrival at or after the warm-up cutoff
+struct SloKeys {
+  unsigned long long* key;
+  int32_t* code;
+  long long cap;
+};
+__device__ __forceinline__ SloKeys slo_keys(const intf_scenario& S, const intf_model* __restrict__ models,
+                                            const intf_replay_buffers& B) {
+  const intf_model& f = models[S.model_off];
+  const intf_model& l = models[S.model_off + S.n_models - 1];
+  SloKeys K;
+  K.key = reinterpret_cast<unsigned long long*>(B.list_t + f.list_off);
+  K.code = B.list_rid + f.list_off;
+  K.cap = (long long)l.list_off + l.list_cap - f.list_off;
+  return K;
+}
+
 __global__ void k_slo_big_count(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
                                 intf_replay_buffers B, int s, const double* __restrict__ warm_cutoff,
                                 int32_t* __restrict__ ws) {
@@ -1574,12 +1595,18 @@ __global__ void k_slo_big_count(const intf_scenario* __restrict__ scen, const in
   const intf_scenario& S = scen[s];
   const int n = B.n_req[s], ro = S.req_off;
   const double cutoff = warm_cutoff ? warm_cutoff[s] : -INFINITY;
+  const SloKeys K = slo_keys(S, models, B);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int b = B.r_batch[ro + i];
     const double at = B.arr_t[ro + i];
     const int m = B.arr_model[ro + i];
-    const bool met = (B.b_completion[ro + b] - at) <= models[S.model_off + m].slo_ms;
+    const double lat = B.b_completion[ro + b] - at;
+    const bool met = lat <= models[S.model_off + m].slo_ms;
     B.r_slo_met[ro + i] = met;
+    if (i < K.cap) {  // the radix passes stream these instead of gathering again
+      K.key[i] = lat_key(lat);
+      K.code[i] = m | (at >= cutoff ? kSloWarm : 0);
+    }
     atomicAdd(&cnt[64 + 2 * m], 1);
     if (met) atomicAdd(&cnt[64 + 2 * m + 1], 1);
     if (at >= cutoff) {
@@ -1622,8 +1649,9 @@ __global__ void k_slo_big_init(const intf_scenario* __restrict__ scen, int s, in
   for (int t = threadIdx.x; t < kMaxModels * 3 * 256; t += blockDim.x) ws[kSloWsHist + t] = 0;
 }
 
-__global__ void k_slo_big_hist(const intf_scenario* __restrict__ scen, intf_replay_buffers B, int s, int pass,
-                               const double* __restrict__ warm_cutoff, int32_t* __restrict__ ws) {
+__global__ void k_slo_big_hist(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                               intf_replay_buffers B, int s, int pass, const double* __restrict__ warm_cutoff,
+                               int32_t* __restrict__ ws) {
   const intf_scenario& S = scen[s];
   const int n = B.n_req[s], ro = S.req_off;
   const double cutoff = (warm_cutoff && !ws[128]) ? warm_cutoff[s] : -INFINITY;
@@ -1634,14 +1662,28 @@ __global__ void k_slo_big_hist(const intf_scenario* __restrict__ scen, intf_repl
   // bytes, so most lanes of a warp hit the same bin (one atomic per distinct bin)
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const SloKeys K = slo_keys(S, models, B);
+  const bool staged = n <= K.cap;
+  const bool all = !(warm_cutoff && !ws[128]);
   for (long long i0 = start - (threadIdx.x & 31); i0 < n; i0 += stride) {
     const long long i = i0 + (threadIdx.x & 31);
     int bins[3] = {-1, -1, -1};
     if (i < n) {
-      const double at = B.arr_t[ro + i];
-      if (at >= cutoff) {
-        const int m = B.arr_model[ro + i];
-        const unsigned long long key = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
+      int m;
+      unsigned long long key;
+      bool in;
+      if (staged) {
+        const int c = K.code[i];
+        m = c & (kSloWarm - 1);
+        in = all || (c & kSloWarm);
+        key = K.key[i];
+      } else {
+        const double at = B.arr_t[ro + i];
+        in = at >= cutoff;
+        m = B.arr_model[ro + i];
+        key = in ? lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at) : 0ull;
+      }
+      if (in) {
         const unsigned d = (unsigned)(key >> shift) & 0xffu;
 #pragma unroll
         for (int q = 0; q < 3; q++)
@@ -1663,23 +1705,45 @@ __global__ void k_slo_big_select(const intf_scenario* __restrict__ scen, int s, 
   unsigned long long* prefix = reinterpret_cast<unsigned long long*>(ws + kSloWsPrefix);
   long long* left = reinterpret_cast<long long*>(ws + kSloWsLeft);
   unsigned int* hist = reinterpret_cast<unsigned int*>(ws + kSloWsHist);
-  for (int t = threadIdx.x; t < S.n_models * 3; t += blockDim.x) {
-    long long l = left[t];
-    unsigned d = 0;
-    for (; d < 255u; d++) {
-      if (l < (long long)hist[t * 256 + d]) break;
-      l -= hist[t * 256 + d];
+  // warp per target (model, percentile): lane owns bins [8 lane, 8 lane + 8);
+  // the digit is the first bin whose running count passes `left`
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < S.n_models * 3; t += blockDim.x >> 5) {
+    unsigned h[8];
+    long long own = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      h[k] = hist[t * 256 + 8 * lane + k];
+      own += h[k];
+      hist[t * 256 + 8 * lane + k] = 0;  // cleared for the next pass
     }
-    left[t] = l;
-    prefix[t] |= (unsigned long long)d << shift;
-    if (pass == 7) {
-      const int m = t / 3;
-      const int nm = ws[(ws[128] ? 64 : 0) + 2 * m];
-      out_p[3 * (S.model_off + m) + t % 3] = nm ? key_lat(prefix[t]) : NAN;
+    long long incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long a = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += a;
+    }
+    const long long l = left[t];
+    // the first lane whose inclusive count exceeds l holds the digit (lane 31 if none: digit 255)
+    const unsigned hit = __ballot_sync(0xffffffffu, incl > l);
+    const int src = hit ? __ffs(hit) - 1 : 31;
+    if (lane == src) {
+      long long r = l - (incl - own);
+      unsigned d = 8u * lane;
+      int k = 0;
+      for (; k < 7; k++, d++) {
+        if (r < (long long)h[k]) break;
+        r -= h[k];
+      }
+      left[t] = r;
+      prefix[t] |= (unsigned long long)d << shift;
+      if (pass == 7) {
+        const int m = t / 3;
+        const int nm = ws[(ws[128] ? 64 : 0) + 2 * m];
+        out_p[3 * (S.model_off + m) + t % 3] = nm ? key_lat(prefix[t]) : NAN;
+      }
     }
   }
-  __syncthreads();
-  for (int t = threadIdx.x; t < kMaxModels * 3 * 256; t += blockDim.x) ws[kSloWsHist + t] = 0;
 }
 
 // ---- K4+K5: features + predictions per outcome; grid (chunks, scenarios).
@@ -1955,8 +2019,8 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
       k_slo_big_init<<<1, 256, 0, st>>>(bt->scen, s, buf->slo_ws, out_n, out_met);
       if ((rc = launch_status("k_slo_big_init"))) return rc;
       for (int pass = 0; pass < 8; pass++) {
-        k_slo_big_hist<<<4 * 148, 256, 0, st>>>(bt->scen, *buf, s, pass, warm_cutoff, buf->slo_ws);
-        k_slo_big_select<<<1, 128, 0, st>>>(bt->scen, s, pass, buf->slo_ws, out_p);
+        k_slo_big_hist<<<4 * 148, 256, 0, st>>>(bt->scen, bt->models, *buf, s, pass, warm_cutoff, buf->slo_ws);
+        k_slo_big_select<<<1, 1024, 0, st>>>(bt->scen, s, pass, buf->slo_ws, out_p);
       }
       if ((rc = launch_status("k_slo_big_select"))) return rc;
     }

@@ -19,7 +19,7 @@ for K in k_cand_step k_replay_warp k_form_models k_merge_batches k_noise_table k
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_${TAG}_$K \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_${TAG}_$K.log 2>&1
 done
-for K in k_scan_gaps k_gen_gaps k_form_double k_jobs_replay k_plan_p3 k_slo_big_hist; do
+for K in k_bin_runs k_bin_classify k_gen_gaps k_form_double k_jobs_replay k_jobs_verify_big k_slo_big_hist; do
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_${TAG}_$K \
     python tools/c4_breakdown.py > $OUT/ncu_${TAG}_$K.log 2>&1
 done
@@ -28,6 +28,6 @@ done
 python tools/ncu_summary.py $TAG $OUT/prof_${TAG}_*.ncu-rep --launches $OUT/launches_$TAG.csv > $OUT/summary_$TAG.log 2>&1
 cp profiles/ncu_$TAG.md profiles/ncu_summary.json $OUT/ 2>/dev/null
 
-find $OUT -name "prof_${TAG}_*.ncu-rep" ! -name "prof_${TAG}_k_cand_step.ncu-rep" ! -name "prof_${TAG}_k_replay_warp.ncu-rep" ! -name "prof_${TAG}_k_scan_gaps.ncu-rep" -delete
+find $OUT -name "prof_${TAG}_*.ncu-rep" ! -name "prof_${TAG}_k_cand_step.ncu-rep" ! -name "prof_${TAG}_k_replay_warp.ncu-rep" ! -name "prof_${TAG}_k_bin_runs.ncu-rep" ! -name "prof_${TAG}_k_ols_windows_tma.ncu-rep" -delete
 du -sh $OUT
 echo done
