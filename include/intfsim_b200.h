@@ -88,7 +88,12 @@ typedef struct intf_batch {
   int32_t max_models;          /* max over scenarios of n_models */
   int32_t max_list_cap;        /* max over deployed models of list_cap */
   int32_t req_slots;           /* sum over scenarios of req_cap (packed request / batch slot space) */
+  const int32_t *long_blocks;  /* optional device [2 * n_long_blocks]: (model, chunk) of every 256-entry
+                                  chunk of every list with list_cap >= INTF_LONG_LIST, so the long-list
+                                  formation launches flat grids (NULL: grids of max_list_cap x models) */
+  int32_t n_long_blocks, pad_;
 } intf_batch;
+#define INTF_LONG_LIST 4096 /* model lists this long form batches by pointer doubling */
 
 #define INTF_SLO_WS_INTS (256 + 32 * 3 * 256 + 32 * 3 * 4)
 

@@ -47,7 +47,10 @@ class Model(ctypes.Structure):
 class Batch(ctypes.Structure):
     _fields_ = [("scen", P), ("models", P), ("n_scen", c_int32), ("n_models", c_int32),
                 ("max_req_cap", c_int32), ("max_models", c_int32), ("max_list_cap", c_int32),
-                ("req_slots", c_int32)]
+                ("req_slots", c_int32), ("long_blocks", P), ("n_long_blocks", c_int32), ("pad_", c_int32)]
+
+
+LONG_LIST = 4096  # INTF_LONG_LIST
 
 
 REPLAY_BUFFER_FIELDS = [

@@ -24,7 +24,7 @@ namespace {
 #define INTF_BIG_LIST 4096
 #endif
 constexpr int kBigList = INTF_BIG_LIST;  // model lists this long: parallel gaps + one-thread scan (long traces)
-constexpr int kLongForm = 4096;         // model lists this long: pointer-doubling batch formation
+constexpr int kLongForm = INTF_LONG_LIST;  // model lists this long: pointer-doubling batch formation
 constexpr int kBigJobs = 1 << 15;  // scenarios this long: block-parallel job plan / verify
 constexpr int kGapRun = 8;      // consecutive draws per thread in k_gen_gaps
 
@@ -275,14 +275,14 @@ __device__ __forceinline__ int form_cnt(const double* lt, int n, int h, double w
   return lo - h;
 }
 
-struct LongModel {  // model g of a long-list launch (grid.y/z = model, grid.x = list chunk)
-  int g, n, i;
+struct LongModel {  // model g of a long-list launch (grid.y/z = model, grid.x = list chunk;
+  int g, n, i;       // or a flat grid over bt->long_blocks: block b = (model, chunk) pair b)
   bool ok;
 };
 __device__ __forceinline__ LongModel long_model(const intf_scenario* scen, const intf_model* models, int n_models,
-                                                const intf_replay_buffers& B) {
+                                                const intf_replay_buffers& B, const int32_t* blk = nullptr) {
   LongModel r;
-  r.g = blockIdx.z * gridDim.y + blockIdx.y;
+  r.g = blk ? blk[2 * blockIdx.x] : blockIdx.z * gridDim.y + blockIdx.y;
   r.ok = false;
   if (r.g >= n_models) return r;
   const intf_model& M = models[r.g];
@@ -292,15 +292,15 @@ __device__ __forceinline__ LongModel long_model(const intf_scenario* scen, const
       S.n_models > kMaxModels)
     return r;
   r.n = min(B.n_list[r.g], M.list_cap);
-  r.i = blockIdx.x * blockDim.x + threadIdx.x;
+  r.i = (blk ? blk[2 * blockIdx.x + 1] : blockIdx.x) * blockDim.x + threadIdx.x;
   r.ok = true;
   return r;
 }
 
 // J_0 = nxt into table 0; path[0] = 0
 __global__ void k_form_nxt(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                           int n_models, intf_replay_buffers B) {
-  const LongModel L = long_model(scen, models, n_models, B);
+                           int n_models, intf_replay_buffers B, const int32_t* blk) {
+  const LongModel L = long_model(scen, models, n_models, B, blk);
   if (!L.ok || L.i >= L.n) return;
   const intf_model& M = models[L.g];
   const intf_scenario& S = scen[M.scen];
@@ -325,8 +325,8 @@ __global__ void k_form_extend(const intf_scenario* __restrict__ scen, const intf
   }
 }
 __global__ void k_form_double(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                              int n_models, intf_replay_buffers B, int k) {
-  const LongModel L = long_model(scen, models, n_models, B);
+                              int n_models, intf_replay_buffers B, int k, const int32_t* blk) {
+  const LongModel L = long_model(scen, models, n_models, B, blk);
   if (!L.ok || L.i >= L.n) return;
   const intf_model& M = models[L.g];
   int32_t* ws = B.form_ws + 3ll * M.list_off;
@@ -338,12 +338,13 @@ __global__ void k_form_double(const intf_scenario* __restrict__ scen, const intf
 
 // batch r of the model: head path[r] (while < n); writes what form_model_warp writes
 __global__ void k_form_emit(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                            int n_models, intf_replay_buffers B) {
-  const LongModel L = long_model(scen, models, n_models, B);
+                            int n_models, intf_replay_buffers B, const int32_t* blk) {
+  const LongModel L = long_model(scen, models, n_models, B, blk);
   if (!L.ok) {
     // long models of bad scenarios form nothing
-    const int g = blockIdx.z * gridDim.y + blockIdx.y;
-    if (g < n_models && models[g].list_cap >= kLongForm && blockIdx.x == 0 && threadIdx.x == 0) B.n_mb[g] = 0;
+    const int g = blk ? blk[2 * blockIdx.x] : blockIdx.z * gridDim.y + blockIdx.y;
+    const int chunk = blk ? blk[2 * blockIdx.x + 1] : blockIdx.x;
+    if (g < n_models && models[g].list_cap >= kLongForm && chunk == 0 && threadIdx.x == 0) B.n_mb[g] = 0;
     return;
   }
   if (L.n == 0) {
@@ -1830,18 +1831,20 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
   if (bt->max_list_cap >= kLongForm) {  // long model lists: pointer-doubling formation
     if (!buf->form_ws) return bad_input("formation of long lists needs form_ws scratch");
     const unsigned m = (unsigned)bt->n_models, y = m < 65535u ? m : 65535u;
-    const dim3 grid(ceil_div(bt->max_list_cap, 256), y, ceil_div(m, y));
-    k_form_nxt<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    // flat grid over the long lists' 256-entry chunks when the caller gave the map
+    const int32_t* blk = bt->long_blocks && bt->n_long_blocks > 0 ? bt->long_blocks : nullptr;
+    const dim3 grid = blk ? dim3((unsigned)bt->n_long_blocks) : dim3(ceil_div(bt->max_list_cap, 256), y, ceil_div(m, y));
+    k_form_nxt<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, blk);
     if ((rc = launch_status("k_form_nxt"))) return rc;
     for (int k = 0; (1ll << k) < bt->max_list_cap; k++) {
       k_form_extend<<<dim3(ceil_div(1ll << k < bt->max_list_cap ? 1ll << k : bt->max_list_cap, 256), y,
                            ceil_div(m, y)), 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, k);
       if ((rc = launch_status("k_form_extend"))) return rc;
       if ((2ll << k) >= bt->max_list_cap) break;  // the path is complete
-      k_form_double<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, k);
+      k_form_double<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, k, blk);
       if ((rc = launch_status("k_form_double"))) return rc;
     }
-    k_form_emit<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    k_form_emit<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, blk);
     if ((rc = launch_status("k_form_emit"))) return rc;
   }
   k_merge_batches<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);

@@ -73,10 +73,14 @@ class ReplayPipeline:
         self.B.seg_stride, self.B.cap_max, self.B.noise_k = self.seg_stride, self.pb.cap_max, self.noise_k
         self.d_scen = to_device(_struct_bytes(self.pb.scen), self.dev)
         self.d_models = to_device(_struct_bytes(self.pb.models), self.dev)
+        # (model, chunk) of every 256-entry chunk of the long lists: flat grids for their formation
+        blk = [(g, c) for g in range(self.pb.n_models) if self.pb.models[g].list_cap >= _abi.LONG_LIST
+               for c in range((self.pb.models[g].list_cap + 255) // 256)]
+        self.d_long_blocks = (torch.tensor(blk, dtype=torch.int32).reshape(-1).to(self.dev) if blk else None)
         self.batch = _abi.Batch(self.d_scen.data_ptr(), self.d_models.data_ptr(), self.pb.n_scen, self.pb.n_models,
                                 self.pb.max_req_cap, max((len(n) for n in self.pb.names), default=0),
                                 max((self.pb.models[g].list_cap for g in range(self.pb.n_models)), default=0),
-                                self.pb.total_req)
+                                self.pb.total_req, _abi.addr(self.d_long_blocks), len(blk), 0)
         n_models = max(self.pb.n_models, 1)
         self.slo_n = torch.zeros(n_models, dtype=torch.int32, device=self.dev)
         self.slo_met = torch.zeros(n_models, dtype=torch.int32, device=self.dev)
