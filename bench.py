@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 N_DEC = 32
 CAP = 4
 ALPHA = 0.5
-C4_PASSES = 4  # replay + verify passes queued per long trace (3 needed at slow 2.0, min_len 64)
+C4_PASSES = 4  # replay + verify passes queued per long trace (3 needed at slow 2.0, min_len 96)
 REPLAY_SCEN = 10000  # BASELINE configs[4]: a sweep of 10^4 synthetic scenarios (per GPU)
 METRIC = "candidate co-location predictions/sec and scenario replays/sec at 1/2/4/8 B200"
 
@@ -299,7 +299,7 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     spec = c4_scenario(t16, arch, n_requests=C4_REQUESTS, seed=1 + rank)
     ta = t16.arrays()
     pipes = [engine.ReplayPipeline([spec], ta, scale=1.2) for _ in range(2)]
-    for p in pipes:  # warm-up (also sizes the job scratch); default slow 2.0, min_len 64
+    for p in pipes:  # warm-up (also sizes the job scratch); default slow 2.0, min_len 96
         engine.replay_segmented(p, passes=C4_PASSES)
     pipe = pipes[0]
     barrier()

@@ -683,20 +683,6 @@ __device__ __forceinline__ int block_excl_sum(int v, int* sh, int* total) {
   __syncthreads();
   return r;
 }
-__device__ __forceinline__ int block_excl_maxi(int v, int* sh) {
-  const int t = threadIdx.x;
-  sh[t] = v;
-  __syncthreads();
-  for (int o = 1; o < kBigThreads; o <<= 1) {
-    const int a = t >= o ? sh[t - o] : -1;
-    __syncthreads();
-    sh[t] = sh[t] > a ? sh[t] : a;
-    __syncthreads();
-  }
-  const int r = t > 0 ? sh[t - 1] : -1;
-  __syncthreads();
-  return r;
-}
 
 // ---- K0a' (long lists), exact and parallel: the cumulative sum t += gap
 // (`workload.py:91`) reproduced bit for bit without a 3x10^5-long add chain.
@@ -1211,47 +1197,34 @@ __global__ void __launch_bounds__(kBigThreads) k_jobs_verify_big(const intf_scen
   if (n == 0) return;
   if (t == 0) any_fail = 0;
   const int R = (n + kBigThreads - 1) / kBigThreads, j0 = t * R, j1 = min(n, j0 + R);
-  // boundary j fails iff the previous job (fresh: every job was just replayed)
-  // ends after job j's first formation
+  // boundary j fails iff the previous job (each job's last completion from its
+  // own start) ends after job j's first formation; failing jobs join the kept
+  // job before them (whole runs at once, as replay_segmented_host); a holding
+  // boundary behind a merged job is checked again next pass
   auto fails = [&](int j) -> bool {
     if (j == 0) return false;
     const int sj = joff + j;
     return !(J.hi[sj] <= J.lo[sj] || J.last[sj - 1] <= B.b_formed[ro + J.lo[sj]]);
   };
-  // L_j = last non-failing index <= j (job 0 never fails); inside a run of
-  // failures the sequential rule keeps every other job: keep_j = !f_j || (j - L_j) even
-  int lastok = -1;
-  for (int j = j0; j < j1; j++)
-    if (!fails(j)) lastok = j;
-  const int Lin = block_excl_maxi(lastok, shi);
-  auto keep_of = [&](int j, int L) -> bool { return !fails(j) || ((j - L) % 2 == 0); };
-  int L = Lin, cnt = 0;
-  for (int j = j0; j < j1; j++) {
-    const bool f = fails(j);
-    if (!f) L = j;
-    cnt += keep_of(j, L) ? 1 : 0;
-  }
+  __shared__ int last_hi;
+  if (t == 0) last_hi = J.hi[joff + n - 1];
+  int cnt = 0;
+  for (int j = j0; j < j1; j++) cnt += fails(j) ? 0 : 1;
   int w = 0;
   int r = block_excl_sum(cnt, shi, &w);
   // compact into the shadow (6 doubles per slot), then copy back
   double* sh = J.scratch + 6ll * joff;
-  L = Lin;
   bool fail_seen = false;
   for (int j = j0; j < j1; j++) {
     const int sj = joff + j;
-    const bool f = fails(j);
-    if (!f) L = j;
-    fail_seen |= f;
-    if (!keep_of(j, L)) continue;
-    bool absorbs = false;
-    if (j + 1 < n) {
-      const bool f1 = fails(j + 1);
-      const int L1 = f1 ? L : j + 1;
-      absorbs = !keep_of(j + 1, L1);
+    if (fails(j)) {
+      fail_seen = true;
+      continue;
     }
+    const bool absorbs = j + 1 < n && fails(j + 1);
     double* d = sh + 6ll * r;
     d[0] = J.lo[sj];
-    d[1] = absorbs ? J.hi[sj + 1] : J.hi[sj];
+    d[1] = 0.0;  // hi: the next kept job's lo (set below)
     d[2] = J.last[sj];
     d[3] = J.info[3 * sj];
     d[4] = J.info[3 * sj + 1];
@@ -1266,7 +1239,7 @@ __global__ void __launch_bounds__(kBigThreads) k_jobs_verify_big(const intf_scen
     const int dj = joff + j;
     const bool dirty = d[5] < 0.0;
     J.lo[dj] = (int)d[0];
-    J.hi[dj] = (int)d[1];
+    J.hi[dj] = j + 1 < w ? (int)sh[6ll * (j + 1)] : last_hi;
     J.last[dj] = d[2];
     J.info[3 * dj] = (int)d[3];
     J.info[3 * dj + 1] = (int)d[4];
@@ -1340,12 +1313,17 @@ __global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen
   const int n = J.n_jobs[s], joff = J.joff[s], ro = S.req_off;
   if (n == 0) return;
   int w = 0;  // write cursor (kept jobs)
-  bool merged_prev = false, failed = false;
+  bool failed = false;
   for (int j = 0; j < n; j++) {
     const int sj = joff + j;
     bool keep = true;
-    if (j > 0 && !merged_prev) {
-      const double prev_last = J.last[sj - 1];  // fresh: every job was replayed before this pass
+    if (j > 0) {
+      // job j-1's own last completion (from its own start; slot sj-1 is not
+      // yet overwritten by the compaction).  A failing boundary merges job j
+      // into the kept job before it -- whole runs of failures at once; a
+      // holding boundary behind a merged job is checked again next pass
+      // against the merged job's fresh last completion.
+      const double prev_last = J.last[sj - 1];
       keep = J.hi[sj] <= J.lo[sj] || prev_last <= B.b_formed[ro + J.lo[sj]];
     }
     if (keep) {
@@ -1360,12 +1338,10 @@ __global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen
         J.dirty[dw] = 0;
       }
       w++;
-      merged_prev = false;
     } else {  // boundary j fails: job j joins the previous kept job
       const int dp = joff + w - 1;
       J.hi[dp] = J.hi[sj];
       J.dirty[dp] = 1;
-      merged_prev = true;
       failed = true;
     }
   }

@@ -690,7 +690,7 @@ def _candidate_starts(pipe, nb, formed_all, bmod, bsz, slow: float, min_len: int
     return js, jl
 
 
-def replay_segmented_host(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 64, max_iters: int = 100000,
+def replay_segmented_host(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 96, max_iters: int = 100000,
                           arrivals: bool = True, slo: bool = True, features: bool = True) -> dict:
     """Busy-period sharding: replay every scenario as parallel
     jobs split at speculated idle points, verify every boundary (previous
@@ -811,7 +811,7 @@ class _DeviceJobs:
         self.key = (float(slow), int(min_len))
 
 
-def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 64, max_iters: int = 100000,
+def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 96, max_iters: int = 100000,
                      arrivals: bool = True, slo: bool = True, features: bool = True, passes: int = 0,
                      stats: bool = True) -> dict:
     """Busy-period sharding, planned and verified on the device:
