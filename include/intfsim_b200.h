@@ -93,7 +93,10 @@ typedef struct intf_batch {
                                   formation launches flat grids (NULL: grids of max_list_cap x models) */
   int32_t n_long_blocks, pad_;
 } intf_batch;
+#ifndef INTF_LONG_LIST
 #define INTF_LONG_LIST 4096 /* model lists this long form batches by pointer doubling */
+#endif
+int intf_long_list(void); /* INTF_LONG_LIST as built (the long_blocks map must use it) */
 
 #define INTF_SLO_WS_INTS (256 + 32 * 3 * 256 + 32 * 3 * 4)
 

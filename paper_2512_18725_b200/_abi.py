@@ -50,8 +50,6 @@ class Batch(ctypes.Structure):
                 ("req_slots", c_int32), ("long_blocks", P), ("n_long_blocks", c_int32), ("pad_", c_int32)]
 
 
-LONG_LIST = 4096  # INTF_LONG_LIST
-
 
 REPLAY_BUFFER_FIELDS = [
     "arr_t", "arr_model", "list_t", "list_rid", "n_req", "n_list",
@@ -109,6 +107,7 @@ SIGNATURES = {
     "intf_ols_stats": (c_int32, [P, P, c_int64, P, P, P]),
     "intf_ols_solve": (c_int32, [P, P, P, P, P]),
     "intf_ols_fit_rows": (c_int32, [P, P, c_int64, P, P, P, P, P, P]),
+    "intf_long_list": (c_int32, []),
     "intf_ols_windows": (c_int32, [P, P, c_int64, c_int32, P, P, P, P]),
     "intf_sgd_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P]),
     "intf_rls_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P, P]),

@@ -1831,6 +1831,8 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
 
 extern "C" {
 
+int intf_long_list(void) { return kLongForm; }
+
 int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, void* stream) {
   if (!bt || !bt->scen || !bt->models || !buf || bt->n_scen <= 0) return bad_input("intf_generate_arrivals: null argument");
   cudaStream_t st = as_stream(stream);

@@ -74,7 +74,8 @@ class ReplayPipeline:
         self.d_scen = to_device(_struct_bytes(self.pb.scen), self.dev)
         self.d_models = to_device(_struct_bytes(self.pb.models), self.dev)
         # (model, chunk) of every 256-entry chunk of the long lists: flat grids for their formation
-        blk = [(g, c) for g in range(self.pb.n_models) if self.pb.models[g].list_cap >= _abi.LONG_LIST
+        long_list = int(self.lib.intf_long_list())  # the library's INTF_LONG_LIST
+        blk = [(g, c) for g in range(self.pb.n_models) if self.pb.models[g].list_cap >= long_list
                for c in range((self.pb.models[g].list_cap + 255) // 256)]
         self.d_long_blocks = (torch.tensor(blk, dtype=torch.int32).reshape(-1).to(self.dev) if blk else None)
         self.batch = _abi.Batch(self.d_scen.data_ptr(), self.d_models.data_ptr(), self.pb.n_scen, self.pb.n_models,
