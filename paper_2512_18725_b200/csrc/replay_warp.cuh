@@ -198,14 +198,20 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
   // formation-time window: lane l holds b_formed of batch fbase + l
   int fbase = J.b_lo;
   double wf = fbase + lane < nb ? B.b_formed[ro + fbase + lane] : 0.0;
-  // dispatch window: lane l holds model/size/noise of batch dbase + l
-  int dbase = J.b_lo, wm = 0, wsz = 0;
+  // dispatch window: lane l holds the profile entry (solo ms, throughputs) and
+  // the first noise draws of batch dbase + l, so a dispatch reads them by
+  // shuffles instead of the dependent model -> entry -> table loads
+  int dbase = J.b_lo;
+  double wsol = 1.0, wt0 = 0.0, wt1 = 0.0, wt2 = 0.0;
   double wn0 = 1.0, wn1 = 1.0, wn2 = 1.0, wn3 = 1.0;
   auto load_dispatch_window = [&](int base) {
     const int b = base + lane;
     if (b < nb) {
-      wm = B.b_model[ro + b];
-      wsz = B.b_size[ro + b];
+      const int e = md[B.b_model[ro + b]].entry_base + B.b_size[ro + b] - 1;
+      wsol = tab.solo_ms[e];
+      wt0 = tab.thr[3 * e];
+      wt1 = tab.thr[3 * e + 1];
+      wt2 = tab.thr[3 * e + 2];
       const double* nt = B.noise_tab + (size_t)(ro + b) * B.noise_k;
       wn0 = K > 0 ? nt[0] : 1.0;
       wn1 = K > 1 ? nt[1] : 1.0;
@@ -333,14 +339,36 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       const double* cseg = B.slot_seg + ((size_t)J.scratch * B.cap_max + cl) * (size_t)B.seg_stride * 5;
       const double* csm = sseg + cl * kSmemSeg * 5;
       for (int k = lane; k < nseg_c; k += W) {
-        const double* p = k < kSmemSeg ? csm + k * 5 : cseg + (size_t)k * 5;
-        const double* q = k + 1 < kSmemSeg ? csm + (k + 1) * 5 : cseg + (size_t)(k + 1) * 5;
-        B.s_tbegin[off + k] = p[0];
-        B.s_tend[off + k] = (k + 1 < nseg_c) ? q[0] : now;
-        B.s_slowdown[off + k] = p[1];
-        B.s_colo[3 * (size_t)(off + k) + 0] = p[2];
-        B.s_colo[3 * (size_t)(off + k) + 1] = p[3];
-        B.s_colo[3 * (size_t)(off + k) + 2] = p[4];
+        // every load before the first store (the history cannot alias the
+        // outputs, but the compiler cannot know: interleaved, each store
+        // would wait for its load on the chain); shared-memory rows by
+        // shared-memory loads
+        double v0, v1, v2, v3, v4, ve;
+        if (k + 1 < kSmemSeg) {
+          const double* p = csm + k * 5;
+          v0 = p[0];
+          v1 = p[1];
+          v2 = p[2];
+          v3 = p[3];
+          v4 = p[4];
+          ve = p[5];  // next row's t_begin
+        } else {
+          const double* p = k < kSmemSeg ? csm + k * 5 : cseg + (size_t)k * 5;
+          const double* q = cseg + (size_t)(k + 1) * 5;
+          v0 = p[0];
+          v1 = p[1];
+          v2 = p[2];
+          v3 = p[3];
+          v4 = p[4];
+          ve = k + 1 < nseg_c ? q[0] : now;
+        }
+        if (k + 1 >= nseg_c) ve = now;
+        B.s_tbegin[off + k] = v0;
+        B.s_tend[off + k] = ve;
+        B.s_slowdown[off + k] = v1;
+        B.s_colo[3 * (size_t)(off + k) + 0] = v2;
+        B.s_colo[3 * (size_t)(off + k) + 1] = v3;
+        B.s_colo[3 * (size_t)(off + k) + 2] = v4;
       }
       seg_cursor += nseg_c;
       // outcome order (completion, batch_id) (`simcore.py:305`): only runs of
@@ -425,16 +453,14 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
         load_dispatch_window(dbase);
       }
       const int src = (b - dbase) & (W - 1);
-      const int m = G.shfl(wm, src), sz = G.shfl(wsz, src);
+      const double t0 = G.shfl(wt0, src), t1 = G.shfl(wt1, src), t2 = G.shfl(wt2, src), sol = G.shfl(wsol, src);
       const double n0 = G.shfl(wn0, src), n1 = G.shfl(wn1, src), n2 = G.shfl(wn2, src), n3 = G.shfl(wn3, src);
       const int L = __ffs(freemask) - 1;
       freemask &= ~(1u << L);
       runlist |= (unsigned long long)L << (4 * nrun);
       nrun++;
       const bool was_act = act;
-      if constexpr (CAPT > 0) {  // every lane appends the new batch's throughputs (broadcast loads)
-        const int e = md[m].entry_base + sz - 1;
-        const double t0 = tab.thr[3 * e], t1 = tab.thr[3 * e + 1], t2 = tab.thr[3 * e + 2];
+      if constexpr (CAPT > 0) {  // every lane appends the new batch's throughputs
 #pragma unroll
         for (int k = 0; k < KU; k++) {
           if (k == nrun - 1) {
@@ -445,18 +471,17 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
         }
       }
       if (lane == L) {
-        const int entry = md[m].entry_base + sz - 1;
         if (B.b_running) B.b_running[ro + b] = nrun;  // dispatch trace
         act = true;
         batch = b;
         start = now;
-        total = tab.solo_ms[entry];
+        total = sol;
         progress = 0.0;
         nseg = 0;
         n_non1 = 0;
-        own0 = tab.thr[3 * entry];
-        own1 = tab.thr[3 * entry + 1];
-        own2 = tab.thr[3 * entry + 2];
+        own0 = t0;
+        own1 = t1;
+        own2 = t2;
         nz0 = n0;
         nz1 = n1;
         nz2 = n2;
