@@ -285,20 +285,53 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
   int red_hi = 1;
   while (red_hi < cap) red_hi <<= 1;
   red_hi >>= 1;
+  // next completion (CAPT > 0): kept across iterations that do not change the
+  // running set (formations while the GPU is full)
+  double dmin = INFINITY;
+  int bmin = 0x7fffffff, cl_min = 0;
+  bool min_ok = false;
   for (;;) {
     // next completion: lexicographic min of (done, batch) over active lanes
-    double dmin = act ? done : INFINITY;
-    int bmin = act ? batch : 0x7fffffff;
-    for (int o = red_hi; o > 0; o >>= 1) {
-      const double d2 = G.shfl_xor(dmin, o);
-      const int b2 = G.shfl_xor(bmin, o);
-      if (d2 < dmin || (d2 == dmin && b2 < bmin)) {
-        dmin = d2;
-        bmin = b2;
+    if constexpr (CAPT > 0) {
+      // slots live in lanes [0, CAPT): every lane reads all of them at once
+      // (independent shuffles) and takes the min locally, with its lane
+      if (!min_ok) {
+        const double dv = act ? done : INFINITY;
+        const int bv = act ? batch : 0x7fffffff;
+        double dk[CAPT];
+        int bk[CAPT];
+#pragma unroll
+        for (int k = 0; k < CAPT; k++) {
+          dk[k] = G.shfl(dv, k);
+          bk[k] = G.shfl(bv, k);
+        }
+        dmin = dk[0];
+        bmin = bk[0];
+        cl_min = 0;
+#pragma unroll
+        for (int k = 1; k < CAPT; k++) {
+          if (dk[k] < dmin || (dk[k] == dmin && bk[k] < bmin)) {
+            dmin = dk[k];
+            bmin = bk[k];
+            cl_min = k;
+          }
+        }
+        min_ok = true;
       }
+    } else {
+      dmin = act ? done : INFINITY;
+      bmin = act ? batch : 0x7fffffff;
+      for (int o = red_hi; o > 0; o >>= 1) {
+        const double d2 = G.shfl_xor(dmin, o);
+        const int b2 = G.shfl_xor(bmin, o);
+        if (d2 < dmin || (d2 == dmin && b2 < bmin)) {
+          dmin = d2;
+          bmin = b2;
+        }
+      }
+      dmin = G.shfl(dmin, 0);
+      bmin = G.shfl(bmin, 0);
     }
-    dmin = G.shfl(dmin, 0);
-    bmin = G.shfl(bmin, 0);
     const bool have_form = n_formed < nb;
     if (have_form && n_formed - fbase >= W) {
       fbase += W;
@@ -310,8 +343,14 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       // ---- COMPLETION (`simcore.py:173-198`)
       if (dmin < now - 1e-9) status |= INTF_ST_PAST_EVENT;
       now = now > dmin ? now : dmin;
-      const unsigned cmask = G.ballot(act && batch == bmin);
-      const int cl = __ffs(cmask) - 1;
+      int cl;
+      if constexpr (CAPT > 0) {
+        cl = cl_min;
+      } else {
+        const unsigned cmask = G.ballot(act && batch == bmin);
+        cl = __ffs(cmask) - 1;
+      }
+      min_ok = false;
       int nseg_c = 0, off = 0;
       // RunningBatch.close_segment of the completing batch (`simcore.py:174`)
       // and of every survivor (`:145`): independent, so one parallel step
@@ -455,6 +494,7 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       const int src = (b - dbase) & (W - 1);
       const double t0 = G.shfl(wt0, src), t1 = G.shfl(wt1, src), t2 = G.shfl(wt2, src), sol = G.shfl(wsol, src);
       const double n0 = G.shfl(wn0, src), n1 = G.shfl(wn1, src), n2 = G.shfl(wn2, src), n3 = G.shfl(wn3, src);
+      min_ok = false;
       const int L = __ffs(freemask) - 1;
       freemask &= ~(1u << L);
       runlist |= (unsigned long long)L << (4 * nrun);
