@@ -183,8 +183,13 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
 
   // ---- group-uniform state
   unsigned long long runlist = 0ull;  // 4-bit lane ids in dispatch order
-  // (CAPT > 0) throughputs of the running batches in running-list order, held
-  // by every lane: colo sums without shuffles
+  // (CAPT > 0) throughputs of the running batches, held by every lane: colo
+  // sums without shuffles.  Cap 4: in running-list order.  Caps 2-3: by slot
+  // (lane), because a batch has at most two peers there and the sum does not
+  // depend on their order: ((0 + a) + b) == ((0 + b) + a) bit for bit (fp
+  // addition commutes; 0 + x only maps -0 to +0), so the list order needs no
+  // upkeep (no shifts at a completion, no list decode per reseat).
+  constexpr bool kBySlot = CAPT == 2 || CAPT == 3;
   double u0[KU], u1[KU], u2[KU];
 #pragma unroll
   for (int k = 0; k < KU; k++) u0[k] = u1[k] = u2[k] = 0.0;
@@ -225,7 +230,16 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
   // the group calls it together (group-uniform shuffles inside)
   auto reseat_lane = [&](bool doit) {
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    if constexpr (CAPT > 0) {
+    if constexpr (kBySlot) {
+#pragma unroll
+      for (int k = 0; k < KU; k++) {  // running peers by slot, skipping this lane's own batch
+        if (k != lane && !((freemask >> k) & 1u)) {
+          c0 = c0 + u0[k];
+          c1 = c1 + u1[k];
+          c2 = c2 + u2[k];
+        }
+      }
+    } else if constexpr (CAPT > 0) {
 #pragma unroll
       for (int k = 0; k < KU; k++) {  // running-list order, skipping this lane's own batch
         if (k < nrun && (int)((runlist >> (4 * k)) & 15ull) != lane) {
@@ -431,18 +445,21 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       n_done++;
       last_done = now;
       // remove cl from the running list, keep order
-      unsigned long long nl = 0ull;
-      int w = 0, pc = 0;
+      if constexpr (kBySlot) {
+        nrun--;
+      } else {
+        unsigned long long nl = 0ull;
+        int w = 0, pc = 0;
 #pragma unroll
-      for (int k = 0; k < KU; k++) {
-        if (k >= nrun) break;
-        const unsigned long long j = (runlist >> (4 * k)) & 15ull;
-        if ((int)j != cl) nl |= j << (4 * w++);
-        else pc = k;
-      }
-      runlist = nl;
-      nrun = w;
-      if constexpr (CAPT > 0) {
+        for (int k = 0; k < KU; k++) {
+          if (k >= nrun) break;
+          const unsigned long long j = (runlist >> (4 * k)) & 15ull;
+          if ((int)j != cl) nl |= j << (4 * w++);
+          else pc = k;
+        }
+        runlist = nl;
+        nrun = w;
+        if constexpr (CAPT > 0) {
 #pragma unroll
         for (int k = 0; k + 1 < KU; k++) {
           if (k >= pc) {
@@ -450,6 +467,7 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
             u1[k] = u1[k + 1];
             u2[k] = u2[k + 1];
           }
+        }
         }
       }
       freemask |= 1u << cl;
@@ -497,13 +515,13 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       min_ok = false;
       const int L = __ffs(freemask) - 1;
       freemask &= ~(1u << L);
-      runlist |= (unsigned long long)L << (4 * nrun);
+      if constexpr (!kBySlot) runlist |= (unsigned long long)L << (4 * nrun);
       nrun++;
       const bool was_act = act;
-      if constexpr (CAPT > 0) {  // every lane appends the new batch's throughputs
+      if constexpr (CAPT > 0) {  // every lane records the new batch's throughputs
 #pragma unroll
         for (int k = 0; k < KU; k++) {
-          if (k == nrun - 1) {
+          if (k == (kBySlot ? L : nrun - 1)) {
             u0[k] = t0;
             u1[k] = t1;
             u2[k] = t2;
