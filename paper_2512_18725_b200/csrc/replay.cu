@@ -466,10 +466,25 @@ __global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __rest
 
 // ---- K2: the replay recurrence, one kReplayW-lane group per scenario (lane
 // l < cap owns running slot l; replay_warp.cuh).
-#ifndef INTF_REPLAY_MINB
-#define INTF_REPLAY_MINB 3  // 170 registers: no spills in the cap-templated replay (B200: C5 10^4 7.36 -> 6.77 ms)
+#ifndef INTF_REPLAY_WARPS
+#define INTF_REPLAY_WARPS 4  // warps per k_replay_warp block
 #endif
-constexpr int kReplayWarps = 4;
+#ifndef INTF_JOB_WARPS
+#define INTF_JOB_WARPS 1  // warps per busy-period job block (k_replay_jobs, k_jobs_replay)
+#endif
+// 12 resident replay warps per SM = 170 registers: no spills in the
+// cap-templated replay (B200: C5 10^4 7.36 -> 6.77 ms at 3 blocks of 4 warps)
+#ifndef INTF_REPLAY_MINB
+#define INTF_REPLAY_MINB (12 / INTF_REPLAY_WARPS)
+#endif
+#define INTF_JOB_MINB (12 / INTF_JOB_WARPS)
+constexpr int kReplayWarps = INTF_REPLAY_WARPS;
+// Job kernels: a block keeps its registers until its LAST warp ends, so with
+// one-warp blocks a long job does not hold finished warps' slots away from
+// the next pass / trace (measured on C4: 3.04 -> 2.85 ms per trace, 2.00 ->
+// 1.87 ms with two traces in flight; the C5 sweep kernel is better at 4,
+// `profiles/replay_block_warps_r1k.txt`).
+constexpr int kJobWarps = INTF_JOB_WARPS;
 constexpr int kReplayW = 32;  // measured: one scenario per warp beats 4 x 8-lane groups (divergence)
 // Replay order = longest-processing-time first by the device's own work
 // estimate: formed batches, cap-1 scenarios weighted 1/5 (their max-plus chain
@@ -550,7 +565,7 @@ __global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_replay_
 // batches [lo[i], hi[i]) of scenario sc[i] from an idle GPU; its segment
 // records go to S.seg_off + lo*(2cap-1) (a disjoint slice: a batch has at
 // most 2cap-1 reseats), its outcome order to positions [lo, hi).
-__global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_replay_jobs(const intf_scenario* __restrict__ scen,
+__global__ void __launch_bounds__(32 * kJobWarps, INTF_JOB_MINB) k_replay_jobs(const intf_scenario* __restrict__ scen,
                                                                     const intf_model* __restrict__ models,
                                                                     intf_table tab, intf_replay_buffers B,
                                                                     const int32_t* __restrict__ sc,
@@ -558,9 +573,9 @@ __global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_replay_
                                                                     const int32_t* __restrict__ hi, int n_jobs,
                                                                     double* __restrict__ last_done,
                                                                     int32_t* __restrict__ info) {
-  __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
+  __shared__ double sseg[kJobWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
   const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
-  const int i = blockIdx.x * kReplayWarps * (32 / kReplayW) + g;
+  const int i = blockIdx.x * kJobWarps * (32 / kReplayW) + g;
   if (i >= n_jobs) return;
   const int s = sc[i];
   const int st0 = B.status[s];
@@ -1274,17 +1289,17 @@ __global__ void __launch_bounds__(kBigThreads) k_jobs_verify_big(const intf_scen
   }
 }
 
-__global__ void __launch_bounds__(32 * kReplayWarps, INTF_REPLAY_MINB) k_jobs_replay(const intf_scenario* __restrict__ scen,
+__global__ void __launch_bounds__(32 * kJobWarps, INTF_JOB_MINB) k_jobs_replay(const intf_scenario* __restrict__ scen,
                                                                     const intf_model* __restrict__ models,
                                                                     intf_table tab, intf_replay_buffers B,
                                                                     intf_jobs J, int n_todo) {
-  __shared__ double sseg[kReplayWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
+  __shared__ double sseg[kJobWarps * (32 / kReplayW)][kMaxCap * kSmemSeg * 5];
   const int g = (threadIdx.x >> 5) * (32 / kReplayW) + ((threadIdx.x & 31) / kReplayW);
   // n_todo < 0: the count is the device's (*J.todo_count, set by the plan /
   // the last verify), so passes can be queued without a host round trip
   const int n = n_todo >= 0 ? n_todo : *J.todo_count;
-  const int stride = gridDim.x * kReplayWarps * (32 / kReplayW);
-  for (int k = blockIdx.x * kReplayWarps * (32 / kReplayW) + g; k < n; k += stride) {
+  const int stride = gridDim.x * kJobWarps * (32 / kReplayW);
+  for (int k = blockIdx.x * kJobWarps * (32 / kReplayW) + g; k < n; k += stride) {
     const int slot = J.todo[k];
     const int s = J.slot_scen[slot];
     const intf_scenario& S = scen[s];
@@ -1900,7 +1915,7 @@ int intf_replay_jobs(const intf_batch* bt, const intf_table* table, const intf_r
   if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1)
     return bad_input("intf_replay_jobs: cap_max must be in [1, 8], seg_stride >= 1");
   if (n_jobs == 0) return INTF_OK;
-  k_replay_jobs<<<ceil_div(n_jobs, kReplayWarps * (32 / kReplayW)), 32 * kReplayWarps, 0, as_stream(stream)>>>(
+  k_replay_jobs<<<ceil_div(n_jobs, kJobWarps * (32 / kReplayW)), 32 * kJobWarps, 0, as_stream(stream)>>>(
       bt->scen, bt->models, *table, *buf, job_scen, job_lo, job_hi, n_jobs, job_last_done, job_info);
   return launch_status("k_replay_jobs");
 }
@@ -1939,9 +1954,9 @@ int intf_jobs_replay(const intf_batch* bt, const intf_table* table, const intf_r
   if (n_todo == 0) return INTF_OK;
   // n_todo < 0: up to -n_todo jobs, the count read on the device; a grid of
   // at most one wave, its warps striding over the todo list
-  const long long want = ceil_div(n_todo > 0 ? n_todo : -(long long)n_todo, kReplayWarps * (32 / kReplayW));
-  const unsigned grid = n_todo > 0 ? (unsigned)want : (unsigned)(want < 148 * INTF_REPLAY_MINB ? want : 148 * INTF_REPLAY_MINB);
-  k_jobs_replay<<<grid, 32 * kReplayWarps, 0, as_stream(stream)>>>(bt->scen, bt->models, *table, *buf, *jobs, n_todo);
+  const long long want = ceil_div(n_todo > 0 ? n_todo : -(long long)n_todo, kJobWarps * (32 / kReplayW));
+  const unsigned grid = n_todo > 0 ? (unsigned)want : (unsigned)(want < 148 * INTF_JOB_MINB ? want : 148 * INTF_JOB_MINB);
+  k_jobs_replay<<<grid, 32 * kJobWarps, 0, as_stream(stream)>>>(bt->scen, bt->models, *table, *buf, *jobs, n_todo);
   return launch_status("k_jobs_replay");
 }
 
