@@ -545,10 +545,10 @@ def product_arm(a):
     specs.sort(key=lambda d: -sum(m["arrival_rate_rps"] for m in d["deployed"]) * d["duration_s"])
     preds = [_abi.Predictor(ewma=0, alpha=1.0, w=tuple(W[-1, 0])), _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[-1, 1])),
              _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[0, 1]))]
-    # two pipelines (double-buffered sweeps) on two streams: consecutive steps
-    # overlap, so one sweep's arrivals / formation / SLO run beside the other
-    # sweep's replay tail (the replay is bounded by its longest scenario's chain)
-    n_pipes = int(os.environ.get("INTF_BENCH_PIPES", "2"))
+    # pipelines (buffer sets) on their own streams: consecutive steps overlap,
+    # so one sweep's arrivals / formation / SLO run beside the other sweeps'
+    # replay tails (the replay is bounded by its longest scenario's chain)
+    n_pipes = int(os.environ.get("INTF_BENCH_PIPES", "3"))  # 2 / 3 / 4: 3.70 / 3.59 / 3.60 ms (profiles/c5_pipes_r1l.txt)
     pipes = [engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5) for _ in range(n_pipes)]
     pipe = pipes[0]
     for _ in range(max(1, a.warmup)):
@@ -556,7 +556,7 @@ def product_arm(a):
             p.run()
     barrier()
     st = pipe.status()
-    r_steps = max(n_pipes, min(a.steps, 3 * n_pipes))
+    r_steps = max(n_pipes, a.steps)  # the K steps asked for (a sweep is ~4 ms)
     # per-scenario SLO metrics of every rank gathered (NCCL all_gather, N > 1):
     # per deployed model n, met, p50/p95/p99, padded to the largest rank
     n_mod = pipe.pb.n_models
@@ -671,8 +671,8 @@ def product_arm(a):
                    "workload": "C5-shape synthetic scenarios (default_rng([2512,i]), 1 s, cap 1-3): arrivals + "
                                "formation + noise + replay (warp per scenario) + SLO + features/3 predictors; N > 1: "
                                "+ all_gather of every rank's per-model SLO metrics each step; consecutive steps "
-                               "double-buffered on two streams (two pipelines), so a step's arrivals/formation/SLO "
-                               "overlap the previous step's replay tail",
+                               f"on {n_pipes} pipelines (buffer sets) on {n_pipes} streams, so a step's "
+                               "arrivals/formation/SLO overlap the other steps' replay tails",
                    "steps_timed": r_steps,
                    "stage_ms": stage_ms, "cpu_baseline": replay_cpu},
         "refit": refit,
