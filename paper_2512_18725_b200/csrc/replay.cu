@@ -443,13 +443,19 @@ constexpr int kPerScenarioMin = 4 * 148;  // below this many scenarios, flatten
 __global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __restrict__ scen, int n_scen,
                                                      long long req_slots, intf_replay_buffers B) {
   const int K = B.noise_k;
+  // concurrency_cap == 1: a batch runs alone as ONE segment, so the replay
+  // (replay_cap1) reads only draw (b, 0): the other K - 1 are not computed
   if (n_scen >= kPerScenarioMin) {
     for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
       const intf_scenario& S = scen[s];
-      const long long n = (long long)B.n_batches[s] * K;
+      const int Ks = S.cap == 1 ? 1 : K;
+      const long long n = (long long)B.n_batches[s] * Ks;
       double* out = B.noise_tab + (long long)S.req_off * K;
-      for (long long i = threadIdx.x; i < n; i += blockDim.x)
-        out[i] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)(i / K), (uint64_t)(i % K), S.sigma);
+      for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        const long long b = i / Ks;
+        const int j = (int)(i - b * Ks);
+        out[b * K + j] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)b, (uint64_t)j, S.sigma);
+      }
     }
     return;
   }
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __rest
     const int s = scen_of_slot(scen, n_scen, slot);
     const intf_scenario& S = scen[s];
     const long long b = slot - S.req_off;
-    if (b < B.n_batches[s])
+    if (b < B.n_batches[s] && (S.cap != 1 || i % K == 0))
       B.noise_tab[i] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)b, (uint64_t)(i % K), S.sigma);
   }
 }
