@@ -8,6 +8,7 @@ constructor raises -- there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -58,13 +59,14 @@ class ReplayPipeline:
     """
 
     def __init__(self, specs, table: _pack.TableArrays, seg_stride: int = 64, scale: float = 1.0,
-                 preds=(), list_caps=None, dtable: DeviceTable | None = None, noise_k: int = 6):
+                 preds=(), list_caps=None, dtable: DeviceTable | None = None, noise_k: int | None = None):
         self.dev = require_cuda()
         self.lib = _abi.load()
         self.pb = _pack.pack(list(specs), table, scale=scale, list_caps=list_caps)
         self.seg_stride = int(seg_stride)
         self.dtable = dtable or DeviceTable(table, self.dev)
-        self.noise_k = int(noise_k)
+        # noise draws precomputed per batch (the rest are drawn on the replay chain)
+        self.noise_k = int(noise_k if noise_k is not None else os.environ.get("INTF_NOISE_K", "6"))
         sz = _pack.sizes(self.pb, self.seg_stride, self.noise_k)
         self.t = {f: torch.zeros(sz[k], dtype=_TORCH_DT[dt], device=self.dev) for f, dt, k in _pack.BUFFER_PLAN}
         self.B = _abi.ReplayBuffers()
