@@ -289,8 +289,8 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     with busy-period sharding (speculative idle boundaries planned, verified
     and merged on the device; C4_PASSES passes queued with device-side job
     counts, one host read per trace, inside the timed region).  Each rank
-    replays its own trace (weak scaling).  Also: back-to-back traces on two
-    streams (`pipelined`)."""
+    replays its own trace (weak scaling).  Also: back-to-back traces on four
+    buffer sets and streams, two traces each (`pipelined`)."""
     import torch
     from paper_2512_18725_b200 import engine
     from paper_2512_18725_b200.sweep import c4_scenario, table16
@@ -298,7 +298,8 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     t16, arch = table16()
     spec = c4_scenario(t16, arch, n_requests=C4_REQUESTS, seed=1 + rank)
     ta = t16.arrays()
-    pipes = [engine.ReplayPipeline([spec], ta, scale=1.2) for _ in range(2)]
+    n_c4_pipes = int(os.environ.get("INTF_BENCH_C4_PIPES", "4"))  # 2 / 3 / 4: 1.87 / 1.68 / 1.59 ms per trace (profiles/c4_pipes_r1m.txt)
+    pipes = [engine.ReplayPipeline([spec], ta, scale=1.2) for _ in range(n_c4_pipes)]
     for p in pipes:  # warm-up (also sizes the job scratch); default slow 2.0, min_len 96
         engine.replay_segmented(p, passes=C4_PASSES)
     pipe = pipes[0]
@@ -313,10 +314,10 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     ms = max_over_ranks(e0.elapsed_time(e1))
     n_req = int(pipe.t["n_req"][0].item())
     st = int(pipe.t["status"][0].item())
-    # back-to-back traces double-buffered on two streams (each trace fully
+    # back-to-back traces on n_c4_pipes buffer sets and streams (each trace fully
     # stream-ordered: its low-parallelism phases overlap the other's work);
     # every trace's pending-job count is kept and checked after the timing
-    K = 6
+    K = 2 * n_c4_pipes
     rstreams = [torch.cuda.Stream() for _ in pipes]
     pending = torch.zeros(K, dtype=torch.int32, device="cuda")
     fins = []
@@ -326,16 +327,17 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     for rs in rstreams:
         rs.wait_stream(stream)
     for k in range(K):
-        with torch.cuda.stream(rstreams[k & 1]):
-            fins.append(engine.replay_segmented(pipes[k & 1], passes=C4_PASSES, stats=False))
-            pending[k:k + 1].copy_(pipes[k & 1]._jobs.t["todo_count"])
+        q = k % n_c4_pipes
+        with torch.cuda.stream(rstreams[q]):
+            fins.append(engine.replay_segmented(pipes[q], passes=C4_PASSES, stats=False))
+            pending[k:k + 1].copy_(pipes[q]._jobs.t["todo_count"])
     for rs in rstreams:
         stream.wait_stream(rs)
     p1.record(stream)
     barrier()
     pms = max_over_ranks(p0.elapsed_time(p1)) / K
     complete = int(pending.sum().item()) == 0 and all(int(p.t["status"][0].item()) == 0 for p in pipes)
-    for f in fins[-2:]:
+    for f in fins[-n_c4_pipes:]:
         f()
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -351,7 +353,7 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     return {"metric": "requests replayed/sec (single long trace)", "value": world * n_req / (ms / 1e3),
             "unit": "requests/s", "ms_per_trace": ms, "requests": n_req, "status": st, **stats,
             "pipelined": {"value": world * n_req / (pms / 1e3), "unit": "requests/s", "ms_per_trace": pms,
-                          "traces": K, "streams": 2, "complete": complete},
+                          "traces": K, "streams": n_c4_pipes, "complete": complete},
             "cpu_baseline": cpu,
             "workload": "C4: 16 models (6 default + 10 rng(123) archetypes), bs 1-64, cap 4, window U(10,20) ms, "
                         "sigma 0.05, total rho 0.5 at bs 64; one trace per GPU; arrivals + formation + noise + "
