@@ -106,24 +106,10 @@ class Clocks:
 # ------------------------------------------------------------- workloads
 def decision_coefs(n_dec: int) -> np.ndarray:
     """[n_dec][2][7]: coarse (static) / fine (EWMA 1/2) OLS refits on growing
-    windows of the bundled trace's samples (windowed refit, `predict.py:53-72`)."""
-    import paper_2512_18725_b200 as p
-    from paper_2512_18725_b200 import engine
-    from paper_2512_18725_b200.colocation import features_for_modes
-    from paper_2512_18725_b200.workload import scenario_from_dict
-    from tests import _golden
+    windows of the bundled trace's samples (`sweep.c2_decision_coefs`)."""
+    from paper_2512_18725_b200.sweep import c2_decision_coefs
 
-    table = p.gen_synthetic_profiles()
-    res = p.run_scenario(scenario_from_dict(_golden.spec("bundled_seed7")), table)
-    X, y, _ = features_for_modes(res.outcomes, table, [p.STATIC_MODE, p.ewma_mode(ALPHA)])
-    n = len(y)
-    W = np.zeros((n_dec, 2, 7))
-    for d in range(n_dec):
-        hi = max(64, int(n * (d + 1) / n_dec))
-        for k in range(2):
-            params, _, _, _ = engine.ols_solve(engine.ols_stats(X[k, :hi], y[:hi]))
-            W[d, k] = params
-    return W
+    return c2_decision_coefs(n_dec, ALPHA)
 
 
 def cpu_candidate_rate(table, W, seconds: float, seed: int = 0):
@@ -459,7 +445,7 @@ def product_arm(a):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2512_18725_b200 import _abi, engine
     from paper_2512_18725_b200.profiles import gen_synthetic_profiles
-    from paper_2512_18725_b200.sweep import c5_scenarios
+    from paper_2512_18725_b200.sweep import c5_scenarios, lpt_order
 
     def barrier():
         if dist is not None:
@@ -542,16 +528,16 @@ def product_arm(a):
     ok = bool(np.isfinite(ho[:1000]).all())
 
     # ---- secondary: scenario replay sweep (C5 shape)
-    specs = c5_scenarios(table, REPLAY_SCEN, start=rank * REPLAY_SCEN)
     # longest-processing-time-first: heaviest scenarios (expected requests) get the first warps
-    specs.sort(key=lambda d: -sum(m["arrival_rate_rps"] for m in d["deployed"]) * d["duration_s"])
+    specs = lpt_order(c5_scenarios(table, REPLAY_SCEN, start=rank * REPLAY_SCEN))
     preds = [_abi.Predictor(ewma=0, alpha=1.0, w=tuple(W[-1, 0])), _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[-1, 1])),
              _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[0, 1]))]
     # pipelines (buffer sets) on their own streams: consecutive steps overlap,
     # so one sweep's arrivals / formation / SLO run beside the other sweeps'
     # replay tails (the replay is bounded by its longest scenario's chain)
     n_pipes = int(os.environ.get("INTF_BENCH_PIPES", "3"))  # 2 / 3 / 4: 3.70 / 3.59 / 3.60 ms (profiles/c5_pipes_r1l.txt)
-    pipes = [engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5) for _ in range(n_pipes)]
+    noise_k = int(os.environ.get("INTF_NOISE_K", engine.NOISE_K))  # tools/noise_k.sh sweeps it
+    pipes = [engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5, noise_k=noise_k) for _ in range(n_pipes)]
     pipe = pipes[0]
     for _ in range(max(1, a.warmup)):
         for p in pipes:

@@ -437,6 +437,79 @@ def candidate_predictions(own, peers, solo, thr, w_coarse, w_fine, alpha):
     return predict(w_coarse[:6], w_coarse[6], xs), predict(w_fine[:6], w_fine[6], xf)
 
 
+def multisets(E: int, cap: int) -> np.ndarray:
+    """Every peer multiset of size <= cap-1 over E entries, as sorted index
+    rows padded with -1, in the product's output order (size-major, colex
+    within a size: rank = sum_j C(E+j-1, j) for j < k + sum_i C(p_i+i-1, i))."""
+    import itertools
+
+    rows = []
+    for k in range(cap):
+        combos = (np.array(list(itertools.combinations_with_replacement(range(E), k)), dtype=np.int64)
+                  if k else np.zeros((1, 0), dtype=np.int64))
+        rank = np.zeros(len(combos), dtype=np.int64)
+        for i in range(k):
+            rank += np.array([math.comb(int(q) + i, i + 1) for q in combos[:, i]], dtype=np.int64)
+        block = np.full((len(combos), cap - 1), -1, dtype=np.int64)
+        block[rank, :k] = combos
+        rows.append(block)
+    return np.concatenate(rows)
+
+
+def candidate_features_all(solo, thr, cap: int, alpha: float):
+    """Vectorised `candidate_history` + `features` for every (own, multiset):
+    (X_static, X_ewma) of shape [E, n_sets, 6], fp64.  Peer sums run from
+    zeros in peer order (`simcore.py:126-131`); a removed peer contributes an
+    exact +0.0, so the sums equal the scalar restatement's bit for bit; the
+    EWMA recursion is `colocation.py:61` unfused."""
+    solo = np.asarray(solo, dtype=float)
+    thr = np.asarray(thr, dtype=float)
+    E = len(solo)
+    M = multisets(E, cap)  # [n_sets, cap-1]
+    k = cap - 1
+    valid = M >= 0
+    Mi = np.where(valid, M, 0)
+    pthr = thr[Mi] * valid[..., None]  # [n, k, 3], zeros for absent peers
+    c0 = np.zeros((len(M), 3))
+    for j in range(k):
+        c0 = c0 + pthr[:, j]
+    Xs = np.empty((E, len(M), 6))
+    Xf = np.empty((E, len(M), 6))
+    psolo = np.where(valid, solo[Mi], np.inf)
+    for own in range(E):
+        dep = valid & (psolo < solo[own])  # peers that finish before own
+        # departure order (solo, entry, position): peers are sorted by entry, so a stable sort by solo is it
+        key = np.where(dep, psolo, np.inf)
+        order = np.argsort(key, axis=1, kind="stable")
+        alive = valid.copy()
+        r = c0.copy()
+        for t in range(k):
+            q = order[:, t]
+            has = dep[np.arange(len(M)), q]
+            alive[np.arange(len(M))[has], q[has]] = False
+            c = np.zeros((len(M), 3))
+            for j in range(k):
+                c = c + np.where(alive[:, j, None], pthr[:, j], 0.0)
+            r = np.where(has[:, None], alpha * c + (1.0 - alpha) * r, r)
+        own_x = np.broadcast_to(thr[own], (len(M), 3))
+        Xs[own] = np.concatenate([own_x, c0], axis=1)
+        Xf[own] = np.concatenate([own_x, r], axis=1)
+    return Xs, Xf
+
+
+def candidate_predictions_all(solo, thr, cap: int, W, alpha: float) -> np.ndarray:
+    """Every candidate's (coarse, fine) prediction for every decision:
+    [n_dec, 2, E, n_sets] fp64, the product's logical output layout
+    (`CandidateScorer.view`).  W = [n_dec][2][7] (w0..w5, b)."""
+    Xs, Xf = candidate_features_all(solo, thr, cap, alpha)
+    W = np.asarray(W, dtype=float).reshape(-1, 2, 7)
+    out = np.empty((len(W), 2, Xs.shape[0], Xs.shape[1]))
+    for d in range(len(W)):
+        out[d, 0] = Xs @ W[d, 0, :6] + W[d, 0, 6]
+        out[d, 1] = Xf @ W[d, 1, :6] + W[d, 1, 6]
+    return out
+
+
 # ------------------------------------------------ calibration driver (§8f)
 def _slowdown(own, colo, betas, noise: float) -> float:
     """`oracle.py:36-47`: (1 + betas @ max(0, own + colo - 1)) * noise, the

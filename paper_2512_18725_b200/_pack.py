@@ -27,6 +27,7 @@ class TableArrays:
     max_bs: int
     solo: np.ndarray  # [rows]
     thr: np.ndarray  # [rows, 3] (l2, dram, sm)
+    missing: frozenset = frozenset()  # rows with no profile entry (zero-filled; a batch there is a ProfileError)
 
     def row(self, model_id: str, bs: int) -> int:
         return self.models.index(model_id) * self.max_bs + bs - 1

@@ -50,16 +50,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
     os.makedirs(OUT_DIR, exist_ok=True)
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
+
+    extra = os.environ.get("INTF_NVCC_EXTRA", "").split()  # tuning experiments (tools/), e.g. -DINTF_REPLAY_MINB=6
+    cmds, objs = [], []
     for src in sources():
         obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
-        extra = os.environ.get("INTF_NVCC_EXTRA", "").split()  # tuning experiments (tools/), e.g. -DINTF_REPLAY_MINB=6
         cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(-4, "-Xptxas=-v")
             print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        cmds.append(cmd)
         objs.append(obj)
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:  # translation units compile independently
+        for f in [ex.submit(subprocess.run, c, check=True) for c in cmds]:
+            f.result()
     cmd = [nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *objs]
     subprocess.run(cmd, check=True)
     os.replace(OUT + ".tmp", OUT)

@@ -632,6 +632,67 @@ __device__ bool chol_solve(const double* A, const double* b, double* x, double* 
   return true;
 }
 
+// rls_init's P0 = np.linalg.inv(G) (`predict.py:126-131`): LAPACK getrf/getri
+// semantics -- LU with partial pivoting (largest |pivot| in the column), and
+// failure ONLY on an exactly zero pivot (numpy's LinAlgError "Singular
+// matrix"), where the caller retries with G + 1e-8 I.  A nearly singular but
+// invertible G is inverted, as the reference does, not regularised.
+__device__ bool lu_inv7(const double* A, double* inv) {
+  double M[7][14];
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = 0; j < 7; j++) {
+      M[i][j] = A[i * 7 + j];
+      M[i][7 + j] = (i == j) ? 1.0 : 0.0;
+    }
+  for (int c = 0; c < 7; c++) {
+    int piv = c;
+    double best = fabs(M[c][c]);
+    for (int i = c + 1; i < 7; i++)
+      if (fabs(M[i][c]) > best) {
+        best = fabs(M[i][c]);
+        piv = i;
+      }
+    if (best == 0.0) return false;
+    if (piv != c)
+      for (int j = 0; j < 14; j++) {
+        double t = M[c][j];
+        M[c][j] = M[piv][j];
+        M[piv][j] = t;
+      }
+    const double d = M[c][c];
+    for (int i = c + 1; i < 7; i++) {
+      const double f = M[i][c] / d;
+      for (int j = c; j < 14; j++) M[i][j] -= f * M[c][j];
+    }
+  }
+  for (int c = 6; c >= 0; c--) {  // back substitution for the 7 right-hand sides
+    for (int j = 7; j < 14; j++) {
+      double v = M[c][j];
+      for (int k = c + 1; k < 7; k++) v -= M[c][k] * M[k][j];
+      M[c][j] = v / M[c][c];
+    }
+  }
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = 0; j < 7; j++) {
+      inv[i * 7 + j] = M[i][7 + j];
+      fin &= isfinite(M[i][7 + j]);
+    }
+  return fin;
+}
+
+__device__ void p0_inverse(const double* G, double* Pinv) {
+  if (lu_inv7(G, Pinv)) return;
+  double B[49];
+  for (int i = 0; i < 49; i++) B[i] = G[i];
+  for (int i = 0; i < 7; i++) B[i * 8] += 1e-8;  // RIDGE_EPS (`predict.py:131`)
+  lu_inv7(B, Pinv);
+}
+
 // inverse of a lower-triangular 7x7 factor (Li = L^-1, lower triangular)
 __device__ __forceinline__ void tri_inv7(const double L[7][7], double Li[7][7]) {
   double d[7];
@@ -831,7 +892,7 @@ __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, 
           info[0] = 0;
           info[1] = fin ? 0 : 1;
         }
-        if (Pinv) chol_solve(G, nullptr, nullptr, Pinv);  // rls_init P0 = inv(Z^T Z) (`predict.py:126-131`)
+        if (Pinv) p0_inverse(G, Pinv);  // rls_init P0 = inv(Z^T Z) (`predict.py:126-131`)
         return;
       }
     }
@@ -863,14 +924,7 @@ __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, 
       info[0] = 0;
       info[1] = fin ? 0 : 1;
     }
-    if (Pinv) {
-      double B[49];
-      for (int i = 0; i < 49; i++) B[i] = G[i];
-      if (!chol_solve(B, nullptr, nullptr, Pinv)) {
-        for (int i = 0; i < 7; i++) B[i * 8] += 1e-8;
-        chol_solve(B, nullptr, nullptr, Pinv);
-      }
-    }
+    if (Pinv) p0_inverse(G, Pinv);
     return;
   }
   const bool ridge = rank < 7;
@@ -893,14 +947,7 @@ __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, 
     info[0] = ridge ? 1 : 0;
     info[1] = fin ? 0 : 1;
   }
-  if (Pinv) {  // rls_init P0 = inv(Z^T Z), ridge on failure (`predict.py:126-131`)
-    double B[49];
-    for (int i = 0; i < 49; i++) B[i] = G[i];
-    if (!chol_solve(B, nullptr, nullptr, Pinv)) {
-      for (int i = 0; i < 7; i++) B[i * 8] += 1e-8;
-      chol_solve(B, nullptr, nullptr, Pinv);
-    }
-  }
+  if (Pinv) p0_inverse(G, Pinv);  // rls_init P0 = inv(Z^T Z), ridge only on an exact zero pivot
 }
 
 __global__ void k_ols_solve(const double* __restrict__ stats, const double* __restrict__ qr, double* params,

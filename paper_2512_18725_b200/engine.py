@@ -51,6 +51,9 @@ class DeviceTable:
         self.struct = _abi.Table(self.solo.data_ptr(), self.thr.data_ptr(), len(table.solo), int(table.max_bs))
 
 
+NOISE_K = 6  # noise draws precomputed per batch (measured best: profiles/noise_k_r1m.txt)
+
+
 class ReplayPipeline:
     """Buffers + launches for one packed batch of scenarios.
 
@@ -66,7 +69,7 @@ class ReplayPipeline:
         self.seg_stride = int(seg_stride)
         self.dtable = dtable or DeviceTable(table, self.dev)
         # noise draws precomputed per batch (the rest are drawn on the replay chain)
-        self.noise_k = int(noise_k if noise_k is not None else os.environ.get("INTF_NOISE_K", "6"))
+        self.noise_k = int(noise_k if noise_k is not None else NOISE_K)
         sz = _pack.sizes(self.pb, self.seg_stride, self.noise_k)
         self.t = {f: torch.zeros(sz[k], dtype=_TORCH_DT[dt], device=self.dev) for f, dt, k in _pack.BUFFER_PLAN}
         self.B = _abi.ReplayBuffers()

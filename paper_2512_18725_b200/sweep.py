@@ -13,6 +13,16 @@ import numpy as np
 
 from .profiles import DEFAULT_ARCHETYPES, Archetype, gen_synthetic_profiles
 
+# C1: the reference's bundled trace `pkg/scenarios/mixed_three_model.json` (3 models, cap 2, seed 7)
+BUNDLED_SEED7 = {
+    "name": "mixed_three_model", "duration_s": 5.0, "batching_window_ms": 4.0, "max_batch_size": 8,
+    "concurrency_cap": 2, "seed": 7, "colocation_mode": "static", "ewma_alpha": 1.0,
+    "oracle": {"beta_l2": 1.0, "beta_dram": 1.5, "beta_sm": 0.5, "noise_sigma": 0.05, "seed": 0},
+    "deployed": [{"model_id": "resnet50", "arrival_rate_rps": 588.2352941176472, "slo_ms": 10.0},
+                 {"model_id": "roberta_b", "arrival_rate_rps": 52.70834726810264, "slo_ms": 30.0},
+                 {"model_id": "vit_b16", "arrival_rate_rps": 116.95906432748538, "slo_ms": 22.5}],
+}
+
 
 def c5_scenario(table, i: int) -> dict:
     rng = np.random.default_rng([2512, i])
@@ -37,6 +47,17 @@ def c5_scenario(table, i: int) -> dict:
 
 def c5_scenarios(table, n: int, start: int = 0) -> list:
     return [c5_scenario(table, i) for i in range(start, start + n)]
+
+
+def expected_requests(spec: dict) -> float:
+    """lambda*T of a scenario dict: its expected request count (shard weight)."""
+    return sum(d["arrival_rate_rps"] for d in spec["deployed"]) * spec["duration_s"]
+
+
+def lpt_order(specs: list) -> list:
+    """Longest-processing-time first by expected requests (stable): the
+    heaviest scenarios get the first replay warps."""
+    return sorted(specs, key=lambda d: -expected_requests(d))
 
 
 def table16():
@@ -71,3 +92,26 @@ def c4_scenario(table16_, arch, n_requests: float = 1e6, rho: float = 0.5, seed:
         "oracle": {"beta_l2": 1.0, "beta_dram": 1.5, "beta_sm": 0.5, "noise_sigma": 0.05, "seed": 1},
         "deployed": dep,
     }
+
+
+def c2_decision_coefs(n_dec: int, alpha: float = 0.5) -> np.ndarray:
+    """C2 decisions: [n_dec][2][7] coarse (static) / fine (EWMA alpha) OLS
+    refits (`predict.py:53-72`) on growing windows of the bundled trace's
+    samples (`mixed_three_model.json`, seed 7) -- the coefficients a
+    scheduler refitting as samples arrive would hold at n_dec decisions."""
+    from . import engine
+    from .colocation import STATIC_MODE, ewma_mode, features_for_modes
+    from .simcore import run_scenario
+    from .workload import scenario_from_dict
+
+    table = gen_synthetic_profiles()
+    res = run_scenario(scenario_from_dict(BUNDLED_SEED7), table)
+    X, y, _ = features_for_modes(res.outcomes, table, [STATIC_MODE, ewma_mode(alpha)])
+    n = len(y)
+    W = np.zeros((n_dec, 2, 7))
+    for d in range(n_dec):
+        hi = max(64, int(n * (d + 1) / n_dec))
+        for k in range(2):
+            params, _, _, _ = engine.ols_solve(engine.ols_stats(X[k, :hi], y[:hi]))
+            W[d, k] = params
+    return W

@@ -337,14 +337,14 @@ def candidates_golden(table):
         fits.append(pr.fit_ols(ex.split_samples(smp)[0]))
     arrs = {"w": np.array([np.append(f.w, f.b) for f in fits]), "alpha": np.array(0.5)}
     profiles = [table.get(models[e // mbs], e % mbs + 1) for e in range(E)]
-    for cap in (2, 3):
+    for cap in (2, 3, 4):
         own_l, peers_l, yc, yf = [], [], [], []
         rng = np.random.default_rng(cap)
         for own in range(E):
             multisets = [()]
             for k in range(1, cap):
                 multisets += list(itertools.combinations_with_replacement(range(E), k))
-            if cap == 3:  # subsample: keep the fixture small
+            if cap >= 3:  # subsample: keep the fixture small
                 pick = rng.choice(len(multisets), size=40, replace=False)
                 multisets = [multisets[i] for i in sorted(pick)]
             for peers in multisets:
@@ -379,6 +379,9 @@ def candidates_golden(table):
 def main():
     table = load_profiles("/root/reference/pkg/profiles/default.csv")
     assert table.entries == gen_synthetic_profiles().entries
+    if "--candidates" in sys.argv:  # only candidates_golden.npz
+        candidates_golden(table)
+        return
     t16 = table16()
     rng_golden()
     replay_golden(table, t16)

@@ -160,3 +160,27 @@ def test_windowed_refit_matches_reference(window):
     # the first window equals the single-fit path
     m0 = p.fit_ols_xy(R["X"][:window], R["y"][:window])
     np.testing.assert_allclose(got[0], m0.w7(), rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("eps", [1e-5, 1e-6, 0.0])
+def test_rls_init_p0_near_collinear_matches_numpy_inv(eps):
+    """rls_init's P0 = np.linalg.inv(Z^T Z) (`predict.py:126-131`): LU with
+    partial pivoting, ridge only on an exactly singular design (eps = 0: two
+    identical columns, numpy's LinAlgError -> inv(G + 1e-8 I)).  At cond(G)
+    5.8e10 / 4.5e12 the reference's P0 differs from the ridge form by 43% / 98%,
+    so a Cholesky-failure ridge would be visible here."""
+    import paper_2512_18725_b200 as p
+
+    rng = np.random.default_rng(3)
+    X = rng.uniform(0, 1, size=(300, 6))
+    X[:, 5] = X[:, 4] + eps * rng.standard_normal(300)
+    Z = np.column_stack([X, np.ones(300)])
+    G = Z.T @ Z
+    try:
+        ref = np.linalg.inv(G)
+    except np.linalg.LinAlgError:
+        ref = np.linalg.inv(G + 1e-8 * np.eye(7))
+    st = p.rls_init(p.LinearModel(w=np.zeros(6), b=0.0), X_train=X)
+    # the device's Z^T Z sums in another order: P0 moves by ~cond(G) * eps_64 relative
+    tol = {1e-5: 1e-3, 1e-6: 3e-2, 0.0: 1e-4}[eps]
+    assert np.linalg.norm(st.P - ref) / np.linalg.norm(ref) < tol

@@ -145,3 +145,29 @@ def test_oracle_percentile_examples():
     assert O.percentile([15, 20, 35, 40, 50], 40) == 20
     assert O.percentile([3, 1, 2], 100) == 3
     assert O.percentile([5], 0) == 5
+
+
+@pytest.mark.parametrize("cap", [2, 3, 4])
+def test_vectorised_candidate_restatement_matches_reference(cap):
+    """`oracle.candidate_predictions_all` (the checker of the full C2
+    enumeration on the GPU) against predictions the reference's own
+    functions composed (cap 2 in full, cap 3/4 subsampled); the only
+    difference allowed is the ddot's fma rounding (~1e-16)."""
+    from paper_2512_18725_b200 import engine
+
+    tab = _golden.table("default")
+    C = _golden.load("candidates_golden.npz")
+    Y = O.candidate_predictions_all(tab.solo, tab.thr, cap, C["w"][None], float(C["alpha"]))[0]
+    own, peers = C[f"cap{cap}/own"], C[f"cap{cap}/peers"]
+    M = O.multisets(len(tab.solo), cap)
+    idx = np.array([engine.multiset_rank([q for q in pe if q >= 0], len(tab.solo), cap) for pe in peers])
+    for i, pe in zip(idx, peers):
+        assert list(M[i][M[i] >= 0]) == sorted(q for q in pe if q >= 0)
+    np.testing.assert_allclose(Y[0, own, idx], C[f"cap{cap}/y_coarse"], rtol=1e-14, atol=0)
+    np.testing.assert_allclose(Y[1, own, idx], C[f"cap{cap}/y_fine"], rtol=1e-14, atol=0)
+    # and the scalar restatement's features bit for bit on a sample
+    Xs, Xf = O.candidate_features_all(tab.solo, tab.thr, cap, float(C["alpha"]))
+    for o, pe, i in list(zip(own, peers, idx))[::37]:
+        hist = O.candidate_history(int(o), [q for q in pe if q >= 0], tab.solo, tab.thr)
+        assert np.array_equal(Xs[o, i], O.features(hist, tab.thr[o], False, 1.0))
+        assert np.array_equal(Xf[o, i], O.features(hist, tab.thr[o], True, float(C["alpha"])))

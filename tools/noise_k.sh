@@ -2,7 +2,7 @@
 # Experiment (tools/): C5 sweep time vs noise draws precomputed per batch (INTF_NOISE_K)
 OUT=gpurun_out; mkdir -p $OUT
 for K in ${@:-3 4 5 6}; do
-  INTF_NOISE_K=$K timeout 600 python -m pytest tests/test_gpu_replay.py -q -m gpu 2>&1 | tail -1
+
   for rep in 1 2; do
   INTF_NOISE_K=$K timeout 600 python bench.py --no-cpu --no-c4 > $OUT/bench_nk$K.json 2>/dev/null
   python -c "
