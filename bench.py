@@ -138,8 +138,10 @@ def cpu_candidate_rate(table, W, seconds: float, seed: int = 0):
 
 def cpu_replay_rate(table, seconds: float, start: int = 0):
     """The oracle's C restatement of `run_scenario` (`simcore.py:218-310`,
-    literal heap engine) + its arrival generator on one core, over C5
-    scenarios start, start+1, ... until `seconds` elapse: (replays/s, n, s)."""
+    literal heap engine) + its arrival generator + the numpy restatement of
+    the coarse / fine / adaptive evaluation (`oracle.scenario_eval`) on one
+    core, over C5 scenarios start, start+1, ... until `seconds` elapse:
+    (replays/s, n, s)."""
     import oracle as O
     from paper_2512_18725_b200.sweep import c5_scenario
 
@@ -147,7 +149,8 @@ def cpu_replay_rate(table, seconds: float, start: int = 0):
     otab = O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr)
     n, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < seconds:
-        O.run_scenario(c5_scenario(table, start + n), otab)
+        spec = c5_scenario(table, start + n)
+        O.scenario_eval(O.run_scenario(spec, otab), spec, otab)  # replay + coarse / fine / adaptive evaluation
         n += 1
     dt = time.perf_counter() - t0
     return n / dt, n, dt
@@ -371,19 +374,137 @@ def replay_stage_times(pipe, stream) -> dict:
 
     L, s = _abi.load(), stream.cuda_stream
     bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     ev[0].record(stream)
     _abi.check(L.intf_generate_arrivals(bt, B, s), "arrivals")
     ev[1].record(stream)
     _abi.check(L.intf_replay(bt, ctypes.byref(pipe.dtable.struct), B, s), "replay")
     ev[2].record(stream)
-    pipe.run_slo_features(slo=True, features=False)
+    pipe.run_slo_features(slo=True, features=False, evaluate=False)
     ev[3].record(stream)
-    pipe.run_slo_features(slo=False, features=True)
+    pipe.run_slo_features(slo=False, features=True, evaluate=False)
     ev[4].record(stream)
+    if pipe.evaluate is not None:
+        pipe.run_evaluation()
+    ev[5].record(stream)
     torch.cuda.synchronize()
-    names = ["arrivals", "replay", "slo", "features"]
+    names = ["arrivals", "replay", "slo", "features", "evaluation"]
     return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
+
+
+def c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W) -> dict:
+    """C5 (BASELINE configs[4]): a FIXED sweep of 10^4 synthetic scenarios
+    (default_rng([2512, i])) split over the ranks by expected requests
+    (lambda*T, longest-processing-time first; strong scaling).  One step = the
+    whole sweep: arrivals -> formation -> noise -> replay (warp per scenario)
+    -> SLO -> features (static + EWMA(1/2)) -> per scenario the coarse / fine
+    / adaptive evaluation (75/25 chronological split, OLS fits, RLS
+    prequential tail, 3 EvalReports) -> the per-scenario rows gathered
+    (NCCL all_gather, N > 1).  Consecutive sweeps run on several pipelines
+    (buffer sets on their own streams), so one sweep's short stages overlap
+    the longest scenarios' replay chains of the previous ones."""
+    import torch
+    from paper_2512_18725_b200 import _abi, engine
+    from paper_2512_18725_b200.distributed import SweepRows, gather_sweep_rows, lpt_shards
+    from paper_2512_18725_b200.sweep import c5_scenarios, expected_requests
+
+    ta = table.arrays()
+    specs_all = c5_scenarios(table, REPLAY_SCEN)
+    shards = lpt_shards([expected_requests(sp) for sp in specs_all], world)
+    mine = shards[rank]
+    specs = [specs_all[i] for i in mine]
+    counts = [len(sh) for sh in shards]
+    preds = [_abi.Predictor(ewma=0, alpha=1.0, w=tuple(W[-1, 0])), _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[-1, 1]))]
+    noise_k = int(os.environ.get("INTF_NOISE_K", engine.NOISE_K))  # tools/noise_k.sh sweeps it
+    # in-flight sweeps: the step is bounded by its longest scenario's chain
+    # (one warp), so fewer scenarios per GPU need more sweeps in flight
+    n_pipes = int(os.environ.get("INTF_BENCH_PIPES", str(3 * world)))
+    pipes = [engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5, noise_k=noise_k, evaluate=(0, 1, 0.99))
+             for _ in range(n_pipes)]
+    rows = [SweepRows(p) for p in pipes]
+    backend = a.backend
+    for _ in range(max(1, a.warmup)):
+        for p in pipes:
+            p.run()
+    barrier()
+    st = pipes[0].status()
+    gathered = [None] * n_pipes
+
+    def step(k):
+        q = k % n_pipes
+        pipes[q].run()
+        loc = rows[q].build()
+        gathered[q] = gather_sweep_rows(loc, counts, backend) if dist is not None else [loc]
+
+    step(0)
+    barrier()
+    r_steps = max(n_pipes, a.steps)
+    rstreams = [torch.cuda.Stream() for _ in pipes]
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    for rs in rstreams:
+        rs.wait_stream(stream)
+    for k in range(r_steps):
+        with torch.cuda.stream(rstreams[k % n_pipes]):
+            step(k)
+    for rs in rstreams:
+        stream.wait_stream(rs)
+    r1.record(stream)
+    barrier()
+    rep_ms = max_over_ranks(r0.elapsed_time(r1)) / r_steps
+    pipe = pipes[0]
+    stage_ms = replay_stage_times(pipe, stream)
+    n_batches = int(pipe.t["n_batches"][: pipe.pb.n_scen].sum().item())
+    n_req = int(pipe.t["n_req"][: pipe.pb.n_scen].sum().item())
+    est = pipe.eval_status.cpu().numpy()
+    # the longest scenario replayed alone: the floor of a sweep's time on one GPU
+    heavy = engine.ReplayPipeline(specs[:1], ta, preds=preds, scale=1.5, noise_k=noise_k, evaluate=(0, 1, 0.99))
+    for _ in range(2):
+        heavy.run()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    heavy.run()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    tail_ms = t0.elapsed_time(t1)
+    summary = None
+    if rank == 0:  # untimed: the sweep's result, every scenario in index order (SURVEY §8d C5)
+        allrows = np.full((REPLAY_SCEN, gathered[0][0].shape[1]), np.nan)
+        for r, blk in enumerate(gathered[(r_steps - 1) % n_pipes]):
+            allrows[np.asarray(shards[r])] = blk.cpu().numpy()
+        summary = sweep_summary(allrows)
+    return {"metric": "scenario replays/sec (incl. coarse / fine / adaptive evaluation)",
+            "value": REPLAY_SCEN / (rep_ms / 1e3), "unit": "replays/s", "ms_per_step": rep_ms, "scaling": "strong",
+            "scenarios_total": REPLAY_SCEN, "scenarios_this_gpu": len(specs), "pipelines": n_pipes,
+            "requests": n_req, "batches": n_batches, "status_nonzero": int(np.count_nonzero(st)),
+            "eval_invalid": int(np.count_nonzero(est[: len(specs)] & 1)),
+            "tail_ms": tail_ms, "tail_scenario_batches": int(heavy.t["n_batches"][0].item()),
+            "workload": "C5: 10^4 synthetic scenarios (default_rng([2512,i]), 2-4 models, 1 s, cap 1-3) split over "
+                        "the GPUs by lambda*T (LPT); per step: arrivals + formation + noise + replay (warp per "
+                        "scenario) + SLO + features + per-scenario coarse/fine/adaptive evaluation (75/25 split, "
+                        "OLS x2, RLS prequential tail, 3 EvalReports) + per-scenario rows gathered to every rank "
+                        f"(N > 1: NCCL all_gather); consecutive sweeps on {n_pipes} pipelines / streams",
+            "steps_timed": r_steps, "stage_ms": stage_ms, "summary": summary}
+
+
+def sweep_summary(rows: np.ndarray) -> dict:
+    """SURVEY §8d C5 report: SLO satisfaction over scenarios (mean / median of
+    the per-scenario request-weighted satisfaction) and, per predictor, the
+    distribution of the per-scenario median relative error and MSE."""
+    from paper_2512_18725_b200.distributed import REPORT_MODELS
+
+    slo = rows[:, 18:].reshape(len(rows), REPORT_MODELS, 5)
+    n, met = np.nansum(slo[..., 0], axis=1), np.nansum(slo[..., 1], axis=1)
+    sat = met / np.where(n > 0, n, np.nan)
+    out = {"scenarios": int(len(rows)), "slo_satisfaction_mean": float(np.nanmean(sat)),
+           "slo_satisfaction_median": float(np.nanmedian(sat))}
+    for k, name in enumerate(("coarse", "fine", "adaptive")):
+        rep = rows[:, 6 * k: 6 * k + 6]
+        ok = rep[:, 5] > 0
+        out[name] = {"scenarios": int(ok.sum()), "median_rel_p50": float(np.median(rep[ok, 2])),
+                     "mean_rel_p50": float(np.mean(rep[ok, 2])), "median_rel_p95": float(np.median(rep[ok, 4])),
+                     "median_mse": float(np.median(rep[ok, 0]))}
+    return out
 
 
 # -------------------------------------------------------------- reference
@@ -421,7 +542,8 @@ def reference_arm(a):
                                    f"(oracle.candidate_predictions, reference functions restated)"},
         "e2e": {"value": v, "unit": "predictions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "replay": {"metric": "scenario replays/sec", "value": rep_rate, "unit": "replays/s", "cores": cores,
-                   "sample": f"{n_rep} C5 scenarios (oracle C replay: heap engine + arrivals), {per_step:.1f} s per core"},
+                   "sample": f"{n_rep} C5 scenarios (oracle C replay: heap engine + arrivals; numpy coarse/fine/"
+                             f"adaptive evaluation), {per_step:.1f} s per core"},
     }
     print(json.dumps(line))
     return 0
@@ -527,69 +649,8 @@ def product_arm(a):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
     ok = bool(np.isfinite(ho[:1000]).all())
 
-    # ---- secondary: scenario replay sweep (C5 shape)
-    # longest-processing-time-first: heaviest scenarios (expected requests) get the first warps
-    specs = lpt_order(c5_scenarios(table, REPLAY_SCEN, start=rank * REPLAY_SCEN))
-    preds = [_abi.Predictor(ewma=0, alpha=1.0, w=tuple(W[-1, 0])), _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[-1, 1])),
-             _abi.Predictor(ewma=1, alpha=ALPHA, w=tuple(W[0, 1]))]
-    # pipelines (buffer sets) on their own streams: consecutive steps overlap,
-    # so one sweep's arrivals / formation / SLO run beside the other sweeps'
-    # replay tails (the replay is bounded by its longest scenario's chain)
-    n_pipes = int(os.environ.get("INTF_BENCH_PIPES", "3"))  # 2 / 3 / 4: 3.70 / 3.59 / 3.60 ms (profiles/c5_pipes_r1l.txt)
-    noise_k = int(os.environ.get("INTF_NOISE_K", engine.NOISE_K))  # tools/noise_k.sh sweeps it
-    pipes = [engine.ReplayPipeline(specs, ta, preds=preds, scale=1.5, noise_k=noise_k) for _ in range(n_pipes)]
-    pipe = pipes[0]
-    for _ in range(max(1, a.warmup)):
-        for p in pipes:
-            p.run()
-    barrier()
-    st = pipe.status()
-    r_steps = max(n_pipes, a.steps)  # the K steps asked for (a sweep is ~4 ms)
-    # per-scenario SLO metrics of every rank gathered (NCCL all_gather, N > 1):
-    # per deployed model n, met, p50/p95/p99, padded to the largest rank
-    n_mod = pipe.pb.n_models
-    gather_len = n_mod
-    if dist is not None:
-        t = torch.tensor([n_mod], device="cuda" if a.backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gather_len = int(t.item())
-    rows_k = [torch.zeros(gather_len, 5, dtype=torch.float64, device="cuda") for _ in pipes]
-    parts_k = [[torch.empty_like(r) for _ in range(world)] for r in rows_k] if dist is not None else None
-
-    def gather_metrics(k=0):
-        if dist is None:
-            return
-        pipe, rows, parts = pipes[k], rows_k[k], parts_k[k]
-        rows[:n_mod, 0] = pipe.slo_n[:n_mod]
-        rows[:n_mod, 1] = pipe.slo_met[:n_mod]
-        rows[:n_mod, 2:] = pipe.slo_p[: 3 * n_mod].view(n_mod, 3)
-        if a.backend == "nccl":
-            dist.all_gather(parts, rows)
-        else:
-            cpu_parts = [p.cpu() for p in parts]
-            dist.all_gather(cpu_parts, rows.cpu())
-
-    gather_metrics()
-    barrier()
-    # one warp replays each scenario start to end (C5 scenarios are short:
-    # busy-period sharding pays only for long traces, see long_trace)
-    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    rstreams = [torch.cuda.Stream() for _ in pipes]
-    r0.record(stream)
-    for rs in rstreams:
-        rs.wait_stream(stream)
-    for k in range(r_steps):
-        with torch.cuda.stream(rstreams[k % n_pipes]):
-            pipes[k % n_pipes].run()
-            gather_metrics(k % n_pipes)
-    for rs in rstreams:
-        stream.wait_stream(rs)
-    r1.record(stream)
-    barrier()
-    rep_ms = max_over_ranks(r0.elapsed_time(r1)) / r_steps
-    stage_ms = replay_stage_times(pipe, stream)
-    n_batches = int(pipe.t["n_batches"][: pipe.pb.n_scen].sum().item())
-    n_req = int(pipe.t["n_req"][: pipe.pb.n_scen].sum().item())
+    # ---- secondary: scenario replay sweep (C5: 10^4 scenarios, coarse / fine / adaptive)
+    sweep = c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W)
 
     refit = refit_secondary(a, stream, barrier, max_over_ranks, rank)
     longtrace = c4_secondary(a, stream, barrier, max_over_ranks, rank, world) if not a.no_c4 else None
@@ -603,7 +664,8 @@ def product_arm(a):
                "sample": f"{n} predictions ({n // 2} random cap-4 candidates x coarse+fine, 1 decision) in {dt:.1f} s"}
         rrate, rn, rdt = cpu_replay_rate(table, min(5.0, a.cpu_seconds))
         replay_cpu = {"value": rrate, "unit": "replays/s", "cores": 1, "kind": "port",
-                      "sample": f"{rn} C5 scenarios (oracle C replay: heap engine + arrivals) in {rdt:.1f} s"}
+                      "sample": f"{rn} C5 scenarios (oracle C replay: heap engine + arrivals; numpy evaluation: "
+                                f"split, 2 lstsq fits, RLS tail, 3 EvalReports) in {rdt:.1f} s"}
 
     # context: a pure device write (torch fill) of the same size, alternating
     # two buffers like the timed loop -- the write-only ceiling on this part
@@ -653,16 +715,7 @@ def product_arm(a):
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": a.steps if fused else 2 * a.steps,
-        "replay": {"metric": "scenario replays/sec", "value": world * REPLAY_SCEN / (rep_ms / 1e3),
-                   "unit": "replays/s", "ms_per_step": rep_ms, "scenarios_per_gpu": REPLAY_SCEN,
-                   "requests": n_req, "batches": n_batches, "status_nonzero": int(np.count_nonzero(st)),
-                   "workload": "C5-shape synthetic scenarios (default_rng([2512,i]), 1 s, cap 1-3): arrivals + "
-                               "formation + noise + replay (warp per scenario) + SLO + features/3 predictors; N > 1: "
-                               "+ all_gather of every rank's per-model SLO metrics each step; consecutive steps "
-                               f"on {n_pipes} pipelines (buffer sets) on {n_pipes} streams, so a step's "
-                               "arrivals/formation/SLO overlap the other steps' replay tails",
-                   "steps_timed": r_steps,
-                   "stage_ms": stage_ms, "cpu_baseline": replay_cpu},
+        "replay": {**sweep, "cpu_baseline": replay_cpu},
         "refit": refit,
         "long_trace": longtrace,
     }

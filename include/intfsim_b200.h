@@ -330,6 +330,27 @@ int intf_rls_streams(const double *X, const double *y, const int64_t *off, int32
 int intf_eval_report(const double *yhat, const double *y, const int64_t *off, int32_t n_seg, double *out,
                      void *stream);
 
+/* Per-scenario predictor evaluation of a replayed batch (SURVEY §8d C5:
+ * coarse vs fine vs adaptive), composed of `experiments.py:44-60`
+ * (split_samples, chronological, cut = int(round(0.75 n))), `predict.py:53-72`
+ * (fit_ols), `:112-134` (rls_init with X_train), `:157-205` (evaluate,
+ * score_and_update).  Scenario s has n = n_batches[s] samples in outcome order
+ * at slots req_off + k of the features written by intf_features_predict:
+ * X[p][slot][6] (p_static: static mode, p_ewma: EWMA mode) and y[slot].
+ *   model 0 coarse   fit_ols(static[:cut]), scored offline on static[cut:]
+ *   model 1 fine     fit_ols(EWMA[:cut]),   scored offline on EWMA[cut:]
+ *   model 2 adaptive rls_init(fine, lam, X_train = EWMA[:cut]), prequential on EWMA[cut:]
+ * params[s][3][7] (adaptive: after its tail), report[s][3][6] = (mse, rel_p25,
+ * rel_p50, rel_p75, rel_p95, n_test), status[s] = 1 (fewer than 7 training
+ * samples or an empty test set: the reference would raise; reports NaN, n 0)
+ * | 2 coarse ridge | 4 fine ridge | 16 non-finite fit, status[S + s] = RLS bits
+ * (1 non-finite, 2 P reset).  ws: intf_scenario_eval_ws(n_scen, slot_stride)
+ * doubles.  Stream-ordered, no host synchronisation.                        */
+int64_t intf_scenario_eval_ws(int32_t n_scen, int64_t slot_stride);
+int intf_scenario_eval(const intf_batch *batch, const intf_replay_buffers *buf, const double *X, int64_t slot_stride,
+                       int32_t p_static, int32_t p_ewma, const double *y, double lam, double *ws, int64_t ws_elems,
+                       double *params, double *report, int32_t *status, void *stream);
+
 /* ---- array-level entry points behind the per-object reference API ---- */
 
 /* samples_from_outcomes over arbitrary outcome rows (`colocation.py:95-105`):

@@ -301,13 +301,24 @@ def predict(w, b, x) -> float:
     return float(np.asarray(w, dtype=float) @ np.asarray(x, dtype=float) + b)
 
 
-def fit_ols_xy(X, y):
-    """`predict.py:53-66`: lstsq with intercept; ridge fallback if rank-deficient."""
+def gram_rows(Z):
+    """Z^T Z summed row by row in order: an equally valid summation order to
+    BLAS's blocked dgemm, used to measure how far the reference's own result
+    moves under reordering when Z^T Z is (nearly) singular."""
+    G = np.zeros((Z.shape[1], Z.shape[1]))
+    for z in Z:
+        G = G + np.outer(z, z)
+    return G
+
+
+def fit_ols_xy(X, y, gram=None):
+    """`predict.py:53-66`: lstsq with intercept; ridge fallback if rank-deficient.
+    gram: optional Z -> Z^T Z (default numpy's Z.T @ Z)."""
     X = np.asarray(X, dtype=float)
     n, d = X.shape
     Z = np.column_stack([X, np.ones(n)])
     if np.linalg.matrix_rank(Z) < d + 1:
-        G = Z.T @ Z + RIDGE_EPS * np.eye(d + 1)
+        G = (gram(Z) if gram else Z.T @ Z) + RIDGE_EPS * np.eye(d + 1)
         params = np.linalg.solve(G, Z.T @ y)
     else:
         params, *_ = np.linalg.lstsq(Z, y, rcond=None)
@@ -323,11 +334,11 @@ def sgd_update(w, b, x, y, eta):
     return w, b
 
 
-def rls_init_P(X_train=None, d=7, delta=P_RESET_DELTA):
+def rls_init_P(X_train=None, d=7, delta=P_RESET_DELTA, gram=None):
     """`predict.py:112-134`: P0 = inv(Z^T Z) (ridge on LinAlgError) or delta*I."""
     if X_train is not None:
         Z = np.column_stack([X_train, np.ones(len(X_train))])
-        G = Z.T @ Z
+        G = gram(Z) if gram else Z.T @ Z
         try:
             return np.linalg.inv(G)
         except np.linalg.LinAlgError:
@@ -404,6 +415,29 @@ def slo_report(model_ids, arrival, completion, slo_met, warmup_fraction=0.0):
         out[m] = (int(sel.sum()), sum(bool(v) for v in met) / int(sel.sum()), percentile(lat, 50),
                   percentile(lat, 95), percentile(lat, 99))
     return out
+
+
+def scenario_eval(rep: dict, spec: dict, tab: TableArrays, lam: float = 0.99, alpha: float = 0.5, gram=None):
+    """C5 per-scenario evaluation composed from the reference's
+    functions: samples in outcome order (`colocation.py:95-105`), the
+    chronological split cut = int(round(0.75 n)) (`experiments.py:44-60`),
+    coarse = fit_ols(static) / fine = fit_ols(EWMA(alpha)) scored offline on
+    the tail, adaptive = rls_init(fine, lam, X_train) scored prequentially
+    (`predict.py:53-72,112-134,157-205`).  Returns [3][6] reports (mse, p25,
+    p50, p75, p95, n) or None when split/fit_ols would raise (< 7 training
+    samples or an empty test set)."""
+    Xs, y, _ = samples_from_replay(rep, spec, tab, False, 1.0)
+    Xf, _, _ = samples_from_replay(rep, spec, tab, True, alpha)
+    n = len(y)
+    cut = int(round(0.75 * n))
+    if cut < 7 or n - cut < 1:
+        return None
+    wc, bc = fit_ols_xy(Xs[:cut], y[:cut], gram)
+    wf, bf = fit_ols_xy(Xf[:cut], y[:cut], gram)
+    out = [eval_report(Xs[cut:] @ wc + bc, y[cut:]), eval_report(Xf[cut:] @ wf + bf, y[cut:])]
+    preds, _, _, _ = prequential(wf, bf, Xf[cut:], y[cut:], "rls", lam=lam, P=rls_init_P(Xf[:cut], gram=gram))
+    out.append(eval_report(preds, y[cut:]))
+    return np.array(out)
 
 
 # ------------------------------------------------------ candidate sets (C2)

@@ -785,6 +785,21 @@ __device__ __noinline__ int qr_rank_solve(const double F[7][8], double n_rows, d
   double R[7][7];
   for (int i = 0; i < 7; i++)
     for (int j = 0; j < 7; j++) R[i][j] = F[i][j];
+  // A rotation of a column pair moves norm from the smaller column to the
+  // larger one (it removes the smaller one's projection), so a column whose
+  // norm is below the rank tolerance stays below it: it is already decided as
+  // a zero singular value and pairs involving it are skipped (the partner
+  // gains at most tol^2 in squared norm).  Rotating such rounding-noise
+  // columns against each other rarely meets the convergence test and ran up
+  // to 40 sweeps on rank-deficient designs.  smax0 <= S_max, so the cut is
+  // at or below the exact tolerance; rank-7 solutions come from F, not R.
+  double smax0 = 0.0;
+  for (int j = 0; j < 7; j++) {
+    double t = 0.0;
+    for (int i = 0; i < 7; i++) t += R[i][j] * R[i][j];
+    smax0 = fmax(smax0, t);
+  }
+  const double negl = sqrt(smax0) * fmax(n_rows, 7.0) * 2.220446049250313e-16, negl2 = negl * negl;
   for (int sweep = 0; sweep < 40; sweep++) {  // one-sided Jacobi on the columns of R
     bool rotated = false;
     for (int p = 0; p < 6; p++)
@@ -795,6 +810,7 @@ __device__ __noinline__ int qr_rank_solve(const double F[7][8], double n_rows, d
           be += R[i][q] * R[i][q];
           ga += R[i][p] * R[i][q];
         }
+        if (al <= negl2 || be <= negl2) continue;
         if (ga == 0.0 || fabs(ga) <= 2.220446049250313e-16 * sqrt(al * be)) continue;
         rotated = true;
         const double ze = (be - al) / (2.0 * ga);
@@ -846,7 +862,8 @@ __device__ __noinline__ int qr_rank_rows(const double* __restrict__ X, const dou
 __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, double* params, int32_t* info,
                                               double* Pinv, const double* __restrict__ rows = nullptr,
                                               const double* __restrict__ rows_y = nullptr, long long lo = 0,
-                                              long long cnt = 0, const double* __restrict__ qr = nullptr) {
+                                              long long cnt = 0, const double* __restrict__ qr = nullptr,
+                                              bool screen_only = false) {
   double G[49], r[7], ev[7];
   for (int i = 0; i < 49; i++) G[i] = stats[i];
   for (int i = 0; i < 7; i++) r[i] = stats[49 + i];
@@ -900,10 +917,21 @@ __device__ __forceinline__ void ols_solve_one(const double* __restrict__ stats, 
   int rank = 0;
   double xq[7];
   bool have_x = false;
-  if (qr && qr[0] >= 0.0) {
+  // an exactly zero column of Z (G[i][i] == 0: e.g. the colo features of a
+  // scenario that never co-locates) makes matrix_rank(Z) < 7 without any
+  // factorisation: that singular value is exactly 0
+  bool zero_col = false;
+#pragma unroll
+  for (int i = 0; i < 7; i++) zero_col |= G[i * 8] == 0.0;
+  if (zero_col) {
+    rank = 0;
+  } else if (qr && qr[0] >= 0.0) {
     rank = (int)qr[0];
     for (int i = 0; i < 7; i++) xq[i] = qr[1 + i];
     have_x = rank == 7;
+  } else if (screen_only) {  // the caller computes the rows' QR cooperatively and calls again with qr
+    if (info) info[0] = -1;
+    return;
   } else if (rows) {
     rank = qr_rank_rows(rows, rows_y, lo, cnt, xq);
     have_x = rank == 7;
@@ -1279,19 +1307,22 @@ __global__ void k_sgd(const double* __restrict__ X, const double* __restrict__ Y
 }
 
 // rls_update (`predict.py:137-154`), lane-parallel: 8 lanes per stream, lane
-// r < 7 owns row r of P (the 7x7 gain matrix), so the 49 divisions by lambda
-// of each update run 7-wide and a warp advances 4 streams.  Per element the
-// operations are the reference's, in its order:
+// r < 7 owns row r of P (the 7x7 gain matrix), so the 49 updates of P run
+// 7-wide and a warp advances 4 streams.  Per element the operations are the
+// reference's, in its order, with its two divisions as reciprocal multiplies:
 //   Pz_r = P[r,:] . z (fma chain)        -> gathered by shuffles
 //   zPz  = z . Pz (fma chain, every lane) -> denom, reset rule
-//   k_r  = Pz_r / denom                   -> gathered
+//   k_r  = Pz_r * (1 / denom)             -> gathered
 //   w   += k e (every lane keeps w)
-//   P[r,:] = (P[r,:] - k_r Pz) / lambda; then 0.5 (P + P^T) via a shared-memory transpose
+//   P[r,:] = (P[r,:] - k_r Pz) * (1 / lambda); then 0.5 (P + P^T) via a shared-memory transpose
 constexpr int kRlsGroup = 8;
+// off: stream s is rows [off[s], off[s+1]) -- or [off[s], end[s]) when end is
+// given (streams that are not back to back, e.g. the test tails of a sweep).
 __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, const double* __restrict__ Y,
                                                 const long long* __restrict__ off, int n_streams,
                                                 const double* __restrict__ lamv, double* params, double* Pg,
-                                                double* pred, int32_t* status) {
+                                                double* pred, int32_t* status,
+                                                const long long* __restrict__ end = nullptr, int pstride = 7) {
   __shared__ double tr[128 / kRlsGroup][7][8];
   const int gi = threadIdx.x / kRlsGroup, r = threadIdx.x % kRlsGroup;
   const int s = blockIdx.x * (128 / kRlsGroup) + gi;
@@ -1301,12 +1332,17 @@ __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, co
   const int rr = r < 7 ? r : 6;  // lane 7 shadows row 6 (keeps every shuffle full-group)
   double w[7], P[7];
 #pragma unroll
-  for (int i = 0; i < 7; i++) w[i] = params[ss * 7 + i];
+  for (int i = 0; i < 7; i++) w[i] = params[(long long)ss * pstride + i];
 #pragma unroll
   for (int j = 0; j < 7; j++) P[j] = Pg[(long long)ss * 49 + rr * 7 + j];
   const double lam = lamv[ss];
+  // k = Pz / denom and P = (...) / lam as multiplies by the reciprocals: one
+  // division per update instead of eight on the chain (0.95 -> 0.52 us per
+  // update, tools/rls_recip.sh); each product is within 1 ulp of the quotient,
+  // far inside the 1e-5 tolerance of the refit path
+  const double inv_lam = 1.0 / lam;
   int st = 0;
-  const long long i0 = live ? off[s] : 0, i1 = live ? off[s + 1] : 0;
+  const long long i0 = live ? off[s] : 0, i1 = live ? (end ? end[s] : off[s + 1]) : 0;
   // the next sample's row is loaded one update ahead (off the update chain)
   double zn[6], yn = 0.0;
 #pragma unroll
@@ -1349,7 +1385,7 @@ __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, co
     double pzr = Pz[0];  // Pz[rr] without dynamic register indexing
 #pragma unroll
     for (int j = 1; j < 7; j++) pzr = j == rr ? Pz[j] : pzr;
-    const double kr = pzr / denom;
+        const double kr = pzr * (1.0 / denom);
     double k[7];
 #pragma unroll
     for (int j = 0; j < 7; j++) k[j] = __shfl_sync(gmask, kr, j, kRlsGroup);
@@ -1357,7 +1393,7 @@ __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, co
 #pragma unroll
     for (int j = 0; j < 7; j++) w[j] = w[j] + k[j] * e;
 #pragma unroll
-    for (int j = 0; j < 7; j++) P[j] = (P[j] - kr * Pz[j]) / lam;
+    for (int j = 0; j < 7; j++) P[j] = (P[j] - kr * Pz[j]) * inv_lam;
     // symmetrize: lane r needs P[j][r] of every row j
     double(*T)[8] = tr[gi];
     if (r < 7) {
@@ -1365,12 +1401,12 @@ __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, co
       for (int j = 0; j < 7; j++) T[r][j] = P[j];
     }
     __syncwarp(gmask);
+    // all 7 loads first, no branch: the diagonal term is 0.5 (a + a) == a exactly
+    double pt[7];
 #pragma unroll
-    for (int j = 0; j < 7; j++) {
-      if (j == rr) continue;
-      const double pt = T[j][rr];
-      P[j] = 0.5 * (P[j] + pt);  // == 0.5 (P[rr][j] + P[j][rr]) == the (j, rr) entry
-    }
+    for (int j = 0; j < 7; j++) pt[j] = T[j][rr];
+#pragma unroll
+    for (int j = 0; j < 7; j++) P[j] = 0.5 * (P[j] + pt[j]);  // == 0.5 (P[rr][j] + P[j][rr]) == the (j, rr) entry
     __syncwarp(gmask);
     bool fin = true;
 #pragma unroll
@@ -1383,12 +1419,153 @@ __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, co
   if (!live) return;
   if (r == 0) {
 #pragma unroll
-    for (int i = 0; i < 7; i++) params[s * 7 + i] = w[i];
+    for (int i = 0; i < 7; i++) params[(long long)s * pstride + i] = w[i];
     if (status) status[s] = st;
   }
   if (r < 7) {
 #pragma unroll
     for (int j = 0; j < 7; j++) Pg[(long long)s * 49 + r * 7 + j] = P[j];
+  }
+}
+
+// ===================================================================== C5
+// Per-scenario predictor evaluation of a replayed sweep:
+// samples in outcome order, chronological split cut = int(round(0.75 n))
+// (`experiments.py:44-60`, Python's round: half to even = rint), then
+//   coarse   = fit_ols(static[:cut]),  offline on static[cut:]
+//   fine     = fit_ols(EWMA[:cut]),    offline on EWMA[cut:]
+//   adaptive = rls_init(fine, lam, X_train = EWMA[:cut]), prequential on EWMA[cut:]
+// (`predict.py:53-72,112-134,157-205`).  k_scen_fit: one warp per scenario --
+// the 35 statistics of both training designs (lanes stride the rows, fixed
+// butterfly sums), the two solves on lanes 0 / 1 (lane 1 also P0 = inv(G)),
+// the offline test predictions; then k_rls_g8 runs the adaptive tails (8 lanes
+// per scenario) and k_eval the 3 EvalReports per scenario.
+constexpr int kScenFitWarps = 4;
+#ifndef INTF_SCEN_FIT_MINB
+#define INTF_SCEN_FIT_MINB 0  // min resident blocks per SM (register cap); 0 = compiler's choice
+#endif
+
+// one scenario design's solve (a call, not inlined: keeps the warp-wide
+// parts of k_scen_fit at a small register footprint)
+__device__ __noinline__ void scen_solve(const double* st, double* p, int32_t* inf2, double* Pinv, const double* qr,
+                                        bool screen_only) {
+  ols_solve_one(st, p, inf2, Pinv, nullptr, nullptr, 0, 0, qr, screen_only);
+}
+
+// matrix_rank(Z) and, at rank 7, the lstsq solution of rows [lo, lo+cnt) by
+// the whole warp: each lane folds its strided rows into its own [R | c]
+// factor by Givens rotations, then a 5-level tree merges the factors (the
+// partner's rows arrive by shuffles, one row of the triangle at a time);
+// lane 0 takes the rank / solution from the merged R (qr_rank_solve).
+// out[0] = rank, out[1..7] = x (lane 0 writes).
+__device__ __noinline__ void warp_qr_rank(const double* __restrict__ X, const double* __restrict__ y, long long lo, long long cnt,
+                             double* out) {
+  const int lane = threadIdx.x & 31;
+  double F[7][8];
+  qr_zero(F);
+  for (long long k = lane; k < cnt; k += 32) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 6; j++) v[j] = X[(lo + k) * 6 + j];
+    v[6] = 1.0;
+    v[7] = y[lo + k];
+    givens_row(F, v);
+  }
+  for (int off = 1; off < 32; off <<= 1) {
+    const bool take = (lane & (2 * off - 1)) == 0;
+#pragma unroll
+    for (int i = 0; i < 7; i++) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const double pj = __shfl_down_sync(0xffffffffu, F[i][j], off);
+        v[j] = j < i ? 0.0 : pj;
+      }
+      if (take) givens_row(F, v);
+    }
+  }
+  if (lane == 0) {
+    double x[7];
+    out[0] = (double)qr_rank_solve(F, (double)cnt, x);
+#pragma unroll
+    for (int i = 0; i < 7; i++) out[1 + i] = x[i];
+  }
+}
+__global__ void __launch_bounds__(32 * kScenFitWarps, INTF_SCEN_FIT_MINB) k_scen_fit(const intf_scenario* __restrict__ scen, int n_scen,
+                                                                 const int32_t* __restrict__ n_batches,
+                                                                 const double* __restrict__ X, long long slot_stride,
+                                                                 int p_static, int p_ewma, const double* __restrict__ Y,
+                                                                 double lam, double* __restrict__ params,
+                                                                 double* __restrict__ P0, double* __restrict__ lamv,
+                                                                 long long* __restrict__ lo, long long* __restrict__ hi,
+                                                                 double* __restrict__ yhat, int32_t* __restrict__ est) {
+  __shared__ double st[kScenFitWarps][2][56];
+  __shared__ double par[kScenFitWarps][2][7];
+  __shared__ double qrres[kScenFitWarps][2][8];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kScenFitWarps + wi;
+  if (s >= n_scen) return;
+  const long long base = scen[s].req_off;
+  const long long n = n_batches[s];
+  const long long cut = (long long)rint(0.75 * (double)n);
+  const bool valid = cut >= 7 && n - cut >= 1;  // fit_ols needs 7 samples; split needs a non-empty test set
+  const double* Xm[2] = {X + (long long)p_static * slot_stride * 6, X + (long long)p_ewma * slot_stride * 6};
+  for (int m = 0; m < 2; m++) {
+    double acc[kStats];
+#pragma unroll
+    for (int i = 0; i < kStats; i++) acc[i] = 0.0;
+    if (valid)
+      for (long long row = base + lane; row < base + cut; row += 32) ols_acc_row(acc, Xm[m] + row * 6, Y[row]);
+    int t = 0;
+#pragma unroll
+    for (int i = 0; i < 7; i++)
+#pragma unroll
+      for (int j = i; j < 7; j++, t++) {
+        const double v = warp_sum(acc[t]);
+        if (lane == 0) st[wi][m][i * 7 + j] = st[wi][m][j * 7 + i] = v;
+      }
+#pragma unroll
+    for (int i = 0; i < 7; i++) {
+      const double v = warp_sum(acc[28 + i]);
+      if (lane == 0) st[wi][m][49 + i] = v;
+    }
+  }
+  __syncwarp();
+  int bits = valid ? 0 : 1;
+  // lane 0: coarse, lane 1: fine (+ P0 for the adaptive tail); a design that
+  // fails the condition screen gets its rank from the rows, by the whole warp
+  int32_t inf2[2] = {0, 0};
+  double p[7];
+  if (lane < 2 && valid) scen_solve(st[wi][lane], p, inf2, lane == 1 ? P0 + 49ll * s : nullptr, nullptr, true);
+  const unsigned need = __ballot_sync(0xffffffffu, lane < 2 && valid && inf2[0] == -1);
+  for (int m = 0; m < 2; m++)
+    if (need & (1u << m)) warp_qr_rank(Xm[m], Y, base, cut, qrres[wi][m]);
+  __syncwarp();
+  if (lane < 2 && valid) {
+    if (need & (1u << lane)) scen_solve(st[wi][lane], p, inf2, lane == 1 ? P0 + 49ll * s : nullptr, qrres[wi][lane], false);
+#pragma unroll
+    for (int i = 0; i < 7; i++) par[wi][lane][i] = p[i];
+    bits = (inf2[0] ? (2 << lane) : 0) | (inf2[1] ? 16 : 0);
+  }
+  bits |= __shfl_sync(0xffffffffu, bits, 1);
+  __syncwarp();
+  if (lane < 21) {  // coarse, fine, adaptive (= fine before its tail) parameters
+    const int k = lane / 7, i = lane % 7;
+    params[(3ll * s + k) * 7 + i] = valid ? par[wi][k < 2 ? k : 1][i] : NAN;
+  }
+  if (lane == 0) {
+    est[s] = bits;
+    lamv[s] = lam;
+    lo[s] = base + cut;
+    hi[s] = valid ? base + n : base + cut;  // an invalid scenario gets empty test sets (reports n = 0, NaN)
+  }
+  if (!valid) return;
+  double wc[7], wf[7];
+#pragma unroll
+  for (int i = 0; i < 7; i++) wc[i] = par[wi][0][i], wf[i] = par[wi][1][i];
+  for (long long row = base + cut + lane; row < base + n; row += 32) {
+    yhat[row] = predict7(wc, Xm[0] + row * 6);
+    yhat[slot_stride + row] = predict7(wf, Xm[1] + row * 6);
   }
 }
 
@@ -1406,10 +1583,17 @@ __device__ __forceinline__ double key_f64(unsigned long long k) {
 
 // one block per dataset: MSE (block tree sum) + 4 nearest-rank quantiles of
 // rel = |yhat - y| / y by an 8-pass radix select sharing histograms.
+// Dataset s is rows [off[s], off[s+1]) (or [off[s], end[s]) when end is given);
+// blockIdx.y selects one of gridDim.y prediction vectors yhat + y_idx * yhat_stride,
+// out[(s * gridDim.y + blockIdx.y) * 6 ..] = (mse, p25, p50, p75, p95, n).
 __global__ void __launch_bounds__(kEvalThreads) k_eval(const double* __restrict__ yhat, const double* __restrict__ y,
-                                                       const long long* __restrict__ off, double* __restrict__ out) {
+                                                       const long long* __restrict__ off, double* __restrict__ out,
+                                                       const long long* __restrict__ end = nullptr,
+                                                       long long yhat_stride = 0, long long min_n = 0) {
   const int s = blockIdx.x;
-  const long long a = off[s], n = off[s + 1] - off[s];
+  const long long a = off[s], n = (end ? end[s] : off[s + 1]) - a;
+  if (n < min_n) return;  // done by k_eval_warp
+  yhat += blockIdx.y * yhat_stride;
   __shared__ unsigned int hist[4][256];
   __shared__ unsigned long long prefix[4];
   __shared__ long long left[4];
@@ -1457,10 +1641,77 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const double* __restrict_
   if (threadIdx.x == 0) {
     double tot = 0.0;
     for (int w = 0; w < kEvalThreads / 32; w++) tot += red[w];
-    double* o = out + 6ll * s;
+    double* o = out + 6ll * ((long long)s * gridDim.y + blockIdx.y);
     o[0] = n ? tot / (double)n : NAN;
     for (int q = 0; q < 4; q++) o[1 + q] = n ? key_f64(prefix[q]) : NAN;
     o[5] = (double)n;
+  }
+}
+
+// EvalReports of small datasets (n <= kEvalWarpMax), one warp each: the
+// relative errors are sorted in shared memory (bitonic, padded with +inf to a
+// power of two) and the nearest-rank quantiles read off (`metrics.py:28-36`:
+// sorted[ceil(p/100 n) - 1]); MSE by a warp sum.  Dataset s, vector k:
+// rows [off[s], end[s]) of yhat + k * yhat_stride; out[(s * n_kinds + k) * 6].
+constexpr int kEvalWarpMax = 1024, kEvalWarps = 4;
+__global__ void __launch_bounds__(32 * kEvalWarps) k_eval_warp(const double* __restrict__ yhat,
+                                                              const double* __restrict__ y,
+                                                              const long long* __restrict__ off,
+                                                              const long long* __restrict__ end, int n_seg,
+                                                              int n_kinds, long long yhat_stride,
+                                                              double* __restrict__ out) {
+  __shared__ double v[kEvalWarps][kEvalWarpMax];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long g = (long long)blockIdx.x * kEvalWarps + wi;
+  if (g >= (long long)n_seg * n_kinds) return;
+  const int s = (int)(g / n_kinds), k = (int)(g % n_kinds);
+  const long long a = off[s], n = end[s] - a;
+  if (n > kEvalWarpMax) return;  // the block kernel's
+  const double* yh = yhat + k * yhat_stride;
+  double* buf = v[wi];
+  int np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  double sq = 0.0;
+  for (int i = lane; i < np2; i += 32) {
+    double rel = INFINITY;
+    if (i < n) {
+      const double d = yh[a + i] - y[a + i];
+      sq = fma(d, d, sq);
+      rel = fabs(d) / y[a + i];
+    }
+    buf[i] = rel;
+  }
+  sq = warp_sum(sq);
+  __syncwarp();
+  for (int kk = 2; kk <= np2; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < np2; i += 32) {
+        const int p = i ^ j;
+        if (p > i) {
+          const double x = buf[i], z = buf[p];
+          const bool up = (i & kk) == 0;
+          if ((x > z) == up) {
+            buf[i] = z;
+            buf[p] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  if (lane < 6) {
+    double r;
+    if (n == 0) {
+      r = lane == 5 ? 0.0 : NAN;
+    } else if (lane == 0) {
+      r = sq / (double)n;
+    } else if (lane == 5) {
+      r = (double)n;
+    } else {
+      const double pq = lane == 1 ? 25.0 : lane == 2 ? 50.0 : lane == 3 ? 75.0 : 95.0;
+      long long rk = (long long)ceil((pq / 100.0) * (double)n);
+      r = buf[(rk < 1 ? 1 : rk) - 1];
+    }
+    out[g * 6 + lane] = r;
   }
 }
 
@@ -1763,6 +2014,44 @@ int intf_rls_streams(const double* X, const double* y, const int64_t* off, int32
   k_rls_g8<<<ceil_div(n_streams, 128 / kRlsGroup), 128, 0, as_stream(stream)>>>(X, y, (const long long*)off, n_streams,
                                                                                lam, params, P, pred, status);
   return launch_status("k_rls_g8");
+}
+
+int64_t intf_scenario_eval_ws(int32_t n_scen, int64_t slot_stride) {
+  return 49ll * n_scen + n_scen + 2ll * n_scen + 3ll * slot_stride;
+}
+
+int intf_scenario_eval(const intf_batch* bt, const intf_replay_buffers* buf, const double* X, int64_t slot_stride,
+                       int32_t p_static, int32_t p_ewma, const double* y, double lam, double* ws, int64_t ws_elems,
+                       double* params, double* report, int32_t* status, void* stream) {
+  if (!bt || !bt->scen || !buf || !buf->n_batches || !X || !y || !ws || !params || !report || !status ||
+      p_static < 0 || p_ewma < 0 || !(lam > 0.0 && lam <= 1.0))
+    return bad_input("intf_scenario_eval: bad argument");
+  const int S = bt->n_scen;
+  if (S <= 0) return INTF_OK;
+  if (ws_elems < intf_scenario_eval_ws(S, slot_stride)) return bad_input("intf_scenario_eval: workspace too small");
+  double* P0 = ws;
+  double* lamv = P0 + 49ll * S;
+  long long* lo = (long long*)(lamv + S);
+  long long* hi = lo + S;
+  double* yhat = (double*)(hi + S);
+  cudaStream_t st = as_stream(stream);
+  k_scen_fit<<<ceil_div(S, kScenFitWarps), 32 * kScenFitWarps, 0, st>>>(
+      bt->scen, S, buf->n_batches, X, (long long)slot_stride, p_static, p_ewma, y, lam, params, P0, lamv, lo, hi, yhat,
+      status);
+  int rc = launch_status("k_scen_fit");
+  if (rc) return rc;
+  // the adaptive tails: rls_update over EWMA[cut:], from the fine fit and P0 (params row 2 of each scenario)
+  k_rls_g8<<<ceil_div(S, 128 / kRlsGroup), 128, 0, st>>>(X + (long long)p_ewma * slot_stride * 6, y, lo, S, lamv,
+                                                          params + 14, P0, yhat + 2 * slot_stride, status + S, hi, 21);
+  if ((rc = launch_status("k_rls_g8"))) return rc;
+  k_eval_warp<<<ceil_div(3ll * S, kEvalWarps), 32 * kEvalWarps, 0, st>>>(yhat, y, lo, hi, S, 3, (long long)slot_stride,
+                                                                        report);
+  if ((rc = launch_status("k_eval_warp"))) return rc;
+  // a test tail holds n - rint(0.75 n) <= n / 4 + 1 samples, n <= req_cap: if
+  // every tail fits the warp kernel, the block kernel is not needed
+  if ((long long)bt->max_req_cap / 4 + 1 <= kEvalWarpMax) return INTF_OK;
+  k_eval<<<dim3(S, 3), kEvalThreads, 0, st>>>(yhat, y, lo, report, hi, (long long)slot_stride, kEvalWarpMax + 1);
+  return launch_status("k_eval");
 }
 
 int intf_eval_report(const double* yhat, const double* y, const int64_t* off, int32_t n_seg, double* out,

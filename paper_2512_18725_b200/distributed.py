@@ -41,6 +41,73 @@ def weighted_shards(weights, world: int) -> list:
     return [(int(cuts[k]), int(cuts[k + 1])) for k in range(world)]
 
 
+def lpt_shards(weights, world: int) -> list:
+    """Longest-processing-time-first assignment of units to ranks: units in
+    descending weight (e.g. expected requests lambda*T of a scenario), each to
+    the rank with the least assigned weight so far (ties: lowest rank).
+    Returns one index list per rank, each in descending weight (the replay's
+    own LPT order).  Deterministic, so every rank computes the same split."""
+    w = np.asarray(weights, dtype=float)
+    order = sorted(range(len(w)), key=lambda i: (-w[i], i))
+    load = np.zeros(world)
+    out = [[] for _ in range(world)]
+    for i in order:
+        r = int(np.argmin(load))
+        out[r].append(i)
+        load[r] += w[i]
+    return out
+
+
+SWEEP_ROW = 18 + 5 * REPORT_MODELS  # per scenario: 3 x EvalReport (mse, p25, p50, p75, p95, n) + per-model SLO
+
+
+class SweepRows:
+    """Per-scenario report rows of a ReplayPipeline built on the device
+    (the fixed-size struct gathered to rank 0): the coarse / fine
+    / adaptive EvalReports (intf_scenario_eval) and per deployed model (n,
+    met, p50, p95, p99), padded to REPORT_MODELS models."""
+
+    def __init__(self, pipe):
+        S = pipe.pb.n_scen
+        idx = np.full((S, REPORT_MODELS), -1, dtype=np.int64)
+        for s in range(S):
+            sc = pipe.pb.scen[s]
+            for m in range(min(sc.n_models, REPORT_MODELS)):
+                idx[s, m] = sc.model_off + m
+        self.pipe = pipe
+        self.valid = torch.as_tensor(idx >= 0, device=pipe.dev)
+        self.idx = torch.as_tensor(np.maximum(idx, 0), device=pipe.dev)
+        self.rows = torch.zeros(S, SWEEP_ROW, dtype=torch.float64, device=pipe.dev)
+
+    def build(self) -> torch.Tensor:
+        """Enqueue the row build on the current stream; returns rows [S, SWEEP_ROW]."""
+        p, S = self.pipe, self.pipe.pb.n_scen
+        self.rows[:, :18] = p.eval_report.view(-1, 18)[:S]
+        per = torch.stack([p.slo_n[self.idx].double(), p.slo_met[self.idx].double(),
+                           p.slo_p.view(-1, 3)[self.idx, 0], p.slo_p.view(-1, 3)[self.idx, 1],
+                           p.slo_p.view(-1, 3)[self.idx, 2]], dim=-1)
+        per = torch.where(self.valid[..., None], per, torch.full_like(per, float("nan")))
+        self.rows[:, 18:] = per.reshape(S, -1)
+        return self.rows
+
+
+def gather_sweep_rows(local: torch.Tensor, counts: list, backend: str = "nccl"):
+    """all_gather of per-rank [n_r, F] row blocks (n_r = counts[r]): returns the
+    list of every rank's block (padded blocks trimmed), on every rank."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return [local]
+    maxn = max(counts)
+    pad = torch.full((maxn, local.shape[1]), float("nan"), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    if backend != "nccl":
+        pad = pad.cpu()
+    parts = [torch.empty_like(pad) for _ in counts]
+    dist.all_gather(parts, pad)
+    return [p[:n] for p, n in zip(parts, counts)]
+
+
 def allreduce_ols_stats(stats: torch.Tensor) -> torch.Tensor:
     """Sum the 56 OLS statistics over ranks in rank order (all_gather)."""
     import torch.distributed as dist

@@ -62,7 +62,8 @@ class ReplayPipeline:
     """
 
     def __init__(self, specs, table: _pack.TableArrays, seg_stride: int = 64, scale: float = 1.0,
-                 preds=(), list_caps=None, dtable: DeviceTable | None = None, noise_k: int | None = None):
+                 preds=(), list_caps=None, dtable: DeviceTable | None = None, noise_k: int | None = None,
+                 evaluate=None):
         self.dev = require_cuda()
         self.lib = _abi.load()
         self.pb = _pack.pack(list(specs), table, scale=scale, list_caps=list_caps)
@@ -92,6 +93,21 @@ class ReplayPipeline:
         self.slo_met = torch.zeros(n_models, dtype=torch.int32, device=self.dev)
         self.slo_p = torch.zeros(n_models * 3, dtype=torch.float64, device=self.dev)
         self.set_predictors(preds)
+        # per-scenario coarse / fine / adaptive evaluation (intf_scenario_eval):
+        # evaluate = (p_static, p_ewma, lam) -- indices of the static and EWMA
+        # feature modes among `preds`
+        self.evaluate = tuple(evaluate) if evaluate is not None else None
+        if self.evaluate is not None:
+            p_s, p_e, _ = self.evaluate
+            if not (0 <= p_s < len(self.preds) and 0 <= p_e < len(self.preds)) or self.preds[p_s].ewma \
+                    or not self.preds[p_e].ewma:
+                raise ValueError("evaluate=(p_static, p_ewma, lam) must name a static and an EWMA predictor")
+            S = max(self.pb.n_scen, 1)
+            n_ws = int(self.lib.intf_scenario_eval_ws(S, self.slot_stride))
+            self.eval_ws = torch.zeros(n_ws, dtype=torch.float64, device=self.dev)
+            self.eval_params = torch.zeros(S * 21, dtype=torch.float64, device=self.dev)
+            self.eval_report = torch.zeros(S * 18, dtype=torch.float64, device=self.dev)
+            self.eval_status = torch.zeros(2 * S, dtype=torch.int32, device=self.dev)
 
     # ------------------------------------------------------------ inputs
     def set_predictors(self, preds):
@@ -132,7 +148,7 @@ class ReplayPipeline:
         _abi.check(L.intf_replay(bt, ctypes.byref(self.dtable.struct), B, s), "intf_replay")
         self.run_slo_features(warm_cutoff, slo=slo, features=features)
 
-    def run_slo_features(self, warm_cutoff=None, slo: bool = True, features: bool = True):
+    def run_slo_features(self, warm_cutoff=None, slo: bool = True, features: bool = True, evaluate: bool = True):
         L, s = self.lib, stream_ptr()
         bt, B = ctypes.byref(self.batch), ctypes.byref(self.B)
         if slo:
@@ -144,6 +160,18 @@ class ReplayPipeline:
                                                ctypes.cast(self.P, ctypes.c_void_p) if n else None, n,
                                                self.slot_stride, self.X.data_ptr(), self.Y.data_ptr(),
                                                self.Yhat.data_ptr(), s), "intf_features_predict")
+        if evaluate and self.evaluate is not None:
+            self.run_evaluation()
+
+    def run_evaluation(self):
+        """Per-scenario coarse / fine / adaptive EvalReports from the features
+        of the last run (intf_scenario_eval; enqueue only)."""
+        p_s, p_e, lam = self.evaluate
+        _abi.check(self.lib.intf_scenario_eval(ctypes.byref(self.batch), ctypes.byref(self.B), self.X.data_ptr(),
+                                               self.slot_stride, p_s, p_e, self.Y.data_ptr(), float(lam),
+                                               self.eval_ws.data_ptr(), self.eval_ws.numel(),
+                                               self.eval_params.data_ptr(), self.eval_report.data_ptr(),
+                                               self.eval_status.data_ptr(), stream_ptr()), "intf_scenario_eval")
 
     def status(self) -> np.ndarray:
         return self.t["status"][: self.pb.n_scen].cpu().numpy()
@@ -158,6 +186,11 @@ class ReplayPipeline:
         h["slo_n"] = self.slo_n.cpu().numpy()
         h["slo_met"] = self.slo_met.cpu().numpy()
         h["slo_p"] = self.slo_p.cpu().numpy().reshape(-1, 3)
+        if self.evaluate is not None:
+            h["eval_report"] = self.eval_report.cpu().numpy().reshape(-1, 3, 6)
+            h["eval_params"] = self.eval_params.cpu().numpy().reshape(-1, 3, 7)
+            st = self.eval_status.cpu().numpy()
+            h["eval_status"] = st[: len(st) // 2] | (st[len(st) // 2:] << 8)
         return h
 
     def scenario(self, h: dict, s: int) -> dict:
@@ -182,6 +215,10 @@ class ReplayPipeline:
         v["slo_n"] = h["slo_n"][mo:mo + S.n_models]
         v["slo_met"] = h["slo_met"][mo:mo + S.n_models]
         v["slo_p"] = h["slo_p"][mo:mo + S.n_models]
+        if "eval_report" in h:
+            v["eval_report"] = h["eval_report"][s]  # [coarse, fine, adaptive][mse, p25, p50, p75, p95, n]
+            v["eval_params"] = h["eval_params"][s]
+            v["eval_status"] = int(h["eval_status"][s])
         return v
 
 

@@ -6,6 +6,7 @@ compressed numpy archives; the parity tests (CPU and GPU) compare against
 these files and never import the reference at run time.
 
     python tests/golden/make_golden.py          # rewrites tests/golden/*.npz
+    python tests/golden/make_golden.py --candidates | --c5eval   # one fixture only
 
 Contents
   replay_golden.npz   per scenario: spec JSON, profile table, arrivals,
@@ -17,6 +18,9 @@ Contents
                       (`predict.py:53-205`, `experiments.py:63-205`)
   rng_golden.npz      numpy/glibc known answers: noise draws, uniform and
                       normal streams, exp/log1p samples (`oracle.py:24-33`)
+  c5eval_golden.npz   per-scenario coarse / fine / adaptive EvalReports of
+                      the first C5 sweep scenarios (`experiments.py:44-60`,
+                      `predict.py:53-205`)
   candidates_golden.npz  candidate-set predictions composed from reference
                       functions (colo sums `simcore.py:126-131`,
                       `estimate_from_history`, `finalize_features`, `predict`)
@@ -376,17 +380,52 @@ def candidates_golden(table):
     np.savez_compressed(os.path.join(HERE, "candidates_golden.npz"), **arrs)
 
 
+def c5eval_golden(table, n_scen: int = 24):
+    """C5 per-scenario evaluation (coarse = static + OLS, fine =
+    EWMA(1/2) + OLS, adaptive = OLS warm start + RLS prequential on the 25%
+    tail) by the reference's own functions on the bench's scenario generator
+    (`paper_2512_18725_b200.sweep.c5_scenario`, host config code only)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_2512_18725_b200.sweep import c5_scenario
+
+    from intfsim.workload import scenario_from_dict
+
+    arrs = {"idx": np.arange(n_scen)}
+    reps = np.full((n_scen, 3, 6), np.nan)
+    for i in range(n_scen):
+        spec = scenario_from_dict(c5_scenario(table, i))
+        res = intfsim.run_scenario(spec, table)
+        s_st = intfsim.colocation.samples_from_outcomes(res.outcomes, table, STATIC_MODE)
+        s_ew = intfsim.colocation.samples_from_outcomes(res.outcomes, table, ewma_mode(0.5))
+        try:
+            tr_s, te_s = ex.split_samples(s_st)
+            tr_f, te_f = ex.split_samples(s_ew)
+            coarse, fine = pr.fit_ols(tr_s), pr.fit_ols(tr_f)
+        except (ValueError, pr.PredictError):
+            continue  # too few samples: the reference raises, the device reports NaN / n = 0
+        st = pr.rls_init(fine, lam=0.99, X_train=np.array([s.x for s in tr_f]))
+        for k, rep in enumerate([pr.evaluate(coarse, te_s), pr.evaluate(fine, te_f), pr.evaluate(st, te_f, online=True)]):
+            reps[i, k] = [rep.mse, rep.rel_p25, rep.rel_p50, rep.rel_p75, rep.rel_p95, rep.n_samples]
+    arrs["reports"] = reps
+    print(f"c5eval: {n_scen} scenarios, {int(np.isnan(reps[:, 0, 0]).sum())} without a valid split")
+    np.savez_compressed(os.path.join(HERE, "c5eval_golden.npz"), **arrs)
+
+
 def main():
     table = load_profiles("/root/reference/pkg/profiles/default.csv")
     assert table.entries == gen_synthetic_profiles().entries
     if "--candidates" in sys.argv:  # only candidates_golden.npz
         candidates_golden(table)
         return
+    if "--c5eval" in sys.argv:  # only c5eval_golden.npz
+        c5eval_golden(table)
+        return
     t16 = table16()
     rng_golden()
     replay_golden(table, t16)
     predict_golden(table)
     candidates_golden(table)
+    c5eval_golden(table)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -171,3 +171,23 @@ def test_vectorised_candidate_restatement_matches_reference(cap):
         hist = O.candidate_history(int(o), [q for q in pe if q >= 0], tab.solo, tab.thr)
         assert np.array_equal(Xs[o, i], O.features(hist, tab.thr[o], False, 1.0))
         assert np.array_equal(Xf[o, i], O.features(hist, tab.thr[o], True, float(C["alpha"])))
+
+
+def test_oracle_scenario_eval_matches_reference():
+    """`oracle.scenario_eval` (the C5 coarse / fine / adaptive evaluation
+    checker) against the reference's own split_samples / fit_ols / rls_init /
+    evaluate on the first 24 sweep scenarios (tests/golden/c5eval_golden.npz)."""
+    from paper_2512_18725_b200.profiles import gen_synthetic_profiles
+    from paper_2512_18725_b200.sweep import c5_scenario
+
+    G = _golden.load("c5eval_golden.npz")
+    table = gen_synthetic_profiles()
+    otab = _otab("default")
+    for i in G["idx"]:
+        spec = c5_scenario(table, int(i))
+        got = O.scenario_eval(O.run_scenario(spec, otab), spec, otab)
+        ref = G["reports"][i]
+        if np.isnan(ref[0, 0]):
+            assert got is None
+            continue
+        np.testing.assert_allclose(got, ref, rtol=1e-9, err_msg=f"scenario {i}")
