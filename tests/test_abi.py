@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "intfsim_b200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^int (intf_\w+)\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t) (intf_\w+)\(", text, flags=re.M)))
 
 
 def test_library_is_built_for_sm100a():
