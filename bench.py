@@ -65,6 +65,26 @@ def _traffic(kernel: str):
     return None
 
 
+def cpu_model() -> str:
+    """Host CPU model and usable cores (every cpu_baseline carries it)."""
+    name = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                name = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{name}, {len(os.sched_getaffinity(0))} cores available"
+
+
+def one_thread_blas():
+    """Context: numpy's BLAS/LAPACK pinned to one thread (the reference as shipped)."""
+    from threadpoolctl import threadpool_limits
+
+    return threadpool_limits(limits=1)
+
+
 # ------------------------------------------------------------------ clocks
 class Clocks:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -336,7 +356,7 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
         t0 = time.perf_counter()
         ref = O.run_scenario(spec, O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr))
         dt = time.perf_counter() - t0
-        cpu = {"value": len(ref["arr_t"]) / dt, "unit": "requests/s", "cores": 1, "kind": "port",
+        cpu = {"value": len(ref["arr_t"]) / dt, "unit": "requests/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
                "sample": f"the whole {len(ref['arr_t'])}-request trace (oracle C replay: heap engine + arrivals) "
                          f"in {dt:.2f} s"}
     return {"metric": "requests replayed/sec (single long trace)", "value": world * n_req / (ms / 1e3),
@@ -507,6 +527,164 @@ def sweep_summary(rows: np.ndarray) -> dict:
     return out
 
 
+def c1_leg(a, stream, barrier, max_over_ranks, rank, world, W) -> dict:
+    """C1 (BASELINE configs[0]): the reference's bundled trace
+    `mixed_three_model.json` at seed 7 (3 models, cap 2; 3,789 requests, 1,528
+    batches), static features, the coarse predictor.  Device: one replay
+    pipeline pass (arrivals -> formation -> noise -> replay -> SLO ->
+    features -> forward), CUDA events, >= 20 repetitions.  e2e: the public
+    API call a user makes -- `run_scenario(spec, table)` (H2D of the scenario,
+    every result materialised as the reference's objects) + `predict_many` of
+    its samples.  CPU: the oracle's C heap-engine replay + numpy features and
+    forward of the same trace on one core.  Replicas only across GPUs (one
+    trace does not shard)."""
+    import torch
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200 import _abi, engine
+    from paper_2512_18725_b200.predict import LinearModel, predict_many
+    from paper_2512_18725_b200.sweep import BUNDLED_SEED7
+    from paper_2512_18725_b200.workload import scenario_from_dict
+
+    table = p.gen_synthetic_profiles()
+    ta = table.arrays()
+    coarse = _abi.Predictor(ewma=0, alpha=1.0, w=tuple(W[-1, 0]))
+    pipe = engine.ReplayPipeline([BUNDLED_SEED7], ta, preds=[coarse])
+    for _ in range(5):
+        pipe.run()
+    reps = max(20, a.steps)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        pipe.run()
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / reps
+    nb = int(pipe.t["n_batches"][0].item())
+    spec = scenario_from_dict(BUNDLED_SEED7)
+    model = LinearModel(w=np.array(W[-1, 0, :6]), b=float(W[-1, 0, 6]))
+
+    def api_call():
+        res = p.run_scenario(spec, table)
+        return res, predict_many(model, np.array([smp.x for smp in res.samples]))
+
+    for _ in range(2):
+        api_call()
+    barrier()
+    t0 = time.perf_counter()
+    n_e2e = 10
+    for _ in range(n_e2e):
+        res, yhat = api_call()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_e2e)
+    ok = len(res.outcomes) == nb == 1528 and len(res.records) == 3789 and bool(np.isfinite(yhat).all())
+    cpu = None
+    if rank == 0 and not a.no_cpu:
+        import oracle as O
+
+        otab = O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr)
+        with one_thread_blas():
+            t0 = time.perf_counter()
+            k = 0
+            while time.perf_counter() - t0 < min(5.0, a.cpu_seconds) or k < 3:
+                rep = O.run_scenario(BUNDLED_SEED7, otab)
+                X, y, _ = O.samples_from_replay(rep, BUNDLED_SEED7, otab, False, 1.0)
+                _ = X @ W[-1, 0, :6] + W[-1, 0, 6]
+                k += 1
+            dt = time.perf_counter() - t0
+        cpu = {"value": k / dt, "unit": "replays/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
+               "sample": f"{k} replays of the bundled trace (oracle C heap engine + arrivals, numpy static "
+                         f"features + forward) in {dt:.2f} s; the reference's own Python run_scenario: "
+                         f"270.5 ms/replay on one core of the build container (SURVEY §6)"}
+    return {"metric": "bundled-trace replays/sec (C1)", "value": world * 1e3 / ms, "unit": "replays/s",
+            "us_per_replay": 1e3 * ms, "scaling": "weak (replicas only: one trace does not shard)",
+            "batches": nb, "consistent": ok,
+            "e2e": {"value": world * 1e3 / e2e_ms, "unit": "replays/s", "ms_per_call": e2e_ms,
+                    "call": "run_scenario(spec, table) + predict_many (objects materialised on the host)",
+                    "h2d_bytes_per_step": int(pipe.d_scen.numel() + pipe.d_models.numel()),
+                    "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in pipe.t.values()))},
+            "cpu_baseline": cpu,
+            "workload": "C1: pkg/scenarios/mixed_three_model.json, seed 7, static mode, coarse predictor "
+                        "(bench C2 decision 31's refit); device pass = arrivals + formation + noise + replay + "
+                        "SLO + features + forward"}
+
+
+def c3_leg(a, stream, barrier, max_over_ranks, rank, world) -> dict:
+    """C3 (BASELINE configs[2]): the reference's drift experiment
+    (`experiments.py:153-205`: 4 datasets, EWMA(1/2) features, OLS warm
+    start, offline / SGD (eta 0.01) / RLS (lambda 0.99) prequential on 300
+    test samples) for seeds 0..19, end to end through the package
+    (`experiments.drift_experiments`: all seeds' 80 scenarios in one batched
+    replay, fits / streams / reports as batched device launches).  CPU: the
+    oracle's composition of the same functions (C replay + numpy) on one core.
+    Seeds shard across ranks (no collective)."""
+    import torch
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200 import experiments as ex
+
+    table = p.gen_synthetic_profiles()
+    seeds = list(range(20))[rank::world]
+    bases = [ex.default_drift_base(table, s) for s in seeds]
+    ex.drift_experiments(bases[:2], table)  # warm-up
+    barrier()
+    t0 = time.perf_counter()
+    cells = ex.drift_experiments(bases, table)
+    torch.cuda.synchronize()
+    dt = max_over_ranks(time.perf_counter() - t0)
+    mean = ex.mean_drift_table(cells)
+    cpu = None
+    if rank == 0 and not a.no_cpu:
+        import oracle as O
+
+        ta = table.arrays()
+        otab = O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr)
+        with one_thread_blas():
+            t1 = time.perf_counter()
+            n_cpu = 0
+            while n_cpu < 2:
+                O.drift_experiment(ex.drift_specs(bases[n_cpu]), otab)
+                n_cpu += 1
+            cdt = time.perf_counter() - t1
+        cpu = {"value": n_cpu / cdt, "unit": "seeds/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
+               "sample": f"drift_experiment seeds 0..{n_cpu - 1} (oracle C replay + numpy OLS / SGD / RLS / "
+                         f"EvalReports) in {cdt:.2f} s; the reference: 2.20 s per seed (SURVEY §6)",
+               "updates": cpu_update_rates(min(2.0, a.cpu_seconds / 5))}
+    return {"metric": "drift experiments/sec (C3, seeds 0..19)", "value": len(bases) * world / dt,
+            "unit": "seeds/s", "s_per_seed": dt / len(bases), "seeds": 20, "scaling": "strong (seeds shard)",
+            "mean_mse": {f"{k[0]}/{k[1]}": v for k, v in sorted(mean.items())},
+            "e2e": {"value": len(bases) * world / dt, "unit": "seeds/s",
+                    "call": "experiments.drift_experiments(bases, table) (public API, host objects out)"},
+            "cpu_baseline": cpu,
+            "workload": "C3: drift_experiment(default_drift_base(table, s)) for s = 0..19: per seed 4 replays "
+                        "(training + 3 shifted test sets), EWMA(1/2) features, OLS warm start, offline / SGD / "
+                        "RLS prequential on <= 300 test samples, MSE per (dataset, method)"}
+
+
+def cpu_update_rates(seconds: float) -> dict:
+    """1-core numpy rates of the reference's learners (`predict.py:75-154`):
+    RLS / SGD updates/s (one prequential stream) and OLS samples/s (fit_ols_xy
+    on 10^5 rows), as the oracle restates them."""
+    import oracle as O
+
+    rng = np.random.default_rng(0)
+    X = rng.uniform(0, 1, size=(100000, 6))
+    y = X @ np.array([0.3, 0.5, 0.2, 0.8, 1.1, 0.4]) + 1.0
+    out = {}
+    with one_thread_blas():
+        for method in ("rls", "sgd"):
+            n, t0 = 0, time.perf_counter()
+            while time.perf_counter() - t0 < seconds:
+                O.prequential(np.zeros(6), 0.0, X[:500], y[:500], method, P=100.0 * np.eye(7))
+                n += 500
+            out[f"{method}_updates_per_s"] = n / (time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        O.fit_ols_xy(X, y)
+        out["ols_samples_per_s"] = len(y) / (time.perf_counter() - t0)
+    out["cpu"] = cpu_model()
+    out["cores"] = 1
+    return out
+
+
 # -------------------------------------------------------------- reference
 def reference_arm(a):
     rank, world, _ = _env()
@@ -537,7 +715,7 @@ def reference_arm(a):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C2 candidate sets, cap 4 over the 48 bundled profile entries, coarse+fine "
                                "predictors (bounded random sample of candidates per step)", "cap": CAP},
-        "cpu_baseline": {"value": v, "unit": "predictions/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "predictions/s", "cores": cores, "kind": "port", "cpu": cpu_model(),
                          "sample": f"{per_step:.1f} s of random cap-4 candidates per core per step "
                                    f"(oracle.candidate_predictions, reference functions restated)"},
         "e2e": {"value": v, "unit": "predictions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -653,6 +831,8 @@ def product_arm(a):
     sweep = c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W)
 
     refit = refit_secondary(a, stream, barrier, max_over_ranks, rank)
+    bundled = c1_leg(a, stream, barrier, max_over_ranks, rank, world, W)
+    drift = c3_leg(a, stream, barrier, max_over_ranks, rank, world)
     longtrace = c4_secondary(a, stream, barrier, max_over_ranks, rank, world) if not a.no_c4 else None
     clk = clocks.stop()
 
@@ -660,10 +840,10 @@ def product_arm(a):
     cpu = replay_cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         rate, n, dt = cpu_candidate_rate(ta, W, a.cpu_seconds)
-        cpu = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port",
+        cpu = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
                "sample": f"{n} predictions ({n // 2} random cap-4 candidates x coarse+fine, 1 decision) in {dt:.1f} s"}
         rrate, rn, rdt = cpu_replay_rate(table, min(5.0, a.cpu_seconds))
-        replay_cpu = {"value": rrate, "unit": "replays/s", "cores": 1, "kind": "port",
+        replay_cpu = {"value": rrate, "unit": "replays/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
                       "sample": f"{rn} C5 scenarios (oracle C replay: heap engine + arrivals; numpy evaluation: "
                                 f"split, 2 lstsq fits, RLS tail, 3 EvalReports) in {rdt:.1f} s"}
 
@@ -717,6 +897,8 @@ def product_arm(a):
         "gpu_launches": a.steps if fused else 2 * a.steps,
         "replay": {**sweep, "cpu_baseline": replay_cpu},
         "refit": refit,
+        "bundled_trace": bundled,
+        "drift": drift,
         "long_trace": longtrace,
     }
     if rank == 0:

@@ -351,6 +351,28 @@ int intf_scenario_eval(const intf_batch *batch, const intf_replay_buffers *buf, 
                        int32_t p_static, int32_t p_ewma, const double *y, double lam, double *ws, int64_t ws_elems,
                        double *params, double *report, int32_t *status, void *stream);
 
+/* Row-segment forms of the refit path (segment g = rows [lo[g], hi[g]) of X
+ * [row][6] / y, e.g. slices of a replay's feature slots), as used by the
+ * batched drift experiment (`experiments.py:153-205`):
+ *   intf_ols_fit_segments  fit_ols_xy per segment (`predict.py:53-72`):
+ *                          params[g][7], info[g][3] = (ridge, non-finite,
+ *                          < 7 rows), Pinv[g][49] = rls_init's P0 (optional)
+ *   intf_predict_segments  yhat[row] = params[model[g]] . [x, 1] (model NULL: g)
+ *   intf_sgd_segments / intf_rls_segments  prequential streams over segments
+ *                          (as intf_sgd_streams / intf_rls_streams)
+ *   intf_eval_segments     out[g][6] EvalReport of yhat vs y over segment g;
+ *                          max_len >= the longest segment.                  */
+int intf_ols_fit_segments(const double *X, const double *y, const int64_t *lo, const int64_t *hi, int32_t n_seg,
+                          double *params, int32_t *info, double *Pinv, void *stream);
+int intf_predict_segments(const double *X, const int64_t *lo, const int64_t *hi, const int32_t *model,
+                          const double *params, int32_t n_seg, double *yhat, void *stream);
+int intf_sgd_segments(const double *X, const double *y, const int64_t *lo, const int64_t *hi, int32_t n_seg,
+                      const double *eta, double *params, double *pred, int32_t *status, void *stream);
+int intf_rls_segments(const double *X, const double *y, const int64_t *lo, const int64_t *hi, int32_t n_seg,
+                      const double *lam, double *params, double *P, double *pred, int32_t *status, void *stream);
+int intf_eval_segments(const double *yhat, const double *y, const int64_t *lo, const int64_t *hi, int32_t n_seg,
+                       int64_t max_len, double *out, void *stream);
+
 /* ---- array-level entry points behind the per-object reference API ---- */
 
 /* samples_from_outcomes over arbitrary outcome rows (`colocation.py:95-105`):

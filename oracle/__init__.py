@@ -440,6 +440,32 @@ def scenario_eval(rep: dict, spec: dict, tab: TableArrays, lam: float = 0.99, al
     return np.array(out)
 
 
+def drift_experiment(specs4, tab: TableArrays, eta: float = 0.01, lam: float = 0.99, alpha: float = 0.5,
+                     max_test: int = 300):
+    """`experiments.py:153-205` over the 4 drift scenario dicts (TrainingSet,
+    TestSet1..3, EWMA(alpha) features): OLS warm start on the training set,
+    its offline training score, then per test set (first max_test samples)
+    offline / SGD / RLS (P0 = inv(Z^T Z) of the training design) scores.
+    Returns [(dataset, method, mse, n)] in the reference's cell order."""
+    data = []
+    for k, spec in enumerate(specs4):
+        X, y, _ = samples_from_replay(run_scenario(spec, tab), spec, tab, True, alpha)
+        if k and max_test:
+            X, y = X[:max_test], y[:max_test]
+        data.append((X, y))
+    (Xt, yt) = data[0]
+    w0, b0 = fit_ols_xy(Xt, yt)
+    tr = eval_report(Xt @ w0 + b0, yt)
+    cells = [("TrainingSet", m, tr[0], tr[5]) for m in ("offline", "sgd", "rls")]
+    P0 = rls_init_P(Xt)
+    for name, (X, y) in zip(("TestSet1", "TestSet2", "TestSet3"), data[1:]):
+        off = eval_report(X @ w0 + b0, y)
+        sg = eval_report(prequential(w0, b0, X, y, "sgd", eta=eta)[0], y)
+        rl = eval_report(prequential(w0, b0, X, y, "rls", lam=lam, P=P0.copy())[0], y)
+        cells += [(name, "offline", off[0], off[5]), (name, "sgd", sg[0], sg[5]), (name, "rls", rl[0], rl[5])]
+    return cells
+
+
 # ------------------------------------------------------ candidate sets (C2)
 def candidate_history(own: int, peers, solo: np.ndarray, thr: np.ndarray):
     """Fine-grained candidate history: snapshot with all peers

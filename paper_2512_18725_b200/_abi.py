@@ -113,6 +113,11 @@ SIGNATURES = {
     "intf_rls_streams": (c_int32, [P, P, P, c_int32, P, P, P, P, P, P]),
     "intf_eval_report": (c_int32, [P, P, P, c_int32, P, P]),
     "intf_scenario_eval_ws": (c_int64, [c_int32, c_int64]),
+    "intf_ols_fit_segments": (c_int32, [P, P, P, P, c_int32, P, P, P, P]),
+    "intf_predict_segments": (c_int32, [P, P, P, P, P, c_int32, P, P]),
+    "intf_sgd_segments": (c_int32, [P, P, P, P, c_int32, P, P, P, P, P]),
+    "intf_rls_segments": (c_int32, [P, P, P, P, c_int32, P, P, P, P, P, P]),
+    "intf_eval_segments": (c_int32, [P, P, P, P, c_int32, c_int64, P, P]),
     "intf_scenario_eval": (c_int32, [P, P, P, c_int64, c_int32, c_int32, P, c_double, P, c_int64, P, P, P, P]),
     "intf_features_rows": (c_int32, [P, P, P, P, P, P, c_int64, P, c_int32, P, P, P, P]),
     "intf_predict_rows": (c_int32, [P, c_int64, P, P, P]),

@@ -1279,14 +1279,16 @@ __global__ void k_ols_window_solve(const double* __restrict__ stats, const doubl
 // sgd_update (`predict.py:88-95`): e = y - (w.x + b); w += (eta*e)*x;
 // b += eta*e -- same rounding sequence as numpy (unfused).
 __global__ void k_sgd(const double* __restrict__ X, const double* __restrict__ Y, const long long* __restrict__ off,
-                      int n_streams, const double* __restrict__ eta, double* params, double* pred, int32_t* status) {
+                      int n_streams, const double* __restrict__ eta, double* params, double* pred, int32_t* status,
+                      const long long* __restrict__ end = nullptr) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_streams) return;
   double w[7];
   for (int i = 0; i < 7; i++) w[i] = params[s * 7 + i];
   const double et = eta[s];
   int st = 0;
-  for (long long i = off[s]; i < off[s + 1]; i++) {
+  const long long i1 = end ? end[s] : off[s + 1];
+  for (long long i = off[s]; i < i1; i++) {
     double x[6];
     for (int j = 0; j < 6; j++) x[j] = X[i * 6 + j];
     const double yh = predict7(w, x);
@@ -1567,6 +1569,71 @@ __global__ void __launch_bounds__(32 * kScenFitWarps, INTF_SCEN_FIT_MINB) k_scen
     yhat[row] = predict7(wc, Xm[0] + row * 6);
     yhat[slot_stride + row] = predict7(wf, Xm[1] + row * 6);
   }
+}
+
+// fit_ols_xy (`predict.py:53-72`) of arbitrary row segments [lo[g], hi[g]) of
+// (X, y), one warp per segment: the 35 statistics by the warp (fixed
+// butterfly sums), the condition screen on lane 0, the rows' QR by the warp
+// when the screen fails, then the solve; Pinv (optional) = rls_init's P0.
+// info[g][3] = (ridge used, non-finite params, fewer than 7 rows).
+__global__ void __launch_bounds__(32 * kScenFitWarps) k_fit_segments(const double* __restrict__ X,
+                                                                     const double* __restrict__ Y,
+                                                                     const long long* __restrict__ lo,
+                                                                     const long long* __restrict__ hi, int n_seg,
+                                                                     double* __restrict__ params,
+                                                                     int32_t* __restrict__ info,
+                                                                     double* __restrict__ Pinv) {
+  __shared__ double st[kScenFitWarps][56];
+  __shared__ double qrres[kScenFitWarps][8];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * kScenFitWarps + wi;
+  if (g >= n_seg) return;
+  const long long a = lo[g], cnt = hi[g] - lo[g];
+  double acc[kStats];
+#pragma unroll
+  for (int i = 0; i < kStats; i++) acc[i] = 0.0;
+  for (long long row = a + lane; row < a + cnt; row += 32) ols_acc_row(acc, X + row * 6, Y[row]);
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = i; j < 7; j++, t++) {
+      const double v = warp_sum(acc[t]);
+      if (lane == 0) st[wi][i * 7 + j] = st[wi][j * 7 + i] = v;
+    }
+#pragma unroll
+  for (int i = 0; i < 7; i++) {
+    const double v = warp_sum(acc[28 + i]);
+    if (lane == 0) st[wi][49 + i] = v;
+  }
+  __syncwarp();
+  int32_t inf2[2] = {0, 0};
+  double p[7];
+  double* pinv = Pinv ? Pinv + 49ll * g : nullptr;
+  if (lane == 0) scen_solve(st[wi], p, inf2, pinv, nullptr, true);
+  const bool need = __shfl_sync(0xffffffffu, inf2[0], 0) == -1;
+  if (need) warp_qr_rank(X, Y, a, cnt, qrres[wi]);
+  __syncwarp();
+  if (lane == 0) {
+    if (need) scen_solve(st[wi], p, inf2, pinv, qrres[wi], false);
+#pragma unroll
+    for (int i = 0; i < 7; i++) params[7ll * g + i] = p[i];
+    info[3 * g] = inf2[0];
+    info[3 * g + 1] = inf2[1];
+    info[3 * g + 2] = cnt < 7 ? 1 : 0;
+  }
+}
+
+// yhat[row] = predict7(params[model[g]], X[row]) for rows [lo[g], hi[g]) (`predict.py:43-44`)
+__global__ void k_predict_segments(const double* __restrict__ X, const long long* __restrict__ lo,
+                                   const long long* __restrict__ hi, const int32_t* __restrict__ model,
+                                   const double* __restrict__ params, double* __restrict__ yhat) {
+  const int g = blockIdx.x;
+  double w[7];
+  const int m = model ? model[g] : g;
+#pragma unroll
+  for (int i = 0; i < 7; i++) w[i] = params[7ll * m + i];
+  for (long long row = lo[g] + threadIdx.x; row < hi[g]; row += blockDim.x) yhat[row] = predict7(w, X + row * 6);
 }
 
 // ===================================================================== K8
@@ -2051,6 +2118,58 @@ int intf_scenario_eval(const intf_batch* bt, const intf_replay_buffers* buf, con
   // every tail fits the warp kernel, the block kernel is not needed
   if ((long long)bt->max_req_cap / 4 + 1 <= kEvalWarpMax) return INTF_OK;
   k_eval<<<dim3(S, 3), kEvalThreads, 0, st>>>(yhat, y, lo, report, hi, (long long)slot_stride, kEvalWarpMax + 1);
+  return launch_status("k_eval");
+}
+
+int intf_ols_fit_segments(const double* X, const double* y, const int64_t* lo, const int64_t* hi, int32_t n_seg,
+                          double* params, int32_t* info, double* Pinv, void* stream) {
+  if (!X || !y || !lo || !hi || !params || !info || n_seg < 0) return bad_input("intf_ols_fit_segments: bad argument");
+  if (n_seg == 0) return INTF_OK;
+  k_fit_segments<<<ceil_div(n_seg, kScenFitWarps), 32 * kScenFitWarps, 0, as_stream(stream)>>>(
+      X, y, (const long long*)lo, (const long long*)hi, n_seg, params, info, Pinv);
+  return launch_status("k_fit_segments");
+}
+
+int intf_predict_segments(const double* X, const int64_t* lo, const int64_t* hi, const int32_t* model,
+                          const double* params, int32_t n_seg, double* yhat, void* stream) {
+  if (!X || !lo || !hi || !params || !yhat || n_seg < 0) return bad_input("intf_predict_segments: bad argument");
+  if (n_seg == 0) return INTF_OK;
+  k_predict_segments<<<n_seg, 128, 0, as_stream(stream)>>>(X, (const long long*)lo, (const long long*)hi, model,
+                                                            params, yhat);
+  return launch_status("k_predict_segments");
+}
+
+int intf_sgd_segments(const double* X, const double* y, const int64_t* lo, const int64_t* hi, int32_t n_seg,
+                      const double* eta, double* params, double* pred, int32_t* status, void* stream) {
+  if (!X || !y || !lo || !hi || !eta || !params || !pred || n_seg < 0) return bad_input("intf_sgd_segments: bad argument");
+  if (n_seg == 0) return INTF_OK;
+  k_sgd<<<ceil_div(n_seg, 64), 64, 0, as_stream(stream)>>>(X, y, (const long long*)lo, n_seg, eta, params, pred, status,
+                                                           (const long long*)hi);
+  return launch_status("k_sgd");
+}
+
+int intf_rls_segments(const double* X, const double* y, const int64_t* lo, const int64_t* hi, int32_t n_seg,
+                      const double* lam, double* params, double* P, double* pred, int32_t* status, void* stream) {
+  if (!X || !y || !lo || !hi || !lam || !params || !P || !pred || n_seg < 0)
+    return bad_input("intf_rls_segments: bad argument");
+  if (n_seg == 0) return INTF_OK;
+  k_rls_g8<<<ceil_div(n_seg, 128 / kRlsGroup), 128, 0, as_stream(stream)>>>(X, y, (const long long*)lo, n_seg, lam,
+                                                                           params, P, pred, status,
+                                                                           (const long long*)hi);
+  return launch_status("k_rls_g8");
+}
+
+int intf_eval_segments(const double* yhat, const double* y, const int64_t* lo, const int64_t* hi, int32_t n_seg,
+                       int64_t max_len, double* out, void* stream) {
+  if (!yhat || !y || !lo || !hi || !out || n_seg < 0) return bad_input("intf_eval_segments: bad argument");
+  if (n_seg == 0) return INTF_OK;
+  cudaStream_t st = as_stream(stream);
+  k_eval_warp<<<ceil_div(n_seg, kEvalWarps), 32 * kEvalWarps, 0, st>>>(yhat, y, (const long long*)lo,
+                                                                      (const long long*)hi, n_seg, 1, 0, out);
+  int rc = launch_status("k_eval_warp");
+  if (rc || max_len <= kEvalWarpMax) return rc;
+  k_eval<<<n_seg, kEvalThreads, 0, st>>>(yhat, y, (const long long*)lo, out, (const long long*)hi, 0,
+                                         kEvalWarpMax + 1);
   return launch_status("k_eval");
 }
 

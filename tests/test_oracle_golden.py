@@ -191,3 +191,18 @@ def test_oracle_scenario_eval_matches_reference():
             assert got is None
             continue
         np.testing.assert_allclose(got, ref, rtol=1e-9, err_msg=f"scenario {i}")
+
+
+def test_oracle_drift_experiment_matches_reference():
+    """`oracle.drift_experiment` (the C3 CPU baseline and checker) against the
+    reference's drift_experiment cells for seeds 0 and 1."""
+    from paper_2512_18725_b200 import experiments as ex
+    from paper_2512_18725_b200.profiles import gen_synthetic_profiles
+
+    P = _golden.load("predict_golden.npz")
+    table = gen_synthetic_profiles()
+    otab = _otab("default")
+    for seed in (0, 1):
+        cells = O.drift_experiment(ex.drift_specs(ex.default_drift_base(table, seed)), otab)
+        assert [f"{d}/{m}" for d, m, _, _ in cells] == [str(k) for k in P[f"drift{seed}/cell_keys"]]
+        np.testing.assert_allclose([[c[2], c[3]] for c in cells], P[f"drift{seed}/cells"], rtol=1e-9)
