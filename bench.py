@@ -808,24 +808,60 @@ def product_arm(a):
     ms_step = ms_total / a.steps
     value = world * n_pred / (ms_step / 1e3)
 
-    # ---- end to end through the host-buffer C-ABI call
-    h_out = torch.empty(n_elems, dtype=torch.float32).pin_memory()
+    # ---- end to end through the host-buffer C-ABI calls: (1) the best
+    # candidate per (decision, kind, own) -- what a scheduling decision
+    # consumes: every candidate is scored, 24 KB of keys come back
+    # (intf_best_candidates_host); (2) every prediction materialised on the
+    # host (intf_predict_candidates_host, PCIe-bound: 256 MB per step)
     h_coefs = torch.tensor(W, dtype=torch.float64).pin_memory()
-    scratch = torch.empty(scorer.scratch_elems(N_DEC), dtype=torch.float32, device="cuda")
     hc = h_coefs.numpy()
+    h_best = torch.empty(2 * N_DEC * scorer.E, dtype=torch.int64).pin_memory()
+    hb = h_best.numpy().view(np.uint64)
+    bscratch = torch.empty(scorer.best_scratch_elems(N_DEC), dtype=torch.float32, device="cuda")
+
+    def best_call():
+        scorer.best_host(hc, hb, bscratch)
+        stream.synchronize()  # the caller consumes the keys on the host
+
+    for _ in range(max(3, a.warmup)):
+        best_call()
+    barrier()
+    e2e_steps = max(10, a.steps)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        best_call()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
+    bval, brank = scorer.decode_best(hb, N_DEC)
+    ok_best = bool(np.isfinite(bval).all() and (brank < scorer.n_sets).all())
+    h_out = torch.empty(n_elems, dtype=torch.float32).pin_memory()
+    scratch = torch.empty(scorer.scratch_elems(N_DEC), dtype=torch.float32, device="cuda")
     ho = h_out.numpy()
     for _ in range(max(1, a.warmup)):
         scorer.score_host(hc, ho, scratch)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(1, min(a.steps, 10))
+    mat_steps = max(1, min(a.steps, 10))
     e0.record(stream)
-    for _ in range(e2e_steps):
+    for _ in range(mat_steps):
         scorer.score_host(hc, ho, scratch)
     e1.record(stream)
     barrier()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+    mat_ms = max_over_ranks(e0.elapsed_time(e1)) / mat_steps
     ok = bool(np.isfinite(ho[:1000]).all())
+    del scratch, h_out
+    # device-resident best steps (the reduction mode's own kernel time)
+    bbufs = [scorer.alloc_best(N_DEC) for _ in range(2)]
+    scorer.pipeline_start(fused=True)
+    for k in range(a.warmup):
+        scorer.best_step(coefs, bbufs[k & 1], bbufs[(k + 1) & 1])
+    barrier()
+    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b0.record(stream)
+    for k in range(a.steps):
+        scorer.best_step(coefs, bbufs[k & 1], bbufs[(k + 1) & 1])
+    b1.record(stream)
+    barrier()
+    best_ms = max_over_ranks(b0.elapsed_time(b1)) / a.steps
 
     # ---- secondary: scenario replay sweep (C5: 10^4 scenarios, coarse / fine / adaptive)
     sweep = c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W)
@@ -878,11 +914,16 @@ def product_arm(a):
                                "candidates) x {coarse static, fine EWMA(1/2)} predictors x 32 refit decisions per "
                                "step per GPU; output fp32", "global_batch": n_pred * world,
                    "parallelism": f"dp{world} (decisions sharded, no collective)", "l2": "output 256 MB/step > L2; two output buffers alternated per step"},
-        "e2e": {"value": world * n_pred / (e2e_ms / 1e3), "unit": "predictions/s",
-                "h2d_bytes_per_step": int(W.size * 8), "d2h_bytes_per_step": int(4 * n_elems),
-                "call": "intf_predict_candidates_host (pinned host buffers)", "finite": ok,
-                "pcie_gbs": (W.size * 8 + 4 * n_elems) / (e2e_ms / 1e3) / 1e9,
-                "bound": "PCIe D2H of every fp32 prediction (the kernel is ~1% of the step)"},
+        "e2e": {"value": world * n_pred / (e2e_ms / 1e3), "unit": "predictions/s", "ms_per_call": e2e_ms,
+                "h2d_bytes_per_step": int(W.size * 8), "d2h_bytes_per_step": int(8 * 2 * N_DEC * scorer.E),
+                "call": "intf_best_candidates_host (pinned host buffers, host-timed incl. the stream sync): every "
+                        "candidate scored, the best per (decision, kind, own) returned", "valid": ok_best,
+                "materialized": {"value": world * n_pred / (mat_ms / 1e3), "unit": "predictions/s",
+                                 "call": "intf_predict_candidates_host (every fp32 prediction to the host)",
+                                 "d2h_bytes_per_step": int(4 * n_elems), "finite": ok,
+                                 "pcie_gbs": (W.size * 8 + 4 * n_elems) / (mat_ms / 1e3) / 1e9}},
+        "best_step": {"value": world * n_pred / (best_ms / 1e3), "unit": "predictions/s", "ms_per_step": best_ms,
+                      "kernel": "k_cand_step<best> (device-resident, PDL-chained, 24 KB of keys per step)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": kname,
                      "kernel_ms": launch_ms, "kernel_ms_isolated": kern_ms,

@@ -265,6 +265,27 @@ int intf_predict_candidates_prepared(const intf_table *table, int32_t cap, const
 int intf_candidate_step(const intf_table *table, int32_t cap, double alpha, const double *coefs, int32_t n_dec,
                         float *out, const float *ws_cur, float *ws_next, int64_t ws_elems, void *stream);
 
+/* Best candidate per (decision, kind, own row) -- what a scheduling decision
+ * consumes instead of every prediction: the minimum predicted interference
+ * ratio over all peer multisets of the own row, ties to the lowest multiset
+ * rank, as best[(dec * 2 + kind) * n_rows + own] =
+ *   (orderable fp32 bits of the value) << 32 | multiset rank
+ * (orderable: v >= 0 ? bits | 1<<31 : ~bits; decode with the inverse).
+ * Every candidate is still scored; only the reduction leaves the chip.
+ *   intf_candidate_best_step: one pipelined step like intf_candidate_step;
+ *     best must hold the all-ones key on entry (the previous step's prep
+ *     blocks reset best_next for the next step); keep >= 2 key buffers and
+ *     read step k's keys before step k + (buffers - 1) is launched.
+ *   intf_best_candidates_host: host coefficients in, host keys out (copies
+ *     on `stream`, caller synchronises); d_scratch holds 4 n_dec * 7 +
+ *     4 n_dec * n_rows + the candidate workspace floats.                    */
+int intf_candidate_best_step(const intf_table *table, int32_t cap, double alpha, const double *coefs, int32_t n_dec,
+                             uint64_t *best, uint64_t *best_next, const float *ws_cur, float *ws_next,
+                             int64_t ws_elems, void *stream);
+int intf_best_candidates_host(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
+                              int32_t n_dec, uint64_t *h_best, float *d_scratch, int64_t scratch_elems,
+                              void *stream);
+
 /* Host-buffer variant (the end-to-end call): copies coefs in and all
  * predictions out (tiled layout above).  h_out: ceil(n_dec/4)*4*2*n_rows*ld
  * floats; d_scratch: device floats = 28*n_dec + that output size (+ the

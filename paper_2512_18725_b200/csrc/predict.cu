@@ -360,13 +360,101 @@ static_assert(kCandThreads * kGroup == kTileR, "k_candidates blocks cover one ti
 // grid: x = groups of 4 multisets, y = own row, z = decision chunks.  The
 // thread's feature loads (L2-resident C0/FE) are issued before the block
 // builds its coefficient slab, so their latency overlaps that setup.
+// kBest: instead of storing every prediction, reduce them per (decision,
+// kind, own) to the best candidate -- the minimum predicted interference
+// ratio, ties to the lowest multiset rank -- as one 64-bit key
+// (orderable(fp32 value) << 32 | rank) folded into best[] by atomicMin:
+// warp minima by redux.sync on the value key and then on the rank among the
+// lanes holding it, block minima through shared memory, one atomic per
+// (decision, kind) per block.
+__device__ __forceinline__ unsigned f32_key(float v) {
+  const unsigned u = __float_as_uint(v);
+  return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+
+constexpr int kBestSpan = 4;  // groups of 4 multisets per thread in the best-candidate reduction
+
+template <bool kBest>
 __device__ __forceinline__ void cand_stream_body(int bx, int by, int bz, const double* __restrict__ thr, int E,
                                                  long long ld, long long n_sets, const double* __restrict__ coefs,
                                                  int n_dec, const float* __restrict__ C0,
-                                                 const float* __restrict__ FE, float* __restrict__ out) {
+                                                 const float* __restrict__ FE, float* __restrict__ out,
+                                                 unsigned long long* __restrict__ best = nullptr) {
   __shared__ float4 cw[kStreamDec][2];
   const int o = by;
   const int d0 = bz * kStreamDec, nd = min(kStreamDec, n_dec - d0);
+  if constexpr (kBest) {
+    // kBestSpan groups of 4 multisets per thread (strided by the block, so
+    // loads stay coalesced): the warp / block reductions amortise over 16
+    // multisets instead of 4; nothing is written per candidate
+    for (int t = threadIdx.x; t < 2 * nd; t += blockDim.x) {
+      const int d = t >> 1, kind = t & 1;
+      const double* w = coefs + ((d0 + d) * 2 + kind) * 7;
+      const double* x = thr + 3 * o;
+      const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
+      cw[d][kind] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
+    }
+    __syncthreads();
+    __shared__ unsigned red_v[kStreamThreads / 32][kStreamDec][2], red_i[kStreamThreads / 32][kStreamDec][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned vc[kStreamDec], vf[kStreamDec], ic[kStreamDec], jf[kStreamDec];
+#pragma unroll
+    for (int d = 0; d < kStreamDec; d++) vc[d] = vf[d] = ic[d] = jf[d] = 0xffffffffu;
+#pragma unroll
+    for (int c = 0; c < kBestSpan; c++) {
+      const long long r0 = (((long long)bx * kBestSpan + c) * blockDim.x + threadIdx.x) * 4;
+      const long long nl = r0 < ld ? n_sets - r0 : 0;  // valid multisets of this group (<= 0: none)
+      const long long rr = r0 < ld ? r0 : 0;
+      const float4 cx = __ldg(reinterpret_cast<const float4*>(C0 + rr));
+      const float4 cy = __ldg(reinterpret_cast<const float4*>(C0 + ld + rr));
+      const float4 cz = __ldg(reinterpret_cast<const float4*>(C0 + 2 * ld + rr));
+      const float4 fx = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 0) * ld + rr));
+      const float4 fy = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 1) * ld + rr));
+      const float4 fz = __ldg(reinterpret_cast<const float4*>(FE + ((long long)o * 3 + 2) * ld + rr));
+#pragma unroll
+      for (int d = 0; d < kStreamDec; d++) {
+        if (d >= nd) break;
+        const float4 a = cw[d][0], b = cw[d][1];
+        const float yc[4] = {fmaf(a.z, cz.x, fmaf(a.y, cy.x, fmaf(a.x, cx.x, a.w))),
+                             fmaf(a.z, cz.y, fmaf(a.y, cy.y, fmaf(a.x, cx.y, a.w))),
+                             fmaf(a.z, cz.z, fmaf(a.y, cy.z, fmaf(a.x, cx.z, a.w))),
+                             fmaf(a.z, cz.w, fmaf(a.y, cy.w, fmaf(a.x, cx.w, a.w)))};
+        const float yf[4] = {fmaf(b.z, fz.x, fmaf(b.y, fy.x, fmaf(b.x, fx.x, b.w))),
+                             fmaf(b.z, fz.y, fmaf(b.y, fy.y, fmaf(b.x, fx.y, b.w))),
+                             fmaf(b.z, fz.z, fmaf(b.y, fy.z, fmaf(b.x, fx.z, b.w))),
+                             fmaf(b.z, fz.w, fmaf(b.y, fy.w, fmaf(b.x, fx.w, b.w)))};
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          if (i < nl) {  // groups in ascending rank: strict < keeps the lowest rank on ties
+            const unsigned kc = f32_key(yc[i]), kf = f32_key(yf[i]);
+            if (kc < vc[d]) vc[d] = kc, ic[d] = (unsigned)(r0 + i);
+            if (kf < vf[d]) vf[d] = kf, jf[d] = (unsigned)(r0 + i);
+          }
+        }
+      }
+    }
+    for (int d = 0; d < nd; d++) {
+      const unsigned wc = __reduce_min_sync(0xffffffffu, vc[d]), wf = __reduce_min_sync(0xffffffffu, vf[d]);
+      const unsigned xc = __reduce_min_sync(0xffffffffu, vc[d] == wc ? ic[d] : 0xffffffffu);
+      const unsigned xf = __reduce_min_sync(0xffffffffu, vf[d] == wf ? jf[d] : 0xffffffffu);
+      if (lane == 0) {
+        red_v[warp][d][0] = wc, red_i[warp][d][0] = xc;
+        red_v[warp][d][1] = wf, red_i[warp][d][1] = xf;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * nd) {
+      const int d = threadIdx.x >> 1, kind = threadIdx.x & 1;
+      unsigned long long key = ~0ull;
+#pragma unroll
+      for (int w = 0; w < kStreamThreads / 32; w++) {
+        const unsigned long long k2 = ((unsigned long long)red_v[w][d][kind] << 32) | red_i[w][d][kind];
+        key = k2 < key ? k2 : key;
+      }
+      if (key != ~0ull) atomicMin(best + ((long long)(d0 + d) * 2 + kind) * E + o, key);
+    }
+    return;
+  }
   const long long r0 = ((long long)bx * blockDim.x + threadIdx.x) * 4;
   const bool inb = r0 < ld;
   const long long rr = inb ? r0 : 0;
@@ -423,7 +511,7 @@ __global__ void __launch_bounds__(kStreamThreads, 8) k_cand_stream(const double*
                                                                    const float* __restrict__ C0,
                                                                    const float* __restrict__ FE,
                                                                    float* __restrict__ out) {
-  cand_stream_body(blockIdx.x, blockIdx.y, blockIdx.z, thr, E, ld, n_sets, coefs, n_dec, C0, FE, out);
+  cand_stream_body<false>(blockIdx.x, blockIdx.y, blockIdx.z, thr, E, ld, n_sets, coefs, n_dec, C0, FE, out);
 }
 
 // One pipelined step in ONE launch: the forward of every candidate from the
@@ -433,11 +521,15 @@ __global__ void __launch_bounds__(kStreamThreads, 8) k_cand_stream(const double*
 // synchronisation or second launch sits between steps.  1-D grid: the first
 // n_prep blocks are prep blocks (dispatched first, they run beside the
 // stream blocks instead of after them).
-template <int KMAX>
+// kBest: the stream blocks reduce to best[] (see cand_stream_body) and the
+// prep blocks also reset best_next[0, n_best) for the next step.
+template <int KMAX, bool kBest = false>
 __global__ void __launch_bounds__(kStreamThreads, 8) k_cand_step(
     const double* __restrict__ solo, const double* __restrict__ thr, int E, int cap, long long n_sets, long long ld,
     double alpha, const double* __restrict__ coefs, int n_dec, const float* __restrict__ ws_cur,
-    float* __restrict__ ws_next, float* __restrict__ out, int prep_x, int prep_y, int prep_own, int stream_x) {
+    float* __restrict__ ws_next, float* __restrict__ out, int prep_x, int prep_y, int prep_own, int stream_x,
+    unsigned long long* __restrict__ best = nullptr, unsigned long long* __restrict__ best_next = nullptr,
+    long long n_best = 0) {
   // programmatic dependent launch: let the next step's grid be scheduled as
   // soon as every CTA of this one is running, and wait for the previous
   // step's grid (its prep blocks wrote ws_cur; its stream blocks read
@@ -449,11 +541,16 @@ __global__ void __launch_bounds__(kStreamThreads, 8) k_cand_step(
   if (b < n_prep) {
     cand_prep_body<KMAX>(b % prep_x, b / prep_x, solo, thr, E, cap, n_sets, ld, alpha, ws_next, ws_next + 3 * ld,
                          prep_own);
+    if constexpr (kBest) {
+      if (best_next)
+        for (long long i = (long long)b * blockDim.x + threadIdx.x; i < n_best; i += (long long)n_prep * blockDim.x)
+          best_next[i] = ~0ull;
+    }
     return;
   }
   b -= n_prep;
   const int bx = b % stream_x, rest = b / stream_x;
-  cand_stream_body(bx, rest % E, rest / E, thr, E, ld, n_sets, coefs, n_dec, ws_cur, ws_cur + 3 * ld, out);
+  cand_stream_body<kBest>(bx, rest % E, rest / E, thr, E, ld, n_sets, coefs, n_dec, ws_cur, ws_cur + 3 * ld, out, best);
 }
 
 // ===================================================================== K6
@@ -1809,14 +1906,18 @@ static int launch_stream(const intf_table* t, int cap, const double* coefs, int 
 
 template <int K>
 static int launch_step(const intf_table* t, int cap, double alpha, const double* coefs, int n_dec, float* out,
-                       const float* ws_cur, float* ws_next, cudaStream_t st) {
+                       const float* ws_cur, float* ws_next, cudaStream_t st, unsigned long long* best = nullptr,
+                       unsigned long long* best_next = nullptr) {
   const int E = t->n_rows;
   const long long sets = n_multisets(E, cap), ld = cand_ld(sets);
   const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_cand_step<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_cand_step<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   const int po = kStepPrepOwn;
   const int px = (int)ceil_div(ld, 128), py = (int)ceil_div(E, po);
-  const int sx = (int)ceil_div(ld / 4, kStreamThreads);
+  const int sx = (int)ceil_div(ld / 4, kStreamThreads * (best ? kBestSpan : 1));
   const long long nblk = (ws_next ? (long long)px * py : 0) + (long long)sx * E * ceil_div(n_dec, kStreamDec);
   if (nblk > 0x7fffffffLL) return bad_input("intf_candidate_step: too many blocks");
   cudaLaunchConfig_t cfg = {};
@@ -1829,8 +1930,14 @@ static int launch_step(const intf_table* t, int cap, double alpha, const double*
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_cand_step<K>, t->solo_ms, t->thr, E, cap, sets, ld, alpha, coefs, n_dec, ws_cur, ws_next,
-                     out, px, py, po, sx);
+  if (best) {
+    const long long n_best = 2ll * n_dec * E;
+    cudaLaunchKernelEx(&cfg, k_cand_step<K, true>, t->solo_ms, t->thr, E, cap, sets, ld, alpha, coefs, n_dec, ws_cur,
+                       ws_next, out, px, py, po, sx, best, best_next, n_best);
+    return launch_status("k_cand_step<best>");
+  }
+  cudaLaunchKernelEx(&cfg, k_cand_step<K, false>, t->solo_ms, t->thr, E, cap, sets, ld, alpha, coefs, n_dec, ws_cur,
+                     ws_next, out, px, py, po, sx, (unsigned long long*)nullptr, (unsigned long long*)nullptr, 0ll);
   return launch_status("k_cand_step");
 }
 
@@ -1946,6 +2053,28 @@ int intf_predict_candidates_prepared(const intf_table* table, int32_t cap, const
   return launch_stream(table, cap, coefs, n_dec, out, const_cast<float*>(ws), as_stream(stream));
 }
 
+int intf_candidate_best_step(const intf_table* table, int32_t cap, double alpha, const double* coefs,
+                             int32_t n_dec, uint64_t* best, uint64_t* best_next, const float* ws_cur, float* ws_next,
+                             int64_t ws_elems, void* stream) {
+  int64_t need = 0;
+  if (!table || !coefs || !best || !ws_cur || !ws_next || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1 ||
+      intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need || ws_next == ws_cur ||
+      best_next == best)
+    return bad_input("intf_candidate_best_step: bad argument or workspace too small");
+  cudaStream_t st = as_stream(stream);
+  unsigned long long *b = (unsigned long long*)best, *bn = (unsigned long long*)best_next;
+  switch (cap - 1) {
+    case 0: return launch_step<0>(table, cap, alpha, coefs, n_dec, nullptr, ws_cur, ws_next, st, b, bn);
+    case 1: return launch_step<1>(table, cap, alpha, coefs, n_dec, nullptr, ws_cur, ws_next, st, b, bn);
+    case 2: return launch_step<2>(table, cap, alpha, coefs, n_dec, nullptr, ws_cur, ws_next, st, b, bn);
+    case 3: return launch_step<3>(table, cap, alpha, coefs, n_dec, nullptr, ws_cur, ws_next, st, b, bn);
+    case 4: return launch_step<4>(table, cap, alpha, coefs, n_dec, nullptr, ws_cur, ws_next, st, b, bn);
+    case 5: return launch_step<5>(table, cap, alpha, coefs, n_dec, nullptr, ws_cur, ws_next, st, b, bn);
+    case 6: return launch_step<6>(table, cap, alpha, coefs, n_dec, nullptr, ws_cur, ws_next, st, b, bn);
+    default: return launch_step<7>(table, cap, alpha, coefs, n_dec, nullptr, ws_cur, ws_next, st, b, bn);
+  }
+}
+
 int intf_candidate_step(const intf_table* table, int32_t cap, double alpha, const double* coefs, int32_t n_dec,
                         float* out, const float* ws_cur, float* ws_next, int64_t ws_elems, void* stream) {
   int64_t need = 0;
@@ -1988,6 +2117,41 @@ int intf_predict_candidates_host(const intf_table* table, int32_t cap, double al
   if (rc) return rc;
   if (cudaMemcpyAsync(h_out, d_out, sizeof(float) * n_out, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return launch_status("copy predictions");
+  return INTF_OK;
+}
+
+int intf_best_candidates_host(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
+                              int32_t n_dec, uint64_t* h_best, float* d_scratch, int64_t scratch_elems,
+                              void* stream) {
+  if (!table || !h_coefs || !h_best || !d_scratch || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1)
+    return bad_input("intf_best_candidates_host: bad argument");
+  int64_t ws = 0;
+  intf_candidate_workspace(table->n_rows, cap, &ws);
+  const long long n_coef = 2LL * n_dec * 2 * 7, n_best = 2LL * n_dec * table->n_rows;
+  if (scratch_elems < n_coef + 2 * n_best + ws) return bad_input("intf_best_candidates_host: scratch too small");
+  cudaStream_t st = as_stream(stream);
+  // scratch: [coefs as doubles][best keys as u64][feature workspace]
+  double* d_coefs = reinterpret_cast<double*>(d_scratch);
+  unsigned long long* d_best = reinterpret_cast<unsigned long long*>(d_scratch + n_coef);
+  float* d_ws = d_scratch + n_coef + 2 * n_best;
+  if (cudaMemcpyAsync(d_coefs, h_coefs, sizeof(double) * n_dec * 2 * 7, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return launch_status("copy coefs");
+  cudaMemsetAsync(d_best, 0xff, sizeof(unsigned long long) * n_best, st);
+  int rc = intf_candidate_prepare(table, cap, alpha, d_ws, ws, stream);
+  if (rc) return rc;
+  switch (cap - 1) {
+    case 0: rc = launch_step<0>(table, cap, alpha, d_coefs, n_dec, nullptr, d_ws, nullptr, st, d_best); break;
+    case 1: rc = launch_step<1>(table, cap, alpha, d_coefs, n_dec, nullptr, d_ws, nullptr, st, d_best); break;
+    case 2: rc = launch_step<2>(table, cap, alpha, d_coefs, n_dec, nullptr, d_ws, nullptr, st, d_best); break;
+    case 3: rc = launch_step<3>(table, cap, alpha, d_coefs, n_dec, nullptr, d_ws, nullptr, st, d_best); break;
+    case 4: rc = launch_step<4>(table, cap, alpha, d_coefs, n_dec, nullptr, d_ws, nullptr, st, d_best); break;
+    case 5: rc = launch_step<5>(table, cap, alpha, d_coefs, n_dec, nullptr, d_ws, nullptr, st, d_best); break;
+    case 6: rc = launch_step<6>(table, cap, alpha, d_coefs, n_dec, nullptr, d_ws, nullptr, st, d_best); break;
+    default: rc = launch_step<7>(table, cap, alpha, d_coefs, n_dec, nullptr, d_ws, nullptr, st, d_best); break;
+  }
+  if (rc) return rc;
+  if (cudaMemcpyAsync(h_best, d_best, sizeof(unsigned long long) * n_best, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return launch_status("copy best candidates");
   return INTF_OK;
 }
 

@@ -601,6 +601,50 @@ class CandidateScorer:
         self._ready[nxt].record(side)
         self._k += 1
 
+    # ---- best candidate per (decision, kind, own): the reduction a scheduler consumes
+    def alloc_best(self, n_dec: int) -> torch.Tensor:
+        """Key buffer [n_dec][2][E] (int64 view of the u64 keys), reset to the all-ones key."""
+        return torch.full((2 * n_dec * self.E,), -1, dtype=torch.int64, device=self.dev)
+
+    def best_step(self, coefs: torch.Tensor, best: torch.Tensor, best_next: torch.Tensor, kernel_events=None) -> None:
+        """One pipelined step (after pipeline_start(fused=True)) that scores
+        every candidate of coefs' decisions but keeps only the best one per
+        (decision, kind, own) in `best` (intf_candidate_best_step); resets
+        best_next and builds the next step's features in the same launch."""
+        s = torch.cuda.current_stream(self.dev)
+        cur, nxt = self._k & 1, (self._k + 1) & 1
+        if kernel_events:
+            kernel_events[0].record(s)
+        _abi.check(_abi.load().intf_candidate_best_step(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
+                                                        coefs.data_ptr(), coefs.numel() // 14, best.data_ptr(),
+                                                        best_next.data_ptr(), self._ws[cur].data_ptr(),
+                                                        self._ws[nxt].data_ptr(), self.ws_elems, s.cuda_stream),
+                   "intf_candidate_best_step")
+        if kernel_events:
+            kernel_events[1].record(s)
+        self._k += 1
+
+    def best_scratch_elems(self, n_dec: int) -> int:
+        """Device floats needed by best_host."""
+        return 28 * n_dec + 4 * n_dec * self.E + self.ws_elems
+
+    def best_host(self, coefs_host: np.ndarray, best_host: np.ndarray, scratch: torch.Tensor) -> None:
+        """End to end, host buffers (intf_best_candidates_host): host coefs in,
+        the best candidate keys [n_dec][2][E] (uint64) out; enqueue only."""
+        n_dec = coefs_host.size // 14
+        _abi.check(_abi.load().intf_best_candidates_host(ctypes.byref(self.dtable.struct), self.cap, self.alpha,
+                                                         coefs_host.ctypes.data, n_dec, best_host.ctypes.data,
+                                                         scratch.data_ptr(), scratch.numel(), stream_ptr()),
+                   "intf_best_candidates_host")
+
+    def decode_best(self, keys, n_dec: int):
+        """(value [n_dec][2][E] float32, multiset rank [n_dec][2][E] int64) of
+        best keys (torch or numpy, int64 or uint64)."""
+        k = np.asarray(keys.cpu().numpy() if hasattr(keys, "cpu") else keys).view(np.uint64).reshape(n_dec, 2, self.E)
+        hi = (k >> np.uint64(32)).astype(np.uint32)
+        bits = np.where(hi >> np.uint32(31), hi & np.uint32(0x7FFFFFFF), ~hi).astype(np.uint32)
+        return bits.view(np.float32), (k & np.uint64(0xFFFFFFFF)).astype(np.int64)
+
     def pipeline_join(self) -> None:
         """Make the current stream wait for the side stream's last feature build."""
         if not self._fused:

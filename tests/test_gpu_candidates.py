@@ -112,3 +112,39 @@ def test_pipelined_steps_equal_one_shot(fused):
         ref = sc.alloc(len(W))
         sc.score(torch.tensor(W, device="cuda").contiguous(), ref)
         np.testing.assert_array_equal(sc.view_full(out.cpu().numpy(), len(W)), sc.view_full(ref.cpu().numpy(), len(W)))
+
+
+def test_best_candidate_step_equals_argmin_of_full_output():
+    """intf_candidate_best_step (the per-decision reduction a scheduler
+    consumes) equals the argmin of the materialised predictions of the same
+    step: the same fp32 values, the lowest multiset rank on ties; the host
+    variant equals the device step; and against the fp64 restatement the
+    chosen candidate is the best one within the 1e-5 tolerance."""
+    from paper_2512_18725_b200.profiles import gen_synthetic_profiles
+    from paper_2512_18725_b200.sweep import c2_decision_coefs
+
+    sc = _scorer(4)
+    W = np.ascontiguousarray(c2_decision_coefs(32, 0.5)[[0, 7, 19, 31]])
+    coefs = torch.tensor(W, dtype=torch.float64, device="cuda").contiguous()
+    out = sc.alloc(4)
+    bufs = [sc.alloc_best(4) for _ in range(3)]
+    sc.pipeline_start(fused=True)
+    sc.pipeline_step(coefs, out)  # materialised step (features of step 0)
+    sc.best_step(coefs, bufs[0], bufs[1])  # best step (features rebuilt by step 0's prep blocks)
+    sc.pipeline_join()
+    y = sc.view(out.cpu().numpy(), 4)
+    val, rank = sc.decode_best(bufs[0], 4)
+    am = y.argmin(axis=-1)
+    assert np.array_equal(rank, am)
+    assert np.array_equal(val, np.take_along_axis(y, am[..., None], -1)[..., 0])
+    assert np.all(bufs[1].cpu().numpy() == -1)  # reset for the next step
+    scratch = torch.empty(sc.best_scratch_elems(4), dtype=torch.float32, device="cuda")
+    hb = np.zeros(4 * 2 * sc.E, dtype=np.uint64)
+    sc.best_host(W, hb, scratch)
+    torch.cuda.synchronize()
+    assert np.array_equal(hb.view(np.int64), bufs[0].cpu().numpy())
+    ta = gen_synthetic_profiles().arrays()
+    ref = O.candidate_predictions_all(ta.solo, ta.thr, 4, W, 0.5)
+    rmin = ref.min(axis=-1)
+    np.testing.assert_allclose(val, rmin, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(np.take_along_axis(ref, rank[..., None], -1)[..., 0], rmin, rtol=2 * RTOL, atol=0)
