@@ -196,6 +196,11 @@ typedef struct intf_jobs {
   int32_t min_len, total_slots;
   double *scratch;             /* [6 * total_slots] doubles: block-parallel plan/verify of long traces
                                   (scenarios with req_cap >= 32768: one 1024-thread block each) */
+  int32_t own_lo, own_hi;      /* multi-GPU sharding of one trace: intf_jobs_replay replays only jobs whose
+                                  first batch lies in [own_lo, own_hi) and writes last = -inf, info = 0 for
+                                  the others, so an element-wise MAX over the ranks (NCCL all_reduce) of
+                                  last[] and info[] gives every rank the full job results before
+                                  intf_jobs_verify; one rank: [0, INT32_MAX) */
 } intf_jobs;
 
 int intf_jobs_plan(const intf_batch *batch, const intf_table *table, const intf_replay_buffers *buf,

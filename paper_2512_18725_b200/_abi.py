@@ -70,7 +70,8 @@ class ReplayBuffers(ctypes.Structure):
 class Jobs(ctypes.Structure):
     _fields_ = [(f, P) for f in ("joff", "jcap", "lo", "hi", "n_jobs", "last", "info", "dirty", "todo",
                                  "todo_count", "slot_scen")] + [("slow", c_double), ("min_len", c_int32),
-                                                                ("total_slots", c_int32), ("scratch", P)]
+                                                                ("total_slots", c_int32), ("scratch", P),
+                                                                ("own_lo", c_int32), ("own_hi", c_int32)]
 
 
 class Predictor(ctypes.Structure):

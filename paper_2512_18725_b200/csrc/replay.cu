@@ -1311,6 +1311,14 @@ __global__ void __launch_bounds__(32 * kJobWarps, INTF_JOB_MINB) k_jobs_replay(c
     const intf_scenario& S = scen[s];
     const int per = 2 * S.cap - 1;
     const int jlo = J.lo[slot], jhi = J.hi[slot];
+    if (jlo < J.own_lo || jlo >= J.own_hi) {  // another rank's job: neutral for the MAX all_reduce
+      if ((threadIdx.x & (kReplayW - 1)) == 0) {
+        J.info[3 * slot] = J.info[3 * slot + 1] = J.info[3 * slot + 2] = 0;
+        J.last[slot] = -INFINITY;
+        J.dirty[slot] = 0;
+      }
+      continue;
+    }
     const ReplayJob RJ{s, jlo, jhi, S.seg_off + jlo * per, (jhi - jlo) * per, k};
     const ReplayJobOut r = replay_group<kReplayW>(RJ, scen, models, tab, B, sseg[g], 0);
     if ((threadIdx.x & (kReplayW - 1)) == 0) {
@@ -1529,6 +1537,7 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
         // as the sequential scan stops at digit 255)
         const bool mine = (left >= excl && left < incl) || (lane == 31 && left >= incl);
         const unsigned who = __ballot_sync(0xffffffffu, mine);
+        __syncwarp();  // every lane has read rank_left[mm][q] before the owner lane rewrites it
         if (lane == __ffs(who) - 1) {
           int l = left - excl;
           unsigned int d = lane * 8;

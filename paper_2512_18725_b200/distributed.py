@@ -171,3 +171,103 @@ def sweep(specs_all: list, table, preds=(), device_rows: bool = True):
     if device_rows:
         local = local.cuda()
     return gather_rows(local, len(specs_all)).cpu().numpy()
+
+
+# per-batch outputs of the replay that the owner of a batch writes (b_* by
+# batch slot, out_order by outcome position = the same job ranges)
+TRACE_GATHER = ("b_start", "b_completion", "b_measured", "b_nseg", "b_seg_off", "b_running", "out_order")
+
+
+def _all_reduce(t: torch.Tensor, op, backend: str) -> None:
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        dist.all_reduce(t, op=op)
+    else:  # gloo: host copies (tests / plumbing runs)
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+
+
+def replay_trace_sharded(pipe, slow: float = 2.0, min_len: int = 96, passes: int = 4, slo: bool = True,
+                         backend: str = "nccl", max_iters: int = 1000) -> dict:
+    """ONE long trace (a single-scenario ReplayPipeline) replayed across the
+    ranks: arrivals, batch formation and the speculative
+    busy-period job plan are computed on every rank (identical, deterministic);
+    the trace's batches are split into contiguous ranges, one per rank, and
+    each rank replays only the jobs that start in its range
+    (intf_jobs.own_lo/own_hi).  After every replay pass the job results (last
+    completion, status/segment/reseat counts) are combined with an
+    element-wise MAX all_reduce (non-owners hold -inf / 0), so every rank runs
+    the same boundary verification and merges failing boundaries the same way
+    -- a merged job belongs to the rank owning its first batch.  At the end
+    each rank zeroes the per-batch outputs outside the batches of its final
+    jobs and a SUM all_reduce assembles the whole trace on every rank, where
+    the SLO report runs.  Bit-identical to the one-GPU replay."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import _abi, engine
+
+    if pipe.pb.n_scen != 1:
+        raise ValueError("replay_trace_sharded shards one trace (a single-scenario pipeline)")
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    L, st = pipe.lib, engine.stream_ptr()
+    bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
+    tab = ctypes.byref(pipe.dtable.struct)
+    jobs = getattr(pipe, "_jobs", None)
+    if jobs is None or jobs.key != (float(slow), int(min_len)):
+        jobs = engine._DeviceJobs(pipe, slow, min_len)
+        pipe._jobs = jobs
+    J = ctypes.byref(jobs.J)
+    _abi.check(L.intf_generate_arrivals(bt, B, st), "intf_generate_arrivals")
+    _abi.check(L.intf_form_batches(bt, B, st), "intf_form_batches")
+    for f in TRACE_GATHER:  # entries this rank does not own must be zero for the final SUM
+        pipe.t[f].zero_()
+    _abi.check(L.intf_jobs_plan(bt, tab, B, J, st), "intf_jobs_plan")
+    nb = int(pipe.t["n_batches"][0].item())
+    lo, hi = shard_range(nb, rank, world)
+    jobs.J.own_lo = 0 if rank == 0 else lo
+    jobs.J.own_hi = 2 ** 31 - 1 if rank == world - 1 else hi
+    total = int(jobs.J.total_slots)
+    need = total * pipe.pb.cap_max * pipe.seg_stride * 5
+    if pipe.t["slot_seg"].numel() < need:
+        pipe.t["slot_seg"] = torch.zeros(need, dtype=torch.float64, device=pipe.dev)
+        pipe.B.slot_seg = pipe.t["slot_seg"].data_ptr()
+
+    def one_pass(n_todo: int) -> None:
+        _abi.check(L.intf_jobs_replay(bt, tab, B, J, n_todo, st), "intf_jobs_replay")
+        if world > 1:
+            _all_reduce(jobs.t["last"], dist.ReduceOp.MAX, backend)
+            _all_reduce(jobs.t["info"], dist.ReduceOp.MAX, backend)
+        _abi.check(L.intf_jobs_verify(bt, B, J, st), "intf_jobs_verify")
+
+    n0 = int(jobs.t["n_jobs"][0].item())
+    for _ in range(passes):  # queued with device-side job counts
+        one_pass(-total)
+    iters = passes
+    while iters < max_iters:
+        n = int(jobs.t["todo_count"].item())
+        if n == 0:
+            break
+        one_pass(n)
+        iters += 1
+    # batches of this rank's final jobs: a contiguous range [first, last)
+    nj = int(jobs.t["n_jobs"][0].item())
+    jlo = jobs.t["lo"][:nj].cpu().numpy()
+    jhi = jobs.t["hi"][:nj].cpu().numpy()
+    mine = (jlo >= jobs.J.own_lo) & (jlo < jobs.J.own_hi)
+    first, last = (int(jlo[mine].min()), int(jhi[mine].max())) if mine.any() else (0, 0)
+    if world > 1:
+        ro = pipe.pb.scen[0].req_off
+        for f in TRACE_GATHER:
+            t = pipe.t[f]
+            t[: ro + first].zero_()
+            t[ro + last:].zero_()
+            _all_reduce(t, dist.ReduceOp.SUM, backend)
+    if slo:
+        pipe.run_slo_features(slo=True, features=False)
+    return {"jobs_initial": n0, "jobs_final": nj, "iterations": iters, "batches": nb,
+            "rank_batches": [first, last], "world": world}

@@ -894,7 +894,7 @@ class _DeviceJobs:
             "scratch": torch.zeros(6 * total, dtype=torch.float64, device=dev),  # long-trace plan/verify
         }
         self.J = _abi.Jobs(**{k: v.data_ptr() for k, v in self.t.items()}, slow=float(slow), min_len=int(min_len),
-                           total_slots=total)
+                           total_slots=total, own_lo=0, own_hi=2**31 - 1)
         self.key = (float(slow), int(min_len))
 
 

@@ -73,3 +73,50 @@ def test_weighted_shards_cover_and_balance():
     assert sh[0][0] == 0 and sh[-1][1] == 1000
     loads = [w[l:h].sum() for l, h in sh]
     assert max(loads) / min(loads) < 1.05
+
+
+def test_lpt_shards_cover_balance_and_order():
+    """C5 strong-scaling split: every scenario exactly once, loads within a
+    few percent, each rank's list in descending weight (its replay order)."""
+    from paper_2512_18725_b200.profiles import gen_synthetic_profiles
+    from paper_2512_18725_b200.sweep import c5_scenarios, expected_requests
+
+    w = [expected_requests(s) for s in c5_scenarios(gen_synthetic_profiles(), 2000)]
+    for world in (1, 2, 4, 8):
+        sh = D.lpt_shards(w, world)
+        assert sorted(i for s in sh for i in s) == list(range(len(w)))
+        loads = [sum(w[i] for i in s) for s in sh]
+        assert max(loads) / min(loads) < 1.01
+        for s in sh:
+            assert all(w[a] >= w[b] for a, b in zip(s, s[1:]))
+    assert D.lpt_shards(w, 8) == D.lpt_shards(list(w), 8)  # deterministic: every rank computes the same split
+
+
+def _sweep_rows_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        counts = [5, 3]
+        local = torch.full((counts[rank], D.SWEEP_ROW), float(rank), dtype=torch.float64)
+        blocks = D.gather_sweep_rows(local, counts, backend="gloo")
+        q.put((rank, [b.numpy() for b in blocks]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_gather_sweep_rows_uneven():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_rows_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, blocks in res:
+        assert [b.shape[0] for b in blocks] == [5, 3]
+        assert (blocks[0] == 0).all() and (blocks[1] == 1).all()

@@ -1,0 +1,42 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck,
+racecheck, synccheck): the smoke (bundled trace replay + features + a cap-3
+candidate step), a 2x10^5-request C4 trace (long-list arrivals / formation /
+busy-period jobs / grid SLO), a 256-scenario C5 sweep with the per-scenario
+evaluation, the best-candidate step, the windowed OLS (TMA) and the
+RLS / SGD / drift paths."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import __graft_entry__  # noqa: E402
+
+__graft_entry__.smoke()
+import paper_2512_18725_b200 as p  # noqa: E402
+from paper_2512_18725_b200 import _abi, engine, experiments as ex  # noqa: E402
+from paper_2512_18725_b200.sweep import c2_decision_coefs, c4_scenario, c5_scenarios, lpt_order, table16  # noqa: E402
+
+t16, arch = table16()
+pipe = engine.ReplayPipeline([c4_scenario(t16, arch, n_requests=2e5)], t16.arrays(), scale=1.5)
+st = engine.replay_segmented(pipe, passes=4)
+print("c4 2e5", st, int(pipe.status()[0]))
+table = p.gen_synthetic_profiles()
+preds = [_abi.Predictor(ewma=0, alpha=1.0, w=(0.0,) * 7), _abi.Predictor(ewma=1, alpha=0.5, w=(0.0,) * 7)]
+pp = engine.ReplayPipeline(lpt_order(c5_scenarios(table, 256)), table.arrays(), preds=preds, scale=1.5,
+                           evaluate=(0, 1, 0.99))
+pp.run()
+torch.cuda.synchronize()
+print("c5 256", int((pp.status() != 0).sum()), int((pp.eval_status.cpu().numpy()[:256] & 1).sum()))
+sc = engine.CandidateScorer(table.arrays(), cap=3, alpha=0.5)
+W = torch.tensor(c2_decision_coefs(8), device="cuda").contiguous()
+bb = [sc.alloc_best(8) for _ in range(2)]
+sc.pipeline_start(fused=True)
+sc.best_step(W, bb[0], bb[1])
+torch.cuda.synchronize()
+X = np.random.default_rng(0).uniform(0, 1, size=(4096, 6))
+y = X @ np.arange(1, 7) + 1.0
+print("ols windows", len(p.predict.fit_ols_windows(X, y, 64)))
+cells = ex.drift_experiment(ex.default_drift_base(table, 0), table)
+print("drift", len(cells))
