@@ -297,17 +297,20 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     """C4 shape: one 10^6-request, 16-model (bs <= 64, cap 4) trace replayed
     with busy-period sharding (speculative idle boundaries planned, verified
     and merged on the device; C4_PASSES passes queued with device-side job
-    counts, one host read per trace, inside the timed region).  Each rank
-    replays its own trace (weak scaling).  Also: back-to-back traces on four
-    buffer sets and streams, two traces each (`pipelined`)."""
+    counts, one host read per trace, inside the timed region).  N > 1: the
+    SAME trace sharded across the ranks (c4_sharded).  Also at N = 1:
+    back-to-back replays of the trace on four buffer sets and streams, two
+    each (`pipelined`: repeated replays of one trace, each checked complete)."""
     import torch
     from paper_2512_18725_b200 import engine
     from paper_2512_18725_b200.sweep import c4_scenario, table16
 
     t16, arch = table16()
-    spec = c4_scenario(t16, arch, n_requests=C4_REQUESTS, seed=1 + rank)
+    spec = c4_scenario(t16, arch, n_requests=C4_REQUESTS, seed=1)  # ONE trace, the same on every rank
     ta = t16.arrays()
-    n_c4_pipes = int(os.environ.get("INTF_BENCH_C4_PIPES", "4"))  # 2 / 3 / 4: 1.87 / 1.68 / 1.59 ms per trace (profiles/c4_pipes_r1m.txt)
+    if world > 1:
+        return c4_sharded(a, spec, ta, stream, barrier, max_over_ranks, rank, world)
+    n_c4_pipes = int(os.environ.get("INTF_BENCH_C4_PIPES", "4"))  # buffer sets / streams in flight (profiles/c4_pipes_r1m.txt)
     pipes = [engine.ReplayPipeline([spec], ta, scale=1.2) for _ in range(n_c4_pipes)]
     for p in pipes:  # warm-up (also sizes the job scratch); default slow 2.0, min_len 96
         engine.replay_segmented(p, passes=C4_PASSES)
@@ -367,6 +370,39 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
             "workload": "C4: 16 models (6 default + 10 rng(123) archetypes), bs 1-64, cap 4, window U(10,20) ms, "
                         "sigma 0.05, total rho 0.5 at bs 64; one trace per GPU; arrivals + formation + noise + "
                         "busy-period-sharded replay + SLO + features"}
+
+
+def c4_sharded(a, spec, ta, stream, barrier, max_over_ranks, rank, world) -> dict:
+    """C4 at N > 1: the one 10^6-request trace sharded across the ranks
+    (distributed.replay_trace_sharded: replicated arrivals / formation / job
+    plan, each rank replays the jobs starting in its batch range, job results
+    MAX-all_reduced before every verification pass, the owned per-batch
+    outputs SUM-all_reduced at the end, SLO report on every rank).  Strong
+    scaling: the same trace for every N; time = max over ranks."""
+    import torch
+    from paper_2512_18725_b200 import engine
+    from paper_2512_18725_b200.distributed import replay_trace_sharded
+
+    pipe = engine.ReplayPipeline([spec], ta, scale=1.2)
+    for _ in range(2):
+        replay_trace_sharded(pipe, passes=C4_PASSES, backend=a.backend)
+    barrier()
+    reps = 4
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        stats = replay_trace_sharded(pipe, passes=C4_PASSES, backend=a.backend)
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / reps
+    n_req = int(pipe.t["n_req"][0].item())
+    return {"metric": "requests replayed/sec (single long trace)", "value": n_req / (ms / 1e3), "unit": "requests/s",
+            "ms_per_trace": ms, "requests": n_req, "status": int(pipe.t["status"][0].item()), "scaling": "strong",
+            **stats, "cpu_baseline": None,
+            "workload": "C4: ONE trace (16 models, bs 1-64, cap 4, seed 1) sharded over the ranks: replicated "
+                        "arrivals + formation + job plan, jobs replayed by the rank owning their first batch, "
+                        "MAX all_reduce of job results per verify pass, SUM all_reduce of the owned per-batch "
+                        "outputs, SLO report on every rank"}
 
 
 def prep_kernel_ms(scorer, stream) -> float:
@@ -579,7 +615,7 @@ def c1_leg(a, stream, barrier, max_over_ranks, rank, world, W) -> dict:
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_e2e)
     ok = len(res.outcomes) == nb == 1528 and len(res.records) == 3789 and bool(np.isfinite(yhat).all())
     cpu = None
-    if rank == 0 and not a.no_cpu:
+    if rank == 0 and world == 1 and not a.no_cpu:
         import oracle as O
 
         otab = O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr)
@@ -633,7 +669,7 @@ def c3_leg(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     dt = max_over_ranks(time.perf_counter() - t0)
     mean = ex.mean_drift_table(cells)
     cpu = None
-    if rank == 0 and not a.no_cpu:
+    if rank == 0 and world == 1 and not a.no_cpu:
         import oracle as O
 
         ta = table.arrays()
