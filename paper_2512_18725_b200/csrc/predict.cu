@@ -1544,6 +1544,71 @@ constexpr int kScenFitWarps = 4;
 #define INTF_SCEN_FIT_MINB 0  // min resident blocks per SM (register cap); 0 = compiler's choice
 #endif
 
+// rls_init's P0 = np.linalg.inv(G) (`predict.py:126-131`) by the whole warp:
+// Gauss-Jordan with partial pivoting on [G | I], lane r < 7 holding row r in
+// registers (the pivot search is a warp arg-max, first index on ties like
+// LAPACK's idamax; the swap and the pivot-row broadcast are shuffles).  It
+// fails only on an exactly zero pivot -- numpy's LinAlgError: two identical
+// columns (and rows) of a symmetric G stay identical under the row operations
+// until one is the pivot row, which zeroes the other exactly -- and then
+// inverts G + 1e-8 I (`predict.py:131`).  Replaces lane-serial LU with
+// dynamically indexed rows (local memory), ~45% of k_scen_fit's samples.
+__device__ __noinline__ void warp_p0_inverse(const double* G, double* inv) {
+  const int lane = threadIdx.x & 31, r = lane < 7 ? lane : 6;
+  for (int attempt = 0; attempt < 2; attempt++) {
+    double row[14];
+#pragma unroll
+    for (int j = 0; j < 7; j++) row[j] = G[r * 7 + j] + ((attempt && j == r) ? 1e-8 : 0.0);
+#pragma unroll
+    for (int j = 0; j < 7; j++) row[7 + j] = (j == r) ? 1.0 : 0.0;
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < 7; c++) {
+      double col = row[0];
+#pragma unroll
+      for (int j = 1; j < 7; j++) col = j == c ? row[j] : col;
+      // arg max |row[c]| over lanes c..6 (first lane on ties)
+      double best = (lane >= c && lane < 7) ? fabs(col) : -1.0;
+      int piv = lane;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, piv, o);
+        if (ob > best || (ob == best && op < piv)) best = ob, piv = op;
+      }
+      if (best == 0.0) {  // warp-uniform
+        ok = false;
+        break;
+      }
+      const int src = lane == c ? piv : (lane == piv ? c : lane);
+      double p[14];
+#pragma unroll
+      for (int j = 0; j < 14; j++) {
+        row[j] = __shfl_sync(0xffffffffu, row[j], src);
+        p[j] = __shfl_sync(0xffffffffu, row[j], c);
+      }
+      double rc = row[0];
+#pragma unroll
+      for (int j = 1; j < 7; j++) rc = j == c ? row[j] : rc;
+      const double f = rc / p[c];
+      if (lane != c) {
+#pragma unroll
+        for (int j = 0; j < 14; j++) row[j] -= f * p[j];
+      }
+    }
+    if (ok) {
+      double d = row[0];
+#pragma unroll
+      for (int j = 1; j < 7; j++) d = j == r ? row[j] : d;
+      if (lane < 7) {
+#pragma unroll
+        for (int j = 0; j < 7; j++) inv[lane * 7 + j] = row[7 + j] / d;
+      }
+      return;
+    }
+  }
+}
+
 // one scenario design's solve (a call, not inlined: keeps the warp-wide
 // parts of k_scen_fit at a small register footprint)
 __device__ __noinline__ void scen_solve(const double* st, double* p, int32_t* inf2, double* Pinv, const double* qr,
@@ -1635,18 +1700,19 @@ __global__ void __launch_bounds__(32 * kScenFitWarps, INTF_SCEN_FIT_MINB) k_scen
   // fails the condition screen gets its rank from the rows, by the whole warp
   int32_t inf2[2] = {0, 0};
   double p[7];
-  if (lane < 2 && valid) scen_solve(st[wi][lane], p, inf2, lane == 1 ? P0 + 49ll * s : nullptr, nullptr, true);
+  if (lane < 2 && valid) scen_solve(st[wi][lane], p, inf2, nullptr, nullptr, true);
   const unsigned need = __ballot_sync(0xffffffffu, lane < 2 && valid && inf2[0] == -1);
   for (int m = 0; m < 2; m++)
     if (need & (1u << m)) warp_qr_rank(Xm[m], Y, base, cut, qrres[wi][m]);
   __syncwarp();
   if (lane < 2 && valid) {
-    if (need & (1u << lane)) scen_solve(st[wi][lane], p, inf2, lane == 1 ? P0 + 49ll * s : nullptr, qrres[wi][lane], false);
+    if (need & (1u << lane)) scen_solve(st[wi][lane], p, inf2, nullptr, qrres[wi][lane], false);
 #pragma unroll
     for (int i = 0; i < 7; i++) par[wi][lane][i] = p[i];
     bits = (inf2[0] ? (2 << lane) : 0) | (inf2[1] ? 16 : 0);
   }
   bits |= __shfl_sync(0xffffffffu, bits, 1);
+  if (valid) warp_p0_inverse(st[wi][1], P0 + 49ll * s);  // the adaptive tail's P0 from the EWMA design
   __syncwarp();
   if (lane < 21) {  // coarse, fine, adaptive (= fine before its tail) parameters
     const int k = lane / 7, i = lane % 7;
@@ -1706,13 +1772,13 @@ __global__ void __launch_bounds__(32 * kScenFitWarps) k_fit_segments(const doubl
   __syncwarp();
   int32_t inf2[2] = {0, 0};
   double p[7];
-  double* pinv = Pinv ? Pinv + 49ll * g : nullptr;
-  if (lane == 0) scen_solve(st[wi], p, inf2, pinv, nullptr, true);
+  if (lane == 0) scen_solve(st[wi], p, inf2, nullptr, nullptr, true);
   const bool need = __shfl_sync(0xffffffffu, inf2[0], 0) == -1;
   if (need) warp_qr_rank(X, Y, a, cnt, qrres[wi]);
   __syncwarp();
+  if (Pinv) warp_p0_inverse(st[wi], Pinv + 49ll * g);
   if (lane == 0) {
-    if (need) scen_solve(st[wi], p, inf2, pinv, qrres[wi], false);
+    if (need) scen_solve(st[wi], p, inf2, nullptr, qrres[wi], false);
 #pragma unroll
     for (int i = 0; i < 7; i++) params[7ll * g + i] = p[i];
     info[3 * g] = inf2[0];

@@ -2,9 +2,9 @@
 
 `run_scenario` / `run_scenarios` replay on the GPU: per-model batch
 formation, FIFO capped admission, piecewise-constant interference segments
-with bit-exact noise, SLO records (one CUDA thread per scenario; the
-reference's heap is replaced by an exact heap-free recurrence, see
-csrc/replay_core.cuh).  Results are materialised as the reference's objects;
+with bit-exact noise, SLO records (one warp per scenario, or busy-period jobs
+for long traces; the reference's heap is replaced by an exact heap-free
+recurrence, see csrc/replay_core.cuh and csrc/replay_warp.cuh).  Results are materialised as the reference's objects;
 `ScenarioResult.arrays` keeps the flat arrays for batched reuse.
 
 `GpuState` is the reference's interactive step API (`simcore.py:103-208`):
