@@ -961,7 +961,10 @@ def product_arm(a):
         "best_step": {"value": world * n_pred / (best_ms / 1e3), "unit": "predictions/s", "ms_per_step": best_ms,
                       "kernel": "k_cand_step<best> (device-resident, PDL-chained, 24 KB of keys per step)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": kname,
+                     "traffic": traffic, "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                                            "from the committed ncu --set full capture "
+                                                            "(profiles/ncu_summary.json), not this run",
+                     "peak_source": peak_src, "kernel": kname,
                      "kernel_ms": launch_ms, "kernel_ms_isolated": kern_ms,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "step": ("one k_cand_step launch per step: forward of every candidate (stream blocks) + feature "
