@@ -448,7 +448,7 @@ def replay_stage_times(pipe, stream) -> dict:
     return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
 
 
-def c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W) -> dict:
+def c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W, scorer=None) -> dict:
     """C5 (BASELINE configs[4]): a FIXED sweep of 10^4 synthetic scenarios
     (default_rng([2512, i])) split over the ranks by expected requests
     (lambda*T, longest-processing-time first; strong scaling).  One step = the
@@ -492,10 +492,12 @@ def c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W) ->
         loc = rows[q].build()
         gathered[q] = gather_sweep_rows(loc, counts, backend) if dist is not None else [loc]
 
-    step(0)
+    rstreams = [torch.cuda.Stream() for _ in pipes]
+    for k in range(n_pipes):  # warm every pipeline's full step on its own stream (row build + gather allocations)
+        with torch.cuda.stream(rstreams[k]):
+            step(k)
     barrier()
     r_steps = max(n_pipes, a.steps)
-    rstreams = [torch.cuda.Stream() for _ in pipes]
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     r0.record(stream)
     for rs in rstreams:
@@ -523,6 +525,7 @@ def c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W) ->
     t1.record(stream)
     torch.cuda.synchronize()
     tail_ms = t0.elapsed_time(t1)
+    decisions = real_decisions(stream, barrier, max_over_ranks, scorer, pipe, W) if scorer is not None else None
     summary = None
     if rank == 0:  # untimed: the sweep's result, every scenario in index order
         allrows = np.full((REPLAY_SCEN, gathered[0][0].shape[1]), np.nan)
@@ -540,7 +543,45 @@ def c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W) ->
                         "scenario) + SLO + features + per-scenario coarse/fine/adaptive evaluation (75/25 split, "
                         "OLS x2, RLS prequential tail, 3 EvalReports) + per-scenario rows gathered to every rank "
                         f"(N > 1: NCCL all_gather); consecutive sweeps on {n_pipes} pipelines / streams",
-            "steps_timed": r_steps, "stage_ms": stage_ms, "summary": summary}
+            "steps_timed": r_steps, "stage_ms": stage_ms, "summary": summary, "decisions": decisions}
+
+
+def real_decisions(stream, barrier, max_over_ranks, scorer, pipe, W) -> dict:
+    """C2 on REAL scheduling decisions ("the per-decision candidate
+    set from C5 replays"): every dispatch of this rank's share of the sweep is
+    a decision whose running set is a column of the cap-4 enumeration; every
+    own row (48) is scored against it by both predictors and reduced to the
+    best own row, plus the FIFO batch's prediction (intf_dispatch_sets +
+    intf_score_decisions, features prepared once)."""
+    import torch
+
+    coefs = torch.tensor(W[-1], dtype=torch.float64, device="cuda").contiguous()
+    scorer.prepare()
+    rank_t, own_t = scorer.dispatch_decisions(pipe)
+    best, chosen = scorer.score_decisions(coefs, rank_t, own_t)
+    torch.cuda.synchronize()
+    n_dec = int((rank_t >= 0).sum().item())
+    reps = 10
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        rank_t, own_t = scorer.dispatch_decisions(pipe)
+        scorer.score_decisions(coefs, rank_t, own_t, best, chosen)
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / reps
+    bk = best.cpu().numpy().view(np.uint64).reshape(-1, 2)
+    valid = rank_t.cpu().numpy() >= 0
+    hi = (bk[valid, 1] >> np.uint64(32)).astype(np.uint32)
+    best_fine = np.where(hi >> np.uint32(31), hi & np.uint32(0x7FFFFFFF), ~hi).astype(np.uint32).view(np.float32)
+    fifo_fine = chosen.cpu().numpy().reshape(-1, 2)[valid, 1]
+    return {"metric": "real scheduling decisions scored/sec", "decisions": n_dec, "value": n_dec / (ms / 1e3),
+            "unit": "decisions/s", "predictions_per_s": n_dec * 2 * scorer.E / (ms / 1e3), "ms": ms,
+            "mean_fine_prediction": {"fifo_batch": float(fifo_fine.mean()), "best_own_row": float(best_fine.mean())},
+            "workload": "every dispatch of the replayed C5 sweep (this GPU's share): running set -> column of the "
+                        "cap-4 enumeration; 48 own rows x {coarse, fine} scored, best own row + the FIFO batch's "
+                        "prediction per decision (intf_dispatch_sets + intf_score_decisions)"}
 
 
 def sweep_summary(rows: np.ndarray) -> dict:
@@ -900,7 +941,7 @@ def product_arm(a):
     best_ms = max_over_ranks(b0.elapsed_time(b1)) / a.steps
 
     # ---- secondary: scenario replay sweep (C5: 10^4 scenarios, coarse / fine / adaptive)
-    sweep = c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W)
+    sweep = c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W, scorer)
 
     refit = refit_secondary(a, stream, barrier, max_over_ranks, rank)
     bundled = c1_leg(a, stream, barrier, max_over_ranks, rank, world, W)

@@ -291,6 +291,22 @@ int intf_best_candidates_host(const intf_table *table, int32_t cap, double alpha
                               int32_t n_dec, uint64_t *h_best, float *d_scratch, int64_t scratch_elems,
                               void *stream);
 
+/* Real scheduling decisions of a replayed batch: for every
+ * batch slot (req_off + b), dec_rank = the multiset rank (enumeration of
+ * cap_enum over n_rows profile rows) of the batches it co-runs with right
+ * after its dispatch -- dispatched before it (FIFO) and completing strictly
+ * after its start -- and dec_own = its own profile row; slots without a
+ * batch get dec_rank -1.  intf_score_decisions scores every own row against
+ * each decision's running set from a prepared candidate workspace
+ * (intf_candidate_prepare, same cap) with one coarse / fine model
+ * coefs[2][7]: best[i][2] = (orderable fp32 value << 32 | best own row),
+ * chosen[i][2] = the prediction for the batch FIFO dispatched.  n_rows <= 64. */
+int intf_dispatch_sets(const intf_batch *batch, const intf_replay_buffers *buf, int32_t n_rows, int32_t cap_enum,
+                       int32_t *dec_rank, int32_t *dec_own, void *stream);
+int intf_score_decisions(const intf_table *table, int32_t cap, const double *coefs, const float *ws, int64_t ws_elems,
+                         const int32_t *dec_rank, const int32_t *dec_own, int64_t n, uint64_t *best, float *chosen,
+                         void *stream);
+
 /* Host-buffer variant (the end-to-end call): copies coefs in and all
  * predictions out (tiled layout above).  h_out: ceil(n_dec/4)*4*2*n_rows*ld
  * floats; d_scratch: device floats = 28*n_dec + that output size (+ the

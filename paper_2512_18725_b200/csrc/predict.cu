@@ -553,6 +553,100 @@ __global__ void __launch_bounds__(kStreamThreads, 8) k_cand_step(
   cand_stream_body<kBest>(bx, rest % E, rest / E, thr, E, ld, n_sets, coefs, n_dec, ws_cur, ws_cur + 3 * ld, out, best);
 }
 
+// ---- real scheduling decisions ("the per-decision candidate
+// set from C5 replays").  Decision = the dispatch of batch b of a replayed
+// scenario; its running set = the batches it co-runs with right after the
+// dispatch (dispatched before b -- FIFO, batch-id order -- and completing
+// strictly after b's start: a batch completing at that very instant leaves
+// within the same timestamp, `simcore.py:56-64`).  The set is written as its
+// multiset rank in the candidate enumeration of cap_enum (size-major, colex),
+// so the candidates of a decision are column r of the enumeration: every own
+// row against that running set.  Thread per batch, block per scenario.
+__global__ void k_dispatch_sets(const intf_scenario* __restrict__ scen, int n_scen,
+                                const intf_model* __restrict__ models, intf_replay_buffers B, int E, int cap_enum,
+                                int32_t* __restrict__ dec_rank, int32_t* __restrict__ dec_own) {
+  for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
+    const intf_scenario& S = scen[s];
+    const long long ro = S.req_off;
+    const int nb = B.n_batches[s];
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      const double tb = B.b_start[ro + b];
+      const int nrun = B.b_running ? B.b_running[ro + b] : cap_enum;
+      int peers[kMaxPeers];
+      int k = 0;
+      // the dispatch trace bounds the scan: nrun - 1 batches were running at the dispatch
+      for (int c = b - 1; c >= 0 && k < nrun - 1 && k < cap_enum - 1; c--)
+        if (B.b_completion[ro + c] > tb)
+          peers[k++] = models[S.model_off + B.b_model[ro + c]].entry_base + B.b_size[ro + c] - 1;
+      for (int i = 1; i < k; i++)  // ascending entries
+        for (int j = i; j > 0 && peers[j - 1] > peers[j]; j--) {
+          const int t = peers[j];
+          peers[j] = peers[j - 1];
+          peers[j - 1] = t;
+        }
+      long long r = 0;
+      for (int j = 0; j < k; j++) r += binom(E + j - 1, j);
+      for (int i = 0; i < k; i++) r += binom(peers[i] + i, i + 1);
+      dec_rank[ro + b] = (int32_t)r;
+      dec_own[ro + b] = models[S.model_off + B.b_model[ro + b]].entry_base + B.b_size[ro + b] - 1;
+    }
+  }
+}
+
+// warp per decision: every own row scored against the decision's running set
+// (column r of the enumeration's features, the same fp32 arithmetic as
+// cand_stream_body, so a prediction equals the enumeration's), then the best
+// own row per predictor kind -- (orderable value << 32 | own) -- and the
+// prediction for the batch FIFO actually dispatched.  n decisions at
+// dec_rank[i] (< 0: none).
+__global__ void __launch_bounds__(128) k_score_decisions(const double* __restrict__ thr, int E, long long ld,
+                                                         const double* __restrict__ coefs,
+                                                         const float* __restrict__ C0,
+                                                         const float* __restrict__ FE,
+                                                         const int32_t* __restrict__ dec_rank,
+                                                         const int32_t* __restrict__ dec_own, long long n,
+                                                         unsigned long long* __restrict__ best,
+                                                         float* __restrict__ chosen) {
+  __shared__ float4 cw[2][64];  // per own row: coarse / fine (w3, w4, w5, bias)
+  for (int t = threadIdx.x; t < 2 * E; t += blockDim.x) {
+    const int kind = t / E, o = t % E;
+    const double* w = coefs + kind * 7;
+    const double* x = thr + 3 * o;
+    const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
+    cw[kind][o] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
+  }
+  __syncthreads();
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int r = dec_rank[i];
+  if (r < 0) {
+    if (lane < 2) best[2 * i + lane] = ~0ull;
+    return;
+  }
+  const int own_b = dec_own[i];
+  const float cx = C0[r], cy = C0[ld + r], cz = C0[2 * ld + r];
+  unsigned vc = 0xffffffffu, vf = 0xffffffffu, oc = 0xffffffffu, of = 0xffffffffu;
+  for (int o = lane; o < E; o += 32) {
+    const float4 a = cw[0][o], b = cw[1][o];
+    const float fx = FE[((long long)o * 3 + 0) * ld + r], fy = FE[((long long)o * 3 + 1) * ld + r],
+                fz = FE[((long long)o * 3 + 2) * ld + r];
+    const float yc = fmaf(a.z, cz, fmaf(a.y, cy, fmaf(a.x, cx, a.w)));
+    const float yf = fmaf(b.z, fz, fmaf(b.y, fy, fmaf(b.x, fx, b.w)));
+    const unsigned kc = f32_key(yc), kf = f32_key(yf);
+    if (kc < vc) vc = kc, oc = (unsigned)o;  // ascending own: strict < keeps the lowest on ties
+    if (kf < vf) vf = kf, of = (unsigned)o;
+    if (o == own_b) chosen[2 * i] = yc, chosen[2 * i + 1] = yf;
+  }
+  const unsigned wc = __reduce_min_sync(0xffffffffu, vc), wf = __reduce_min_sync(0xffffffffu, vf);
+  const unsigned xc = __reduce_min_sync(0xffffffffu, vc == wc ? oc : 0xffffffffu);
+  const unsigned xf = __reduce_min_sync(0xffffffffu, vf == wf ? of : 0xffffffffu);
+  if (lane == 0) {
+    best[2 * i] = ((unsigned long long)wc << 32) | xc;
+    best[2 * i + 1] = ((unsigned long long)wf << 32) | xf;
+  }
+}
+
 // ===================================================================== K6
 constexpr int kOlsThreads = 256;
 constexpr int kOlsBlocks = 296;  // one wave: 2 x 148 SMs at 128 registers x 256 threads
@@ -2219,6 +2313,34 @@ int intf_best_candidates_host(const intf_table* table, int32_t cap, double alpha
   if (cudaMemcpyAsync(h_best, d_best, sizeof(unsigned long long) * n_best, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return launch_status("copy best candidates");
   return INTF_OK;
+}
+
+int intf_dispatch_sets(const intf_batch* bt, const intf_replay_buffers* buf, int32_t n_rows, int32_t cap_enum,
+                       int32_t* dec_rank, int32_t* dec_own, void* stream) {
+  if (!bt || !bt->scen || !bt->models || !buf || !buf->b_start || !buf->b_completion || !dec_rank || !dec_own ||
+      cap_enum < 1 || cap_enum > kMaxPeers + 1 || buf->cap_max > cap_enum || n_rows < 1)
+    return bad_input("intf_dispatch_sets: bad argument (the enumeration cap must cover every scenario's cap)");
+  if (bt->n_scen <= 0) return INTF_OK;
+  cudaMemsetAsync(dec_rank, 0xff, sizeof(int32_t) * (size_t)bt->req_slots, as_stream(stream));  // -1: no decision
+  const int grid = bt->n_scen < 65535 ? bt->n_scen : 65535;
+  k_dispatch_sets<<<grid, 128, 0, as_stream(stream)>>>(bt->scen, bt->n_scen, bt->models, *buf, n_rows, cap_enum,
+                                                       dec_rank, dec_own);
+  return launch_status("k_dispatch_sets");
+}
+
+int intf_score_decisions(const intf_table* table, int32_t cap, const double* coefs, const float* ws, int64_t ws_elems,
+                         const int32_t* dec_rank, const int32_t* dec_own, int64_t n, uint64_t* best, float* chosen,
+                         void* stream) {
+  int64_t need = 0;
+  if (!table || !coefs || !ws || !dec_rank || !dec_own || !best || !chosen || n < 0 || table->n_rows > 64 ||
+      intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need)
+    return bad_input("intf_score_decisions: bad argument, workspace too small or more than 64 profile rows");
+  if (n == 0) return INTF_OK;
+  const long long ld = cand_ld(n_multisets(table->n_rows, cap));
+  k_score_decisions<<<(unsigned)ceil_div(n * 32, 128), 128, 0, as_stream(stream)>>>(
+      table->thr, table->n_rows, ld, coefs, ws, ws + 3 * ld, dec_rank, dec_own, (long long)n,
+      (unsigned long long*)best, chosen);
+  return launch_status("k_score_decisions");
 }
 
 int intf_ols_stats(const double* X, const double* y, int64_t n, double* out, double* ws, void* stream) {

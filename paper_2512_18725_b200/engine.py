@@ -645,6 +645,33 @@ class CandidateScorer:
         bits = np.where(hi >> np.uint32(31), hi & np.uint32(0x7FFFFFFF), ~hi).astype(np.uint32)
         return bits.view(np.float32), (k & np.uint64(0xFFFFFFFF)).astype(np.int64)
 
+    # ---- real decisions: the running set at every dispatch of a replayed batch
+    def dispatch_decisions(self, pipe: "ReplayPipeline"):
+        """(dec_rank, dec_own) per batch slot of a replayed pipeline
+        (intf_dispatch_sets): the running set at each dispatch as a column of
+        this scorer's enumeration, and the dispatched batch's own row."""
+        n = int(pipe.batch.req_slots)
+        rank = torch.empty(n, dtype=torch.int32, device=self.dev)
+        own = torch.empty(n, dtype=torch.int32, device=self.dev)
+        _abi.check(_abi.load().intf_dispatch_sets(ctypes.byref(pipe.batch), ctypes.byref(pipe.B), self.E, self.cap,
+                                                  rank.data_ptr(), own.data_ptr(), stream_ptr()),
+                   "intf_dispatch_sets")
+        return rank, own
+
+    def score_decisions(self, coefs: torch.Tensor, rank: torch.Tensor, own: torch.Tensor, best=None, chosen=None):
+        """Every own row against each decision's running set under one coarse /
+        fine model coefs[2][7] (device f64; features from prepare()):
+        best keys [n][2] (int64 view of u64) and the FIFO batch's predictions
+        [n][2]; enqueue only."""
+        n = rank.numel()
+        best = best if best is not None else torch.empty(2 * n, dtype=torch.int64, device=self.dev)
+        chosen = chosen if chosen is not None else torch.empty(2 * n, dtype=torch.float32, device=self.dev)
+        _abi.check(_abi.load().intf_score_decisions(ctypes.byref(self.dtable.struct), self.cap, coefs.data_ptr(),
+                                                    self.ws.data_ptr(), self.ws_elems, rank.data_ptr(), own.data_ptr(),
+                                                    n, best.data_ptr(), chosen.data_ptr(), stream_ptr()),
+                   "intf_score_decisions")
+        return best, chosen
+
     def pipeline_join(self) -> None:
         """Make the current stream wait for the side stream's last feature build."""
         if not self._fused:

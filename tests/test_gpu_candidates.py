@@ -148,3 +148,56 @@ def test_best_candidate_step_equals_argmin_of_full_output():
     rmin = ref.min(axis=-1)
     np.testing.assert_allclose(val, rmin, rtol=RTOL, atol=0)
     np.testing.assert_allclose(np.take_along_axis(ref, rank[..., None], -1)[..., 0], rmin, rtol=2 * RTOL, atol=0)
+
+
+def test_real_decisions_from_replayed_sweep():
+    """The candidate set of every real decision of a replayed C5 sweep (the
+    running set at each dispatch, `simcore.py:150-171`) against the heap-engine
+    oracle's replay: the same running multiset for every batch; every own row
+    scored against it equals the enumeration's prediction for that column
+    (materialised by the C2 kernel), the best own row is its argmin, and the
+    FIFO batch's prediction is its own entry."""
+    from paper_2512_18725_b200 import engine
+    from paper_2512_18725_b200.profiles import gen_synthetic_profiles
+    from paper_2512_18725_b200.sweep import c2_decision_coefs, c5_scenarios
+
+    table = gen_synthetic_profiles()
+    ta = table.arrays()
+    specs = c5_scenarios(table, 64, start=300)
+    pipe = engine.ReplayPipeline(specs, ta, scale=1.5)
+    pipe.run()
+    sc = engine.CandidateScorer(ta, cap=4, alpha=0.5)
+    sc.prepare()
+    W = c2_decision_coefs(32, 0.5)[-1]
+    coefs = torch.tensor(W, dtype=torch.float64, device="cuda").contiguous()
+    rank, own = sc.dispatch_decisions(pipe)
+    best, chosen = sc.score_decisions(coefs, rank, own)
+    out = sc.alloc(1)
+    sc.score(coefs.reshape(1, 2, 7).contiguous(), out)
+    y = sc.view(out.cpu().numpy(), 1)[0]  # [2][E][n_sets]
+    h = pipe.fetch()
+    rank, own = rank.cpu().numpy(), own.cpu().numpy()
+    bk = best.cpu().numpy().view(np.uint64).reshape(-1, 2)
+    ch = chosen.cpu().numpy().reshape(-1, 2)
+    otab = O.TableArrays(ta.models, ta.max_bs, ta.solo, ta.thr)
+    n_dec = 0
+    for s, spec in enumerate(specs):
+        v = pipe.scenario(h, s)
+        ref = O.run_scenario(spec, otab)
+        ro = pipe.pb.scen[s].req_off
+        ids = [d["model_id"] for d in spec["deployed"]]
+        rows = [ta.row(ids[m], int(z)) for m, z in zip(ref["b_model"], ref["b_size"])]
+        for b in range(len(rows)):
+            peers = [rows[c] for c in range(b) if ref["b_completion"][c] > ref["b_start"][b]]
+            r = engine.multiset_rank(peers, sc.E, 4)
+            assert rank[ro + b] == r and own[ro + b] == rows[b], (s, b)
+            for k in range(2):
+                col = y[k, :, r]
+                key = int(bk[ro + b, k])
+                hi = np.uint32(key >> 32)
+                val = np.array([hi & np.uint32(0x7FFFFFFF) if hi >> np.uint32(31) else ~hi], dtype=np.uint32)
+                assert val.view(np.float32)[0] == col.min() and (key & 0xFFFFFFFF) == int(col.argmin())
+                assert ch[ro + b, k] == col[rows[b]]
+            n_dec += 1
+        assert np.all(rank[ro + len(rows): ro + pipe.pb.scen[s].req_cap] == -1)
+    assert n_dec > 10000
