@@ -556,7 +556,7 @@ def real_decisions(stream, barrier, max_over_ranks, scorer, pipe, W) -> dict:
     import torch
 
     coefs = torch.tensor(W[-1], dtype=torch.float64, device="cuda").contiguous()
-    scorer.prepare()
+    scorer.prepare_decisions()
     rank_t, own_t = scorer.dispatch_decisions(pipe)
     best, chosen = scorer.score_decisions(coefs, rank_t, own_t)
     torch.cuda.synchronize()

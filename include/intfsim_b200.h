@@ -306,6 +306,16 @@ int intf_dispatch_sets(const intf_batch *batch, const intf_replay_buffers *buf, 
 int intf_score_decisions(const intf_table *table, int32_t cap, const double *coefs, const float *ws, int64_t ws_elems,
                          const int32_t *dec_rank, const int32_t *dec_own, int64_t n, uint64_t *best, float *chosen,
                          void *stream);
+/* The same with the EWMA candidate features in decision-major order
+ * ft[r][own][3] (intf_decision_features: one transpose of a prepared
+ * workspace, intf_decision_features_elems floats): a decision's 48 x 3
+ * features are contiguous.                                                 */
+int64_t intf_decision_features_elems(int32_t n_rows, int32_t cap);
+int intf_decision_features(const intf_table *table, int32_t cap, const float *ws, int64_t ws_elems, float *ft,
+                           void *stream);
+int intf_score_decisions_ft(const intf_table *table, int32_t cap, const double *coefs, const float *ws,
+                            int64_t ws_elems, const float *ft, const int32_t *dec_rank, const int32_t *dec_own,
+                            int64_t n, uint64_t *best, float *chosen, void *stream);
 
 /* Host-buffer variant (the end-to-end call): copies coefs in and all
  * predictions out (tiled layout above).  h_out: ceil(n_dec/4)*4*2*n_rows*ld

@@ -107,6 +107,9 @@ SIGNATURES = {
     "intf_best_candidates_host": (c_int32, [P, c_int32, c_double, P, c_int32, P, P, c_int64, P]),
     "intf_dispatch_sets": (c_int32, [P, P, c_int32, c_int32, P, P, P]),
     "intf_score_decisions": (c_int32, [P, c_int32, P, P, c_int64, P, P, c_int64, P, P, P]),
+    "intf_decision_features_elems": (c_int64, [c_int32, c_int32]),
+    "intf_decision_features": (c_int32, [P, c_int32, P, c_int64, P, P]),
+    "intf_score_decisions_ft": (c_int32, [P, c_int32, P, P, c_int64, P, P, P, c_int64, P, P, P]),
     "intf_csv_rows": (c_int32, [c_int64, c_int32, P, P, P, P, P, c_int64, P]),
     "intf_repr_f64": (c_int32, [c_double, P, c_int32]),
     "intf_ols_stats": (c_int32, [P, P, c_int64, P, P, P]),

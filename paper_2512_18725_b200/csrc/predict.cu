@@ -606,7 +606,8 @@ __global__ void __launch_bounds__(128) k_score_decisions(const double* __restric
                                                          const int32_t* __restrict__ dec_rank,
                                                          const int32_t* __restrict__ dec_own, long long n,
                                                          unsigned long long* __restrict__ best,
-                                                         float* __restrict__ chosen) {
+                                                         float* __restrict__ chosen,
+                                                         const float* __restrict__ FT = nullptr) {
   __shared__ float4 cw[2][64];  // per own row: coarse / fine (w3, w4, w5, bias)
   for (int t = threadIdx.x; t < 2 * E; t += blockDim.x) {
     const int kind = t / E, o = t % E;
@@ -616,21 +617,38 @@ __global__ void __launch_bounds__(128) k_score_decisions(const double* __restric
     cw[kind][o] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
   }
   __syncthreads();
-  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (i >= n) return;
-  const int r = dec_rank[i];
-  if (r < 0) {
-    if (lane < 2) best[2 * i + lane] = ~0ull;
-    return;
+  const long long n_warps = (long long)gridDim.x * (blockDim.x >> 5);
+  // warps stride over 32-slot groups (the block's coefficient table is built
+  // once): the group's ranks load coalesced, empty slots (no batch) are
+  // marked in one store each, and the warp scores the group's decisions one
+  // after the other
+  for (long long base = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n;
+       base += n_warps * 32) {
+  const long long slot = base + lane;
+  const int my_r = slot < n ? dec_rank[slot] : -1;
+  const int my_own = slot < n ? dec_own[slot] : 0;
+  if (slot < n && my_r < 0) {
+    best[2 * slot] = best[2 * slot + 1] = ~0ull;
+    chosen[2 * slot] = chosen[2 * slot + 1] = NAN;
   }
-  const int own_b = dec_own[i];
+  for (unsigned todo = __ballot_sync(0xffffffffu, my_r >= 0); todo; todo &= todo - 1) {
+  const int j = __ffs(todo) - 1;
+  const long long i = base + j;
+  const int r = __shfl_sync(0xffffffffu, my_r, j);
+  const int own_b = __shfl_sync(0xffffffffu, my_own, j);
   const float cx = C0[r], cy = C0[ld + r], cz = C0[2 * ld + r];
   unsigned vc = 0xffffffffu, vf = 0xffffffffu, oc = 0xffffffffu, of = 0xffffffffu;
   for (int o = lane; o < E; o += 32) {
     const float4 a = cw[0][o], b = cw[1][o];
-    const float fx = FE[((long long)o * 3 + 0) * ld + r], fy = FE[((long long)o * 3 + 1) * ld + r],
-                fz = FE[((long long)o * 3 + 2) * ld + r];
+    float fx, fy, fz;
+    if (FT) {  // decision-major copy: the 48 x 3 features of column r are contiguous
+      const float* f = FT + ((long long)r * E + o) * 3;
+      fx = f[0], fy = f[1], fz = f[2];
+    } else {
+      fx = FE[((long long)o * 3 + 0) * ld + r], fy = FE[((long long)o * 3 + 1) * ld + r],
+      fz = FE[((long long)o * 3 + 2) * ld + r];
+    }
     const float yc = fmaf(a.z, cz, fmaf(a.y, cy, fmaf(a.x, cx, a.w)));
     const float yf = fmaf(b.z, fz, fmaf(b.y, fy, fmaf(b.x, fx, b.w)));
     const unsigned kc = f32_key(yc), kf = f32_key(yf);
@@ -638,13 +656,41 @@ __global__ void __launch_bounds__(128) k_score_decisions(const double* __restric
     if (kf < vf) vf = kf, of = (unsigned)o;
     if (o == own_b) chosen[2 * i] = yc, chosen[2 * i + 1] = yf;
   }
+#ifdef INTF_DECISION_REDUX
   const unsigned wc = __reduce_min_sync(0xffffffffu, vc), wf = __reduce_min_sync(0xffffffffu, vf);
   const unsigned xc = __reduce_min_sync(0xffffffffu, vc == wc ? oc : 0xffffffffu);
   const unsigned xf = __reduce_min_sync(0xffffffffu, vf == wf ? of : 0xffffffffu);
-  if (lane == 0) {
-    best[2 * i] = ((unsigned long long)wc << 32) | xc;
-    best[2 * i + 1] = ((unsigned long long)wf << 32) | xf;
+  const unsigned long long kc = ((unsigned long long)wc << 32) | xc, kf = ((unsigned long long)wf << 32) | xf;
+#else
+  // packed (value << 32 | own) keys: one 64-bit butterfly min per kind gives value and lowest own at once
+  unsigned long long kc = ((unsigned long long)vc << 32) | oc, kf = ((unsigned long long)vf << 32) | of;
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) {
+    const unsigned long long pc = __shfl_xor_sync(0xffffffffu, kc, o2), pf = __shfl_xor_sync(0xffffffffu, kf, o2);
+    kc = pc < kc ? pc : kc;
+    kf = pf < kf ? pf : kf;
   }
+#endif
+  if (lane == 0) {
+    best[2 * i] = kc;
+    best[2 * i + 1] = kf;
+  }
+  }
+  }
+}
+
+// FT[r][own][3] = FE[own][a][r]: the EWMA candidate features in
+// decision-major order (one transpose per table / cap / alpha) so a decision
+// reads its column's 48 x 3 features contiguously instead of 144 rows apart
+__global__ void k_decision_transpose(const float* __restrict__ FE, int E, long long ld, long long n_sets,
+                                     float* __restrict__ FT) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (r, own, a) in output order
+  if (i >= n_sets * E * 3) return;
+  const int a = (int)(i % 3);
+  const long long t = i / 3;
+  const int o = (int)(t % E);
+  const long long r = t / E;
+  FT[i] = FE[((long long)o * 3 + a) * ld + r];
 }
 
 // ===================================================================== K6
@@ -2328,18 +2374,45 @@ int intf_dispatch_sets(const intf_batch* bt, const intf_replay_buffers* buf, int
   return launch_status("k_dispatch_sets");
 }
 
+int64_t intf_decision_features_elems(int32_t n_rows, int32_t cap) {
+  return n_multisets(n_rows, cap) * 3ll * n_rows;
+}
+
+int intf_decision_features(const intf_table* table, int32_t cap, const float* ws, int64_t ws_elems, float* ft,
+                           void* stream) {
+  int64_t need = 0;
+  if (!table || !ws || !ft || intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need)
+    return bad_input("intf_decision_features: bad argument or workspace too small");
+  const long long sets = n_multisets(table->n_rows, cap), ld = cand_ld(sets);
+  const long long total = sets * 3ll * table->n_rows;
+  k_decision_transpose<<<(unsigned)ceil_div(total, 256), 256, 0, as_stream(stream)>>>(ws + 3 * ld, table->n_rows, ld,
+                                                                                    sets, ft);
+  return launch_status("k_decision_transpose");
+}
+
+int intf_score_decisions_ft(const intf_table* table, int32_t cap, const double* coefs, const float* ws,
+                            int64_t ws_elems, const float* ft, const int32_t* dec_rank, const int32_t* dec_own,
+                            int64_t n, uint64_t* best, float* chosen, void* stream);
+
 int intf_score_decisions(const intf_table* table, int32_t cap, const double* coefs, const float* ws, int64_t ws_elems,
                          const int32_t* dec_rank, const int32_t* dec_own, int64_t n, uint64_t* best, float* chosen,
                          void* stream) {
+  return intf_score_decisions_ft(table, cap, coefs, ws, ws_elems, nullptr, dec_rank, dec_own, n, best, chosen, stream);
+}
+
+int intf_score_decisions_ft(const intf_table* table, int32_t cap, const double* coefs, const float* ws,
+                            int64_t ws_elems, const float* ft, const int32_t* dec_rank, const int32_t* dec_own,
+                            int64_t n, uint64_t* best, float* chosen, void* stream) {
   int64_t need = 0;
   if (!table || !coefs || !ws || !dec_rank || !dec_own || !best || !chosen || n < 0 || table->n_rows > 64 ||
       intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need)
     return bad_input("intf_score_decisions: bad argument, workspace too small or more than 64 profile rows");
   if (n == 0) return INTF_OK;
   const long long ld = cand_ld(n_multisets(table->n_rows, cap));
-  k_score_decisions<<<(unsigned)ceil_div(n * 32, 128), 128, 0, as_stream(stream)>>>(
+  const long long want = ceil_div(n, 128);  // a warp per 32-slot group
+  k_score_decisions<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 128, 0, as_stream(stream)>>>(
       table->thr, table->n_rows, ld, coefs, ws, ws + 3 * ld, dec_rank, dec_own, (long long)n,
-      (unsigned long long*)best, chosen);
+      (unsigned long long*)best, chosen, ft);
   return launch_status("k_score_decisions");
 }
 

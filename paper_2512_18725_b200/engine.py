@@ -666,11 +666,23 @@ class CandidateScorer:
         n = rank.numel()
         best = best if best is not None else torch.empty(2 * n, dtype=torch.int64, device=self.dev)
         chosen = chosen if chosen is not None else torch.empty(2 * n, dtype=torch.float32, device=self.dev)
-        _abi.check(_abi.load().intf_score_decisions(ctypes.byref(self.dtable.struct), self.cap, coefs.data_ptr(),
-                                                    self.ws.data_ptr(), self.ws_elems, rank.data_ptr(), own.data_ptr(),
-                                                    n, best.data_ptr(), chosen.data_ptr(), stream_ptr()),
-                   "intf_score_decisions")
+        ft = getattr(self, "_ft", None)
+        _abi.check(_abi.load().intf_score_decisions_ft(ctypes.byref(self.dtable.struct), self.cap, coefs.data_ptr(),
+                                                       self.ws.data_ptr(), self.ws_elems, _abi.addr(ft),
+                                                       rank.data_ptr(), own.data_ptr(), n, best.data_ptr(),
+                                                       chosen.data_ptr(), stream_ptr()), "intf_score_decisions_ft")
         return best, chosen
+
+    def prepare_decisions(self) -> None:
+        """prepare() + the decision-major copy of the EWMA features
+        (intf_decision_features) used by score_decisions."""
+        L = _abi.load()
+        self.prepare()
+        n = int(L.intf_decision_features_elems(self.E, self.cap))
+        if getattr(self, "_ft", None) is None or self._ft.numel() != n:
+            self._ft = torch.empty(n, dtype=torch.float32, device=self.dev)
+        _abi.check(L.intf_decision_features(ctypes.byref(self.dtable.struct), self.cap, self.ws.data_ptr(),
+                                            self.ws_elems, self._ft.data_ptr(), stream_ptr()), "intf_decision_features")
 
     def pipeline_join(self) -> None:
         """Make the current stream wait for the side stream's last feature build."""

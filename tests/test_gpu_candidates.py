@@ -171,7 +171,12 @@ def test_real_decisions_from_replayed_sweep():
     W = c2_decision_coefs(32, 0.5)[-1]
     coefs = torch.tensor(W, dtype=torch.float64, device="cuda").contiguous()
     rank, own = sc.dispatch_decisions(pipe)
-    best, chosen = sc.score_decisions(coefs, rank, own)
+    best0, chosen0 = sc.score_decisions(coefs, rank, own)  # features read in the enumeration's layout
+    sc.prepare_decisions()
+    best, chosen = sc.score_decisions(coefs, rank, own)  # decision-major copy
+    live = (rank >= 0).repeat_interleave(2)
+    assert torch.equal(best, best0) and torch.equal(chosen[live], chosen0[live])
+    assert torch.isnan(chosen[~live]).all()
     out = sc.alloc(1)
     sc.score(coefs.reshape(1, 2, 7).contiguous(), out)
     y = sc.view(out.cpu().numpy(), 1)[0]  # [2][E][n_sets]
