@@ -679,14 +679,76 @@ __device__ __forceinline__ void form_model_win(const LaneGroup<W>& G, const intf
   if (lane == 0) B.n_mb[g] = c;
 }
 
+// The same batches with the per-head work taken off the chain: the warp loads
+// the 64 arrivals from the current head h, and lane l computes the batch that
+// WOULD start at head h + l -- its member count (1 + #(t[h+l+j] < t[h+l] +
+// window), 0 < j < max_bs, a prefix of the sorted list), its event time, kind
+// and key -- for all 32 candidate heads at once (max_bs - 1 shuffles).  The
+// serial chain h -> h + cnt(h) then costs one shuffle per batch; the lanes
+// on the chain are the batches, which write their events directly to their
+// output slots (consecutive lanes -> consecutive slots).  Every iteration
+// advances at least 32 arrivals.  Same recurrence as form_model_win.
+__device__ __forceinline__ void form_model_heads(const intf_scenario& S, const intf_model& Md, int n_list,
+                                                 const intf_replay_buffers& B, int g) {
+  const double* lt = B.list_t + Md.list_off;
+  const int32_t* lrid = B.list_rid + Md.list_off;
+  const int lane = threadIdx.x & 31;
+  const int mbs = S.max_bs;
+  int h = 0, c = 0;
+  while (h < n_list) {
+    const double w0 = h + lane < n_list ? lt[h + lane] : INFINITY;
+    const double w1 = h + 32 + lane < n_list ? lt[h + 32 + lane] : INFINITY;
+    const int r0 = h + lane < n_list ? lrid[h + lane] : 0;
+    const int r1 = h + 32 + lane < n_list ? lrid[h + 32 + lane] : 0;
+    // the batch starting at head h + lane
+    const double D = w0 + S.window_ms;  // arm_window at the first arrival (`batcher.py:66-68`)
+    int cnt = 1;
+    bool open = true;
+    for (int j = 1; j < 32; j++) {
+      if (j >= mbs) break;
+      const int src = lane + j;  // window element lane + j: w0 of lane src, or w1 of lane src - 32
+      const double a = __shfl_sync(0xffffffffu, w0, src & 31), b = __shfl_sync(0xffffffffu, w1, src & 31);
+      const double v = src < 32 ? a : b;
+      open = open && v < D;
+      cnt += open ? 1 : 0;
+    }
+    const int last = lane + cnt - 1;  // < 64
+    const double ta = __shfl_sync(0xffffffffu, w0, last & 31), tb = __shfl_sync(0xffffffffu, w1, last & 31);
+    const int ra = __shfl_sync(0xffffffffu, r0, last & 31), rb = __shfl_sync(0xffffffffu, r1, last & 31);
+    const bool full = cnt == mbs;  // early emit at max_batch_size (`batcher.py:70-71`), else window expiry
+    const double et = full ? (last < 32 ? ta : tb) : D;
+    const int ekind = full ? KIND_ARRIVAL : KIND_WINDOW;
+    const int ekey = full ? (last < 32 ? ra : rb) : (int32_t)Md.crc;
+    // walk the chain from offset 0 while the head lies in this window
+    unsigned heads = 0u;
+    int o = 0;
+    while (o < 32 && h + o < n_list) {
+      heads |= 1u << o;
+      o += __shfl_sync(0xffffffffu, cnt, o);
+    }
+    if ((heads >> lane) & 1u) {
+      const int idx = c + __popc(heads & ((1u << lane) - 1u));
+      B.mb_t[Md.list_off + idx] = et;
+      reinterpret_cast<int4*>(B.mb_info)[Md.list_off + idx] = make_int4(ekind, ekey, cnt, h + lane);
+    }
+    c += __popc(heads);
+    h += o;
+  }
+  if (lane == 0) B.n_mb[g] = c;
+}
+
 // Per-model formation by a warp (max_batch_size > 32: the original walk with
-// global loads; <= 32: the windowed form).  A rank-merge then orders all
+// global loads; <= 32: the head-parallel form).  A rank-merge then orders all
 // batches of a scenario exactly as the reference heap pops formation events.
 __device__ __forceinline__ void form_model_warp(const intf_scenario& S, const intf_model& Md, int n_list,
                                                 const intf_replay_buffers& B, int g) {
   const LaneGroup<32> G;
   if (S.max_bs <= 32) {
+#ifdef INTF_FORM_WIN
     form_model_win<32>(G, S, Md, n_list, B, g);
+#else
+    form_model_heads(S, Md, n_list, B, g);
+#endif
     return;
   }
   const double* lt = B.list_t + Md.list_off;
