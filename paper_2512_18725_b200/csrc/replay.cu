@@ -1398,7 +1398,7 @@ __global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen
 constexpr int kSloThreads = 256;
 constexpr int kSloGroup = 4;          // models per radix pass group (smem: 12 KB of histograms)
 constexpr int kSloBigReq = 1 << 16;  // above this request capacity: grid-wide SLO passes
-constexpr int kSloCache = 2048;      // records whose latency keys k_slo keeps in shared memory (18 KB)
+constexpr int kSloCache = 2048;      // records whose latency keys k_slo keeps in shared memory (26 KB with indices)
 
 __device__ __forceinline__ unsigned long long lat_key(double v) {
   unsigned long long u = (unsigned long long)__double_as_longlong(v);
@@ -1469,6 +1469,17 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
   // re-read shared memory instead of four global arrays
   extern __shared__ unsigned long long kcache[];
   unsigned char* mcache = reinterpret_cast<unsigned char*>(kcache + kSloCache);
+  // cached path: the records still matching one of the group's quantile
+  // prefixes, compacted after every radix pass (double-buffered index lists),
+  // so the later passes touch a few percent of the records instead of all
+  unsigned short* cand[2] = {reinterpret_cast<unsigned short*>(mcache + kSloCache),
+                             reinterpret_cast<unsigned short*>(mcache + kSloCache) + kSloCache};
+  __shared__ int n_cand[2];
+  // a (model, quantile) whose selected digit holds ONE record is resolved: that
+  // record's key is the answer; when all are, the remaining passes are skipped
+  __shared__ int unresolved;
+  __shared__ unsigned char resolved[kSloGroup][3];
+  __shared__ unsigned long long found[kSloGroup][3];
   const bool cached = n <= kSloCache;
   if (cached) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1489,11 +1500,32 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
       rank_left[mm][q] = rk - 1;
       prefix[mm][q] = 0ull;
     }
+    if (cached) {  // pass 0's candidates: the group's (trimmed) records
+      if (threadIdx.x == 0) n_cand[0] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int m = (int)mcache[i] - g0;
+        const bool want = m >= 0 && m < gm;
+        const unsigned act = __activemask(), bal = __ballot_sync(act, want);
+        const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+        int base = 0;
+        if (lane == leader && bal) base = atomicAdd(&n_cand[0], __popc(bal));
+        base = __shfl_sync(act, base, leader);
+        if (want) cand[0][base + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
+      }
+    }
     for (int pass = 0; pass < 8; pass++) {
       const int shift = 56 - 8 * pass;
       for (int k = threadIdx.x; k < gm * 3 * 256; k += blockDim.x) (&hist[0][0][0])[k] = 0u;  // used rows only
+      if (threadIdx.x == 0) {
+        n_cand[(pass + 1) & 1] = 0;
+        unresolved = 0;
+      }
       __syncthreads();
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned short* cur = cand[pass & 1];
+      const int n_iter = cached ? n_cand[pass & 1] : n;
+      for (int ii = threadIdx.x; ii < n_iter; ii += blockDim.x) {
+        const int i = cached ? (int)cur[ii] : ii;
         int m;
         unsigned long long key;
         if (cached) {
@@ -1541,15 +1573,47 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
         if (lane == __ffs(who) - 1) {
           int l = left - excl;
           unsigned int d = lane * 8;
+          int held = 0;
           for (int j = 0; j < 8; j++, d++) {
+            held = c8[j];
             if (d == 255u || l < c8[j]) break;
             l -= c8[j];
           }
           rank_left[mm][q] = l;
           prefix[mm][q] |= (unsigned long long)d << shift;
+          resolved[mm][q] = held == 1;
+          if (held != 1) atomicAdd(&unresolved, 1);
         }
       }
       __syncthreads();
+      if (cached && pass < 7) {  // keep the records that still match one of their model's prefixes
+        int* nn = &n_cand[(pass + 1) & 1];
+        unsigned short* nxt = cand[(pass + 1) & 1];
+        for (int ii = threadIdx.x; ii < n_iter; ii += blockDim.x) {
+          const int i = (int)cur[ii];
+          const int m = (int)mcache[i] - g0;
+          const unsigned long long key = kcache[i];
+          bool keep = false;
+#pragma unroll
+          for (int q = 0; q < 3; q++) {
+            const bool match = ((key ^ prefix[m][q]) >> shift) == 0ull;
+            keep |= match;
+            if (match && resolved[m][q]) found[m][q] = key;  // the one record with this prefix
+          }
+          const unsigned act = __activemask(), bal = __ballot_sync(act, keep);
+          const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+          int base = 0;
+          if (lane == leader && bal) base = atomicAdd(nn, __popc(bal));
+          base = __shfl_sync(act, base, leader);
+          if (keep) nxt[base + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
+        }
+        __syncthreads();
+        if (unresolved == 0) {  // every quantile is a known record: done with this group
+          if (threadIdx.x < gm * 3) prefix[threadIdx.x / 3][threadIdx.x % 3] = found[threadIdx.x / 3][threadIdx.x % 3];
+          __syncthreads();
+          break;
+        }
+      }
     }
     if (threadIdx.x < gm * 3) {
       const int mm = threadIdx.x / 3, q = threadIdx.x % 3;
@@ -2039,7 +2103,7 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
   }
   // keys (8 B) + model ids (1 B): 36 KB dynamic on top of ~25 KB static -> opt-in
   // attribute, set once per device (setting it twice is harmless)
-  const size_t smem = (size_t)kSloCache * 9;
+  const size_t smem = (size_t)kSloCache * (9 + 4);  // keys + model ids + two candidate index lists
   int dev = 0;
   cudaGetDevice(&dev);
   static bool attr_set[64] = {};
