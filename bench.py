@@ -626,18 +626,30 @@ def c1_leg(a, stream, barrier, max_over_ranks, rank, world, W) -> dict:
     ta = table.arrays()
     coarse = _abi.Predictor(ewma=0, alpha=1.0, w=tuple(W[-1, 0]))
     pipe = engine.ReplayPipeline([BUNDLED_SEED7], ta, preds=[coarse])
-    for _ in range(5):
-        pipe.run()
     reps = max(20, a.steps)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        pipe.run()
-    e1.record(stream)
-    barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1)) / reps
+
+    def timed(f):
+        for _ in range(5):
+            f()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            f()
+        e1.record(stream)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1)) / reps
+
+    warp_ms = timed(pipe.run)  # one warp replays the whole trace
+    jpipe = engine.ReplayPipeline([BUNDLED_SEED7], ta, preds=[coarse])
+
+    def jobs():  # the trace as speculative busy-period jobs, 3 device-queued passes, one host check
+        engine.replay_segmented(jpipe, min_len=16, passes=3, stats=False)()
+
+    ms = timed(jobs)
     nb = int(pipe.t["n_batches"][0].item())
+    jv, wv = jpipe.scenario(jpipe.fetch(), 0), pipe.scenario(pipe.fetch(), 0)
+    same = all(np.array_equal(jv[k], wv[k]) for k in ("order", "b_completion", "r_slo_met", "Yhat"))
     spec = scenario_from_dict(BUNDLED_SEED7)
     model = LinearModel(w=np.array(W[-1, 0, :6]), b=float(W[-1, 0, 6]))
 
@@ -674,7 +686,8 @@ def c1_leg(a, stream, barrier, max_over_ranks, rank, world, W) -> dict:
                          f"features + forward) in {dt:.2f} s; the reference's own Python run_scenario: "
                          f"270.5 ms/replay on one core of the build container (SURVEY §6)"}
     return {"metric": "bundled-trace replays/sec (C1)", "value": world * 1e3 / ms, "unit": "replays/s",
-            "us_per_replay": 1e3 * ms, "scaling": "weak (replicas only: one trace does not shard)",
+            "us_per_replay": 1e3 * ms, "us_per_replay_one_warp": 1e3 * warp_ms, "jobs_equal_one_warp": same,
+            "scaling": "weak (replicas only: one trace does not shard)",
             "batches": nb, "consistent": ok,
             "e2e": {"value": world * 1e3 / e2e_ms, "unit": "replays/s", "ms_per_call": e2e_ms,
                     "call": "run_scenario(spec, table) + predict_many (objects materialised on the host)",
@@ -682,8 +695,9 @@ def c1_leg(a, stream, barrier, max_over_ranks, rank, world, W) -> dict:
                     "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in pipe.t.values()))},
             "cpu_baseline": cpu,
             "workload": "C1: pkg/scenarios/mixed_three_model.json, seed 7, static mode, coarse predictor "
-                        "(bench C2 decision 31's refit); device pass = arrivals + formation + noise + replay + "
-                        "SLO + features + forward"}
+                        "(bench C2 decision 31's refit); device pass = arrivals + formation + noise + replay as "
+                        "busy-period jobs (min_len 16, 3 queued passes + one host check) + SLO + features + "
+                        "forward; us_per_replay_one_warp = the same with one warp replaying the whole trace"}
 
 
 def c3_leg(a, stream, barrier, max_over_ranks, rank, world) -> dict:

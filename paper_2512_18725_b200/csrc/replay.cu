@@ -1477,7 +1477,7 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
   __shared__ int n_cand[2];
   // a (model, quantile) whose selected digit holds ONE record is resolved: that
   // record's key is the answer; when all are, the remaining passes are skipped
-  __shared__ int unresolved;
+  __shared__ int unresolved[2];  // by pass parity: pass p's check and pass p+1's reset never share a word
   __shared__ unsigned char resolved[kSloGroup][3];
   __shared__ unsigned long long found[kSloGroup][3];
   const bool cached = n <= kSloCache;
@@ -1519,7 +1519,7 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
       for (int k = threadIdx.x; k < gm * 3 * 256; k += blockDim.x) (&hist[0][0][0])[k] = 0u;  // used rows only
       if (threadIdx.x == 0) {
         n_cand[(pass + 1) & 1] = 0;
-        unresolved = 0;
+        unresolved[pass & 1] = 0;
       }
       __syncthreads();
       const unsigned short* cur = cand[pass & 1];
@@ -1582,7 +1582,7 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
           rank_left[mm][q] = l;
           prefix[mm][q] |= (unsigned long long)d << shift;
           resolved[mm][q] = held == 1;
-          if (held != 1) atomicAdd(&unresolved, 1);
+          if (held != 1) atomicAdd(&unresolved[pass & 1], 1);
         }
       }
       __syncthreads();
@@ -1608,7 +1608,7 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
           if (keep) nxt[base + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
         }
         __syncthreads();
-        if (unresolved == 0) {  // every quantile is a known record: done with this group
+        if (unresolved[pass & 1] == 0) {  // every quantile is a known record: done with this group
           if (threadIdx.x < gm * 3) prefix[threadIdx.x / 3][threadIdx.x % 3] = found[threadIdx.x / 3][threadIdx.x % 3];
           __syncthreads();
           break;

@@ -35,6 +35,12 @@ bb = [sc.alloc_best(8) for _ in range(2)]
 sc.pipeline_start(fused=True)
 sc.best_step(W, bb[0], bb[1])
 torch.cuda.synchronize()
+sc4 = engine.CandidateScorer(table.arrays(), cap=4, alpha=0.5)
+sc4.prepare_decisions()
+rank, own = sc4.dispatch_decisions(pp)
+best, chosen = sc4.score_decisions(W[0].contiguous(), rank, own)
+torch.cuda.synchronize()
+print("decisions", int((rank >= 0).sum()))
 X = np.random.default_rng(0).uniform(0, 1, size=(4096, 6))
 y = X @ np.arange(1, 7) + 1.0
 print("ols windows", len(p.predict.fit_ols_windows(X, y, 64)))
