@@ -425,6 +425,29 @@ int intf_rls_segments(const double *X, const double *y, const int64_t *lo, const
 int intf_eval_segments(const double *yhat, const double *y, const int64_t *lo, const int64_t *hi, int32_t n_seg,
                        int64_t max_len, double *out, void *stream);
 
+/* Scalar calls of the per-object API (a hand-driven GpuState, per-sample
+ * learner updates): arguments as 64-bit patterns (doubles by their bits),
+ * passed as kernel parameters; results written to mapped pinned memory and
+ * copied to out after a stream synchronisation (one launch + one sync).
+ * Same device functions and operation order as the batched entry points.
+ *   NOISE    (oracle_seed, batch_id, seg_idx, sigma)   -> noise           (`oracle.py:24-33`)
+ *   SLOWDOWN (own[3], colo[3], beta[3], noise)         -> slowdown        (`oracle.py:36-47`)
+ *   PREDICT  (w[7], x[6])                              -> w.x + b         (`predict.py:43-44`)
+ *   EWMA     (r[3], x[3], alpha)                       -> r'[3]           (`colocation.py:61`)
+ *   SGD      (w[7], x[6], y, eta)                      -> w'[7], yhat, status        (`predict.py:88-95`)
+ *   RLS      (w[7], P[49], x[6], y, lambda)            -> w'[7], P'[49], yhat, status (`predict.py:137-154`)
+ * status: 1 non-finite parameters, 2 P reset.  Not reentrant within a host
+ * thread (one mapped buffer per thread).                                    */
+enum {
+  INTF_SCALAR_NOISE = 0,
+  INTF_SCALAR_SLOWDOWN = 1,
+  INTF_SCALAR_PREDICT = 2,
+  INTF_SCALAR_EWMA = 3,
+  INTF_SCALAR_SGD = 4,
+  INTF_SCALAR_RLS = 5
+};
+int intf_scalar(int32_t op, const uint64_t *args, int32_t n_args, double *out, int32_t n_out, void *stream);
+
 /* ---- array-level entry points behind the per-object reference API ---- */
 
 /* samples_from_outcomes over arbitrary outcome rows (`colocation.py:95-105`):

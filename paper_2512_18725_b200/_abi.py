@@ -133,6 +133,7 @@ SIGNATURES = {
     "intf_latency_report": (c_int32, [P, P, P, P, c_int64, c_int32, c_double, P, P, P, P]),
     "intf_noise_draws": (c_int32, [ctypes.c_uint64, c_double, P, P, c_int64, P, P]),
     "intf_slowdowns": (c_int32, [P, P, P, P, c_int64, P, P]),
+    "intf_scalar": (c_int32, [c_int32, P, c_int32, P, c_int32, P]),
     "intf_rng_stream": (c_int32, [P, c_int32, c_int64, c_int32, P, P]),
     "intf_last_error": (c_int32, [ctypes.c_char_p, c_int32]),
     "intf_abi_version": (c_int32, []),

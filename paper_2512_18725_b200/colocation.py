@@ -76,7 +76,11 @@ def observe(est: CoLocationEstimate, x_t) -> CoLocationEstimate:
     """One co-location change (`colocation.py:54-63`); no-op in static mode."""
     x_t = _check_nonneg(x_t)
     if est.mode.kind == EWMA:
-        est.r_hat = _fold(np.stack([est.r_hat, x_t]), est.mode)
+        from . import engine
+
+        est.r_hat = engine.scalar(engine.SCALAR_EWMA, (), np.concatenate([np.asarray(est.r_hat, dtype=float)
+                                                                          .reshape(3), x_t.reshape(3),
+                                                                          [float(est.mode.alpha)]]))
         est.n_observations += 1
     return est
 

@@ -3,6 +3,7 @@
 // `predict.py:43-44` predict over rows, `metrics.py:28-36,49-79` percentile
 // and slo_report over record lists).  Same arithmetic as replay.cu/predict.cu.
 #include <math.h>
+#include <string.h>
 
 #include "capi_common.h"
 #include "replay_core.cuh"
@@ -199,9 +200,132 @@ __global__ void k_normals(const uint32_t* __restrict__ words, int nw, long long 
   for (long long i = 0; i < n; i++) out[i] = uniform ? pcg_next_double(g) : zig_normal(g);
 }
 
+// ---- scalar calls of the per-object API (one value per call: a hand-driven
+// GpuState's reseat, a per-sample learner update, ...): the arguments travel
+// as kernel parameters (bit patterns) and the results land in mapped pinned
+// host memory, so a call is one launch + one stream synchronisation instead
+// of tensor allocations and copies.  Same device functions / operation order
+// as the batched kernels, so a scalar result equals its batched twin.
+struct ScalarArgs {
+  unsigned long long u[72];
+};
+
+__device__ __forceinline__ double dbits(unsigned long long v) { return __longlong_as_double((long long)v); }
+
+__global__ void k_scalar(int op, ScalarArgs a, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  switch (op) {
+    case INTF_SCALAR_NOISE:  // (seed, batch, seg, sigma) -> noise (`oracle.py:24-33`)
+      out[0] = noise_draw(a.u[0], a.u[1], a.u[2], dbits(a.u[3]));
+      break;
+    case INTF_SCALAR_SLOWDOWN: {  // (own3, colo3, beta3, noise) -> slowdown (`oracle.py:36-47`)
+      double o[3], c[3], b[3];
+      for (int i = 0; i < 3; i++) o[i] = dbits(a.u[i]), c[i] = dbits(a.u[3 + i]), b[i] = dbits(a.u[6 + i]);
+      out[0] = slowdown(o, c, b, dbits(a.u[9]));
+      break;
+    }
+    case INTF_SCALAR_PREDICT: {  // (w7, x6) -> w.x + b (`predict.py:43-44`)
+      double w[7], x[6];
+      for (int i = 0; i < 7; i++) w[i] = dbits(a.u[i]);
+      for (int i = 0; i < 6; i++) x[i] = dbits(a.u[7 + i]);
+      out[0] = predict7(w, x);
+      break;
+    }
+    case INTF_SCALAR_EWMA: {  // (r3, x3, alpha) -> alpha x + (1 - alpha) r (`colocation.py:61`)
+      const double al = dbits(a.u[6]), om = 1.0 - al;
+      for (int i = 0; i < 3; i++) out[i] = al * dbits(a.u[3 + i]) + om * dbits(a.u[i]);
+      break;
+    }
+    case INTF_SCALAR_SGD: {  // (w7, x6, y, eta) -> (w7', yhat, status) as k_sgd (`predict.py:88-95`)
+      double w[7], x[6];
+      for (int i = 0; i < 7; i++) w[i] = dbits(a.u[i]);
+      for (int i = 0; i < 6; i++) x[i] = dbits(a.u[7 + i]);
+      const double y = dbits(a.u[13]), et = dbits(a.u[14]);
+      const double yh = predict7(w, x);
+      const double e = y - yh, ee = et * e;
+      for (int j = 0; j < 6; j++) w[j] = w[j] + ee * x[j];
+      w[6] = w[6] + et * e;
+      bool fin = true;
+      for (int j = 0; j < 7; j++) fin &= isfinite(w[j]);
+      for (int j = 0; j < 7; j++) out[j] = w[j];
+      out[7] = yh;
+      out[8] = fin ? 0.0 : 1.0;
+      break;
+    }
+    case INTF_SCALAR_RLS: {  // (w7, P49, x6, y, lam) -> (w7', P49', yhat, status) as k_rls_g8 (`predict.py:137-154`)
+      double w[7], P[49], z[7], Pz[7], k[7];
+      for (int i = 0; i < 7; i++) w[i] = dbits(a.u[i]);
+      for (int i = 0; i < 49; i++) P[i] = dbits(a.u[7 + i]);
+      for (int i = 0; i < 6; i++) z[i] = dbits(a.u[56 + i]);
+      z[6] = 1.0;
+      const double y = dbits(a.u[62]), lam = dbits(a.u[63]), inv_lam = 1.0 / lam;
+      const double yh = predict7(w, z);
+      for (int r = 0; r < 7; r++) {
+        double acc = 0.0;
+        for (int j = 0; j < 7; j++) acc = fma(P[r * 7 + j], z[j], acc);
+        Pz[r] = acc;
+      }
+      double zPz = 0.0;
+      for (int j = 0; j < 7; j++) zPz = fma(z[j], Pz[j], zPz);
+      double denom = lam + zPz;
+      int st = 0;
+      if (!(denom > 0.0) || !isfinite(denom)) {  // P reset (`predict.py:142-146`)
+        st |= 2;
+        double zr = 0.0;
+        for (int j = 0; j < 7; j++) zr = fma(z[j], 100.0 * z[j], zr);
+        for (int i = 0; i < 49; i++) P[i] = (i % 8 == 0) ? 100.0 : 0.0;
+        for (int j = 0; j < 7; j++) Pz[j] = 100.0 * z[j];
+        denom = lam + zr;
+      }
+      const double inv_den = 1.0 / denom;
+      for (int r = 0; r < 7; r++) k[r] = Pz[r] * inv_den;
+      const double e = y - yh;
+      for (int j = 0; j < 7; j++) w[j] = w[j] + k[j] * e;
+      double Pn[49];
+      for (int r = 0; r < 7; r++)
+        for (int j = 0; j < 7; j++) Pn[r * 7 + j] = (P[r * 7 + j] - k[r] * Pz[j]) * inv_lam;
+      for (int r = 0; r < 7; r++)
+        for (int j = 0; j < 7; j++) P[r * 7 + j] = 0.5 * (Pn[r * 7 + j] + Pn[j * 7 + r]);
+      bool fin = true;
+      for (int j = 0; j < 7; j++) fin &= isfinite(w[j]);
+      for (int j = 0; j < 7; j++) out[j] = w[j];
+      for (int i = 0; i < 49; i++) out[7 + i] = P[i];
+      out[56] = yh;
+      out[57] = (double)(st | (fin ? 0 : 1));
+      break;
+    }
+    default:
+      out[0] = NAN;
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int intf_scalar(int32_t op, const uint64_t* args, int32_t n_args, double* out, int32_t n_out, void* stream) {
+  if (!args || !out || n_args < 0 || n_args > 72 || n_out < 1 || n_out > 64 || op < 0 || op > INTF_SCALAR_RLS)
+    return bad_input("intf_scalar: bad argument");
+  static thread_local double* mapped = nullptr;  // per host thread: 64 doubles of mapped pinned memory
+  static thread_local double* mapped_dev = nullptr;
+  if (!mapped) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&mapped), 64 * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped_dev), mapped, 0) != cudaSuccess) {
+      mapped = nullptr;
+      return launch_status("intf_scalar: mapped host buffer");
+    }
+  }
+  ScalarArgs a;
+  memset(&a, 0, sizeof(a));
+  memcpy(a.u, args, sizeof(uint64_t) * n_args);
+  cudaStream_t st = as_stream(stream);
+  k_scalar<<<1, 32, 0, st>>>(op, a, mapped_dev);
+  int rc = launch_status("k_scalar");
+  if (rc) return rc;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return launch_status("intf_scalar: synchronize");
+  memcpy(out, mapped, sizeof(double) * n_out);
+  return INTF_OK;
+}
 
 int intf_noise_draws(uint64_t seed, double sigma, const int64_t* batch, const int64_t* seg, int64_t n, double* out,
                      void* stream) {

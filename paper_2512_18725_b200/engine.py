@@ -739,6 +739,23 @@ def arrivals(specs, table: _pack.TableArrays, max_retries: int = 6):
     raise RuntimeError("arrival buffers still overflowing after retries")
 
 
+SCALAR_NOISE, SCALAR_SLOWDOWN, SCALAR_PREDICT, SCALAR_EWMA, SCALAR_SGD, SCALAR_RLS = range(6)
+_SCALAR_OUT = {SCALAR_NOISE: 1, SCALAR_SLOWDOWN: 1, SCALAR_PREDICT: 1, SCALAR_EWMA: 3, SCALAR_SGD: 9, SCALAR_RLS: 58}
+
+
+def scalar(op: int, ints=(), floats=()) -> np.ndarray:
+    """One scalar call (intf_scalar): `ints` as uint64 words, then `floats`
+    by their float64 bits; returns the op's outputs (float64)."""
+    require_cuda()
+    args = np.concatenate([np.asarray(ints, dtype=np.uint64).reshape(-1),
+                           np.ascontiguousarray(np.asarray(floats, dtype=np.float64).reshape(-1)).view(np.uint64)])
+    n_out = _SCALAR_OUT[op]
+    out = np.empty(n_out, dtype=np.float64)
+    _abi.check(_abi.load().intf_scalar(op, args.ctypes.data, len(args), out.ctypes.data, n_out, stream_ptr()),
+               "intf_scalar")
+    return out
+
+
 def noise_draws(seed: int, sigma: float, batch_ids, seg_idx) -> np.ndarray:
     dev = require_cuda()
     b = torch.as_tensor(np.ascontiguousarray(batch_ids, dtype=np.int64)).to(dev)

@@ -48,7 +48,8 @@ def predict(model: LinearModel, x) -> float:
     """w @ x + b (`predict.py:43-44`) on the device (fma chain == BLAS ddot)."""
     from . import engine
 
-    return float(engine.predict_rows(np.asarray(x, dtype=float).reshape(1, 6), model.w7())[0])
+    return float(engine.scalar(engine.SCALAR_PREDICT, (), np.concatenate([model.w7(),
+                                                                        np.asarray(x, dtype=float).reshape(6)]))[0])
 
 
 def predict_many(model: LinearModel, X) -> np.ndarray:
@@ -127,8 +128,15 @@ def _sgd_run(state: SgdState, X, y):
 
 
 def sgd_update(state: SgdState, sample) -> SgdState:
-    """One LMS step (`predict.py:88-95`), in place."""
-    _sgd_run(state, np.asarray(sample.x, dtype=float)[None], [sample.y])
+    """One LMS step (`predict.py:88-95`), in place (one scalar device call)."""
+    from . import engine
+
+    out = engine.scalar(engine.SCALAR_SGD, (), np.concatenate([state.model.w7(), np.asarray(sample.x, dtype=float)
+                                                               .reshape(6), [float(sample.y), float(state.eta)]]))
+    state.model.w[:] = out[:6]
+    state.model.b = float(out[6])
+    if out[8]:
+        raise PredictError(f"non-finite model parameters after SGD step (eta={state.eta})")
     return state
 
 
@@ -175,8 +183,20 @@ def _rls_run(state: RlsState, X, y):
 
 
 def rls_update(state: RlsState, sample) -> RlsState:
-    """`predict.py:137-154`, in place."""
-    _rls_run(state, np.asarray(sample.x, dtype=float)[None], [sample.y])
+    """`predict.py:137-154`, in place (one scalar device call)."""
+    from . import engine
+
+    out = engine.scalar(engine.SCALAR_RLS, (), np.concatenate([state.model.w7(), np.asarray(state.P, dtype=float)
+                                                               .reshape(49), np.asarray(sample.x, dtype=float)
+                                                               .reshape(6), [float(sample.y), float(state.lam)]]))
+    st = int(out[57])
+    if st & 2:
+        log.warning("RLS gain matrix lost positive-definiteness; resetting P")
+    state.model.w[:] = out[:6]
+    state.model.b = float(out[6])
+    state.P = out[7:56].reshape(7, 7).copy()
+    if st & 1:
+        raise PredictError("non-finite model parameters after RLS step")
     return state
 
 
