@@ -146,8 +146,9 @@ def features_for_modes(outcomes, table, modes):
 def samples_from_outcomes(outcomes, table, mode: Mode, scenario: str = "") -> list:
     """One Sample per completed batch, in outcome order (`colocation.py:95-105`)."""
     X, y, a = features_for_modes(outcomes, table, [mode])
-    return [Sample(x=X[0, i].copy(), y=float(y[i]), batch_id=int(a["batch_id"][i]), scenario=scenario)
-            for i in range(len(y))]
+    Xs = np.array(X[0], dtype=float)  # private copy: every Sample views its own row
+    ys, bids = np.asarray(y, dtype=float).tolist(), np.asarray(a["batch_id"]).tolist()
+    return [Sample(x=Xs[i], y=ys[i], batch_id=bids[i], scenario=scenario) for i in range(len(ys))]
 
 
 SAMPLE_CSV_HEADER = ["batch_id", "scenario", "own_l2", "own_dram", "own_sm", "colo_l2", "colo_dram", "colo_sm",

@@ -177,9 +177,11 @@ class ReplayPipeline:
         return self.t["status"][: self.pb.n_scen].cpu().numpy()
 
     # ------------------------------------------------------------ results
-    def fetch(self) -> dict:
-        """Copy every buffer to host numpy (one sync)."""
-        h = {k: v.cpu().numpy() for k, v in self.t.items()}
+    SCRATCH = ("slot_seg", "noise_tab", "mb_t", "mb_info", "n_mb", "slo_ws", "form_ws", "order")
+
+    def fetch(self, scratch: bool = False) -> dict:
+        """Copy the result buffers to host numpy (scratch buffers too if asked)."""
+        h = {k: v.cpu().numpy() for k, v in self.t.items() if scratch or k not in self.SCRATCH}
         h["Y"] = self.Y.cpu().numpy()
         h["Yhat"] = self.Yhat.cpu().numpy().reshape(-1, self.slot_stride)
         h["X"] = self.X.cpu().numpy().reshape(-1, self.slot_stride, 6)

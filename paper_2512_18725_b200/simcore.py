@@ -332,32 +332,42 @@ def _check_rows(spec, ta, v) -> None:
 
 
 def _materialize(spec, table, v) -> ScenarioResult:
+    """The reference's result objects from the flat device arrays: outcomes in
+    (completion, batch_id) order with their segments, records by request id,
+    samples in outcome order.  Vectorised gathers first, then one pass of
+    object construction from Python lists (the per-object cost is the
+    dataclass __init__ alone)."""
     ta = table.arrays()
-    dep = spec.deployed
-    ids = [d.model_id for d in dep]
-    order = np.asarray(v["order"])
-    bm, bsz = v["b_model"], v["b_size"]
-    rows = np.array([ta.row(ids[bm[b]], int(bsz[b])) for b in order], dtype=np.int64)
-    soff, nseg = v["b_seg_off"][order].astype(np.int64), v["b_nseg"][order].astype(np.int32)
-    colo = v["s_colo"]
-    outcomes = OutcomeList()
-    tb, te, sd = v["s_tbegin"], v["s_tend"], v["s_slowdown"]
+    ids = [d.model_id for d in spec.deployed]
+    order = np.asarray(v["order"], dtype=np.int64)
+    bm, bsz = np.asarray(v["b_model"]), np.asarray(v["b_size"])
+    base = np.array([ta.models.index(m) * ta.max_bs for m in ids], dtype=np.int64)
+    rows = base[bm[order]] + bsz[order].astype(np.int64) - 1 if len(order) else np.zeros(0, np.int64)
+    soff, nseg = v["b_seg_off"][order].astype(np.int64), v["b_nseg"][order].astype(np.int64)
+    # segment records of every outcome, in outcome order (one gather)
+    seg_start = np.concatenate([[0], np.cumsum(nseg)[:-1]]) if len(order) else np.zeros(0, np.int64)
+    idx = (np.repeat(soff - seg_start, nseg) + np.arange(int(nseg.sum()))) if len(order) else np.zeros(0, np.int64)
+    colo = np.array(v["s_colo"][idx], dtype=float).reshape(-1, 3)  # private copy; each Segment views its row
+    tb, te, sd = v["s_tbegin"][idx].tolist(), v["s_tend"][idx].tolist(), v["s_slowdown"][idx].tolist()
     start, comp, meas = v["b_start"], v["b_completion"], v["b_measured"]
+    o_start, o_comp, o_meas = start[order].tolist(), comp[order].tolist(), meas[order].tolist()
+    o_prof, o_model, o_size = ta.solo[rows].tolist(), bm[order].tolist(), bsz[order].tolist()
+    outcomes = OutcomeList()
+    q = 0
     for k, b in enumerate(order.tolist()):
-        o, n = int(soff[k]), int(nseg[k])
-        segs = [Segment(float(tb[q]), float(te[q]), float(sd[q]), colo[q].copy()) for q in range(o, o + n)]
-        outcomes.append(BatchOutcome(b, ids[bm[b]], int(bsz[b]), float(start[b]), float(meas[b]),
-                                     float(ta.solo[rows[k]]), float(comp[b]), segs))
-    # compact colo histories in outcome order for batched feature reuse
-    idx = np.concatenate([np.arange(o, o + n) for o, n in zip(soff, nseg)]) if len(order) else np.zeros(0, np.int64)
+        n = int(nseg[k])
+        segs = [Segment(tb[j], te[j], sd[j], colo[j]) for j in range(q, q + n)]
+        q += n
+        outcomes.append(BatchOutcome(b, ids[o_model[k]], o_size[k], o_start[k], o_meas[k], o_prof[k], o_comp[k], segs))
     outcomes.arrays = {
-        "own": ta.thr[rows].reshape(-1, 3), "seg_off": np.concatenate([[0], np.cumsum(nseg)[:-1]]).astype(np.int64)
-        if len(order) else np.zeros(0, np.int64), "nseg": nseg, "colo": colo[idx].reshape(-1, 3),
-        "measured": meas[order], "profiled": ta.solo[rows], "batch_id": order.astype(np.int64),
+        "own": ta.thr[rows].reshape(-1, 3), "seg_off": seg_start.astype(np.int64), "nseg": nseg.astype(np.int32),
+        "colo": colo, "measured": meas[order], "profiled": ta.solo[rows], "batch_id": order,
     }
     at, am, rb, met = v["arr_t"], v["arr_model"], v["r_batch"], v["r_slo_met"]
-    records = [RequestRecord(i, ids[am[i]], float(at[i]), int(rb[i]), float(start[rb[i]]), float(comp[rb[i]]),
-                             bool(met[i])) for i in range(len(at))]
+    r_t, r_model, r_b = at.tolist(), np.asarray(am).tolist(), np.asarray(rb).tolist()
+    r_start, r_comp, r_met = start[rb].tolist(), comp[rb].tolist(), np.asarray(met, dtype=bool).tolist()
+    records = [RequestRecord(i, ids[r_model[i]], r_t[i], r_b[i], r_start[i], r_comp[i], r_met[i])
+               for i in range(len(r_t))]
     samples = samples_from_outcomes(outcomes, table, spec.colocation_mode, scenario=spec.name)
     return ScenarioResult(outcomes=outcomes, records=records, samples=samples, arrays=dict(v))
 
