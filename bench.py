@@ -351,6 +351,12 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
     complete = int(pending.sum().item()) == 0 and all(int(p.t["status"][0].item()) == 0 for p in pipes)
     for f in fins[-n_c4_pipes:]:
         f()
+    stage = c4_stages(pipe)
+    peak, _ = _peaks()
+    fs_ms = stage["formation+noise"] + stage["slo"]
+    stage_roofline = {"stages": "formation (+ noise table) + SLO report", "algorithmic_bytes_per_request": 23,
+                      "achieved_gbs": 23.0 * n_req / (fs_ms / 1e3) / 1e9, "peak": peak,
+                      "frac": 23.0 * n_req / (fs_ms / 1e3) / 1e9 / peak}
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         # the oracle's C heap-engine replay of the same trace (+ its arrivals), one core, once
@@ -366,10 +372,48 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
             "unit": "requests/s", "ms_per_trace": ms, "requests": n_req, "status": st, **stats,
             "pipelined": {"value": world * n_req / (pms / 1e3), "unit": "requests/s", "ms_per_trace": pms,
                           "traces": K, "streams": n_c4_pipes, "complete": complete},
-            "cpu_baseline": cpu,
+            "cpu_baseline": cpu, "stage_ms": stage, "stage_roofline": stage_roofline,
             "workload": "C4: 16 models (6 default + 10 rng(123) archetypes), bs 1-64, cap 4, window U(10,20) ms, "
                         "sigma 0.05, total rho 0.5 at bs 64; one trace per GPU; arrivals + formation + noise + "
                         "busy-period-sharded replay + SLO + features"}
+
+
+def c4_stages(pipe) -> dict:
+    """One extra (untimed) pass of the long-trace path with events between its
+    launches: per-stage device time in ms (`tools/c4_breakdown.py`)."""
+    import ctypes
+
+    import torch
+    from paper_2512_18725_b200 import _abi
+
+    L, st = pipe.lib, torch.cuda.current_stream().cuda_stream
+    bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
+    J, tab = ctypes.byref(pipe._jobs.J), ctypes.byref(pipe.dtable.struct)
+    marks = []
+
+    def mark(name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append((name, e))
+
+    mark("start")
+    _abi.check(L.intf_generate_arrivals(bt, B, st), "arrivals")
+    mark("arrivals")
+    _abi.check(L.intf_form_batches(bt, B, st), "formation")
+    mark("formation+noise")
+    _abi.check(L.intf_jobs_plan(bt, tab, B, J, st), "plan")
+    mark("plan")
+    total = int(pipe._jobs.J.total_slots)
+    for _ in range(C4_PASSES):
+        _abi.check(L.intf_jobs_replay(bt, tab, B, J, -total, st), "jobs replay")
+        _abi.check(L.intf_jobs_verify(bt, B, J, st), "jobs verify")
+    mark("replay+verify passes")
+    pipe.run_slo_features(slo=True, features=False)
+    mark("slo")
+    pipe.run_slo_features(slo=False, features=True)
+    mark("features")
+    torch.cuda.synchronize()
+    return {b: ea.elapsed_time(eb) for (_, ea), (b, eb) in zip(marks, marks[1:])}
 
 
 def c4_sharded(a, spec, ta, stream, barrier, max_over_ranks, rank, world) -> dict:
