@@ -5,6 +5,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/intfsim_b200.h"
 
 namespace intf {
@@ -29,5 +31,16 @@ inline int bad_input(const char* what) {
 }
 
 inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+// NVTX range over one C-ABI call (host side: the launches it enqueues), so a
+// profiler timeline (nsys / ncu --nvtx) shows the hot path's stages by name;
+// a no-op unless a tool is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define INTF_RANGE(name) ::intf::NvtxRange intf_nvtx_range_(name)
 
 }  // namespace intf

@@ -103,6 +103,7 @@ int intf_repr_f64(double v, char* out, int32_t cap) {
 int intf_csv_rows(int64_t n_rows, int32_t n_cols, const int32_t* kinds, const void* const* cols,
                   const char* const* strtab, const int32_t* strlen_tab, char* out, int64_t out_cap,
                   int64_t* out_len) {
+  INTF_RANGE("intf_csv_rows");
   if (n_rows < 0 || n_cols < 1 || !kinds || !cols || !out_len) return bad_input("intf_csv_rows: bad argument");
   char* q = out;
   char* const end = out ? out + out_cap : nullptr;

@@ -2237,6 +2237,7 @@ static int dispatch_candidates(const intf_table* table, int32_t cap, double alph
 
 int intf_predict_candidates(const intf_table* table, int32_t cap, double alpha, const double* coefs, int32_t n_dec,
                             float* out, float* ws, int64_t ws_elems, void* stream) {
+  INTF_RANGE("intf_predict_candidates");
   if (!table || !coefs || !out || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1 || table->n_rows < 1)
     return bad_input("intf_predict_candidates: bad argument (n_dec >= 1, 1 <= cap <= 8)");
   return dispatch_candidates(table, cap, alpha, coefs, n_dec, out, ws, ws_elems, stream, 3);
@@ -2244,6 +2245,7 @@ int intf_predict_candidates(const intf_table* table, int32_t cap, double alpha, 
 
 int intf_candidate_prepare(const intf_table* table, int32_t cap, double alpha, float* ws, int64_t ws_elems,
                            void* stream) {
+  INTF_RANGE("intf_candidate_prepare");
   int64_t need = 0;
   if (!table || !ws || intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need)
     return bad_input("intf_candidate_prepare: bad argument or workspace too small");
@@ -2252,6 +2254,7 @@ int intf_candidate_prepare(const intf_table* table, int32_t cap, double alpha, f
 
 int intf_predict_candidates_prepared(const intf_table* table, int32_t cap, const double* coefs, int32_t n_dec,
                                      float* out, const float* ws, int64_t ws_elems, void* stream) {
+  INTF_RANGE("intf_predict_candidates_prepared");
   int64_t need = 0;
   if (!table || !coefs || !out || !ws || n_dec < 1 || intf_candidate_workspace(table->n_rows, cap, &need) ||
       ws_elems < need)
@@ -2262,6 +2265,7 @@ int intf_predict_candidates_prepared(const intf_table* table, int32_t cap, const
 int intf_candidate_best_step(const intf_table* table, int32_t cap, double alpha, const double* coefs,
                              int32_t n_dec, uint64_t* best, uint64_t* best_next, const float* ws_cur, float* ws_next,
                              int64_t ws_elems, void* stream) {
+  INTF_RANGE("intf_candidate_best_step");
   int64_t need = 0;
   if (!table || !coefs || !best || !ws_cur || !ws_next || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1 ||
       intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need || ws_next == ws_cur ||
@@ -2283,6 +2287,7 @@ int intf_candidate_best_step(const intf_table* table, int32_t cap, double alpha,
 
 int intf_candidate_step(const intf_table* table, int32_t cap, double alpha, const double* coefs, int32_t n_dec,
                         float* out, const float* ws_cur, float* ws_next, int64_t ws_elems, void* stream) {
+  INTF_RANGE("intf_candidate_step");
   int64_t need = 0;
   if (!table || !coefs || !out || !ws_cur || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1 ||
       intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need || ws_next == ws_cur)
@@ -2303,6 +2308,7 @@ int intf_candidate_step(const intf_table* table, int32_t cap, double alpha, cons
 int intf_predict_candidates_host(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
                                  int32_t n_dec, float* h_out, float* d_scratch, int64_t scratch_elems,
                                  void* stream) {
+  INTF_RANGE("intf_predict_candidates_host");
   if (!table || !h_coefs || !h_out || !d_scratch) return bad_input("intf_predict_candidates_host: null argument");
   int64_t n_cand = 0, n_sets = 0, ld = 0, ws = 0;
   int rc = intf_candidate_count(table->n_rows, cap, &n_cand, &n_sets, &ld);
@@ -2329,6 +2335,7 @@ int intf_predict_candidates_host(const intf_table* table, int32_t cap, double al
 int intf_best_candidates_host(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
                               int32_t n_dec, uint64_t* h_best, float* d_scratch, int64_t scratch_elems,
                               void* stream) {
+  INTF_RANGE("intf_best_candidates_host");
   if (!table || !h_coefs || !h_best || !d_scratch || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1)
     return bad_input("intf_best_candidates_host: bad argument");
   int64_t ws = 0;
@@ -2363,6 +2370,7 @@ int intf_best_candidates_host(const intf_table* table, int32_t cap, double alpha
 
 int intf_dispatch_sets(const intf_batch* bt, const intf_replay_buffers* buf, int32_t n_rows, int32_t cap_enum,
                        int32_t* dec_rank, int32_t* dec_own, void* stream) {
+  INTF_RANGE("intf_dispatch_sets");
   if (!bt || !bt->scen || !bt->models || !buf || !buf->b_start || !buf->b_completion || !dec_rank || !dec_own ||
       cap_enum < 1 || cap_enum > kMaxPeers + 1 || buf->cap_max > cap_enum || n_rows < 1)
     return bad_input("intf_dispatch_sets: bad argument (the enumeration cap must cover every scenario's cap)");
@@ -2380,6 +2388,7 @@ int64_t intf_decision_features_elems(int32_t n_rows, int32_t cap) {
 
 int intf_decision_features(const intf_table* table, int32_t cap, const float* ws, int64_t ws_elems, float* ft,
                            void* stream) {
+  INTF_RANGE("intf_decision_features");
   int64_t need = 0;
   if (!table || !ws || !ft || intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need)
     return bad_input("intf_decision_features: bad argument or workspace too small");
@@ -2397,12 +2406,14 @@ int intf_score_decisions_ft(const intf_table* table, int32_t cap, const double* 
 int intf_score_decisions(const intf_table* table, int32_t cap, const double* coefs, const float* ws, int64_t ws_elems,
                          const int32_t* dec_rank, const int32_t* dec_own, int64_t n, uint64_t* best, float* chosen,
                          void* stream) {
+  INTF_RANGE("intf_score_decisions");
   return intf_score_decisions_ft(table, cap, coefs, ws, ws_elems, nullptr, dec_rank, dec_own, n, best, chosen, stream);
 }
 
 int intf_score_decisions_ft(const intf_table* table, int32_t cap, const double* coefs, const float* ws,
                             int64_t ws_elems, const float* ft, const int32_t* dec_rank, const int32_t* dec_own,
                             int64_t n, uint64_t* best, float* chosen, void* stream) {
+  INTF_RANGE("intf_score_decisions_ft");
   int64_t need = 0;
   if (!table || !coefs || !ws || !dec_rank || !dec_own || !best || !chosen || n < 0 || table->n_rows > 64 ||
       intf_candidate_workspace(table->n_rows, cap, &need) || ws_elems < need)
@@ -2417,6 +2428,7 @@ int intf_score_decisions_ft(const intf_table* table, int32_t cap, const double* 
 }
 
 int intf_ols_stats(const double* X, const double* y, int64_t n, double* out, double* ws, void* stream) {
+  INTF_RANGE("intf_ols_stats");
   if (!X || !y || !out || !ws || n < 0) return bad_input("intf_ols_stats: bad argument");
   cudaStream_t st = as_stream(stream);
   const int nblk = (int)((n + kOlsThreads - 1) / kOlsThreads) < kOlsBlocks ? (int)((n + kOlsThreads - 1) / kOlsThreads)
@@ -2431,6 +2443,7 @@ int intf_ols_stats(const double* X, const double* y, int64_t n, double* out, dou
 }
 
 int intf_ols_solve(const double* stats, double* out_params, int32_t* out_info, double* out_Pinv, void* stream) {
+  INTF_RANGE("intf_ols_solve");
   if (!stats || !out_params) return bad_input("intf_ols_solve: null argument");
   k_ols_solve<<<1, 32, 0, as_stream(stream)>>>(stats, nullptr, out_params, out_info, out_Pinv);
   return launch_status("k_ols_solve");
@@ -2438,6 +2451,7 @@ int intf_ols_solve(const double* stats, double* out_params, int32_t* out_info, d
 
 int intf_ols_fit_rows(const double* X, const double* y, int64_t n, const double* stats, double* ws,
                       double* out_params, int32_t* out_info, double* out_Pinv, void* stream) {
+  INTF_RANGE("intf_ols_fit_rows");
   if (!X || !y || !stats || !ws || !out_params || n < 0) return bad_input("intf_ols_fit_rows: bad argument");
   cudaStream_t st = as_stream(stream);
   const long long want = (n + 32ll * kQrThreads - 1) / (32ll * kQrThreads);  // >= 32 rows per thread
@@ -2454,6 +2468,7 @@ int intf_ols_fit_rows(const double* X, const double* y, int64_t n, const double*
 
 int intf_ols_windows(const double* X, const double* y, int64_t n, int32_t window, double* stats, double* params,
                      int32_t* info, void* stream) {
+  INTF_RANGE("intf_ols_windows");
   if (!X || !y || !params || !info || n < 0 || window < 1)
     return bad_input("intf_ols_windows: bad argument");
   const long long n_win = (n + window - 1) / window;
@@ -2491,6 +2506,7 @@ int intf_ols_windows(const double* X, const double* y, int64_t n, int32_t window
 
 int intf_sgd_streams(const double* X, const double* y, const int64_t* off, int32_t n_streams, const double* eta,
                      double* params, double* pred, int32_t* status, void* stream) {
+  INTF_RANGE("intf_sgd_streams");
   if (!X || !y || !off || !eta || !params || !pred || n_streams < 0) return bad_input("intf_sgd_streams: bad argument");
   if (n_streams == 0) return INTF_OK;
   k_sgd<<<ceil_div(n_streams, 64), 64, 0, as_stream(stream)>>>(X, y, (const long long*)off, n_streams, eta, params,
@@ -2500,6 +2516,7 @@ int intf_sgd_streams(const double* X, const double* y, const int64_t* off, int32
 
 int intf_rls_streams(const double* X, const double* y, const int64_t* off, int32_t n_streams, const double* lam,
                      double* params, double* P, double* pred, int32_t* status, void* stream) {
+  INTF_RANGE("intf_rls_streams");
   if (!X || !y || !off || !lam || !params || !P || !pred || n_streams < 0)
     return bad_input("intf_rls_streams: bad argument");
   if (n_streams == 0) return INTF_OK;
@@ -2515,6 +2532,7 @@ int64_t intf_scenario_eval_ws(int32_t n_scen, int64_t slot_stride) {
 int intf_scenario_eval(const intf_batch* bt, const intf_replay_buffers* buf, const double* X, int64_t slot_stride,
                        int32_t p_static, int32_t p_ewma, const double* y, double lam, double* ws, int64_t ws_elems,
                        double* params, double* report, int32_t* status, void* stream) {
+  INTF_RANGE("intf_scenario_eval");
   if (!bt || !bt->scen || !buf || !buf->n_batches || !X || !y || !ws || !params || !report || !status ||
       p_static < 0 || p_ewma < 0 || !(lam > 0.0 && lam <= 1.0))
     return bad_input("intf_scenario_eval: bad argument");
@@ -2548,6 +2566,7 @@ int intf_scenario_eval(const intf_batch* bt, const intf_replay_buffers* buf, con
 
 int intf_ols_fit_segments(const double* X, const double* y, const int64_t* lo, const int64_t* hi, int32_t n_seg,
                           double* params, int32_t* info, double* Pinv, void* stream) {
+  INTF_RANGE("intf_ols_fit_segments");
   if (!X || !y || !lo || !hi || !params || !info || n_seg < 0) return bad_input("intf_ols_fit_segments: bad argument");
   if (n_seg == 0) return INTF_OK;
   k_fit_segments<<<ceil_div(n_seg, kScenFitWarps), 32 * kScenFitWarps, 0, as_stream(stream)>>>(
@@ -2557,6 +2576,7 @@ int intf_ols_fit_segments(const double* X, const double* y, const int64_t* lo, c
 
 int intf_predict_segments(const double* X, const int64_t* lo, const int64_t* hi, const int32_t* model,
                           const double* params, int32_t n_seg, double* yhat, void* stream) {
+  INTF_RANGE("intf_predict_segments");
   if (!X || !lo || !hi || !params || !yhat || n_seg < 0) return bad_input("intf_predict_segments: bad argument");
   if (n_seg == 0) return INTF_OK;
   k_predict_segments<<<n_seg, 128, 0, as_stream(stream)>>>(X, (const long long*)lo, (const long long*)hi, model,
@@ -2566,6 +2586,7 @@ int intf_predict_segments(const double* X, const int64_t* lo, const int64_t* hi,
 
 int intf_sgd_segments(const double* X, const double* y, const int64_t* lo, const int64_t* hi, int32_t n_seg,
                       const double* eta, double* params, double* pred, int32_t* status, void* stream) {
+  INTF_RANGE("intf_sgd_segments");
   if (!X || !y || !lo || !hi || !eta || !params || !pred || n_seg < 0) return bad_input("intf_sgd_segments: bad argument");
   if (n_seg == 0) return INTF_OK;
   k_sgd<<<ceil_div(n_seg, 64), 64, 0, as_stream(stream)>>>(X, y, (const long long*)lo, n_seg, eta, params, pred, status,
@@ -2575,6 +2596,7 @@ int intf_sgd_segments(const double* X, const double* y, const int64_t* lo, const
 
 int intf_rls_segments(const double* X, const double* y, const int64_t* lo, const int64_t* hi, int32_t n_seg,
                       const double* lam, double* params, double* P, double* pred, int32_t* status, void* stream) {
+  INTF_RANGE("intf_rls_segments");
   if (!X || !y || !lo || !hi || !lam || !params || !P || !pred || n_seg < 0)
     return bad_input("intf_rls_segments: bad argument");
   if (n_seg == 0) return INTF_OK;
@@ -2586,6 +2608,7 @@ int intf_rls_segments(const double* X, const double* y, const int64_t* lo, const
 
 int intf_eval_segments(const double* yhat, const double* y, const int64_t* lo, const int64_t* hi, int32_t n_seg,
                        int64_t max_len, double* out, void* stream) {
+  INTF_RANGE("intf_eval_segments");
   if (!yhat || !y || !lo || !hi || !out || n_seg < 0) return bad_input("intf_eval_segments: bad argument");
   if (n_seg == 0) return INTF_OK;
   cudaStream_t st = as_stream(stream);
@@ -2600,6 +2623,7 @@ int intf_eval_segments(const double* yhat, const double* y, const int64_t* lo, c
 
 int intf_eval_report(const double* yhat, const double* y, const int64_t* off, int32_t n_seg, double* out,
                      void* stream) {
+  INTF_RANGE("intf_eval_report");
   if (!yhat || !y || !off || !out || n_seg < 0) return bad_input("intf_eval_report: bad argument");
   if (n_seg == 0) return INTF_OK;
   k_eval<<<n_seg, kEvalThreads, 0, as_stream(stream)>>>(yhat, y, (const long long*)off, out);

@@ -1928,6 +1928,7 @@ extern "C" {
 int intf_long_list(void) { return kLongForm; }
 
 int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, void* stream) {
+  INTF_RANGE("intf_generate_arrivals");
   if (!bt || !bt->scen || !bt->models || !buf || bt->n_scen <= 0) return bad_input("intf_generate_arrivals: null argument");
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(buf->n_req, 0, sizeof(int32_t) * bt->n_scen, st);
@@ -1964,6 +1965,7 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
 }
 
 int intf_split_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, void* stream) {
+  INTF_RANGE("intf_split_arrivals");
   if (!bt || !bt->scen || !bt->models || !buf || bt->n_scen <= 0) return bad_input("intf_split_arrivals: null argument");
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(buf->status, 0, sizeof(int32_t) * bt->n_scen, st);
@@ -1972,6 +1974,7 @@ int intf_split_arrivals(const intf_batch* bt, const intf_replay_buffers* buf, vo
 }
 
 int intf_form_batches(const intf_batch* bt, const intf_replay_buffers* buf, void* stream) {
+  INTF_RANGE("intf_form_batches");
   if (!bt || !bt->scen || !bt->models || !buf || bt->n_scen <= 0) return bad_input("intf_form_batches: null argument");
   if (buf->noise_k > 0 && !buf->noise_tab) return bad_input("intf_form_batches: noise_k > 0 needs noise_tab");
   cudaStream_t st = as_stream(stream);
@@ -1988,6 +1991,7 @@ int intf_form_batches(const intf_batch* bt, const intf_replay_buffers* buf, void
 int intf_replay_jobs(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
                      const int32_t* job_scen, const int32_t* job_lo, const int32_t* job_hi, int32_t n_jobs,
                      double* job_last_done, int32_t* job_info, void* stream) {
+  INTF_RANGE("intf_replay_jobs");
   if (!bt || !bt->scen || !bt->models || !buf || !table || !job_scen || !job_lo || !job_hi || !job_last_done ||
       !job_info || n_jobs < 0)
     return bad_input("intf_replay_jobs: null argument");
@@ -2001,6 +2005,7 @@ int intf_replay_jobs(const intf_batch* bt, const intf_table* table, const intf_r
 
 int intf_jobs_plan(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf, const intf_jobs* jobs,
                    void* stream) {
+  INTF_RANGE("intf_jobs_plan");
   if (!bt || !bt->scen || !table || !buf || !jobs || !jobs->todo_count || jobs->min_len < 1)
     return bad_input("intf_jobs_plan: bad argument");
   cudaStream_t st = as_stream(stream);
@@ -2026,6 +2031,7 @@ int intf_jobs_plan(const intf_batch* bt, const intf_table* table, const intf_rep
 
 int intf_jobs_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
                      const intf_jobs* jobs, int32_t n_todo, void* stream) {
+  INTF_RANGE("intf_jobs_replay");
   if (!bt || !bt->scen || !table || !buf || !jobs || (n_todo < 0 && !jobs->todo_count))
     return bad_input("intf_jobs_replay: bad argument");
   if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1)
@@ -2040,6 +2046,7 @@ int intf_jobs_replay(const intf_batch* bt, const intf_table* table, const intf_r
 }
 
 int intf_jobs_verify(const intf_batch* bt, const intf_replay_buffers* buf, const intf_jobs* jobs, void* stream) {
+  INTF_RANGE("intf_jobs_verify");
   if (!bt || !bt->scen || !buf || !jobs || !jobs->todo_count) return bad_input("intf_jobs_verify: bad argument");
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(jobs->todo_count, 0, sizeof(int32_t), st);
@@ -2052,6 +2059,7 @@ int intf_jobs_verify(const intf_batch* bt, const intf_replay_buffers* buf, const
 }
 
 int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf, void* stream) {
+  INTF_RANGE("intf_replay");
   if (!bt || !bt->scen || !bt->models || !buf || !table || bt->n_scen <= 0) return bad_input("intf_replay: null argument");
   if (buf->cap_max > kMaxCap || buf->cap_max < 1 || buf->seg_stride < 1 || buf->noise_k < 0)
     return bad_input("intf_replay: cap_max must be in [1, 8], seg_stride >= 1, noise_k >= 0");
@@ -2080,6 +2088,7 @@ int intf_replay(const intf_batch* bt, const intf_table* table, const intf_replay
 
 int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const double* warm_cutoff, int32_t* out_n,
                     int32_t* out_met, double* out_p, void* stream) {
+  INTF_RANGE("intf_slo_report");
   if (!bt || !bt->scen || !bt->models || !buf || !out_n || !out_met || !out_p || bt->n_scen <= 0)
     return bad_input("intf_slo_report: null argument");
   if (bt->max_req_cap > kSloBigReq) {  // long traces: grid-wide passes, one scenario at a time
@@ -2119,6 +2128,7 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
 int intf_features_predict(const intf_batch* bt, const intf_table* table, const intf_replay_buffers* buf,
                           const intf_predictor* preds, int32_t n_pred, int64_t slot_stride, double* X, double* y,
                           double* yhat, void* stream) {
+  INTF_RANGE("intf_features_predict");
   if (!bt || !bt->scen || !bt->models || !buf || !table || !y || (n_pred && !yhat) || bt->n_scen <= 0)
     return bad_input("intf_features_predict: bad argument");
   if (n_pred < 0 || n_pred > kMaxPred || (n_pred && !preds)) return bad_input("intf_features_predict: n_pred in [0,8]");

@@ -304,6 +304,7 @@ __global__ void k_scalar(int op, ScalarArgs a, double* __restrict__ out) {
 extern "C" {
 
 int intf_scalar(int32_t op, const uint64_t* args, int32_t n_args, double* out, int32_t n_out, void* stream) {
+  INTF_RANGE("intf_scalar");
   if (!args || !out || n_args < 0 || n_args > 72 || n_out < 1 || n_out > 64 || op < 0 || op > INTF_SCALAR_RLS)
     return bad_input("intf_scalar: bad argument");
   static thread_local double* mapped = nullptr;  // per host thread: 64 doubles of mapped pinned memory
@@ -329,6 +330,7 @@ int intf_scalar(int32_t op, const uint64_t* args, int32_t n_args, double* out, i
 
 int intf_noise_draws(uint64_t seed, double sigma, const int64_t* batch, const int64_t* seg, int64_t n, double* out,
                      void* stream) {
+  INTF_RANGE("intf_noise_draws");
   if (!batch || !seg || !out || n < 0) return bad_input("intf_noise_draws: bad argument");
   if (n == 0) return INTF_OK;
   k_noise<<<ceil_div(n, 128), 128, 0, as_stream(stream)>>>(seed, sigma, batch, seg, (long long)n, out);
@@ -337,6 +339,7 @@ int intf_noise_draws(uint64_t seed, double sigma, const int64_t* batch, const in
 
 int intf_slowdowns(const double* own, const double* colo, const double* beta, const double* noise, int64_t n,
                    double* out, void* stream) {
+  INTF_RANGE("intf_slowdowns");
   if (!own || !colo || !beta || !out || n < 0) return bad_input("intf_slowdowns: bad argument");
   if (n == 0) return INTF_OK;
   k_slowdowns<<<ceil_div(n, 128), 128, 0, as_stream(stream)>>>(own, colo, beta[0], beta[1], beta[2], noise,
@@ -345,6 +348,7 @@ int intf_slowdowns(const double* own, const double* colo, const double* beta, co
 }
 
 int intf_rng_stream(const uint32_t* words, int32_t n_words, int64_t n, int32_t uniform, double* out, void* stream) {
+  INTF_RANGE("intf_rng_stream");
   if (!words || !out || n_words < 1 || n_words > 8 || n < 0) return bad_input("intf_rng_stream: bad argument");
   k_normals<<<1, 32, 0, as_stream(stream)>>>(words, n_words, (long long)n, uniform, out);
   return launch_status("k_normals");
@@ -354,6 +358,7 @@ int intf_rng_stream(const uint32_t* words, int32_t n_words, int64_t n, int32_t u
 int intf_features_rows(const double* own, const int64_t* seg_off, const int32_t* nseg, const double* colo,
                        const double* measured, const double* profiled, int64_t n, const intf_predictor* preds,
                        int32_t n_pred, double* X, double* y, double* yhat, void* stream) {
+  INTF_RANGE("intf_features_rows");
   if (!own || !seg_off || !nseg || !colo || n < 0 || n_pred < 0 || n_pred > kMaxPredRows || (n_pred && !preds))
     return bad_input("intf_features_rows: bad argument");
   if (y && (!measured || !profiled)) return bad_input("intf_features_rows: y needs measured and profiled");
@@ -367,6 +372,7 @@ int intf_features_rows(const double* own, const int64_t* seg_off, const int32_t*
 }
 
 int intf_predict_rows(const double* X, int64_t n, const double* w, double* out, void* stream) {
+  INTF_RANGE("intf_predict_rows");
   if (!X || !w || !out || n < 0) return bad_input("intf_predict_rows: bad argument");
   if (n == 0) return INTF_OK;
   k_predict_rows<<<ceil_div(n, 256), 256, 0, as_stream(stream)>>>(X, (long long)n, w, out);
@@ -374,6 +380,7 @@ int intf_predict_rows(const double* X, int64_t n, const double* w, double* out, 
 }
 
 int intf_quantiles(const double* values, int64_t n, const double* ps, int32_t nq, double* out, void* stream) {
+  INTF_RANGE("intf_quantiles");
   if (!values || !ps || !out || n < 1 || nq < 1 || nq > kMaxQ) return bad_input("intf_quantiles: bad argument");
   k_quantiles<<<1, kSelThreads, 0, as_stream(stream)>>>(values, (long long)n, ps, nq, out);
   return launch_status("k_quantiles");
@@ -382,6 +389,7 @@ int intf_quantiles(const double* values, int64_t n, const double* ps, int32_t nq
 int intf_latency_report(const int32_t* group, const double* arrival, const double* completion, const uint8_t* met,
                         int64_t n, int32_t n_groups, double cutoff, int32_t* out_n, int32_t* out_met, double* out_p,
                         void* stream) {
+  INTF_RANGE("intf_latency_report");
   if (!group || !arrival || !completion || !met || !out_n || !out_met || !out_p || n < 0 || n_groups < 1)
     return bad_input("intf_latency_report: bad argument");
   k_latency_report<<<n_groups, kSelThreads, 0, as_stream(stream)>>>(group, arrival, completion, met, (long long)n,
