@@ -397,9 +397,12 @@ __device__ __forceinline__ void cand_stream_body(int bx, int by, int bz, const d
     __syncthreads();
     __shared__ unsigned red_v[kStreamThreads / 32][kStreamDec][2], red_i[kStreamThreads / 32][kStreamDec][2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned vc[kStreamDec], vf[kStreamDec], ic[kStreamDec], jf[kStreamDec];
+    // per thread: the running minimum as a float and its rank (a key only for
+    // the warp reduction: one FSETP + two selects per prediction)
+    float bc[kStreamDec], bf[kStreamDec];
+    unsigned ic[kStreamDec], jf[kStreamDec];
 #pragma unroll
-    for (int d = 0; d < kStreamDec; d++) vc[d] = vf[d] = ic[d] = jf[d] = 0xffffffffu;
+    for (int d = 0; d < kStreamDec; d++) bc[d] = bf[d] = INFINITY, ic[d] = jf[d] = 0xffffffffu;
 #pragma unroll
     for (int c = 0; c < kBestSpan; c++) {
       const long long r0 = (((long long)bx * kBestSpan + c) * blockDim.x + threadIdx.x) * 4;
@@ -426,17 +429,18 @@ __device__ __forceinline__ void cand_stream_body(int bx, int by, int bz, const d
 #pragma unroll
         for (int i = 0; i < 4; i++) {
           if (i < nl) {  // groups in ascending rank: strict < keeps the lowest rank on ties
-            const unsigned kc = f32_key(yc[i]), kf = f32_key(yf[i]);
-            if (kc < vc[d]) vc[d] = kc, ic[d] = (unsigned)(r0 + i);
-            if (kf < vf[d]) vf[d] = kf, jf[d] = (unsigned)(r0 + i);
+            if (yc[i] < bc[d]) bc[d] = yc[i], ic[d] = (unsigned)(r0 + i);
+            if (yf[i] < bf[d]) bf[d] = yf[i], jf[d] = (unsigned)(r0 + i);
           }
         }
       }
     }
     for (int d = 0; d < nd; d++) {
-      const unsigned wc = __reduce_min_sync(0xffffffffu, vc[d]), wf = __reduce_min_sync(0xffffffffu, vf[d]);
-      const unsigned xc = __reduce_min_sync(0xffffffffu, vc[d] == wc ? ic[d] : 0xffffffffu);
-      const unsigned xf = __reduce_min_sync(0xffffffffu, vf[d] == wf ? jf[d] : 0xffffffffu);
+      const unsigned vc = ic[d] == 0xffffffffu ? 0xffffffffu : f32_key(bc[d]);
+      const unsigned vf = jf[d] == 0xffffffffu ? 0xffffffffu : f32_key(bf[d]);
+      const unsigned wc = __reduce_min_sync(0xffffffffu, vc), wf = __reduce_min_sync(0xffffffffu, vf);
+      const unsigned xc = __reduce_min_sync(0xffffffffu, vc == wc ? ic[d] : 0xffffffffu);
+      const unsigned xf = __reduce_min_sync(0xffffffffu, vf == wf ? jf[d] : 0xffffffffu);
       if (lane == 0) {
         red_v[warp][d][0] = wc, red_i[warp][d][0] = xc;
         red_v[warp][d][1] = wf, red_i[warp][d][1] = xf;
