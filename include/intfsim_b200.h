@@ -290,6 +290,15 @@ int intf_candidate_best_step(const intf_table *table, int32_t cap, double alpha,
 int intf_best_candidates_host(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
                               int32_t n_dec, uint64_t *h_best, float *d_scratch, int64_t scratch_elems,
                               void *stream);
+/* The host-buffer call as a pipeline of decisions: call k scores from the
+ * features call k-1 built and builds call k+1's in the same launch (the
+ * fused step's prep blocks), so the feature build overlaps the scoring.
+ * *state counts the calls (0: build first; reset to 0 whenever table, cap or
+ * alpha change); d_scratch holds intf_best_candidates_host's floats plus one
+ * more candidate workspace.                                                 */
+int intf_best_candidates_host_pipelined(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
+                                        int32_t n_dec, uint64_t *h_best, float *d_scratch, int64_t scratch_elems,
+                                        int64_t *state, void *stream);
 
 /* Real scheduling decisions of a replayed batch: for every
  * batch slot (req_off + b), dec_rank = the multiset rank (enumeration of

@@ -2431,6 +2431,47 @@ int intf_score_decisions_ft(const intf_table* table, int32_t cap, const double* 
   return launch_status("k_score_decisions");
 }
 
+int intf_best_candidates_host_pipelined(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
+                                        int32_t n_dec, uint64_t* h_best, float* d_scratch, int64_t scratch_elems,
+                                        int64_t* state, void* stream) {
+  INTF_RANGE("intf_best_candidates_host_pipelined");
+  if (!table || !h_coefs || !h_best || !d_scratch || !state || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1)
+    return bad_input("intf_best_candidates_host_pipelined: bad argument");
+  int64_t ws = 0;
+  intf_candidate_workspace(table->n_rows, cap, &ws);
+  const long long n_coef = 2LL * n_dec * 2 * 7, n_best = 2LL * n_dec * table->n_rows;
+  if (scratch_elems < n_coef + 2 * n_best + 2 * ws)
+    return bad_input("intf_best_candidates_host_pipelined: scratch too small");
+  cudaStream_t st = as_stream(stream);
+  // scratch: [coefs as doubles][best keys as u64][workspace 0][workspace 1]; *state counts calls:
+  // call k reads the features call k-1 built into workspace k & 1 and builds call k+1's into the other
+  double* d_coefs = reinterpret_cast<double*>(d_scratch);
+  unsigned long long* d_best = reinterpret_cast<unsigned long long*>(d_scratch + n_coef);
+  float* d_ws[2] = {d_scratch + n_coef + 2 * n_best, d_scratch + n_coef + 2 * n_best + ws};
+  if (cudaMemcpyAsync(d_coefs, h_coefs, sizeof(double) * n_dec * 2 * 7, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return launch_status("copy coefs");
+  int rc;
+  const long long k = *state;
+  if (k == 0 && (rc = intf_candidate_prepare(table, cap, alpha, d_ws[0], ws, stream))) return rc;
+  cudaMemsetAsync(d_best, 0xff, sizeof(unsigned long long) * n_best, st);
+  float *cur = d_ws[k & 1], *nxt = d_ws[(k + 1) & 1];
+  switch (cap - 1) {
+    case 0: rc = launch_step<0>(table, cap, alpha, d_coefs, n_dec, nullptr, cur, nxt, st, d_best); break;
+    case 1: rc = launch_step<1>(table, cap, alpha, d_coefs, n_dec, nullptr, cur, nxt, st, d_best); break;
+    case 2: rc = launch_step<2>(table, cap, alpha, d_coefs, n_dec, nullptr, cur, nxt, st, d_best); break;
+    case 3: rc = launch_step<3>(table, cap, alpha, d_coefs, n_dec, nullptr, cur, nxt, st, d_best); break;
+    case 4: rc = launch_step<4>(table, cap, alpha, d_coefs, n_dec, nullptr, cur, nxt, st, d_best); break;
+    case 5: rc = launch_step<5>(table, cap, alpha, d_coefs, n_dec, nullptr, cur, nxt, st, d_best); break;
+    case 6: rc = launch_step<6>(table, cap, alpha, d_coefs, n_dec, nullptr, cur, nxt, st, d_best); break;
+    default: rc = launch_step<7>(table, cap, alpha, d_coefs, n_dec, nullptr, cur, nxt, st, d_best); break;
+  }
+  if (rc) return rc;
+  if (cudaMemcpyAsync(h_best, d_best, sizeof(unsigned long long) * n_best, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return launch_status("copy best candidates");
+  *state = k + 1;
+  return INTF_OK;
+}
+
 int intf_ols_stats(const double* X, const double* y, int64_t n, double* out, double* ws, void* stream) {
   INTF_RANGE("intf_ols_stats");
   if (!X || !y || !out || !ws || n < 0) return bad_input("intf_ols_stats: bad argument");

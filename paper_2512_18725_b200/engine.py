@@ -639,6 +639,19 @@ class CandidateScorer:
                                                          scratch.data_ptr(), scratch.numel(), stream_ptr()),
                    "intf_best_candidates_host")
 
+    def best_host_pipelined(self, coefs_host: np.ndarray, best_host: np.ndarray, scratch: torch.Tensor) -> None:
+        """best_host as a pipeline of decisions (intf_best_candidates_host_pipelined):
+        each call scores from the features the previous call built and builds
+        the next call's in the same launch; scratch holds
+        best_scratch_elems(n_dec) + one more workspace."""
+        n_dec = coefs_host.size // 14
+        if getattr(self, "_host_state", None) is None:
+            self._host_state = np.zeros(1, dtype=np.int64)
+        _abi.check(_abi.load().intf_best_candidates_host_pipelined(
+            ctypes.byref(self.dtable.struct), self.cap, self.alpha, coefs_host.ctypes.data, n_dec, best_host.ctypes.data,
+            scratch.data_ptr(), scratch.numel(), self._host_state.ctypes.data, stream_ptr()),
+            "intf_best_candidates_host_pipelined")
+
     def decode_best(self, keys, n_dec: int):
         """(value [n_dec][2][E] float32, multiset rank [n_dec][2][E] int64) of
         best keys (torch or numpy, int64 or uint64)."""

@@ -206,3 +206,23 @@ def test_real_decisions_from_replayed_sweep():
             n_dec += 1
         assert np.all(rank[ro + len(rows): ro + pipe.pb.scen[s].req_cap] == -1)
     assert n_dec > 10000
+
+
+def test_pipelined_host_best_calls_equal_single_calls():
+    """intf_best_candidates_host_pipelined (each call scores from the features
+    the previous call built and builds the next call's in the same launch)
+    returns the same keys as the one-shot host call, call after call."""
+    from paper_2512_18725_b200.sweep import c2_decision_coefs
+
+    sc = _scorer(4)
+    W = c2_decision_coefs(32, 0.5)
+    scr1 = torch.empty(sc.best_scratch_elems(8), dtype=torch.float32, device="cuda")
+    scr2 = torch.empty(sc.best_scratch_elems(8) + sc.ws_elems, dtype=torch.float32, device="cuda")
+    for k in range(4):
+        Wk = np.ascontiguousarray(W[8 * k: 8 * k + 8])
+        a = np.zeros(2 * 8 * sc.E, dtype=np.uint64)
+        b = np.zeros_like(a)
+        sc.best_host(Wk, a, scr1)
+        sc.best_host_pipelined(Wk, b, scr2)
+        torch.cuda.synchronize()
+        assert np.array_equal(a, b), k

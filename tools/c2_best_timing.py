@@ -43,3 +43,12 @@ for _ in range(K):
     sc.best_host(hc, hb, scr)
     torch.cuda.synchronize()
 print(f"best_host e2e: {1e6 * (time.perf_counter() - t0) / K:.1f} us/call")
+scr2 = torch.empty(sc.best_scratch_elems(32) + sc.ws_elems, dtype=torch.float32, device="cuda")
+for _ in range(10):
+    sc.best_host_pipelined(hc, hb, scr2)
+    torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(K):
+    sc.best_host_pipelined(hc, hb, scr2)
+    torch.cuda.synchronize()
+print(f"best_host_pipelined e2e: {1e6 * (time.perf_counter() - t0) / K:.1f} us/call")
