@@ -1690,8 +1690,8 @@ constexpr int kScenFitWarps = 4;
 
 // rls_init's P0 = np.linalg.inv(G) (`predict.py:126-131`) by the whole warp:
 // Gauss-Jordan with partial pivoting on [G | I], lane r < 7 holding row r in
-// registers (the pivot search is a warp arg-max, first index on ties like
-// LAPACK's idamax; the swap and the pivot-row broadcast are shuffles).  It
+// registers (the pivot search is a warp arg-max over the rows not yet used,
+// first lane on ties; the pivot row's live columns are broadcast by shuffles).  It
 // fails only on an exactly zero pivot -- numpy's LinAlgError: two identical
 // columns (and rows) of a symmetric G stay identical under the row operations
 // until one is the pivot row, which zeroes the other exactly -- and then
@@ -1705,14 +1705,14 @@ __device__ __noinline__ void warp_p0_inverse(const double* G, double* inv) {
     for (int j = 0; j < 7; j++) row[j] = G[r * 7 + j] + ((attempt && j == r) ? 1e-8 : 0.0);
 #pragma unroll
     for (int j = 0; j < 7; j++) row[7 + j] = (j == r) ? 1.0 : 0.0;
+    // rows stay in their lanes: the pivot lane of column c is remembered
+    // (no swap shuffles); eliminated entries are exact zeros (not updated)
+    bool used = lane >= 7;
+    int my_col = -1;
     bool ok = true;
 #pragma unroll
     for (int c = 0; c < 7; c++) {
-      double col = row[0];
-#pragma unroll
-      for (int j = 1; j < 7; j++) col = j == c ? row[j] : col;
-      // arg max |row[c]| over lanes c..6 (first lane on ties)
-      double best = (lane >= c && lane < 7) ? fabs(col) : -1.0;
+      double best = used ? -1.0 : fabs(row[c]);
       int piv = lane;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -1724,29 +1724,26 @@ __device__ __noinline__ void warp_p0_inverse(const double* G, double* inv) {
         ok = false;
         break;
       }
-      const int src = lane == c ? piv : (lane == piv ? c : lane);
       double p[14];
 #pragma unroll
-      for (int j = 0; j < 14; j++) {
-        row[j] = __shfl_sync(0xffffffffu, row[j], src);
-        p[j] = __shfl_sync(0xffffffffu, row[j], c);
-      }
-      double rc = row[0];
+      for (int j = c; j < 14; j++) p[j] = __shfl_sync(0xffffffffu, row[j], piv);
+      if (lane == piv) {
+        used = true;
+        my_col = c;
+      } else if (lane < 7) {
+        const double f = row[c] / p[c];
 #pragma unroll
-      for (int j = 1; j < 7; j++) rc = j == c ? row[j] : rc;
-      const double f = rc / p[c];
-      if (lane != c) {
-#pragma unroll
-        for (int j = 0; j < 14; j++) row[j] -= f * p[j];
+        for (int j = c + 1; j < 14; j++) row[j] -= f * p[j];
+        row[c] = 0.0;
       }
     }
     if (ok) {
       double d = row[0];
 #pragma unroll
-      for (int j = 1; j < 7; j++) d = j == r ? row[j] : d;
+      for (int j = 1; j < 7; j++) d = j == my_col ? row[j] : d;
       if (lane < 7) {
 #pragma unroll
-        for (int j = 0; j < 7; j++) inv[lane * 7 + j] = row[7 + j] / d;
+        for (int j = 0; j < 7; j++) inv[my_col * 7 + j] = row[7 + j] / d;
       }
       return;
     }
@@ -1822,8 +1819,24 @@ __global__ void __launch_bounds__(32 * kScenFitWarps, INTF_SCEN_FIT_MINB) k_scen
     double acc[kStats];
 #pragma unroll
     for (int i = 0; i < kStats; i++) acc[i] = 0.0;
-    if (valid)
-      for (long long row = base + lane; row < base + cut; row += 32) ols_acc_row(acc, Xm[m] + row * 6, Y[row]);
+    if (valid) {
+      // 4 rows in flight per lane: the loads of the next rows are issued before
+      // the 35-fma updates of the current ones (load latency, not fma, bounds this)
+      const double* Xb = Xm[m];
+      long long row = base + lane;
+      for (; row + 96 < base + cut; row += 128) {
+        double x[4][6], yv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+#pragma unroll
+          for (int i = 0; i < 6; i++) x[u][i] = Xb[(row + 32 * u) * 6 + i];
+          yv[u] = Y[row + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) ols_acc_row(acc, x[u], yv[u]);
+      }
+      for (; row < base + cut; row += 32) ols_acc_row(acc, Xb + row * 6, Y[row]);
+    }
     int t = 0;
 #pragma unroll
     for (int i = 0; i < 7; i++)
