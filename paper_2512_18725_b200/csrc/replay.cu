@@ -210,6 +210,64 @@ __global__ void k_merge_arrivals(const intf_scenario* __restrict__ scen, const i
   }
 }
 
+// The same merge with one block per SCENARIO for sweeps of many short
+// scenarios: the scenario's model lists are staged in shared memory once and
+// every element's rank is a binary search there (the per-model-list blocks
+// above re-read the other lists from L2 on every search step).  Scenarios
+// whose lists do not fit (kMergeSmem elements) take the global searches.
+constexpr int kMergeSmem = 4096;
+__global__ void __launch_bounds__(256) k_merge_arrivals_scen(const intf_scenario* __restrict__ scen, int n_scen,
+                                                              const intf_model* __restrict__ models,
+                                                              intf_replay_buffers B) {
+  __shared__ double sl[kMergeSmem];
+  __shared__ int soff[kMaxModels + 1];
+  for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
+    const intf_scenario S = scen[s];
+    if (B.status[s] & INTF_ST_OVERFLOW) continue;
+    if (threadIdx.x == 0) {
+      int o = 0;
+      for (int q = 0; q < S.n_models; q++) {
+        soff[q] = o;
+        const intf_model& Q = models[S.model_off + q];
+        o += min(B.n_list[S.model_off + q], Q.list_cap);
+      }
+      soff[S.n_models] = o;
+    }
+    __syncthreads();
+    const int total = soff[S.n_models];
+    const bool fits = total <= kMergeSmem;
+    if (fits) {
+      for (int q = 0; q < S.n_models; q++) {
+        const double* lt = B.list_t + models[S.model_off + q].list_off;
+        for (int j = threadIdx.x; j < soff[q + 1] - soff[q]; j += blockDim.x) sl[soff[q] + j] = lt[j];
+      }
+    }
+    __syncthreads();
+    for (int q = 0; q < S.n_models; q++) {
+      const int g = S.model_off + q;
+      const intf_model& M = models[g];
+      const int n = soff[q + 1] - soff[q];
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double t = fits ? sl[soff[q] + j] : B.list_t[M.list_off + j];
+        int pos = j;
+        for (int r = 0; r < S.n_models; r++) {
+          if (r == q) continue;
+          const intf_model& Q = models[S.model_off + r];
+          const int nq = soff[r + 1] - soff[r];
+          pos += fits ? count_before(sl + soff[r], nq, t, Q.name_rank < M.name_rank)
+                      : count_before(B.list_t + Q.list_off, nq, t, Q.name_rank < M.name_rank);
+        }
+        if (pos < S.req_cap) {
+          B.list_rid[M.list_off + j] = pos;
+          B.arr_t[S.req_off + pos] = t;
+          B.arr_model[S.req_off + pos] = q;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- split caller-supplied merged arrivals into per-model lists (serial
 // per scenario; only for externally supplied traces).
 __global__ void k_split_arrivals(const intf_scenario* __restrict__ scen, int n_scen,
@@ -1959,6 +2017,11 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
     k_fill_gaps<<<dim3(ceil_div(ceil_div(bt->max_list_cap, kScanChunk), 128), y, ceil_div(m, y)), 128, 0, st>>>(
         bt->scen, bt->models, bt->n_models, *buf);
     if ((rc = launch_status("k_fill_gaps"))) return rc;
+  }
+  if (bt->n_scen >= kPerScenarioMin && bt->max_list_cap < kLongForm) {  // sweeps of short scenarios
+    k_merge_arrivals_scen<<<bt->n_scen < 65535 ? bt->n_scen : 65535, 256, 0, st>>>(bt->scen, bt->n_scen, bt->models,
+                                                                                 *buf);
+    return launch_status("k_merge_arrivals_scen");
   }
   k_merge_arrivals<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
   return launch_status("k_merge_arrivals");
