@@ -225,9 +225,11 @@ class ReplayPipeline:
 
 
 def run_batch(specs, table: _pack.TableArrays, preds=(), slo=True, warmup_fraction=0.0, arrivals=None,
-              seg_stride: int = 64, max_retries: int = 4):
+              seg_stride: int = 64, max_retries: int = 4, fetch: bool = True):
     """Run a batch of scenarios to completion, growing capacities on
-    overflow; returns (pipeline, fetched host dict)."""
+    overflow; returns (pipeline, fetched host dict) -- with fetch=False only
+    the per-scenario counters (n_req, n_batches, n_segments, n_reseats,
+    status) are copied and the results stay on the device."""
     scale = 1.0
     list_caps = None
     if arrivals is not None:
@@ -255,6 +257,10 @@ def run_batch(specs, table: _pack.TableArrays, preds=(), slo=True, warmup_fracti
         if np.any(st & _abi.ST_SEG_STRIDE):
             seg_stride *= 4
             continue
+        if not fetch:
+            S = pipe.pb.n_scen
+            return pipe, {k: pipe.t[k][:S].cpu().numpy() for k in ("n_req", "n_batches", "n_segments", "n_reseats",
+                                                                   "status")}
         return pipe, pipe.fetch()
     raise RuntimeError("replay buffers still overflowing after retries")
 
