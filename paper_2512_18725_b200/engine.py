@@ -17,6 +17,7 @@ from . import _abi, _pack
 
 _TORCH_DT = {np.float64: torch.float64, np.int32: torch.int32, np.uint8: torch.uint8, np.float32: torch.float32,
              np.int64: torch.int64}
+_NP_DT = {v: np.dtype(k) for k, v in _TORCH_DT.items()}
 
 
 def require_cuda() -> torch.device:
@@ -180,18 +181,31 @@ class ReplayPipeline:
     SCRATCH = ("slot_seg", "noise_tab", "mb_t", "mb_info", "n_mb", "slo_ws", "form_ws", "order")
 
     def fetch(self, scratch: bool = False) -> dict:
-        """Copy the result buffers to host numpy (scratch buffers too if asked)."""
-        h = {k: v.cpu().numpy() for k, v in self.t.items() if scratch or k not in self.SCRATCH}
-        h["Y"] = self.Y.cpu().numpy()
-        h["Yhat"] = self.Yhat.cpu().numpy().reshape(-1, self.slot_stride)
-        h["X"] = self.X.cpu().numpy().reshape(-1, self.slot_stride, 6)
-        h["slo_n"] = self.slo_n.cpu().numpy()
-        h["slo_met"] = self.slo_met.cpu().numpy()
-        h["slo_p"] = self.slo_p.cpu().numpy().reshape(-1, 3)
+        """Copy the result buffers to host numpy (scratch buffers too if asked)
+        in ONE device-to-host transfer: the buffers are packed byte-wise on
+        the device (stream-ordered copies) and split on the host."""
+        src = {k: v for k, v in self.t.items() if scratch or k not in self.SCRATCH}
+        src.update(Y=self.Y, Yhat=self.Yhat, X=self.X, slo_n=self.slo_n, slo_met=self.slo_met, slo_p=self.slo_p)
         if self.evaluate is not None:
-            h["eval_report"] = self.eval_report.cpu().numpy().reshape(-1, 3, 6)
-            h["eval_params"] = self.eval_params.cpu().numpy().reshape(-1, 3, 7)
-            st = self.eval_status.cpu().numpy()
+            src.update(eval_report=self.eval_report, eval_params=self.eval_params, eval_status=self.eval_status)
+        parts, offs, off = [], {}, 0
+        for k, v in src.items():
+            b = v.reshape(-1).view(torch.uint8)
+            pad = (-b.numel()) % 8  # keep every buffer 8-byte aligned in the packed copy
+            parts.append(b)
+            if pad:
+                parts.append(torch.zeros(pad, dtype=torch.uint8, device=self.dev))
+            offs[k] = (off, v.numel(), v.dtype)
+            off += b.numel() + pad
+        flat = torch.cat(parts).cpu().numpy()
+        h = {k: flat[o:o + n * t.itemsize].view(_NP_DT[t]) for k, (o, n, t) in offs.items()}
+        h["Yhat"] = h["Yhat"].reshape(-1, self.slot_stride)
+        h["X"] = h["X"].reshape(-1, self.slot_stride, 6)
+        h["slo_p"] = h["slo_p"].reshape(-1, 3)
+        if self.evaluate is not None:
+            h["eval_report"] = h["eval_report"].reshape(-1, 3, 6)
+            h["eval_params"] = h["eval_params"].reshape(-1, 3, 7)
+            st = h["eval_status"]
             h["eval_status"] = st[: len(st) // 2] | (st[len(st) // 2:] << 8)
         return h
 
