@@ -184,3 +184,18 @@ def test_rls_init_p0_near_collinear_matches_numpy_inv(eps):
     # the device's Z^T Z sums in another order: P0 moves by ~cond(G) * eps_64 relative
     tol = {1e-5: 1e-3, 1e-6: 3e-2, 0.0: 1e-4}[eps]
     assert np.linalg.norm(st.P - ref) / np.linalg.norm(ref) < tol
+
+
+def test_batched_drift_equals_per_seed():
+    """drift_experiments over several bases (one batched device flow) equals
+    drift_experiment per base, bit for bit."""
+    import paper_2512_18725_b200 as p
+    from paper_2512_18725_b200 import experiments as ex
+
+    table = p.gen_synthetic_profiles()
+    bases = [ex.default_drift_base(table, s) for s in (3, 4, 5)]
+    together = ex.drift_experiments(bases, table)
+    for b, cells in zip(bases, together):
+        alone = ex.drift_experiment(b, table)
+        assert [(c.dataset, c.method, c.n_samples) for c in cells] == [(c.dataset, c.method, c.n_samples) for c in alone]
+        np.testing.assert_array_equal([c.mse for c in cells], [c.mse for c in alone])
