@@ -1264,88 +1264,149 @@ __global__ void __launch_bounds__(kBigThreads) k_plan_p4(const intf_scenario* __
   }
 }
 
-__global__ void __launch_bounds__(kBigThreads) k_jobs_verify_big(const intf_scenario* __restrict__ scen,
+// Verify of a long trace (`replay_segmented_host`'s check, block-parallel):
+// boundary j fails iff the previous job (each job's last completion from its
+// own start) ends after job j's first formation; failing jobs join the kept
+// job before them (whole runs at once), and a holding boundary behind a
+// merged job is checked again next pass.  Tiles of kVerR rows x kVerThreads
+// jobs (job = base + row * kVerThreads + thread: coalesced loads and
+// stores), every field of a thread's jobs held in registers (all loads
+// issued together), the kept jobs ranked by warp ballots + one warp scan of
+// the per-(row, warp) counts, and compacted IN PLACE: a kept job's rank never
+// exceeds its index, so a tile only overwrites slots below its own first job
+// (the slot just below holds either that same job or a later tile's, not yet
+// written), and every read of the tile precedes the barrier before its writes.
+constexpr int kVerThreads = 512, kVerR = 12, kVerWarps = kVerThreads / 32;
+constexpr int kVerWords = kVerR * kVerWarps;  // one ballot word per (row, warp)
+static_assert(kVerWords <= 32 * 8, "k_jobs_verify_big: one warp scans the (row, warp) counts, <= 8 per lane");
+__global__ void __launch_bounds__(kVerThreads) k_jobs_verify_big(const intf_scenario* __restrict__ scen,
                                                                  intf_replay_buffers B, intf_jobs J) {
-  __shared__ int shi[kBigThreads];
-  __shared__ int todo_base, any_fail;
+  __shared__ unsigned fwd[kVerWords];  // failing boundaries, bit = tile position & 31
+  __shared__ int koff[kVerWords];      // kept jobs before each (row, warp) word in the tile
+  __shared__ int tile_kept, next_fails, any_fail, tot_segs, tot_res, last_hi;
   const int s = blockIdx.x;
   const intf_scenario& S = scen[s];
   if (S.req_cap < kBigJobs) return;
-  const int t = threadIdx.x;
-  const int n = J.n_jobs[s], joff = J.joff[s], ro = S.req_off;
+  const int n = J.n_jobs[s], joff = J.joff[s];
   if (n == 0) return;
-  if (t == 0) any_fail = 0;
-  const int R = (n + kBigThreads - 1) / kBigThreads, j0 = t * R, j1 = min(n, j0 + R);
-  // boundary j fails iff the previous job (each job's last completion from its
-  // own start) ends after job j's first formation; failing jobs join the kept
-  // job before them (whole runs at once, as replay_segmented_host); a holding
-  // boundary behind a merged job is checked again next pass
-  auto fails = [&](int j) -> bool {
-    if (j == 0) return false;
-    const int sj = joff + j;
-    return !(J.hi[sj] <= J.lo[sj] || J.last[sj - 1] <= B.b_formed[ro + J.lo[sj]]);
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, ro = S.req_off;
+  const unsigned lt = (1u << lane) - 1u;
+  if (t == 0) {
+    last_hi = J.hi[joff + n - 1];
+    tot_segs = tot_res = any_fail = 0;
+  }
+  auto fails = [&](int j, int l, int h, double pv) -> bool {
+    return j > 0 && !(h <= l || pv <= B.b_formed[ro + l]);
   };
-  __shared__ int last_hi;
-  if (t == 0) last_hi = J.hi[joff + n - 1];
-  int cnt = 0;
-  for (int j = j0; j < j1; j++) cnt += fails(j) ? 0 : 1;
-  int w = 0;
-  int r = block_excl_sum(cnt, shi, &w);
-  // compact into the shadow (6 doubles per slot), then copy back
-  double* sh = J.scratch + 6ll * joff;
-  bool fail_seen = false;
-  for (int j = j0; j < j1; j++) {
-    const int sj = joff + j;
-    if (fails(j)) {
-      fail_seen = true;
-      continue;
+  int w = 0;  // kept jobs so far (block-uniform)
+  int st = 0, segs = 0, res = 0;
+  for (int base = 0; base < n; base += kVerThreads * kVerR) {
+    const int tn = min(n - base, kVerThreads * kVerR);
+    int lo[kVerR], i0[kVerR], i1[kVerR], i2[kVerR];
+    double last[kVerR];
+    unsigned fm = 0u, vm = 0u;  // bit k: row k's job fails / exists
+#pragma unroll
+    for (int k = 0; k < kVerR; k++) {
+      const int p = k * kVerThreads + t, sj = joff + base + p;
+      if (p < tn) {
+        lo[k] = J.lo[sj];
+        const int h = J.hi[sj];
+        const double pv = base + p > 0 ? J.last[sj - 1] : -INFINITY;
+        last[k] = J.last[sj];
+        i0[k] = J.info[3 * sj];
+        i1[k] = J.info[3 * sj + 1];
+        i2[k] = J.info[3 * sj + 2];
+        vm |= 1u << k;
+        if (fails(base + p, lo[k], h, pv)) fm |= 1u << k;
+      }
     }
-    const bool absorbs = j + 1 < n && fails(j + 1);
-    double* d = sh + 6ll * r;
-    d[0] = J.lo[sj];
-    d[1] = 0.0;  // hi: the next kept job's lo (set below)
-    d[2] = J.last[sj];
-    d[3] = J.info[3 * sj];
-    d[4] = J.info[3 * sj + 1];
-    d[5] = absorbs ? -1.0 - (double)J.info[3 * sj + 2] : (double)J.info[3 * sj + 2];  // sign = dirty
-    r++;
-  }
-  if (fail_seen) atomicOr(&any_fail, 1);
-  __syncthreads();
-  int st = 0, segs = 0, res = 0, nd = 0;
-  for (int j = t; j < w; j += kBigThreads) {
-    const double* d = sh + 6ll * j;
-    const int dj = joff + j;
-    const bool dirty = d[5] < 0.0;
-    J.lo[dj] = (int)d[0];
-    J.hi[dj] = j + 1 < w ? (int)sh[6ll * (j + 1)] : last_hi;
-    J.last[dj] = d[2];
-    J.info[3 * dj] = (int)d[3];
-    J.info[3 * dj + 1] = (int)d[4];
-    J.info[3 * dj + 2] = dirty ? (int)(-1.0 - d[5]) : (int)d[5];
-    J.dirty[dj] = dirty ? 1 : 0;
-    st |= (int)d[3];
-    segs += (int)d[4];
-    res += dirty ? 0 : (int)d[5];
-    nd += dirty ? 1 : 0;
-  }
-  if (t == 0) J.n_jobs[s] = w;
-  if (any_fail) {  // queue the merged (dirty) jobs
-    int ndt = 0;
-    int base = block_excl_sum(nd, shi, &ndt);
-    if (t == 0) todo_base = ndt ? atomicAdd(J.todo_count, ndt) : 0;
+    if (t == 0) {  // the next tile's first boundary (the absorb flag of this tile's last job)
+      const int j = base + tn, sj = joff + j;
+      next_fails = j < n && fails(j, J.lo[sj], J.hi[sj], J.last[sj - 1]);
+    }
+#pragma unroll
+    for (int k = 0; k < kVerR; k++) {
+      const unsigned bf = __ballot_sync(0xffffffffu, (fm >> k) & 1u);
+      const unsigned bk = __ballot_sync(0xffffffffu, ((vm & ~fm) >> k) & 1u);
+      if (lane == 0) {
+        fwd[k * kVerWarps + wid] = bf;
+        koff[k * kVerWarps + wid] = __popc(bk);
+      }
+    }
+    __syncthreads();  // (every read of the tile done)
+    if (wid == 0) {  // exclusive scan of the per-word kept counts, in job order
+      constexpr int per = (kVerWords + 31) / 32;
+      int c[per], sum = 0;
+      unsigned f = 0u;
+#pragma unroll
+      for (int i = 0; i < per; i++) {
+        const int q = lane * per + i;
+        c[i] = q < kVerWords ? koff[q] : 0;
+        f |= q < kVerWords ? fwd[q] : 0u;
+        sum += c[i];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int i = 0; i < per; i++) {
+        const int q = lane * per + i;
+        if (q < kVerWords) koff[q] = run;
+        run += c[i];
+      }
+      if (lane == 31) tile_kept = incl;
+      if (__any_sync(0xffffffffu, f != 0u) && lane == 0) any_fail = 1;
+    }
     __syncthreads();
-    for (int j = t; j < w; j += kBigThreads)
-      if (J.dirty[joff + j]) J.todo[todo_base + base++] = joff + j;
-    return;
+#pragma unroll
+    for (int k = 0; k < kVerR; k++) {
+      const int p = k * kVerThreads + t, word = k * kVerWarps + wid;
+      const bool kept = ((vm & ~fm) >> k) & 1u;
+      const unsigned bk = __ballot_sync(0xffffffffu, kept);
+      // the boundary after job p: the next lane, the next word's bit 0, or the next tile
+      const bool absorbs = p + 1 < tn ? ((fwd[(p + 1) >> 5] >> ((p + 1) & 31)) & 1u) != 0u : next_fails != 0;
+      const bool dirty = kept && absorbs;
+      const int r = w + koff[word] + __popc(bk & lt);
+      if (kept) {
+        const int dj = joff + r;
+        J.lo[dj] = lo[k];
+        J.last[dj] = last[k];
+        J.info[3 * dj] = i0[k];
+        J.info[3 * dj + 1] = i1[k];
+        J.info[3 * dj + 2] = i2[k];
+        J.dirty[dj] = dirty ? 1 : 0;
+        st |= i0[k];
+        segs += i1[k];
+        res += dirty ? 0 : i2[k];
+      }
+      // a dirty job exists iff some boundary failed: queue it now (replay order is immaterial)
+      const unsigned bd = __ballot_sync(0xffffffffu, dirty);
+      if (bd) {
+        int at = 0;
+        if (lane == 0) at = atomicAdd(J.todo_count, __popc(bd));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (dirty) J.todo[at + __popc(bd & lt)] = joff + r;
+      }
+    }
+    w += tile_kept;
+    __syncthreads();  // the tile's writes land before the next tile reads the slot below it
   }
+  // hi of each kept job = lo of the next kept job
+  for (int q = t; q < w; q += kVerThreads) J.hi[joff + q] = q + 1 < w ? J.lo[joff + q + 1] : last_hi;
+  if (t == 0) J.n_jobs[s] = w;
+  if (any_fail) return;  // merged jobs queued: totals after the next pass
   // every boundary holds: per-scenario totals
-  atomicOr(&B.status[s], st);
-  __shared__ int tot_segs, tot_res;
-  if (t == 0) tot_segs = tot_res = 0;
-  __syncthreads();
-  atomicAdd(&tot_segs, segs);
-  atomicAdd(&tot_res, res);
+  const int st_w = (int)__reduce_or_sync(0xffffffffu, (unsigned)st);
+  const int segs_w = __reduce_add_sync(0xffffffffu, segs), res_w = __reduce_add_sync(0xffffffffu, res);
+  if (lane == 0) {
+    if (st_w) atomicOr(&B.status[s], st_w);
+    atomicAdd(&tot_segs, segs_w);
+    atomicAdd(&tot_res, res_w);
+  }
   __syncthreads();
   if (t == 0) {
     B.n_segments[s] = tot_segs;
@@ -2117,7 +2178,7 @@ int intf_jobs_verify(const intf_batch* bt, const intf_replay_buffers* buf, const
   int rc = launch_status("k_jobs_verify");
   if (rc || bt->max_req_cap < kBigJobs) return rc;
   if (!jobs->scratch) return bad_input("intf_jobs_verify: long traces need jobs->scratch");
-  k_jobs_verify_big<<<bt->n_scen, kBigThreads, 0, st>>>(bt->scen, *buf, *jobs);
+  k_jobs_verify_big<<<bt->n_scen, kVerThreads, 0, st>>>(bt->scen, *buf, *jobs);
   return launch_status("k_jobs_verify_big");
 }
 
