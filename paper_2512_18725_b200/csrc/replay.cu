@@ -1511,13 +1511,29 @@ __global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen
 }
 
 // ---- K3: SLO records + per-model nearest-rank percentiles, one block per
-// scenario.  Percentiles by 8-pass MSB radix select on the latency bits
-// (latency >= 0, so IEEE bit order == numeric order); three order
-// statistics per model share each pass's histograms (shared memory).
+// scenario.  Percentiles by MSB radix select on v = key - base, the latency
+// bits (latency >= 0, so IEEE bit order == numeric order) offset by the
+// scenario's smallest key: base = (min of the keys' high words) << 32 and
+// v < 2^T with T = 32 + bit length of the high words' span, so the first
+// 8-bit digit (bits T-1..T-8) spreads over the range actually used (starting
+// at bit 63, one pass would hold every record in one bin: latencies on both
+// sides of 2 ms already differ in bit 62).  The first pass's histogram is
+// shared by the three quantiles (same empty prefix); in the cached path the
+// records still matching a quantile's prefix are compacted after each pass,
+// and once every (model, quantile)'s selected bin holds <= kSloFinish records
+// one warp per (model, quantile) ranks them directly.
 constexpr int kSloThreads = 256;
 constexpr int kSloGroup = 4;          // models per radix pass group (smem: 12 KB of histograms)
 constexpr int kSloBigReq = 1 << 16;  // above this request capacity: grid-wide SLO passes
-constexpr int kSloCache = 2048;      // records whose latency keys k_slo keeps in shared memory (26 KB with indices)
+#ifndef INTF_SLO_CACHE
+#define INTF_SLO_CACHE 2048
+#endif
+constexpr int kSloCache = INTF_SLO_CACHE;  // records whose latency keys k_slo keeps in shared memory (26 KB with indices)
+constexpr int kSloFinish = 32;       // a selected bin this small is ranked by one warp
+#ifndef INTF_SLO_UNROLL
+#define INTF_SLO_UNROLL 4
+#endif
+constexpr int kSloUnroll = INTF_SLO_UNROLL;  // records per thread whose loads are issued together
 
 __device__ __forceinline__ unsigned long long lat_key(double v) {
   unsigned long long u = (unsigned long long)__double_as_longlong(v);
@@ -1526,6 +1542,17 @@ __device__ __forceinline__ unsigned long long lat_key(double v) {
 __device__ __forceinline__ double key_lat(unsigned long long k) {
   unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)u);
+}
+// digit of v at [shift, shift + 8) (shift < 0: the low bits, left-aligned)
+__device__ __forceinline__ unsigned slo_digit(unsigned long long v, int shift) {
+  return (unsigned)((shift >= 0 ? v >> shift : v << -shift) & 0xffull);
+}
+__device__ __forceinline__ unsigned long long slo_put(unsigned d, int shift) {
+  return shift >= 0 ? (unsigned long long)d << shift : (unsigned long long)(d >> -shift);
+}
+// v agrees with prefix pv on every bit at or above `from` (from >= 64: no bits)
+__device__ __forceinline__ bool slo_match(unsigned long long v, unsigned long long pv, int from) {
+  return from >= 64 || ((v ^ pv) >> (from > 0 ? from : 0)) == 0ull;
 }
 
 __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __restrict__ scen,
@@ -1541,23 +1568,78 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
   __shared__ unsigned long long prefix[kSloGroup][3];
   __shared__ int rank_left[kSloGroup][3];
   __shared__ int use_all;
+  __shared__ unsigned hi_min, hi_max;
+  __shared__ unsigned long long fin[kSloThreads / 32][kSloFinish];
   if ((B.status[s] & (INTF_ST_OVERFLOW | INTF_ST_SEG_STRIDE)) || S.n_models > kMaxModels) return;
   const double cutoff = warm_cutoff ? warm_cutoff[s] : -INFINITY;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int m = threadIdx.x; m < kMaxModels; m += blockDim.x) cnt_n[m] = cnt_met[m] = 0;
-  if (threadIdx.x == 0) use_all = 0;
+  if (threadIdx.x == 0) {
+    use_all = 0;
+    hi_min = 0xffffffffu;
+    hi_max = 0u;
+  }
   __syncthreads();
-  // pass 0: records (`simcore.py:264-279`) and counts
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int b = B.r_batch[ro + i];
-    const double at = B.arr_t[ro + i];
-    const int m = B.arr_model[ro + i];
-    const double lat = B.b_completion[ro + b] - at;
-    const bool met = lat <= models[S.model_off + m].slo_ms;
-    B.r_slo_met[ro + i] = met;
-    if (at >= cutoff) {
-      atomicAdd(&cnt_n[m], 1);
-      atomicAdd(&cnt_met[m], met ? 1 : 0);
+  // latency keys (and model ids) of the trimmed records, cached in shared
+  // memory when they fit (kSloCache records): the radix passes re-read shared
+  // memory, not four global arrays.  Cached path: the records still matching
+  // one of the group's quantile prefixes, compacted after every radix pass
+  // (double-buffered index lists), so later passes touch a few percent.
+  extern __shared__ unsigned long long kcache[];
+  unsigned char* mcache = reinterpret_cast<unsigned char*>(kcache + kSloCache);
+  unsigned short* cand[2] = {reinterpret_cast<unsigned short*>(mcache + kSloCache),
+                             reinterpret_cast<unsigned short*>(mcache + kSloCache) + kSloCache};
+  __shared__ int n_cand[2];
+  __shared__ int unresolved[2];  // by pass parity: pass p's check and pass p+1's reset never share a word
+  const bool cached = n <= kSloCache;
+  // one pass over the records (`simcore.py:264-279`): SLO flags, counts, key
+  // cache, key range; kSloUnroll records per thread with their loads together
+  unsigned kmin = 0xffffffffu, kmax = 0u;
+  for (int i0 = 0; i0 < n; i0 += kSloUnroll * kSloThreads) {
+    int bb[kSloUnroll], mm[kSloUnroll];
+    double at[kSloUnroll], bc[kSloUnroll];
+#pragma unroll
+    for (int u = 0; u < kSloUnroll; u++) {
+      const int i = i0 + u * kSloThreads + threadIdx.x;
+      if (i < n) {
+        bb[u] = B.r_batch[ro + i];
+        at[u] = B.arr_t[ro + i];
+        mm[u] = B.arr_model[ro + i];
+      }
     }
+#pragma unroll
+    for (int u = 0; u < kSloUnroll; u++) {
+      const int i = i0 + u * kSloThreads + threadIdx.x;
+      if (i < n) bc[u] = B.b_completion[ro + bb[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < kSloUnroll; u++) {
+      const int i = i0 + u * kSloThreads + threadIdx.x;
+      if (i < n) {
+        const double lat = bc[u] - at[u];
+        const bool met = lat <= models[S.model_off + mm[u]].slo_ms;
+        B.r_slo_met[ro + i] = met;
+        const bool in = at[u] >= cutoff;
+        if (in) {
+          atomicAdd(&cnt_n[mm[u]], 1);
+          atomicAdd(&cnt_met[mm[u]], met ? 1 : 0);
+        }
+        const unsigned long long key = lat_key(lat);
+        if (cached) {
+          kcache[i] = key;
+          mcache[i] = in ? (unsigned char)mm[u] : (unsigned char)255;
+        }
+        const unsigned hk = (unsigned)(key >> 32);
+        kmin = hk < kmin ? hk : kmin;
+        kmax = hk > kmax ? hk : kmax;
+      }
+    }
+  }
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (lane == 0 && kmin <= kmax) {
+    atomicMin(&hi_min, kmin);
+    atomicMax(&hi_max, kmax);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1574,6 +1656,7 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
       const int m = B.arr_model[ro + i];
       atomicAdd(&cnt_n[m], 1);
       atomicAdd(&cnt_met[m], B.r_slo_met[ro + i] ? 1 : 0);
+      if (cached) mcache[i] = (unsigned char)m;
     }
     __syncthreads();
   }
@@ -1583,31 +1666,9 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
     out_met[S.model_off + m] = cnt_met[m];
   }
   const double pq[3] = {50.0, 95.0, 99.0};
-  // latency keys (and model ids) of the trimmed records, cached in shared
-  // memory once when they fit (kSloCache records), so the 8 radix passes
-  // re-read shared memory instead of four global arrays
-  extern __shared__ unsigned long long kcache[];
-  unsigned char* mcache = reinterpret_cast<unsigned char*>(kcache + kSloCache);
-  // cached path: the records still matching one of the group's quantile
-  // prefixes, compacted after every radix pass (double-buffered index lists),
-  // so the later passes touch a few percent of the records instead of all
-  unsigned short* cand[2] = {reinterpret_cast<unsigned short*>(mcache + kSloCache),
-                             reinterpret_cast<unsigned short*>(mcache + kSloCache) + kSloCache};
-  __shared__ int n_cand[2];
-  // a (model, quantile) whose selected digit holds ONE record is resolved: that
-  // record's key is the answer; when all are, the remaining passes are skipped
-  __shared__ int unresolved[2];  // by pass parity: pass p's check and pass p+1's reset never share a word
-  __shared__ unsigned char resolved[kSloGroup][3];
-  __shared__ unsigned long long found[kSloGroup][3];
-  const bool cached = n <= kSloCache;
-  if (cached) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double at = B.arr_t[ro + i];
-      const bool in = at >= cut;
-      kcache[i] = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
-      mcache[i] = in ? (unsigned char)B.arr_model[ro + i] : (unsigned char)255;
-    }
-  }
+  const unsigned long long base = n > 0 ? (unsigned long long)hi_min << 32 : 0ull;
+  const unsigned span = n > 0 ? hi_max - hi_min : 0u;
+  const int T = 32 + (span ? 32 - __clz(span) : 0);  // every v = key - base < 2^T
   for (int g0 = 0; g0 < S.n_models; g0 += kSloGroup) {
     const int gm = min(kSloGroup, S.n_models - g0);
     if (threadIdx.x < gm * 3) {
@@ -1626,16 +1687,18 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
         const int m = (int)mcache[i] - g0;
         const bool want = m >= 0 && m < gm;
         const unsigned act = __activemask(), bal = __ballot_sync(act, want);
-        const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
-        int base = 0;
-        if (lane == leader && bal) base = atomicAdd(&n_cand[0], __popc(bal));
-        base = __shfl_sync(act, base, leader);
-        if (want) cand[0][base + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
+        const int leader = __ffs(act) - 1;
+        int cb = 0;
+        if (lane == leader && bal) cb = atomicAdd(&n_cand[0], __popc(bal));
+        cb = __shfl_sync(act, cb, leader);
+        if (want) cand[0][cb + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
       }
     }
-    for (int pass = 0; pass < 8; pass++) {
-      const int shift = 56 - 8 * pass;
-      for (int k = threadIdx.x; k < gm * 3 * 256; k += blockDim.x) (&hist[0][0][0])[k] = 0u;  // used rows only
+    int pass = 0;
+    for (int shift = T - 8; shift > -8; shift -= 8, pass++) {
+      const int nq = pass == 0 ? 1 : 3;  // the first pass: one histogram per model (every prefix empty)
+      for (int k = threadIdx.x; k < gm * 3 * 256; k += blockDim.x)
+        if ((k >> 8) % 3 < nq) (&hist[0][0][0])[k] = 0u;  // rows in use only
       if (threadIdx.x == 0) {
         n_cand[(pass + 1) & 1] = 0;
         unresolved[pass & 1] = 0;
@@ -1658,19 +1721,21 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
           if (!(at >= cut)) continue;
           key = lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at);
         }
-        const unsigned int d = (unsigned int)(key >> shift) & 0xffu;
+        const unsigned long long v = key - base;
+        const unsigned d = slo_digit(v, shift);
+        if (pass == 0) {
+          atomicAdd(&hist[m][0][d], 1u);
+        } else {
 #pragma unroll
-        for (int q = 0; q < 3; q++) {
-          const bool match = pass == 0 || ((key ^ prefix[m][q]) >> (shift + 8)) == 0ull;
-          if (match) atomicAdd(&hist[m][q][d], 1u);
+          for (int q = 0; q < 3; q++)
+            if (slo_match(v, prefix[m][q], shift + 8)) atomicAdd(&hist[m][q][d], 1u);
         }
       }
       __syncthreads();
       // digit selection: one warp per (model, quantile), lanes scan 8 bins each
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       for (int t = warp; t < gm * 3; t += kSloThreads / 32) {
         const int mm = t / 3, q = t % 3;
-        const unsigned int* h = hist[mm][q];
+        const unsigned int* h = hist[mm][pass == 0 ? 0 : q];
         int c8[8], sum = 0;
 #pragma unroll
         for (int j = 0; j < 8; j++) {
@@ -1680,8 +1745,8 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
         int incl = sum;  // inclusive scan over lanes
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
         }
         const int excl = incl - sum, left = rank_left[mm][q];
         // the lane whose bins contain rank `left` (the last lane if ranks run out,
@@ -1699,36 +1764,65 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
             l -= c8[j];
           }
           rank_left[mm][q] = l;
-          prefix[mm][q] |= (unsigned long long)d << shift;
-          resolved[mm][q] = held == 1;
-          if (held != 1) atomicAdd(&unresolved[pass & 1], 1);
+          prefix[mm][q] |= slo_put(d, shift);
+          if (held > kSloFinish) atomicAdd(&unresolved[pass & 1], 1);
         }
       }
       __syncthreads();
-      if (cached && pass < 7) {  // keep the records that still match one of their model's prefixes
+      if (cached && shift > 0) {  // keep the records that still match one of their model's prefixes
         int* nn = &n_cand[(pass + 1) & 1];
         unsigned short* nxt = cand[(pass + 1) & 1];
         for (int ii = threadIdx.x; ii < n_iter; ii += blockDim.x) {
           const int i = (int)cur[ii];
           const int m = (int)mcache[i] - g0;
-          const unsigned long long key = kcache[i];
+          const unsigned long long v = kcache[i] - base;
           bool keep = false;
 #pragma unroll
-          for (int q = 0; q < 3; q++) {
-            const bool match = ((key ^ prefix[m][q]) >> shift) == 0ull;
-            keep |= match;
-            if (match && resolved[m][q]) found[m][q] = key;  // the one record with this prefix
-          }
+          for (int q = 0; q < 3; q++) keep |= slo_match(v, prefix[m][q], shift);
           const unsigned act = __activemask(), bal = __ballot_sync(act, keep);
-          const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
-          int base = 0;
-          if (lane == leader && bal) base = atomicAdd(nn, __popc(bal));
-          base = __shfl_sync(act, base, leader);
-          if (keep) nxt[base + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
+          const int leader = __ffs(act) - 1;
+          int cb = 0;
+          if (lane == leader && bal) cb = atomicAdd(nn, __popc(bal));
+          cb = __shfl_sync(act, cb, leader);
+          if (keep) nxt[cb + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)i;
         }
         __syncthreads();
-        if (unresolved[pass & 1] == 0) {  // every quantile is a known record: done with this group
-          if (threadIdx.x < gm * 3) prefix[threadIdx.x / 3][threadIdx.x % 3] = found[threadIdx.x / 3][threadIdx.x % 3];
+        if (unresolved[pass & 1] == 0) {
+          // every selected bin holds <= kSloFinish records: one warp per
+          // (model, quantile) gathers its bin's records and ranks them
+          const int nc = n_cand[(pass + 1) & 1];
+          for (int t = warp; t < gm * 3; t += kSloThreads / 32) {
+            const int mm = t / 3, q = t % 3;
+            const unsigned long long pv = prefix[mm][q];
+            int c = 0;
+            for (int j0 = 0; j0 < nc; j0 += 32) {
+              const int j = j0 + lane;
+              bool hit = false;
+              unsigned long long v = 0ull;
+              if (j < nc) {
+                const int i = (int)nxt[j];
+                v = kcache[i] - base;
+                hit = (int)mcache[i] - g0 == mm && slo_match(v, pv, shift);
+              }
+              const unsigned bal = __ballot_sync(0xffffffffu, hit);
+              const int pos = c + __popc(bal & ((1u << lane) - 1u));
+              if (hit && pos < kSloFinish) fin[warp][pos] = v;  // (<= kSloFinish hits by construction)
+              c += __popc(bal);
+            }
+            __syncwarp();
+            const int want = rank_left[mm][q];
+            c = c < kSloFinish ? c : kSloFinish;
+            if (lane < c) {
+              const unsigned long long x = fin[warp][lane];
+              int r = 0;
+              for (int k = 0; k < c; k++) {
+                const unsigned long long y = fin[warp][k];
+                r += (y < x || (y == x && k < lane)) ? 1 : 0;
+              }
+              if (r == want) prefix[mm][q] = x;
+            }
+            __syncwarp();
+          }
           __syncthreads();
           break;
         }
@@ -1736,7 +1830,7 @@ __global__ void __launch_bounds__(kSloThreads) k_slo(const intf_scenario* __rest
     }
     if (threadIdx.x < gm * 3) {
       const int mm = threadIdx.x / 3, q = threadIdx.x % 3;
-      out_p[3 * (S.model_off + g0 + mm) + q] = cnt_n[g0 + mm] ? key_lat(prefix[mm][q]) : NAN;
+      out_p[3 * (S.model_off + g0 + mm) + q] = cnt_n[g0 + mm] ? key_lat(prefix[mm][q] + base) : NAN;
     }
     __syncthreads();
   }
@@ -1774,6 +1868,19 @@ __device__ __forceinline__ SloKeys slo_keys(const intf_scenario& S, const intf_m
   return K;
 }
 
+// ws scalars after the counters: [129] T, [130] ~(min key high word),
+// [131] max key high word (both by atomicMax on the zeroed words), [132]
+// state (0 radix passes, 1 every selected bin <= kSloFinish: fetch and rank,
+// 2 prefixes complete), [134] the shift the prefixes are complete down to.  In state 1 the histogram region holds
+// the fetched bins: counts [96], then [96][kSloFinish] keys (u64).
+constexpr int kSloWsT = 129, kSloWsMin = 130, kSloWsMax = 131, kSloWsState = 132,
+              kSloWsShift = 134;
+constexpr int kSloWsFetchCnt = kSloWsHist, kSloWsFetch = kSloWsHist + kMaxModels * 3;
+static_assert(kSloWsFetch % 2 == 0, "fetched keys must be 8-byte aligned");
+__device__ __forceinline__ unsigned long long slo_big_base(const int32_t* ws) {
+  return (unsigned long long)(~(unsigned)ws[kSloWsMin]) << 32;
+}
+
 __global__ void k_slo_big_count(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
                                 intf_replay_buffers B, int s, const double* __restrict__ warm_cutoff,
                                 int32_t* __restrict__ ws) {
@@ -1786,23 +1893,42 @@ __global__ void k_slo_big_count(const intf_scenario* __restrict__ scen, const in
   const int n = B.n_req[s], ro = S.req_off;
   const double cutoff = warm_cutoff ? warm_cutoff[s] : -INFINITY;
   const SloKeys K = slo_keys(S, models, B);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int b = B.r_batch[ro + i];
-    const double at = B.arr_t[ro + i];
-    const int m = B.arr_model[ro + i];
-    const double lat = B.b_completion[ro + b] - at;
-    const bool met = lat <= models[S.model_off + m].slo_ms;
-    B.r_slo_met[ro + i] = met;
-    if (i < K.cap) {  // the radix passes stream these instead of gathering again
-      K.key[i] = lat_key(lat);
-      K.code[i] = m | (at >= cutoff ? kSloWarm : 0);
+  unsigned kmin = 0xffffffffu, kmax = 0u;  // key high words: the radix range
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+    const long long i = i0 + threadIdx.x;
+    if (i < n) {
+      const int b = B.r_batch[ro + i];
+      const double at = B.arr_t[ro + i];
+      const int m = B.arr_model[ro + i];
+      const double lat = B.b_completion[ro + b] - at;
+      const bool met = lat <= models[S.model_off + m].slo_ms;
+      B.r_slo_met[ro + i] = met;
+      const unsigned long long key = lat_key(lat);
+      if (i < K.cap) {  // the radix passes stream these instead of gathering again
+        K.key[i] = key;
+        K.code[i] = m | (at >= cutoff ? kSloWarm : 0);
+      }
+      const unsigned hk = (unsigned)(key >> 32);
+      kmin = hk < kmin ? hk : kmin;
+      kmax = hk > kmax ? hk : kmax;
+      // one shared atomic per (model, counter) and warp, not per record
+      const unsigned act = __activemask();
+      const unsigned same = __match_any_sync(act, m);
+      const unsigned bm = __ballot_sync(act, met), bw = __ballot_sync(act, at >= cutoff);
+      if ((threadIdx.x & 31) == __ffs(same) - 1) {
+        atomicAdd(&cnt[64 + 2 * m], __popc(same));
+        atomicAdd(&cnt[64 + 2 * m + 1], __popc(same & bm));
+        atomicAdd(&cnt[2 * m], __popc(same & bw));
+        atomicAdd(&cnt[2 * m + 1], __popc(same & bw & bm));
+      }
     }
-    atomicAdd(&cnt[64 + 2 * m], 1);
-    if (met) atomicAdd(&cnt[64 + 2 * m + 1], 1);
-    if (at >= cutoff) {
-      atomicAdd(&cnt[2 * m], 1);
-      if (met) atomicAdd(&cnt[2 * m + 1], 1);
-    }
+  }
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if ((threadIdx.x & 31) == 0 && kmin <= kmax) {
+    atomicMax(reinterpret_cast<unsigned*>(ws + kSloWsMin), ~kmin);
+    atomicMax(reinterpret_cast<unsigned*>(ws + kSloWsMax), kmax);
   }
   __syncthreads();
   for (int k = threadIdx.x; k < 128; k += blockDim.x)
@@ -1820,6 +1946,10 @@ __global__ void k_slo_big_init(const intf_scenario* __restrict__ scen, int s, in
     for (int m = 0; m < S.n_models; m++) all += ws[64 + 2 * m];
     use_all = tot == 0 && all > 0;  // `metrics.py:67`: trimmed or records
     ws[128] = use_all;
+    const unsigned lo = ~(unsigned)ws[kSloWsMin], hi = (unsigned)ws[kSloWsMax];
+    const unsigned span = all > 0 && hi > lo ? hi - lo : 0u;
+    ws[kSloWsT] = 32 + (span ? 32 - __clz(span) : 0);  // every v = key - base < 2^T
+    ws[kSloWsState] = 0;
   }
   __syncthreads();
   const double pq[3] = {50.0, 95.0, 99.0};
@@ -1839,13 +1969,18 @@ __global__ void k_slo_big_init(const intf_scenario* __restrict__ scen, int s, in
   for (int t = threadIdx.x; t < kMaxModels * 3 * 256; t += blockDim.x) ws[kSloWsHist + t] = 0;
 }
 
+// radix pass `pass` over v = key - base at digit [T - 8 (pass + 1), + 8);
+// the first pass has one histogram per model (every prefix empty)
 __global__ void k_slo_big_hist(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
                                intf_replay_buffers B, int s, int pass, const double* __restrict__ warm_cutoff,
                                int32_t* __restrict__ ws) {
+  if (ws[kSloWsState] != 0) return;  // every (model, quantile) already narrowed
+  const int shift = ws[kSloWsT] - 8 * (pass + 1);
+  if (shift <= -8) return;
   const intf_scenario& S = scen[s];
   const int n = B.n_req[s], ro = S.req_off;
   const double cutoff = (warm_cutoff && !ws[128]) ? warm_cutoff[s] : -INFINITY;
-  const int shift = 56 - 8 * pass;
+  const unsigned long long base = slo_big_base(ws);
   const unsigned long long* prefix = reinterpret_cast<const unsigned long long*>(ws + kSloWsPrefix);
   unsigned int* hist = reinterpret_cast<unsigned int*>(ws + kSloWsHist);
   // warp-aggregated increments: latencies of one model share the high key
@@ -1855,6 +1990,15 @@ __global__ void k_slo_big_hist(const intf_scenario* __restrict__ scen, const int
   const SloKeys K = slo_keys(S, models, B);
   const bool staged = n <= K.cap;
   const bool all = !(warm_cutoff && !ws[128]);
+  const int nq = pass == 0 ? 1 : 3;
+  // pass 0 (every in-window record, few hot bins): block-private histogram in
+  // shared memory, flushed once (global atomics on the hot bins serialised:
+  // 92 us of 1e6 records)
+  __shared__ unsigned sh0[kMaxModels * 256];
+  if (pass == 0) {
+    for (int k = threadIdx.x; k < S.n_models * 256; k += blockDim.x) sh0[k] = 0u;
+    __syncthreads();
+  }
   for (long long i0 = start - (threadIdx.x & 31); i0 < n; i0 += stride) {
     const long long i = i0 + (threadIdx.x & 31);
     int bins[3] = {-1, -1, -1};
@@ -1874,38 +2018,57 @@ __global__ void k_slo_big_hist(const intf_scenario* __restrict__ scen, const int
         key = in ? lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at) : 0ull;
       }
       if (in) {
-        const unsigned d = (unsigned)(key >> shift) & 0xffu;
+        const unsigned long long v = key - base;
+        const int d = (int)slo_digit(v, shift);
+        if (pass == 0) {
+          bins[0] = m * 256 + d;  // (shared row m)
+        } else {
 #pragma unroll
-        for (int q = 0; q < 3; q++)
-          if (pass == 0 || ((key ^ prefix[m * 3 + q]) >> (shift + 8)) == 0ull) bins[q] = (m * 3 + q) * 256 + (int)d;
+          for (int q = 0; q < 3; q++)
+            if (slo_match(v, prefix[m * 3 + q], shift + 8)) bins[q] = (m * 3 + q) * 256 + d;
+        }
       }
     }
 #pragma unroll
     for (int q = 0; q < 3; q++) {
+      if (q >= nq || !__any_sync(0xffffffffu, bins[q] >= 0)) continue;  // (most records match no prefix)
       const unsigned same = __match_any_sync(0xffffffffu, bins[q]);
-      if (bins[q] >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&hist[bins[q]], (unsigned)__popc(same));
+      if (bins[q] >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) {
+        if (pass == 0) atomicAdd(&sh0[bins[q]], (unsigned)__popc(same));
+        else atomicAdd(&hist[bins[q]], (unsigned)__popc(same));
+      }
     }
+  }
+  if (pass == 0) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < S.n_models * 256; k += blockDim.x)
+      if (sh0[k]) atomicAdd(&hist[(k >> 8) * 3 * 256 + (k & 255)], sh0[k]);
   }
 }
 
-__global__ void k_slo_big_select(const intf_scenario* __restrict__ scen, int s, int pass, int32_t* __restrict__ ws,
-                                 double* out_p) {
+__global__ void __launch_bounds__(1024) k_slo_big_select(const intf_scenario* __restrict__ scen, int s, int pass,
+                                                         int32_t* __restrict__ ws, double* out_p) {
+  if (ws[kSloWsState] != 0) return;
+  const int shift = ws[kSloWsT] - 8 * (pass + 1);
+  if (shift <= -8) return;
   const intf_scenario& S = scen[s];
-  const int shift = 56 - 8 * pass;
   unsigned long long* prefix = reinterpret_cast<unsigned long long*>(ws + kSloWsPrefix);
   long long* left = reinterpret_cast<long long*>(ws + kSloWsLeft);
   unsigned int* hist = reinterpret_cast<unsigned int*>(ws + kSloWsHist);
+  __shared__ int unres;
+  if (threadIdx.x == 0) unres = 0;
+  __syncthreads();
   // warp per target (model, percentile): lane owns bins [8 lane, 8 lane + 8);
   // the digit is the first bin whose running count passes `left`
   const int lane = threadIdx.x & 31;
   for (int t = threadIdx.x >> 5; t < S.n_models * 3; t += blockDim.x >> 5) {
+    const int row = pass == 0 ? t - t % 3 : t;
     unsigned h[8];
     long long own = 0;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      h[k] = hist[t * 256 + 8 * lane + k];
+      h[k] = hist[row * 256 + 8 * lane + k];
       own += h[k];
-      hist[t * 256 + 8 * lane + k] = 0;  // cleared for the next pass
     }
     long long incl = own;
 #pragma unroll
@@ -1926,12 +2089,96 @@ __global__ void k_slo_big_select(const intf_scenario* __restrict__ scen, int s, 
         r -= h[k];
       }
       left[t] = r;
-      prefix[t] |= (unsigned long long)d << shift;
-      if (pass == 7) {
-        const int m = t / 3;
-        const int nm = ws[(ws[128] ? 64 : 0) + 2 * m];
-        out_p[3 * (S.model_off + m) + t % 3] = nm ? key_lat(prefix[t]) : NAN;
+      prefix[t] |= slo_put(d, shift);
+      if (h[k] > (unsigned)kSloFinish) atomicAdd(&unres, 1);
+    }
+  }
+  __syncthreads();  // every row read: clear for the next pass
+  for (int k = threadIdx.x; k < S.n_models * 3 * 256; k += blockDim.x) hist[k] = 0u;
+  if (threadIdx.x == 0) {
+    if (shift <= 0) {
+      ws[kSloWsState] = 2;  // every bit selected: the prefixes are the keys
+    } else if (unres == 0) {
+      ws[kSloWsState] = 1;  // every selected bin holds <= kSloFinish records: fetch them
+      ws[kSloWsShift] = shift;
+    }
+  }
+}
+
+// state 1: the records of every (model, quantile)'s selected bin into the
+// (cleared) histogram region, <= kSloFinish each
+__global__ void k_slo_big_fetch(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                                intf_replay_buffers B, int s, const double* __restrict__ warm_cutoff,
+                                int32_t* __restrict__ ws) {
+  if (ws[kSloWsState] != 1) return;
+  const int shift = ws[kSloWsShift];
+  const intf_scenario& S = scen[s];
+  const int n = B.n_req[s], ro = S.req_off;
+  const double cutoff = (warm_cutoff && !ws[128]) ? warm_cutoff[s] : -INFINITY;
+  const unsigned long long base = slo_big_base(ws);
+  const unsigned long long* prefix = reinterpret_cast<const unsigned long long*>(ws + kSloWsPrefix);
+  int* fcnt = ws + kSloWsFetchCnt;
+  unsigned long long* fkey = reinterpret_cast<unsigned long long*>(ws + kSloWsFetch);
+  const SloKeys K = slo_keys(S, models, B);
+  const bool staged = n <= K.cap;
+  const bool all = !(warm_cutoff && !ws[128]);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    int m;
+    unsigned long long key;
+    bool in;
+    if (staged) {
+      const int c = K.code[i];
+      m = c & (kSloWarm - 1);
+      in = all || (c & kSloWarm);
+      key = K.key[i];
+    } else {
+      const double at = B.arr_t[ro + i];
+      in = at >= cutoff;
+      m = B.arr_model[ro + i];
+      key = in ? lat_key(B.b_completion[ro + B.r_batch[ro + i]] - at) : 0ull;
+    }
+    if (!in) continue;
+    const unsigned long long v = key - base;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      if (slo_match(v, prefix[m * 3 + q], shift)) {
+        const int at = atomicAdd(&fcnt[m * 3 + q], 1);
+        if (at < kSloFinish) fkey[(m * 3 + q) * kSloFinish + at] = v;
       }
+    }
+  }
+}
+
+// the percentiles: state 1 ranks each fetched bin (one warp per target),
+// state 2 reads the complete prefixes
+__global__ void __launch_bounds__(1024) k_slo_big_finish(const intf_scenario* __restrict__ scen, int s,
+                                                         int32_t* __restrict__ ws, double* out_p) {
+  const intf_scenario& S = scen[s];
+  const int state = ws[kSloWsState];
+  const unsigned long long base = slo_big_base(ws);
+  unsigned long long* prefix = reinterpret_cast<unsigned long long*>(ws + kSloWsPrefix);
+  const long long* left = reinterpret_cast<const long long*>(ws + kSloWsLeft);
+  const int* fcnt = ws + kSloWsFetchCnt;
+  const unsigned long long* fkey = reinterpret_cast<const unsigned long long*>(ws + kSloWsFetch);
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < S.n_models * 3; t += blockDim.x >> 5) {
+    unsigned long long p = prefix[t];
+    if (state == 1) {
+      const int c = min(fcnt[t], kSloFinish);
+      const unsigned long long x = lane < c ? fkey[t * kSloFinish + lane] : 0ull;
+      int r = 0;
+      for (int k = 0; k < c; k++) {
+        const unsigned long long y = __shfl_sync(0xffffffffu, x, k);
+        r += (y < x || (y == x && k < lane)) ? 1 : 0;
+      }
+      const unsigned win = __ballot_sync(0xffffffffu, lane < c && r == (int)left[t]);
+      if (win) p = __shfl_sync(0xffffffffu, x, __ffs(win) - 1);
+    }
+    if (lane == 0) {
+      const int m = t / 3;
+      const int nm = ws[(ws[128] ? 64 : 0) + 2 * m];
+      out_p[3 * (S.model_off + m) + t % 3] = nm ? key_lat(p + base) : NAN;
     }
   }
 }
@@ -2226,11 +2473,16 @@ int intf_slo_report(const intf_batch* bt, const intf_replay_buffers* buf, const 
       if ((rc = launch_status("k_slo_big_count"))) return rc;
       k_slo_big_init<<<1, 256, 0, st>>>(bt->scen, s, buf->slo_ws, out_n, out_met);
       if ((rc = launch_status("k_slo_big_init"))) return rc;
+      // <= 8 radix passes (v < 2^64); once every selected bin is small the
+      // remaining ones return at once and the bins are fetched and ranked
       for (int pass = 0; pass < 8; pass++) {
         k_slo_big_hist<<<4 * 148, 256, 0, st>>>(bt->scen, bt->models, *buf, s, pass, warm_cutoff, buf->slo_ws);
         k_slo_big_select<<<1, 1024, 0, st>>>(bt->scen, s, pass, buf->slo_ws, out_p);
       }
       if ((rc = launch_status("k_slo_big_select"))) return rc;
+      k_slo_big_fetch<<<4 * 148, 256, 0, st>>>(bt->scen, bt->models, *buf, s, warm_cutoff, buf->slo_ws);
+      k_slo_big_finish<<<1, 1024, 0, st>>>(bt->scen, s, buf->slo_ws, out_p);
+      if ((rc = launch_status("k_slo_big_finish"))) return rc;
     }
     return INTF_OK;
   }
