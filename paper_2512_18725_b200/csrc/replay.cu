@@ -469,6 +469,43 @@ __global__ void k_merge_batches(const intf_scenario* __restrict__ scen, const in
   }
 }
 
+// The same merge with one warp per model (sweeps of short lists: a C5 model
+// forms ~100 batches, so k_merge_batches' 256-thread chunks were mostly idle
+// block prologues)
+__device__ __forceinline__ void merge_batch(const intf_scenario& S, const intf_model* __restrict__ models,
+                                            const intf_replay_buffers& B, int g, int mloc, int j) {
+  const intf_model& M = models[g];
+  const double t = B.mb_t[M.list_off + j];
+  const int4 info = reinterpret_cast<const int4*>(B.mb_info)[M.list_off + j];
+  const int kind = info.x, cnt = info.z, head = info.w;
+  const uint32_t key = (uint32_t)info.y;
+  int rank = j;
+  for (int q = 0; q < S.n_models; q++) {
+    const int gq = S.model_off + q;
+    if (gq == g) continue;
+    const intf_model& Q = models[gq];
+    rank += count_form_before(B.mb_t + Q.list_off, B.mb_info + 4ll * Q.list_off, B.n_mb[gq], t, kind, key);
+  }
+  const int ro = S.req_off;
+  B.b_model[ro + rank] = mloc;
+  B.b_size[ro + rank] = cnt;
+  B.b_formed[ro + rank] = t;
+  const int32_t* lrid = B.list_rid + M.list_off;
+  for (int k = 0; k < cnt; k++) B.r_batch[ro + lrid[head + k]] = rank;
+}
+constexpr int kMergeWarps = 8;
+__global__ void __launch_bounds__(32 * kMergeWarps) k_merge_batches_warp(const intf_scenario* __restrict__ scen,
+                                                                         const intf_model* __restrict__ models,
+                                                                         intf_replay_buffers B, int n_models) {
+  const int g = blockIdx.x * kMergeWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (g >= n_models) return;
+  const intf_model& M = models[g];
+  const intf_scenario& S = scen[M.scen];
+  const int n = B.n_mb[g];
+  if (lane == 0 && n) atomicAdd(&B.n_batches[M.scen], n);
+  for (int j = lane; j < n; j += 32) merge_batch(S, models, B, g, g - S.model_off, j);
+}
+
 // scenarios whose configuration the replay cannot run are flagged INTF_ST_CAP
 __global__ void k_form_status(const intf_scenario* __restrict__ scen, int n_scen, intf_replay_buffers B) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2282,6 +2319,11 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
     }
     k_form_emit<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, blk);
     if ((rc = launch_status("k_form_emit"))) return rc;
+  }
+  if (bt->max_list_cap < kLongForm) {  // short lists: one warp per model
+    k_merge_batches_warp<<<ceil_div(bt->n_models, kMergeWarps), 32 * kMergeWarps, 0, st>>>(bt->scen, bt->models,
+                                                                                          *buf, bt->n_models);
+    return launch_status("k_merge_batches_warp");
   }
   k_merge_batches<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
   return launch_status("k_merge_batches");

@@ -700,18 +700,24 @@ __device__ __forceinline__ void form_model_heads(const intf_scenario& S, const i
     const double w1 = h + 32 + lane < n_list ? lt[h + 32 + lane] : INFINITY;
     const int r0 = h + lane < n_list ? lrid[h + lane] : 0;
     const int r1 = h + 32 + lane < n_list ? lrid[h + 32 + lane] : 0;
-    // the batch starting at head h + lane
+    // the batch starting at head h + lane: 1 + the number of following
+    // arrivals before its window closes, a prefix of the sorted list -- the
+    // first j in [1, max_bs) with t[h + lane + j] >= D by binary search
+    // (5 probes instead of max_bs - 1)
     const double D = w0 + S.window_ms;  // arm_window at the first arrival (`batcher.py:66-68`)
-    int cnt = 1;
-    bool open = true;
-    for (int j = 1; j < 32; j++) {
-      if (j >= mbs) break;
-      const int src = lane + j;  // window element lane + j: w0 of lane src, or w1 of lane src - 32
+    int lo = 1, hi = mbs;
+#pragma unroll
+    for (int step = 0; step < 5; step++) {  // 2^5 >= max_bs - 1 (this form: max_bs <= 32)
+      const int mid = (lo + hi) >> 1;
+      const int src = lane + mid;  // window element lane + mid (< 64): w0 of lane src, or w1 of lane src - 32
       const double a = __shfl_sync(0xffffffffu, w0, src & 31), b = __shfl_sync(0xffffffffu, w1, src & 31);
       const double v = src < 32 ? a : b;
-      open = open && v < D;
-      cnt += open ? 1 : 0;
+      if (lo < hi) {
+        if (v < D) lo = mid + 1;
+        else hi = mid;
+      }
     }
+    const int cnt = lo;
     const int last = lane + cnt - 1;  // < 64
     const double ta = __shfl_sync(0xffffffffu, w0, last & 31), tb = __shfl_sync(0xffffffffu, w1, last & 31);
     const int ra = __shfl_sync(0xffffffffu, r0, last & 31), rb = __shfl_sync(0xffffffffu, r1, last & 31);
