@@ -178,7 +178,7 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
   // ---- per-lane slot state (valid while `act`)
   bool act = false;
   double start = 0.0, total = 0.0, progress = 0.0, done = 0.0, own0 = 0.0, own1 = 0.0, own2 = 0.0;
-  double cur_tb = 0.0, cur_sd = 1.0, nz0 = 1.0, nz1 = 1.0, nz2 = 1.0, nz3 = 1.0;
+  double cur_tb = 0.0, cur_sd = 1.0, cur_rsd = 1.0, nz0 = 1.0, nz1 = 1.0, nz2 = 1.0, nz3 = 1.0;
   int batch = 0, nseg = 0, n_non1 = 0;
 
   // ---- group-uniform state
@@ -281,6 +281,7 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
     nseg++;
     cur_tb = now;
     cur_sd = sd;
+    cur_rsd = 1.0 / sd;  // RN(1/sd), off the chain: the segment's close divides by sd
     if (sd != 1.0) n_non1++;
     done = now + (total - progress) * sd;
     if (done < now - 1e-9) status |= INTF_ST_PAST_EVENT;
@@ -291,7 +292,12 @@ __device__ __forceinline__ ReplayJobOut replay_group_t(const ReplayJob J, const 
       nseg--;
       if (cur_sd != 1.0) n_non1--;
     } else {
-      progress = progress + (now - cur_tb) / cur_sd;
+      // (now - cur_tb) / cur_sd, correctly rounded (Markstein: with r = RN(1/y)
+      // and q0 = RN(x r) within an ulp, RN(q0 + RN(x - y q0) r) = RN(x / y);
+      // no overflow / underflow at these magnitudes): three dependent
+      // multiply-adds on the chain instead of the division sequence
+      const double x = now - cur_tb, q0 = x * cur_rsd;
+      progress = progress + fma(fma(-cur_sd, q0, x), cur_rsd, q0);
     }
   };
 
