@@ -1678,15 +1678,16 @@ __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, co
 //   coarse   = fit_ols(static[:cut]),  offline on static[cut:]
 //   fine     = fit_ols(EWMA[:cut]),    offline on EWMA[cut:]
 //   adaptive = rls_init(fine, lam, X_train = EWMA[:cut]), prequential on EWMA[cut:]
-// (`predict.py:53-72,112-134,157-205`).  k_scen_fit: one warp per scenario --
-// the 35 statistics of both training designs (lanes stride the rows, fixed
-// butterfly sums), the two solves on lanes 0 / 1 (lane 1 also P0 = inv(G)),
-// the offline test predictions; then k_rls_g8 runs the adaptive tails (8 lanes
-// per scenario) and k_eval the 3 EvalReports per scenario.
+// (`predict.py:53-72,112-134,157-205`).  Each part at the parallel grain and
+// register footprint it needs: k_scen_stats (a warp per training design: the
+// 35 statistics, lanes stride the rows, fixed butterfly sums), k_scen_solve (a
+// thread per design: condition screen + solve), k_scen_qr (the rare designs
+// that fail the screen: rank from the rows by the warp), k_scen_finish (a warp
+// per scenario: P0 = inv(G) of the EWMA design, the offline test
+// predictions); then k_rls_g8 runs the adaptive tails (8 lanes per scenario)
+// and k_eval the 3 EvalReports per scenario.  (One warp per scenario for all
+// of it kept 2 of 32 lanes busy in the solves at 8 warps per SM.)
 constexpr int kScenFitWarps = 4;
-#ifndef INTF_SCEN_FIT_MINB
-#define INTF_SCEN_FIT_MINB 0  // min resident blocks per SM (register cap); 0 = compiler's choice
-#endif
 
 // rls_init's P0 = np.linalg.inv(G) (`predict.py:126-131`) by the whole warp:
 // Gauss-Jordan with partial pivoting on [G | I], lane r < 7 holding row r in
@@ -1696,7 +1697,7 @@ constexpr int kScenFitWarps = 4;
 // columns (and rows) of a symmetric G stay identical under the row operations
 // until one is the pivot row, which zeroes the other exactly -- and then
 // inverts G + 1e-8 I (`predict.py:131`).  Replaces lane-serial LU with
-// dynamically indexed rows (local memory), ~45% of k_scen_fit's samples.
+// dynamically indexed rows (local memory), ~45% of the then fused fit kernel's samples.
 __device__ __noinline__ void warp_p0_inverse(const double* G, double* inv) {
   const int lane = threadIdx.x & 31, r = lane < 7 ? lane : 6;
   for (int attempt = 0; attempt < 2; attempt++) {
@@ -1750,8 +1751,7 @@ __device__ __noinline__ void warp_p0_inverse(const double* G, double* inv) {
   }
 }
 
-// one scenario design's solve (a call, not inlined: keeps the warp-wide
-// parts of k_scen_fit at a small register footprint)
+// one scenario design's solve (a call, not inlined)
 __device__ __noinline__ void scen_solve(const double* st, double* p, int32_t* inf2, double* Pinv, const double* qr,
                                         bool screen_only) {
   ols_solve_one(st, p, inf2, Pinv, nullptr, nullptr, 0, 0, qr, screen_only);
@@ -1796,96 +1796,168 @@ __device__ __noinline__ void warp_qr_rank(const double* __restrict__ X, const do
     for (int i = 0; i < 7; i++) out[1 + i] = x[i];
   }
 }
-__global__ void __launch_bounds__(32 * kScenFitWarps, INTF_SCEN_FIT_MINB) k_scen_fit(const intf_scenario* __restrict__ scen, int n_scen,
-                                                                 const int32_t* __restrict__ n_batches,
-                                                                 const double* __restrict__ X, long long slot_stride,
-                                                                 int p_static, int p_ewma, const double* __restrict__ Y,
-                                                                 double lam, double* __restrict__ params,
-                                                                 double* __restrict__ P0, double* __restrict__ lamv,
-                                                                 long long* __restrict__ lo, long long* __restrict__ hi,
-                                                                 double* __restrict__ yhat, int32_t* __restrict__ est) {
-  __shared__ double st[kScenFitWarps][2][56];
-  __shared__ double par[kScenFitWarps][2][7];
+// the chronological split of scenario s (`experiments.py:44-60`): cut =
+// int(round(0.75 n)); fit_ols needs 7 samples, the split a non-empty test set
+struct ScenSplit {
+  long long base, n, cut;
+  bool valid;
+};
+__device__ __forceinline__ ScenSplit scen_split(const intf_scenario* __restrict__ scen,
+                                                const int32_t* __restrict__ n_batches, int s) {
+  ScenSplit q;
+  q.base = scen[s].req_off;
+  q.n = n_batches[s];
+  q.cut = (long long)rint(0.75 * (double)q.n);
+  q.valid = q.cut >= 7 && q.n - q.cut >= 1;
+  return q;
+}
+
+// (1) the 35 statistics of one training design (m = 0 static, 1 EWMA) of one
+// scenario per warp: lanes stride the rows (lane l: rows l, l+32, ... in
+// order), fixed butterfly sums -> stats[2s + m][56] (G row-major, then Z^T y).
+// Low register footprint, so 16+ warps per SM hide the row loads.
+__global__ void __launch_bounds__(32 * kScenFitWarps, 4) k_scen_stats(const intf_scenario* __restrict__ scen, int n_scen,
+                                                                      const int32_t* __restrict__ n_batches,
+                                                                      const double* __restrict__ X, long long slot_stride,
+                                                                      int p_static, int p_ewma,
+                                                                      const double* __restrict__ Y,
+                                                                      double* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * kScenFitWarps + (threadIdx.x >> 5);
+  if (g >= 2 * n_scen) return;
+  const ScenSplit q = scen_split(scen, n_batches, g >> 1);
+  const double* Xb = X + (long long)((g & 1) ? p_ewma : p_static) * slot_stride * 6;
+  double acc[kStats];
+#pragma unroll
+  for (int i = 0; i < kStats; i++) acc[i] = 0.0;
+  if (q.valid) {
+    // 4 rows in flight per lane: the loads of the next rows are issued before
+    // the 35-fma updates of the current ones
+    long long row = q.base + lane;
+    for (; row + 96 < q.base + q.cut; row += 128) {
+      double x[4][6], yv[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+#pragma unroll
+        for (int i = 0; i < 6; i++) x[u][i] = Xb[(row + 32 * u) * 6 + i];
+        yv[u] = Y[row + 32 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) ols_acc_row(acc, x[u], yv[u]);
+    }
+    for (; row < q.base + q.cut; row += 32) ols_acc_row(acc, Xb + row * 6, Y[row]);
+  }
+  double* out = stats + 56ll * g;
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+#pragma unroll
+    for (int j = i; j < 7; j++, t++) {
+      const double v = warp_sum(acc[t]);
+      if (lane == (t & 31)) {  // spread the stores over the lanes
+        out[i * 7 + j] = v;
+        out[j * 7 + i] = v;
+      }
+    }
+#pragma unroll
+  for (int i = 0; i < 7; i++) {
+    const double v = warp_sum(acc[28 + i]);
+    if (lane == i) out[49 + i] = v;
+  }
+}
+
+// (2) the condition screen + solve of every design, one THREAD per design
+// (lane-serial work: every lane busy, where a warp per scenario kept 2 of 32)
+__global__ void __launch_bounds__(128) k_scen_solve(const intf_scenario* __restrict__ scen, int n_scen,
+                                                    const int32_t* __restrict__ n_batches,
+                                                    const double* __restrict__ stats, double* __restrict__ par,
+                                                    int32_t* __restrict__ inf) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= 2 * n_scen) return;
+  const ScenSplit q = scen_split(scen, n_batches, g >> 1);
+  int32_t inf2[2] = {0, 0};
+  double p[7];
+#pragma unroll
+  for (int i = 0; i < 7; i++) p[i] = NAN;
+  if (q.valid) scen_solve(stats + 56ll * g, p, inf2, nullptr, nullptr, true);
+#pragma unroll
+  for (int i = 0; i < 7; i++) par[7ll * g + i] = p[i];
+  inf[2ll * g] = inf2[0];
+  inf[2ll * g + 1] = inf2[1];
+}
+
+// (3) the designs that failed the condition screen (rare): rank from the
+// rows by the whole warp of their scenario, then the solve on lane m
+__global__ void __launch_bounds__(32 * kScenFitWarps) k_scen_qr(const intf_scenario* __restrict__ scen, int n_scen,
+                                                                const int32_t* __restrict__ n_batches,
+                                                                const double* __restrict__ X, long long slot_stride,
+                                                                int p_static, int p_ewma, const double* __restrict__ Y,
+                                                                const double* __restrict__ stats,
+                                                                double* __restrict__ par, int32_t* __restrict__ inf) {
   __shared__ double qrres[kScenFitWarps][2][8];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = blockIdx.x * kScenFitWarps + wi;
   if (s >= n_scen) return;
-  const long long base = scen[s].req_off;
-  const long long n = n_batches[s];
-  const long long cut = (long long)rint(0.75 * (double)n);
-  const bool valid = cut >= 7 && n - cut >= 1;  // fit_ols needs 7 samples; split needs a non-empty test set
+  const ScenSplit q = scen_split(scen, n_batches, s);
+  const bool mine = lane < 2 && q.valid && inf[2ll * (2 * s + lane)] == -1;
+  const unsigned need = __ballot_sync(0xffffffffu, mine);
+  if (!need) return;
   const double* Xm[2] = {X + (long long)p_static * slot_stride * 6, X + (long long)p_ewma * slot_stride * 6};
-  for (int m = 0; m < 2; m++) {
-    double acc[kStats];
-#pragma unroll
-    for (int i = 0; i < kStats; i++) acc[i] = 0.0;
-    if (valid) {
-      // 4 rows in flight per lane: the loads of the next rows are issued before
-      // the 35-fma updates of the current ones (load latency, not fma, bounds this)
-      const double* Xb = Xm[m];
-      long long row = base + lane;
-      for (; row + 96 < base + cut; row += 128) {
-        double x[4][6], yv[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-#pragma unroll
-          for (int i = 0; i < 6; i++) x[u][i] = Xb[(row + 32 * u) * 6 + i];
-          yv[u] = Y[row + 32 * u];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) ols_acc_row(acc, x[u], yv[u]);
-      }
-      for (; row < base + cut; row += 32) ols_acc_row(acc, Xb + row * 6, Y[row]);
-    }
-    int t = 0;
-#pragma unroll
-    for (int i = 0; i < 7; i++)
-#pragma unroll
-      for (int j = i; j < 7; j++, t++) {
-        const double v = warp_sum(acc[t]);
-        if (lane == 0) st[wi][m][i * 7 + j] = st[wi][m][j * 7 + i] = v;
-      }
-#pragma unroll
-    for (int i = 0; i < 7; i++) {
-      const double v = warp_sum(acc[28 + i]);
-      if (lane == 0) st[wi][m][49 + i] = v;
-    }
-  }
-  __syncwarp();
-  int bits = valid ? 0 : 1;
-  // lane 0: coarse, lane 1: fine (+ P0 for the adaptive tail); a design that
-  // fails the condition screen gets its rank from the rows, by the whole warp
-  int32_t inf2[2] = {0, 0};
-  double p[7];
-  if (lane < 2 && valid) scen_solve(st[wi][lane], p, inf2, nullptr, nullptr, true);
-  const unsigned need = __ballot_sync(0xffffffffu, lane < 2 && valid && inf2[0] == -1);
   for (int m = 0; m < 2; m++)
-    if (need & (1u << m)) warp_qr_rank(Xm[m], Y, base, cut, qrres[wi][m]);
+    if (need & (1u << m)) warp_qr_rank(Xm[m], Y, q.base, q.cut, qrres[wi][m]);
   __syncwarp();
-  if (lane < 2 && valid) {
-    if (need & (1u << lane)) scen_solve(st[wi][lane], p, inf2, nullptr, qrres[wi][lane], false);
+  if (mine) {
+    const int g = 2 * s + lane;
+    int32_t inf2[2] = {inf[2ll * g], inf[2ll * g + 1]};
+    double p[7];
+    scen_solve(stats + 56ll * g, p, inf2, nullptr, qrres[wi][lane], false);
 #pragma unroll
-    for (int i = 0; i < 7; i++) par[wi][lane][i] = p[i];
-    bits = (inf2[0] ? (2 << lane) : 0) | (inf2[1] ? 16 : 0);
+    for (int i = 0; i < 7; i++) par[7ll * g + i] = p[i];
+    inf[2ll * g] = inf2[0];
+    inf[2ll * g + 1] = inf2[1];
   }
+}
+
+// (4) per scenario, one warp: P0 = inv(G) of the EWMA design for the
+// adaptive tail, the parameter rows, the offline test predictions, the tail
+// bounds
+__global__ void __launch_bounds__(32 * kScenFitWarps) k_scen_finish(const intf_scenario* __restrict__ scen, int n_scen,
+                                                                    const int32_t* __restrict__ n_batches,
+                                                                    const double* __restrict__ X, long long slot_stride,
+                                                                    int p_static, int p_ewma, double lam,
+                                                                    const double* __restrict__ stats,
+                                                                    const double* __restrict__ par,
+                                                                    const int32_t* __restrict__ inf,
+                                                                    double* __restrict__ params, double* __restrict__ P0,
+                                                                    double* __restrict__ lamv, long long* __restrict__ lo,
+                                                                    long long* __restrict__ hi,
+                                                                    double* __restrict__ yhat, int32_t* __restrict__ est) {
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kScenFitWarps + wi;
+  if (s >= n_scen) return;
+  (void)wi;
+  const ScenSplit q = scen_split(scen, n_batches, s);
+  const double* Xm[2] = {X + (long long)p_static * slot_stride * 6, X + (long long)p_ewma * slot_stride * 6};
+  int bits = q.valid ? 0 : 1;
+  if (lane < 2 && q.valid) bits = (inf[2ll * (2 * s + lane)] ? (2 << lane) : 0) | (inf[2ll * (2 * s + lane) + 1] ? 16 : 0);
   bits |= __shfl_sync(0xffffffffu, bits, 1);
-  if (valid) warp_p0_inverse(st[wi][1], P0 + 49ll * s);  // the adaptive tail's P0 from the EWMA design
+  if (q.valid) warp_p0_inverse(stats + 56ll * (2 * s + 1), P0 + 49ll * s);  // the adaptive tail's P0 from the EWMA design
   __syncwarp();
   if (lane < 21) {  // coarse, fine, adaptive (= fine before its tail) parameters
     const int k = lane / 7, i = lane % 7;
-    params[(3ll * s + k) * 7 + i] = valid ? par[wi][k < 2 ? k : 1][i] : NAN;
+    params[(3ll * s + k) * 7 + i] = q.valid ? par[7ll * (2 * s + (k < 2 ? k : 1)) + i] : NAN;
   }
   if (lane == 0) {
     est[s] = bits;
     lamv[s] = lam;
-    lo[s] = base + cut;
-    hi[s] = valid ? base + n : base + cut;  // an invalid scenario gets empty test sets (reports n = 0, NaN)
+    lo[s] = q.base + q.cut;
+    hi[s] = q.valid ? q.base + q.n : q.base + q.cut;  // an invalid scenario gets empty test sets (reports n = 0, NaN)
   }
-  if (!valid) return;
+  if (!q.valid) return;
   double wc[7], wf[7];
 #pragma unroll
-  for (int i = 0; i < 7; i++) wc[i] = par[wi][0][i], wf[i] = par[wi][1][i];
-  for (long long row = base + cut + lane; row < base + n; row += 32) {
+  for (int i = 0; i < 7; i++) wc[i] = par[7ll * (2 * s) + i], wf[i] = par[7ll * (2 * s + 1) + i];
+  for (long long row = q.base + q.cut + lane; row < q.base + q.n; row += 32) {
     yhat[row] = predict7(wc, Xm[0] + row * 6);
     yhat[slot_stride + row] = predict7(wf, Xm[1] + row * 6);
   }
@@ -2584,7 +2656,8 @@ int intf_rls_streams(const double* X, const double* y, const int64_t* off, int32
 }
 
 int64_t intf_scenario_eval_ws(int32_t n_scen, int64_t slot_stride) {
-  return 49ll * n_scen + n_scen + 2ll * n_scen + 3ll * slot_stride;
+  // P0, lam, lo, hi, yhat; the designs' statistics, parameters and solve info
+  return 49ll * n_scen + n_scen + 2ll * n_scen + 3ll * slot_stride + 112ll * n_scen + 14ll * n_scen + 2ll * n_scen;
 }
 
 int intf_scenario_eval(const intf_batch* bt, const intf_replay_buffers* buf, const double* X, int64_t slot_stride,
@@ -2602,12 +2675,23 @@ int intf_scenario_eval(const intf_batch* bt, const intf_replay_buffers* buf, con
   long long* lo = (long long*)(lamv + S);
   long long* hi = lo + S;
   double* yhat = (double*)(hi + S);
+  double* stats = yhat + 3ll * slot_stride;  // [2S][56]
+  double* par = stats + 112ll * S;          // [2S][7]
+  int32_t* inf = (int32_t*)(par + 14ll * S);  // [2S][2]
   cudaStream_t st = as_stream(stream);
-  k_scen_fit<<<ceil_div(S, kScenFitWarps), 32 * kScenFitWarps, 0, st>>>(
-      bt->scen, S, buf->n_batches, X, (long long)slot_stride, p_static, p_ewma, y, lam, params, P0, lamv, lo, hi, yhat,
-      status);
-  int rc = launch_status("k_scen_fit");
+  k_scen_stats<<<ceil_div(2 * S, kScenFitWarps), 32 * kScenFitWarps, 0, st>>>(
+      bt->scen, S, buf->n_batches, X, (long long)slot_stride, p_static, p_ewma, y, stats);
+  int rc = launch_status("k_scen_stats");
   if (rc) return rc;
+  k_scen_solve<<<ceil_div(2 * S, 128), 128, 0, st>>>(bt->scen, S, buf->n_batches, stats, par, inf);
+  if ((rc = launch_status("k_scen_solve"))) return rc;
+  k_scen_qr<<<ceil_div(S, kScenFitWarps), 32 * kScenFitWarps, 0, st>>>(
+      bt->scen, S, buf->n_batches, X, (long long)slot_stride, p_static, p_ewma, y, stats, par, inf);
+  if ((rc = launch_status("k_scen_qr"))) return rc;
+  k_scen_finish<<<ceil_div(S, kScenFitWarps), 32 * kScenFitWarps, 0, st>>>(
+      bt->scen, S, buf->n_batches, X, (long long)slot_stride, p_static, p_ewma, lam, stats, par, inf, params, P0,
+      lamv, lo, hi, yhat, status);
+  if ((rc = launch_status("k_scen_finish"))) return rc;
   // the adaptive tails: rls_update over EWMA[cut:], from the fine fit and P0 (params row 2 of each scenario)
   k_rls_g8<<<ceil_div(S, 128 / kRlsGroup), 128, 0, st>>>(X + (long long)p_ewma * slot_stride * 6, y, lo, S, lamv,
                                                           params + 14, P0, yhat + 2 * slot_stride, status + S, hi, 21);
