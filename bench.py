@@ -474,21 +474,23 @@ def replay_stage_times(pipe, stream) -> dict:
 
     L, s = _abi.load(), stream.cuda_stream
     bt, B = ctypes.byref(pipe.batch), ctypes.byref(pipe.B)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     ev[0].record(stream)
     _abi.check(L.intf_generate_arrivals(bt, B, s), "arrivals")
     ev[1].record(stream)
-    _abi.check(L.intf_replay(bt, ctypes.byref(pipe.dtable.struct), B, s), "replay")
+    _abi.check(L.intf_form_batches(bt, B, s), "formation")  # timed on its own (intf_replay forms again)
     ev[2].record(stream)
-    pipe.run_slo_features(slo=True, features=False, evaluate=False)
+    _abi.check(L.intf_replay(bt, ctypes.byref(pipe.dtable.struct), B, s), "replay")
     ev[3].record(stream)
-    pipe.run_slo_features(slo=False, features=True, evaluate=False)
+    pipe.run_slo_features(slo=True, features=False, evaluate=False)
     ev[4].record(stream)
+    pipe.run_slo_features(slo=False, features=True, evaluate=False)
+    ev[5].record(stream)
     if pipe.evaluate is not None:
         pipe.run_evaluation()
-    ev[5].record(stream)
+    ev[6].record(stream)
     torch.cuda.synchronize()
-    names = ["arrivals", "replay", "slo", "features", "evaluation"]
+    names = ["arrivals", "formation+noise", "replay", "slo", "features", "evaluation"]
     return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
 
 
@@ -587,7 +589,20 @@ def c5_sweep(a, stream, barrier, max_over_ranks, rank, world, dist, table, W, sc
                         "scenario) + SLO + features + per-scenario coarse/fine/adaptive evaluation (75/25 split, "
                         "OLS x2, RLS prequential tail, 3 EvalReports) + per-scenario rows gathered to every rank "
                         f"(N > 1: NCCL all_gather); consecutive sweeps on {n_pipes} pipelines / streams",
-            "steps_timed": r_steps, "stage_ms": stage_ms, "summary": summary, "decisions": decisions}
+            "steps_timed": r_steps, "stage_ms": stage_ms, "stage_roofline": c5_stage_roofline(stage_ms, n_req),
+            "summary": summary, "decisions": decisions}
+
+
+def c5_stage_roofline(stage_ms: dict, n_req: int) -> dict:
+    """SURVEY §8d's HBM figure for formation + SLO (~23 B per request) against
+    the stages' isolated device time (the noise table, RNG compute, is inside
+    intf_form_batches and counted as formation time)."""
+    peak, _ = _peaks()
+    ms = stage_ms["formation+noise"] + stage_ms["slo"]
+    gbs = 23.0 * n_req / (ms / 1e3) / 1e9
+    return {"stages": "formation (+ noise table) + SLO report", "algorithmic_bytes_per_request": 23,
+            "ms": ms, "achieved_gbs": gbs, "peak": peak, "frac": gbs / peak,
+            "note": "per-scenario work of ~800 requests in ~300 batches: latency / issue bound, not HBM bound"}
 
 
 def real_decisions(stream, barrier, max_over_ranks, scorer, pipe, W) -> dict:
