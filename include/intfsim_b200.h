@@ -295,10 +295,22 @@ int intf_best_candidates_host(const intf_table *table, int32_t cap, double alpha
  * fused step's prep blocks), so the feature build overlaps the scoring.
  * *state counts the calls (0: build first; reset to 0 whenever table, cap or
  * alpha change); d_scratch holds intf_best_candidates_host's floats plus one
- * more candidate workspace.                                                 */
+ * more candidate workspace.  With a pinned (page-locked) h_best and n_dec <=
+ * 32 a call is ONE kernel launch: the coefficients travel as a kernel
+ * parameter and the last block writes the keys into h_best over the bus
+ * (no copies, no memset); otherwise the keys are copied back.  Either way the
+ * keys are valid once the stream has synchronised.                         */
 int intf_best_candidates_host_pipelined(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
                                         int32_t n_dec, uint64_t *h_best, float *d_scratch, int64_t scratch_elems,
                                         int64_t *state, void *stream);
+/* The same call, synchronous: returns once the keys are in h_best.  On the
+ * one-launch path (pinned h_best, n_dec <= 32) the kernel's last block also
+ * writes a per-thread pinned completion word after the keys and the call
+ * spins on it (no stream synchronisation); otherwise it synchronises the
+ * stream.  The call a scheduler makes per decision batch.                   */
+int intf_best_candidates_host_sync(const intf_table *table, int32_t cap, double alpha, const double *h_coefs,
+                                   int32_t n_dec, uint64_t *h_best, float *d_scratch, int64_t scratch_elems,
+                                   int64_t *state, void *stream);
 
 /* Real scheduling decisions of a replayed batch: for every
  * batch slot (req_off + b), dec_rank = the multiset rank (enumeration of

@@ -106,6 +106,7 @@ SIGNATURES = {
     "intf_candidate_best_step": (c_int32, [P, c_int32, c_double, P, c_int32, P, P, P, P, c_int64, P]),
     "intf_best_candidates_host": (c_int32, [P, c_int32, c_double, P, c_int32, P, P, c_int64, P]),
     "intf_best_candidates_host_pipelined": (c_int32, [P, c_int32, c_double, P, c_int32, P, P, c_int64, P, P]),
+    "intf_best_candidates_host_sync": (c_int32, [P, c_int32, c_double, P, c_int32, P, P, c_int64, P, P]),
     "intf_dispatch_sets": (c_int32, [P, P, c_int32, c_int32, P, P, P]),
     "intf_score_decisions": (c_int32, [P, c_int32, P, P, c_int64, P, P, c_int64, P, P, P]),
     "intf_decision_features_elems": (c_int64, [c_int32, c_int32]),

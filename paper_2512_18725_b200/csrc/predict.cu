@@ -557,6 +557,62 @@ __global__ void __launch_bounds__(kStreamThreads, 8) k_cand_step(
   cand_stream_body<kBest>(bx, rest % E, rest / E, thr, E, ld, n_sets, coefs, n_dec, ws_cur, ws_cur + 3 * ld, out, best);
 }
 
+// The host-buffer best-candidate call in ONE launch (intf_best_candidates_host_
+// pipelined with a pinned result buffer): the decisions' coefficients arrive
+// as a kernel parameter (no host->device copy), and the last stream block to
+// finish (a completion counter) copies the reduced keys straight into the
+// caller's pinned buffer over the bus and re-arms them (~0) for the next
+// call (no device->host copy, no memset).  The next call's blocks wait for
+// this grid (griddepcontrol.wait) before touching memory.
+constexpr int kHostDecMax = 32;  // decisions whose coefficients fit the 4 KB parameter space
+struct CandCoefs {
+  double c[kHostDecMax * 2 * 7];
+};
+template <int KMAX>
+__global__ void __launch_bounds__(kStreamThreads, 8) k_cand_step_host(
+    const double* __restrict__ solo, const double* __restrict__ thr, int E, int cap, long long n_sets, long long ld,
+    double alpha, const __grid_constant__ CandCoefs cp, int n_dec, const float* __restrict__ ws_cur,
+    float* __restrict__ ws_next, int prep_x, int prep_y, int prep_own, int stream_x,
+    unsigned long long* __restrict__ best, long long n_best, unsigned* __restrict__ done, int n_stream_blocks,
+    unsigned long long* __restrict__ host_best, volatile unsigned long long* flag, unsigned long long seq) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int n_prep = ws_next ? prep_x * prep_y : 0;
+  int b = blockIdx.x;
+  if (b < n_prep) {
+    cand_prep_body<KMAX>(b % prep_x, b / prep_x, solo, thr, E, cap, n_sets, ld, alpha, ws_next, ws_next + 3 * ld,
+                         prep_own);
+    return;
+  }
+  b -= n_prep;
+  const int bx = b % stream_x, rest = b / stream_x;
+  cand_stream_body<true>(bx, rest % E, rest / E, thr, E, ld, n_sets, cp.c, n_dec, ws_cur, ws_cur + 3 * ld, nullptr,
+                         best);
+  __shared__ bool last;
+  __threadfence();  // this block's atomicMin results before its count
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == (unsigned)n_stream_blocks - 1u;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const ulonglong2* src = reinterpret_cast<const ulonglong2*>(best);
+  ulonglong2* dst = reinterpret_cast<ulonglong2*>(host_best);
+  for (long long i = threadIdx.x; i < n_best / 2; i += blockDim.x) {
+    dst[i] = __ldcg(src + i);
+    reinterpret_cast<ulonglong2*>(best)[i] = make_ulonglong2(~0ull, ~0ull);
+  }
+  if ((n_best & 1) && threadIdx.x == 0) {
+    host_best[n_best - 1] = __ldcg(best + n_best - 1);
+    best[n_best - 1] = ~0ull;
+  }
+  if (threadIdx.x == 0) *done = 0u;
+  if (flag) {  // the waiting host thread's signal: every key store of the block before it
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = seq;
+  }
+}
+
 // ---- real scheduling decisions ("the per-decision candidate
 // set from C5 replays").  Decision = the dispatch of batch b of a replayed
 // scenario; its running set = the batches it co-runs with right after the
@@ -2236,6 +2292,55 @@ static int launch_step(const intf_table* t, int cap, double alpha, const double*
   return launch_status("k_cand_step");
 }
 
+// the device address of a pinned (page-locked, mapped) host buffer, or null
+// for pageable memory (then the call copies); the last buffer is remembered
+static unsigned long long* host_device_ptr(void* h) {
+  static thread_local void* last_h = nullptr;
+  static thread_local void* last_d = nullptr;
+  if (h == last_h) return reinterpret_cast<unsigned long long*>(last_d);
+  cudaPointerAttributes a = {};
+  void* d = nullptr;
+  if (cudaPointerGetAttributes(&a, h) == cudaSuccess && a.type == cudaMemoryTypeHost) d = a.devicePointer;
+  cudaGetLastError();  // (pageable memory: clear any error of the query)
+  last_h = h;
+  last_d = d;
+  return reinterpret_cast<unsigned long long*>(d);
+}
+
+template <int K>
+static int launch_step_host(const intf_table* t, int cap, double alpha, const double* h_coefs, int n_dec,
+                            const float* ws_cur, float* ws_next, cudaStream_t st, unsigned long long* best,
+                            unsigned* done, unsigned long long* host_best,
+                            unsigned long long* flag = nullptr, unsigned long long seq = 0) {
+  const int E = t->n_rows;
+  const long long sets = n_multisets(E, cap), ld = cand_ld(sets);
+  const size_t smem = sizeof(unsigned long long) * (K + 1) * (E + K + 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_cand_step_host<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int po = kStepPrepOwn;
+  const int px = (int)ceil_div(ld, 128), py = (int)ceil_div(E, po);
+  const int sx = (int)ceil_div(ld / 4, kStreamThreads * kBestSpan);
+  const long long n_stream = (long long)sx * E * ceil_div(n_dec, kStreamDec);
+  const long long nblk = (long long)px * py + n_stream;
+  if (nblk > 0x7fffffffLL) return bad_input("intf_candidate_step: too many blocks");
+  CandCoefs cp;
+  memcpy(cp.c, h_coefs, sizeof(double) * n_dec * 2 * 7);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nblk);
+  cfg.blockDim = dim3(kStreamThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const long long n_best = 2ll * n_dec * E;
+  cudaLaunchKernelEx(&cfg, k_cand_step_host<K>, t->solo_ms, t->thr, E, cap, sets, ld, alpha, cp, n_dec, ws_cur,
+                     ws_next, px, py, po, sx, best, n_best, done, (int)n_stream, host_best,
+                     (volatile unsigned long long*)flag, seq);
+  return launch_status("k_cand_step_host");
+}
+
 // phase: 1 = feature prep, 2 = forward stream, 3 = both (two-phase path only)
 template <int K>
 static int launch_candidates(const intf_table* t, int cap, double alpha, const double* coefs, int n_dec, float* out,
@@ -2516,10 +2621,81 @@ int intf_score_decisions_ft(const intf_table* table, int32_t cap, const double* 
   return launch_status("k_score_decisions");
 }
 
+static int best_host_pipelined(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
+                               int32_t n_dec, uint64_t* h_best, float* d_scratch, int64_t scratch_elems,
+                               int64_t* state, void* stream, unsigned long long* flag, unsigned long long seq,
+                               bool* one_launch);
+
 int intf_best_candidates_host_pipelined(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
                                         int32_t n_dec, uint64_t* h_best, float* d_scratch, int64_t scratch_elems,
                                         int64_t* state, void* stream) {
   INTF_RANGE("intf_best_candidates_host_pipelined");
+  bool one = false;
+  return best_host_pipelined(table, cap, alpha, h_coefs, n_dec, h_best, d_scratch, scratch_elems, state, stream,
+                             nullptr, 0, &one);
+}
+
+// the per-thread pinned completion word of intf_best_candidates_host_sync
+struct HostFlag {
+  unsigned long long* h = nullptr;  // host view
+  unsigned long long* d = nullptr;  // device view
+  unsigned long long seq = 0;
+  int dev = -1;
+};
+static HostFlag* host_flag() {
+  static thread_local HostFlag f[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 16) return nullptr;
+  HostFlag& x = f[dev];
+  if (!x.h) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    void* dp = nullptr;
+    cudaHostGetDevicePointer(&dp, p, 0);
+    x.h = reinterpret_cast<unsigned long long*>(p);
+    x.d = reinterpret_cast<unsigned long long*>(dp);
+    *x.h = 0;
+    x.dev = dev;
+  }
+  return &x;
+}
+
+int intf_best_candidates_host_sync(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
+                                   int32_t n_dec, uint64_t* h_best, float* d_scratch, int64_t scratch_elems,
+                                   int64_t* state, void* stream) {
+  INTF_RANGE("intf_best_candidates_host_sync");
+  HostFlag* f = host_flag();
+  const unsigned long long seq = f ? ++f->seq : 0;
+  bool one = false;
+  int rc = best_host_pipelined(table, cap, alpha, h_coefs, n_dec, h_best, d_scratch, scratch_elems, state, stream,
+                               f ? f->d : nullptr, seq, &one);
+  if (rc) return rc;
+  if (!one || !f) {  // copy path: the stream's completion
+    if (cudaStreamSynchronize(as_stream(stream)) != cudaSuccess) return launch_status("intf_best_candidates_host_sync");
+    return INTF_OK;
+  }
+  // one-launch path: spin on the word the kernel's last block writes after the keys (a stream
+  // synchronisation would add the completion's propagation); a stall falls back to it
+  volatile unsigned long long* w = f->h;
+  for (long long spin = 0; *w != seq; spin++) {
+    if (spin > (1ll << 26)) {
+      if (cudaStreamSynchronize(as_stream(stream)) != cudaSuccess)
+        return launch_status("intf_best_candidates_host_sync");
+      if (*w != seq) return bad_input("intf_best_candidates_host_sync: the kernel did not signal");
+      break;
+    }
+  }
+  return INTF_OK;
+}
+
+static int best_host_pipelined(const intf_table* table, int32_t cap, double alpha, const double* h_coefs,
+                               int32_t n_dec, uint64_t* h_best, float* d_scratch, int64_t scratch_elems,
+                               int64_t* state, void* stream, unsigned long long* flag, unsigned long long seq,
+                               bool* one_launch) {
   if (!table || !h_coefs || !h_best || !d_scratch || !state || n_dec < 1 || cap < 1 || cap > kMaxPeers + 1)
     return bad_input("intf_best_candidates_host_pipelined: bad argument");
   int64_t ws = 0;
@@ -2528,15 +2704,44 @@ int intf_best_candidates_host_pipelined(const intf_table* table, int32_t cap, do
   if (scratch_elems < n_coef + 2 * n_best + 2 * ws)
     return bad_input("intf_best_candidates_host_pipelined: scratch too small");
   cudaStream_t st = as_stream(stream);
-  // scratch: [coefs as doubles][best keys as u64][workspace 0][workspace 1]; *state counts calls:
-  // call k reads the features call k-1 built into workspace k & 1 and builds call k+1's into the other
-  double* d_coefs = reinterpret_cast<double*>(d_scratch);
-  unsigned long long* d_best = reinterpret_cast<unsigned long long*>(d_scratch + n_coef);
-  float* d_ws[2] = {d_scratch + n_coef + 2 * n_best, d_scratch + n_coef + 2 * n_best + ws};
+  // scratch: [workspace 0][workspace 1][best keys as u64][coefs as doubles ... completion counter in
+  // the last float], the workspaces and keys at offsets that do not depend on n_dec (consecutive
+  // calls may score different numbers of decisions); *state counts calls: call k reads the
+  // features call k-1 built into workspace k & 1 and builds call k+1's into the other
+  float* d_ws[2] = {d_scratch, d_scratch + ws};
+  unsigned long long* d_best = reinterpret_cast<unsigned long long*>(d_scratch + 2 * ws);
+  double* d_coefs = reinterpret_cast<double*>(d_scratch + 2 * ws + 2 * n_best);
+  int rc;
+  // *state: bits 0-47 count the calls; bits 48-55 = the decisions whose keys
+  // the one-launch path has armed (~0; each call re-arms its own range) and
+  // whose completion counter is zero -- 0 after a copy-path call, which
+  // overwrites them
+  constexpr long long kCount = (1ll << 48) - 1;
+  const long long k = *state & kCount;
+  const int armed = (int)((*state >> 48) & 0xff);
+  unsigned long long* h_dev = n_dec <= kHostDecMax ? host_device_ptr(h_best) : nullptr;
+  if (h_dev) {  // one launch: coefficients as a parameter, keys written into the pinned buffer by the last block
+    unsigned* done = reinterpret_cast<unsigned*>(d_scratch + scratch_elems - 1);  // (past the keys: n_coef >= 28)
+    if (k == 0 && (rc = intf_candidate_prepare(table, cap, alpha, d_ws[0], ws, stream))) return rc;
+    if (armed == 0) cudaMemsetAsync(done, 0, sizeof(unsigned), st);
+    if (n_dec > armed) cudaMemsetAsync(d_best, 0xff, sizeof(unsigned long long) * n_best, st);
+    switch (cap - 1) {
+      case 0: rc = launch_step_host<0>(table, cap, alpha, h_coefs, n_dec, d_ws[k & 1], d_ws[(k + 1) & 1], st, d_best, done, h_dev, flag, seq); break;
+      case 1: rc = launch_step_host<1>(table, cap, alpha, h_coefs, n_dec, d_ws[k & 1], d_ws[(k + 1) & 1], st, d_best, done, h_dev, flag, seq); break;
+      case 2: rc = launch_step_host<2>(table, cap, alpha, h_coefs, n_dec, d_ws[k & 1], d_ws[(k + 1) & 1], st, d_best, done, h_dev, flag, seq); break;
+      case 3: rc = launch_step_host<3>(table, cap, alpha, h_coefs, n_dec, d_ws[k & 1], d_ws[(k + 1) & 1], st, d_best, done, h_dev, flag, seq); break;
+      case 4: rc = launch_step_host<4>(table, cap, alpha, h_coefs, n_dec, d_ws[k & 1], d_ws[(k + 1) & 1], st, d_best, done, h_dev, flag, seq); break;
+      case 5: rc = launch_step_host<5>(table, cap, alpha, h_coefs, n_dec, d_ws[k & 1], d_ws[(k + 1) & 1], st, d_best, done, h_dev, flag, seq); break;
+      case 6: rc = launch_step_host<6>(table, cap, alpha, h_coefs, n_dec, d_ws[k & 1], d_ws[(k + 1) & 1], st, d_best, done, h_dev, flag, seq); break;
+      default: rc = launch_step_host<7>(table, cap, alpha, h_coefs, n_dec, d_ws[k & 1], d_ws[(k + 1) & 1], st, d_best, done, h_dev, flag, seq); break;
+    }
+    if (rc) return rc;
+    *state = (k + 1) | ((long long)(n_dec > armed ? n_dec : armed) << 48);
+    *one_launch = true;
+    return INTF_OK;
+  }
   if (cudaMemcpyAsync(d_coefs, h_coefs, sizeof(double) * n_dec * 2 * 7, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return launch_status("copy coefs");
-  int rc;
-  const long long k = *state;
   if (k == 0 && (rc = intf_candidate_prepare(table, cap, alpha, d_ws[0], ws, stream))) return rc;
   cudaMemsetAsync(d_best, 0xff, sizeof(unsigned long long) * n_best, st);
   float *cur = d_ws[k & 1], *nxt = d_ws[(k + 1) & 1];

@@ -659,18 +659,37 @@ class CandidateScorer:
                                                          scratch.data_ptr(), scratch.numel(), stream_ptr()),
                    "intf_best_candidates_host")
 
-    def best_host_pipelined(self, coefs_host: np.ndarray, best_host: np.ndarray, scratch: torch.Tensor) -> None:
+    def best_host_pipelined(self, coefs_host: np.ndarray, best_host: np.ndarray, scratch: torch.Tensor,
+                            sync: bool = False) -> None:
         """best_host as a pipeline of decisions (intf_best_candidates_host_pipelined):
         each call scores from the features the previous call built and builds
         the next call's in the same launch; scratch holds
-        best_scratch_elems(n_dec) + one more workspace."""
+        best_scratch_elems(n_dec) + one more workspace.  With a pinned
+        best_host and <= 32 decisions a call is one kernel launch.  sync:
+        return with the keys in best_host (intf_best_candidates_host_sync)."""
         n_dec = coefs_host.size // 14
-        if getattr(self, "_host_state", None) is None:
+        c = getattr(self, "_host_call", None)
+        if c is None:  # per-call marshalling cached (a call is ~50 us; the argument objects cost ~5)
             self._host_state = np.zeros(1, dtype=np.int64)
-        _abi.check(_abi.load().intf_best_candidates_host_pipelined(
-            ctypes.byref(self.dtable.struct), self.cap, self.alpha, coefs_host.ctypes.data, n_dec, best_host.ctypes.data,
-            scratch.data_ptr(), scratch.numel(), self._host_state.ctypes.data, stream_ptr()),
-            "intf_best_candidates_host_pipelined")
+            L = _abi.load()
+            c = self._host_call = {"fn": L.intf_best_candidates_host_pipelined,
+                                   "fn_sync": L.intf_best_candidates_host_sync,
+                                   "table": ctypes.byref(self.dtable.struct),
+                                   "state": self._host_state.ctypes.data, "ptrs": {}}
+        ptrs = c["ptrs"]
+
+        def ptr(a):
+            hit = ptrs.get(id(a))
+            if hit is None or hit[0] is not a:
+                if len(ptrs) > 64:
+                    ptrs.clear()
+                hit = ptrs[id(a)] = (a, a.ctypes.data)
+            return hit[1]
+
+        _abi.check(c["fn_sync" if sync else "fn"](c["table"], self.cap, self.alpha, ptr(coefs_host), n_dec,
+                                                   ptr(best_host), scratch.data_ptr(), scratch.numel(), c["state"],
+                                                   torch.cuda.current_stream().cuda_stream),
+                   "intf_best_candidates_host_sync" if sync else "intf_best_candidates_host_pipelined")
 
     def decode_best(self, keys, n_dec: int):
         """(value [n_dec][2][E] float32, multiset rank [n_dec][2][E] int64) of

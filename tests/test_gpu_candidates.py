@@ -226,3 +226,52 @@ def test_pipelined_host_best_calls_equal_single_calls():
         sc.best_host_pipelined(Wk, b, scr2)
         torch.cuda.synchronize()
         assert np.array_equal(a, b), k
+
+
+def test_pipelined_host_best_pinned_one_launch():
+    """With a pinned result buffer and <= 32 decisions the pipelined host call
+    is ONE launch (coefficients as a kernel parameter, the last block writes
+    the keys into the pinned buffer and re-arms them): the same keys as the
+    one-shot call, call after call, with the decision count changing and with
+    pageable (copy path) and pinned calls interleaved on the same scratch."""
+    from paper_2512_18725_b200.sweep import c2_decision_coefs
+
+    sc = _scorer(4)
+    W = c2_decision_coefs(32, 0.5)
+    scr1 = torch.empty(sc.best_scratch_elems(32), dtype=torch.float32, device="cuda")
+    scr2 = torch.empty(sc.best_scratch_elems(32) + sc.ws_elems, dtype=torch.float32, device="cuda")
+    pinned = torch.empty(2 * 32 * sc.E, dtype=torch.int64).pin_memory()
+    plan = [(0, 32, True), (3, 11, True), (7, 32, True), (1, 5, False), (2, 8, True), (9, 23, True), (0, 32, False),
+            (4, 32, True)]
+    for k, (lo, hi, pin) in enumerate(plan):
+        Wk = np.ascontiguousarray(W[lo:hi])
+        n = hi - lo
+        a = np.zeros(2 * n * sc.E, dtype=np.uint64)
+        sc.best_host(Wk, a, scr1)
+        b = pinned.numpy().view(np.uint64)[: 2 * n * sc.E] if pin else np.zeros_like(a)
+        b[:] = 0
+        sc.best_host_pipelined(Wk, b, scr2)
+        torch.cuda.synchronize()
+        assert np.array_equal(a, b), (k, lo, hi, pin)
+
+
+def test_host_sync_call_equals_single_calls():
+    """intf_best_candidates_host_sync returns with the keys in host memory
+    (pinned: the kernel's completion word; pageable: a stream sync), equal to
+    the one-shot call, for pinned and pageable buffers."""
+    from paper_2512_18725_b200.sweep import c2_decision_coefs
+
+    sc = _scorer(4)
+    W = c2_decision_coefs(32, 0.5)
+    scr1 = torch.empty(sc.best_scratch_elems(32), dtype=torch.float32, device="cuda")
+    scr2 = torch.empty(sc.best_scratch_elems(32) + sc.ws_elems, dtype=torch.float32, device="cuda")
+    pinned = torch.empty(2 * 32 * sc.E, dtype=torch.int64).pin_memory()
+    for k, (lo, hi, pin) in enumerate([(0, 32, True), (5, 21, True), (2, 9, False), (0, 32, True), (8, 12, True)]):
+        Wk = np.ascontiguousarray(W[lo:hi])
+        a = np.zeros(2 * (hi - lo) * sc.E, dtype=np.uint64)
+        sc.best_host(Wk, a, scr1)
+        torch.cuda.synchronize()
+        b = pinned.numpy().view(np.uint64)[: a.size] if pin else np.zeros_like(a)
+        b[:] = 0
+        sc.best_host_pipelined(Wk, b, scr2, sync=True)
+        assert np.array_equal(a, b), (k, lo, hi, pin)  # no synchronisation: the call returned with the keys
