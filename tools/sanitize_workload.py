@@ -2,8 +2,9 @@
 racecheck, synccheck): the smoke (bundled trace replay + features + a cap-3
 candidate step), a 2x10^5-request C4 trace (long-list arrivals / formation /
 busy-period jobs / grid SLO), a 256-scenario C5 sweep with the per-scenario
-evaluation, the best-candidate step, the windowed OLS (TMA) and the
-RLS / SGD / drift paths."""
+evaluation, the best-candidate step, the windowed OLS (TMA), the
+RLS / SGD / drift paths, the one-launch host best-candidate call and the
+SLO edge cases (ties above the warp-rank limit, > 2,048 records)."""
 import os
 import sys
 
@@ -46,3 +47,22 @@ y = X @ np.arange(1, 7) + 1.0
 print("ols windows", len(p.predict.fit_ols_windows(X, y, 64)))
 cells = ex.drift_experiment(ex.default_drift_base(table, 0), table)
 print("drift", len(cells))
+# the one-launch host call (pinned keys written by the last block, completion word) and the copy path
+hc = torch.tensor(c2_decision_coefs(8), dtype=torch.float64).pin_memory().numpy()
+hb = torch.empty(2 * 8 * sc.E, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+scr = torch.empty(sc.best_scratch_elems(8) + sc.ws_elems, dtype=torch.float32, device="cuda")
+for _ in range(3):
+    sc.best_host_pipelined(hc, hb, scr, sync=True)
+sc.best_host_pipelined(hc, np.zeros_like(hb), scr, sync=True)
+print("host calls", int(hb[0] >> 32))
+# SLO edges: tied latencies beyond the warp-rank limit, > 2,048 records (crafted arrivals)
+bursts = np.repeat(np.arange(0.0, 1000.0, 14.0), 35)
+t_arr = np.sort(np.concatenate([bursts, np.linspace(1.0, 999.0, 120)]))
+m_arr = np.zeros(len(t_arr), dtype=np.int32)
+m_arr[np.isin(t_arr, bursts, invert=True)] = 1
+spec = {"name": "ties", "duration_s": 1.0, "batching_window_ms": 2.0, "max_batch_size": 64, "concurrency_cap": 3,
+        "seed": 0, "colocation_mode": "static", "ewma_alpha": 1.0,
+        "oracle": {"beta_l2": 1.0, "beta_dram": 1.5, "beta_sm": 0.5, "noise_sigma": 0.05, "seed": 0},
+        "deployed": [{"model_id": m, "arrival_rate_rps": 100.0, "slo_ms": 100.0} for m in t16.models()[:2]]}
+pt, _ = engine.run_batch([spec], t16.arrays(), arrivals=[(t_arr, m_arr)], warmup_fraction=0.3)
+print("slo edges", int(pt.status()[0]))
