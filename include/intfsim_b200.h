@@ -127,7 +127,7 @@ typedef struct intf_replay_buffers {
   int32_t *n_mb;               /* scratch: [total models] batches formed per model */
   int32_t *slo_ws;             /* scratch: INTF_SLO_WS_INTS int32 for the grid-wide SLO path (long traces);
                                   slo_ws[0] is also intf_replay's scenario work counter */
-  int32_t *form_ws;            /* scratch: 3 int32 per list slot, pointer-doubling formation of long lists */
+  int32_t *form_ws;            /* scratch: 3 int32 per list slot, chunked formation of long lists */
   int32_t *order;              /* scratch: [n_scen + 1] replay order (longest-processing-time first) */
   int32_t seg_stride, cap_max;
   int32_t noise_k, pad_;       /* segments per batch whose noise is precomputed (0 = inline) */

@@ -355,88 +355,178 @@ __device__ __forceinline__ LongModel long_model(const intf_scenario* scen, const
   return r;
 }
 
-// J_0 = nxt into table 0; path[0] = 0
+// nxt(i) = i + cnt(i): the head after a batch starting at element i
 __global__ void k_form_nxt(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
                            int n_models, intf_replay_buffers B, const int32_t* blk) {
   const LongModel L = long_model(scen, models, n_models, B, blk);
   if (!L.ok || L.i >= L.n) return;
   const intf_model& M = models[L.g];
   const intf_scenario& S = scen[M.scen];
-  int32_t* ws = B.form_ws + 3ll * M.list_off;  // [J table A | J table B | path], list_cap each
+  int32_t* ws = B.form_ws + 3ll * M.list_off;  // [nxt | exit | count], list_cap each
   ws[L.i] = L.i + form_cnt(B.list_t + M.list_off, L.n, L.i, S.window_ms, S.max_bs);
-  if (L.i == 0) ws[2 * M.list_cap] = 0;
 }
 
-// level k: path[r] = J_k(path[r - 2^k]) for r in [2^k, 2^{k+1}); then J_{k+1} = J_k o J_k
-__global__ void k_form_extend(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                              int n_models, intf_replay_buffers B, int k) {
-  const LongModel L = long_model(scen, models, n_models, B);
-  if (!L.ok) return;
-  const intf_model& M = models[L.g];
-  int32_t* ws = B.form_ws + 3ll * M.list_off;
-  const int32_t* J = ws + (k & 1) * M.list_cap;
-  int32_t* path = ws + 2 * M.list_cap;
-  const int step = 1 << k, r = step + L.i;
-  if (L.i < step && r < L.n) {
-    const int prev = path[r - step];
-    path[r] = prev < L.n ? J[prev] : L.n;
-  }
-}
-__global__ void k_form_double(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                              int n_models, intf_replay_buffers B, int k, const int32_t* blk) {
-  const LongModel L = long_model(scen, models, n_models, B, blk);
-  if (!L.ok || L.i >= L.n) return;
-  const intf_model& M = models[L.g];
-  int32_t* ws = B.form_ws + 3ll * M.list_off;
-  const int32_t* J = ws + (k & 1) * M.list_cap;
-  int32_t* Jn = ws + ((k + 1) & 1) * M.list_cap;
-  const int a = J[L.i];
-  Jn[L.i] = a < L.n ? J[a] : L.n;
-}
-
-// batch r of the model: head path[r] (while < n); writes what form_model_warp writes
-__global__ void k_form_emit(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
-                            int n_models, intf_replay_buffers B, const int32_t* blk) {
-  const LongModel L = long_model(scen, models, n_models, B, blk);
-  if (!L.ok) {
-    // long models of bad scenarios form nothing
-    const int g = blk ? blk[2 * blockIdx.x] : blockIdx.z * gridDim.y + blockIdx.y;
-    const int chunk = blk ? blk[2 * blockIdx.x + 1] : blockIdx.x;
-    if (g < n_models && models[g].list_cap >= kLongForm && chunk == 0 && threadIdx.x == 0) B.n_mb[g] = 0;
-    return;
-  }
-  if (L.n == 0) {
-    if (L.i == 0) B.n_mb[L.g] = 0;
-    return;
-  }
-  if (L.i >= L.n) return;
-  const intf_model& M = models[L.g];
+// Long lists, chunked: the heads are the orbit of 0 under nxt(i) = i +
+// cnt(i).  (1) k_form_chunks, a block per 2,048-element chunk: for EVERY
+// element i of the chunk, the first head at or past the chunk's end reached
+// from i and the heads visited on the way (pointer doubling in shared
+// memory, 11 rounds) -> exit[i], count[i].  (2) k_form_compose, a thread per
+// model: the walk from 0 jumps chunk to chunk through exit[] (one step per
+// chunk), leaving each chunk's entry head and its first batch index in the
+// chunk's first slot.  (3) k_form_emit_chunks, a block per chunk: one lane
+// walks from the entry collecting the chunk's heads in shared memory, then the
+// block writes their batch records (what form_model_warp writes).  Four
+// launches instead of two per doubling level.
+constexpr int kFormChunk = 2048;
+constexpr int kFormChunkThreads = 256;
+struct FormChunk {
+  int g, c, n, lo, hi;  // model, chunk, list length, chunk [lo, hi)
+  bool ok;
+};
+__device__ __forceinline__ FormChunk form_chunk(const intf_scenario* scen, const intf_model* models, int n_models,
+                                                const intf_replay_buffers& B) {
+  FormChunk f;
+  f.g = blockIdx.z * gridDim.y + blockIdx.y;
+  f.c = blockIdx.x;
+  f.ok = false;
+  if (f.g >= n_models) return f;
+  const intf_model& M = models[f.g];
   const intf_scenario& S = scen[M.scen];
-  const int32_t* path = B.form_ws + 3ll * M.list_off + 2 * M.list_cap;
-  const int h = path[L.i];
-  if (h >= L.n) return;
-  if (L.i + 1 == L.n || path[L.i + 1] >= L.n) B.n_mb[L.g] = L.i + 1;  // last batch of the orbit
+  if (M.list_cap < kLongForm) return f;
+  if ((B.status[M.scen] & INTF_ST_OVERFLOW) || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 || S.max_bs < 1 ||
+      S.n_models > kMaxModels)
+    return f;
+  f.n = min(B.n_list[f.g], M.list_cap);
+  f.lo = f.c * kFormChunk;
+  f.hi = min(f.n, f.lo + kFormChunk);
+  f.ok = f.lo < f.n;
+  return f;
+}
+
+__global__ void __launch_bounds__(kFormChunkThreads) k_form_chunks(const intf_scenario* __restrict__ scen,
+                                                                   const intf_model* __restrict__ models,
+                                                                   int n_models, intf_replay_buffers B) {
+  const FormChunk f = form_chunk(scen, models, n_models, B);
+  if (!f.ok) return;
+  const intf_model& M = models[f.g];
+  const int32_t* nxt = B.form_ws + 3ll * M.list_off;
+  int32_t* exitv = B.form_ws + 3ll * M.list_off + M.list_cap;
+  int32_t* count = B.form_ws + 3ll * M.list_off + 2ll * M.list_cap;
+  __shared__ int32_t E[kFormChunk], K[kFormChunk];
+  const int len = f.hi - f.lo;
+  for (int j = threadIdx.x; j < len; j += blockDim.x) {
+    E[j] = nxt[f.lo + j];
+    K[j] = 1;
+  }
+  __syncthreads();
+  // E[j]: the element reached; inside the chunk it is a head still to be followed
+  for (int r = 0; (1 << r) < len; r++) {
+    int e2[kFormChunk / kFormChunkThreads], k2[kFormChunk / kFormChunkThreads];
+#pragma unroll
+    for (int u = 0; u < kFormChunk / kFormChunkThreads; u++) {
+      const int j = u * kFormChunkThreads + threadIdx.x;
+      e2[u] = -1;
+      if (j < len) {
+        const int e = E[j];
+        if (e < f.hi) {  // (e > lo + j >= lo: inside the chunk)
+          e2[u] = E[e - f.lo];
+          k2[u] = K[j] + K[e - f.lo];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kFormChunk / kFormChunkThreads; u++) {
+      const int j = u * kFormChunkThreads + threadIdx.x;
+      if (e2[u] >= 0) {
+        E[j] = e2[u];
+        K[j] = k2[u];
+      }
+    }
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < len; j += blockDim.x) {
+    exitv[f.lo + j] = E[j];
+    count[f.lo + j] = K[j];
+  }
+}
+
+// per long model: chunk entries and first batch indices into each chunk's
+// first exit / count slot (-1: no head in the chunk); n_mb = the batches
+__global__ void k_form_compose(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                               int n_models, intf_replay_buffers B) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_models) return;
+  const intf_model& M = models[g];
+  if (M.list_cap < kLongForm) return;
+  const intf_scenario& S = scen[M.scen];
+  if ((B.status[M.scen] & INTF_ST_OVERFLOW) || S.cap > B.cap_max || S.cap > kMaxCap || S.cap < 1 || S.max_bs < 1 ||
+      S.n_models > kMaxModels) {
+    B.n_mb[g] = 0;  // long models of bad scenarios form nothing
+    return;
+  }
+  const int n = min(B.n_list[g], M.list_cap);
+  int32_t* exitv = B.form_ws + 3ll * M.list_off + M.list_cap;
+  int32_t* count = B.form_ws + 3ll * M.list_off + 2ll * M.list_cap;
+  int h = 0, base = 0;
+  for (int c = 0; c * kFormChunk < n; c++) {
+    const int lo = c * kFormChunk;
+    if (h >= lo + kFormChunk || h >= n) {  // a batch skipped this whole chunk (or the orbit ended)
+      exitv[lo] = -1;
+      continue;
+    }
+    const int e = exitv[h], k = count[h];
+    exitv[lo] = h;
+    count[lo] = base;
+    base += k;
+    h = e;
+  }
+  B.n_mb[g] = base;
+}
+
+__global__ void __launch_bounds__(kFormChunkThreads) k_form_emit_chunks(const intf_scenario* __restrict__ scen,
+                                                                        const intf_model* __restrict__ models,
+                                                                        int n_models, intf_replay_buffers B) {
+  const FormChunk f = form_chunk(scen, models, n_models, B);
+  if (!f.ok) return;
+  const intf_model& M = models[f.g];
+  const intf_scenario& S = scen[M.scen];
+  const int32_t* nxt = B.form_ws + 3ll * M.list_off;
+  const int entry = B.form_ws[3ll * M.list_off + M.list_cap + f.lo];
+  const int base = B.form_ws[3ll * M.list_off + 2ll * M.list_cap + f.lo];
+  if (entry < 0) return;
+  __shared__ int32_t nx[kFormChunk], heads[kFormChunk];
+  __shared__ int n_heads;
+  const int len = f.hi - f.lo;
+  for (int j = threadIdx.x; j < len; j += blockDim.x) nx[j] = nxt[f.lo + j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int h = entry; h < f.hi; h = nx[h - f.lo]) heads[k++] = h;
+    n_heads = k;
+  }
+  __syncthreads();
   const double* lt = B.list_t + M.list_off;
   const int32_t* lrid = B.list_rid + M.list_off;
-  const int cnt = form_cnt(lt, L.n, h, S.window_ms, S.max_bs);
-  double t;
-  int kind;
-  uint32_t key;
-  if (cnt == S.max_bs) {  // early emit at max_batch_size (`batcher.py:70-71`)
-    t = lt[h + cnt - 1];
-    kind = KIND_ARRIVAL;
-    key = (uint32_t)lrid[h + cnt - 1];
-  } else {  // window expiry (`batcher.py:74-85`)
-    t = lt[h] + S.window_ms;
-    kind = KIND_WINDOW;
-    key = M.crc;
+  for (int j = threadIdx.x; j < n_heads; j += blockDim.x) {
+    const int h = heads[j];
+    const int cnt = nx[h - f.lo] - h;
+    double t;
+    int kind;
+    uint32_t key;
+    if (cnt == S.max_bs) {  // early emit at max_batch_size (`batcher.py:70-71`)
+      t = lt[h + cnt - 1];
+      kind = KIND_ARRIVAL;
+      key = (uint32_t)lrid[h + cnt - 1];
+    } else {  // window expiry (`batcher.py:74-85`)
+      t = lt[h] + S.window_ms;
+      kind = KIND_WINDOW;
+      key = M.crc;
+    }
+    const int i = base + j;
+    B.mb_t[M.list_off + i] = t;
+    reinterpret_cast<int4*>(B.mb_info)[M.list_off + i] = make_int4(kind, (int32_t)key, cnt, h);
   }
-  B.mb_t[M.list_off + L.i] = t;
-  int32_t* info = B.mb_info + 4ll * (M.list_off + L.i);
-  info[0] = kind;
-  info[1] = (int32_t)key;
-  info[2] = cnt;
-  info[3] = h;
 }
 
 __global__ void k_merge_batches(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
@@ -2309,16 +2399,13 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
     const dim3 grid = blk ? dim3((unsigned)bt->n_long_blocks) : dim3(ceil_div(bt->max_list_cap, 256), y, ceil_div(m, y));
     k_form_nxt<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, blk);
     if ((rc = launch_status("k_form_nxt"))) return rc;
-    for (int k = 0; (1ll << k) < bt->max_list_cap; k++) {
-      k_form_extend<<<dim3(ceil_div(1ll << k < bt->max_list_cap ? 1ll << k : bt->max_list_cap, 256), y,
-                           ceil_div(m, y)), 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, k);
-      if ((rc = launch_status("k_form_extend"))) return rc;
-      if ((2ll << k) >= bt->max_list_cap) break;  // the path is complete
-      k_form_double<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, k, blk);
-      if ((rc = launch_status("k_form_double"))) return rc;
-    }
-    k_form_emit<<<grid, 256, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf, blk);
-    if ((rc = launch_status("k_form_emit"))) return rc;
+    const dim3 cgrid(ceil_div(bt->max_list_cap, kFormChunk), y, ceil_div(m, y));
+    k_form_chunks<<<cgrid, kFormChunkThreads, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_form_chunks"))) return rc;
+    k_form_compose<<<ceil_div(bt->n_models, 128), 128, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_form_compose"))) return rc;
+    k_form_emit_chunks<<<cgrid, kFormChunkThreads, 0, st>>>(bt->scen, bt->models, bt->n_models, *buf);
+    if ((rc = launch_status("k_form_emit_chunks"))) return rc;
   }
   if (bt->max_list_cap < kLongForm) {  // short lists: one warp per model
     k_merge_batches_warp<<<ceil_div(bt->n_models, kMergeWarps), 32 * kMergeWarps, 0, st>>>(bt->scen, bt->models,
