@@ -210,6 +210,206 @@ __global__ void k_merge_arrivals(const intf_scenario* __restrict__ scen, const i
   }
 }
 
+// The same merge by time buckets (long traces: a 10^6-request C4 trace spent
+// 180 us in the 15 binary searches per element above).  Per scenario, in its
+// share of form_ws (free until formation): nb = 2^k >= req_cap / 16 bucket
+// counters and req_cap member slots.  Buckets are floor(t * nb / horizon),
+// monotone in t; an element's merged position = its bucket's start + the
+// members of its bucket that precede it under the same order as
+// count_before ((t, name rank), then list index).  A bucket above 64 members
+// (bursts) falls back to the binary searches for its elements.
+constexpr int kArrBucketAvg = 16, kArrBucketMax = 64;
+constexpr int kArrTile = 4096;  // buckets per scan tile (a block: 1024 threads x int4)
+struct ArrBuckets {
+  int32_t *cnt, *slot, *tile;  // local (per-tile) bucket offsets, members, tile offsets
+  int nb;
+  double scale;
+  bool ok;
+};
+__device__ __forceinline__ ArrBuckets arr_buckets(const intf_scenario& S, const intf_model* __restrict__ models,
+                                                  const intf_replay_buffers& B) {
+  const intf_model& f = models[S.model_off];
+  const intf_model& l = models[S.model_off + S.n_models - 1];
+  const long long room = 3ll * ((long long)l.list_off + l.list_cap - f.list_off);
+  int nb = 1;
+  while ((long long)nb * kArrBucketAvg < S.req_cap) nb <<= 1;
+  ArrBuckets A;
+  A.cnt = B.form_ws + 3ll * f.list_off;
+  A.slot = A.cnt + nb;
+  A.tile = A.slot + S.req_cap;
+  A.nb = nb;
+  A.scale = (double)nb / (S.duration_s * 1000.0);
+  A.ok = B.form_ws && S.duration_s > 0.0 && (long long)nb + S.req_cap + nb / kArrTile + 1 <= room &&
+         S.n_models <= kMaxModels;
+  return A;
+}
+// global offset of bucket b's current local counter
+__device__ __forceinline__ int arr_at(const ArrBuckets& A, int b) { return A.cnt[b] + A.tile[b / kArrTile]; }
+__device__ __forceinline__ int arr_bucket(const ArrBuckets& A, double t) {
+  const double v = t * A.scale;
+  return v < 0.0 ? 0 : (v >= (double)A.nb ? A.nb - 1 : (int)v);
+}
+// model list element (g, j) of a merge grid (as k_merge_arrivals)
+struct ArrElem {
+  int g, j, n;
+  bool ok;
+};
+__device__ __forceinline__ ArrElem arr_elem(const intf_scenario* scen, const intf_model* models, int n_models,
+                                            const intf_replay_buffers& B, int j) {
+  ArrElem e;
+  e.g = blockIdx.z * gridDim.y + blockIdx.y;
+  e.j = j;
+  e.ok = false;
+  if (e.g >= n_models) return e;
+  const intf_model& M = models[e.g];
+  if (B.status[M.scen] & INTF_ST_OVERFLOW) return e;
+  e.n = min(B.n_list[e.g], M.list_cap);
+  e.ok = true;
+  return e;
+}
+__global__ void __launch_bounds__(1024) k_arr_zero(const intf_scenario* __restrict__ scen,
+                                                   const intf_model* __restrict__ models, intf_replay_buffers B) {
+  const int s = blockIdx.y;  // (grid: tiles x scenarios)
+  if (B.status[s] & INTF_ST_OVERFLOW) return;
+  const ArrBuckets A = arr_buckets(scen[s], models, B);
+  if (!A.ok) return;
+  const int t0 = blockIdx.x * kArrTile;
+  for (int b = t0 + threadIdx.x; b < min(A.nb, t0 + kArrTile); b += blockDim.x) A.cnt[b] = 0;
+}
+__global__ void k_arr_hist(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                           intf_replay_buffers B, int n_models) {
+  const ArrElem e = arr_elem(scen, models, n_models, B, 0);
+  if (!e.ok) return;
+  const intf_model& M = models[e.g];
+  const ArrBuckets A = arr_buckets(scen[M.scen], models, B);
+  if (!A.ok) return;
+  const double* lt = B.list_t + M.list_off;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < e.n; j += gridDim.x * blockDim.x)
+    atomicAdd(&A.cnt[arr_bucket(A, lt[j])], 1);
+}
+// exclusive scan of the bucket counts: (1) per tile of kArrTile buckets, one
+// block each (coalesced int4 loads), local offsets + the tile's total into
+// tile[]; (2) one block per scenario scans the tile totals
+__global__ void __launch_bounds__(1024) k_arr_scan_tiles(const intf_scenario* __restrict__ scen,
+                                                         const intf_model* __restrict__ models,
+                                                         intf_replay_buffers B) {
+  __shared__ int wsum[32];
+  const int s = blockIdx.y;  // (grid: tiles x scenarios)
+  if (B.status[s] & INTF_ST_OVERFLOW) return;
+  const ArrBuckets A = arr_buckets(scen[s], models, B);
+  if (!A.ok) return;
+  const int t0 = blockIdx.x * kArrTile;
+  if (t0 >= A.nb) return;
+  const int b0 = t0 + 4 * threadIdx.x;  // (4 consecutive counters per thread; form_ws offsets are only 4-byte aligned)
+  int4 v = make_int4(0, 0, 0, 0);
+  if (b0 < A.nb) v.x = A.cnt[b0];
+  if (b0 + 1 < A.nb) v.y = A.cnt[b0 + 1];
+  if (b0 + 2 < A.nb) v.z = A.cnt[b0 + 2];
+  if (b0 + 3 < A.nb) v.w = A.cnt[b0 + 3];
+  const int sum = v.x + v.y + v.z + v.w;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int u = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, u, o);
+      if (lane >= o) u += y;
+    }
+    wsum[lane] = u;
+  }
+  __syncthreads();
+  const int run = (w ? wsum[w - 1] : 0) + x - sum;
+  if (b0 < A.nb) A.cnt[b0] = run;
+  if (b0 + 1 < A.nb) A.cnt[b0 + 1] = run + v.x;
+  if (b0 + 2 < A.nb) A.cnt[b0 + 2] = run + v.x + v.y;
+  if (b0 + 3 < A.nb) A.cnt[b0 + 3] = run + v.x + v.y + v.z;
+  if (threadIdx.x == blockDim.x - 1) A.tile[blockIdx.x] = wsum[31];  // the tile's total (before the scan below)
+}
+__global__ void k_arr_scan_top(const intf_scenario* __restrict__ scen, int n_scen,
+                               const intf_model* __restrict__ models, intf_replay_buffers B) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_scen; s += gridDim.x * blockDim.x) {
+    if (B.status[s] & INTF_ST_OVERFLOW) continue;
+    const ArrBuckets A = arr_buckets(scen[s], models, B);
+    if (!A.ok) continue;
+    int run = 0;
+    for (int k = 0; k * kArrTile < A.nb; k++) {
+      const int c = A.tile[k];
+      A.tile[k] = run;
+      run += c;
+    }
+  }
+}
+__global__ void k_arr_scatter(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                              intf_replay_buffers B, int n_models) {
+  const ArrElem e = arr_elem(scen, models, n_models, B, 0);
+  if (!e.ok) return;
+  const intf_model& M = models[e.g];
+  const intf_scenario& S = scen[M.scen];
+  const ArrBuckets A = arr_buckets(S, models, B);
+  if (!A.ok) return;
+  const double* lt = B.list_t + M.list_off;
+  const int q = e.g - S.model_off;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < e.n; j += gridDim.x * blockDim.x) {
+    const int b = arr_bucket(A, lt[j]);
+    const int p = atomicAdd(&A.cnt[b], 1) + A.tile[b / kArrTile];  // (afterwards cnt[b] = the bucket's local end)
+    if (p < S.req_cap) A.slot[p] = (q << 24) | j;
+  }
+}
+__global__ void k_arr_place(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                            intf_replay_buffers B, int n_models) {
+  const ArrElem e = arr_elem(scen, models, n_models, B, 0);
+  if (!e.ok) return;
+  const intf_model& M = models[e.g];
+  const intf_scenario& S = scen[M.scen];
+  const ArrBuckets A = arr_buckets(S, models, B);
+  const double* lt = B.list_t + M.list_off;
+  const int q = e.g - S.model_off;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < e.n; j += gridDim.x * blockDim.x) {
+    const double t = lt[j];
+    int pos = -1;
+    if (A.ok) {
+      const int b = arr_bucket(A, t);
+      const int lo = b ? arr_at(A, b - 1) : 0, hi = arr_at(A, b);
+      if (hi - lo <= kArrBucketMax) {
+        int r = 0;
+        for (int k = lo; k < hi; k++) {
+          const int v = A.slot[k], q2 = v >> 24, j2 = v & 0xffffff;
+          if (q2 == q) {
+            r += j2 < j ? 1 : 0;
+          } else {
+            const intf_model& Q = models[S.model_off + q2];
+            const double t2 = B.list_t[Q.list_off + j2];
+            r += (t2 < t || (t2 == t && Q.name_rank < M.name_rank)) ? 1 : 0;
+          }
+        }
+        pos = lo + r;
+      }
+    }
+    if (pos < 0) {  // (no buckets for this scenario, or a burst bucket)
+      pos = j;
+      for (int q2 = 0; q2 < S.n_models; q2++) {
+        if (q2 == q) continue;
+        const intf_model& Q = models[S.model_off + q2];
+        pos += count_before(B.list_t + Q.list_off, min(B.n_list[S.model_off + q2], Q.list_cap), t,
+                            Q.name_rank < M.name_rank);
+      }
+    }
+    if (pos < S.req_cap) {
+      B.list_rid[M.list_off + j] = pos;
+      B.arr_t[S.req_off + pos] = t;
+      B.arr_model[S.req_off + pos] = q;
+    }
+  }
+}
+
 // The same merge with one block per SCENARIO for sweeps of many short
 // scenarios: the scenario's model lists are staged in shared memory once and
 // every element's rank is a binary search there (the per-model-list blocks
@@ -2459,6 +2659,17 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
     k_merge_arrivals_scen<<<bt->n_scen < 65535 ? bt->n_scen : 65535, 256, 0, st>>>(bt->scen, bt->n_scen, bt->models,
                                                                                  *buf);
     return launch_status("k_merge_arrivals_scen");
+  }
+  if (buf->form_ws && bt->max_list_cap >= kLongForm && bt->n_scen <= 65535) {  // long traces: time buckets
+    const dim3 g = merge_grid(bt);
+    const dim3 tiles(ceil_div(bt->max_req_cap / kArrBucketAvg * 2 + 1, kArrTile), bt->n_scen);
+    k_arr_zero<<<tiles, 1024, 0, st>>>(bt->scen, bt->models, *buf);
+    k_arr_hist<<<g, 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
+    k_arr_scan_tiles<<<tiles, 1024, 0, st>>>(bt->scen, bt->models, *buf);
+    k_arr_scan_top<<<ceil_div(bt->n_scen, 128), 128, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
+    k_arr_scatter<<<g, 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
+    k_arr_place<<<g, 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
+    return launch_status("k_arr_place");
   }
   k_merge_arrivals<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
   return launch_status("k_merge_arrivals");
