@@ -222,20 +222,8 @@ INTF_FN double pcg_next_double(Pcg64& g) {
   return (double)(pcg_next64(g) >> 11) * (1.0 / 9007199254740992.0);
 }
 
-// words: entropy as uint32 words (n in [1, 8]).
-INTF_FN Pcg64 pcg_seed_words(const uint32_t* w, int n) {
-  uint32_t pool[4];
-  uint32_t hc = 0x43b0d7e5u;
-#pragma unroll
-  for (int i = 0; i < 4; i++) pool[i] = ss_hashmix(i < n ? w[i] : 0u, hc);
-#pragma unroll
-  for (int s = 0; s < 4; s++)
-#pragma unroll
-    for (int d = 0; d < 4; d++)
-      if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], hc));
-  for (int s = 4; s < n; s++)
-#pragma unroll
-    for (int d = 0; d < 4; d++) pool[d] = ss_mix(pool[d], ss_hashmix(w[s], hc));
+// generate_state(4, uint64) from the mixed pool, then numpy's PCG64 seeding
+INTF_FN Pcg64 pcg_from_pool(const uint32_t pool[4]) {
   uint32_t hb = 0x8b51f9ddu, out[8];
 #pragma unroll
   for (int i = 0; i < 8; i++) {
@@ -252,6 +240,23 @@ INTF_FN Pcg64 pcg_seed_words(const uint32_t* w, int n) {
   g.state = g.inc + (((unsigned __int128)s0 << 64) | s1);
   pcg_step(g);
   return g;
+}
+
+// words: entropy as uint32 words (n in [1, 8]).
+INTF_FN Pcg64 pcg_seed_words(const uint32_t* w, int n) {
+  uint32_t pool[4];
+  uint32_t hc = 0x43b0d7e5u;
+#pragma unroll
+  for (int i = 0; i < 4; i++) pool[i] = ss_hashmix(i < n ? w[i] : 0u, hc);
+#pragma unroll
+  for (int s = 0; s < 4; s++)
+#pragma unroll
+    for (int d = 0; d < 4; d++)
+      if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], hc));
+  for (int s = 4; s < n; s++)
+#pragma unroll
+    for (int d = 0; d < 4; d++) pool[d] = ss_mix(pool[d], ss_hashmix(w[s], hc));
+  return pcg_from_pool(pool);
 }
 
 // numpy _int_to_uint32_array: little-endian 32-bit words, 0 -> [0].
@@ -311,6 +316,56 @@ INTF_FN double noise_draw(uint64_t oracle_seed, uint64_t batch_id, uint64_t seg_
   Pcg64 g = pcg_seed_words(w, n);
   double z = zig_normal(g);
   return glibc_exp(0.0 + sigma * z);
+}
+
+// noise_draw(seed, batch, j) for j = 0 .. K-1 at once: with seed and batch
+// below 2^32 the entropy is [seed, batch, j] (three words), and the pool
+// values that do not involve j -- pool[0], pool[1], pool[3] through the first
+// two mixing rounds and the hashes they mix into pool[2] -- are computed once
+// (9 of the 16 hashmix calls); each draw then pays pool[2]'s init, two
+// mixing rounds and the output stage.  Bit-identical to noise_draw (the
+// hashmix constant advances identically: it depends only on the call index).
+INTF_FN void noise_draws_k(uint64_t oracle_seed, uint64_t batch_id, int K, double sigma, double* out) {
+  if (sigma == 0.0) {
+    for (int j = 0; j < K; j++) out[j] = 1.0;
+    return;
+  }
+  if ((oracle_seed >> 32) || (batch_id >> 32)) {
+    for (int j = 0; j < K; j++) out[j] = noise_draw(oracle_seed, batch_id, (uint64_t)j, sigma);
+    return;
+  }
+  uint32_t hc = 0x43b0d7e5u;
+  uint32_t p0 = ss_hashmix((uint32_t)oracle_seed, hc);  // call 0
+  uint32_t p1 = ss_hashmix((uint32_t)batch_id, hc);     // call 1
+  const uint32_t hc2 = hc;                              // call 2: pool[2] = hashmix(j), per draw
+  hc *= 0x931e8875u;
+  uint32_t p3 = ss_hashmix(0u, hc);  // call 3
+  // round 0 (source pool[0]) and round 1 (source pool[1]): independent of j
+  p1 = ss_mix(p1, ss_hashmix(p0, hc));
+  const uint32_t h02 = ss_hashmix(p0, hc);
+  p3 = ss_mix(p3, ss_hashmix(p0, hc));
+  p0 = ss_mix(p0, ss_hashmix(p1, hc));
+  const uint32_t h12 = ss_hashmix(p1, hc);
+  p3 = ss_mix(p3, ss_hashmix(p1, hc));
+  const uint32_t hc_r2 = hc;
+  for (int j = 0; j < K; j++) {
+    uint32_t h = hc2;
+    uint32_t q2 = ss_hashmix((uint32_t)j, h);
+    q2 = ss_mix(q2, h02);
+    q2 = ss_mix(q2, h12);
+    uint32_t a0 = p0, a1 = p1, a3 = p3;
+    h = hc_r2;
+    // round 2 (source pool[2]), round 3 (source pool[3])
+    a0 = ss_mix(a0, ss_hashmix(q2, h));
+    a1 = ss_mix(a1, ss_hashmix(q2, h));
+    a3 = ss_mix(a3, ss_hashmix(q2, h));
+    a0 = ss_mix(a0, ss_hashmix(a3, h));
+    a1 = ss_mix(a1, ss_hashmix(a3, h));
+    q2 = ss_mix(q2, ss_hashmix(a3, h));
+    const uint32_t pool[4] = {a0, a1, q2, a3};
+    Pcg64 g = pcg_from_pool(pool);
+    out[j] = glibc_exp(0.0 + sigma * zig_normal(g));
+  }
 }
 
 // oracle_slowdown (`oracle.py:36-47`); dot = OpenBLAS ddot (fma chain).

@@ -834,24 +834,21 @@ __global__ void __launch_bounds__(256) k_noise_table(const intf_scenario* __rest
     for (int s = blockIdx.x; s < n_scen; s += gridDim.x) {
       const intf_scenario& S = scen[s];
       const int Ks = S.cap == 1 ? 1 : K;
-      const long long n = (long long)B.n_batches[s] * Ks;
       double* out = B.noise_tab + (long long)S.req_off * K;
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-        const long long b = i / Ks;
-        const int j = (int)(i - b * Ks);
-        out[b * K + j] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)b, (uint64_t)j, S.sigma);
-      }
+      // a thread per batch: its Ks draws share the SeedSequence work that does
+      // not involve the segment index (noise_draws_k)
+      for (long long b = threadIdx.x; b < B.n_batches[s]; b += blockDim.x)
+        noise_draws_k(S.oracle_seed, S.batch_id_base + (uint64_t)b, Ks, S.sigma, out + b * K);
     }
     return;
   }
-  const long long n = req_slots * K;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long slot = i / K;
+  for (long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x; slot < req_slots;
+       slot += (long long)gridDim.x * blockDim.x) {
     const int s = scen_of_slot(scen, n_scen, slot);
     const intf_scenario& S = scen[s];
     const long long b = slot - S.req_off;
-    if (b < B.n_batches[s] && (S.cap != 1 || i % K == 0))
-      B.noise_tab[i] = noise_draw(S.oracle_seed, S.batch_id_base + (uint64_t)b, (uint64_t)(i % K), S.sigma);
+    if (b < B.n_batches[s])
+      noise_draws_k(S.oracle_seed, S.batch_id_base + (uint64_t)b, S.cap == 1 ? 1 : K, S.sigma, B.noise_tab + slot * K);
   }
 }
 
@@ -2565,8 +2562,9 @@ __global__ void k_features(const intf_scenario* __restrict__ scen, int n_scen, l
 }
 
 unsigned noise_grid(const intf_batch* bt, int K) {
+  (void)K;
   if (bt->n_scen >= kPerScenarioMin) return bt->n_scen < 65535 ? bt->n_scen : 65535;
-  const long long n = (long long)bt->req_slots * K;
+  const long long n = (long long)bt->req_slots;  // (a thread per batch slot)
   const long long blocks = (n + 255) / 256;
   return (unsigned)(blocks < 148 * 16 ? (blocks > 0 ? blocks : 1) : 148 * 16);
 }

@@ -25,6 +25,9 @@ def lib():
         L.hc_features.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_longlong] + [ctypes.c_void_p] * 3
         L.hc_noise.restype = ctypes.c_double
         L.hc_noise.argtypes = [ctypes.c_ulonglong, ctypes.c_uint, ctypes.c_uint, ctypes.c_double]
+        L.hc_noise_k_mismatch.restype = ctypes.c_longlong
+        L.hc_noise_k_mismatch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int,
+                                          ctypes.c_double]
         for f in ("hc_exp", "hc_log1p"):
             getattr(L, f).restype = ctypes.c_double
             getattr(L, f).argtypes = [ctypes.c_double]

@@ -85,5 +85,17 @@ extern "C" void hc_features(const intf_batch* bt, const intf_table* tab, const i
 extern "C" double hc_noise(unsigned long long seed, unsigned b, unsigned k, double sigma) {
   return noise_draw(seed, b, k, sigma);
 }
+// noise_draws_k (the noise table's shared-prefix form) vs noise_draw per
+// draw: mismatching draws counted over n (seed, batch) pairs x K segments
+extern "C" long long hc_noise_k_mismatch(const unsigned long long* seed, const unsigned long long* batch, long long n,
+                                         int K, double sigma) {
+  long long bad = 0;
+  double out[16];
+  for (long long i = 0; i < n; i++) {
+    noise_draws_k(seed[i], batch[i], K, sigma, out);
+    for (int j = 0; j < K; j++) bad += out[j] != noise_draw(seed[i], batch[i], (uint64_t)j, sigma);
+  }
+  return bad;
+}
 extern "C" double hc_exp(double x) { return glibc_exp(x); }
 extern "C" double hc_log1p(double x) { return glibc_log1p(x); }

@@ -75,3 +75,22 @@ def test_hostcheck_empty_and_tiny_scenarios():
     res = driver.run([empty, tiny], tab)
     assert int(res["bufs"]["n_req"][0]) == 0 and int(res["bufs"]["n_batches"][0]) == 0
     assert int(res["bufs"]["status"][0]) == 0 and int(res["bufs"]["status"][1]) == 0
+
+
+def test_noise_table_shared_prefix_equals_per_draw():
+    """noise_draws_k (the noise table: K draws of one batch sharing the
+    SeedSequence work that does not involve the segment index) equals
+    noise_draw draw by draw, for seeds / batch ids below and above 2^32 (the
+    latter take the per-draw path) and sigma 0."""
+    import ctypes
+
+    import numpy as np
+
+    L = driver.lib()
+    rng = np.random.default_rng(3)
+    seed = np.concatenate([rng.integers(0, 2**32, 3000), [0, 1, 2**32 - 1, 2**32, 2**40 + 5]]).astype(np.uint64)
+    batch = np.concatenate([rng.integers(0, 2**32, 3000), [0, 2**32 - 1, 7, 3, 2**33]]).astype(np.uint64)
+    for sigma in (0.05, 0.3, 0.0):
+        bad = L.hc_noise_k_mismatch(seed.ctypes.data_as(ctypes.c_void_p), batch.ctypes.data_as(ctypes.c_void_p),
+                                    len(seed), 8, sigma)
+        assert bad == 0, (sigma, bad)
