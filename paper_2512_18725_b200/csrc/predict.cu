@@ -1641,6 +1641,22 @@ __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, co
   // far inside the 1e-5 tolerance of the refit path
   const double inv_lam = 1.0 / lam;
   int st = 0;
+  // P exactly symmetric: from the start if P0 is (one transpose), else after
+  // the first update's symmetrization
+  bool sym;
+  {
+    double(*T)[8] = tr[gi];
+    if (r < 7) {
+#pragma unroll
+      for (int j = 0; j < 7; j++) T[r][j] = P[j];
+    }
+    __syncwarp(gmask);
+    bool mine = true;
+#pragma unroll
+    for (int j = 0; j < 7; j++) mine &= P[j] == T[j][rr];
+    sym = __all_sync(gmask, mine);
+    __syncwarp(gmask);
+  }
   const long long i0 = live ? off[s] : 0, i1 = live ? (end ? end[s] : off[s + 1]) : 0;
   // the next sample's row is loaded one update ahead (off the update chain)
   double zn[6], yn = 0.0;
@@ -1684,29 +1700,38 @@ __global__ void __launch_bounds__(128) k_rls_g8(const double* __restrict__ X, co
     double pzr = Pz[0];  // Pz[rr] without dynamic register indexing
 #pragma unroll
     for (int j = 1; j < 7; j++) pzr = j == rr ? Pz[j] : pzr;
-        const double kr = pzr * (1.0 / denom);
-    double k[7];
-#pragma unroll
-    for (int j = 0; j < 7; j++) k[j] = __shfl_sync(gmask, kr, j, kRlsGroup);
+    const double rd = 1.0 / denom;
+    // k = Pz / denom, every lane from the shuffled Pz (no second shuffle round)
     const double e = ycur - yh;
 #pragma unroll
-    for (int j = 0; j < 7; j++) w[j] = w[j] + k[j] * e;
+    for (int j = 0; j < 7; j++) w[j] = w[j] + (Pz[j] * rd) * e;
+    if (sym) {
+      // P is exactly symmetric: (Pz_r Pz_j) rd is the same product for (r, j)
+      // and (j, r), so the update keeps it symmetric bit for bit and the
+      // symmetrization (`predict.py:152`) is the identity -- no transpose
 #pragma unroll
-    for (int j = 0; j < 7; j++) P[j] = (P[j] - kr * Pz[j]) * inv_lam;
-    // symmetrize: lane r needs P[j][r] of every row j
-    double(*T)[8] = tr[gi];
-    if (r < 7) {
+      for (int j = 0; j < 7; j++) P[j] = (P[j] - (pzr * Pz[j]) * rd) * inv_lam;
+    } else {
+      // P not exactly symmetric (P0 = inv(G) is symmetric only up to rounding):
+      // the reference's order, update then symmetrize; lane r needs P[j][r] of every row j
+      const double kr = pzr * rd;
 #pragma unroll
-      for (int j = 0; j < 7; j++) T[r][j] = P[j];
+      for (int j = 0; j < 7; j++) P[j] = (P[j] - kr * Pz[j]) * inv_lam;
+      double(*T)[8] = tr[gi];
+      if (r < 7) {
+#pragma unroll
+        for (int j = 0; j < 7; j++) T[r][j] = P[j];
+      }
+      __syncwarp(gmask);
+      // all 7 loads first, no branch: the diagonal term is 0.5 (a + a) == a exactly
+      double pt[7];
+#pragma unroll
+      for (int j = 0; j < 7; j++) pt[j] = T[j][rr];
+#pragma unroll
+      for (int j = 0; j < 7; j++) P[j] = 0.5 * (P[j] + pt[j]);  // == 0.5 (P[rr][j] + P[j][rr]) == the (j, rr) entry
+      __syncwarp(gmask);
+      sym = true;
     }
-    __syncwarp(gmask);
-    // all 7 loads first, no branch: the diagonal term is 0.5 (a + a) == a exactly
-    double pt[7];
-#pragma unroll
-    for (int j = 0; j < 7; j++) pt[j] = T[j][rr];
-#pragma unroll
-    for (int j = 0; j < 7; j++) P[j] = 0.5 * (P[j] + pt[j]);  // == 0.5 (P[rr][j] + P[j][rr]) == the (j, rr) entry
-    __syncwarp(gmask);
     bool fin = true;
 #pragma unroll
     for (int j = 0; j < 7; j++) fin &= isfinite(w[j]);

@@ -260,6 +260,9 @@ __global__ void k_scalar(int op, ScalarArgs a, double* __restrict__ out) {
       z[6] = 1.0;
       const double y = dbits(a.u[62]), lam = dbits(a.u[63]), inv_lam = 1.0 / lam;
       const double yh = predict7(w, z);
+      bool sym = true;  // as k_rls_g8: an exactly symmetric P takes the symmetric update, no symmetrization
+      for (int r = 0; r < 7; r++)
+        for (int j = 0; j < 7; j++) sym &= P[r * 7 + j] == P[j * 7 + r];
       for (int r = 0; r < 7; r++) {
         double acc = 0.0;
         for (int j = 0; j < 7; j++) acc = fma(P[r * 7 + j], z[j], acc);
@@ -281,11 +284,16 @@ __global__ void k_scalar(int op, ScalarArgs a, double* __restrict__ out) {
       for (int r = 0; r < 7; r++) k[r] = Pz[r] * inv_den;
       const double e = y - yh;
       for (int j = 0; j < 7; j++) w[j] = w[j] + k[j] * e;
-      double Pn[49];
-      for (int r = 0; r < 7; r++)
-        for (int j = 0; j < 7; j++) Pn[r * 7 + j] = (P[r * 7 + j] - k[r] * Pz[j]) * inv_lam;
-      for (int r = 0; r < 7; r++)
-        for (int j = 0; j < 7; j++) P[r * 7 + j] = 0.5 * (Pn[r * 7 + j] + Pn[j * 7 + r]);
+      if (sym) {
+        for (int r = 0; r < 7; r++)
+          for (int j = 0; j < 7; j++) P[r * 7 + j] = (P[r * 7 + j] - (Pz[r] * Pz[j]) * inv_den) * inv_lam;
+      } else {
+        double Pn[49];
+        for (int r = 0; r < 7; r++)
+          for (int j = 0; j < 7; j++) Pn[r * 7 + j] = (P[r * 7 + j] - k[r] * Pz[j]) * inv_lam;
+        for (int r = 0; r < 7; r++)
+          for (int j = 0; j < 7; j++) P[r * 7 + j] = 0.5 * (Pn[r * 7 + j] + Pn[j * 7 + r]);
+      }
       bool fin = true;
       for (int j = 0; j < 7; j++) fin &= isfinite(w[j]);
       for (int j = 0; j < 7; j++) out[j] = w[j];
