@@ -15,6 +15,8 @@ P = int(os.environ.get("PIPES", "3"))
 ev = os.environ.get("EVAL", "1") == "1"
 nk = int(os.environ.get("NOISE_K", "6"))
 steps = int(os.environ.get("STEPS", "20"))
+feat = os.environ.get("FEAT", "1") == "1"  # (EVAL=0 only)
+slo = os.environ.get("SLO", "1") == "1"
 table = gen_synthetic_profiles()
 preds = [_abi.Predictor(ewma=0, alpha=1.0, w=(0.0,) * 7), _abi.Predictor(ewma=1, alpha=0.5, w=(0.0,) * 7)]
 specs = lpt_order(c5_scenarios(table, 10000))
@@ -32,9 +34,9 @@ for s in streams:
     s.wait_event(e0)
 for k in range(steps):
     with torch.cuda.stream(streams[k % P]):
-        pipes[k % P].run()
+        pipes[k % P].run(features=feat, slo=slo)
 for s in streams:
     torch.cuda.current_stream().wait_stream(s)
 e1.record()
 torch.cuda.synchronize()
-print(f"PIPES={P} EVAL={int(ev)} NOISE_K={nk}: {e0.elapsed_time(e1) / steps:.3f} ms per sweep")
+print(f"PIPES={P} EVAL={int(ev)} FEAT={int(feat)} SLO={int(slo)} NOISE_K={nk}: {e0.elapsed_time(e1) / steps:.3f} ms per sweep")
