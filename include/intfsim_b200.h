@@ -94,7 +94,7 @@ typedef struct intf_batch {
   int32_t n_long_blocks, pad_;
 } intf_batch;
 #ifndef INTF_LONG_LIST
-#define INTF_LONG_LIST 4096 /* model lists this long form batches by pointer doubling */
+#define INTF_LONG_LIST 4096 /* model lists this long form batches by chunks (and merge arrivals by time buckets) */
 #endif
 int intf_long_list(void); /* INTF_LONG_LIST as built (the long_blocks map must use it) */
 

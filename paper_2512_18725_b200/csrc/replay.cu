@@ -24,7 +24,7 @@ namespace {
 #define INTF_BIG_LIST 4096
 #endif
 constexpr int kBigList = INTF_BIG_LIST;  // model lists this long: parallel gaps + one-thread scan (long traces)
-constexpr int kLongForm = INTF_LONG_LIST;  // model lists this long: pointer-doubling batch formation
+constexpr int kLongForm = INTF_LONG_LIST;  // model lists this long: chunked batch formation, time-bucket arrival merge
 constexpr int kBigJobs = 1 << 15;  // scenarios this long: block-parallel job plan / verify
 constexpr int kGapRun = 8;      // consecutive draws per thread in k_gen_gaps
 
@@ -2589,7 +2589,7 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
   k_form_models<<<ceil_div(bt->n_models, kFormModelWarps), 32 * kFormModelWarps, 0, st>>>(bt->scen, bt->models,
                                                                                          bt->n_models, *buf);
   if ((rc = launch_status("k_form_models"))) return rc;
-  if (bt->max_list_cap >= kLongForm) {  // long model lists: pointer-doubling formation
+  if (bt->max_list_cap >= kLongForm) {  // long model lists: chunked formation
     if (!buf->form_ws) return bad_input("formation of long lists needs form_ws scratch");
     const unsigned m = (unsigned)bt->n_models, y = m < 65535u ? m : 65535u;
     // flat grid over the long lists' 256-entry chunks when the caller gave the map
