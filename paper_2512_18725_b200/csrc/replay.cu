@@ -1846,7 +1846,10 @@ __global__ void k_jobs_verify(const intf_scenario* __restrict__ scen, int n_scen
 // records still matching a quantile's prefix are compacted after each pass,
 // and once every (model, quantile)'s selected bin holds <= kSloFinish records
 // one warp per (model, quantile) ranks them directly.
-constexpr int kSloThreads = 256;
+#ifndef INTF_SLO_THREADS
+#define INTF_SLO_THREADS 256
+#endif
+constexpr int kSloThreads = INTF_SLO_THREADS;
 constexpr int kSloGroup = 4;          // models per radix pass group (smem: 12 KB of histograms)
 constexpr int kSloBigReq = 1 << 16;  // above this request capacity: grid-wide SLO passes
 #ifndef INTF_SLO_CACHE
