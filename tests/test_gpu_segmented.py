@@ -47,6 +47,8 @@ def test_long_trace_segmented_equals_serial(slow, min_len, passes):
     if passes >= 0:
         pipe, h, stats = _run([spec], ta, slow=slow, min_len=min_len, passes=passes)
         assert stats["jobs_final"] > 10, stats  # the trace really was replayed in parallel pieces
+        if min_len <= 4:  # more jobs than one 6,144-job verify tile (k_jobs_verify_big's tile loop)
+            assert stats["jobs_initial"] > 6144, stats
     else:
         pipe = engine.ReplayPipeline([spec], ta, scale=1.5)
         fin = engine.replay_segmented(pipe, slow=slow, min_len=min_len, passes=-passes, stats=False)
