@@ -739,6 +739,70 @@ __global__ void __launch_bounds__(128) k_score_decisions(const double* __restric
   }
 }
 
+// The same scores with a LANE per decision (decision-major features FT):
+// each lane walks the 48 own rows of its decision's column, the coefficient
+// rows are shared-memory broadcasts, and the features are the lane's own
+// contiguous 576 B -- no shuffles, no per-decision reductions.  The same
+// fp32 arithmetic per (rank, own) as cand_stream_body, the lowest own row on
+// ties (ascending, strict <), so the results equal k_score_decisions'.
+__global__ void __launch_bounds__(128) k_score_decisions_lane(const double* __restrict__ thr, int E, long long ld,
+                                                              const double* __restrict__ coefs,
+                                                              const float* __restrict__ C0,
+                                                              const float* __restrict__ FT,
+                                                              const int32_t* __restrict__ dec_rank,
+                                                              const int32_t* __restrict__ dec_own, long long n,
+                                                              unsigned long long* __restrict__ best,
+                                                              float* __restrict__ chosen) {
+  __shared__ float4 cw[2][64];  // per own row: coarse / fine (w3, w4, w5, bias)
+  for (int t = threadIdx.x; t < 2 * E; t += blockDim.x) {
+    const int kind = t / E, o = t % E;
+    const double* w = coefs + kind * 7;
+    const double* x = thr + 3 * o;
+    const double bias = fma(w[2], x[2], fma(w[1], x[1], fma(w[0], x[0], 0.0))) + w[6];
+    cw[kind][o] = make_float4((float)w[3], (float)w[4], (float)w[5], (float)bias);
+  }
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = dec_rank[i];
+    if (r < 0) {
+      best[2 * i] = best[2 * i + 1] = ~0ull;
+      chosen[2 * i] = chosen[2 * i + 1] = NAN;
+      continue;
+    }
+    const int own_b = dec_own[i];
+    const float cx = C0[r], cy = C0[ld + r], cz = C0[2 * ld + r];
+    const float* f = FT + (long long)r * E * 3;
+    unsigned vc = 0xffffffffu, vf = 0xffffffffu, oc = 0xffffffffu, of = 0xffffffffu;
+    float yc_b = NAN, yf_b = NAN;
+    auto own_row = [&](int o, float fx, float fy, float fz) {
+      const float4 a = cw[0][o], b = cw[1][o];
+      const float yc = fmaf(a.z, cz, fmaf(a.y, cy, fmaf(a.x, cx, a.w)));
+      const float yf = fmaf(b.z, fz, fmaf(b.y, fy, fmaf(b.x, fx, b.w)));
+      const unsigned kc = f32_key(yc), kf = f32_key(yf);
+      if (kc < vc) vc = kc, oc = (unsigned)o;
+      if (kf < vf) vf = kf, of = (unsigned)o;
+      if (o == own_b) yc_b = yc, yf_b = yf;
+    };
+    int o = 0;
+    if ((((unsigned long long)f) & 15) == 0) {  // 4 own rows = 12 floats = 3 aligned float4 loads
+      for (; o + 4 <= E; o += 4) {
+        const float4 p0 = *reinterpret_cast<const float4*>(f + 3 * o);
+        const float4 p1 = *reinterpret_cast<const float4*>(f + 3 * o + 4);
+        const float4 p2 = *reinterpret_cast<const float4*>(f + 3 * o + 8);
+        own_row(o, p0.x, p0.y, p0.z);
+        own_row(o + 1, p0.w, p1.x, p1.y);
+        own_row(o + 2, p1.z, p1.w, p2.x);
+        own_row(o + 3, p2.y, p2.z, p2.w);
+      }
+    }
+    for (; o < E; o++) own_row(o, f[3 * o], f[3 * o + 1], f[3 * o + 2]);
+    best[2 * i] = ((unsigned long long)vc << 32) | oc;
+    best[2 * i + 1] = ((unsigned long long)vf << 32) | of;
+    chosen[2 * i] = yc_b;
+    chosen[2 * i + 1] = yf_b;
+  }
+}
+
 // FT[r][own][3] = FE[own][a][r]: the EWMA candidate features in
 // decision-major order (one transpose per table / cap / alpha) so a decision
 // reads its column's 48 x 3 features contiguously instead of 144 rows apart
@@ -2639,6 +2703,13 @@ int intf_score_decisions_ft(const intf_table* table, int32_t cap, const double* 
     return bad_input("intf_score_decisions: bad argument, workspace too small or more than 64 profile rows");
   if (n == 0) return INTF_OK;
   const long long ld = cand_ld(n_multisets(table->n_rows, cap));
+  if (ft) {  // decision-major features: a lane per decision
+    const long long want = ceil_div(n, 128);
+    k_score_decisions_lane<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 128, 0, as_stream(stream)>>>(
+        table->thr, table->n_rows, ld, coefs, ws, ft, dec_rank, dec_own, (long long)n, (unsigned long long*)best,
+        chosen);
+    return launch_status("k_score_decisions_lane");
+  }
   const long long want = ceil_div(n, 128);  // a warp per 32-slot group
   k_score_decisions<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 128, 0, as_stream(stream)>>>(
       table->thr, table->n_rows, ld, coefs, ws, ws + 3 * ld, dec_rank, dec_own, (long long)n,
