@@ -15,7 +15,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --
     python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_launch_$TAG.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c4_$TAG.csv \
     python tools/c4_breakdown.py > $OUT/ncu_launch_c4_$TAG.log 2>&1
-for K in k_cand_step k_replay_warp k_form_models k_merge_batches_warp k_merge_arrivals_scen k_noise_table k_gen_arrivals k_slo k_features k_scen_stats k_scen_solve k_scen_qr k_scen_finish k_rls_g8 k_eval_warp k_score_decisions k_dispatch_sets k_sgd k_ols_partial k_ols_windows_tma k_cand_step_host; do
+for K in k_cand_step k_replay_warp k_form_models k_merge_batches_warp k_merge_arrivals_scen k_noise_table k_gen_arrivals k_slo k_features k_scen_stats k_scen_solve k_scen_qr k_scen_finish k_rls_g8 k_eval_warp k_score_decisions_lane k_dispatch_sets k_sgd k_ols_partial k_ols_windows_tma k_cand_step_host; do
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_${TAG}_$K \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_${TAG}_$K.log 2>&1
 done
