@@ -190,7 +190,7 @@ typedef struct intf_jobs {
   int32_t *info;               /* [slots][3] status, segment records, reseats */
   uint8_t *dirty;              /* [slots] */
   int32_t *todo;               /* [slots] slots to replay */
-  int32_t *todo_count;         /* [1] */
+  int32_t *todo_count;         /* [2]: [0] entries in todo, [1] intf_jobs_replay's work counter */
   int32_t *slot_scen;          /* [slots] owning scenario of each slot (host-filled) */
   double slow;                 /* optimism factor of the speculative end estimate */
   int32_t min_len, total_slots;

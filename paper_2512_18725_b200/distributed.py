@@ -249,7 +249,7 @@ def replay_trace_sharded(pipe, slow: float = 2.0, min_len: int = 96, passes: int
         one_pass(-total)
     iters = passes
     while iters < max_iters:
-        n = int(jobs.t["todo_count"].item())
+        n = int(jobs.t["todo_count"][0].item())
         if n == 0:
             break
         one_pass(n)

@@ -999,7 +999,7 @@ class _DeviceJobs:
             "info": torch.zeros(3 * total, dtype=torch.int32, device=dev),
             "dirty": torch.zeros(total, dtype=torch.uint8, device=dev),
             "todo": torch.zeros(total, dtype=torch.int32, device=dev),
-            "todo_count": torch.zeros(1, dtype=torch.int32, device=dev),
+            "todo_count": torch.zeros(2, dtype=torch.int32, device=dev),
             "slot_scen": torch.from_numpy(np.repeat(np.arange(pb.n_scen, dtype=np.int32), jcap)).to(dev),
             "scratch": torch.zeros(6 * total, dtype=torch.float64, device=dev),  # long-trace plan/verify
         }
@@ -1054,7 +1054,7 @@ def replay_segmented(pipe: "ReplayPipeline", slow: float = 2.0, min_len: int = 9
             pipe.run_slo_features(slo=slo, features=features)
 
             def finish() -> dict:
-                if int(jobs.t["todo_count"].item()) == 0:
+                if int(jobs.t["todo_count"][0].item()) == 0:
                     return {"iterations": passes}
                 return replay_segmented_continue(pipe, jobs, passes, max_iters, slo, features, None)
 
@@ -1070,7 +1070,7 @@ def replay_segmented_continue(pipe, jobs, iters, max_iters, slo, features, first
     bt, B, J = ctypes.byref(pipe.batch), ctypes.byref(pipe.B), ctypes.byref(jobs.J)
     tab = ctypes.byref(pipe.dtable.struct)
     for iters in range(iters + 1, max_iters + 1):
-        n = int(jobs.t["todo_count"].item())
+        n = int(jobs.t["todo_count"][0].item())
         if first is None:
             first = n
         if n == 0:

@@ -38,7 +38,7 @@ L.intf_jobs_plan(bt, tab, B, J, st)
 mark("plan")
 it = 0
 while True:
-    n = int(pipe._jobs.t["todo_count"].item())
+    n = int(pipe._jobs.t["todo_count"][0].item())
     if n == 0:
         break
     it += 1
