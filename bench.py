@@ -342,7 +342,7 @@ def c4_secondary(a, stream, barrier, max_over_ranks, rank, world) -> dict:
         q = k % n_c4_pipes
         with torch.cuda.stream(rstreams[q]):
             fins.append(engine.replay_segmented(pipes[q], passes=C4_PASSES, stats=False))
-            pending[k:k + 1].copy_(pipes[q]._jobs.t["todo_count"])
+            pending[k:k + 1].copy_(pipes[q]._jobs.t["todo_count"][:1])
     for rs in rstreams:
         stream.wait_stream(rs)
     p1.record(stream)
