@@ -410,6 +410,93 @@ __global__ void k_arr_place(const intf_scenario* __restrict__ scen, const intf_m
   }
 }
 
+// The batch rank-merge of long traces by the same time buckets (over the
+// formation times; window expiries past the horizon fall in the last
+// bucket): a batch's global id = its bucket's start + the batches of its
+// bucket preceding it in (t, kind, key) heap order (`simcore.py:122`), or,
+// for the same model, in list order.  A bucket above 64 batches falls back to
+// the binary searches of k_merge_batches.
+__global__ void k_bat_hist(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                           intf_replay_buffers B, int n_models) {
+  const int g = blockIdx.z * gridDim.y + blockIdx.y;
+  if (g >= n_models) return;
+  const intf_model& M = models[g];
+  if (B.status[M.scen] & INTF_ST_OVERFLOW) return;
+  const ArrBuckets A = arr_buckets(scen[M.scen], models, B);
+  if (!A.ok) return;
+  const int n = B.n_mb[g];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    atomicAdd(&A.cnt[arr_bucket(A, B.mb_t[M.list_off + j])], 1);
+}
+__global__ void k_bat_scatter(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                              intf_replay_buffers B, int n_models) {
+  const int g = blockIdx.z * gridDim.y + blockIdx.y;
+  if (g >= n_models) return;
+  const intf_model& M = models[g];
+  const intf_scenario& S = scen[M.scen];
+  if (B.status[M.scen] & INTF_ST_OVERFLOW) return;
+  const ArrBuckets A = arr_buckets(S, models, B);
+  if (!A.ok) return;
+  const int n = B.n_mb[g], q = g - S.model_off;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&B.n_batches[M.scen], n);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int b = arr_bucket(A, B.mb_t[M.list_off + j]);
+    const int p = atomicAdd(&A.cnt[b], 1) + A.tile[b / kArrTile];
+    if (p < S.req_cap) A.slot[p] = (q << 24) | j;
+  }
+}
+__global__ void k_bat_place(const intf_scenario* __restrict__ scen, const intf_model* __restrict__ models,
+                            intf_replay_buffers B, int n_models) {
+  const int g = blockIdx.z * gridDim.y + blockIdx.y;
+  if (g >= n_models) return;
+  const intf_model& M = models[g];
+  const intf_scenario& S = scen[M.scen];
+  if (B.status[M.scen] & INTF_ST_OVERFLOW) return;
+  const ArrBuckets A = arr_buckets(S, models, B);
+  const int n = B.n_mb[g], q = g - S.model_off;
+  if (!A.ok && blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&B.n_batches[M.scen], n);  // (else: scatter's)
+  const int ro = S.req_off;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double t = B.mb_t[M.list_off + j];
+    const int4 info = reinterpret_cast<const int4*>(B.mb_info)[M.list_off + j];
+    const int kind = info.x, cnt = info.z, head = info.w;
+    const uint32_t key = (uint32_t)info.y;
+    int rank = -1;
+    if (A.ok) {
+      const int b = arr_bucket(A, t);
+      const int lo = b ? arr_at(A, b - 1) : 0, hi = arr_at(A, b);
+      if (hi - lo <= kArrBucketMax) {
+        int r = 0;
+        for (int k = lo; k < hi; k++) {
+          const int v = A.slot[k], q2 = v >> 24, j2 = v & 0xffffff;
+          if (q2 == q) {
+            r += j2 < j ? 1 : 0;
+          } else {
+            const intf_model& Q = models[S.model_off + q2];
+            const int4 i2 = reinterpret_cast<const int4*>(B.mb_info)[Q.list_off + j2];
+            r += form_key_less(B.mb_t[Q.list_off + j2], i2.x, (uint32_t)i2.y, t, kind, key) ? 1 : 0;
+          }
+        }
+        rank = lo + r;
+      }
+    }
+    if (rank < 0) {  // (no buckets, or a burst bucket)
+      rank = j;
+      for (int q2 = 0; q2 < S.n_models; q2++) {
+        const int gq = S.model_off + q2;
+        if (gq == g) continue;
+        const intf_model& Q = models[gq];
+        rank += count_form_before(B.mb_t + Q.list_off, B.mb_info + 4ll * Q.list_off, B.n_mb[gq], t, kind, key);
+      }
+    }
+    B.b_model[ro + rank] = q;
+    B.b_size[ro + rank] = cnt;
+    B.b_formed[ro + rank] = t;
+    const int32_t* lrid = B.list_rid + M.list_off;
+    for (int k = 0; k < cnt; k++) B.r_batch[ro + lrid[head + k]] = rank;
+  }
+}
+
 // The same merge with one block per SCENARIO for sweeps of many short
 // scenarios: the scenario's model lists are staged in shared memory once and
 // every element's rank is a binary search there (the per-model-list blocks
@@ -2659,6 +2746,17 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
     k_merge_batches_warp<<<ceil_div(bt->n_models, kMergeWarps), 32 * kMergeWarps, 0, st>>>(bt->scen, bt->models,
                                                                                           *buf, bt->n_models);
     return launch_status("k_merge_batches_warp");
+  }
+  if (buf->form_ws && bt->n_scen <= 65535) {  // long traces: time buckets (form_ws is free after the emit)
+    const dim3 g = merge_grid(bt);
+    const dim3 tiles(ceil_div(bt->max_req_cap / kArrBucketAvg * 2 + 1, kArrTile), bt->n_scen);
+    k_arr_zero<<<tiles, 1024, 0, st>>>(bt->scen, bt->models, *buf);
+    k_bat_hist<<<g, 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
+    k_arr_scan_tiles<<<tiles, 1024, 0, st>>>(bt->scen, bt->models, *buf);
+    k_arr_scan_top<<<ceil_div(bt->n_scen, 128), 128, 0, st>>>(bt->scen, bt->n_scen, bt->models, *buf);
+    k_bat_scatter<<<g, 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
+    k_bat_place<<<g, 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
+    return launch_status("k_bat_place");
   }
   k_merge_batches<<<merge_grid(bt), 256, 0, st>>>(bt->scen, bt->models, *buf, bt->n_models);
   return launch_status("k_merge_batches");
