@@ -19,7 +19,7 @@ for K in k_cand_step k_replay_warp k_form_models k_merge_batches_warp k_merge_ar
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_${TAG}_$K \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-c4 > $OUT/ncu_${TAG}_$K.log 2>&1
 done
-for K in k_bin_runs k_bin_classify k_gen_gaps k_form_chunks k_arr_place k_jobs_replay k_jobs_verify_big k_slo_big_hist; do
+for K in k_bin_runs k_bin_classify k_gen_gaps k_form_chunks k_arr_place k_bat_place k_jobs_replay k_jobs_verify_big k_slo_big_hist; do
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_${TAG}_$K \
     python tools/c4_breakdown.py > $OUT/ncu_${TAG}_$K.log 2>&1
 done
