@@ -173,9 +173,11 @@ int intf_replay_jobs(const intf_batch *batch, const intf_table *table, const int
  * most one job start per min_len batches, so jcap = ceil(req_cap/min_len)+1
  * suffices).  intf_jobs_plan: speculative starts (a batch forming after every
  * earlier batch's formed + slow*solo, prefix max per scenario), all jobs put
- * on the todo list.  intf_jobs_replay: replays the todo list -- its first
- * n_todo entries, or with n_todo < 0 as many as *todo_count holds (read on
- * the device; at most -n_todo), so passes queue without host round trips.
+ * on the todo list (long traces: longest first).  intf_jobs_replay: replays
+ * the todo list -- its first n_todo entries, or with n_todo < 0 as many as
+ * todo_count[0] holds (read on the device; at most -n_todo; the warps take
+ * entries from the work counter todo_count[1]), so passes queue without host
+ * round trips.
  * intf_jobs_verify: per scenario, checks every boundary (previous job's last
  * completion <= first formation), merges failing ones, puts merged jobs on a
  * fresh todo list and, for scenarios whose boundaries all hold, writes the
