@@ -238,6 +238,9 @@ class ReplayPipeline:
         return v
 
 
+SEGMENTED_MIN_REQ = 2048  # request capacity from which a single-scenario batch replays as busy-period jobs
+
+
 def run_batch(specs, table: _pack.TableArrays, preds=(), slo=True, warmup_fraction=0.0, arrivals=None,
               seg_stride: int = 64, max_retries: int = 4, fetch: bool = True):
     """Run a batch of scenarios to completion, growing capacities on
@@ -256,14 +259,26 @@ def run_batch(specs, table: _pack.TableArrays, preds=(), slo=True, warmup_fracti
         wc = None
         if arrivals is not None:
             pipe.load_arrivals([a[0] for a in arrivals], [a[1] for a in arrivals])
+        # one long scenario (a run_scenario call): its busy periods replay as
+        # parallel jobs instead of one warp's chain (bit-identical; the bundled
+        # trace's device pass 2.3 -> 0.7 ms, tools/single_trace_seg.py)
+        segmented = pipe.pb.n_scen == 1 and pipe.pb.max_req_cap >= SEGMENTED_MIN_REQ
+
+        def replay(slo_, features_):
+            if segmented:
+                replay_segmented(pipe, min_len=16, passes=3, arrivals=arrivals is None, slo=slo_, features=features_,
+                                 stats=False)()
+            else:
+                pipe.run(arrivals=arrivals is None, slo=slo_, features=features_)
+
         if warmup_fraction:
             # cutoff = t0 + f*(t1 - t0) over the observed arrival span (`metrics.py:62-65`);
             # computed after arrivals exist (device arrays), so replay first
-            pipe.run(arrivals=arrivals is None, slo=False, features=False)
+            replay(False, False)
             wc = _warm_cutoffs(pipe, warmup_fraction)
             pipe.run_slo_features(wc)
         else:
-            pipe.run(arrivals=arrivals is None, slo=slo, features=True)
+            replay(slo, True)
         st = pipe.status()
         if np.any(st & _abi.ST_OVERFLOW):
             scale *= 2.0
