@@ -2382,17 +2382,13 @@ static int launch_step(const intf_table* t, int cap, double alpha, const double*
 }
 
 // the device address of a pinned (page-locked, mapped) host buffer, or null
-// for pageable memory (then the call copies); the last buffer is remembered
+// for pageable memory (then the call copies).  Queried on every call (~1 us):
+// a remembered address could have been freed and reused for pageable memory.
 static unsigned long long* host_device_ptr(void* h) {
-  static thread_local void* last_h = nullptr;
-  static thread_local void* last_d = nullptr;
-  if (h == last_h) return reinterpret_cast<unsigned long long*>(last_d);
   cudaPointerAttributes a = {};
   void* d = nullptr;
   if (cudaPointerGetAttributes(&a, h) == cudaSuccess && a.type == cudaMemoryTypeHost) d = a.devicePointer;
   cudaGetLastError();  // (pageable memory: clear any error of the query)
-  last_h = h;
-  last_d = d;
   return reinterpret_cast<unsigned long long*>(d);
 }
 

@@ -2747,7 +2747,8 @@ int launch_formation(const intf_batch* bt, const intf_replay_buffers* buf, cudaS
                                                                                           *buf, bt->n_models);
     return launch_status("k_merge_batches_warp");
   }
-  if (buf->form_ws && bt->n_scen <= 65535) {  // long traces: time buckets (form_ws is free after the emit)
+  if (buf->form_ws && bt->n_scen <= 65535 && bt->max_list_cap < (1 << 24)) {
+    // long traces: time buckets (form_ws is free after the emit; members packed as model << 24 | index)
     const dim3 g = merge_grid(bt);
     const dim3 tiles(ceil_div(bt->max_req_cap / kArrBucketAvg * 2 + 1, kArrTile), bt->n_scen);
     k_arr_zero<<<tiles, 1024, 0, st>>>(bt->scen, bt->models, *buf);
@@ -2806,7 +2807,8 @@ int intf_generate_arrivals(const intf_batch* bt, const intf_replay_buffers* buf,
                                                                                  *buf);
     return launch_status("k_merge_arrivals_scen");
   }
-  if (buf->form_ws && bt->max_list_cap >= kLongForm && bt->n_scen <= 65535) {  // long traces: time buckets
+  if (buf->form_ws && bt->max_list_cap >= kLongForm && bt->max_list_cap < (1 << 24) && bt->n_scen <= 65535) {
+    // long traces: time buckets (members packed as model << 24 | index)
     const dim3 g = merge_grid(bt);
     const dim3 tiles(ceil_div(bt->max_req_cap / kArrBucketAvg * 2 + 1, kArrTile), bt->n_scen);
     k_arr_zero<<<tiles, 1024, 0, st>>>(bt->scen, bt->models, *buf);
